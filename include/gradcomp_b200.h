@@ -1,0 +1,127 @@
+/*
+ * gradcomp_b200.h -- C ABI of the B200-native gradient-compression engine.
+ *
+ * Drop-in boundary: the reference `gradcomp` package (pure NumPy) has no FFI;
+ * its seam is the Python class `GradientPipeline` (pkg/src/gradcomp/pipelines.py:97-393)
+ * and the codec functions it calls.  Every entry point below replaces one
+ * piece of that path and cites the reference code it restates.  The Python
+ * package `paper_2407_01378_b200` binds these symbols with ctypes (see
+ * INTEGRATION.md for the binding a maintainer of the reference would add).
+ *
+ * Conventions
+ *  - Every device buffer is caller-owned (torch tensors in the Python host).
+ *    The library never allocates device memory and never synchronises the host.
+ *  - `stream` is a cudaStream_t passed as void*; all work is stream-ordered.
+ *  - Return value: GC_OK (0) or a negative status; gc_last_error() gives a
+ *    thread-local message.  Argument checks happen before any launch.
+ *  - Reentrant: no mutable global state besides the per-thread error string.
+ */
+#ifndef GRADCOMP_B200_H
+#define GRADCOMP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GC_OK 0
+#define GC_ERR_INVALID (-1)
+#define GC_ERR_CUDA (-2)
+#define GC_ERR_UNSUPPORTED (-3)
+
+/* numpy PCG64 BitGenerator state (128-bit LCG state and increment). */
+typedef struct gc_pcg64 {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;
+} gc_pcg64;
+
+int gc_version(void);
+const char *gc_last_error(void);
+
+/* ---------------------------------------------------------------- seeding
+ * vectors.py:26-39 (splitmix64, fnv1a64), vectors.py:64-76 (SeedSpec.stream_seed / rng)
+ * plus numpy's SeedSequence -> PCG64 initialisation (numpy 2.3, bit_generator.pyx /
+ * pcg64.c), restated natively so kernels can regenerate the reference's draws. */
+uint64_t gc_splitmix64(uint64_t value);
+uint64_t gc_fnv1a64(const char *text, size_t len);
+/* worker < 0 means "no worker component" (shared stream). */
+uint64_t gc_stream_seed(uint64_t experiment_seed, const char *tag, size_t tag_len,
+                        uint64_t round_index, int64_t worker);
+/* np.random.PCG64(seed).state  (SeedSequence(seed) -> pcg64_set_seed). */
+void gc_pcg64_from_seed(uint64_t seed, gc_pcg64 *out);
+/* bit_generator.advance(delta) with delta = (delta_hi << 64) | delta_lo. */
+void gc_pcg64_advance(gc_pcg64 *g, uint64_t delta_hi, uint64_t delta_lo);
+/* next_uint64 (step, then XSL-RR output). */
+uint64_t gc_pcg64_next(gc_pcg64 *g);
+
+/* ---------------------------------------------------------------- THC
+ * RotatedQuantConfig round: pipelines.py:260-322. */
+typedef struct gc_thc_geom {
+  int64_t dim;        /* logical length d */
+  int64_t padded;     /* P = next power of two >= d (pipelines.py:263, transforms.py:74-83) */
+  int64_t block;      /* rotation block B = min(rotation_block, P) (transforms.py:78) */
+  int32_t quant_bits; /* q (compressors.py:92) */
+  int32_t wire_bits;  /* b, saturating aggregation width (compressors.py:94) */
+  double scale;       /* float(B) ** -0.5 (transforms.py:116) */
+} gc_thc_geom;
+
+/* Coordinates that can hold non-zero data: ceil(d/B)*B.  Blocks past it are
+ * all-zero in every worker: range (0,0), code 0, decode 0. */
+int64_t gc_thc_active_len(const gc_thc_geom *g);
+/* Device scratch (bytes) the THC entry points need for L workers (0 when B <= 4096). */
+int64_t gc_thc_workspace_bytes(const gc_thc_geom *g, int32_t workers);
+
+/* Rotation signs for one round as a bitmask (bit i of word i/32 set <=> sign +1):
+ * RotationSpec.for_round, transforms.py:60-83 (PCG64.integers(0,2,P), Lemire on u32 halves). */
+int gc_thc_signs(const gc_pcg64 *rotation_stream, int64_t count, uint32_t *bits, void *stream);
+
+/* Forward rotation of L workers: corrected = f32(g + r) (compressors.py:624-626),
+ * x_rot = f32(fp64 blockwise WHT(signs * corrected) * scale) (transforms.py:86-117),
+ * ranges[w][blk] = (min, max) (compressors.py:447-453).
+ * grads/resid rows have leading dimension ld (elements); resid may be NULL (EF off).
+ * x_rot: [L][active] f32 (may be NULL if only ranges are wanted), ranges: [L][nb][2] f32. */
+int gc_thc_rotate(const gc_thc_geom *g, int32_t workers, const float *grads, const float *resid,
+                  int64_t ld, const uint32_t *sign_bits, float *x_rot, float *ranges,
+                  void *workspace, void *stream);
+
+/* Elementwise min of lo / max of hi over L range tables (ElemMin/ElemMax,
+ * collectives.py:146-161; order-free, exact). in: [L][nb][2], out: [nb][2]. */
+int gc_range_consensus(int32_t workers, int64_t num_blocks, const float *ranges_in,
+                       float *ranges_out, void *stream);
+
+/* quantize_stochastic (compressors.py:456-498) for L workers on the shared grid.
+ * coin_streams: host array of L PCG64 states ("stochastic-round", round, worker),
+ * coin for coordinate i = (next64 at step i+1) >> 11 * 2^-53.
+ * codes: [L][active] int8.  counters (device int64[4], accumulated):
+ * [0] clamp count, [1] sum z, [2] sum z^2. */
+int gc_thc_quantize(const gc_thc_geom *g, int32_t workers, const float *x_rot,
+                    const float *shared_ranges, const gc_pcg64 *coin_streams, int8_t *codes,
+                    int64_t *counters, void *stream);
+
+/* Ordered saturating fold (SatIntSum.combine in ring order, collectives.py:123-143,215-226):
+ * for element e (global index offset+e) start worker s = floor((offset+e)/ring_block);
+ * acc = z[s]; acc = clip(acc + z[(s+k)%n], +-(2^(bits-1)-1)) for k=1..n-1.
+ * codes: n rows of `len` int8 with leading dimension ld.  sums: int8 (bits<=8),
+ * int16 (bits<=16) or int32.  counters[0] += clip events. */
+int gc_sat_fold(int32_t n, int64_t len, const int8_t *codes, int64_t ld, int64_t offset,
+                int64_t ring_block, int32_t bits, void *sums, int64_t *clip_counter, void *stream);
+
+/* Decode of summed codes: estimate = f32(f32(inv_WHT(f32(n*mu + delta*z_sum))) / n)
+ * (dequantize_sum compressors.py:501-521, rht_inverse transforms.py:120-126,
+ * pipelines.py:307-311).  sums element size is sum_bytes (1, 2 or 4). estimate: [d] f32. */
+int gc_thc_decode_estimate(const gc_thc_geom *g, int32_t n, const void *sums, int32_t sum_bytes,
+                           const float *shared_ranges, const uint32_t *sign_bits,
+                           float *estimate, void *workspace, void *stream);
+
+/* Own decode + error-feedback update for L workers (pipelines.py:312-318,168-170):
+ * resid[w] = f32((g[w] + resid[w]) - inv_WHT(dequantize_sum(z_w, ranges, q, 1))).
+ * codes: [L][active] int8.  When resid is NULL nothing is written (EF off). */
+int gc_thc_decode_ef(const gc_thc_geom *g, int32_t workers, const int8_t *codes,
+                     const float *shared_ranges, const uint32_t *sign_bits, const float *grads,
+                     float *resid, int64_t ld, void *workspace, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRADCOMP_B200_H */
