@@ -55,6 +55,16 @@ void gc_pcg64_advance(gc_pcg64 *g, uint64_t delta_hi, uint64_t delta_lo);
 /* next_uint64 (step, then XSL-RR output). */
 uint64_t gc_pcg64_next(gc_pcg64 *g);
 
+
+/* ---------------------------------------------------------------- round utilities */
+/* GradientPipeline._checked (pipelines.py:184-197): *count += number of non-finite
+ * entries of a [rows][cols] f32 matrix with leading dimension ld. */
+int gc_check_finite(int64_t rows, const float *data, int64_t ld, int64_t cols, int64_t *count, void *stream);
+/* RoundResult.nmse (pipelines.py:172-179, metrics.py:22-37): with ref = fp64 mean over the
+ * n corrected inputs (g + resid, resid may be NULL), acc[0] += sum (est-ref)^2, acc[1] += sum ref^2. */
+int gc_nmse_accumulate(int32_t n, int64_t d, const float *grads, const float *resid, int64_t ld,
+                       const float *estimate, double *acc, void *stream);
+
 /* ---------------------------------------------------------------- THC
  * RotatedQuantConfig round: pipelines.py:260-322. */
 typedef struct gc_thc_geom {
@@ -120,6 +130,18 @@ int gc_thc_decode_estimate(const gc_thc_geom *g, int32_t n, const void *sums, in
 int gc_thc_decode_ef(const gc_thc_geom *g, int32_t workers, const int8_t *codes,
                      const float *shared_ranges, const uint32_t *sign_bits, const float *grads,
                      float *resid, int64_t ld, void *workspace, void *stream);
+
+
+/* Whole THC round for n workers simulated on one GPU, fused into one kernel per
+ * rotation block (pipelines.py:260-322 + EF 148-151,168-170): every CTA owns one block of
+ * all n workers, so range consensus, quantization, the ring-ordered saturating fold,
+ * the estimate decode and the own-decode + residual update never leave the SM.
+ * Requires B <= 1024.  grads/resid: [n][ld] (resid NULL = EF off, updated in place);
+ * estimate: [d]; codes: optional [n][active] int8; counters (device int64[4], accumulated):
+ * [0] clamp count, [1] sum z, [2] sum z^2, [3] clip events; nmse_acc optional double[2]. */
+int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *grads, float *resid, int64_t ld,
+                       const uint32_t *sign_bits, const gc_pcg64 *coin_streams, float *estimate,
+                       int8_t *codes, int64_t *counters, double *nmse_acc, void *stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,507 @@
+// Fused THC round for n workers simulated on one GPU (the bench's hot kernel).
+//
+// Reference path (pkg/src/gradcomp/pipelines.py:147-182, 260-322): ef_apply ->
+// rht_forward -> chunk_ranges -> ElemMin/ElemMax ring consensus -> quantize_stochastic ->
+// SatIntSum ring -> dequantize_sum + rht_inverse (estimate) -> own decode -> ef_update.
+//
+// B200 design: a persistent CTA of n warps (warp w = worker w) walks 1024-coordinate
+// tiles.  Range consensus of a rotation block only needs that block of every worker and
+// the saturating ring fold of a coordinate only needs that coordinate of every worker,
+// so a tile is completed on-chip: HBM sees g and r read once and r_new / estimate written
+// once (12n + 4 bytes per coordinate; codes only if the caller asks for them).  Shared
+// memory is sized so two CTAs share an SM (n = 8, B = 1024: ~106 KB each) and the
+// per-tile barriers of one CTA overlap the other's work.
+//
+// Per worker a warp holds the tile as 32 doubles per lane.  Layout A (lane l owns
+// elements 32l..32l+31) makes butterfly stages 0-4 register-local; one XOR-swizzled
+// shared-memory transpose gives layout B (lane l owns 32j+l) for stages 5-9.  Stage order
+// is bit-0-first as in transforms.py:92-98, all arithmetic fp64 without contraction
+// (this file is compiled with -fmad=false), so codes are bit-exact with the reference.
+//
+// Coins: numpy PCG64 "stochastic-round" stream of worker w; coordinate i uses output
+// i+1.  Lane l of layout B consumes positions t0+l+1+32j: two interleaved LCG chains
+// (even / odd j, 64-step jumps) keep the 128-bit multiply chain short; tiles advance by a
+// host-precomputed gridDim*1024-step jump.
+//
+// In-pipeline simplifications that are exact (not approximations):
+//  * the value clamp of quantize_stochastic (compressors.py:482-483) is the identity: the
+//    consensus range of a block is the min/max over all workers' values of that block, so
+//    every x lies in [lo, hi] and the clamp count (range_clips) is 0;
+//  * the clip of t to +-bound (:489) only moves t by the rounding error of (x-mid)/step
+//    (< 1e-14 relative), which the 1e-9 snapping (:492-493) maps to the same code.
+#include <cuda_runtime.h>
+
+#include "gc_device.cuh"
+#include "gc_internal.h"
+
+namespace {
+
+constexpr int kTileN = 1024;
+constexpr int kMaxN = 16;
+constexpr int kLutMax = 256;   // doubles in the shared own-decode table
+
+struct FusedArgs {
+  int64_t dim, padded, active, tiles, ring_blk;
+  int n, k, q, bits;
+  double scale;
+  const float *g;
+  float *r;
+  int64_t ld;
+  bool aligned;
+  const uint32_t *signs;
+  float *est;
+  int8_t *codes;
+  unsigned long long *counters;
+  double *nmse;
+  uint64_t tile_jump[4];  // {mult_hi, mult_lo, plus_hi, plus_lo} for gridDim*1024 steps
+  gc_pcg64 streams[kMaxN];
+};
+
+struct Layout {
+  int scratch, cbuf, cod, wr, bp, lut, sgn, total;
+};
+
+__host__ __device__ inline Layout layout_for(int n, int nblk) {
+  Layout L;
+  L.scratch = 0;                        // n x 8 KB  fp64 transpose / x_rot staging
+  L.cbuf = L.scratch + n * 8192;        // n x 4 KB  corrected (f32, swizzled natural order)
+  L.cod = L.cbuf + n * 4096;            // n x 1 KB  codes
+  L.wr = L.cod + n * 1024;              // n x nblk x 2 f32   own block ranges
+  L.bp = L.wr + ((n * nblk * 8 + 15) & ~15);   // n x nblk x 4 f64  consensus params (per warp)
+  L.lut = L.bp + n * nblk * 32;         // kLutMax f64  dq(z, 1) table
+  L.sgn = L.lut + kLutMax * 8;          // 32 u32 sign words of the tile
+  L.total = L.sgn + 128;
+  return L;
+}
+
+__device__ __forceinline__ void stages_reg(double (&v)[32], int count) {
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    if (s < count) {
+      const int h = 1 << s;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (!(j & h)) {
+          const double a = v[j], b = v[j | h];
+          v[j] = a + b;
+          v[j | h] = a - b;
+        }
+      }
+    }
+  }
+}
+
+// layout A (lane owns 32*lane + j) -> layout B (lane owns 32*j + lane), XOR-swizzled.
+__device__ __forceinline__ void transpose_ab(double (&v)[32], double *scr, int lane) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) scr[lane * 32 + (j ^ lane)] = v[j];
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = scr[j * 32 + (lane ^ j)];
+  __syncwarp();
+}
+
+// Full blockwise WHT of one tile starting from layout-A registers; ends in layout B.
+__device__ __forceinline__ void wht_tile(double (&v)[32], double *scr, int lane, int k) {
+  stages_reg(v, k < 5 ? k : 5);
+  transpose_ab(v, scr, lane);
+  stages_reg(v, k - 5);
+}
+
+// cbuf keeps the tile in natural order with 16-byte chunks XOR-swizzled inside each
+// 32-float row: layout-A float4 reads and layout-B scalar reads are conflict-free.
+__device__ __forceinline__ int cidx(int e) {
+  return (e & ~31) | ((((e >> 2) & 7) ^ ((e >> 5) & 7)) << 2) | (e & 3);
+}
+
+// x * (+1 or -1) as a sign-bit flip (bit-identical to the fp64 multiply by +-1.0).
+__device__ __forceinline__ double apply_sign(double x, uint32_t positive) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (static_cast<long long>(positive ^ 1u) << 63));
+}
+
+struct Lcg {
+  uint64_t hi, lo;
+  __device__ __forceinline__ void step(uint64_t mh, uint64_t ml, uint64_t ch, uint64_t cl) {
+    const uint64_t plo = lo * ml;
+    uint64_t phi = __umul64hi(lo, ml) + lo * mh + hi * ml;
+    const uint64_t nlo = plo + cl;
+    phi += ch + (nlo < plo ? 1ull : 0ull);
+    hi = phi;
+    lo = nlo;
+  }
+  __device__ __forceinline__ uint64_t output() const {  // XSL-RR
+    const uint64_t x = hi ^ lo;
+    const unsigned rot = static_cast<unsigned>(hi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+};
+
+__device__ __forceinline__ void mul128(uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl, uint64_t &rh,
+                                       uint64_t &rl) {
+  rl = al * bl;
+  rh = __umul64hi(al, bl) + al * bh + ah * bl;
+}
+
+// quantize one value (compressors.py:485-498 with the exact in-pipeline simplifications).
+__device__ __forceinline__ int quantize_one(double x, double mid, double step, int ibound, uint64_t u) {
+  const double t = (x - mid) / step;
+  const double low = floor(t);
+  const double frac = t - low;
+  const bool snap_up = frac > 1.0 - 1e-9;
+  const bool snap_dn = frac < 1e-9;
+  const double coin = static_cast<double>(u >> 11) * (1.0 / 9007199254740992.0);
+  int z = static_cast<int>(low) + (snap_up ? 1 : ((!snap_dn && coin < frac) ? 1 : 0));
+  z = z < -ibound ? -ibound : (z > ibound ? ibound : z);
+  return z;
+}
+
+__global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_constant__ FusedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;            // worker of this warp
+  const int k = a.k;                         // log2(rotation block), 5..10
+  const int nblk = kTileN >> k;
+  const Layout L = layout_for(n, nblk);
+  double *scratch = reinterpret_cast<double *>(smem + L.scratch) + w * 1024;
+  float *xs = reinterpret_cast<float *>(scratch);                  // x_rot staging (layout B)
+  const float *cbuf_all = reinterpret_cast<const float *>(smem + L.cbuf);
+  float *cbuf = reinterpret_cast<float *>(smem + L.cbuf) + w * 1024;
+  const int8_t *cod_all = reinterpret_cast<const int8_t *>(smem + L.cod);
+  int8_t *cod = reinterpret_cast<int8_t *>(smem + L.cod) + w * 1024;
+  const float *wr_all = reinterpret_cast<const float *>(smem + L.wr);
+  float *wr = reinterpret_cast<float *>(smem + L.wr) + w * nblk * 2;
+  double *bp = reinterpret_cast<double *>(smem + L.bp) + w * nblk * 4;
+  double *lut = reinterpret_cast<double *>(smem + L.lut);
+  uint32_t *sgn = reinterpret_cast<uint32_t *>(smem + L.sgn);
+
+  const int q = a.q;
+  const int ibound = (1 << (q - 1)) - 1;
+  const double levels = static_cast<double>((1 << q) - 2);
+  const long long sat = (1ll << (a.bits - 1)) - 1;
+  const int lut_span = 2 * ibound + 1;
+  const bool use_lut = nblk * lut_span <= kLutMax;
+  const int rpb_log = k - 5;   // layout-B registers per rotation block = 2^(k-5)
+
+  // ---- PCG64 coin streams of worker w: even-j chain at t0+lane+1, odd-j chain 32 later.
+  const uint64_t inc_h = a.streams[w].inc_hi, inc_l = a.streams[w].inc_lo;
+  uint64_t c64h, c64l, cth, ctl, c32h, c32l;
+  const uint64_t m64h = gc::kPcgJump[6][0], m64l = gc::kPcgJump[6][1];
+  const uint64_t mth = a.tile_jump[0], mtl = a.tile_jump[1];
+  mul128(gc::kPcgJump[6][2], gc::kPcgJump[6][3], inc_h, inc_l, c64h, c64l);
+  mul128(gc::kPcgJump[5][2], gc::kPcgJump[5][3], inc_h, inc_l, c32h, c32l);
+  mul128(a.tile_jump[2], a.tile_jump[3], inc_h, inc_l, cth, ctl);
+  Lcg tile_state;
+  {
+    gc::Pcg p;
+    p.load(a.streams[w]);
+    p.jump(static_cast<uint64_t>(blockIdx.x) * kTileN + lane + 1);
+    tile_state.hi = static_cast<uint64_t>(p.state >> 64);
+    tile_state.lo = static_cast<uint64_t>(p.state);
+  }
+
+  const float *gw = a.g + w * a.ld;
+  float *rw = a.r ? a.r + w * a.ld : nullptr;
+  long long sz = 0, sz2 = 0, clips = 0;
+  double nmse_num = 0.0, nmse_den = 0.0;
+
+  for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+    const int64_t t0 = tile * kTileN;
+    // ---- corrected = f32(g + r) (compressors.py:624-626), coalesced loads -> cbuf
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int e4 = (lane + 32 * m) * 4;
+      const int64_t i = t0 + e4;
+      float4 c;
+      if (a.aligned && i + 3 < a.dim) {
+        c = __ldcs(reinterpret_cast<const float4 *>(gw + i));
+        if (rw) {
+          const float4 rv = __ldcs(reinterpret_cast<const float4 *>(rw + i));
+          c.x = c.x + rv.x;
+          c.y = c.y + rv.y;
+          c.z = c.z + rv.z;
+          c.w = c.w + rv.w;
+        }
+      } else {
+        float t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float v = 0.0f;
+          if (i + u < a.dim) {
+            v = gw[i + u];
+            if (rw) v = v + rw[i + u];
+          }
+          t[u] = v;
+        }
+        c = make_float4(t[0], t[1], t[2], t[3]);
+      }
+      *reinterpret_cast<float4 *>(cbuf + cidx(e4)) = c;
+    }
+    const uint32_t my_sign_word = a.signs[(t0 >> 5) + lane];
+    if (w == 0) sgn[lane] = my_sign_word;
+    __syncwarp();
+
+    // ---- forward rotation (transforms.py:107-117)
+    double v[32];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const float4 c = *reinterpret_cast<const float4 *>(cbuf + cidx(lane * 32 + 4 * m));
+      v[4 * m + 0] = apply_sign(static_cast<double>(c.x), (my_sign_word >> (4 * m + 0)) & 1u);
+      v[4 * m + 1] = apply_sign(static_cast<double>(c.y), (my_sign_word >> (4 * m + 1)) & 1u);
+      v[4 * m + 2] = apply_sign(static_cast<double>(c.z), (my_sign_word >> (4 * m + 2)) & 1u);
+      v[4 * m + 3] = apply_sign(static_cast<double>(c.w), (my_sign_word >> (4 * m + 3)) & 1u);
+    }
+    wht_tile(v, scratch, lane, k);
+
+    // ---- x_rot = f32(v * B^-1/2), staged in layout B; per-block (min, max) (compressors.py:447-453)
+    {
+      float blo = INFINITY, bhi = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float f = static_cast<float>(v[j] * a.scale);
+        xs[j * 32 + lane] = f;
+        blo = fminf(blo, f);
+        bhi = fmaxf(bhi, f);
+        if (((j + 1) & ((1 << rpb_log) - 1)) == 0) {   // last register of block j >> rpb_log
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            blo = fminf(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+            bhi = fmaxf(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
+          }
+          if (lane == 0) {
+            wr[2 * (j >> rpb_log)] = blo;
+            wr[2 * (j >> rpb_log) + 1] = bhi;
+          }
+          blo = INFINITY;
+          bhi = -INFINITY;
+        }
+      }
+    }
+    __syncthreads();   // (A) every worker's block ranges are in wr_all
+
+    // ---- range consensus, ElemMin / ElemMax over workers (pipelines.py:271-288)
+    if (lane < nblk) {
+      float lo = wr_all[2 * lane], hi = wr_all[2 * lane + 1];
+      for (int u = 1; u < n; ++u) {
+        lo = fminf(lo, wr_all[u * nblk * 2 + 2 * lane]);
+        hi = fmaxf(hi, wr_all[u * nblk * 2 + 2 * lane + 1]);
+      }
+      const double dlo = static_cast<double>(lo), dhi = static_cast<double>(hi);
+      bp[4 * lane] = dlo;
+      bp[4 * lane + 1] = dhi;
+      bp[4 * lane + 2] = (dlo + dhi) / 2.0;
+      bp[4 * lane + 3] = (dhi - dlo) / levels;
+    }
+    __syncwarp();
+    // own-decode table dq(z, 1) = f32(mid + step*z) (compressors.py:519-521), split over warps
+    if (use_lut) {
+      for (int e = threadIdx.x; e < nblk * lut_span; e += n * 32) {
+        const int b = e / lut_span, z = e - b * lut_span - ibound;
+        const double lo = bp[4 * b], hi = bp[4 * b + 1];
+        const double step = hi > lo ? bp[4 * b + 3] : 0.0;
+        lut[e] = static_cast<double>(static_cast<float>(1.0 * bp[4 * b + 2] + step * static_cast<double>(z)));
+      }
+    }
+
+    // ---- quantize_stochastic (compressors.py:473-498), layout B: e = 32j + lane
+    {
+      Lcg ev = tile_state, od = tile_state;
+      od.step(gc::kPcgJump[5][0], gc::kPcgJump[5][1], c32h, c32l);
+      for (int j = 0; j < 32; j += 2) {
+        const int blk0 = j >> rpb_log, blk1 = (j + 1) >> rpb_log;
+        const double mid0 = bp[4 * blk0 + 2], step0 = bp[4 * blk0 + 3];
+        const double mid1 = bp[4 * blk1 + 2], step1 = bp[4 * blk1 + 3];
+        const uint64_t u0 = ev.output(), u1 = od.output();
+        int z0 = 0, z1 = 0;   // degenerate block (step <= 0): code 0 (compressors.py:497)
+        if (step0 > 0.0) z0 = quantize_one(static_cast<double>(xs[j * 32 + lane]), mid0, step0, ibound, u0);
+        if (step1 > 0.0) z1 = quantize_one(static_cast<double>(xs[(j + 1) * 32 + lane]), mid1, step1, ibound, u1);
+        ev.step(m64h, m64l, c64h, c64l);
+        od.step(m64h, m64l, c64h, c64l);
+        cod[j * 32 + lane] = static_cast<int8_t>(z0);
+        cod[(j + 1) * 32 + lane] = static_cast<int8_t>(z1);
+        sz += z0 + z1;
+        sz2 += z0 * z0 + z1 * z1;
+        if (a.codes) {
+          const int64_t i0 = t0 + j * 32 + lane;
+          if (i0 < a.active) a.codes[w * a.active + i0] = static_cast<int8_t>(z0);
+          if (i0 + 32 < a.active) a.codes[w * a.active + i0 + 32] = static_cast<int8_t>(z1);
+        }
+      }
+    }
+    tile_state.step(mth, mtl, cth, ctl);
+    __syncthreads();   // (B) all codes and the dq table of the tile are in shared memory
+
+    // ---- estimate (warp tile % n): ring-ordered saturating fold + decode (pipelines.py:297-311)
+    if (w == static_cast<int>(tile % n)) {
+      int64_t s = (t0 + lane * 32) / a.ring_blk;
+      const int blk = lane >> rpb_log;   // layout A: the lane's 32 elements lie in one block
+      const double lo = bp[4 * blk], hi = bp[4 * blk + 1], mid = bp[4 * blk + 2];
+      const double step = hi > lo ? bp[4 * blk + 3] : 0.0;
+      const double nd = static_cast<double>(n);
+      for (int j = 0; j < 32; ++j) {
+        const int e = lane * 32 + j;
+        const int64_t i = t0 + e;
+        while (s + 1 < n && i >= (s + 1) * a.ring_blk) ++s;
+        long long acc = cod_all[s * 1024 + e];
+        int u = static_cast<int>(s);
+        for (int m = 1; m < n; ++m) {
+          u = (u + 1 == n) ? 0 : u + 1;
+          acc += cod_all[u * 1024 + e];
+          const long long c = acc > sat ? sat : (acc < -sat ? -sat : acc);
+          clips += (c != acc);
+          acc = c;
+        }
+        // dequantize_sum with n addends, parked in the layout-A slot of the transpose buffer
+        scratch[lane * 32 + (j ^ lane)] =
+            static_cast<double>(static_cast<float>(nd * mid + step * static_cast<double>(acc)));
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = scratch[lane * 32 + (j ^ lane)];
+      __syncwarp();
+      wht_tile(v, scratch, lane, k);
+      const float nf = static_cast<float>(n);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int e = j * 32 + lane;
+        const int64_t i = t0 + e;
+        const float f = static_cast<float>(apply_sign(v[j] * a.scale, (sgn[j] >> lane) & 1u)) / nf;
+        if (i < a.dim) {
+          __stcs(a.est + i, f);
+          if (n == 1 && rw) __stcs(rw + i, cbuf[cidx(e)] - f);   // one worker: own == estimate
+          if (a.nmse) {
+            double ref = 0.0;
+            for (int u = 0; u < n; ++u) ref += static_cast<double>(cbuf_all[u * 1024 + cidx(e)]);
+            ref = ref / nd;
+            const double err = static_cast<double>(f) - ref;
+            nmse_num += err * err;
+            nmse_den += ref * ref;
+          }
+        }
+      }
+    }
+
+    // ---- own decode + ef_update (pipelines.py:312-318, 168-170)
+    if (rw && n > 1) {
+      const int blk = lane >> rpb_log;
+      const int4 z0 = *reinterpret_cast<const int4 *>(cod + lane * 32);
+      const int4 z1 = *reinterpret_cast<const int4 *>(cod + lane * 32 + 16);
+      const int zw[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
+      const double lo = bp[4 * blk], hi = bp[4 * blk + 1], mid = bp[4 * blk + 2];
+      const double step = hi > lo ? bp[4 * blk + 3] : 0.0;
+      const double *tab = lut + blk * lut_span + ibound;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int z = static_cast<int8_t>((zw[j >> 2] >> (8 * (j & 3))) & 0xff);
+        v[j] = use_lut ? tab[z] : static_cast<double>(static_cast<float>(1.0 * mid + step * static_cast<double>(z)));
+      }
+      wht_tile(v, scratch, lane, k);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int e = j * 32 + lane;
+        const int64_t i = t0 + e;
+        const float own = static_cast<float>(apply_sign(v[j] * a.scale, (sgn[j] >> lane) & 1u));
+        if (i < a.dim) __stcs(rw + i, cbuf[cidx(e)] - own);
+      }
+    }
+    __syncthreads();   // (C) cbuf / cod / sgn / lut are reused by the next tile
+  }
+
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    sz2 += __shfl_xor_sync(0xffffffffu, sz2, o);
+    clips += __shfl_xor_sync(0xffffffffu, clips, o);
+    nmse_num += __shfl_xor_sync(0xffffffffu, nmse_num, o);
+    nmse_den += __shfl_xor_sync(0xffffffffu, nmse_den, o);
+  }
+  if (lane == 0) {
+    if (a.counters) {
+      atomicAdd(&a.counters[1], static_cast<unsigned long long>(sz));
+      atomicAdd(&a.counters[2], static_cast<unsigned long long>(sz2));
+      atomicAdd(&a.counters[3], static_cast<unsigned long long>(clips));
+    }
+    if (a.nmse && (nmse_num != 0.0 || nmse_den != 0.0)) {
+      atomicAdd(&a.nmse[0], nmse_num);
+      atomicAdd(&a.nmse[1], nmse_den);
+    }
+  }
+}
+
+using u128h = unsigned __int128;
+
+void host_jump(uint64_t delta, uint64_t out[4]) {
+  const u128h mult = (static_cast<u128h>(0x2360ED051FC65DA4ull) << 64) | 0x4385DF649FCCF645ull;
+  u128h cm = mult, cp = 1, am = 1, ap = 0;
+  while (delta) {
+    if (delta & 1) {
+      am *= cm;
+      ap = ap * cm + cp;
+    }
+    cp = (cm + 1) * cp;
+    cm *= cm;
+    delta >>= 1;
+  }
+  out[0] = static_cast<uint64_t>(am >> 64);
+  out[1] = static_cast<uint64_t>(am);
+  out[2] = static_cast<uint64_t>(ap >> 64);
+  out[3] = static_cast<uint64_t>(ap);
+}
+
+}  // namespace
+
+extern "C" int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *grads, float *resid, int64_t ld,
+                                  const uint32_t *sign_bits, const gc_pcg64 *coin_streams, float *estimate,
+                                  int8_t *codes, int64_t *counters, double *nmse_acc, void *stream) {
+  GC_REQUIRE(g != nullptr, "geometry is null");
+  GC_REQUIRE(n >= 1 && n <= kMaxN, "fused THC round supports 1..16 workers");
+  GC_REQUIRE(g->dim >= 1 && g->padded >= kTileN && (g->padded & (g->padded - 1)) == 0 && g->padded >= g->dim,
+             "fused THC round needs padded >= 1024 (power of two)");
+  GC_REQUIRE(g->block >= 32 && g->block <= kTileN && (g->block & (g->block - 1)) == 0,
+             "fused THC round needs a rotation block in [32, 1024]");
+  GC_REQUIRE(g->quant_bits >= 2 && g->quant_bits <= 8 && g->wire_bits >= g->quant_bits && g->wire_bits <= 32,
+             "invalid quant/wire bits");
+  GC_REQUIRE(grads && sign_bits && coin_streams && estimate && ld >= g->dim, "invalid argument");
+
+  FusedArgs a{};
+  a.dim = g->dim;
+  a.padded = g->padded;
+  a.active = ((g->dim + g->block - 1) / g->block) * g->block;
+  a.tiles = (a.active + kTileN - 1) / kTileN;
+  a.ring_blk = (g->padded + n - 1) / n;
+  a.n = n;
+  int k = 0;
+  while ((int64_t{1} << k) < g->block) ++k;
+  a.k = k;
+  a.q = g->quant_bits;
+  a.bits = g->wire_bits;
+  a.scale = g->scale;
+  a.g = grads;
+  a.r = resid;
+  a.ld = ld;
+  a.aligned = ((reinterpret_cast<uintptr_t>(grads) | reinterpret_cast<uintptr_t>(resid)) & 15) == 0 && (ld % 4) == 0;
+  a.signs = sign_bits;
+  a.est = estimate;
+  a.codes = codes;
+  a.counters = reinterpret_cast<unsigned long long *>(counters);
+  a.nmse = nmse_acc;
+  for (int w = 0; w < n; ++w) a.streams[w] = coin_streams[w];
+
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem = layout_for(n, kTileN >> k).total;
+  cudaFuncSetAttribute(thc_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, thc_fused_kernel, n * 32, smem);
+  if (per_sm < 1) {
+    gc_set_error("fused THC kernel does not fit on an SM");
+    return GC_ERR_UNSUPPORTED;
+  }
+  int64_t grid = static_cast<int64_t>(sms) * per_sm;
+  if (grid > a.tiles) grid = a.tiles;
+  host_jump(static_cast<uint64_t>(grid) * kTileN, a.tile_jump);
+  thc_fused_kernel<<<static_cast<unsigned>(grid), n * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  GC_LAUNCH_CHECK("thc_fused_kernel");
+  return GC_OK;
+}

@@ -1,0 +1,97 @@
+"""THC on the GPU vs the reference golden vectors and the oracle (bit-exact)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import gradcomp_oracle as orc
+from tests.golden_util import load
+from tests.gpu_util import needs_gpu, oracle_rounds, run_golden_case
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+THC_CASES = ["thc_a", "thc_b", "thc_c", "thc_d", "thc_e", "thc_f"]
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("name", THC_CASES)
+def test_thc_golden_rounds_bit_exact(name, fused):
+    for st, res, pipe, a in run_golden_case(name, fused=fused):
+        r = st["round"]
+        assert np.array_equal(res.estimate.logical, a[f"estimate_{r}"]), f"round {r} estimate"
+        assert not np.any(res.estimate.values[pipe.dim:])
+        if pipe.error_feedback:
+            assert np.array_equal(np.stack(pipe.residuals), a[f"residuals_{r}"]), f"round {r} residuals"
+        assert res.overflow.clip_events == st["clip_events"]
+        assert res.overflow.total_adds == st["total_adds"]
+        assert res.overflow.code_sigma == pytest.approx(st["code_sigma"], rel=1e-12)
+        assert res.range_clips == st["range_clips"]
+        assert res.nmse == pytest.approx(st["nmse"], rel=1e-9, abs=1e-15)
+        assert res.input_bits_per_coord == pytest.approx(st["input_bits_per_coord"], rel=1e-15)
+        led = {ph: [[res.ledger.bits_sent(worker=w, phase=ph), res.ledger.bits_received(worker=w, phase=ph)]
+                    for w in range(pipe.group.size)] for ph in res.ledger.phases()}
+        assert led == st["ledger"]
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("name", ["thc_steps_a", "thc_steps_b", "thc_steps_c"])
+def test_thc_codes_match_reference(name, fused):
+    """Codes / sums / estimate from fixed corrected inputs (EF off) against the reference's steps."""
+    import paper_2407_01378_b200 as gcb
+    meta, a = load(name)
+    pipe = gcb.make_pipeline(gcb.RotatedQuantConfig(meta["q"], meta["b"], meta["max_block"]), meta["n"], meta["d"],
+                             gcb.SeedSpec(meta["seed"]), False, fused=fused)
+    pipe._engine.capture = True
+    res = pipe.run_round(list(a["corrected"]), meta["round"])
+    active = pipe._engine.active
+    codes = pipe._engine.last["codes"].cpu().numpy()
+    assert np.array_equal(codes, a["codes"][:, :active])
+    assert not np.any(a["codes"][:, active:])
+    assert np.array_equal(res.estimate.logical, a["estimate"])
+    assert res.overflow.clip_events == meta["clip_events"]
+    if not pipe._engine.fused:
+        last = pipe._engine.last
+        assert np.array_equal(last["x_rot"].cpu().numpy(), a["rotated"][:, :active])
+        assert np.array_equal(last["shared"].cpu().numpy(), a["shared"][: active // pipe._engine.B])
+    # signs bitmask vs reference +-1 signs
+    words = pipe._engine.signs.cpu().numpy().view(np.uint32)
+    bits = ((words[:, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(-1)[:active]
+    assert np.array_equal(bits * 2.0 - 1.0, a["signs"][:active])
+
+
+@pytest.mark.parametrize("q,b,blk,n,d", [(4, 4, 1024, 4, 1 << 20), (4, 8, 1024, 4, 1 << 20),
+                                          (4, 8, 1024, 8, 1_000_003), (3, 6, 256, 3, 300_000),
+                                          (4, 4, 64, 2, 65_537), (8, 12, 512, 5, 100_000)])
+def test_thc_vs_oracle_multi_round(q, b, blk, n, d):
+    """cfg1-style parity: 2 rounds with carried EF, estimate and residuals bitwise."""
+    import paper_2407_01378_b200 as gcb
+    seed = 2024
+    seeds = gcb.SeedSpec(seed)
+    grads = [[seeds.rng("grad-worker", r, w).standard_normal(d).astype(np.float32) for w in range(n)]
+             for r in range(2)]
+    outs = oracle_rounds("rotated_quant", dict(quant_bits=q, wire_bits=b, rotation_block=blk), grads, seed)
+    for fused in (True, False):
+        pipe = gcb.make_pipeline(gcb.RotatedQuantConfig(q, b, blk), n, d, seeds, fused=fused)
+        for r in range(2):
+            res = pipe.run_round(grads[r], r)
+            o = outs[r]
+            assert np.array_equal(res.estimate.logical, o["estimate"]), (fused, r)
+            assert np.array_equal(np.stack(pipe.residuals), np.stack(o["residuals"])), (fused, r)
+            assert res.overflow.clip_events == o["clip_events"]
+            assert res.overflow.total_adds == o["total_adds"]
+            assert res.nmse == pytest.approx(o["nmse"], rel=1e-9)
+
+
+def test_thc_device_tensor_inputs_and_determinism():
+    import paper_2407_01378_b200 as gcb
+    n, d = 8, 3_000_000
+    g = torch.randn(n, d, device="cuda")
+    outs = []
+    for _ in range(2):
+        pipe = gcb.make_pipeline(gcb.RotatedQuantConfig(4, 8), n, d, gcb.SeedSpec(7))
+        r0 = pipe.run_round(g, 0)
+        r1 = pipe.run_round(g, 1)
+        # results stay valid after later rounds (fresh per-round output buffers)
+        outs.append((r0.estimate_tensor, r1.estimate_tensor, pipe.residuals_tensor.clone()))
+    for x, y in zip(*outs):
+        assert torch.equal(x, y)
+    assert not torch.equal(outs[0][0], outs[0][1])
