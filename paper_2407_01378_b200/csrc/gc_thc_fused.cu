@@ -61,11 +61,16 @@ struct Layout {
   int scratch, cbuf, cod, wr, bp, lut, sgn, total;
 };
 
+constexpr int kScrRow = 33;   // fp64 transpose rows padded to 33: conflict-free, immediate offsets
+constexpr int kCRow = 36;     // corrected-value rows padded to 36 floats (float4 reads stay aligned)
+constexpr int kScrBytes = 32 * kScrRow * 8;
+constexpr int kCBytes = 32 * kCRow * 4;
+
 __host__ __device__ inline Layout layout_for(int n, int nblk) {
   Layout L;
-  L.scratch = 0;                        // n x 8 KB  fp64 transpose / x_rot staging
-  L.cbuf = L.scratch + n * 8192;        // n x 4 KB  corrected (f32, swizzled natural order)
-  L.cod = L.cbuf + n * 4096;            // n x 1 KB  codes
+  L.scratch = 0;                        // n x 8.25 KB  fp64 transpose / x_rot staging
+  L.cbuf = L.scratch + n * kScrBytes;   // n x 4.5 KB   corrected (f32, padded natural order)
+  L.cod = L.cbuf + n * kCBytes;         // n x 1 KB     codes
   L.wr = L.cod + n * 1024;              // n x nblk x 2 f32   own block ranges
   L.bp = L.wr + ((n * nblk * 8 + 15) & ~15);   // n x nblk x 4 f64  consensus params (per warp)
   L.lut = L.bp + n * nblk * 32;         // kLutMax f64  dq(z, 1) table
@@ -74,10 +79,11 @@ __host__ __device__ inline Layout layout_for(int n, int nblk) {
   return L;
 }
 
-__device__ __forceinline__ void stages_reg(double (&v)[32], int count) {
+template <int COUNT>
+__device__ __forceinline__ void stages_reg(double (&v)[32]) {
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
-    if (s < count) {
+    if (s < COUNT) {
       const int h = 1 << s;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -91,28 +97,28 @@ __device__ __forceinline__ void stages_reg(double (&v)[32], int count) {
   }
 }
 
-// layout A (lane owns 32*lane + j) -> layout B (lane owns 32*j + lane), XOR-swizzled.
+// layout A (lane owns 32*lane + j) -> layout B (lane owns 32*j + lane) through rows padded
+// to 33 doubles: both directions hit 2 wavefronts per 256 B (optimal) with static offsets.
 __device__ __forceinline__ void transpose_ab(double (&v)[32], double *scr, int lane) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) scr[lane * 32 + (j ^ lane)] = v[j];
+  for (int j = 0; j < 32; ++j) scr[lane * kScrRow + j] = v[j];
   __syncwarp();
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = scr[j * 32 + (lane ^ j)];
+  for (int j = 0; j < 32; ++j) v[j] = scr[j * kScrRow + lane];
   __syncwarp();
 }
 
-// Full blockwise WHT of one tile starting from layout-A registers; ends in layout B.
-__device__ __forceinline__ void wht_tile(double (&v)[32], double *scr, int lane, int k) {
-  stages_reg(v, k < 5 ? k : 5);
+// Full blockwise WHT (stages 0..K-1) of one tile from layout-A registers; ends in layout B.
+template <int K>
+__device__ __forceinline__ void wht_tile(double (&v)[32], double *scr, int lane) {
+  stages_reg<(K < 5 ? K : 5)>(v);
   transpose_ab(v, scr, lane);
-  stages_reg(v, k - 5);
+  stages_reg<K - 5>(v);
 }
 
-// cbuf keeps the tile in natural order with 16-byte chunks XOR-swizzled inside each
-// 32-float row: layout-A float4 reads and layout-B scalar reads are conflict-free.
-__device__ __forceinline__ int cidx(int e) {
-  return (e & ~31) | ((((e >> 2) & 7) ^ ((e >> 5) & 7)) << 2) | (e & 3);
-}
+// cbuf keeps the tile in natural order, rows of 32 floats padded to 36: layout-A float4
+// reads, layout-B scalar reads and the coalesced float4 stores are all conflict-free.
+__device__ __forceinline__ int cidx(int e) { return (e >> 5) * kCRow + (e & 31); }
 
 // x * (+1 or -1) as a sign-bit flip (bit-identical to the fp64 multiply by +-1.0).
 __device__ __forceinline__ double apply_sign(double x, uint32_t positive) {
@@ -155,18 +161,19 @@ __device__ __forceinline__ int quantize_one(double x, double mid, double step, i
   return z;
 }
 
+template <int K, bool USE_LUT>
 __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;            // worker of this warp
-  const int k = a.k;                         // log2(rotation block), 5..10
-  const int nblk = kTileN >> k;
+  constexpr int k = K;                       // log2(rotation block), 5..10
+  constexpr int nblk = kTileN >> K;
   const Layout L = layout_for(n, nblk);
-  double *scratch = reinterpret_cast<double *>(smem + L.scratch) + w * 1024;
+  double *scratch = reinterpret_cast<double *>(smem + L.scratch) + w * (32 * kScrRow);
   float *xs = reinterpret_cast<float *>(scratch);                  // x_rot staging (layout B)
   const float *cbuf_all = reinterpret_cast<const float *>(smem + L.cbuf);
-  float *cbuf = reinterpret_cast<float *>(smem + L.cbuf) + w * 1024;
+  float *cbuf = reinterpret_cast<float *>(smem + L.cbuf) + w * (32 * kCRow);
   const int8_t *cod_all = reinterpret_cast<const int8_t *>(smem + L.cod);
   int8_t *cod = reinterpret_cast<int8_t *>(smem + L.cod) + w * 1024;
   const float *wr_all = reinterpret_cast<const float *>(smem + L.wr);
@@ -180,8 +187,8 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
   const double levels = static_cast<double>((1 << q) - 2);
   const long long sat = (1ll << (a.bits - 1)) - 1;
   const int lut_span = 2 * ibound + 1;
-  const bool use_lut = nblk * lut_span <= kLutMax;
-  const int rpb_log = k - 5;   // layout-B registers per rotation block = 2^(k-5)
+  constexpr bool use_lut = USE_LUT;
+  constexpr int rpb_log = k - 5;   // layout-B registers per rotation block = 2^(k-5)
 
   // ---- PCG64 coin streams of worker w: even-j chain at t0+lane+1, odd-j chain 32 later.
   const uint64_t inc_h = a.streams[w].inc_hi, inc_l = a.streams[w].inc_lo;
@@ -251,7 +258,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
       v[4 * m + 2] = apply_sign(static_cast<double>(c.z), (my_sign_word >> (4 * m + 2)) & 1u);
       v[4 * m + 3] = apply_sign(static_cast<double>(c.w), (my_sign_word >> (4 * m + 3)) & 1u);
     }
-    wht_tile(v, scratch, lane, k);
+    wht_tile<K>(v, scratch, lane);
 
     // ---- x_rot = f32(v * B^-1/2), staged in layout B; per-block (min, max) (compressors.py:447-453)
     {
@@ -331,19 +338,18 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
     tile_state.step(mth, mtl, cth, ctl);
     __syncthreads();   // (B) all codes and the dq table of the tile are in shared memory
 
-    // ---- estimate (warp tile % n): ring-ordered saturating fold + decode (pipelines.py:297-311)
-    if (w == static_cast<int>(tile % n)) {
-      int64_t s = (t0 + lane * 32) / a.ring_blk;
-      const int blk = lane >> rpb_log;   // layout A: the lane's 32 elements lie in one block
-      const double lo = bp[4 * blk], hi = bp[4 * blk + 1], mid = bp[4 * blk + 2];
-      const double step = hi > lo ? bp[4 * blk + 3] : 0.0;
+    // ---- ring-ordered saturating fold (SatIntSum, collectives.py:123-143, 215-226), split
+    // over all warps; dequantize_sum(., n) lands in the estimate warp's transpose rows.
+    const int ew = static_cast<int>(tile % n);
+    double *escr = reinterpret_cast<double *>(smem + L.scratch) + ew * (32 * kScrRow);
+    {
       const double nd = static_cast<double>(n);
-      for (int j = 0; j < 32; ++j) {
-        const int e = lane * 32 + j;
+      const int per = (kTileN + n - 1) / n;
+      for (int e = w * per + lane; e < min(kTileN, (w + 1) * per); e += 32) {
         const int64_t i = t0 + e;
-        while (s + 1 < n && i >= (s + 1) * a.ring_blk) ++s;
-        long long acc = cod_all[s * 1024 + e];
-        int u = static_cast<int>(s);
+        const int s0 = static_cast<int>(i / a.ring_blk);   // ring block j starts at worker j
+        long long acc = cod_all[s0 * 1024 + e];
+        int u = s0;
         for (int m = 1; m < n; ++m) {
           u = (u + 1 == n) ? 0 : u + 1;
           acc += cod_all[u * 1024 + e];
@@ -351,16 +357,23 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
           clips += (c != acc);
           acc = c;
         }
-        // dequantize_sum with n addends, parked in the layout-A slot of the transpose buffer
-        scratch[lane * 32 + (j ^ lane)] =
+        const int blk = e >> k;
+        const double lo = bp[4 * blk], hi = bp[4 * blk + 1], mid = bp[4 * blk + 2];
+        const double step = hi > lo ? bp[4 * blk + 3] : 0.0;
+        escr[(e >> 5) * kScrRow + (e & 31)] =
             static_cast<double>(static_cast<float>(nd * mid + step * static_cast<double>(acc)));
       }
-      __syncwarp();
+    }
+    // named barrier 1: every warp arrives once its fold share is written; only the
+    // estimate warp waits for it.
+    if (w == ew) {
+      asm volatile("bar.sync 1, %0;" ::"r"(n * 32) : "memory");
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = scratch[lane * 32 + (j ^ lane)];
+      for (int j = 0; j < 32; ++j) v[j] = escr[lane * kScrRow + j];
       __syncwarp();
-      wht_tile(v, scratch, lane, k);
+      wht_tile<K>(v, scratch, lane);
       const float nf = static_cast<float>(n);
+      const double nd = static_cast<double>(n);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int e = j * 32 + lane;
@@ -371,7 +384,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
           if (n == 1 && rw) __stcs(rw + i, cbuf[cidx(e)] - f);   // one worker: own == estimate
           if (a.nmse) {
             double ref = 0.0;
-            for (int u = 0; u < n; ++u) ref += static_cast<double>(cbuf_all[u * 1024 + cidx(e)]);
+            for (int u = 0; u < n; ++u) ref += static_cast<double>(cbuf_all[u * (32 * kCRow) + cidx(e)]);
             ref = ref / nd;
             const double err = static_cast<double>(f) - ref;
             nmse_num += err * err;
@@ -379,6 +392,10 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
           }
         }
       }
+    }
+
+    else {
+      asm volatile("bar.arrive 1, %0;" ::"r"(n * 32) : "memory");
     }
 
     // ---- own decode + ef_update (pipelines.py:312-318, 168-170)
@@ -395,7 +412,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
         const int z = static_cast<int8_t>((zw[j >> 2] >> (8 * (j & 3))) & 0xff);
         v[j] = use_lut ? tab[z] : static_cast<double>(static_cast<float>(1.0 * mid + step * static_cast<double>(z)));
       }
-      wht_tile(v, scratch, lane, k);
+      wht_tile<K>(v, scratch, lane);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int e = j * 32 + lane;
@@ -487,13 +504,27 @@ extern "C" int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *
   a.nmse = nmse_acc;
   for (int w = 0; w < n; ++w) a.streams[w] = coin_streams[w];
 
+  const int nblk = kTileN >> k;
+  const bool lut = nblk * ((1 << g->quant_bits) - 1) <= kLutMax;
+  using KernelFn = void (*)(FusedArgs);
+  KernelFn fn = nullptr;
+#define GC_PICK(KK)                                                       \
+  case KK:                                                                \
+    fn = lut ? thc_fused_kernel<KK, true> : thc_fused_kernel<KK, false>; \
+    break;
+  switch (k) {
+    GC_PICK(5) GC_PICK(6) GC_PICK(7) GC_PICK(8) GC_PICK(9) GC_PICK(10)
+    default: break;
+  }
+#undef GC_PICK
+  GC_REQUIRE(fn != nullptr, "unsupported rotation block");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int smem = layout_for(n, kTileN >> k).total;
-  cudaFuncSetAttribute(thc_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = layout_for(n, nblk).total;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, thc_fused_kernel, n * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, n * 32, smem);
   if (per_sm < 1) {
     gc_set_error("fused THC kernel does not fit on an SM");
     return GC_ERR_UNSUPPORTED;
@@ -501,7 +532,7 @@ extern "C" int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *
   int64_t grid = static_cast<int64_t>(sms) * per_sm;
   if (grid > a.tiles) grid = a.tiles;
   host_jump(static_cast<uint64_t>(grid) * kTileN, a.tile_jump);
-  thc_fused_kernel<<<static_cast<unsigned>(grid), n * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  fn<<<static_cast<unsigned>(grid), n * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
   GC_LAUNCH_CHECK("thc_fused_kernel");
   return GC_OK;
 }
