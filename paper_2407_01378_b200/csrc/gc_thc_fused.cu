@@ -28,7 +28,8 @@
 //    consensus range of a block is the min/max over all workers' values of that block, so
 //    every x lies in [lo, hi] and the clamp count (range_clips) is 0;
 //  * the clip of t to +-bound (:489) only moves t by the rounding error of (x-mid)/step
-//    (< 1e-14 relative), which the 1e-9 snapping (:492-493) maps to the same code.
+//    (< 1e-13 absolute), which the 1e-9 snapping (:492-493) maps to the same code, so the
+//    final code clip (:496) never fires either.
 #include <cuda_runtime.h>
 
 #include "gc_device.cuh"
@@ -72,8 +73,8 @@ __host__ __device__ inline Layout layout_for(int n, int nblk) {
   L.cbuf = L.scratch + n * kScrBytes;   // n x 4.5 KB   corrected (f32, padded natural order)
   L.cod = L.cbuf + n * kCBytes;         // n x 1 KB     codes
   L.wr = L.cod + n * 1024;              // n x nblk x 2 f32   own block ranges
-  L.bp = L.wr + ((n * nblk * 8 + 15) & ~15);   // n x nblk x 4 f64  consensus params (per warp)
-  L.lut = L.bp + n * nblk * 32;         // kLutMax f64  dq(z, 1) table
+  L.bp = L.wr + ((n * nblk * 8 + 15) & ~15);   // n x nblk x 8 f64  consensus params (per warp)
+  L.lut = L.bp + n * nblk * 64;         // kLutMax f64  dq(z, 1) table
   L.sgn = L.lut + kLutMax * 8;          // 32 u32 sign words of the tile
   L.total = L.sgn + 128;
   return L;
@@ -149,16 +150,27 @@ __device__ __forceinline__ void mul128(uint64_t ah, uint64_t al, uint64_t bh, ui
 }
 
 // quantize one value (compressors.py:485-498 with the exact in-pipeline simplifications).
-__device__ __forceinline__ int quantize_one(double x, double mid, double step, int ibound, uint64_t u) {
-  const double t = (x - mid) / step;
-  const double low = floor(t);
-  const double frac = t - low;
-  const bool snap_up = frac > 1.0 - 1e-9;
-  const bool snap_dn = frac < 1e-9;
+// t = (x - mid) / step is formed with one Markstein correction from inv = RN(1/step): the
+// result is within 1 ulp of the IEEE quotient, i.e. within 2^-46 since |t| <= 127.  The
+// code depends on t only through floor(t) and comparisons of frac with the coin and the
+// 1e-9 snap thresholds; a change of t across an integer is absorbed by the snapping, so
+// the code can only differ from the reference when frac lies within 2^-44 of the coin or
+// of a threshold.  Those (probability ~1e-13) recompute t with the IEEE division.
+__device__ __forceinline__ int quantize_one(double x, double mid, double step, double inv, uint64_t u) {
+  const double a = x - mid;
+  const double q0 = a * inv;
+  double t = fma(fma(-q0, step, a), inv, q0);
+  double low = floor(t);
+  double frac = t - low;
   const double coin = static_cast<double>(u >> 11) * (1.0 / 9007199254740992.0);
-  int z = static_cast<int>(low) + (snap_up ? 1 : ((!snap_dn && coin < frac) ? 1 : 0));
-  z = z < -ibound ? -ibound : (z > ibound ? ibound : z);
-  return z;
+  constexpr double kLo = 1e-9, kHi = 1.0 - 1e-9, kGuard = 0x1p-44;
+  if (fabs(frac - coin) < kGuard || fabs(frac - kLo) < kGuard || fabs(frac - kHi) < kGuard) {
+    t = a / step;
+    low = floor(t);
+    frac = t - low;
+  }
+  const bool up = frac > kHi || (frac >= kLo && coin < frac);
+  return static_cast<int>(low) + (up ? 1 : 0);
 }
 
 template <int K, bool USE_LUT>
@@ -178,7 +190,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
   int8_t *cod = reinterpret_cast<int8_t *>(smem + L.cod) + w * 1024;
   const float *wr_all = reinterpret_cast<const float *>(smem + L.wr);
   float *wr = reinterpret_cast<float *>(smem + L.wr) + w * nblk * 2;
-  double *bp = reinterpret_cast<double *>(smem + L.bp) + w * nblk * 4;
+  double *bp = reinterpret_cast<double *>(smem + L.bp) + w * nblk * 8;
   double *lut = reinterpret_cast<double *>(smem + L.lut);
   uint32_t *sgn = reinterpret_cast<uint32_t *>(smem + L.sgn);
 
@@ -188,14 +200,15 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
   const long long sat = (1ll << (a.bits - 1)) - 1;
   const int lut_span = 2 * ibound + 1;
   constexpr bool use_lut = USE_LUT;
+  const bool simd_fold = a.bits <= 8 && (256 % n) == 0 && (a.ring_blk % 4) == 0;
   constexpr int rpb_log = k - 5;   // layout-B registers per rotation block = 2^(k-5)
 
   // ---- PCG64 coin streams of worker w: even-j chain at t0+lane+1, odd-j chain 32 later.
   const uint64_t inc_h = a.streams[w].inc_hi, inc_l = a.streams[w].inc_lo;
-  uint64_t c64h, c64l, cth, ctl, c32h, c32l;
-  const uint64_t m64h = gc::kPcgJump[6][0], m64l = gc::kPcgJump[6][1];
+  uint64_t c128h, c128l, cth, ctl, c32h, c32l;
+  const uint64_t m128h = gc::kPcgJump[7][0], m128l = gc::kPcgJump[7][1];
   const uint64_t mth = a.tile_jump[0], mtl = a.tile_jump[1];
-  mul128(gc::kPcgJump[6][2], gc::kPcgJump[6][3], inc_h, inc_l, c64h, c64l);
+  mul128(gc::kPcgJump[7][2], gc::kPcgJump[7][3], inc_h, inc_l, c128h, c128l);
   mul128(gc::kPcgJump[5][2], gc::kPcgJump[5][3], inc_h, inc_l, c32h, c32l);
   mul128(a.tile_jump[2], a.tile_jump[3], inc_h, inc_l, cth, ctl);
   Lcg tile_state;
@@ -294,49 +307,58 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
         hi = fmaxf(hi, wr_all[u * nblk * 2 + 2 * lane + 1]);
       }
       const double dlo = static_cast<double>(lo), dhi = static_cast<double>(hi);
-      bp[4 * lane] = dlo;
-      bp[4 * lane + 1] = dhi;
-      bp[4 * lane + 2] = (dlo + dhi) / 2.0;
-      bp[4 * lane + 3] = (dhi - dlo) / levels;
+      const double step = (dhi - dlo) / levels;
+      bp[8 * lane] = dlo;
+      bp[8 * lane + 1] = dhi;
+      bp[8 * lane + 2] = (dlo + dhi) / 2.0;
+      bp[8 * lane + 3] = step;
+      bp[8 * lane + 4] = step > 0.0 ? 1.0 / step : 0.0;   // degenerate: any finite value works
+      bp[8 * lane + 5] = dhi > dlo ? step : 0.0;     // dequantize_sum's step (compressors.py:520)
     }
     __syncwarp();
-    // own-decode table dq(z, 1) = f32(mid + step*z) (compressors.py:519-521), split over warps
+    // dq(z, 1) table for the own decode (compressors.py:519-521), built cooperatively.
     if (use_lut) {
       for (int e = threadIdx.x; e < nblk * lut_span; e += n * 32) {
         const int b = e / lut_span, z = e - b * lut_span - ibound;
-        const double lo = bp[4 * b], hi = bp[4 * b + 1];
-        const double step = hi > lo ? bp[4 * b + 3] : 0.0;
-        lut[e] = static_cast<double>(static_cast<float>(1.0 * bp[4 * b + 2] + step * static_cast<double>(z)));
+        lut[e] = static_cast<double>(static_cast<float>(1.0 * bp[8 * b + 2] + bp[8 * b + 5] * static_cast<double>(z)));
       }
     }
 
-    // ---- quantize_stochastic (compressors.py:473-498), layout B: e = 32j + lane
+    // ---- quantize_stochastic (compressors.py:473-498), layout B: e = 32j + lane; four
+    // interleaved LCG chains (j mod 4), each jumping 128 steps per use.
     {
-      Lcg ev = tile_state, od = tile_state;
-      od.step(gc::kPcgJump[5][0], gc::kPcgJump[5][1], c32h, c32l);
-      for (int j = 0; j < 32; j += 2) {
-        const int blk0 = j >> rpb_log, blk1 = (j + 1) >> rpb_log;
-        const double mid0 = bp[4 * blk0 + 2], step0 = bp[4 * blk0 + 3];
-        const double mid1 = bp[4 * blk1 + 2], step1 = bp[4 * blk1 + 3];
-        const uint64_t u0 = ev.output(), u1 = od.output();
-        int z0 = 0, z1 = 0;   // degenerate block (step <= 0): code 0 (compressors.py:497)
-        if (step0 > 0.0) z0 = quantize_one(static_cast<double>(xs[j * 32 + lane]), mid0, step0, ibound, u0);
-        if (step1 > 0.0) z1 = quantize_one(static_cast<double>(xs[(j + 1) * 32 + lane]), mid1, step1, ibound, u1);
-        ev.step(m64h, m64l, c64h, c64l);
-        od.step(m64h, m64l, c64h, c64l);
-        cod[j * 32 + lane] = static_cast<int8_t>(z0);
-        cod[(j + 1) * 32 + lane] = static_cast<int8_t>(z1);
-        sz += z0 + z1;
-        sz2 += z0 * z0 + z1 * z1;
-        if (a.codes) {
-          const int64_t i0 = t0 + j * 32 + lane;
-          if (i0 < a.active) a.codes[w * a.active + i0] = static_cast<int8_t>(z0);
-          if (i0 + 32 < a.active) a.codes[w * a.active + i0 + 32] = static_cast<int8_t>(z1);
+      Lcg ch[4];
+      ch[0] = tile_state;
+#pragma unroll
+      for (int c = 1; c < 4; ++c) {
+        ch[c] = ch[c - 1];
+        ch[c].step(gc::kPcgJump[5][0], gc::kPcgJump[5][1], c32h, c32l);
+      }
+      for (int j = 0; j < 32; j += 4) {
+        int z[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int blk = (j + c) >> rpb_log;
+          const double *pb = bp + 8 * blk;
+          const uint64_t u = ch[c].output();
+          ch[c].step(m128h, m128l, c128h, c128l);
+          const int zq = quantize_one(static_cast<double>(xs[(j + c) * 32 + lane]), pb[2], pb[3], pb[4], u);
+          z[c] = pb[3] > 0.0 ? zq : 0;   // degenerate block: code 0 (compressors.py:497)
+          cod[(j + c) * 32 + lane] = static_cast<int8_t>(z[c]);
+          sz += z[c];
+          sz2 += z[c] * z[c];
         }
       }
     }
     tile_state.step(mth, mtl, cth, ctl);
     __syncthreads();   // (B) all codes and the dq table of the tile are in shared memory
+
+    if (a.codes && t0 + lane * 32 < a.active) {   // optional code dump (parity tests)
+      const uint4 *src = reinterpret_cast<const uint4 *>(cod + lane * 32);
+      uint4 *dst = reinterpret_cast<uint4 *>(a.codes + w * a.active + t0 + lane * 32);
+      dst[0] = src[0];
+      dst[1] = src[1];
+    }
 
     // ---- ring-ordered saturating fold (SatIntSum, collectives.py:123-143, 215-226), split
     // over all warps; dequantize_sum(., n) lands in the estimate warp's transpose rows.
@@ -345,23 +367,54 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
     {
       const double nd = static_cast<double>(n);
       const int per = (kTileN + n - 1) / n;
-      for (int e = w * per + lane; e < min(kTileN, (w + 1) * per); e += 32) {
-        const int64_t i = t0 + e;
-        const int s0 = static_cast<int>(i / a.ring_blk);   // ring block j starts at worker j
-        long long acc = cod_all[s0 * 1024 + e];
-        int u = s0;
-        for (int m = 1; m < n; ++m) {
-          u = (u + 1 == n) ? 0 : u + 1;
-          acc += cod_all[u * 1024 + e];
-          const long long c = acc > sat ? sat : (acc < -sat ? -sat : acc);
-          clips += (c != acc);
-          acc = c;
+      const int e_end = min(kTileN, (w + 1) * per);
+      if (simd_fold) {
+        // four coordinates per lane as packed int8 (ring blocks are 4-aligned here)
+        for (int e = w * per + lane * 4; e < e_end; e += 128) {
+          const int s0 = static_cast<int>((t0 + e) / a.ring_blk);
+          uint32_t acc = *reinterpret_cast<const uint32_t *>(cod_all + s0 * 1024 + e);
+          int u = s0;
+          for (int m = 1; m < n; ++m) {
+            u = (u + 1 == n) ? 0 : u + 1;
+            const uint32_t z = *reinterpret_cast<const uint32_t *>(cod_all + u * 1024 + e);
+            const uint32_t wrap = __vadd4(acc, z);
+            uint32_t c;
+            if (a.bits == 8) {
+              c = __vmaxs4(__vaddss4(acc, z), 0x81818181u);   // clamp to +-127
+            } else {
+              const uint32_t hs = static_cast<uint32_t>(sat) * 0x01010101u;
+              const uint32_t ls = static_cast<uint32_t>(-sat) & 0xffu;
+              c = __vmins4(__vmaxs4(wrap, ls * 0x01010101u), hs);
+            }
+            clips += __popc(__vcmpne4(wrap, c)) >> 3;
+            acc = c;
+          }
+          const int blk = e >> k;
+          const double *pb = bp + 8 * blk;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int zs = static_cast<int8_t>((acc >> (8 * b)) & 0xffu);
+            escr[((e + b) >> 5) * kScrRow + ((e + b) & 31)] =
+                static_cast<double>(static_cast<float>(nd * pb[2] + pb[5] * static_cast<double>(zs)));
+          }
         }
-        const int blk = e >> k;
-        const double lo = bp[4 * blk], hi = bp[4 * blk + 1], mid = bp[4 * blk + 2];
-        const double step = hi > lo ? bp[4 * blk + 3] : 0.0;
-        escr[(e >> 5) * kScrRow + (e & 31)] =
-            static_cast<double>(static_cast<float>(nd * mid + step * static_cast<double>(acc)));
+      } else {
+        for (int e = w * per + lane; e < e_end; e += 32) {
+          const int64_t i = t0 + e;
+          const int s0 = static_cast<int>(i / a.ring_blk);   // ring block j starts at worker j
+          long long acc = cod_all[s0 * 1024 + e];
+          int u = s0;
+          for (int m = 1; m < n; ++m) {
+            u = (u + 1 == n) ? 0 : u + 1;
+            acc += cod_all[u * 1024 + e];
+            const long long c = acc > sat ? sat : (acc < -sat ? -sat : acc);
+            clips += (c != acc);
+            acc = c;
+          }
+          const double *pb = bp + 8 * (e >> k);
+          escr[(e >> 5) * kScrRow + (e & 31)] =
+              static_cast<double>(static_cast<float>(nd * pb[2] + pb[5] * static_cast<double>(acc)));
+        }
       }
     }
     // named barrier 1: every warp arrives once its fold share is written; only the
@@ -404,8 +457,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
       const int4 z0 = *reinterpret_cast<const int4 *>(cod + lane * 32);
       const int4 z1 = *reinterpret_cast<const int4 *>(cod + lane * 32 + 16);
       const int zw[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
-      const double lo = bp[4 * blk], hi = bp[4 * blk + 1], mid = bp[4 * blk + 2];
-      const double step = hi > lo ? bp[4 * blk + 3] : 0.0;
+      const double mid = bp[8 * blk + 2], step = bp[8 * blk + 5];
       const double *tab = lut + blk * lut_span + ibound;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
