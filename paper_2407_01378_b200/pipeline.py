@@ -178,6 +178,7 @@ class GradientPipeline:
         if self.validate:
             bad = torch.zeros(1, dtype=torch.int64, device=self.device)
             _native.call("gc_check_finite", n, g.data_ptr(), g.stride(0), d, bad.data_ptr(), _stream_ptr())
+            self._engine.launches += 1
             if int(bad.item()):
                 raise ValueError("gradients must be finite")
         return g

@@ -68,6 +68,15 @@ class Engine:
         self.n, self.dim, self.seeds, self.device = n, dim, seeds, device
         self.capture = False       # keep intermediates for parity tests
         self.last = {}
+        self.kernel_events = None  # list -> (start, end) CUDA events around the dominant kernel
+        self.launches = 0          # native kernel launches issued (for the bench's gpu_launches)
+
+    def _ev(self):
+        if self.kernel_events is None:
+            return None
+        e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self.kernel_events.append(e)
+        return e
 
     def warm_q(self):
         return None
@@ -144,9 +153,15 @@ class ThcEngine(Engine):
             if self.capture:
                 codes = torch.zeros(n, self.active, dtype=torch.int8, device=self.device)
                 self.last = {"codes": codes, "signs": self.signs}
+            ev = self._ev()
+            if ev:
+                ev[0].record()
             _native.call("gc_thc_round_fused", ctypes.byref(self.geom), n, grads.data_ptr(), _ptr(res),
                          g_ld, self.signs.data_ptr(), coins, self.est.data_ptr(), _ptr(codes),
                          self.counters.data_ptr(), self.nmse_acc.data_ptr() if nmse else None, sp)
+            if ev:
+                ev[1].record()
+            self.launches += 2
         else:
             b = self._generic_buffers()
             ws = _ptr(self.workspace)
@@ -171,6 +186,7 @@ class ThcEngine(Engine):
                              res.stride(0), ws, sp)
             if self.capture:
                 self.last = dict(b, signs=self.signs)
+            self.launches += 5 + (n > 1) + bool(nmse) + (res is not None)
         # ledger + bits (pipelines.py:271-305, 321)
         num_blocks = self.P // self.B
         ledger.charge_ring("range-consensus", n, num_blocks, 32)
