@@ -11,7 +11,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC) -Xptxas -v
 EXACT    := -fmad=false
 
-CU_EXACT := gc_thc.cu gc_thc_fused.cu gc_util.cu
+CU_EXACT := gc_thc.cu gc_thc_fused.cu gc_util.cu gc_dense.cu gc_topk.cu
 CU_FAST  :=
 CPP      := gc_host.cpp
 

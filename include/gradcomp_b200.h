@@ -132,6 +132,39 @@ int gc_thc_decode_ef(const gc_thc_geom *g, int32_t workers, const int8_t *codes,
                      float *resid, int64_t ld, void *workspace, void *stream);
 
 
+/* ---------------------------------------------------------------- float ring folds
+ * FloatSum ring_all_reduce (collectives.py:112-120, 177-236) as an ordered fold per element:
+ * element e (global index offset+e) starts at worker (offset+e)/ring_block and folds in ring
+ * order; wire_fp16 rounds every transmitted partial and the final value through binary16
+ * (fp16_round_trip, vectors.py:136-152); round_inputs first rounds the inputs to fp16
+ * (DenseConfig(16), pipelines.py:373); divisor > 0 divides the result (estimate = sum / n).
+ * Used for the dense FP16/FP32 baselines (pipelines.py:370-393), TopK-Chunked's norm and chunk
+ * aggregation (pipelines.py:224-244) and PowerSGD's factor sums (pipelines.py:327-363). */
+int gc_float_fold(int32_t n, int64_t len, const float *inputs, int64_t ld, int64_t offset, int64_t ring_block,
+                  int32_t wire_fp16, int32_t round_inputs, int32_t divisor, float *out, void *stream);
+/* out = in / divisor (f32, may alias). */
+int gc_scale_div(int64_t len, const float *in, int32_t divisor, float *out, void *stream);
+/* out = fp16_round_trip(in) (vectors.py:136-152; may alias). */
+int gc_fp16_round(int64_t len, const float *in, float *out, void *stream);
+
+/* ---------------------------------------------------------------- TopK
+ * topk_indices / topk_compress (compressors.py:387-403): per row, the k largest |x| with the
+ * lower index winning ties, emitted in ascending index order (idx_out [L][k] int32) with the
+ * values (val_out [L][k], optional; fp16-rounded when fp16_vals != 0).
+ * Values come from `values`, or when values is NULL from grads (+ resid): with resid != NULL the
+ * selection is fused with ef_apply and the corrected vector f32(g + r) is written over resid. */
+int64_t gc_topk_workspace_bytes(int32_t workers, int64_t len);
+int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld, int64_t k, const float *grads,
+                   float *resid, int32_t *idx_out, float *val_out, int32_t fp16_vals, void *workspace,
+                   void *stream);
+/* TopK aggregation (pipelines.py:206-209): estimate = 0; estimate[idx_w] += val_w for w in
+ * worker order (f32, the np.add.at order).  Dividing by n is gc_scale_div. */
+int gc_sparse_accumulate(int32_t workers, int64_t k, const int32_t *idx, const float *val, int64_t dim,
+                         float *estimate, void *stream);
+/* ef_update with a sparse own payload (compressors.py:629-631, 406-409): resid[w][idx] -= val. */
+int gc_sparse_ef_update(int32_t workers, int64_t k, const int32_t *idx, const float *val, float *resid, int64_t ld,
+                        void *stream);
+
 /* Whole THC round for n workers simulated on one GPU, fused into one kernel per
  * rotation block (pipelines.py:260-322 + EF 148-151,168-170): every CTA owns one block of
  * all n workers, so range consensus, quantization, the ring-ordered saturating fold,

@@ -74,6 +74,15 @@ SIGNATURES = {
     "gc_thc_decode_estimate": (c_int, [POINTER(ThcGeom), I32, P, I32, P, P, P, P, P]),
     "gc_thc_decode_ef": (c_int, [POINTER(ThcGeom), I32, P, P, P, P, P, I64, P, P]),
     "gc_thc_round_fused": (c_int, [POINTER(ThcGeom), I32, P, P, I64, P, POINTER(Pcg64), P, P, P, P, P]),
+    # float folds
+    "gc_float_fold": (c_int, [I32, I64, P, I64, I64, I64, I32, I32, I32, P, P]),
+    "gc_scale_div": (c_int, [I64, P, I32, P, P]),
+    "gc_fp16_round": (c_int, [I64, P, P, P]),
+    # TopK
+    "gc_topk_workspace_bytes": (c_int64, [I32, I64]),
+    "gc_topk_select": (c_int, [I32, I64, P, I64, I64, P, P, P, P, I32, P, P]),
+    "gc_sparse_accumulate": (c_int, [I32, I64, P, P, I64, P, P]),
+    "gc_sparse_ef_update": (c_int, [I32, I64, P, P, P, I64, P]),
 }
 
 _lib = None

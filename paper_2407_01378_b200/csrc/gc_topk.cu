@@ -1,0 +1,378 @@
+// Top-k selection by magnitude with the reference tie-break, and the sparse aggregation.
+//
+// topk_indices (compressors.py:387-396) = argsort(-|x|, stable)[:k] sorted ascending: the k
+// largest |x|, lower index first among equal magnitudes, emitted in ascending index order.
+// Used for TopK (pipelines.py:201-211) and for the chunk selection of TopK-Chunked
+// (select_chunks, compressors.py:412-414).
+//
+// B200 design (HBM-bound integer work): keys are the f32 bit patterns with the sign
+// cleared (order-preserving for |x|, +-0 equal).  A three-level radix select (11 + 10 + 10
+// bits) finds the threshold key T and m = how many elements equal to T are taken; each
+// level is one coalesced histogram pass (shared-memory histograms, one global atomic per
+// bin) plus a one-CTA bin search.  Per 8192-element tile, counts of (key > T) and
+// (key == T) are scanned into output offsets and tie ranks; the write pass emits indices in
+// ascending order with warp ballots, so no sort is needed.  All L rows (workers) run in the
+// same launches (grid.y = worker).
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cuda_runtime.h>
+
+#include "gc_device.cuh"
+#include "gc_internal.h"
+
+namespace {
+
+constexpr int kNT = 256;
+constexpr int kTileE = 8192;          // elements per tile (8 warps x 32 steps x 32 lanes)
+constexpr int kSteps = kTileE / kNT;  // 32
+
+struct RowState {  // per worker, lives in the workspace
+  unsigned int prefix;     // key bits fixed so far
+  unsigned int pad;
+  long long k_rem;         // elements still to take at the current level
+  long long gt;            // elements strictly above the current prefix
+  unsigned int thresh;     // final threshold key T
+  unsigned int pad2;
+  long long take_eq;       // m: number of T-keyed elements taken (lowest indices)
+};
+
+struct Work {
+  RowState *state;              // [L]
+  unsigned int *hist;           // [L][2048]
+  unsigned int *tile_gt;        // [L][tiles]
+  unsigned int *tile_eq;        // [L][tiles]
+  long long *tile_sel_off;      // [L][tiles]
+  long long *tile_eq_off;       // [L][tiles]
+};
+
+__host__ __device__ inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t{255}; }
+
+__host__ __device__ inline Work carve(void *ws, int L, int64_t tiles) {
+  char *p = static_cast<char *>(ws);
+  Work w;
+  w.state = reinterpret_cast<RowState *>(p);
+  p += align256(sizeof(RowState) * L);
+  w.hist = reinterpret_cast<unsigned int *>(p);
+  p += align256(int64_t{4} * 2048 * L);
+  w.tile_gt = reinterpret_cast<unsigned int *>(p);
+  p += align256(int64_t{4} * tiles * L);
+  w.tile_eq = reinterpret_cast<unsigned int *>(p);
+  p += align256(int64_t{4} * tiles * L);
+  w.tile_sel_off = reinterpret_cast<long long *>(p);
+  p += align256(int64_t{8} * tiles * L);
+  w.tile_eq_off = reinterpret_cast<long long *>(p);
+  return w;
+}
+
+int64_t ws_bytes(int L, int64_t tiles) {
+  return align256(sizeof(RowState) * L) + align256(int64_t{4} * 2048 * L) + 2 * align256(int64_t{4} * tiles * L) +
+         2 * align256(int64_t{8} * tiles * L);
+}
+
+__device__ __forceinline__ unsigned int key_of(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
+
+// level 0: bits 30..20 (2048 bins); level 1: bits 19..10 for keys with the level-0 prefix;
+// level 2: bits 9..0 for keys with the level-1 prefix.
+__device__ __forceinline__ int bin_of(unsigned int key, int level, unsigned int prefix) {
+  if (level == 0) return static_cast<int>(key >> 20);
+  if (level == 1) return (key >> 20) == prefix ? static_cast<int>((key >> 10) & 1023u) : -1;
+  return (key >> 10) == prefix ? static_cast<int>(key & 1023u) : -1;
+}
+
+__global__ void __launch_bounds__(kNT) init_kernel(Work wk, int L, int64_t k) {
+  for (int i = blockIdx.x * kNT + threadIdx.x; i < 2048 * L; i += gridDim.x * kNT) wk.hist[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < L) {
+    RowState &s = wk.state[threadIdx.x];
+    s.prefix = 0;
+    s.k_rem = k;
+    s.gt = 0;
+    s.thresh = 0;
+    s.take_eq = 0;
+  }
+}
+
+// Optional fused producer for level 0: corrected = f32(g + r) written over r (ef_apply,
+// compressors.py:624-626) while building the level-0 histogram of |corrected|.
+__global__ void __launch_bounds__(kNT) hist_kernel(Work wk, int level, int64_t len, const float *vals, int64_t ld,
+                                                   const float *grads, float *resid) {
+  __shared__ unsigned int h[2048];
+  const int w = blockIdx.y;
+  const int nb = level == 0 ? 2048 : 1024;
+  for (int i = threadIdx.x; i < nb; i += kNT) h[i] = 0;
+  __syncthreads();
+  const unsigned int prefix = wk.state[w].prefix;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
+  const int64_t end = min(base + kTileE, len);
+  for (int64_t i = base + threadIdx.x; i < end; i += kNT) {
+    float x;
+    if (grads) {   // fused ef_apply
+      x = grads[w * ld + i];
+      if (resid) {
+        x = x + resid[w * ld + i];
+        resid[w * ld + i] = x;
+      }
+    } else {
+      x = vals[w * ld + i];
+    }
+    const int b = bin_of(key_of(x), level, prefix);
+    if (b >= 0) atomicAdd(&h[b], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += kNT)
+    if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
+}
+
+// One CTA per worker: find bin b (scanning bins from the top) with
+// above < k_rem <= above + count[b]; extend the prefix; reset the histogram.
+__global__ void __launch_bounds__(1024) find_kernel(Work wk, int level) {
+  using Scan = cub::BlockScan<unsigned long long, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int found;
+  __shared__ unsigned long long s_above, s_krem;
+  const int w = blockIdx.x;
+  RowState &s = wk.state[w];
+  const int nb = level == 0 ? 2048 : 1024;
+  const int per = nb / 1024;   // bins per thread, owned top-down
+  unsigned int *h = wk.hist + w * 2048;
+  if (threadIdx.x == 0) {
+    found = -1;
+    s_krem = static_cast<unsigned long long>(s.k_rem);
+  }
+  unsigned long long c[2] = {0, 0};
+  unsigned long long local = 0;
+  for (int j = 0; j < per; ++j) {
+    c[j] = h[nb - 1 - (threadIdx.x * per + j)];
+    local += c[j];
+  }
+  unsigned long long excl;
+  Scan(tmp).ExclusiveSum(local, excl);
+  __syncthreads();
+  const unsigned long long k_rem = s_krem;
+  unsigned long long run = excl;
+  for (int j = 0; j < per; ++j) {
+    if (run < k_rem && k_rem <= run + c[j]) {   // exactly one bin qualifies
+      found = nb - 1 - (threadIdx.x * per + j);
+      s_above = run;
+    }
+    run += c[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int b = static_cast<unsigned int>(found);
+    s.gt += static_cast<long long>(s_above);
+    s.k_rem = static_cast<long long>(k_rem - s_above);
+    s.prefix = (level == 0) ? b : ((s.prefix << 10) | b);
+    if (level == 2) {
+      s.thresh = s.prefix;
+      s.take_eq = s.k_rem;
+    }
+  }
+  for (int i = threadIdx.x; i < 2048; i += 1024) h[i] = 0;
+}
+
+__global__ void __launch_bounds__(kNT) tile_count_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
+                                                         int64_t tiles) {
+  const int w = blockIdx.y;
+  const unsigned int T = wk.state[w].thresh;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
+  const int64_t end = min(base + kTileE, len);
+  unsigned int gt = 0, eq = 0;
+  for (int64_t i = base + threadIdx.x; i < end; i += kNT) {
+    const unsigned int key = key_of(vals[w * ld + i]);
+    gt += key > T;
+    eq += key == T;
+  }
+  using R = cub::BlockReduce<unsigned int, kNT>;
+  __shared__ typename R::TempStorage t1, t2;
+  const unsigned int sgt = R(t1).Sum(gt);
+  const unsigned int seq = R(t2).Sum(eq);
+  if (threadIdx.x == 0) {
+    wk.tile_gt[w * tiles + blockIdx.x] = sgt;
+    wk.tile_eq[w * tiles + blockIdx.x] = seq;
+  }
+}
+
+// One CTA per worker: eq prefix (tie ranks) and selected-count prefix (output offsets).
+__global__ void __launch_bounds__(1024) tile_scan_kernel(Work wk, int64_t tiles) {
+  using Scan = cub::BlockScan<long long, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ long long carry_eq, carry_sel;
+  const int w = blockIdx.x;
+  const long long m = wk.state[w].take_eq;
+  if (threadIdx.x == 0) carry_eq = carry_sel = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < tiles; t0 += 1024) {
+    const int64_t t = t0 + threadIdx.x;
+    const long long eq = t < tiles ? wk.tile_eq[w * tiles + t] : 0;
+    long long eq_ex;
+    Scan(tmp).ExclusiveSum(eq, eq_ex);
+    __syncthreads();
+    eq_ex += carry_eq;
+    long long take = m - eq_ex;
+    take = take < 0 ? 0 : (take > eq ? eq : take);
+    const long long sel = (t < tiles ? wk.tile_gt[w * tiles + t] : 0) + take;
+    long long sel_ex;
+    long long sel_tot;
+    Scan(tmp).ExclusiveSum(sel, sel_ex, sel_tot);
+    __syncthreads();
+    if (t < tiles) {
+      wk.tile_eq_off[w * tiles + t] = eq_ex;
+      wk.tile_sel_off[w * tiles + t] = sel_ex + carry_sel;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry_eq = eq_ex + eq;
+    if (threadIdx.x == 0) carry_sel += sel_tot;
+    __syncthreads();
+  }
+}
+
+// Emit selected indices in ascending order (and optionally fp16-rounded values).
+__global__ void __launch_bounds__(kNT) write_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
+                                                    int64_t tiles, int64_t k, int32_t *idx_out, float *val_out,
+                                                    int fp16_vals) {
+  __shared__ unsigned int s_eq[kNT / 32], s_sel[kNT / 32];
+  const int w = blockIdx.y;
+  const unsigned int T = wk.state[w].thresh;
+  const long long m = wk.state[w].take_eq;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE + warp * (kSteps * 32);
+  const unsigned int lt_mask = (1u << lane) - 1u;
+  unsigned int keys[kSteps];
+  unsigned int eq_tot = 0;
+#pragma unroll
+  for (int s = 0; s < kSteps; ++s) {
+    const int64_t i = base + s * 32 + lane;
+    keys[s] = i < len ? key_of(vals[w * ld + i]) : 0u;
+    const bool valid = i < len;
+    eq_tot += __popc(__ballot_sync(0xffffffffu, valid && keys[s] == T));
+  }
+  if (lane == 0) s_eq[warp] = eq_tot;
+  __syncthreads();
+  long long eq_base = wk.tile_eq_off[w * tiles + blockIdx.x];
+  for (int j = 0; j < warp; ++j) eq_base += s_eq[j];
+  // selected flags and per-warp totals
+  unsigned int sel_masks[kSteps];
+  unsigned int sel_tot = 0;
+  long long eq_run = eq_base;
+#pragma unroll
+  for (int s = 0; s < kSteps; ++s) {
+    const int64_t i = base + s * 32 + lane;
+    const bool valid = i < len;
+    const bool is_eq = valid && keys[s] == T;
+    const unsigned int eqm = __ballot_sync(0xffffffffu, is_eq);
+    const long long rank = eq_run + __popc(eqm & lt_mask);
+    const bool sel = valid && (keys[s] > T || (is_eq && rank < m));
+    sel_masks[s] = __ballot_sync(0xffffffffu, sel);
+    sel_tot += __popc(sel_masks[s]);
+    eq_run += __popc(eqm);
+  }
+  if (lane == 0) s_sel[warp] = sel_tot;
+  __syncthreads();
+  long long out = wk.tile_sel_off[w * tiles + blockIdx.x];
+  for (int j = 0; j < warp; ++j) out += s_sel[j];
+#pragma unroll
+  for (int s = 0; s < kSteps; ++s) {
+    const unsigned int sm = sel_masks[s];
+    if ((sm >> lane) & 1u) {
+      const long long pos = out + __popc(sm & lt_mask);
+      const int64_t i = base + s * 32 + lane;
+      if (pos < k) {
+        idx_out[w * k + pos] = static_cast<int32_t>(i);
+        if (val_out) {
+          const float x = vals[w * ld + i];
+          val_out[w * k + pos] = fp16_vals ? gc::fp16_round_trip(x) : x;
+        }
+      }
+    }
+    out += __popc(sm);
+  }
+}
+
+// ---------------------------------------------------------------- sparse aggregation
+// estimate[idx] += val for one worker's payload (indices unique within a payload), launched
+// once per worker in worker order: the f32 sum per coordinate follows the reference's
+// np.add.at order (pipelines.py:206-209).
+__global__ void scatter_add_kernel(int64_t k, const int32_t *idx, const float *val, float *acc) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < k;
+       e += static_cast<int64_t>(gridDim.x) * kNT)
+    acc[idx[e]] += val[e];
+}
+
+// resid[idx] = resid[idx] - val (ef_update at the selected coordinates; elsewhere own = 0).
+__global__ void sparse_ef_kernel(int L, int64_t k, const int32_t *idx, const float *val, float *resid, int64_t ld) {
+  const int w = blockIdx.y;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < k;
+       e += static_cast<int64_t>(gridDim.x) * kNT) {
+    const int64_t i = idx[w * k + e];
+    resid[w * ld + i] = resid[w * ld + i] - val[w * k + e];
+  }
+}
+
+int grid_for(int64_t work) {
+  int64_t g = (work + kNT - 1) / kNT;
+  if (g > 148 * 16) g = 148 * 16;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t gc_topk_workspace_bytes(int32_t workers, int64_t len) {
+  const int64_t tiles = (len + kTileE - 1) / kTileE;
+  return ws_bytes(workers, tiles);
+}
+
+int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld, int64_t k, const float *grads,
+                   float *resid, int32_t *idx_out, float *val_out, int32_t fp16_vals, void *workspace,
+                   void *stream) {
+  GC_REQUIRE(workers >= 1 && workers <= 65535 && len >= 1 && ld >= len, "invalid shape");
+  GC_REQUIRE(k >= 1 && k <= len, "need 1 <= k <= len");
+  GC_REQUIRE(len <= 0x7fffffff, "rows longer than 2^31-1 are not supported (int32 indices)");
+  GC_REQUIRE(workspace && idx_out && (values || grads), "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t tiles = (len + kTileE - 1) / kTileE;
+  Work wk = carve(workspace, workers, tiles);
+  const dim3 grid(static_cast<unsigned>(tiles), workers);
+  init_kernel<<<grid_for(2048 * workers), kNT, 0, st>>>(wk, workers, k);
+  GC_LAUNCH_CHECK("init_kernel");
+  // level 0 (optionally fused with ef_apply: values then live in resid, or in grads if EF is off)
+  hist_kernel<<<grid, kNT, 0, st>>>(wk, 0, len, values, ld, grads, resid);
+  GC_LAUNCH_CHECK("hist_kernel");
+  const float *vals = values ? values : (resid ? resid : grads);
+  find_kernel<<<workers, 1024, 0, st>>>(wk, 0);
+  for (int level = 1; level <= 2; ++level) {
+    hist_kernel<<<grid, kNT, 0, st>>>(wk, level, len, vals, ld, nullptr, nullptr);
+    find_kernel<<<workers, 1024, 0, st>>>(wk, level);
+  }
+  GC_LAUNCH_CHECK("radix select");
+  tile_count_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles);
+  tile_scan_kernel<<<workers, 1024, 0, st>>>(wk, tiles);
+  write_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles, k, idx_out, val_out, fp16_vals);
+  GC_LAUNCH_CHECK("topk write");
+  return GC_OK;
+}
+
+int gc_sparse_accumulate(int32_t workers, int64_t k, const int32_t *idx, const float *val, int64_t dim,
+                         float *estimate, void *stream) {
+  GC_REQUIRE(workers >= 1 && k >= 0 && dim >= 1 && idx && val && estimate, "invalid argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(estimate, 0, sizeof(float) * dim, st);
+  for (int w = 0; w < workers; ++w) {   // worker-id order (pipelines.py:207)
+    scatter_add_kernel<<<grid_for(k), kNT, 0, st>>>(k, idx + w * k, val + w * k, estimate);
+  }
+  GC_LAUNCH_CHECK("scatter_add_kernel");
+  return GC_OK;
+}
+
+int gc_sparse_ef_update(int32_t workers, int64_t k, const int32_t *idx, const float *val, float *resid, int64_t ld,
+                        void *stream) {
+  GC_REQUIRE(workers >= 1 && k >= 0 && idx && val && resid, "invalid argument");
+  if (k == 0) return GC_OK;
+  sparse_ef_kernel<<<dim3(grid_for(k), workers), kNT, 0, static_cast<cudaStream_t>(stream)>>>(workers, k, idx, val,
+                                                                                              resid, ld);
+  GC_LAUNCH_CHECK("sparse_ef_kernel");
+  return GC_OK;
+}
+
+}  // extern "C"

@@ -206,7 +206,88 @@ class ThcEngine(Engine):
         return self.est, input_bits, RoundStats(self.counters, self.nmse_acc if nmse else None, finalize)
 
 
+def _simple_stats(nmse_acc):
+    return RoundStats(None, nmse_acc, lambda c, m: {"nmse": nmse_from(m), "range_clips": 0,
+                                                    "overflow": OverflowStats()})
+
+
+# -------------------------------------------------------------------------------- dense
+class DenseEngine(Engine):
+    """pipelines.py:370-393: FP16 bar (fp16 inputs, fp16 wire per hop) or exact FP32 ring; no EF."""
+
+    def __init__(self, cfg: DenseConfig, n, dim, seeds, device):
+        super().__init__(n, dim, seeds, device)
+        self.bits = cfg.bits
+
+    def run(self, grads, res, round_index, ledger, nmse=True):
+        n, d = self.n, self.dim
+        est = torch.empty(d, dtype=torch.float32, device=self.device)
+        wire16 = 1 if self.bits == 16 else 0
+        ev = self._ev()
+        if ev:
+            ev[0].record()
+        _native.call("gc_float_fold", n, d, grads.data_ptr(), grads.stride(0), 0, -(-d // n), wire16, wire16, n,
+                     est.data_ptr(), _sp())
+        if ev:
+            ev[1].record()
+        self.launches += 1
+        acc = None
+        if nmse:
+            acc = torch.zeros(2, dtype=torch.float64, device=self.device)
+            self._nmse(grads, None, est, acc)
+            self.launches += 1
+        ledger.charge_ring("dense", n, d, self.bits)
+        return est, float(self.bits) * d, _simple_stats(acc)
+
+
+# -------------------------------------------------------------------------------- TopK
+class TopKEngine(Engine):
+    """pipelines.py:201-211 (TopKConfig)."""
+
+    def __init__(self, cfg: TopKConfig, n, dim, seeds, device):
+        super().__init__(n, dim, seeds, device)
+        self.k = cfg.k
+        ws = int(_native.lib().gc_topk_workspace_bytes(n, dim))
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
+
+    def run(self, grads, res, round_index, ledger, nmse=True):
+        n, d, k = self.n, self.dim, self.k
+        sp = _sp()
+        idx = torch.empty(n, k, dtype=torch.int32, device=self.device)
+        val = torch.empty(n, k, dtype=torch.float32, device=self.device)
+        ev = self._ev()
+        if ev:
+            ev[0].record()
+        # selection fused with ef_apply: the corrected vectors land in `res` (EF on)
+        _native.call("gc_topk_select", n, d, None, grads.stride(0), k, grads.data_ptr(), _ptr(res),
+                     idx.data_ptr(), val.data_ptr(), 1, self.ws.data_ptr(), sp)
+        if ev:
+            ev[1].record()
+        est = torch.empty(d, dtype=torch.float32, device=self.device)
+        _native.call("gc_sparse_accumulate", n, k, idx.data_ptr(), val.data_ptr(), d, est.data_ptr(), sp)
+        _native.call("gc_scale_div", d, est.data_ptr(), n, est.data_ptr(), sp)
+        self.launches += 10 + n
+        acc = None
+        corrected = res if res is not None else grads
+        if nmse:
+            acc = torch.zeros(2, dtype=torch.float64, device=self.device)
+            self._nmse(corrected, None, est, acc)
+            self.launches += 1
+        if res is not None:
+            _native.call("gc_sparse_ef_update", n, k, idx.data_ptr(), val.data_ptr(), res.data_ptr(),
+                         res.stride(0), sp)
+            self.launches += 1
+        if self.capture:
+            self.last = {"idx": idx, "val": val}
+        ledger.charge_gather("sparse-gather", [48 * k] * n)
+        return est, float(48 * k), _simple_stats(acc)
+
+
 def make_engine(cfg, n, dim, seeds, device, fused=True) -> Engine:
     if isinstance(cfg, RotatedQuantConfig):
         return ThcEngine(cfg, n, dim, seeds, device, fused)
+    if isinstance(cfg, DenseConfig):
+        return DenseEngine(cfg, n, dim, seeds, device)
+    if isinstance(cfg, TopKConfig):
+        return TopKEngine(cfg, n, dim, seeds, device)
     raise NotImplementedError(f"{type(cfg).__name__} engine not built yet")

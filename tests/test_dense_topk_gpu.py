@@ -1,0 +1,72 @@
+"""Dense baselines and TopK on the GPU vs the reference golden vectors and the oracle."""
+import numpy as np
+import pytest
+import torch
+
+from tests.gpu_util import needs_gpu, oracle_rounds, run_golden_case
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+
+def _ledger(res, n):
+    return {ph: [[res.ledger.bits_sent(worker=w, phase=ph), res.ledger.bits_received(worker=w, phase=ph)]
+                 for w in range(n)] for ph in res.ledger.phases()}
+
+
+@pytest.mark.parametrize("name", ["dense16", "dense32", "topk_a", "topk_b"])
+def test_golden_rounds_bit_exact(name):
+    for st, res, pipe, a in run_golden_case(name):
+        r = st["round"]
+        assert np.array_equal(res.estimate.logical, a[f"estimate_{r}"]), f"round {r} estimate"
+        if pipe.error_feedback:
+            assert np.array_equal(np.stack(pipe.residuals), a[f"residuals_{r}"]), f"round {r} residuals"
+        assert res.nmse == pytest.approx(st["nmse"], rel=1e-9, abs=1e-15)
+        assert res.input_bits_per_coord == pytest.approx(st["input_bits_per_coord"], rel=1e-15)
+        assert _ledger(res, pipe.group.size) == st["ledger"]
+
+
+@pytest.mark.parametrize("bits,n,d", [(16, 8, 1_000_003), (32, 8, 1_000_003), (16, 3, 4097), (16, 1, 5000),
+                                      (32, 5, 77)])
+def test_dense_vs_oracle(bits, n, d):
+    import paper_2407_01378_b200 as gcb
+    seeds = gcb.SeedSpec(11)
+    grads = [[seeds.rng("grad-worker", 0, w).standard_normal(d).astype(np.float32) * 100 for w in range(n)]]
+    # a few values beyond the fp16 range exercise the +-65504 saturation
+    grads[0][0][:3] = [1e5, -7e4, 65519.0]
+    o = oracle_rounds("dense", dict(bits=bits), grads, 11, ef=False)[0]
+    res = gcb.make_pipeline(gcb.DenseConfig(bits), n, d, seeds).run_round(grads[0], 0)
+    assert np.array_equal(res.estimate.logical, o["estimate"])
+
+
+@pytest.mark.parametrize("n,d,k", [(8, 1_000_000, 10_000), (4, 300_001, 3), (3, 65_536, 65_536), (2, 5000, 1),
+                                   (5, 123_457, 4321)])
+def test_topk_vs_oracle_multi_round(n, d, k):
+    import paper_2407_01378_b200 as gcb
+    seeds = gcb.SeedSpec(5)
+    rng = np.random.default_rng(5)
+    # quarter-valued inputs: heavy ties, exactly representable -> exercises the lower-index tie-break
+    grads = [[(rng.integers(-40, 41, d) / 4.0).astype(np.float32) for _ in range(n)] for _ in range(3)]
+    outs = oracle_rounds("topk", dict(k=k), grads, 5)
+    pipe = gcb.make_pipeline(gcb.TopKConfig(k), n, d, seeds)
+    pipe._engine.capture = True
+    for r in range(3):
+        res = pipe.run_round(grads[r], r)
+        idx = pipe._engine.last["idx"].cpu().numpy()
+        for w in range(n):
+            assert np.array_equal(idx[w], outs[r]["payloads"][w][0]), (r, w)
+        assert np.array_equal(res.estimate.logical, outs[r]["estimate"])
+        assert np.array_equal(np.stack(pipe.residuals), np.stack(outs[r]["residuals"]))
+
+
+def test_topk_gaussian_large():
+    """BERT-like shape reduced: d = 11M, k = 1%, n = 2 (bit-exact indices, estimate and residuals)."""
+    import paper_2407_01378_b200 as gcb
+    n, d = 2, 11_000_000
+    k = d // 100
+    seeds = gcb.SeedSpec(3)
+    grads = [[seeds.rng("grad-worker", 0, w).standard_normal(d).astype(np.float32) for w in range(n)]]
+    o = oracle_rounds("topk", dict(k=k), grads, 3)[0]
+    pipe = gcb.make_pipeline(gcb.TopKConfig(k), n, d, seeds)
+    res = pipe.run_round(grads[0], 0)
+    assert np.array_equal(res.estimate.logical, o["estimate"])
+    assert np.array_equal(np.stack(pipe.residuals), np.stack(o["residuals"]))
