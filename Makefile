@@ -11,8 +11,8 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC) -Xptxas -v
 EXACT    := -fmad=false
 
-CU_EXACT := gc_thc.cu gc_thc_fused.cu gc_util.cu gc_dense.cu gc_topk.cu
-CU_FAST  :=
+CU_EXACT := gc_thc.cu gc_thc_fused.cu gc_util.cu gc_dense.cu gc_topk.cu gc_chunk.cu
+CU_FAST  := gc_psgd.cu
 CPP      := gc_host.cpp
 
 OBJS := $(patsubst %.cu,$(OBJDIR)/%.o,$(CU_EXACT) $(CU_FAST)) $(patsubst %.cpp,$(OBJDIR)/%.o,$(CPP))

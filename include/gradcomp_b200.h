@@ -165,6 +165,55 @@ int gc_sparse_accumulate(int32_t workers, int64_t k, const int32_t *idx, const f
 int gc_sparse_ef_update(int32_t workers, int64_t k, const int32_t *idx, const float *val, float *resid, int64_t ld,
                         void *stream);
 
+/* ---------------------------------------------------------------- TopK-Chunked
+ * _round_chunked building blocks (pipelines.py:213-258).  `perm` (nullable, int64 [d]) is the
+ * shared coordinate permutation of the ablation (transforms.py:129-151): the chunked vector is
+ * work[i] = vals[perm[i]] and results are scattered back through it. */
+/* ef_apply (compressors.py:624-626): out[w] = f32(g[w] + resid[w]) (resid NULL: copy). */
+int gc_ef_apply(int32_t workers, int64_t d, const float *grads, const float *resid, int64_t ld, float *out,
+                int64_t ld_out, void *stream);
+/* fp16(f32(chunk_sq_norms)) per worker (vectors.py:180-192, pipelines.py:221-223), numpy's
+ * pairwise fp64 order: norms [L][ceil(d/chunk)]. */
+int gc_chunk_norms(int32_t workers, int64_t d, int64_t chunk, const float *vals, int64_t ld, const int64_t *perm,
+                   float *norms, void *stream);
+/* chunk_values (compressors.py:417-430): packs[w][j*chunk + t] = fp16(work_w[sel[j]*chunk + t]). */
+int gc_chunk_pack(int32_t workers, int64_t d, int64_t chunk, int64_t selected, const int32_t *sel,
+                  const float *vals, int64_t ld, const int64_t *perm, float *packs, void *stream);
+/* chunkset_to_dense / n (compressors.py:433-438, pipelines.py:246-247): estimate zeroed, then
+ * estimate[sel[j]*chunk + t] = summed[j*chunk + t] / divisor. */
+int gc_chunk_scatter(int64_t d, int64_t chunk, int64_t selected, const int32_t *sel, const float *summed,
+                     int32_t divisor, const int64_t *perm, float *estimate, void *stream);
+/* ef_update with own = the worker's chunk values (pipelines.py:248-251, 168-170): resid holds the
+ * corrected vector; resid[w][sel chunk coords] -= packs[w]. */
+int gc_chunk_ef_update(int32_t workers, int64_t d, int64_t chunk, int64_t selected, const int32_t *sel,
+                       const float *packs, const int64_t *perm, float *resid, int64_t ld, void *stream);
+
+/* ---------------------------------------------------------------- PowerSGD
+ * _round_powersgd (pipelines.py:324-368).  Matrices are the corrected vectors zero-padded to
+ * rows x cols (matrix_shape_for, compressors.py:530-548), row-major, leading dimension ld per
+ * worker.  Supported ranks: 1..8 and 16.  Products accumulate in fp64 and round to f32. */
+int gc_psgd_splits(int32_t workers, int64_t cols);
+int64_t gc_psgd_workspace_bytes(int32_t workers, int64_t rows, int64_t cols, int32_t rank);
+/* P_w = M_w Q (pipelines.py:348): q [cols][rank], p [L][rows][rank]. */
+int gc_psgd_mq(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c, int64_t ld,
+               const float *q, float *p, void *stream);
+/* Q_w = M_w^T P_hat (pipelines.py:354): p_hat [rows][rank], q [L][cols][rank]. */
+int gc_psgd_mtp(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c, int64_t ld,
+                const float *p_hat, float *q, void *workspace, void *stream);
+/* orthonormalize (compressors.py:555-588): fp64 modified Gram-Schmidt with canonical-basis
+ * completion of degenerate columns; *status = 1 if completion failed (DegenerateMatrixError). */
+int gc_psgd_orthonormalize(int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace, int32_t *status,
+                           void *stream);
+/* own_w = P_hat Q_w^T, resid_w -= own_w (resid holds the corrected matrix; NULL skips);
+ * estimate = P_hat Q_sum^T / n (NULL skips) (pipelines.py:355, 365, 168-170). */
+int gc_psgd_decode(int32_t workers, int32_t n, int64_t d, int64_t cols, int32_t rank, const float *p_hat,
+                   const float *q_workers, const float *q_sum, float *resid, int64_t ld, float *estimate,
+                   void *stream);
+/* gram = Q^T Q in fp64 (rank check of ensure_full_rank, compressors.py:595-603). */
+int gc_psgd_gram(int64_t cols, int32_t rank, const float *q, double *gram, void *stream);
+/* cudaMemsetAsync wrapper (residual reset of the dense bypass, pipelines.py:336). */
+int gc_fill_zero(void *ptr, int64_t bytes, void *stream);
+
 /* Whole THC round for n workers simulated on one GPU, fused into one kernel per
  * rotation block (pipelines.py:260-322 + EF 148-151,168-170): every CTA owns one block of
  * all n workers, so range consensus, quantization, the ring-ordered saturating fold,

@@ -83,6 +83,21 @@ SIGNATURES = {
     "gc_topk_select": (c_int, [I32, I64, P, I64, I64, P, P, P, P, I32, P, P]),
     "gc_sparse_accumulate": (c_int, [I32, I64, P, P, I64, P, P]),
     "gc_sparse_ef_update": (c_int, [I32, I64, P, P, P, I64, P]),
+    # TopK-Chunked
+    "gc_ef_apply": (c_int, [I32, I64, P, P, I64, P, I64, P]),
+    "gc_chunk_norms": (c_int, [I32, I64, I64, P, I64, P, P, P]),
+    "gc_chunk_pack": (c_int, [I32, I64, I64, I64, P, P, I64, P, P, P]),
+    "gc_chunk_scatter": (c_int, [I64, I64, I64, P, P, I32, P, P, P]),
+    "gc_chunk_ef_update": (c_int, [I32, I64, I64, I64, P, P, P, P, I64, P]),
+    # PowerSGD
+    "gc_psgd_splits": (c_int, [I32, I64]),
+    "gc_psgd_workspace_bytes": (c_int64, [I32, I64, I64, I32]),
+    "gc_psgd_mq": (c_int, [I32, I64, I64, I64, I32, P, I64, P, P, P]),
+    "gc_psgd_mtp": (c_int, [I32, I64, I64, I64, I32, P, I64, P, P, P, P]),
+    "gc_psgd_orthonormalize": (c_int, [I64, I32, P, P, P, P, P]),
+    "gc_psgd_decode": (c_int, [I32, I32, I64, I64, I32, P, P, P, P, I64, P, P]),
+    "gc_psgd_gram": (c_int, [I64, I32, P, P, P]),
+    "gc_fill_zero": (c_int, [P, I64, P]),
 }
 
 _lib = None

@@ -1,0 +1,382 @@
+// PowerSGD (rank-r factorisation with error feedback) on B200.
+//
+// Reference: _round_powersgd (pipelines.py:324-368) with matrix_shape_for / to_matrix
+// (compressors.py:530-548), orthonormalize (compressors.py:555-588), warm start (:366).
+// M_w = corrected_w zero-padded to rows x cols (row-major); P_w = M_w Q; P_hat =
+// orthonormalize(sum_w P_w); Q_w = M_w^T P_hat; own_w = P_hat Q_w^T; estimate =
+// P_hat (sum_w Q_w)^T / n; warm Q = sum_w Q_w / n.
+//
+// B200 design: with r = 4 both products are matrix-vector-like (about 1 flop per byte), so
+// they are HBM-bound streams over M, not tensor-core work.  Each is one pass over M with
+// fp64 accumulation (more accurate than the reference's fp32 BLAS; results agree to
+// ~1e-7 relative):
+//   * mq:  a CTA owns a band of 64 rows, stages Q in 1024-column chunks in shared memory
+//          (Q is read from L2 once per band), a warp accumulates 8 rows x r in registers;
+//   * mtp: a CTA owns 256 columns x a row range (thread = column, coalesced row reads, the
+//          P_hat rows broadcast from shared memory); row ranges are reduced in a fixed order;
+//   * decode: one pass per coordinate over all workers writes r_new = c - own and the
+//          estimate.
+// MGS runs in one CTA in fp64 (column-by-column projections, block reductions), including
+// the reference's canonical-basis completion of degenerate columns.
+#include <cuda_runtime.h>
+
+#include "gc_device.cuh"
+#include "gc_internal.h"
+
+namespace {
+
+constexpr int kMaxRank = 16;
+
+int grid_cap(int64_t g) { return static_cast<int>(g < 1 ? 1 : (g > 65535 ? 65535 : g)); }
+
+// ------------------------------------------------------------------ P = M Q
+template <int R>
+struct MqShape {
+  static constexpr int kRowsPerWarp = R <= 4 ? 8 : 32 / R;   // register budget: rows x R doubles
+  static constexpr int kRowsPerCta = 8 * kRowsPerWarp;
+  static constexpr int kChunk = 4096 / R;                     // 16 KB of Q per stage
+};
+
+template <int R>
+__global__ void __launch_bounds__(256) mq_kernel(int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld,
+                                                 const float *q, float *p) {
+  constexpr int kRowsPerWarp = MqShape<R>::kRowsPerWarp, kChunk = MqShape<R>::kChunk;
+  __shared__ float qs[kChunk * R];
+  const int w = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * MqShape<R>::kRowsPerCta + warp * kRowsPerWarp;
+  const float *cw = c + w * ld;
+  double acc[kRowsPerWarp][R];
+#pragma unroll
+  for (int a = 0; a < kRowsPerWarp; ++a)
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc[a][b] = 0.0;
+  for (int64_t j0 = 0; j0 < cols; j0 += kChunk) {
+    const int nj = static_cast<int>(min(static_cast<int64_t>(kChunk), cols - j0));
+    __syncthreads();
+    for (int e = threadIdx.x; e < nj * R; e += 256) qs[e] = q[j0 * R + e];
+    __syncthreads();
+    for (int jj = lane; jj < nj; jj += 32) {
+      float qv[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) qv[b] = qs[jj * R + b];
+#pragma unroll
+      for (int a = 0; a < kRowsPerWarp; ++a) {
+        const int64_t i = (row0 + a) * cols + j0 + jj;   // flat index into the padded matrix
+        const double m = (row0 + a < rows && i < d) ? static_cast<double>(cw[i]) : 0.0;
+#pragma unroll
+        for (int b = 0; b < R; ++b) acc[a][b] += m * static_cast<double>(qv[b]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < kRowsPerWarp; ++a)
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      double v = acc[a][b];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && row0 + a < rows) p[(w * rows + row0 + a) * R + b] = static_cast<float>(v);
+    }
+}
+
+// ------------------------------------------------------------------ Q = M^T P_hat
+// partial[w][s][col][R] over row range s; then reduced in order s = 0, 1, ...
+template <int R>
+__global__ void __launch_bounds__(256) mtp_kernel(int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld,
+                                                  const float *ph, int64_t rows_per_split, double *partial,
+                                                  int splits) {
+  constexpr int kChunk = R <= 8 ? 512 : 256;
+  __shared__ float ps[kChunk * R];
+  const int w = blockIdx.z;
+  const int s = blockIdx.y;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  const int64_t r0 = s * rows_per_split;
+  const int64_t r1 = min(rows, r0 + rows_per_split);
+  const float *cw = c + w * ld;
+  double acc[R];
+#pragma unroll
+  for (int b = 0; b < R; ++b) acc[b] = 0.0;
+  for (int64_t i0 = r0; i0 < r1; i0 += kChunk) {
+    const int ni = static_cast<int>(min(static_cast<int64_t>(kChunk), r1 - i0));
+    __syncthreads();
+    for (int e = threadIdx.x; e < ni * R; e += 256) ps[e] = ph[i0 * R + e];
+    __syncthreads();
+    if (col < cols) {
+#pragma unroll 4
+      for (int ii = 0; ii < ni; ++ii) {
+        const int64_t i = (i0 + ii) * cols + col;
+        const double m = i < d ? static_cast<double>(__ldcs(cw + i)) : 0.0;
+#pragma unroll
+        for (int b = 0; b < R; ++b) acc[b] += m * static_cast<double>(ps[ii * R + b]);
+      }
+    }
+  }
+  if (col < cols) {
+#pragma unroll
+    for (int b = 0; b < R; ++b) partial[((static_cast<int64_t>(w) * splits + s) * cols + col) * R + b] = acc[b];
+  }
+}
+
+__global__ void mtp_reduce_kernel(int L, int splits, int64_t cols, int R, const double *partial, float *q) {
+  const int64_t total = static_cast<int64_t>(L) * cols * R;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = e / (cols * R), rest = e - w * cols * R;
+    double v = 0.0;
+    for (int s = 0; s < splits; ++s) v += partial[(w * splits + s) * cols * R + rest];
+    q[e] = static_cast<float>(v);
+  }
+}
+
+// ------------------------------------------------------------------ MGS (compressors.py:555-588)
+__device__ double block_sum(double v, double *red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// a: [rows][R] fp64 workspace (row-major, like the reference's (rows, r) array).
+__global__ void __launch_bounds__(1024) mgs_kernel(int64_t rows, int R, const float *in, double *a, float *out,
+                                                   int *status) {
+  __shared__ double red[33];
+  double fro = 0.0;
+  for (int64_t i = threadIdx.x; i < rows * R; i += blockDim.x) {
+    const double v = static_cast<double>(in[i]);
+    a[i] = v;
+    fro += v * v;
+  }
+  fro = block_sum(fro, red);
+  const double scale = sqrt(fro) / fmax(1.0, sqrt(static_cast<double>(R)));
+  const double floor_ = fmax(scale * 1e-8, 1e-300);
+  for (int c = 0; c < R; ++c) {
+    for (int p = 0; p < c; ++p) {   // col -= (a_p . col) a_p, modified Gram-Schmidt
+      double dot = 0.0;
+      for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) dot += a[i * R + p] * a[i * R + c];
+      dot = block_sum(dot, red);
+      for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) a[i * R + c] -= dot * a[i * R + p];
+      __syncthreads();
+    }
+    double nn = 0.0;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) nn += a[i * R + c] * a[i * R + c];
+    const double norm = sqrt(block_sum(nn, red));
+    if (norm > floor_) {
+      for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) a[i * R + c] /= norm;
+      __syncthreads();
+      continue;
+    }
+    // canonical completion: first e_basis whose residual after projection has norm > 0.5
+    bool done = false;
+    for (int64_t basis = 0; basis < rows && !done; ++basis) {
+      // cand = e_basis, then cand -= (a_p . cand) a_p for p < c (recomputed after each step)
+      double cn = 0.0;
+      for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) a[i * R + c] = (i == basis) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int p = 0; p < c; ++p) {
+        double dot = 0.0;
+        for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) dot += a[i * R + p] * a[i * R + c];
+        dot = block_sum(dot, red);
+        for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) a[i * R + c] -= dot * a[i * R + p];
+        __syncthreads();
+      }
+      for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) cn += a[i * R + c] * a[i * R + c];
+      const double cnorm = sqrt(block_sum(cn, red));
+      if (cnorm > 0.5) {
+        for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) a[i * R + c] /= cnorm;
+        done = true;
+      }
+      __syncthreads();
+    }
+    if (!done && threadIdx.x == 0) *status = 1;   // DegenerateMatrixError
+    __syncthreads();
+  }
+  for (int64_t i = threadIdx.x; i < rows * R; i += blockDim.x) out[i] = static_cast<float>(a[i]);
+}
+
+// ------------------------------------------------------------------ decode + EF
+// For flat index i < d: row = i / cols, col = i % cols.
+//   own_w = sum_b P_hat[row][b] * Q_w[col][b]      (p_hat @ r.T, pipelines.py:355)
+//   resid_w = c_w - own_w                          (ef_update, c_w held in resid)
+//   est = (sum_b P_hat[row][b] * Qsum[col][b]) / n (pipelines.py:365)
+template <int R>
+__global__ void __launch_bounds__(256) decode_kernel(int L, int n, int64_t d, int64_t cols, const float *ph,
+                                                     const float *qw, const float *qsum, float *resid, int64_t ld,
+                                                     float *est) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < d;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / cols, col = i - row * cols;
+    float p[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) p[b] = ph[row * R + b];
+    if (resid) {
+      for (int w = 0; w < L; ++w) {
+        double own = 0.0;
+#pragma unroll
+        for (int b = 0; b < R; ++b) own += static_cast<double>(p[b]) * static_cast<double>(qw[(w * cols + col) * R + b]);
+        resid[w * ld + i] = resid[w * ld + i] - static_cast<float>(own);
+      }
+    }
+    if (est) {
+      double e = 0.0;
+#pragma unroll
+      for (int b = 0; b < R; ++b) e += static_cast<double>(p[b]) * static_cast<double>(qsum[col * R + b]);
+      est[i] = static_cast<float>(e) / static_cast<float>(n);
+    }
+  }
+}
+
+// Gram matrix Q^T Q (fp64) for the rank check of ensure_full_rank (compressors.py:595-603).
+__global__ void __launch_bounds__(256) gram_kernel(int64_t cols, int R, const float *q, double *gram) {
+  __shared__ double red[33];
+  for (int a = 0; a < R; ++a)
+    for (int b = a; b < R; ++b) {
+      double v = 0.0;
+      for (int64_t j = threadIdx.x; j < cols; j += blockDim.x)
+        v += static_cast<double>(q[j * R + a]) * static_cast<double>(q[j * R + b]);
+      v = block_sum(v, red);
+      if (threadIdx.x == 0) gram[a * R + b] = gram[b * R + a] = v;
+    }
+}
+
+template <int R>
+int launch_rank(int L, int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld, const float *q, float *p,
+                cudaStream_t st) {
+  constexpr int rpc = MqShape<R>::kRowsPerCta;
+  mq_kernel<R><<<dim3(grid_cap((rows + rpc - 1) / rpc), L), 256, 0, st>>>(d, rows, cols, c, ld, q, p);
+  return GC_OK;
+}
+
+template <int R>
+void launch_mtp(int L, int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld, const float *ph,
+                double *partial, int splits, cudaStream_t st) {
+  const int64_t per = (rows + splits - 1) / splits;
+  mtp_kernel<R><<<dim3(grid_cap((cols + 255) / 256), splits, L), 256, 0, st>>>(d, rows, cols, c, ld, ph, per,
+                                                                              partial, splits);
+}
+
+template <int R>
+void launch_decode(int L, int n, int64_t d, int64_t cols, const float *ph, const float *qw, const float *qsum,
+                   float *resid, int64_t ld, float *est, cudaStream_t st) {
+  const int64_t g = (d + 255) / 256;
+  decode_kernel<R><<<grid_cap(g > 148 * 16 ? 148 * 16 : g), 256, 0, st>>>(L, n, d, cols, ph, qw, qsum, resid, ld,
+                                                                           est);
+}
+
+}  // namespace
+
+extern "C" {
+
+int gc_psgd_splits(int32_t workers, int64_t cols) {
+  const int64_t slabs = (cols + 255) / 256 * workers;
+  int s = static_cast<int>((2 * 148 + slabs - 1) / slabs);
+  return s < 1 ? 1 : (s > 64 ? 64 : s);
+}
+
+int64_t gc_psgd_workspace_bytes(int32_t workers, int64_t rows, int64_t cols, int32_t rank) {
+  const int64_t splits = gc_psgd_splits(workers, cols);
+  return 8 * (static_cast<int64_t>(workers) * splits * cols * rank) + 8 * rows * rank + 256;
+}
+
+int gc_psgd_mq(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c, int64_t ld,
+               const float *q, float *p, void *stream) {
+  GC_REQUIRE(workers >= 1 && workers <= 65535 && d >= 1 && rows * cols >= d && c && q && p, "invalid argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (rank) {
+    case 1: launch_rank<1>(workers, d, rows, cols, c, ld, q, p, st); break;
+    case 2: launch_rank<2>(workers, d, rows, cols, c, ld, q, p, st); break;
+    case 3: launch_rank<3>(workers, d, rows, cols, c, ld, q, p, st); break;
+    case 4: launch_rank<4>(workers, d, rows, cols, c, ld, q, p, st); break;
+    case 5: launch_rank<5>(workers, d, rows, cols, c, ld, q, p, st); break;
+    case 6: launch_rank<6>(workers, d, rows, cols, c, ld, q, p, st); break;
+    case 7: launch_rank<7>(workers, d, rows, cols, c, ld, q, p, st); break;
+    case 8: launch_rank<8>(workers, d, rows, cols, c, ld, q, p, st); break;
+    case 16: launch_rank<16>(workers, d, rows, cols, c, ld, q, p, st); break;
+    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
+  }
+  GC_LAUNCH_CHECK("mq_kernel");
+  return GC_OK;
+}
+
+int gc_psgd_mtp(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c, int64_t ld,
+                const float *p_hat, float *q, void *workspace, void *stream) {
+  GC_REQUIRE(workers >= 1 && workers <= 65535 && d >= 1 && rows * cols >= d && c && p_hat && q && workspace,
+             "invalid argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int splits = gc_psgd_splits(workers, cols);
+  double *partial = static_cast<double *>(workspace);
+  switch (rank) {
+    case 1: launch_mtp<1>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+    case 2: launch_mtp<2>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+    case 3: launch_mtp<3>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+    case 4: launch_mtp<4>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+    case 5: launch_mtp<5>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+    case 6: launch_mtp<6>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+    case 7: launch_mtp<7>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+    case 8: launch_mtp<8>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+    case 16: launch_mtp<16>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
+  }
+  GC_LAUNCH_CHECK("mtp_kernel");
+  const int64_t total = static_cast<int64_t>(workers) * cols * rank;
+  mtp_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(
+      workers, splits, cols, rank, partial, q);
+  GC_LAUNCH_CHECK("mtp_reduce_kernel");
+  return GC_OK;
+}
+
+int gc_psgd_orthonormalize(int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace, int32_t *status,
+                           void *stream) {
+  GC_REQUIRE(rows >= rank && rank >= 1 && rank <= kMaxRank && p && p_hat && workspace && status, "invalid argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  mgs_kernel<<<1, 1024, 0, st>>>(rows, rank, p, static_cast<double *>(workspace), p_hat, status);
+  GC_LAUNCH_CHECK("mgs_kernel");
+  return GC_OK;
+}
+
+int gc_psgd_decode(int32_t workers, int32_t n, int64_t d, int64_t cols, int32_t rank, const float *p_hat,
+                   const float *q_workers, const float *q_sum, float *resid, int64_t ld, float *estimate,
+                   void *stream) {
+  GC_REQUIRE(workers >= 1 && n >= 1 && d >= 1 && cols >= 1 && p_hat, "invalid argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (rank) {
+    case 1: launch_decode<1>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 2: launch_decode<2>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 3: launch_decode<3>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 4: launch_decode<4>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 5: launch_decode<5>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 6: launch_decode<6>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 7: launch_decode<7>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 8: launch_decode<8>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 16: launch_decode<16>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
+  }
+  GC_LAUNCH_CHECK("decode_kernel");
+  return GC_OK;
+}
+
+int gc_psgd_gram(int64_t cols, int32_t rank, const float *q, double *gram, void *stream) {
+  GC_REQUIRE(cols >= 1 && rank >= 1 && rank <= kMaxRank && q && gram, "invalid argument");
+  gram_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(cols, rank, q, gram);
+  GC_LAUNCH_CHECK("gram_kernel");
+  return GC_OK;
+}
+
+int gc_fill_zero(void *ptr, int64_t bytes, void *stream) {
+  GC_REQUIRE(bytes >= 0 && (ptr || bytes == 0), "invalid argument");
+  if (bytes && cudaMemsetAsync(ptr, 0, static_cast<size_t>(bytes), static_cast<cudaStream_t>(stream)) != cudaSuccess) {
+    gc_set_error("cudaMemsetAsync failed");
+    return GC_ERR_CUDA;
+  }
+  return GC_OK;
+}
+
+}  // extern "C"

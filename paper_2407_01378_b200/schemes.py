@@ -14,7 +14,8 @@ import math
 import torch
 
 from . import _native
-from .configs import ChunkedTopKConfig, DenseConfig, PowerSgdConfig, RotatedQuantConfig, TopKConfig
+from .configs import (ChunkedTopKConfig, DenseConfig, PowerSgdConfig, RotatedQuantConfig, TopKConfig,
+                      matrix_shape_for)
 from .ledger import OverflowStats, TrafficLedger
 from .vectors import SeedSpec, next_pow2
 
@@ -283,7 +284,197 @@ class TopKEngine(Engine):
         return est, float(48 * k), _simple_stats(acc)
 
 
+# ------------------------------------------------------------------------- TopK-Chunked
+class ChunkedEngine(Engine):
+    """pipelines.py:213-258 (ChunkedTopKConfig), incl. the permutation ablation."""
+
+    def __init__(self, cfg: ChunkedTopKConfig, n, dim, seeds, device):
+        super().__init__(n, dim, seeds, device)
+        self.cfg = cfg
+        self.C = cfg.chunk_size
+        self.J = cfg.chunks_selected
+        self.nc = -(-dim // self.C)
+        ws = int(_native.lib().gc_topk_workspace_bytes(1, self.nc))
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
+        self._work = None
+
+    def _perm(self, round_index):
+        """coordinate_permutation (transforms.py:129-133): host numpy draw, uploaded."""
+        p = self.seeds.rng("coordinate-permutation", round_index).permutation(self.dim)
+        return torch.from_numpy(p.astype("int64")).to(self.device, non_blocking=True)
+
+    def run(self, grads, res, round_index, ledger, nmse=True):
+        n, d, C, J, nc = self.n, self.dim, self.C, self.J, self.nc
+        sp = _sp()
+        dev = self.device
+        if res is not None:   # corrected = g + r, kept in r until the EF update
+            _native.call("gc_ef_apply", n, d, grads.data_ptr(), res.data_ptr(), grads.stride(0), res.data_ptr(),
+                         res.stride(0), sp)
+            work = res
+        else:
+            work = grads
+        perm = self._perm(round_index) if self.cfg.permute else None
+        pp = _ptr(perm)
+        norms = torch.empty(n, nc, dtype=torch.float32, device=dev)
+        ev = self._ev()
+        if ev:
+            ev[0].record()
+        _native.call("gc_chunk_norms", n, d, C, work.data_ptr(), work.stride(0), pp, norms.data_ptr(), sp)
+        energy = torch.empty(nc, dtype=torch.float32, device=dev)
+        _native.call("gc_float_fold", n, nc, norms.data_ptr(), nc, 0, -(-nc // n), 1, 0, 0, energy.data_ptr(), sp)
+        sel = torch.empty(J, dtype=torch.int32, device=dev)
+        _native.call("gc_topk_select", 1, nc, energy.data_ptr(), nc, J, None, None, sel.data_ptr(), None, 0,
+                     self.ws.data_ptr(), sp)
+        L = J * C
+        packs = torch.empty(n, L, dtype=torch.float32, device=dev)
+        _native.call("gc_chunk_pack", n, d, C, J, sel.data_ptr(), work.data_ptr(), work.stride(0), pp,
+                     packs.data_ptr(), sp)
+        summed = torch.empty(L, dtype=torch.float32, device=dev)
+        _native.call("gc_float_fold", n, L, packs.data_ptr(), L, 0, -(-L // n), 1, 0, 0, summed.data_ptr(), sp)
+        est = torch.empty(d, dtype=torch.float32, device=dev)
+        _native.call("gc_chunk_scatter", d, C, J, sel.data_ptr(), summed.data_ptr(), n, pp, est.data_ptr(), sp)
+        if ev:
+            ev[1].record()
+        self.launches += 14 + (res is not None)
+        acc = None
+        if nmse:
+            acc = torch.zeros(2, dtype=torch.float64, device=dev)
+            self._nmse(work, None, est, acc)
+            self.launches += 1
+        if res is not None:
+            _native.call("gc_chunk_ef_update", n, d, C, J, sel.data_ptr(), packs.data_ptr(), pp, res.data_ptr(),
+                         res.stride(0), sp)
+            self.launches += 1
+        if self.capture:
+            self.last = {"norms": norms, "energy": energy, "selected": sel, "summed": summed}
+        ledger.charge_ring("norm-consensus", n, nc, 16)
+        ledger.charge_ring("chunk-aggregate", n, L, 16)
+        return est, 16.0 * (nc + J * C), _simple_stats(acc)
+
+
+# ----------------------------------------------------------------------------- PowerSGD
+class PowerSgdEngine(Engine):
+    """pipelines.py:324-368 (PowerSgdConfig), warm start and dense bypass included."""
+
+    RANKS = (1, 2, 3, 4, 5, 6, 7, 8, 16)
+
+    def __init__(self, cfg: PowerSgdConfig, n, dim, seeds, device):
+        super().__init__(n, dim, seeds, device)
+        self.cfg = cfg
+        self.rows, self.cols = matrix_shape_for(dim)
+        self.rank = cfg.rank
+        self.bypass = dim < cfg.bypass_below
+        if not self.bypass:
+            if self.rank not in self.RANKS:
+                raise NotImplementedError(f"PowerSGD rank {self.rank} not compiled (supported: {self.RANKS})")
+            if self.rows < self.rank:
+                raise ValueError("need a tall matrix (rows >= cols)")
+            ws = int(_native.lib().gc_psgd_workspace_bytes(n, self.rows, self.cols, self.rank))
+            self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
+            self.mgs_ws = torch.empty(self.rows * self.rank, dtype=torch.float64, device=device)
+        self.warm = None
+
+    def warm_q(self):
+        return self.warm
+
+    def _rank_ok(self, q_dev) -> bool:
+        """np.linalg.matrix_rank(q) == rank (compressors.py:599), via the fp64 Gram matrix on the
+        device; near the numpy tolerance the exact numpy call on a host copy decides."""
+        import numpy as np
+        r, cols = self.rank, self.cols
+        gram = torch.empty(r, r, dtype=torch.float64, device=self.device)
+        _native.call("gc_psgd_gram", cols, r, q_dev.data_ptr(), gram.data_ptr(), _sp())
+        ev = np.clip(np.linalg.eigvalsh(gram.cpu().numpy()), 0.0, None)
+        sig = np.sqrt(ev)
+        tol = sig.max() * max(cols, r) * np.finfo(np.float32).eps
+        if np.all((sig > 2 * tol) | (sig < 0.5 * tol)):
+            return int(np.count_nonzero(sig > tol)) == r
+        return int(np.linalg.matrix_rank(q_dev.cpu().numpy())) == r
+
+    def _seed_q(self, round_index):
+        """Seed matrix with ensure_full_rank's redraws (pipelines.py:341-346, compressors.py:591-603)."""
+        import numpy as np
+        from .configs import DegenerateMatrixError
+        rng = self.seeds.rng("lowrank-seed", round_index)
+        if self.cfg.warm_start and self.warm is not None:
+            q = self.warm
+        else:
+            q = torch.from_numpy(rng.standard_normal((self.cols, self.rank)).astype(np.float32)).to(self.device)
+        for remaining in range(3, -1, -1):
+            if self._rank_ok(q):
+                return q.contiguous()
+            if remaining:
+                q = torch.from_numpy(rng.standard_normal((self.cols, self.rank)).astype(np.float32)).to(self.device)
+        raise DegenerateMatrixError("seed matrix rank-deficient after redraws")
+
+    def run(self, grads, res, round_index, ledger, nmse=True):
+        n, d = self.n, self.dim
+        sp = _sp()
+        dev = self.device
+        est = torch.empty(d, dtype=torch.float32, device=dev)
+        if res is not None:   # corrected lives in r from here on
+            _native.call("gc_ef_apply", n, d, grads.data_ptr(), res.data_ptr(), grads.stride(0), res.data_ptr(),
+                         res.stride(0), sp)
+            c = res
+        else:
+            c = grads
+        ld = c.stride(0)
+        acc = torch.zeros(2, dtype=torch.float64, device=dev) if nmse else None
+        if self.bypass:   # dense fp32 ring (pipelines.py:326-336); own = corrected -> r_new = 0
+            _native.call("gc_float_fold", n, d, c.data_ptr(), ld, 0, -(-d // n), 0, 0, n, est.data_ptr(), sp)
+            if nmse:
+                self._nmse(c, None, est, acc)
+            if res is not None:
+                _native.call("gc_fill_zero", res.data_ptr(), res.numel() * 4, sp)
+            self.launches += 3
+            ledger.charge_ring("dense-bypass", n, d, 32)
+            return est, 32.0 * d, _simple_stats(acc)
+
+        rows, cols, r = self.rows, self.cols, self.rank
+        q = self._seed_q(round_index)
+        ev = self._ev()
+        if ev:
+            ev[0].record()
+        p = torch.empty(n, rows, r, dtype=torch.float32, device=dev)
+        _native.call("gc_psgd_mq", n, d, rows, cols, r, c.data_ptr(), ld, q.data_ptr(), p.data_ptr(), sp)
+        p_sum = torch.empty(rows, r, dtype=torch.float32, device=dev)
+        L1 = rows * r
+        _native.call("gc_float_fold", n, L1, p.data_ptr(), L1, 0, -(-L1 // n), 0, 0, 0, p_sum.data_ptr(), sp)
+        p_hat = torch.empty(rows, r, dtype=torch.float32, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        _native.call("gc_psgd_orthonormalize", rows, r, p_sum.data_ptr(), p_hat.data_ptr(), self.mgs_ws.data_ptr(),
+                     status.data_ptr(), sp)
+        qw = torch.empty(n, cols, r, dtype=torch.float32, device=dev)
+        _native.call("gc_psgd_mtp", n, d, rows, cols, r, c.data_ptr(), ld, p_hat.data_ptr(), qw.data_ptr(),
+                     self.ws.data_ptr(), sp)
+        q_sum = torch.empty(cols, r, dtype=torch.float32, device=dev)
+        L2 = cols * r
+        _native.call("gc_float_fold", n, L2, qw.data_ptr(), L2, 0, -(-L2 // n), 0, 0, 0, q_sum.data_ptr(), sp)
+        _native.call("gc_psgd_decode", n, n, d, cols, r, p_hat.data_ptr(), qw.data_ptr(), q_sum.data_ptr(), None,
+                     ld, est.data_ptr(), sp)
+        if ev:
+            ev[1].record()
+        if nmse:
+            self._nmse(c, None, est, acc)
+        if res is not None:
+            _native.call("gc_psgd_decode", n, n, d, cols, r, p_hat.data_ptr(), qw.data_ptr(), q_sum.data_ptr(),
+                         res.data_ptr(), ld, None, sp)
+        warm = torch.empty(cols, r, dtype=torch.float32, device=dev)
+        _native.call("gc_scale_div", L2, q_sum.data_ptr(), n, warm.data_ptr(), sp)   # pipelines.py:366
+        self.warm = warm
+        self.launches += 12
+        if self.capture:
+            self.last = {"p_hat": p_hat, "q_sum": q_sum, "seed_q": q, "status": status}
+        ledger.charge_ring("left-factor", n, rows * r, 32)
+        ledger.charge_ring("right-factor", n, cols * r, 32)
+        return est, 32.0 * r * (rows + cols), _simple_stats(acc)
+
+
 def make_engine(cfg, n, dim, seeds, device, fused=True) -> Engine:
+    if isinstance(cfg, PowerSgdConfig):
+        return PowerSgdEngine(cfg, n, dim, seeds, device)
+    if isinstance(cfg, ChunkedTopKConfig):
+        return ChunkedEngine(cfg, n, dim, seeds, device)
     if isinstance(cfg, RotatedQuantConfig):
         return ThcEngine(cfg, n, dim, seeds, device, fused)
     if isinstance(cfg, DenseConfig):

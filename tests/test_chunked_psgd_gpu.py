@@ -1,0 +1,97 @@
+"""TopK-Chunked (bit-exact) and PowerSGD (fp32 tolerance) on the GPU vs golden vectors / oracle."""
+import numpy as np
+import pytest
+
+from tests.gpu_util import needs_gpu, oracle_rounds, run_golden_case
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+# north star: PowerSGD floats within 1e-5 relative (fp32).  Relative to the vector's scale:
+# normwise ||ours - ref|| <= 1e-5 ||ref|| and elementwise |ours - ref| <= 1e-5 max|ref|.
+PSGD_TOL = 1e-5
+
+
+def assert_close_fp32(ours, ref, what=""):
+    ours, ref = np.asarray(ours, np.float64), np.asarray(ref, np.float64)
+    scale = float(np.max(np.abs(ref))) if ref.size else 0.0
+    assert np.linalg.norm(ours - ref) <= PSGD_TOL * max(np.linalg.norm(ref), 1e-30), what
+    assert np.max(np.abs(ours - ref), initial=0.0) <= PSGD_TOL * max(scale, 1e-30), what
+
+
+def _ledger(res, n):
+    return {ph: [[res.ledger.bits_sent(worker=w, phase=ph), res.ledger.bits_received(worker=w, phase=ph)]
+                 for w in range(n)] for ph in res.ledger.phases()}
+
+
+@pytest.mark.parametrize("name", ["chunked_a", "chunked_b", "chunked_c"])
+def test_chunked_golden_bit_exact(name):
+    for st, res, pipe, a in run_golden_case(name):
+        r = st["round"]
+        assert np.array_equal(res.estimate.logical, a[f"estimate_{r}"]), f"round {r} estimate"
+        assert np.array_equal(np.stack(pipe.residuals), a[f"residuals_{r}"]), f"round {r} residuals"
+        assert res.nmse == pytest.approx(st["nmse"], rel=1e-9, abs=1e-15)
+        assert res.input_bits_per_coord == pytest.approx(st["input_bits_per_coord"], rel=1e-15)
+        assert _ledger(res, pipe.group.size) == st["ledger"]
+
+
+@pytest.mark.parametrize("n,d,C,J", [(8, 1_000_000, 64, 156), (3, 100_003, 100, 17), (4, 70_000, 7, 1000),
+                                     (2, 65_536, 1024, 8), (5, 4096, 64, 64)])
+def test_chunked_vs_oracle(n, d, C, J):
+    import paper_2407_01378_b200 as gcb
+    seeds = gcb.SeedSpec(21)
+    rng = np.random.default_rng(21)
+    grads = [[(rng.standard_normal(d) * rng.uniform(0.1, 3)).astype(np.float32) for _ in range(n)]
+             for _ in range(2)]
+    outs = oracle_rounds("chunked_topk", dict(chunk_size=C, chunks_selected=J), grads, 21)
+    pipe = gcb.make_pipeline(gcb.ChunkedTopKConfig(C, J), n, d, seeds)
+    pipe._engine.capture = True
+    for r in range(2):
+        res = pipe.run_round(grads[r], r)
+        assert np.array_equal(pipe._engine.last["selected"].cpu().numpy(), outs[r]["selected"])
+        assert np.array_equal(pipe._engine.last["norms"].cpu().numpy(), np.stack(outs[r]["norms"]))
+        assert np.array_equal(res.estimate.logical, outs[r]["estimate"])
+        assert np.array_equal(np.stack(pipe.residuals), np.stack(outs[r]["residuals"]))
+
+
+@pytest.mark.parametrize("name", ["psgd_a", "psgd_b", "psgd_c"])
+def test_psgd_golden_within_tolerance(name):
+    for st, res, pipe, a in run_golden_case(name):
+        r = st["round"]
+        assert_close_fp32(res.estimate.logical, a[f"estimate_{r}"], f"round {r} estimate")
+        assert_close_fp32(np.stack(pipe.residuals), a[f"residuals_{r}"], f"round {r} residuals")
+        if f"warm_q_{r}" in a:
+            assert_close_fp32(pipe._warm_q, a[f"warm_q_{r}"], f"round {r} warm q")
+        assert res.nmse == pytest.approx(st["nmse"], rel=1e-5)
+        assert res.input_bits_per_coord == pytest.approx(st["input_bits_per_coord"], rel=1e-15)
+        assert _ledger(res, pipe.group.size) == st["ledger"]
+
+
+@pytest.mark.parametrize("n,d,rank", [(4, 1_000_000, 4), (2, 350_001, 1), (3, 100_000, 8), (8, 4096, 2),
+                                      (2, 50_000, 16)])
+def test_psgd_vs_oracle_multi_round(n, d, rank):
+    import paper_2407_01378_b200 as gcb
+    seeds = gcb.SeedSpec(31)
+    grads = [[seeds.rng("grad-worker", r, w).standard_normal(d).astype(np.float32) for w in range(n)]
+             for r in range(3)]
+    outs = oracle_rounds("powersgd", dict(rank=rank), grads, 31)
+    pipe = gcb.make_pipeline(gcb.PowerSgdConfig(rank), n, d, seeds)
+    for r in range(3):
+        res = pipe.run_round(grads[r], r)
+        assert_close_fp32(res.estimate.logical, outs[r]["estimate"], f"round {r}")
+        assert_close_fp32(np.stack(pipe.residuals), np.stack(outs[r]["residuals"]), f"round {r} residuals")
+
+
+def test_psgd_zero_gradients_complete_basis_and_redraw():
+    """All-zero gradients: MGS completes with canonical vectors; round 1's warm Q is zero and is redrawn."""
+    import paper_2407_01378_b200 as gcb
+    n, d, rank = 2, 10_000, 4
+    grads = [[np.zeros(d, np.float32) for _ in range(n)] for _ in range(2)]
+    outs = oracle_rounds("powersgd", dict(rank=rank), grads, 41)
+    pipe = gcb.make_pipeline(gcb.PowerSgdConfig(rank), n, d, gcb.SeedSpec(41))
+    pipe._engine.capture = True
+    for r in range(2):
+        res = pipe.run_round(grads[r], r)
+        assert not np.any(res.estimate.logical)
+        ph = pipe._engine.last["p_hat"].cpu().numpy()
+        assert np.array_equal(ph, outs[r]["p_hat"])
+        assert_close_fp32(pipe._engine.last["seed_q"].cpu().numpy(), outs[r]["seed_q"])

@@ -1,0 +1,136 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared symbol, host seeding
+matches the reference's golden vectors, and host-side accounting follows the reference."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.golden_util import CASES, load, seeds
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    import paper_2407_01378_b200 as gcb
+    header = open(os.path.join(ROOT, "include", "gradcomp_b200.h")).read()
+    declared = set(re.findall(r"\b(gc_[a-z0-9_]+)\s*\(", header))
+    lib = gcb._native.lib()
+    missing = [s for s in sorted(declared) if getattr(lib, s, None) is None]
+    assert not missing, missing
+    # and every binding in the Python table is declared in the header
+    assert set(gcb._native.SIGNATURES) <= declared
+    assert not gcb._native.missing_symbols()
+    assert gcb._native.lib().gc_version() >= 1
+
+
+def test_native_seeding_matches_reference():
+    import paper_2407_01378_b200 as gcb
+    s = seeds()
+    for k, v in s["splitmix64"].items():
+        assert gcb.splitmix64(int(k)) == v
+    for k, v in s["fnv1a64"].items():
+        assert gcb.fnv1a64(k) == v
+    spec = gcb.SeedSpec(2024)
+    for entry, pcg in zip(s["stream_seed"], s["pcg"]):
+        assert spec.stream_seed(entry["tag"], entry["round"], entry["worker"]) == entry["seed"]
+        st = spec.pcg(entry["tag"], entry["round"], entry["worker"])
+        assert (st.state, st.inc) == (pcg["state"], pcg["inc"])
+        draws = [(gcb._native.lib().gc_pcg64_next(st) >> 11) * 2.0 ** -53 for _ in range(5)]
+        assert draws == pcg["random5"]
+
+
+def test_native_pcg_advance_matches_numpy():
+    import paper_2407_01378_b200 as gcb
+    spec = gcb.SeedSpec(7)
+    for delta in (0, 1, 12345, 299_999, (1 << 40) + 17):
+        st = spec.pcg("stochastic-round", 3, 1)
+        gcb._native.lib().gc_pcg64_advance(st, delta >> 64, delta & ((1 << 64) - 1))
+        bg = np.random.PCG64(spec.stream_seed("stochastic-round", 3, 1))
+        bg.advance(delta)
+        ref = bg.state["state"]
+        assert (st.state, st.inc) == (ref["state"], ref["inc"])
+
+
+def test_seedspec_validation():
+    import paper_2407_01378_b200 as gcb
+    with pytest.raises(ValueError):
+        gcb.SeedSpec(-1)
+    with pytest.raises(ValueError):
+        gcb.SeedSpec(1).stream_seed("x", -1)
+    with pytest.raises(ValueError):
+        gcb.SeedSpec(1).stream_seed("x", 0, -2)
+
+
+def test_config_validation_matches_reference():
+    import paper_2407_01378_b200 as gcb
+    bad = [lambda: gcb.TopKConfig(0), lambda: gcb.ChunkedTopKConfig(0, 1), lambda: gcb.RotatedQuantConfig(1, 4),
+           lambda: gcb.RotatedQuantConfig(9, 9), lambda: gcb.RotatedQuantConfig(4, 3),
+           lambda: gcb.RotatedQuantConfig(4, 33), lambda: gcb.RotatedQuantConfig(4, 4, 3),
+           lambda: gcb.RotatedQuantConfig(4, 4, 1), lambda: gcb.PowerSgdConfig(0),
+           lambda: gcb.PowerSgdConfig(1, bypass_below=-1), lambda: gcb.DenseConfig(8)]
+    for f in bad:
+        with pytest.raises(ValueError):
+            f()
+    assert gcb.scheme_label(gcb.ChunkedTopKConfig(4, 1, True)) == "chunked_topk_perm"
+    assert gcb.scheme_label(gcb.DenseConfig(32)) == "dense_fp32"
+    with pytest.raises(TypeError):
+        gcb.scheme_label(object())
+    assert gcb.matrix_shape_for(4096) == (64, 64)
+    assert gcb.matrix_shape_for(10) == (4, 3)
+    assert gcb.matrix_shape_for(350_000_000) == (18709, 18708)
+    assert gcb.topk_for_budget(1000, 0.48) == 10
+    assert gcb.chunks_for_budget(6400, 64, 1.0) == 5   # same as the reference solver
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_ledger_closed_forms_match_reference(name):
+    """The ledger charges of every golden round follow from the reference's closed forms."""
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.ledger import TrafficLedger
+    scheme, params = CASES[name]
+    meta, _ = load(name)
+    n, d = meta["n"], meta["d"]
+    for st in meta["stats"]:
+        led = TrafficLedger()
+        if scheme == "rotated_quant":
+            P = 1 << (d - 1).bit_length()
+            B = 1 << min(P.bit_length() - 1, params["rotation_block"].bit_length() - 1)
+            led.charge_ring("range-consensus", n, P // B, 32)
+            led.charge_ring("range-consensus", n, P // B, 32)
+            led.charge_ring("code-aggregate", n, P, params["wire_bits"])
+        elif scheme == "topk":
+            led.charge_gather("sparse-gather", [48 * params["k"]] * n)
+        elif scheme == "chunked_topk":
+            nc = -(-d // params["chunk_size"])
+            led.charge_ring("norm-consensus", n, nc, 16)
+            led.charge_ring("chunk-aggregate", n, params["chunks_selected"] * params["chunk_size"], 16)
+        elif scheme == "powersgd":
+            if d < params.get("bypass_below", 4096):
+                led.charge_ring("dense-bypass", n, d, 32)
+            else:
+                rows, cols = gcb.matrix_shape_for(d)
+                led.charge_ring("left-factor", n, rows * params["rank"], 32)
+                led.charge_ring("right-factor", n, cols * params["rank"], 32)
+        else:
+            led.charge_ring("dense", n, d, params["bits"])
+        got = {ph: [[led.bits_sent(worker=w, phase=ph), led.bits_received(worker=w, phase=ph)] for w in range(n)]
+               for ph in led.phases()}
+        assert got == st["ledger"]
+        assert led.max_egress_bits() == st["max_egress_bits"]
+
+
+def test_overflow_rate_and_ledger_api():
+    from paper_2407_01378_b200.ledger import OverflowStats, TrafficLedger, overflow_rate
+    assert overflow_rate(OverflowStats()) == 0.0
+    assert overflow_rate(OverflowStats(3, 12, 1.0)) == 0.25
+    led = TrafficLedger()
+    led.add("a", 0, sent=5)
+    led.add("b", 1, received=7)
+    other = TrafficLedger()
+    other.add("a", 0, sent=1, received=2)
+    led.merge(other)
+    assert led.bits_sent(worker=0) == 6 and led.bits_received(phase="b") == 7
+    assert led.to_csv().splitlines()[0] == "phase,worker,bits_sent,bits_received"
+    with pytest.raises(ValueError):
+        led.add("a", 0, sent=-1)
