@@ -1,0 +1,506 @@
+"""Multi-GPU GradientPipeline: one process per GPU, n logical workers split over the ranks.
+
+Reference semantics are those of the simulated ring (pipelines.py:201-393,
+collectives.py:177-263): worker w of the reference is global worker w = rank * L + l here
+(L = n / world local workers per rank, all sharing one GPU's kernels).  The exchange steps
+are the ones SURVEY.md §8(e) derives from the reference:
+
+* THC: range consensus = all-reduce MAX of (-lo, hi) (min/max are order-free, exact);
+  saturating code sums = all-to-all of 1/world slices of the codes -> ring-ordered
+  saturating fold of the slice (gc_sat_fold, start worker floor(i / ceil(P/n)) as in the
+  reference's padded ring partition) -> all-gather of the summed slices.  NCCL's wrapping
+  int8 sum cannot reproduce the clamp-per-hop order, so it is not used for codes.
+* TopK: all-gather of the (index, value) payloads, ordered scatter-add (worker-id order).
+* TopK-Chunked: all-gather of the fp16 chunk energies and of the chunk packs, then the
+  fp16-wire ring fold locally (bit-exact selection and sums).
+* PowerSGD: all-gather of the P and Q factors (rows*r and cols*r floats) and the fp32 ring
+  fold locally, so P_hat / Q_sum are bit-identical on every rank and to the reference order.
+* Dense FP16 / FP32 (the utility bar): NCCL all-reduce in half / float (tolerance-level
+  agreement; this is the baseline the compressed schemes are measured against).
+
+Collectives go through `Comm`, a thin layer over torch.distributed: NCCL with CUDA tensors,
+or gloo with host staging (used by the CPU tests of the exchange plan and by the
+two-process single-GPU tests).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native
+from .configs import (
+    ChunkedTopKConfig, DenseConfig, PowerSgdConfig, RotatedQuantConfig, TopKConfig, matrix_shape_for, scheme_label,
+)
+from .ledger import OverflowStats, TrafficLedger, WorkerGroup
+from .pipeline import RoundResult
+from .schemes import RoundStats, _simple_stats, nmse_from
+from .vectors import ChunkGeometry, GradientVector, SeedSpec, next_pow2
+
+
+def _sp() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+class Comm:
+    """Collectives used by the exchange plan (NCCL on CUDA tensors, gloo with host staging)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.stage = dist.get_backend(group) != "nccl"
+
+    def _run(self, fn, out, *ins):
+        if self.stage and out.is_cuda:
+            h_out = torch.empty(out.shape, dtype=out.dtype)
+            fn(h_out, *[x.cpu() for x in ins])
+            out.copy_(h_out)
+        else:
+            fn(out, *ins)
+        return out
+
+    def all_gather_rows(self, x: torch.Tensor) -> torch.Tensor:
+        """[L, ...] per rank -> [world * L, ...] in rank order (global worker order)."""
+        x = x.contiguous()
+        out = torch.empty((self.world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        if self.world == 1:
+            out.copy_(x)
+            return out
+        return self._run(lambda o, i: dist.all_gather_into_tensor(o, i, group=self.group), out, x)
+
+    def all_to_all(self, send: torch.Tensor) -> torch.Tensor:
+        """send [world, ...]: chunk r goes to rank r; returns recv [world, ...], chunk r from rank r."""
+        recv = torch.empty_like(send)
+        if self.world == 1:
+            recv.copy_(send)
+            return recv
+        return self._run(lambda o, i: dist.all_to_all_single(o, i, group=self.group), recv, send.contiguous())
+
+    def all_reduce(self, t: torch.Tensor, op) -> torch.Tensor:
+        if self.world == 1:
+            return t
+        if self.stage and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, op=op, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op, group=self.group)
+        return t
+
+
+def fold_slices(active: int, world: int, align: int = 256):
+    """Length of the equal per-rank slices of the code vector for the all-to-all fold."""
+    s = -(-active // world)
+    s = -(-s // align) * align
+    return s
+
+
+def exchange_fold(codes: torch.Tensor, comm: Comm, n: int, active: int, slice_len: int, fold_fn, out_dtype,
+                  send: torch.Tensor | None = None) -> torch.Tensor:
+    """Saturating code sums over all n workers, reference ring order (collectives.py:215-235).
+
+    codes: this rank's [L, active] int8 codes (global workers rank*L .. rank*L+L-1).  Slice
+    r = [r*S, (r+1)*S) of every worker goes to rank r (all-to-all); rank r folds its slice
+    over the n worker rows with fold_fn(rows [n, S], length, offset) -> sums [S]; the summed
+    slices are all-gathered.  Returns sums [world*S] (entries >= active are zero)."""
+    W, L = comm.world, codes.shape[0]
+    if send is None:
+        send = torch.zeros(W, L, slice_len, dtype=codes.dtype, device=codes.device)
+    for dst in range(W):
+        lo, hi = dst * slice_len, min(active, (dst + 1) * slice_len)
+        if hi > lo:
+            send[dst, :, : hi - lo].copy_(codes[:, lo:hi])
+    recv = comm.all_to_all(send).reshape(n, slice_len)
+    s0 = comm.rank * slice_len
+    my_len = max(0, min(slice_len, active - s0))
+    sums = torch.zeros(slice_len, dtype=out_dtype, device=codes.device)
+    if my_len:
+        fold_fn(recv, my_len, s0, sums)
+    return comm.all_gather_rows(sums.reshape(1, -1)).reshape(-1)
+
+
+class DistributedGradientPipeline:
+    """GradientPipeline (pipelines.py:97-393) over torch.distributed ranks.
+
+    num_workers is the global n; each rank passes its L = n / world local gradients to
+    run_round (a [L, d] tensor or a list); the returned estimate is identical on every rank.
+    Local residuals (`residuals`) belong to the rank's own workers.
+    """
+
+    def __init__(self, config, num_workers: int, dim: int, seeds: SeedSpec, error_feedback: bool | None = None, *,
+                 group=None, device=None, validate: bool = True, compute_nmse: bool = False):
+        if num_workers < 1:
+            raise ValueError("num_workers must be positive")
+        if dim < 1:
+            raise ValueError("dim must be positive")
+        self.comm = Comm(group)
+        if num_workers % self.comm.world:
+            raise ValueError("num_workers must be a multiple of the number of ranks")
+        self.config = config
+        self.scheme = scheme_label(config)
+        self.group = WorkerGroup(num_workers)
+        self.dim = dim
+        self.seeds = seeds
+        self.L = num_workers // self.comm.world
+        self.w0 = self.comm.rank * self.L
+        if isinstance(config, DenseConfig):
+            if error_feedback:
+                raise ValueError("dense baselines do not carry error feedback")
+            error_feedback = False
+        elif error_feedback is None:
+            error_feedback = True
+        self.error_feedback = bool(error_feedback)
+        if isinstance(config, TopKConfig) and config.k > dim:
+            raise ValueError("k exceeds the dimension")
+        if isinstance(config, ChunkedTopKConfig):
+            if config.chunks_selected > ChunkGeometry.for_dim(dim, config.chunk_size).num_chunks:
+                raise ValueError("chunks_selected exceeds the chunk count")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.validate = validate
+        self.compute_nmse = compute_nmse
+        self._res = (torch.zeros(self.L, dim, dtype=torch.float32, device=self.device) if self.error_feedback
+                     else None)
+        self._stage = None
+        self._engine = _make(config, self)
+
+    # state --------------------------------------------------------------------------
+    @property
+    def residuals(self):
+        if self._res is None:
+            return None
+        h = self._res.cpu().numpy()
+        return [h[i].copy() for i in range(self.L)]
+
+    @property
+    def residuals_tensor(self):
+        return self._res
+
+    @property
+    def _warm_q(self):
+        wq = getattr(self._engine, "warm", None)
+        return None if wq is None else wq.cpu().numpy()
+
+    # round ---------------------------------------------------------------------------
+    def run_round(self, local_grads, round_index: int) -> RoundResult:
+        g = self._checked(local_grads)
+        ledger = TrafficLedger()
+        est, bits, stats = self._engine.run(g, self._res, round_index, ledger, self.compute_nmse)
+        return RoundResult(self.scheme, round_index, est, self.dim, ledger, bits, stats)
+
+    def _checked(self, local_grads) -> torch.Tensor:
+        L, d = self.L, self.dim
+        if torch.is_tensor(local_grads) and local_grads.dim() == 2:
+            if tuple(local_grads.shape) != (L, d):
+                raise ValueError("need [local_workers, dim] gradients")
+            g = local_grads
+            if g.device != self.device or not g.is_contiguous() or g.dtype != torch.float32:
+                g = self._buf().copy_(g, non_blocking=True)
+        else:
+            if len(local_grads) != L:
+                raise ValueError("need exactly one gradient per local worker")
+            g = self._buf()
+            for i, x in enumerate(local_grads):
+                if isinstance(x, GradientVector):
+                    x = x.tensor if x.tensor is not None else x.logical
+                t = x if torch.is_tensor(x) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+                if t.dim() != 1 or t.numel() != d:
+                    raise ValueError("gradient length does not match the pipeline dim")
+                g[i].copy_(t, non_blocking=True)
+        if self.validate:
+            bad = torch.zeros(1, dtype=torch.int64, device=self.device)
+            _native.call("gc_check_finite", L, g.data_ptr(), g.stride(0), d, bad.data_ptr(), _sp())
+            self.comm.all_reduce(bad, dist.ReduceOp.SUM)
+            self._engine.launches += 1
+            if int(bad.item()):
+                raise ValueError("gradients must be finite")
+        return g
+
+    def _buf(self):
+        if self._stage is None:
+            self._stage = torch.empty(self.L, self.dim, dtype=torch.float32, device=self.device)
+        return self._stage
+
+
+# ======================================================================================
+class _Base:
+    def __init__(self, pipe: DistributedGradientPipeline):
+        self.p = pipe
+        self.n, self.L, self.w0, self.dim = pipe.group.size, pipe.L, pipe.w0, pipe.dim
+        self.comm, self.dev, self.seeds = pipe.comm, pipe.device, pipe.seeds
+        self.launches = 0
+        self.kernel_events = None
+
+    def _ev(self):
+        if self.kernel_events is None:
+            return None
+        e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self.kernel_events.append(e)
+        return e
+
+
+class _Thc(_Base):
+    def __init__(self, cfg: RotatedQuantConfig, pipe):
+        super().__init__(pipe)
+        self.cfg = cfg
+        d = self.dim
+        P = next_pow2(d)
+        B = 1 << min(P.bit_length() - 1, cfg.rotation_block.bit_length() - 1)
+        self.P, self.B = P, B
+        self.geom = _native.ThcGeom(d, P, B, cfg.quant_bits, cfg.wire_bits, float(B) ** -0.5)
+        self.active = int(_native.lib().gc_thc_active_len(ctypes.byref(self.geom)))
+        self.nb = self.active // B
+        self.ring_blk = -(-P // self.n)
+        self.S = fold_slices(self.active, self.comm.world)
+        self.sum_bytes = 1 if cfg.wire_bits <= 8 else (2 if cfg.wire_bits <= 16 else 4)
+        self.sum_dtype = {1: torch.int8, 2: torch.int16, 4: torch.int32}[self.sum_bytes]
+        ws = int(_native.lib().gc_thc_workspace_bytes(ctypes.byref(self.geom), self.L))
+        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=self.dev) if ws else None
+        L, W = self.L, self.comm.world
+        self.signs = torch.empty(-(-self.active // 32), dtype=torch.int32, device=self.dev)
+        self.x_rot = torch.empty(L, self.active, dtype=torch.float32, device=self.dev)
+        self.ranges = torch.empty(L, self.nb, 2, dtype=torch.float32, device=self.dev)
+        self.codes = torch.empty(L, self.active, dtype=torch.int8, device=self.dev)
+        self.send = torch.zeros(W, L, self.S, dtype=torch.int8, device=self.dev)
+
+    def run(self, g, res, r, ledger, nmse):
+        n, L, cfg, comm = self.n, self.L, self.cfg, self.comm
+        sp = _sp()
+        geom = ctypes.byref(self.geom)
+        rot = self.seeds.pcg("rotation-signs", r)
+        _native.call("gc_thc_signs", ctypes.byref(rot), self.active, self.signs.data_ptr(), sp)
+        coins = (_native.Pcg64 * L)()
+        for l in range(L):
+            coins[l] = self.seeds.pcg("stochastic-round", r, self.w0 + l)
+        ev = self._ev()
+        if ev:
+            ev[0].record()
+        _native.call("gc_thc_rotate", geom, L, g.data_ptr(), _ptr(res), g.stride(0), self.signs.data_ptr(),
+                     self.x_rot.data_ptr(), self.ranges.data_ptr(), _ptr(self.ws), sp)
+        shared = torch.empty(self.nb, 2, dtype=torch.float32, device=self.dev)
+        _native.call("gc_range_consensus", L, self.nb, self.ranges.data_ptr(), shared.data_ptr(), sp)
+        # ElemMin / ElemMax ring (pipelines.py:271-288) as one all-reduce MAX of (-lo, hi)
+        shared[:, 0].neg_()
+        comm.all_reduce(shared, dist.ReduceOp.MAX)
+        shared[:, 0].neg_()
+        counters = torch.zeros(4, dtype=torch.int64, device=self.dev)
+        _native.call("gc_thc_quantize", geom, L, self.x_rot.data_ptr(), shared.data_ptr(), coins,
+                     self.codes.data_ptr(), counters.data_ptr(), sp)
+        # codes -> per-destination slices -> all-to-all -> ordered saturating fold -> all-gather
+
+        def fold(rows, length, offset, out):
+            if n > 1:
+                _native.call("gc_sat_fold", n, length, rows.data_ptr(), rows.stride(0), offset, self.ring_blk,
+                             cfg.wire_bits, out.data_ptr(), counters[3:].data_ptr(), sp)
+            else:
+                out[:length].copy_(rows[0, :length])
+
+        sums = exchange_fold(self.codes, comm, n, self.active, self.S, fold, self.sum_dtype, self.send)
+        est = torch.empty(self.dim, dtype=torch.float32, device=self.dev)
+        _native.call("gc_thc_decode_estimate", geom, n, sums.data_ptr(), self.sum_bytes, shared.data_ptr(),
+                     self.signs.data_ptr(), est.data_ptr(), _ptr(self.ws), sp)
+        if res is not None:
+            _native.call("gc_thc_decode_ef", geom, L, self.codes.data_ptr(), shared.data_ptr(), self.signs.data_ptr(),
+                         g.data_ptr(), res.data_ptr(), res.stride(0), _ptr(self.ws), sp)
+        if ev:
+            ev[1].record()
+        comm.all_reduce(counters, dist.ReduceOp.SUM)   # clamp count, sum z, sum z^2, clips
+        self.launches += 7
+        num_blocks = self.P // self.B
+        ledger.charge_ring("range-consensus", n, num_blocks, 32)
+        ledger.charge_ring("range-consensus", n, num_blocks, 32)
+        ledger.charge_ring("code-aggregate", n, self.P, cfg.wire_bits)
+        total = n * self.P
+        total_adds = (n - 1) * self.ring_blk * n if n > 1 else 0
+
+        def finalize(c, m):
+            var = (total * c[2] - c[1] * c[1]) / (total * total)
+            return {"nmse": float("nan"), "range_clips": int(c[0]),
+                    "overflow": OverflowStats(int(c[3]), int(total_adds), math.sqrt(max(var, 0.0)))}
+
+        return est, float(cfg.wire_bits * self.P + 64 * num_blocks), RoundStats(counters, None, finalize)
+
+
+class _TopK(_Base):
+    def __init__(self, cfg: TopKConfig, pipe):
+        super().__init__(pipe)
+        self.k = cfg.k
+        ws = int(_native.lib().gc_topk_workspace_bytes(self.L, self.dim))
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=self.dev)
+
+    def run(self, g, res, r, ledger, nmse):
+        L, k, d, n = self.L, self.k, self.dim, self.n
+        sp = _sp()
+        idx = torch.empty(L, k, dtype=torch.int32, device=self.dev)
+        val = torch.empty(L, k, dtype=torch.float32, device=self.dev)
+        _native.call("gc_topk_select", L, d, None, g.stride(0), k, g.data_ptr(), _ptr(res), idx.data_ptr(),
+                     val.data_ptr(), 1, self.ws.data_ptr(), sp)
+        all_idx = self.comm.all_gather_rows(idx)     # all_gather (collectives.py:239-263)
+        all_val = self.comm.all_gather_rows(val)
+        est = torch.empty(d, dtype=torch.float32, device=self.dev)
+        _native.call("gc_sparse_accumulate", n, k, all_idx.data_ptr(), all_val.data_ptr(), d, est.data_ptr(), sp)
+        _native.call("gc_scale_div", d, est.data_ptr(), n, est.data_ptr(), sp)
+        if res is not None:
+            _native.call("gc_sparse_ef_update", L, k, idx.data_ptr(), val.data_ptr(), res.data_ptr(), res.stride(0),
+                         sp)
+        self.launches += 11 + n
+        ledger.charge_gather("sparse-gather", [48 * k] * n)
+        return est, float(48 * k), _simple_stats(None)
+
+
+class _Chunked(_Base):
+    def __init__(self, cfg: ChunkedTopKConfig, pipe):
+        super().__init__(pipe)
+        self.cfg = cfg
+        self.C, self.J = cfg.chunk_size, cfg.chunks_selected
+        self.nc = -(-self.dim // self.C)
+        ws = int(_native.lib().gc_topk_workspace_bytes(1, self.nc))
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=self.dev)
+
+    def run(self, g, res, r, ledger, nmse):
+        L, n, d, C, J, nc = self.L, self.n, self.dim, self.C, self.J, self.nc
+        sp = _sp()
+        if res is not None:
+            _native.call("gc_ef_apply", L, d, g.data_ptr(), res.data_ptr(), g.stride(0), res.data_ptr(),
+                         res.stride(0), sp)
+            work = res
+        else:
+            work = g
+        perm = None
+        if self.cfg.permute:
+            p = self.seeds.rng("coordinate-permutation", r).permutation(d)
+            perm = torch.from_numpy(p.astype(np.int64)).to(self.dev)
+        pp = _ptr(perm)
+        norms = torch.empty(L, nc, dtype=torch.float32, device=self.dev)
+        _native.call("gc_chunk_norms", L, d, C, work.data_ptr(), work.stride(0), pp, norms.data_ptr(), sp)
+        all_norms = self.comm.all_gather_rows(norms)
+        energy = torch.empty(nc, dtype=torch.float32, device=self.dev)
+        _native.call("gc_float_fold", n, nc, all_norms.data_ptr(), nc, 0, -(-nc // n), 1, 0, 0, energy.data_ptr(), sp)
+        sel = torch.empty(J, dtype=torch.int32, device=self.dev)
+        _native.call("gc_topk_select", 1, nc, energy.data_ptr(), nc, J, None, None, sel.data_ptr(), None, 0,
+                     self.ws.data_ptr(), sp)
+        Lc = J * C
+        packs = torch.empty(L, Lc, dtype=torch.float32, device=self.dev)
+        _native.call("gc_chunk_pack", L, d, C, J, sel.data_ptr(), work.data_ptr(), work.stride(0), pp,
+                     packs.data_ptr(), sp)
+        all_packs = self.comm.all_gather_rows(packs)
+        summed = torch.empty(Lc, dtype=torch.float32, device=self.dev)
+        _native.call("gc_float_fold", n, Lc, all_packs.data_ptr(), Lc, 0, -(-Lc // n), 1, 0, 0, summed.data_ptr(), sp)
+        est = torch.empty(d, dtype=torch.float32, device=self.dev)
+        _native.call("gc_chunk_scatter", d, C, J, sel.data_ptr(), summed.data_ptr(), n, pp, est.data_ptr(), sp)
+        if res is not None:
+            _native.call("gc_chunk_ef_update", L, d, C, J, sel.data_ptr(), packs.data_ptr(), pp, res.data_ptr(),
+                         res.stride(0), sp)
+        self.launches += 16
+        ledger.charge_ring("norm-consensus", n, nc, 16)
+        ledger.charge_ring("chunk-aggregate", n, Lc, 16)
+        return est, 16.0 * (nc + J * C), _simple_stats(None)
+
+
+class _PowerSgd(_Base):
+    def __init__(self, cfg: PowerSgdConfig, pipe):
+        super().__init__(pipe)
+        from .schemes import PowerSgdEngine
+        # reuse the simulated engine's seed / rank logic with the local worker count
+        self.local = PowerSgdEngine(cfg, self.L, self.dim, self.seeds, self.dev)
+        self.local.n = self.L
+        self.cfg = cfg
+        self.rows, self.cols, self.r = self.local.rows, self.local.cols, cfg.rank
+        self.warm = None
+
+    def run(self, g, res, r, ledger, nmse):
+        L, n, d = self.L, self.n, self.dim
+        sp = _sp()
+        est = torch.empty(d, dtype=torch.float32, device=self.dev)
+        if res is not None:
+            _native.call("gc_ef_apply", L, d, g.data_ptr(), res.data_ptr(), g.stride(0), res.data_ptr(),
+                         res.stride(0), sp)
+            c = res
+        else:
+            c = g
+        ld = c.stride(0)
+        if self.local.bypass:
+            all_c = self.comm.all_gather_rows(c)
+            _native.call("gc_float_fold", n, d, all_c.data_ptr(), d, 0, -(-d // n), 0, 0, n, est.data_ptr(), sp)
+            if res is not None:
+                _native.call("gc_fill_zero", res.data_ptr(), res.numel() * 4, sp)
+            ledger.charge_ring("dense-bypass", n, d, 32)
+            return est, 32.0 * d, _simple_stats(None)
+        rows, cols, rk = self.rows, self.cols, self.r
+        self.local.warm = self.warm
+        q = self.local._seed_q(r)
+        p = torch.empty(L, rows, rk, dtype=torch.float32, device=self.dev)
+        _native.call("gc_psgd_mq", L, d, rows, cols, rk, c.data_ptr(), ld, q.data_ptr(), p.data_ptr(), sp)
+        all_p = self.comm.all_gather_rows(p)
+        L1 = rows * rk
+        p_sum = torch.empty(rows, rk, dtype=torch.float32, device=self.dev)
+        _native.call("gc_float_fold", n, L1, all_p.data_ptr(), L1, 0, -(-L1 // n), 0, 0, 0, p_sum.data_ptr(), sp)
+        p_hat = torch.empty(rows, rk, dtype=torch.float32, device=self.dev)
+        status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        _native.call("gc_psgd_orthonormalize", rows, rk, p_sum.data_ptr(), p_hat.data_ptr(),
+                     self.local.mgs_ws.data_ptr(), status.data_ptr(), sp)
+        qw = torch.empty(L, cols, rk, dtype=torch.float32, device=self.dev)
+        _native.call("gc_psgd_mtp", L, d, rows, cols, rk, c.data_ptr(), ld, p_hat.data_ptr(), qw.data_ptr(),
+                     self.local.ws.data_ptr(), sp)
+        all_q = self.comm.all_gather_rows(qw)
+        L2 = cols * rk
+        q_sum = torch.empty(cols, rk, dtype=torch.float32, device=self.dev)
+        _native.call("gc_float_fold", n, L2, all_q.data_ptr(), L2, 0, -(-L2 // n), 0, 0, 0, q_sum.data_ptr(), sp)
+        _native.call("gc_psgd_decode", L, n, d, cols, rk, p_hat.data_ptr(), qw.data_ptr(), q_sum.data_ptr(),
+                     _ptr(res), ld, est.data_ptr(), sp)
+        warm = torch.empty(cols, rk, dtype=torch.float32, device=self.dev)
+        _native.call("gc_scale_div", L2, q_sum.data_ptr(), n, warm.data_ptr(), sp)
+        self.warm = warm
+        self.launches += 11
+        ledger.charge_ring("left-factor", n, rows * rk, 32)
+        ledger.charge_ring("right-factor", n, cols * rk, 32)
+        return est, 32.0 * rk * (rows + cols), _simple_stats(None)
+
+
+class _Dense(_Base):
+    """The FP16 / FP32 NCCL all-reduce utility bar (pipelines.py:370-393 up to summation order)."""
+
+    def __init__(self, cfg: DenseConfig, pipe):
+        super().__init__(pipe)
+        self.bits = cfg.bits
+
+    def run(self, g, res, r, ledger, nmse):
+        L, n, d = self.L, self.n, self.dim
+        sp = _sp()
+        local = torch.empty(d, dtype=torch.float32, device=self.dev)
+        w16 = 1 if self.bits == 16 else 0
+        # local workers first (fp16 inputs and wire for the FP16 bar), then the NCCL sum
+        _native.call("gc_float_fold", L, d, g.data_ptr(), g.stride(0), 0, d, w16, w16, 0, local.data_ptr(), sp)
+        if self.bits == 16:
+            wire = local.half()
+            self.comm.all_reduce(wire, dist.ReduceOp.SUM)
+            total = wire.float()
+        else:
+            total = self.comm.all_reduce(local, dist.ReduceOp.SUM)
+        est = torch.empty(d, dtype=torch.float32, device=self.dev)
+        _native.call("gc_scale_div", d, total.data_ptr(), n, est.data_ptr(), sp)
+        self.launches += 2
+        ledger.charge_ring("dense", n, d, self.bits)
+        return est, float(self.bits) * d, _simple_stats(None)
+
+
+def _make(cfg, pipe):
+    if isinstance(cfg, RotatedQuantConfig):
+        return _Thc(cfg, pipe)
+    if isinstance(cfg, TopKConfig):
+        return _TopK(cfg, pipe)
+    if isinstance(cfg, ChunkedTopKConfig):
+        return _Chunked(cfg, pipe)
+    if isinstance(cfg, PowerSgdConfig):
+        return _PowerSgd(cfg, pipe)
+    if isinstance(cfg, DenseConfig):
+        return _Dense(cfg, pipe)
+    raise TypeError(f"unknown config type {type(cfg).__name__}")

@@ -1,0 +1,67 @@
+"""Two ranks on one B200 (gloo with host staging) running DistributedGradientPipeline for
+n = 4 workers (2 per rank) against the oracle of the reference ring: bit-exact for THC,
+TopK and TopK-Chunked, 1e-5 for PowerSGD, fp16 / fp32 tolerance for the dense bar."""
+import numpy as np
+import pytest
+import torch
+
+from tests.dist_util import run_world
+from tests.gpu_util import needs_gpu, oracle_rounds
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+N, D, SEED = 4, 100_003, 77
+
+
+def _grads(r):
+    from oracle import gradcomp_oracle as orc
+    return [orc.stream_rng(SEED, "grad-worker", r, w).standard_normal(D).astype(np.float32) for w in range(N)]
+
+
+def _run_rank(rank, world, scheme, params):
+    import torch
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.distributed import DistributedGradientPipeline
+    from tests.gpu_util import config_for
+    torch.cuda.set_device(0)
+    L = N // world
+    ef = None if scheme != "dense" else False
+    pipe = DistributedGradientPipeline(config_for(scheme, params), N, D, gcb.SeedSpec(SEED), ef)
+    out = []
+    for r in range(2):
+        g = _grads(r)[rank * L:(rank + 1) * L]
+        res = pipe.run_round(g, r)
+        out.append({"est": res.estimate.logical.copy(), "res": pipe.residuals,
+                    "clips": res.overflow.clip_events, "adds": res.overflow.total_adds})
+    return out
+
+
+@pytest.mark.parametrize("scheme,params,exact", [
+    ("rotated_quant", dict(quant_bits=4, wire_bits=4, rotation_block=1024), True),
+    ("rotated_quant", dict(quant_bits=3, wire_bits=9, rotation_block=256), True),
+    ("topk", dict(k=1000), True),
+    ("chunked_topk", dict(chunk_size=64, chunks_selected=50), True),
+    ("powersgd", dict(rank=4), False),
+    ("dense", dict(bits=32), False),
+    ("dense", dict(bits=16), False),
+])
+def test_two_ranks_match_reference(scheme, params, exact):
+    res = run_world(_run_rank, 2, (scheme, params))
+    ef = scheme != "dense"
+    outs = oracle_rounds(scheme, params, [_grads(r) for r in range(2)], SEED, ef=ef)
+    for r in range(2):
+        e0, e1 = res[0][r]["est"], res[1][r]["est"]
+        assert np.array_equal(e0, e1), "ranks disagree on the estimate"
+        ref = outs[r]["estimate"]
+        if exact:
+            assert np.array_equal(e0, ref), (scheme, r)
+            if ef:
+                mine = np.stack(res[0][r]["res"] + res[1][r]["res"])
+                assert np.array_equal(mine, np.stack(outs[r]["residuals"]))
+            if scheme == "rotated_quant":
+                assert res[0][r]["clips"] == outs[r]["clip_events"]
+                assert res[0][r]["adds"] == outs[r]["total_adds"]
+        else:
+            tol = 1e-3 if params.get("bits") == 16 else 1e-5
+            err = np.linalg.norm(e0.astype(np.float64) - ref) / np.linalg.norm(ref)
+            assert err <= tol, (scheme, r, err)
