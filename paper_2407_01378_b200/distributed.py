@@ -69,21 +69,28 @@ class Comm:
         return out
 
     def all_gather_rows(self, x: torch.Tensor) -> torch.Tensor:
-        """[L, ...] per rank -> [world * L, ...] in rank order (global worker order)."""
+        """[L, ...] per rank -> [world * L, ...] in rank order (global worker order).
+
+        Pure data movement, done on a byte view (int16 sums are not an NCCL / gloo type)."""
         x = x.contiguous()
         out = torch.empty((self.world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         if self.world == 1:
             out.copy_(x)
             return out
-        return self._run(lambda o, i: dist.all_gather_into_tensor(o, i, group=self.group), out, x)
+        self._run(lambda o, i: dist.all_gather_into_tensor(o, i, group=self.group),
+                  out.view(-1).view(torch.uint8), x.view(-1).view(torch.uint8))
+        return out
 
     def all_to_all(self, send: torch.Tensor) -> torch.Tensor:
         """send [world, ...]: chunk r goes to rank r; returns recv [world, ...], chunk r from rank r."""
+        send = send.contiguous()
         recv = torch.empty_like(send)
         if self.world == 1:
             recv.copy_(send)
             return recv
-        return self._run(lambda o, i: dist.all_to_all_single(o, i, group=self.group), recv, send.contiguous())
+        self._run(lambda o, i: dist.all_to_all_single(o, i, group=self.group),
+                  recv.view(-1).view(torch.uint8), send.view(-1).view(torch.uint8))
+        return recv
 
     def all_reduce(self, t: torch.Tensor, op) -> torch.Tensor:
         if self.world == 1:
