@@ -209,6 +209,16 @@ int gc_psgd_orthonormalize(int64_t rows, int32_t rank, const float *p, float *p_
 int gc_psgd_decode(int32_t workers, int32_t n, int64_t d, int64_t cols, int32_t rank, const float *p_hat,
                    const float *q_workers, const float *q_sum, float *resid, int64_t ld, float *estimate,
                    void *stream);
+/* Vectorised fused passes (cols % 4 == 0, ld % 4 == 0, 16-byte aligned rows):
+ * gc_psgd_mq_fused = ef_apply (corrected written over resid when resid != NULL) + P = M Q in one
+ * pass over (g, r) (split-K partials in the workspace, reduced in a fixed order);
+ * gc_psgd_decode_fused = the residual update of every worker and the estimate in one pass. */
+int gc_psgd_vectorizable(int64_t cols, const void *a, const void *b, int64_t ld);
+int gc_psgd_mq_fused(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
+                     float *resid, int64_t ld, const float *q, float *p, void *workspace, void *stream);
+int gc_psgd_decode_fused(int32_t workers, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                         const float *p_hat, const float *q_workers, const float *q_sum, float *resid, int64_t ld,
+                         float *estimate, void *stream);
 /* gram = Q^T Q in fp64 (rank check of ensure_full_rank, compressors.py:595-603). */
 int gc_psgd_gram(int64_t cols, int32_t rank, const float *q, double *gram, void *stream);
 /* cudaMemsetAsync wrapper (residual reset of the dense bypass, pipelines.py:336). */

@@ -96,6 +96,9 @@ SIGNATURES = {
     "gc_psgd_mtp": (c_int, [I32, I64, I64, I64, I32, P, I64, P, P, P, P]),
     "gc_psgd_orthonormalize": (c_int, [I64, I32, P, P, P, P, P]),
     "gc_psgd_decode": (c_int, [I32, I32, I64, I64, I32, P, P, P, P, I64, P, P]),
+    "gc_psgd_vectorizable": (c_int, [I64, P, P, I64]),
+    "gc_psgd_mq_fused": (c_int, [I32, I64, I64, I64, I32, P, P, I64, P, P, P, P]),
+    "gc_psgd_decode_fused": (c_int, [I32, I32, I64, I64, I64, I32, P, P, P, P, I64, P, P]),
     "gc_psgd_gram": (c_int, [I64, I32, P, P, P]),
     "gc_fill_zero": (c_int, [P, I64, P]),
 }

@@ -202,6 +202,207 @@ __global__ void __launch_bounds__(1024) mgs_kernel(int64_t rows, int R, const fl
   for (int64_t i = threadIdx.x; i < rows * R; i += blockDim.x) out[i] = static_cast<float>(a[i]);
 }
 
+
+// ------------------------------------------------------------------ vectorised kernels
+// Used when cols % 4 == 0 and the buffers are 16-byte aligned (cfg4: 18709 x 18708).
+//
+// P = M Q fused with ef_apply.  Column-slab split-K: a CTA owns 1024 columns (a thread 4
+// columns with its Q rows in registers) x a chunk of kMqRows rows; per row the corrected
+// values f32(g + r) are formed from float4 loads, written over r (EF on) and dotted with Q;
+// warp shuffles + a shared-memory pass give the CTA's partial P[row] for its slab, written
+// to partial[w][slab][row][R] and reduced over slabs in a fixed order (deterministic).
+constexpr int kMqRows = 32;
+
+template <int R>
+__global__ void __launch_bounds__(256) mq_fused_kernel(int64_t d, int64_t rows, int64_t cols, const float *g,
+                                                       float *r, int64_t ld, const float *q, double *partial,
+                                                       int slabs) {
+  __shared__ double red[kMqRows][8][R];
+  const int w = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slab = blockIdx.x;
+  const int64_t col = (static_cast<int64_t>(slab) * 256 + threadIdx.x) * 4;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kMqRows;
+  const float *gw = g + w * ld;
+  float *rw = r ? r + w * ld : nullptr;
+  float qv[4][R];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) qv[t][b] = col + t < cols ? q[(col + t) * R + b] : 0.0f;
+  const int nrows = static_cast<int>(min(static_cast<int64_t>(kMqRows), rows - row0));
+#pragma unroll 4
+  for (int a = 0; a < nrows; ++a) {
+    const int64_t i = (row0 + a) * cols + col;
+    float c4[4] = {0.f, 0.f, 0.f, 0.f};
+    if (col < cols) {
+      if (i + 3 < d) {
+        float4 c = __ldcs(reinterpret_cast<const float4 *>(gw + i));
+        if (rw) {
+          const float4 rv = __ldcs(reinterpret_cast<const float4 *>(rw + i));
+          c.x = c.x + rv.x; c.y = c.y + rv.y; c.z = c.z + rv.z; c.w = c.w + rv.w;
+          *reinterpret_cast<float4 *>(rw + i) = c;   // corrected kept in r for the later passes
+        }
+        c4[0] = c.x; c4[1] = c.y; c4[2] = c.z; c4[3] = c.w;
+      } else {
+        for (int t = 0; t < 4; ++t)
+          if (i + t < d) {
+            float v = gw[i + t];
+            if (rw) {
+              v = v + rw[i + t];
+              rw[i + t] = v;
+            }
+            c4[t] = v;
+          }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      double v = 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) v += static_cast<double>(c4[t]) * static_cast<double>(qv[t][b]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[a][warp][b] = v;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nrows * R; e += 256) {
+    const int a = e / R, b = e - a * R;
+    double v = 0.0;
+    for (int k = 0; k < 8; ++k) v += red[a][k][b];
+    partial[((static_cast<int64_t>(w) * slabs + slab) * rows + row0 + a) * R + b] = v;
+  }
+}
+
+__global__ void mq_reduce_kernel(int L, int slabs, int64_t rows, int R, const double *partial, float *p) {
+  const int64_t total = static_cast<int64_t>(L) * rows * R;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = e / (rows * R), rest = e - w * rows * R;
+    double v = 0.0;
+    for (int s = 0; s < slabs; ++s) v += partial[(w * slabs + s) * rows * R + rest];
+    p[e] = static_cast<float>(v);
+  }
+}
+
+// Q = M^T P_hat: a thread owns 4 consecutive columns (a CTA 1024), rows in 4-row steps.
+template <int R>
+__global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, int64_t cols, const float *c,
+                                                      int64_t ld, const float *ph, int64_t rows_per_split,
+                                                      double *partial, int splits) {
+  constexpr int kChunk = R <= 8 ? 512 : 256;
+  __shared__ float ps[kChunk * R];
+  const int w = blockIdx.z;
+  const int s = blockIdx.y;
+  const int64_t col = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * 4;
+  const int64_t r0 = s * rows_per_split;
+  const int64_t r1 = min(rows, r0 + rows_per_split);
+  const float *cw = c + w * ld;
+  double acc[4][R];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc[t][b] = 0.0;
+  for (int64_t i0 = r0; i0 < r1; i0 += kChunk) {
+    const int ni = static_cast<int>(min(static_cast<int64_t>(kChunk), r1 - i0));
+    __syncthreads();
+    for (int e = threadIdx.x; e < ni * R; e += 256) ps[e] = ph[i0 * R + e];
+    __syncthreads();
+    if (col < cols) {
+#pragma unroll 4
+      for (int ii = 0; ii < ni; ++ii) {
+        const int64_t i = (i0 + ii) * cols + col;
+        float4 m;
+        if (i + 3 < d) {
+          m = __ldcs(reinterpret_cast<const float4 *>(cw + i));
+        } else {
+          float t4[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int t = 0; t < 4; ++t)
+            if (i + t < d) t4[t] = cw[i + t];
+          m = make_float4(t4[0], t4[1], t4[2], t4[3]);
+        }
+        const float m4[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int b = 0; b < R; ++b) acc[t][b] += static_cast<double>(m4[t]) * static_cast<double>(ps[ii * R + b]);
+      }
+    }
+  }
+  if (col < cols) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b)
+        partial[((static_cast<int64_t>(w) * splits + s) * cols + col + t) * R + b] = acc[t][b];
+  }
+}
+
+// Decode with a CTA per (1024-column slab, 64-row chunk): a thread keeps the Q rows of its 4
+// columns in registers and streams its rows -- per worker r_new = c - P_hat Q_w^T (c held in
+// resid), then estimate = P_hat Q_sum^T / n.  Float4 loads/stores, Q read from L2 once per CTA.
+constexpr int kDecRows = 64;
+
+template <int R>
+__global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d, int64_t rows, int64_t cols,
+                                                         const float *ph, const float *qw, const float *qsum,
+                                                         float *resid, int64_t ld, float *est) {
+  __shared__ float ps[kDecRows * R];
+  const int64_t col = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * 4;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kDecRows;
+  const int nrows = static_cast<int>(min(static_cast<int64_t>(kDecRows), rows - row0));
+  for (int e = threadIdx.x; e < nrows * R; e += 256) ps[e] = ph[row0 * R + e];
+  __syncthreads();
+  if (col >= cols) return;
+  for (int w = 0; w <= L; ++w) {   // w == L: the estimate with Q_sum
+    const float *qsrc = w < L ? qw + static_cast<int64_t>(w) * cols * R : qsum;
+    float qv[4][R];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b) qv[t][b] = col + t < cols ? qsrc[(col + t) * R + b] : 0.0f;
+    float *dst = w < L ? resid + w * ld : est;
+#pragma unroll 4
+    for (int a = 0; a < nrows; ++a) {
+      const int64_t i = (row0 + a) * cols + col;
+      if (i >= d) break;
+      float o4[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        double v = 0.0;
+#pragma unroll
+        for (int b = 0; b < R; ++b) v += static_cast<double>(ps[a * R + b]) * static_cast<double>(qv[t][b]);
+        o4[t] = static_cast<float>(v);
+      }
+      if (i + 3 < d) {
+        if (w < L) {
+          const float4 c = *reinterpret_cast<const float4 *>(dst + i);
+          __stcs(reinterpret_cast<float4 *>(dst + i), make_float4(c.x - o4[0], c.y - o4[1], c.z - o4[2], c.w - o4[3]));
+        } else {
+          const float nf = static_cast<float>(n);
+          __stcs(reinterpret_cast<float4 *>(dst + i), make_float4(o4[0] / nf, o4[1] / nf, o4[2] / nf, o4[3] / nf));
+        }
+      } else {
+        for (int t = 0; t < 4; ++t)
+          if (i + t < d) dst[i + t] = w < L ? dst[i + t] - o4[t] : o4[t] / static_cast<float>(n);
+      }
+    }
+  }
+}
+
+__global__ void sum_pairs_kernel(int64_t count, const double *part, double *out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int64_t c = 0; c < count; ++c) {
+      a += part[2 * c];
+      b += part[2 * c + 1];
+    }
+    out[0] += a;
+    out[1] += b;
+  }
+}
+
 // ------------------------------------------------------------------ decode + EF
 // For flat index i < d: row = i / cols, col = i % cols.
 //   own_w = sum_b P_hat[row][b] * Q_w[col][b]      (p_hat @ r.T, pipelines.py:355)
@@ -271,19 +472,100 @@ void launch_decode(int L, int n, int64_t d, int64_t cols, const float *ph, const
                                                                            est);
 }
 
+template <int R>
+void launch_mq_fused(int L, int64_t d, int64_t rows, int64_t cols, const float *g, float *r, int64_t ld,
+                     const float *q, double *partial, cudaStream_t st) {
+  const int slabs = static_cast<int>((cols + 1023) / 1024);
+  mq_fused_kernel<R><<<dim3(slabs, grid_cap((rows + kMqRows - 1) / kMqRows), L), 256, 0, st>>>(
+      d, rows, cols, g, r, ld, q, partial, slabs);
+}
+
+template <int R>
+void launch_mtp_vec(int L, int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld, const float *ph,
+                    double *partial, int splits, cudaStream_t st) {
+  const int64_t per = (rows + splits - 1) / splits;
+  mtp_vec_kernel<R><<<dim3(grid_cap((cols + 1023) / 1024), splits, L), 256, 0, st>>>(d, rows, cols, c, ld, ph, per,
+                                                                                   partial, splits);
+}
+
+template <int R>
+void launch_decode_vec(int L, int n, int64_t d, int64_t rows, int64_t cols, const float *ph, const float *qw,
+                       const float *qsum, float *resid, int64_t ld, float *est, cudaStream_t st) {
+  decode_vec_kernel<R><<<dim3(grid_cap((cols + 1023) / 1024), grid_cap((rows + kDecRows - 1) / kDecRows)), 256, 0,
+                         st>>>(L, n, d, rows, cols, ph, qw, qsum, resid, ld, est);
+}
+
 }  // namespace
 
 extern "C" {
 
+int gc_psgd_vectorizable(int64_t cols, const void *a, const void *b, int64_t ld) {
+  return cols % 4 == 0 && ld % 4 == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+}
+
+
+int gc_psgd_mq_fused(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
+                     float *resid, int64_t ld, const float *q, float *p, void *workspace, void *stream) {
+  GC_REQUIRE(workers >= 1 && workers <= 65535 && d >= 1 && rows * cols >= d && grads && q && p && workspace,
+             "invalid argument");
+  GC_REQUIRE(gc_psgd_vectorizable(cols, grads, resid ? resid : grads, ld), "mq_fused needs cols % 4 == 0 and aligned rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double *partial = static_cast<double *>(workspace);
+  switch (rank) {
+    case 1: launch_mq_fused<1>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
+    case 2: launch_mq_fused<2>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
+    case 3: launch_mq_fused<3>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
+    case 4: launch_mq_fused<4>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
+    case 5: launch_mq_fused<5>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
+    case 6: launch_mq_fused<6>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
+    case 7: launch_mq_fused<7>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
+    case 8: launch_mq_fused<8>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
+    case 16: launch_mq_fused<16>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
+    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
+  }
+  GC_LAUNCH_CHECK("mq_fused_kernel");
+  const int slabs = static_cast<int>((cols + 1023) / 1024);
+  const int64_t total = static_cast<int64_t>(workers) * rows * rank;
+  mq_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(
+      workers, slabs, rows, rank, partial, p);
+  GC_LAUNCH_CHECK("mq_reduce_kernel");
+  return GC_OK;
+}
+
+int gc_psgd_decode_fused(int32_t workers, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                         const float *p_hat, const float *q_workers, const float *q_sum, float *resid, int64_t ld,
+                         float *estimate, void *stream) {
+  GC_REQUIRE(workers >= 1 && n >= 1 && d >= 1 && p_hat && q_workers && q_sum && resid && estimate, "invalid argument");
+  GC_REQUIRE(gc_psgd_vectorizable(cols, resid, estimate, ld), "decode_fused needs cols % 4 == 0 and aligned rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (rank) {
+    case 1: launch_decode_vec<1>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 2: launch_decode_vec<2>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 3: launch_decode_vec<3>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 4: launch_decode_vec<4>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 5: launch_decode_vec<5>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 6: launch_decode_vec<6>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 7: launch_decode_vec<7>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 8: launch_decode_vec<8>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    case 16: launch_decode_vec<16>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
+    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
+  }
+  GC_LAUNCH_CHECK("decode_vec_kernel");
+  return GC_OK;
+}
+
+
 int gc_psgd_splits(int32_t workers, int64_t cols) {
-  const int64_t slabs = (cols + 255) / 256 * workers;
-  int s = static_cast<int>((2 * 148 + slabs - 1) / slabs);
+  const int64_t slabs = (cols % 4 == 0 ? (cols + 1023) / 1024 : (cols + 255) / 256) * workers;
+  int s = static_cast<int>((4 * 148 + slabs - 1) / slabs);
   return s < 1 ? 1 : (s > 64 ? 64 : s);
 }
 
 int64_t gc_psgd_workspace_bytes(int32_t workers, int64_t rows, int64_t cols, int32_t rank) {
   const int64_t splits = gc_psgd_splits(workers, cols);
-  return 8 * (static_cast<int64_t>(workers) * splits * cols * rank) + 8 * rows * rank + 256;
+  const int64_t mtp = 8 * (static_cast<int64_t>(workers) * splits * cols * rank);
+  const int64_t mq = 8 * (static_cast<int64_t>(workers) * ((cols + 1023) / 1024) * rows * rank);
+  return (mtp > mq ? mtp : mq) + 256;
 }
 
 int gc_psgd_mq(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c, int64_t ld,
@@ -313,7 +595,20 @@ int gc_psgd_mtp(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int splits = gc_psgd_splits(workers, cols);
   double *partial = static_cast<double *>(workspace);
-  switch (rank) {
+  if (gc_psgd_vectorizable(cols, c, c, ld)) {
+    switch (rank) {
+      case 1: launch_mtp_vec<1>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+      case 2: launch_mtp_vec<2>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+      case 3: launch_mtp_vec<3>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+      case 4: launch_mtp_vec<4>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+      case 5: launch_mtp_vec<5>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+      case 6: launch_mtp_vec<6>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+      case 7: launch_mtp_vec<7>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+      case 8: launch_mtp_vec<8>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+      case 16: launch_mtp_vec<16>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
+      default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
+    }
+  } else switch (rank) {
     case 1: launch_mtp<1>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
     case 2: launch_mtp<2>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
     case 3: launch_mtp<3>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;

@@ -177,10 +177,20 @@ __global__ void __launch_bounds__(kNT) tile_count_kernel(Work wk, int64_t len, c
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
   const int64_t end = min(base + kTileE, len);
   unsigned int gt = 0, eq = 0;
-  for (int64_t i = base + threadIdx.x; i < end; i += kNT) {
-    const unsigned int key = key_of(vals[w * ld + i]);
-    gt += key > T;
-    eq += key == T;
+  const float *row = vals + w * ld;
+  if (end - base == kTileE) {
+#pragma unroll 8
+    for (int s = 0; s < kSteps; ++s) {
+      const unsigned int key = key_of(__ldcs(row + base + s * kNT + threadIdx.x));
+      gt += key > T;
+      eq += key == T;
+    }
+  } else {
+    for (int64_t i = base + threadIdx.x; i < end; i += kNT) {
+      const unsigned int key = key_of(row[i]);
+      gt += key > T;
+      eq += key == T;
+    }
   }
   using R = cub::BlockReduce<unsigned int, kNT>;
   __shared__ typename R::TempStorage t1, t2;
@@ -238,12 +248,22 @@ __global__ void __launch_bounds__(kNT) write_kernel(Work wk, int64_t len, const 
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE + warp * (kSteps * 32);
   const unsigned int lt_mask = (1u << lane) - 1u;
   unsigned int keys[kSteps];
+  // all loads first (independent, coalesced), then the ballots
+  const float *row = vals + w * ld;
+  if (base + kSteps * 32 <= len) {
+#pragma unroll
+    for (int s = 0; s < kSteps; ++s) keys[s] = key_of(__ldcs(row + base + s * 32 + lane));
+  } else {
+#pragma unroll
+    for (int s = 0; s < kSteps; ++s) {
+      const int64_t i = base + s * 32 + lane;
+      keys[s] = i < len ? key_of(row[i]) : 0u;
+    }
+  }
   unsigned int eq_tot = 0;
 #pragma unroll
   for (int s = 0; s < kSteps; ++s) {
-    const int64_t i = base + s * 32 + lane;
-    keys[s] = i < len ? key_of(vals[w * ld + i]) : 0u;
-    const bool valid = i < len;
+    const bool valid = base + s * 32 + lane < len;
     eq_tot += __popc(__ballot_sync(0xffffffffu, valid && keys[s] == T));
   }
   if (lane == 0) s_eq[warp] = eq_tot;

@@ -412,14 +412,21 @@ class PowerSgdEngine(Engine):
         sp = _sp()
         dev = self.device
         est = torch.empty(d, dtype=torch.float32, device=dev)
-        if res is not None:   # corrected lives in r from here on
-            _native.call("gc_ef_apply", n, d, grads.data_ptr(), res.data_ptr(), grads.stride(0), res.data_ptr(),
-                         res.stride(0), sp)
-            c = res
-        else:
-            c = grads
-        ld = c.stride(0)
         acc = torch.zeros(2, dtype=torch.float64, device=dev) if nmse else None
+        rows, cols, r = self.rows, self.cols, self.rank
+        lib = _native.lib()
+        vec = (not self.bypass and res is not None and
+               bool(lib.gc_psgd_vectorizable(cols, grads.data_ptr(), res.data_ptr(), grads.stride(0))) and
+               grads.stride(0) == res.stride(0))
+        if not vec:
+            if res is not None:   # corrected lives in r from here on
+                _native.call("gc_ef_apply", n, d, grads.data_ptr(), res.data_ptr(), grads.stride(0), res.data_ptr(),
+                             res.stride(0), sp)
+                self.launches += 1
+            c = res if res is not None else grads
+        else:
+            c = res
+        ld = c.stride(0)
         if self.bypass:   # dense fp32 ring (pipelines.py:326-336); own = corrected -> r_new = 0
             _native.call("gc_float_fold", n, d, c.data_ptr(), ld, 0, -(-d // n), 0, 0, n, est.data_ptr(), sp)
             if nmse:
@@ -430,13 +437,16 @@ class PowerSgdEngine(Engine):
             ledger.charge_ring("dense-bypass", n, d, 32)
             return est, 32.0 * d, _simple_stats(acc)
 
-        rows, cols, r = self.rows, self.cols, self.rank
         q = self._seed_q(round_index)
         ev = self._ev()
         if ev:
             ev[0].record()
         p = torch.empty(n, rows, r, dtype=torch.float32, device=dev)
-        _native.call("gc_psgd_mq", n, d, rows, cols, r, c.data_ptr(), ld, q.data_ptr(), p.data_ptr(), sp)
+        if vec:   # ef_apply fused into the P = M Q pass
+            _native.call("gc_psgd_mq_fused", n, d, rows, cols, r, grads.data_ptr(), res.data_ptr(), ld, q.data_ptr(),
+                         p.data_ptr(), self.ws.data_ptr(), sp)
+        else:
+            _native.call("gc_psgd_mq", n, d, rows, cols, r, c.data_ptr(), ld, q.data_ptr(), p.data_ptr(), sp)
         p_sum = torch.empty(rows, r, dtype=torch.float32, device=dev)
         L1 = rows * r
         _native.call("gc_float_fold", n, L1, p.data_ptr(), L1, 0, -(-L1 // n), 0, 0, 0, p_sum.data_ptr(), sp)
@@ -450,19 +460,27 @@ class PowerSgdEngine(Engine):
         q_sum = torch.empty(cols, r, dtype=torch.float32, device=dev)
         L2 = cols * r
         _native.call("gc_float_fold", n, L2, qw.data_ptr(), L2, 0, -(-L2 // n), 0, 0, 0, q_sum.data_ptr(), sp)
-        _native.call("gc_psgd_decode", n, n, d, cols, r, p_hat.data_ptr(), qw.data_ptr(), q_sum.data_ptr(), None,
-                     ld, est.data_ptr(), sp)
-        if ev:
-            ev[1].record()
-        if nmse:
-            self._nmse(c, None, est, acc)
-        if res is not None:
-            _native.call("gc_psgd_decode", n, n, d, cols, r, p_hat.data_ptr(), qw.data_ptr(), q_sum.data_ptr(),
-                         res.data_ptr(), ld, None, sp)
+        if vec and not nmse:   # residual updates and the estimate in one pass
+            _native.call("gc_psgd_decode_fused", n, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
+                         q_sum.data_ptr(), res.data_ptr(), ld, est.data_ptr(), sp)
+            if ev:
+                ev[1].record()
+            self.launches += 9
+        else:
+            _native.call("gc_psgd_decode", n, n, d, cols, r, p_hat.data_ptr(), qw.data_ptr(), q_sum.data_ptr(), None,
+                         ld, est.data_ptr(), sp)
+            if ev:
+                ev[1].record()
+            if nmse:
+                self._nmse(c, None, est, acc)
+            if res is not None:
+                _native.call("gc_psgd_decode", n, n, d, cols, r, p_hat.data_ptr(), qw.data_ptr(),
+                             q_sum.data_ptr(), res.data_ptr(), ld, None, sp)
+            self.launches += 10
         warm = torch.empty(cols, r, dtype=torch.float32, device=dev)
         _native.call("gc_scale_div", L2, q_sum.data_ptr(), n, warm.data_ptr(), sp)   # pipelines.py:366
         self.warm = warm
-        self.launches += 12
+        self.launches += 1
         if self.capture:
             self.last = {"p_hat": p_hat, "q_sum": q_sum, "seed_q": q, "status": status}
         ledger.charge_ring("left-factor", n, rows * r, 32)

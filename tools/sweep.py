@@ -1,0 +1,70 @@
+"""Time every scheme at its SURVEY §8(d) config, n simulated workers on one B200.
+
+python tools/sweep.py [--n 8] [--steps 10] [--only thc,topk,...]
+Prints one JSON line per scheme: ms/round, Gelem/s (d / T), algorithmic HBM bytes and the
+fraction of the measured HBM bandwidth those bytes imply."""
+import argparse, json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2407_01378_b200 as gcb
+
+HBM = 6539.2e9
+
+
+def alg_bytes(name, n, d, cfg):
+    # compulsory bytes: g, r read; r_new, estimate written
+    if name.startswith("dense"):
+        return (4 * n + 4) * d
+    if name.startswith("topk_"):
+        k = cfg.k
+        return 12 * n * d + 4 * d + 6 * k * n * 2
+    return 12 * n * d + 4 * d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--only", default="")
+    a = ap.parse_args()
+    n = a.n
+    cases = [
+        ("thc_q4b8_cfg2", gcb.RotatedQuantConfig(4, 8), 25_557_032),
+        ("thc_q4b4_cfg2", gcb.RotatedQuantConfig(4, 4), 25_557_032),
+        ("topk_1pct_cfg3", gcb.TopKConfig(1_100_000), 110_000_000),
+        ("topkc_1pct_cfg3", gcb.ChunkedTopKConfig(64, 17_187), 110_000_000),
+        ("powersgd_r4_cfg4", gcb.PowerSgdConfig(4), 350_000_000),
+        ("dense16_cfg2", gcb.DenseConfig(16), 25_557_032),
+        ("dense16_cfg4", gcb.DenseConfig(16), 350_000_000),
+        ("dense32_cfg4", gcb.DenseConfig(32), 350_000_000),
+    ]
+    only = set(a.only.split(",")) if a.only else None
+    for name, cfg, d in cases:
+        if only and not any(name.startswith(o) for o in only):
+            continue
+        torch.cuda.empty_cache()
+        g = torch.randn(n, d, device="cuda")
+        pipe = gcb.make_pipeline(cfg, n, d, gcb.SeedSpec(2024), validate=False, compute_nmse=False)
+        eng = pipe._engine
+        for r in range(2):
+            pipe.run_round(g, r)
+        torch.cuda.synchronize()
+        eng.kernel_events = []
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        for r in range(a.steps):
+            pipe.run_round(g, 2 + r)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / a.steps
+        kms = sum(x.elapsed_time(y) for x, y in eng.kernel_events) / max(1, len(eng.kernel_events))
+        b = alg_bytes(name, n, d, cfg)
+        print(json.dumps({"case": name, "n": n, "d": d, "ms": round(ms, 4), "gelem_s": round(d / ms / 1e6, 3),
+                          "core_ms": round(kms, 4), "alg_GB": round(b / 1e9, 3),
+                          "hbm_frac": round(b / (ms * 1e-3) / HBM, 4)}), flush=True)
+        del pipe, g, eng
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
