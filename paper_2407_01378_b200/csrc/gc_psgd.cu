@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
     for (int e = threadIdx.x; e < ni * R; e += 256) ps[e] = ph[i0 * R + e];
     __syncthreads();
     if (col < cols) {
-#pragma unroll 4
+#pragma unroll 8
       for (int ii = 0; ii < ni; ++ii) {
         const int64_t i = (i0 + ii) * cols + col;
         float4 m;
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
 #pragma unroll
       for (int b = 0; b < R; ++b) qv[t][b] = col + t < cols ? qsrc[(col + t) * R + b] : 0.0f;
     float *dst = w < L ? resid + w * ld : est;
-#pragma unroll 4
+#pragma unroll 8
     for (int a = 0; a < nrows; ++a) {
       const int64_t i = (row0 + a) * cols + col;
       if (i >= d) break;
@@ -557,7 +557,7 @@ int gc_psgd_decode_fused(int32_t workers, int32_t n, int64_t d, int64_t rows, in
 
 int gc_psgd_splits(int32_t workers, int64_t cols) {
   const int64_t slabs = (cols % 4 == 0 ? (cols + 1023) / 1024 : (cols + 255) / 256) * workers;
-  int s = static_cast<int>((4 * 148 + slabs - 1) / slabs);
+  int s = static_cast<int>((8 * 148 + slabs - 1) / slabs);
   return s < 1 ? 1 : (s > 64 ? 64 : s);
 }
 
