@@ -478,39 +478,78 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
         }
       }
     }
-    // named barrier 1: every warp arrives once its fold share is written; only the
-    // estimate warp waits for it.
-    if (w == ew) {
-      asm volatile("bar.sync 1, %0;" ::"r"(n * 32) : "memory");
+    __syncthreads();   // (D) the tile's dequantized sums are complete
+
+    // ---- estimate inverse rotation spread over all warps (transforms.py:120-126): a 32-lane
+    // step covers 4 rows x 32 columns of the 32 x 32 tile, 4 elements per lane.  Row phase:
+    // stages 0-1 in registers, 2-4 by shuffles; column phase: stages 5-6 in registers, 7-9 by
+    // shuffles.  Butterfly order is bit 0 first, exactly as in the single-warp transform.
+    {
+      const int sub = lane >> 3, q4 = (lane & 7) * 4;
+#pragma unroll 1
+      for (int gi = w; gi < 8; gi += n) {
+        double* rowp = escr + (4 * gi + sub) * kScrRow + q4;
+        double e[4] = {rowp[0], rowp[1], rowp[2], rowp[3]};
+        if (K > 0) { double x = e[0], y = e[1]; e[0] = x + y; e[1] = x - y; x = e[2]; y = e[3]; e[2] = x + y; e[3] = x - y; }
+        if (K > 1) { double x = e[0], y = e[2]; e[0] = x + y; e[2] = x - y; x = e[1]; y = e[3]; e[1] = x + y; e[3] = x - y; }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = escr[lane * kScrRow + j];
-      __syncwarp();
-      wht_tile<K>(v, scratch, lane);
+        for (int b = 0; b < 3; ++b) {
+          if (K > 2 + b) {
+            const bool upper = (lane >> b) & 1;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const double o = __shfl_xor_sync(0xffffffffu, e[t], 1 << b);
+              e[t] = upper ? o - e[t] : e[t] + o;
+            }
+          }
+        }
+        rowp[0] = e[0]; rowp[1] = e[1]; rowp[2] = e[2]; rowp[3] = e[3];
+      }
+      __syncthreads();   // (E) row stages done
       const float nf = static_cast<float>(n);
       const double nd = static_cast<double>(n);
+#pragma unroll 1
+      for (int gi = w; gi < 8; gi += n) {
+        const int col = 4 * gi + sub;
+        double e[4];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int e = j * 32 + lane;
-        const int64_t i = t0 + e;
-        const float f = static_cast<float>(apply_sign(v[j] * a.scale, (sgn[j] >> lane) & 1u)) / nf;
-        if (i < a.dim) {
-          __stcs(a.est + i, f);
-          if (n == 1 && rw) __stcs(rw + i, cbuf[cidx(e)] - f);   // one worker: own == estimate
-          if (a.nmse) {
-            double ref = 0.0;
-            for (int u = 0; u < n; ++u) ref += static_cast<double>(cbuf_all[u * (32 * kCRow) + cidx(e)]);
-            ref = ref / nd;
-            const double err = static_cast<double>(f) - ref;
-            nmse_num += err * err;
-            nmse_den += ref * ref;
+        for (int t = 0; t < 4; ++t) e[t] = escr[(q4 + t) * kScrRow + col];
+        if (K > 5) { double x = e[0], y = e[1]; e[0] = x + y; e[1] = x - y; x = e[2]; y = e[3]; e[2] = x + y; e[3] = x - y; }
+        if (K > 6) { double x = e[0], y = e[2]; e[0] = x + y; e[2] = x - y; x = e[1]; y = e[3]; e[1] = x + y; e[3] = x - y; }
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          if (K > 7 + b) {
+            const bool upper = (lane >> b) & 1;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const double o = __shfl_xor_sync(0xffffffffu, e[t], 1 << b);
+              e[t] = upper ? o - e[t] : e[t] + o;
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int row = q4 + t;
+          const int el = row * 32 + col;
+          const int64_t i = t0 + el;
+          const float f = static_cast<float>(apply_sign(e[t] * a.scale, (sgn[row] >> col) & 1u)) / nf;
+          if (i < a.dim) {
+            __stcs(a.est + i, f);
+            if (n == 1 && rw) __stcs(rw + i, cbuf[cidx(el)] - f);   // one worker: own == estimate
+            if (a.nmse) {
+              double ref = 0.0;
+              for (int u = 0; u < n; ++u) ref += static_cast<double>(cbuf_all[u * (32 * kCRow) + cidx(el)]);
+              ref = ref / nd;
+              const double err = static_cast<double>(f) - ref;
+              nmse_num += err * err;
+              nmse_den += ref * ref;
+            }
           }
         }
       }
     }
 
-    else {
-      asm volatile("bar.arrive 1, %0;" ::"r"(n * 32) : "memory");
-    }
+    __syncthreads();   // (F) the estimate buffer (warp ew's scratch) is free again
 
     // ---- own decode + ef_update (pipelines.py:312-318, 168-170)
     if (rw && n > 1) {
@@ -534,10 +573,9 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
         if (i < a.dim) __stcs(rw + i, cbuf[cidx(e)] - own);
       }
     }
-    // (C) end of tile.  Only the nmse reduction needs it for correctness (every other buffer is
-    // protected by barrier A / B of the next tile; sign words are double-buffered), but keeping
-    // the warps in lockstep measured faster (2.50 vs 2.65 ms at cfg2).
-    __syncthreads();
+    // (C) end of tile: only the nmse reduction needs it (it reads every warp's cbuf); all other
+    // buffers are protected by barriers A / B / D of the next tile (sign words double-buffered).
+    if (a.nmse) __syncthreads();
   }
 
 #pragma unroll
