@@ -23,8 +23,8 @@
 namespace {
 
 constexpr int kNT = 256;
-constexpr int kTileE = 8192;          // elements per tile (8 warps x 32 steps x 32 lanes)
-constexpr int kSteps = kTileE / kNT;  // 32
+constexpr int kTileE = 4096;          // elements per tile (8 warps x 16 steps x 32 lanes)
+constexpr int kSteps = kTileE / kNT;  // 16
 
 struct RowState {  // per worker, lives in the workspace
   unsigned int prefix;     // key bits fixed so far
@@ -236,7 +236,9 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(Work wk, int64_t tiles)
   }
 }
 
-// Emit selected indices in ascending order (and optionally fp16-rounded values).
+// Emit selected indices in ascending order (and optionally fp16-rounded values).  Each warp
+// owns kSteps groups of 32 consecutive elements; a group with no key >= T (most of them at
+// 1 % density) costs one ballot.  Ties (key == T) are taken in index order up to m.
 __global__ void __launch_bounds__(kNT) write_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
                                                     int64_t tiles, int64_t k, int32_t *idx_out, float *val_out,
                                                     int fp16_vals) {
@@ -247,9 +249,8 @@ __global__ void __launch_bounds__(kNT) write_kernel(Work wk, int64_t len, const 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE + warp * (kSteps * 32);
   const unsigned int lt_mask = (1u << lane) - 1u;
-  unsigned int keys[kSteps];
-  // all loads first (independent, coalesced), then the ballots
   const float *row = vals + w * ld;
+  unsigned int keys[kSteps];
   if (base + kSteps * 32 <= len) {
 #pragma unroll
     for (int s = 0; s < kSteps; ++s) keys[s] = key_of(__ldcs(row + base + s * 32 + lane));
@@ -257,34 +258,46 @@ __global__ void __launch_bounds__(kNT) write_kernel(Work wk, int64_t len, const 
 #pragma unroll
     for (int s = 0; s < kSteps; ++s) {
       const int64_t i = base + s * 32 + lane;
-      keys[s] = i < len ? key_of(row[i]) : 0u;
+      keys[s] = i < len ? key_of(row[i]) : 0u;   // key 0 <= T: never selected past the end
     }
   }
+  // masks per group: ge (key >= T) and eq (key == T); padding lanes read key 0
+  unsigned int gem[kSteps], eqm[kSteps];
   unsigned int eq_tot = 0;
+  const bool t_zero = T == 0u;
 #pragma unroll
   for (int s = 0; s < kSteps; ++s) {
     const bool valid = base + s * 32 + lane < len;
-    eq_tot += __popc(__ballot_sync(0xffffffffu, valid && keys[s] == T));
+    gem[s] = __ballot_sync(0xffffffffu, valid && keys[s] >= T);
+    eqm[s] = 0u;
+    if (gem[s]) {
+      eqm[s] = __ballot_sync(0xffffffffu, valid && keys[s] == T);
+      eq_tot += __popc(eqm[s]);
+    }
   }
+  (void)t_zero;
   if (lane == 0) s_eq[warp] = eq_tot;
   __syncthreads();
-  long long eq_base = wk.tile_eq_off[w * tiles + blockIdx.x];
-  for (int j = 0; j < warp; ++j) eq_base += s_eq[j];
-  // selected flags and per-warp totals
-  unsigned int sel_masks[kSteps];
+  long long eq_run = wk.tile_eq_off[w * tiles + blockIdx.x];
+  for (int j = 0; j < warp; ++j) eq_run += s_eq[j];
   unsigned int sel_tot = 0;
-  long long eq_run = eq_base;
 #pragma unroll
   for (int s = 0; s < kSteps; ++s) {
-    const int64_t i = base + s * 32 + lane;
-    const bool valid = i < len;
-    const bool is_eq = valid && keys[s] == T;
-    const unsigned int eqm = __ballot_sync(0xffffffffu, is_eq);
-    const long long rank = eq_run + __popc(eqm & lt_mask);
-    const bool sel = valid && (keys[s] > T || (is_eq && rank < m));
-    sel_masks[s] = __ballot_sync(0xffffffffu, sel);
-    sel_tot += __popc(sel_masks[s]);
-    eq_run += __popc(eqm);
+    unsigned int sm = gem[s] & ~eqm[s];   // strictly above T: always taken
+    if (eqm[s]) {
+      // ties: the first max(0, min(popc, m - eq_run)) set bits of eqm, in lane (= index) order
+      const long long room = m - eq_run;
+      const int take = room <= 0 ? 0 : (room >= 32 ? 32 : static_cast<int>(room));
+      unsigned int e = eqm[s];
+      for (int t = 0; t < take && e; ++t) {
+        const unsigned int lowbit = e & (0u - e);
+        sm |= lowbit;
+        e ^= lowbit;
+      }
+      eq_run += __popc(eqm[s]);
+    }
+    gem[s] = sm;   // reuse as the selected mask
+    sel_tot += __popc(sm);
   }
   if (lane == 0) s_sel[warp] = sel_tot;
   __syncthreads();
@@ -292,19 +305,21 @@ __global__ void __launch_bounds__(kNT) write_kernel(Work wk, int64_t len, const 
   for (int j = 0; j < warp; ++j) out += s_sel[j];
 #pragma unroll
   for (int s = 0; s < kSteps; ++s) {
-    const unsigned int sm = sel_masks[s];
-    if ((sm >> lane) & 1u) {
-      const long long pos = out + __popc(sm & lt_mask);
-      const int64_t i = base + s * 32 + lane;
-      if (pos < k) {
-        idx_out[w * k + pos] = static_cast<int32_t>(i);
-        if (val_out) {
-          const float x = vals[w * ld + i];
-          val_out[w * k + pos] = fp16_vals ? gc::fp16_round_trip(x) : x;
+    const unsigned int sm = gem[s];
+    if (sm) {
+      if ((sm >> lane) & 1u) {
+        const long long pos = out + __popc(sm & lt_mask);
+        const int64_t i = base + s * 32 + lane;
+        if (pos < k) {
+          idx_out[w * k + pos] = static_cast<int32_t>(i);
+          if (val_out) {
+            const float x = row[i];
+            val_out[w * k + pos] = fp16_vals ? gc::fp16_round_trip(x) : x;
+          }
         }
       }
+      out += __popc(sm);
     }
-    out += __popc(sm);
   }
 }
 
