@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--rotation-block", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bar", action="store_true", help="skip the FP16-bar comparison line")
+    ap.add_argument("--sweep", action="store_true", help="also time TopK / TopK-C / PowerSGD at their configs")
     return ap.parse_args()
 
 
@@ -78,54 +80,54 @@ def workload(args, n_gpus):
 
 # ------------------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region (NVML thread, every 2 ms;
+    nvidia-smi --query-gpu is the fallback)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.proc = None
+        self.samples = []
+        self.max_mhz = None
+        self._stop = None
+        self._thread = None
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self._stop = threading.Event()
+
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        clk = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((float(clk), int(rs)))
+                    except pynvml.NVMLError:
+                        pass
+                    self._stop.wait(0.002)
+
+            self._thread = threading.Thread(target=loop, daemon=True)
+            self._thread.start()
+        except Exception:
+            self._thread = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = max(mx, float(f[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0, "source": "nvml"}
+        reasons = sorted({name for _, r in self.samples for name, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(c for c, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml, 2 ms"}
 
 
 # ------------------------------------------------------------------------------ CPU side
@@ -169,6 +171,35 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ GPU side
+def time_pipeline(gcb, cfg, n, d, seeds, world, local_n, pool, args, dev):
+    """CUDA-event time of run_round for another scheme at the same worker split (max over ranks)."""
+    import torch
+    if world == 1:
+        pipe = gcb.make_pipeline(cfg, n, d, seeds, validate=False, compute_nmse=False)
+    else:
+        from paper_2407_01378_b200.distributed import DistributedGradientPipeline
+        pipe = DistributedGradientPipeline(cfg, n, d, seeds, validate=False, compute_nmse=False)
+    for s in range(args.warmup):
+        pipe.run_round(pool[s % len(pool)], s)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, min(args.steps, 10))
+    e0.record()
+    for s in range(steps):
+        pipe.run_round(pool[s % len(pool)], args.warmup + s)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    del pipe
+    return {"scheme": gcb.scheme_label(cfg), "d": d, "workers": n, "ms_per_step": ms,
+            "value": d / (ms * 1e-3) / 1e9, "unit": "Gelem/s", "steps": steps}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -305,13 +336,32 @@ def main():
                "sample": f"oracle port (NumPy restatement of the reference THC round), n={n}, d={d_sample:,}, "
                          f"median of 3 rounds; numpy elementwise ops are single-threaded"}
 
+    bar = None
+    if not args.no_bar:
+        bar = time_pipeline(gcb, gcb.DenseConfig(16), n, d, seeds, world, local_n, pool, args, dev)
+        bar["what"] = ("dense FP16 round at the same d and n (fp16 inputs, fp16 wire per hop; NCCL half "
+                       "all-reduce across ranks): the utility bar of BASELINE.json's metric")
+        bar["thc_vs_bar_time_ratio"] = ms / bar["ms_per_step"]
+    sweep = None
+    if args.sweep:
+        sweep = {}
+        for name, cfg, dd in (("topk_1pct_cfg3", gcb.TopKConfig(1_100_000), 110_000_000),
+                              ("topkc_1pct_cfg3", gcb.ChunkedTopKConfig(64, 17_187), 110_000_000),
+                              ("powersgd_r4_cfg4", gcb.PowerSgdConfig(4), 350_000_000)):
+            del pool
+            torch.cuda.empty_cache()
+            pool = [torch.randn(local_n, dd, device=dev, generator=gen)]
+            sweep[name] = time_pipeline(gcb, cfg, n, dd, seeds, world, local_n, pool, args, dev)
+
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": n_gpus, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic (Gaussian gradients, random per rank)",
                "config": workload(args, n_gpus), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches, "clocks": clk.summary(),
-               "worker_elements_per_s": n * d / (ms * 1e-3)}
+               "worker_elements_per_s": n * d / (ms * 1e-3), "fp16_bar": bar}
+        if sweep is not None:
+            out["sweep"] = sweep
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
