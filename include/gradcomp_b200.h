@@ -142,6 +142,17 @@ int gc_thc_decode_ef(const gc_thc_geom *g, int32_t workers, const int8_t *codes,
  * aggregation (pipelines.py:224-244) and PowerSGD's factor sums (pipelines.py:327-363). */
 int gc_float_fold(int32_t n, int64_t len, const float *inputs, int64_t ld, int64_t offset, int64_t ring_block,
                   int32_t wire_fp16, int32_t round_inputs, int32_t divisor, float *out, void *stream);
+/* Batched form: B independent folds, inputs [B][n][len] (row stride ld, batch stride
+ * in_stride), outputs [B][len] (batch stride out_stride). */
+int gc_float_fold_batched(int32_t batch, int32_t n, int64_t len, const float *inputs, int64_t ld, int64_t in_stride,
+                          int32_t wire_fp16, int32_t round_inputs, int32_t divisor, float *out, int64_t out_stride,
+                          void *stream);
+/* Dense-fp32 bypass of many small tensors in one launch (pipelines.py:326-336): for segment s
+ * (offsets/lengths device int64 [nseg]) of the flat [n][ld] corrected vectors, estimate =
+ * ring-ordered fp32 sum / n, and resid = 0 there (own == corrected; resid may alias corrected
+ * or be NULL). */
+int gc_segment_fold_ef(int32_t n, int32_t nseg, const int64_t *seg_off, const int64_t *seg_len,
+                       const float *corrected, float *resid, int64_t ld, float *estimate, void *stream);
 /* out = in / divisor (f32, may alias). */
 int gc_scale_div(int64_t len, const float *in, int32_t divisor, float *out, void *stream);
 /* out = fp16_round_trip(in) (vectors.py:136-152; may alias). */
@@ -190,37 +201,54 @@ int gc_chunk_ef_update(int32_t workers, int64_t d, int64_t chunk, int64_t select
 
 /* ---------------------------------------------------------------- PowerSGD
  * _round_powersgd (pipelines.py:324-368).  Matrices are the corrected vectors zero-padded to
- * rows x cols (matrix_shape_for, compressors.py:530-548), row-major, leading dimension ld per
- * worker.  Supported ranks: 1..8 and 16.  Products accumulate in fp64 and round to f32. */
-int gc_psgd_splits(int32_t workers, int64_t cols);
-int64_t gc_psgd_workspace_bytes(int32_t workers, int64_t rows, int64_t cols, int32_t rank);
-/* P_w = M_w Q (pipelines.py:348): q [cols][rank], p [L][rows][rank]. */
-int gc_psgd_mq(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c, int64_t ld,
+ * rows x cols (matrix_shape_for, compressors.py:530-548), row-major.  Supported ranks: 1..8, 16.
+ * Products accumulate in fp64 and round to f32.
+ *
+ * A batch is T independent tensors of the same length d (so the same rows x cols), each with L
+ * workers: virtual row v = t*L + w.  Row v of M starts at row_offsets[v] in the flat buffers
+ * (device int64, e.g. tensor t's slice of worker w's flat gradient) or at v*ld when row_offsets
+ * is NULL (the single-matrix reference path: T = 1).  Factors are per tensor: Q [T][cols][r]
+ * (mq input), P [T*L][rows][r], P_hat [T][rows][r], Q_w [T*L][cols][r], Q_sum [T][cols][r];
+ * tensor t's estimate starts at est_offsets[t] (NULL: 0).  This is the "chunked PowerSGD" of
+ * one reference pipeline per layer tensor, batched by shape. */
+typedef struct gc_psgd_batch {
+  int32_t tensors;
+  int32_t workers;
+  const int64_t *row_offsets;
+  int64_t ld;
+  const int64_t *est_offsets;
+  int32_t rows_aligned;   /* 1 if every row start (and the estimate slices) is 16-byte aligned */
+} gc_psgd_batch;
+
+int gc_psgd_splits(int32_t rows_total, int64_t cols);
+int64_t gc_psgd_workspace_bytes(int32_t rows_total, int64_t rows, int64_t cols, int32_t rank);
+int gc_psgd_vectorizable(int64_t cols, const void *a, const void *b, int64_t ld);
+/* P_w = M_w Q (pipelines.py:348). */
+int gc_psgd_mq(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                const float *q, float *p, void *stream);
-/* Q_w = M_w^T P_hat (pipelines.py:354): p_hat [rows][rank], q [L][cols][rank]. */
-int gc_psgd_mtp(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c, int64_t ld,
+/* ef_apply fused into P = M Q (cols % 4 == 0, 16-byte aligned rows): corrected f32(g + r) is
+ * written over resid (when non-NULL) in the same pass; split-K partials in the workspace. */
+int gc_psgd_mq_fused(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
+                     float *resid, const float *q, float *p, void *workspace, void *stream);
+/* Q_w = M_w^T P_hat (pipelines.py:354). */
+int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                 const float *p_hat, float *q, void *workspace, void *stream);
-/* orthonormalize (compressors.py:555-588): fp64 modified Gram-Schmidt with canonical-basis
- * completion of degenerate columns; *status = 1 if completion failed (DegenerateMatrixError). */
-int gc_psgd_orthonormalize(int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace, int32_t *status,
-                           void *stream);
+/* orthonormalize (compressors.py:555-588) for T tensors: fp64 modified Gram-Schmidt with
+ * canonical-basis completion; status[t] = 1 if completion failed (DegenerateMatrixError).
+ * workspace: T*rows*rank doubles. */
+int gc_psgd_orthonormalize(int32_t tensors, int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace,
+                           int32_t *status, void *stream);
 /* own_w = P_hat Q_w^T, resid_w -= own_w (resid holds the corrected matrix; NULL skips);
  * estimate = P_hat Q_sum^T / n (NULL skips) (pipelines.py:355, 365, 168-170). */
-int gc_psgd_decode(int32_t workers, int32_t n, int64_t d, int64_t cols, int32_t rank, const float *p_hat,
-                   const float *q_workers, const float *q_sum, float *resid, int64_t ld, float *estimate,
+int gc_psgd_decode(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                   const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
                    void *stream);
-/* Vectorised fused passes (cols % 4 == 0, ld % 4 == 0, 16-byte aligned rows):
- * gc_psgd_mq_fused = ef_apply (corrected written over resid when resid != NULL) + P = M Q in one
- * pass over (g, r) (split-K partials in the workspace, reduced in a fixed order);
- * gc_psgd_decode_fused = the residual update of every worker and the estimate in one pass. */
-int gc_psgd_vectorizable(int64_t cols, const void *a, const void *b, int64_t ld);
-int gc_psgd_mq_fused(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
-                     float *resid, int64_t ld, const float *q, float *p, void *workspace, void *stream);
-int gc_psgd_decode_fused(int32_t workers, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
-                         const float *p_hat, const float *q_workers, const float *q_sum, float *resid, int64_t ld,
-                         float *estimate, void *stream);
-/* gram = Q^T Q in fp64 (rank check of ensure_full_rank, compressors.py:595-603). */
-int gc_psgd_gram(int64_t cols, int32_t rank, const float *q, double *gram, void *stream);
+/* Same, vectorised (cols % 4 == 0, aligned rows): both outputs in one pass. */
+int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                         const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
+                         void *stream);
+/* gram[t] = Q_t^T Q_t in fp64 (rank check of ensure_full_rank, compressors.py:595-603). */
+int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, double *gram, void *stream);
 /* cudaMemsetAsync wrapper (residual reset of the dense bypass, pipelines.py:336). */
 int gc_fill_zero(void *ptr, int64_t bytes, void *stream);
 

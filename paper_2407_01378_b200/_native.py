@@ -43,8 +43,11 @@ class ThcGeom(ctypes.Structure):
                 ("wire_bits", c_int32), ("scale", c_double)]
 
 
-class ChunkGeom(ctypes.Structure):
-    _fields_ = [("dim", c_int64), ("chunk", c_int64), ("num_chunks", c_int64), ("selected", c_int64)]
+class PsgdBatch(ctypes.Structure):
+    """gc_psgd_batch: T same-shape tensors x L workers (row_offsets / est_offsets are device int64)."""
+
+    _fields_ = [("tensors", c_int32), ("workers", c_int32), ("row_offsets", c_void_p), ("ld", c_int64),
+                ("est_offsets", c_void_p), ("rows_aligned", c_int32)]
 
 
 P = c_void_p
@@ -76,6 +79,8 @@ SIGNATURES = {
     "gc_thc_round_fused": (c_int, [POINTER(ThcGeom), I32, P, P, I64, P, POINTER(Pcg64), P, P, P, P, P]),
     # float folds
     "gc_float_fold": (c_int, [I32, I64, P, I64, I64, I64, I32, I32, I32, P, P]),
+    "gc_float_fold_batched": (c_int, [I32, I32, I64, P, I64, I64, I32, I32, I32, P, I64, P]),
+    "gc_segment_fold_ef": (c_int, [I32, I32, P, P, P, P, I64, P, P]),
     "gc_scale_div": (c_int, [I64, P, I32, P, P]),
     "gc_fp16_round": (c_int, [I64, P, P, P]),
     # TopK
@@ -92,14 +97,14 @@ SIGNATURES = {
     # PowerSGD
     "gc_psgd_splits": (c_int, [I32, I64]),
     "gc_psgd_workspace_bytes": (c_int64, [I32, I64, I64, I32]),
-    "gc_psgd_mq": (c_int, [I32, I64, I64, I64, I32, P, I64, P, P, P]),
-    "gc_psgd_mtp": (c_int, [I32, I64, I64, I64, I32, P, I64, P, P, P, P]),
-    "gc_psgd_orthonormalize": (c_int, [I64, I32, P, P, P, P, P]),
-    "gc_psgd_decode": (c_int, [I32, I32, I64, I64, I32, P, P, P, P, I64, P, P]),
     "gc_psgd_vectorizable": (c_int, [I64, P, P, I64]),
-    "gc_psgd_mq_fused": (c_int, [I32, I64, I64, I64, I32, P, P, I64, P, P, P, P]),
-    "gc_psgd_decode_fused": (c_int, [I32, I32, I64, I64, I64, I32, P, P, P, P, I64, P, P]),
-    "gc_psgd_gram": (c_int, [I64, I32, P, P, P]),
+    "gc_psgd_mq": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P]),
+    "gc_psgd_mq_fused": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P, P, P]),
+    "gc_psgd_mtp": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P, P]),
+    "gc_psgd_orthonormalize": (c_int, [I32, I64, I32, P, P, P, P, P]),
+    "gc_psgd_decode": (c_int, [POINTER(PsgdBatch), I32, I64, I64, I64, I32, P, P, P, P, P, P]),
+    "gc_psgd_decode_fused": (c_int, [POINTER(PsgdBatch), I32, I64, I64, I64, I32, P, P, P, P, P, P]),
+    "gc_psgd_gram": (c_int, [I32, I64, I32, P, P, P]),
     "gc_fill_zero": (c_int, [P, I64, P]),
 }
 

@@ -21,7 +21,9 @@ constexpr int kNT = 256;
 template <bool WIRE16, bool ROUND_IN>
 __global__ void __launch_bounds__(kNT) float_fold_kernel(int n, int64_t len, const float *in, int64_t ld,
                                                          int64_t offset, int64_t ring_block, int divisor,
-                                                         float *out) {
+                                                         float *out, int64_t in_stride, int64_t out_stride) {
+  in += blockIdx.y * in_stride;   // batch of independent folds
+  out += blockIdx.y * out_stride;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < len;
        e += static_cast<int64_t>(gridDim.x) * kNT) {
     const int s = static_cast<int>((offset + e) / ring_block);
@@ -37,6 +39,30 @@ __global__ void __launch_bounds__(kNT) float_fold_kernel(int n, int64_t len, con
     }
     if (WIRE16 && n > 1) acc = gc::fp16_round_trip(acc);
     out[e] = divisor > 0 ? acc / static_cast<float>(divisor) : acc;
+  }
+}
+
+// Dense fp32 bypass of a batch of small tensors: segment blockIdx.y, ring block ceil(len/n).
+// c holds the corrected values; zero (may alias c) receives the new residual 0.
+__global__ void __launch_bounds__(kNT) segment_fold_kernel(int n, const int64_t *seg_off, const int64_t *seg_len,
+                                                           const float *g, float *r, int64_t ld, float *est) {
+  // g: corrected values, r: residual rows to zero (nullable)
+  const int64_t off = seg_off[blockIdx.y], len = seg_len[blockIdx.y];
+  const int64_t blk = (len + n - 1) / n;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < len;
+       e += static_cast<int64_t>(gridDim.x) * kNT) {
+    const int64_t i = off + e;
+    const int s = static_cast<int>(e / blk);
+    float acc = 0.0f;
+    int w = s;
+    for (int k = 0; k < n; ++k) {
+      const float c = g[w * ld + i];
+      acc = (k == 0) ? c : acc + c;
+      w = (w + 1 == n) ? 0 : w + 1;
+    }
+    est[i] = acc / static_cast<float>(n);
+    if (r)
+      for (int u = 0; u < n; ++u) r[u * ld + i] = 0.0f;   // corrected - own with own = corrected
   }
 }
 
@@ -58,6 +84,26 @@ int grid_for(int64_t work) {
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
+int fold_launch(int32_t batch, int32_t n, int64_t len, const float *inputs, int64_t ld, int64_t in_stride,
+                int64_t offset, int64_t ring_block, int32_t wire_fp16, int32_t round_inputs, int32_t divisor,
+                float *out, int64_t out_stride, cudaStream_t st) {
+  const dim3 g(grid_for(len), batch);
+  if (wire_fp16 && round_inputs)
+    float_fold_kernel<true, true><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out, in_stride,
+                                                     out_stride);
+  else if (wire_fp16)
+    float_fold_kernel<true, false><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out,
+                                                      in_stride, out_stride);
+  else if (round_inputs)
+    float_fold_kernel<false, true><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out,
+                                                      in_stride, out_stride);
+  else
+    float_fold_kernel<false, false><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out,
+                                                       in_stride, out_stride);
+  GC_LAUNCH_CHECK("float_fold_kernel");
+  return GC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -66,17 +112,27 @@ int gc_float_fold(int32_t n, int64_t len, const float *inputs, int64_t ld, int64
                   int32_t wire_fp16, int32_t round_inputs, int32_t divisor, float *out, void *stream) {
   GC_REQUIRE(n >= 1 && len >= 0 && ld >= len && ring_block >= 1 && inputs && out, "invalid argument");
   if (len == 0) return GC_OK;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int g = grid_for(len);
-  if (wire_fp16 && round_inputs)
-    float_fold_kernel<true, true><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out);
-  else if (wire_fp16)
-    float_fold_kernel<true, false><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out);
-  else if (round_inputs)
-    float_fold_kernel<false, true><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out);
-  else
-    float_fold_kernel<false, false><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out);
-  GC_LAUNCH_CHECK("float_fold_kernel");
+  return fold_launch(1, n, len, inputs, ld, 0, offset, ring_block, wire_fp16, round_inputs, divisor, out, 0,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int gc_float_fold_batched(int32_t batch, int32_t n, int64_t len, const float *inputs, int64_t ld, int64_t in_stride,
+                          int32_t wire_fp16, int32_t round_inputs, int32_t divisor, float *out, int64_t out_stride,
+                          void *stream) {
+  GC_REQUIRE(batch >= 1 && batch <= 65535 && n >= 1 && len >= 0 && ld >= len && inputs && out, "invalid argument");
+  if (len == 0) return GC_OK;
+  return fold_launch(batch, n, len, inputs, ld, in_stride, 0, (len + n - 1) / n, wire_fp16, round_inputs, divisor,
+                     out, out_stride, static_cast<cudaStream_t>(stream));
+}
+
+int gc_segment_fold_ef(int32_t n, int32_t nseg, const int64_t *seg_off, const int64_t *seg_len, const float *grads,
+                       float *resid, int64_t ld, float *estimate, void *stream) {
+  GC_REQUIRE(n >= 1 && nseg >= 0 && nseg <= 65535 && (nseg == 0 || (seg_off && seg_len)) && grads && estimate,
+             "invalid argument");
+  if (nseg == 0) return GC_OK;
+  segment_fold_kernel<<<dim3(4, nseg), kNT, 0, static_cast<cudaStream_t>(stream)>>>(n, seg_off, seg_len, grads, resid,
+                                                                                  ld, estimate);
+  GC_LAUNCH_CHECK("segment_fold_kernel");
   return GC_OK;
 }
 

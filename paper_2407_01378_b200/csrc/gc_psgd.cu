@@ -29,6 +29,17 @@ constexpr int kMaxRank = 16;
 
 int grid_cap(int64_t g) { return static_cast<int>(g < 1 ? 1 : (g > 65535 ? 65535 : g)); }
 
+// Batched layout: virtual row v = t * n_per + w (tensor t, worker w).  Row v of M starts at
+// offs[v] (a tensor's slice of the flat gradient) or v * ld when offs is NULL; per-tensor
+// factors are strided by tensor.  The single-matrix path is n_per = L, one tensor.
+struct Rows {
+  const int64_t *offs;
+  int64_t ld;
+  int n_per;
+  __device__ __forceinline__ int64_t at(int v) const { return offs ? offs[v] : static_cast<int64_t>(v) * ld; }
+  __device__ __forceinline__ int tensor(int v) const { return v / n_per; }
+};
+
 // ------------------------------------------------------------------ P = M Q
 template <int R>
 struct MqShape {
@@ -38,14 +49,15 @@ struct MqShape {
 };
 
 template <int R>
-__global__ void __launch_bounds__(256) mq_kernel(int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld,
+__global__ void __launch_bounds__(256) mq_kernel(int64_t d, int64_t rows, int64_t cols, const float *c, Rows rw_,
                                                  const float *q, float *p) {
   constexpr int kRowsPerWarp = MqShape<R>::kRowsPerWarp, kChunk = MqShape<R>::kChunk;
   __shared__ float qs[kChunk * R];
   const int w = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * MqShape<R>::kRowsPerCta + warp * kRowsPerWarp;
-  const float *cw = c + w * ld;
+  const float *cw = c + rw_.at(w);
+  q += static_cast<int64_t>(rw_.tensor(w)) * cols * R;
   double acc[kRowsPerWarp][R];
 #pragma unroll
   for (int a = 0; a < kRowsPerWarp; ++a)
@@ -82,7 +94,7 @@ __global__ void __launch_bounds__(256) mq_kernel(int64_t d, int64_t rows, int64_
 // ------------------------------------------------------------------ Q = M^T P_hat
 // partial[w][s][col][R] over row range s; then reduced in order s = 0, 1, ...
 template <int R>
-__global__ void __launch_bounds__(256) mtp_kernel(int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld,
+__global__ void __launch_bounds__(256) mtp_kernel(int64_t d, int64_t rows, int64_t cols, const float *c, Rows rw_,
                                                   const float *ph, int64_t rows_per_split, double *partial,
                                                   int splits) {
   constexpr int kChunk = R <= 8 ? 512 : 256;
@@ -92,7 +104,8 @@ __global__ void __launch_bounds__(256) mtp_kernel(int64_t d, int64_t rows, int64
   const int64_t col = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
   const int64_t r0 = s * rows_per_split;
   const int64_t r1 = min(rows, r0 + rows_per_split);
-  const float *cw = c + w * ld;
+  const float *cw = c + rw_.at(w);
+  ph += static_cast<int64_t>(rw_.tensor(w)) * rows * R;
   double acc[R];
 #pragma unroll
   for (int b = 0; b < R; ++b) acc[b] = 0.0;
@@ -149,6 +162,13 @@ __device__ double block_sum(double v, double *red) {
 __global__ void __launch_bounds__(1024) mgs_kernel(int64_t rows, int R, const float *in, double *a, float *out,
                                                    int *status) {
   __shared__ double red[33];
+  {   // one CTA per tensor of the batch
+    const int64_t t = blockIdx.x;
+    in += t * rows * R;
+    a += t * rows * R;
+    out += t * rows * R;
+    status += t;
+  }
   double fro = 0.0;
   for (int64_t i = threadIdx.x; i < rows * R; i += blockDim.x) {
     const double v = static_cast<double>(in[i]);
@@ -215,7 +235,7 @@ constexpr int kMqRows = 32;
 
 template <int R>
 __global__ void __launch_bounds__(256) mq_fused_kernel(int64_t d, int64_t rows, int64_t cols, const float *g,
-                                                       float *r, int64_t ld, const float *q, double *partial,
+                                                       float *r, Rows rw_, const float *q, double *partial,
                                                        int slabs) {
   __shared__ double red[kMqRows][8][R];
   const int w = blockIdx.z;
@@ -223,8 +243,9 @@ __global__ void __launch_bounds__(256) mq_fused_kernel(int64_t d, int64_t rows, 
   const int slab = blockIdx.x;
   const int64_t col = (static_cast<int64_t>(slab) * 256 + threadIdx.x) * 4;
   const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kMqRows;
-  const float *gw = g + w * ld;
-  float *rw = r ? r + w * ld : nullptr;
+  const float *gw = g + rw_.at(w);
+  float *rw = r ? r + rw_.at(w) : nullptr;
+  q += static_cast<int64_t>(rw_.tensor(w)) * cols * R;
   float qv[4][R];
 #pragma unroll
   for (int t = 0; t < 4; ++t)
@@ -289,7 +310,7 @@ __global__ void mq_reduce_kernel(int L, int slabs, int64_t rows, int R, const do
 // Q = M^T P_hat: a thread owns 4 consecutive columns (a CTA 1024), rows in 4-row steps.
 template <int R>
 __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, int64_t cols, const float *c,
-                                                      int64_t ld, const float *ph, int64_t rows_per_split,
+                                                      Rows rw_, const float *ph, int64_t rows_per_split,
                                                       double *partial, int splits) {
   constexpr int kChunk = R <= 8 ? 512 : 256;
   __shared__ float ps[kChunk * R];
@@ -298,7 +319,8 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
   const int64_t col = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * 4;
   const int64_t r0 = s * rows_per_split;
   const int64_t r1 = min(rows, r0 + rows_per_split);
-  const float *cw = c + w * ld;
+  const float *cw = c + rw_.at(w);
+  ph += static_cast<int64_t>(rw_.tensor(w)) * rows * R;
   double acc[4][R];
 #pragma unroll
   for (int t = 0; t < 4; ++t)
@@ -347,8 +369,15 @@ constexpr int kDecRows = 64;
 template <int R>
 __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d, int64_t rows, int64_t cols,
                                                          const float *ph, const float *qw, const float *qsum,
-                                                         float *resid, int64_t ld, float *est) {
+                                                         float *resid, Rows rw_, float *est, const int64_t *est_offs) {
   __shared__ float ps[kDecRows * R];
+  {   // tensor t of a batch: its factors, workers t*L .. t*L+L-1, its slice of the estimate
+    const int t = blockIdx.z;
+    ph += static_cast<int64_t>(t) * rows * R;
+    qw += static_cast<int64_t>(t) * L * cols * R;
+    qsum += static_cast<int64_t>(t) * cols * R;
+    if (est) est += est_offs ? est_offs[t] : 0;
+  }
   const int64_t col = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * 4;
   const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kDecRows;
   const int nrows = static_cast<int>(min(static_cast<int64_t>(kDecRows), rows - row0));
@@ -362,7 +391,9 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
     for (int t = 0; t < 4; ++t)
 #pragma unroll
       for (int b = 0; b < R; ++b) qv[t][b] = col + t < cols ? qsrc[(col + t) * R + b] : 0.0f;
-    float *dst = w < L ? resid + w * ld : est;
+    if (w < L && !resid) continue;
+    if (w == L && !est) continue;
+    float *dst = w < L ? resid + rw_.at(blockIdx.z * L + w) : est;
 #pragma unroll 8
     for (int a = 0; a < nrows; ++a) {
       const int64_t i = (row0 + a) * cols + col;
@@ -391,17 +422,6 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
   }
 }
 
-__global__ void sum_pairs_kernel(int64_t count, const double *part, double *out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int64_t c = 0; c < count; ++c) {
-      a += part[2 * c];
-      b += part[2 * c + 1];
-    }
-    out[0] += a;
-    out[1] += b;
-  }
-}
 
 // ------------------------------------------------------------------ decode + EF
 // For flat index i < d: row = i / cols, col = i % cols.
@@ -410,8 +430,15 @@ __global__ void sum_pairs_kernel(int64_t count, const double *part, double *out)
 //   est = (sum_b P_hat[row][b] * Qsum[col][b]) / n (pipelines.py:365)
 template <int R>
 __global__ void __launch_bounds__(256) decode_kernel(int L, int n, int64_t d, int64_t cols, const float *ph,
-                                                     const float *qw, const float *qsum, float *resid, int64_t ld,
-                                                     float *est) {
+                                                     const float *qw, const float *qsum, float *resid, Rows rw_,
+                                                     float *est, const int64_t *est_offs, int64_t rows) {
+  {
+    const int t = blockIdx.y;
+    ph += static_cast<int64_t>(t) * rows * R;
+    qw += static_cast<int64_t>(t) * L * cols * R;
+    qsum += static_cast<int64_t>(t) * cols * R;
+    if (est) est += est_offs ? est_offs[t] : 0;
+  }
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < d;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t row = i / cols, col = i - row * cols;
@@ -423,7 +450,8 @@ __global__ void __launch_bounds__(256) decode_kernel(int L, int n, int64_t d, in
         double own = 0.0;
 #pragma unroll
         for (int b = 0; b < R; ++b) own += static_cast<double>(p[b]) * static_cast<double>(qw[(w * cols + col) * R + b]);
-        resid[w * ld + i] = resid[w * ld + i] - static_cast<float>(own);
+        const int64_t o = rw_.at(blockIdx.y * L + w) + i;
+        resid[o] = resid[o] - static_cast<float>(own);
       }
     }
     if (est) {
@@ -438,6 +466,8 @@ __global__ void __launch_bounds__(256) decode_kernel(int L, int n, int64_t d, in
 // Gram matrix Q^T Q (fp64) for the rank check of ensure_full_rank (compressors.py:595-603).
 __global__ void __launch_bounds__(256) gram_kernel(int64_t cols, int R, const float *q, double *gram) {
   __shared__ double red[33];
+  q += static_cast<int64_t>(blockIdx.x) * cols * R;
+  gram += static_cast<int64_t>(blockIdx.x) * R * R;
   for (int a = 0; a < R; ++a)
     for (int b = a; b < R; ++b) {
       double v = 0.0;
@@ -448,219 +478,159 @@ __global__ void __launch_bounds__(256) gram_kernel(int64_t cols, int R, const fl
     }
 }
 
-template <int R>
-int launch_rank(int L, int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld, const float *q, float *p,
-                cudaStream_t st) {
-  constexpr int rpc = MqShape<R>::kRowsPerCta;
-  mq_kernel<R><<<dim3(grid_cap((rows + rpc - 1) / rpc), L), 256, 0, st>>>(d, rows, cols, c, ld, q, p);
+#define GC_RANK_SWITCH(rank, CALL)                                                      \
+  switch (rank) {                                                                        \
+    case 1: { constexpr int R = 1; CALL; } break;                                        \
+    case 2: { constexpr int R = 2; CALL; } break;                                        \
+    case 3: { constexpr int R = 3; CALL; } break;                                        \
+    case 4: { constexpr int R = 4; CALL; } break;                                        \
+    case 5: { constexpr int R = 5; CALL; } break;                                        \
+    case 6: { constexpr int R = 6; CALL; } break;                                        \
+    case 7: { constexpr int R = 7; CALL; } break;                                        \
+    case 8: { constexpr int R = 8; CALL; } break;                                        \
+    case 16: { constexpr int R = 16; CALL; } break;                                      \
+    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;          \
+  }
+
+int check_batch(const gc_psgd_batch *b) {
+  GC_REQUIRE(b != nullptr, "batch descriptor is null");
+  GC_REQUIRE(b->tensors >= 1 && b->workers >= 1 && static_cast<int64_t>(b->tensors) * b->workers <= 65535,
+             "batch must have 1..65535 (tensor, worker) rows");
+  GC_REQUIRE(b->row_offsets != nullptr || b->ld >= 1, "need row_offsets or ld");
   return GC_OK;
 }
 
-template <int R>
-void launch_mtp(int L, int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld, const float *ph,
-                double *partial, int splits, cudaStream_t st) {
-  const int64_t per = (rows + splits - 1) / splits;
-  mtp_kernel<R><<<dim3(grid_cap((cols + 255) / 256), splits, L), 256, 0, st>>>(d, rows, cols, c, ld, ph, per,
-                                                                              partial, splits);
-}
-
-template <int R>
-void launch_decode(int L, int n, int64_t d, int64_t cols, const float *ph, const float *qw, const float *qsum,
-                   float *resid, int64_t ld, float *est, cudaStream_t st) {
-  const int64_t g = (d + 255) / 256;
-  decode_kernel<R><<<grid_cap(g > 148 * 16 ? 148 * 16 : g), 256, 0, st>>>(L, n, d, cols, ph, qw, qsum, resid, ld,
-                                                                           est);
-}
-
-template <int R>
-void launch_mq_fused(int L, int64_t d, int64_t rows, int64_t cols, const float *g, float *r, int64_t ld,
-                     const float *q, double *partial, cudaStream_t st) {
-  const int slabs = static_cast<int>((cols + 1023) / 1024);
-  mq_fused_kernel<R><<<dim3(slabs, grid_cap((rows + kMqRows - 1) / kMqRows), L), 256, 0, st>>>(
-      d, rows, cols, g, r, ld, q, partial, slabs);
-}
-
-template <int R>
-void launch_mtp_vec(int L, int64_t d, int64_t rows, int64_t cols, const float *c, int64_t ld, const float *ph,
-                    double *partial, int splits, cudaStream_t st) {
-  const int64_t per = (rows + splits - 1) / splits;
-  mtp_vec_kernel<R><<<dim3(grid_cap((cols + 1023) / 1024), splits, L), 256, 0, st>>>(d, rows, cols, c, ld, ph, per,
-                                                                                   partial, splits);
-}
-
-template <int R>
-void launch_decode_vec(int L, int n, int64_t d, int64_t rows, int64_t cols, const float *ph, const float *qw,
-                       const float *qsum, float *resid, int64_t ld, float *est, cudaStream_t st) {
-  decode_vec_kernel<R><<<dim3(grid_cap((cols + 1023) / 1024), grid_cap((rows + kDecRows - 1) / kDecRows)), 256, 0,
-                         st>>>(L, n, d, rows, cols, ph, qw, qsum, resid, ld, est);
-}
+Rows rows_of(const gc_psgd_batch *b) { return Rows{b->row_offsets, b->ld, b->workers}; }
 
 }  // namespace
 
 extern "C" {
 
-int gc_psgd_vectorizable(int64_t cols, const void *a, const void *b, int64_t ld) {
-  return cols % 4 == 0 && ld % 4 == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
-}
-
-
-int gc_psgd_mq_fused(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
-                     float *resid, int64_t ld, const float *q, float *p, void *workspace, void *stream) {
-  GC_REQUIRE(workers >= 1 && workers <= 65535 && d >= 1 && rows * cols >= d && grads && q && p && workspace,
-             "invalid argument");
-  GC_REQUIRE(gc_psgd_vectorizable(cols, grads, resid ? resid : grads, ld), "mq_fused needs cols % 4 == 0 and aligned rows");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  double *partial = static_cast<double *>(workspace);
-  switch (rank) {
-    case 1: launch_mq_fused<1>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
-    case 2: launch_mq_fused<2>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
-    case 3: launch_mq_fused<3>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
-    case 4: launch_mq_fused<4>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
-    case 5: launch_mq_fused<5>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
-    case 6: launch_mq_fused<6>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
-    case 7: launch_mq_fused<7>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
-    case 8: launch_mq_fused<8>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
-    case 16: launch_mq_fused<16>(workers, d, rows, cols, grads, resid, ld, q, partial, st); break;
-    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
-  }
-  GC_LAUNCH_CHECK("mq_fused_kernel");
-  const int slabs = static_cast<int>((cols + 1023) / 1024);
-  const int64_t total = static_cast<int64_t>(workers) * rows * rank;
-  mq_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(
-      workers, slabs, rows, rank, partial, p);
-  GC_LAUNCH_CHECK("mq_reduce_kernel");
-  return GC_OK;
-}
-
-int gc_psgd_decode_fused(int32_t workers, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
-                         const float *p_hat, const float *q_workers, const float *q_sum, float *resid, int64_t ld,
-                         float *estimate, void *stream) {
-  GC_REQUIRE(workers >= 1 && n >= 1 && d >= 1 && p_hat && q_workers && q_sum && resid && estimate, "invalid argument");
-  GC_REQUIRE(gc_psgd_vectorizable(cols, resid, estimate, ld), "decode_fused needs cols % 4 == 0 and aligned rows");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  switch (rank) {
-    case 1: launch_decode_vec<1>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 2: launch_decode_vec<2>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 3: launch_decode_vec<3>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 4: launch_decode_vec<4>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 5: launch_decode_vec<5>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 6: launch_decode_vec<6>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 7: launch_decode_vec<7>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 8: launch_decode_vec<8>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 16: launch_decode_vec<16>(workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
-  }
-  GC_LAUNCH_CHECK("decode_vec_kernel");
-  return GC_OK;
-}
-
-
-int gc_psgd_splits(int32_t workers, int64_t cols) {
-  const int64_t slabs = (cols % 4 == 0 ? (cols + 1023) / 1024 : (cols + 255) / 256) * workers;
+int gc_psgd_splits(int32_t rows_total, int64_t cols) {
+  const int64_t slabs = (cols % 4 == 0 ? (cols + 1023) / 1024 : (cols + 255) / 256) * rows_total;
   int s = static_cast<int>((8 * 148 + slabs - 1) / slabs);
   return s < 1 ? 1 : (s > 64 ? 64 : s);
 }
 
-int64_t gc_psgd_workspace_bytes(int32_t workers, int64_t rows, int64_t cols, int32_t rank) {
-  const int64_t splits = gc_psgd_splits(workers, cols);
-  const int64_t mtp = 8 * (static_cast<int64_t>(workers) * splits * cols * rank);
-  const int64_t mq = 8 * (static_cast<int64_t>(workers) * ((cols + 1023) / 1024) * rows * rank);
+int64_t gc_psgd_workspace_bytes(int32_t rows_total, int64_t rows, int64_t cols, int32_t rank) {
+  const int64_t splits = gc_psgd_splits(rows_total, cols);
+  const int64_t mtp = 8 * (static_cast<int64_t>(rows_total) * splits * cols * rank);
+  const int64_t mq = 8 * (static_cast<int64_t>(rows_total) * ((cols + 1023) / 1024) * rows * rank);
   return (mtp > mq ? mtp : mq) + 256;
 }
 
-int gc_psgd_mq(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c, int64_t ld,
+int gc_psgd_vectorizable(int64_t cols, const void *a, const void *b, int64_t ld) {
+  return cols % 4 == 0 && ld % 4 == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+}
+
+int gc_psgd_mq(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                const float *q, float *p, void *stream) {
-  GC_REQUIRE(workers >= 1 && workers <= 65535 && d >= 1 && rows * cols >= d && c && q && p, "invalid argument");
+  if (int rc = check_batch(b)) return rc;
+  GC_REQUIRE(d >= 1 && rows * cols >= d && c && q && p, "invalid argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  switch (rank) {
-    case 1: launch_rank<1>(workers, d, rows, cols, c, ld, q, p, st); break;
-    case 2: launch_rank<2>(workers, d, rows, cols, c, ld, q, p, st); break;
-    case 3: launch_rank<3>(workers, d, rows, cols, c, ld, q, p, st); break;
-    case 4: launch_rank<4>(workers, d, rows, cols, c, ld, q, p, st); break;
-    case 5: launch_rank<5>(workers, d, rows, cols, c, ld, q, p, st); break;
-    case 6: launch_rank<6>(workers, d, rows, cols, c, ld, q, p, st); break;
-    case 7: launch_rank<7>(workers, d, rows, cols, c, ld, q, p, st); break;
-    case 8: launch_rank<8>(workers, d, rows, cols, c, ld, q, p, st); break;
-    case 16: launch_rank<16>(workers, d, rows, cols, c, ld, q, p, st); break;
-    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
-  }
+  const int L = b->tensors * b->workers;
+  GC_RANK_SWITCH(rank, ({
+    constexpr int rpc = MqShape<R>::kRowsPerCta;
+    mq_kernel<R><<<dim3(grid_cap((rows + rpc - 1) / rpc), L), 256, 0, st>>>(d, rows, cols, c, rows_of(b), q, p);
+  }));
   GC_LAUNCH_CHECK("mq_kernel");
   return GC_OK;
 }
 
-int gc_psgd_mtp(int32_t workers, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c, int64_t ld,
-                const float *p_hat, float *q, void *workspace, void *stream) {
-  GC_REQUIRE(workers >= 1 && workers <= 65535 && d >= 1 && rows * cols >= d && c && p_hat && q && workspace,
-             "invalid argument");
+int gc_psgd_mq_fused(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
+                     float *resid, const float *q, float *p, void *workspace, void *stream) {
+  if (int rc = check_batch(b)) return rc;
+  GC_REQUIRE(d >= 1 && rows * cols >= d && grads && q && p && workspace, "invalid argument");
+  GC_REQUIRE(cols % 4 == 0 && b->rows_aligned, "mq_fused needs cols % 4 == 0 and 16-byte aligned rows");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int splits = gc_psgd_splits(workers, cols);
+  const int L = b->tensors * b->workers;
+  const int slabs = static_cast<int>((cols + 1023) / 1024);
   double *partial = static_cast<double *>(workspace);
-  if (gc_psgd_vectorizable(cols, c, c, ld)) {
-    switch (rank) {
-      case 1: launch_mtp_vec<1>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-      case 2: launch_mtp_vec<2>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-      case 3: launch_mtp_vec<3>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-      case 4: launch_mtp_vec<4>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-      case 5: launch_mtp_vec<5>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-      case 6: launch_mtp_vec<6>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-      case 7: launch_mtp_vec<7>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-      case 8: launch_mtp_vec<8>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-      case 16: launch_mtp_vec<16>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-      default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
-    }
-  } else switch (rank) {
-    case 1: launch_mtp<1>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-    case 2: launch_mtp<2>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-    case 3: launch_mtp<3>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-    case 4: launch_mtp<4>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-    case 5: launch_mtp<5>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-    case 6: launch_mtp<6>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-    case 7: launch_mtp<7>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-    case 8: launch_mtp<8>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-    case 16: launch_mtp<16>(workers, d, rows, cols, c, ld, p_hat, partial, splits, st); break;
-    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
+  GC_RANK_SWITCH(rank, ({
+    mq_fused_kernel<R><<<dim3(slabs, grid_cap((rows + kMqRows - 1) / kMqRows), L), 256, 0, st>>>(
+        d, rows, cols, grads, resid, rows_of(b), q, partial, slabs);
+  }));
+  GC_LAUNCH_CHECK("mq_fused_kernel");
+  const int64_t total = static_cast<int64_t>(L) * rows * rank;
+  mq_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(
+      L, slabs, rows, rank, partial, p);
+  GC_LAUNCH_CHECK("mq_reduce_kernel");
+  return GC_OK;
+}
+
+int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
+                const float *p_hat, float *q, void *workspace, void *stream) {
+  if (int rc = check_batch(b)) return rc;
+  GC_REQUIRE(d >= 1 && rows * cols >= d && c && p_hat && q && workspace, "invalid argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int L = b->tensors * b->workers;
+  const int splits = gc_psgd_splits(L, cols);
+  const int64_t per = (rows + splits - 1) / splits;
+  double *partial = static_cast<double *>(workspace);
+  const bool vec = cols % 4 == 0 && b->rows_aligned && (reinterpret_cast<uintptr_t>(c) & 15) == 0;
+  if (vec) {
+    GC_RANK_SWITCH(rank, ({
+      mtp_vec_kernel<R><<<dim3(grid_cap((cols + 1023) / 1024), splits, L), 256, 0, st>>>(
+          d, rows, cols, c, rows_of(b), p_hat, per, partial, splits);
+    }));
+  } else {
+    GC_RANK_SWITCH(rank, ({
+      mtp_kernel<R><<<dim3(grid_cap((cols + 255) / 256), splits, L), 256, 0, st>>>(d, rows, cols, c, rows_of(b),
+                                                                                  p_hat, per, partial, splits);
+    }));
   }
   GC_LAUNCH_CHECK("mtp_kernel");
-  const int64_t total = static_cast<int64_t>(workers) * cols * rank;
+  const int64_t total = static_cast<int64_t>(L) * cols * rank;
   mtp_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(
-      workers, splits, cols, rank, partial, q);
+      L, splits, cols, rank, partial, q);
   GC_LAUNCH_CHECK("mtp_reduce_kernel");
   return GC_OK;
 }
 
-int gc_psgd_orthonormalize(int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace, int32_t *status,
-                           void *stream) {
-  GC_REQUIRE(rows >= rank && rank >= 1 && rank <= kMaxRank && p && p_hat && workspace && status, "invalid argument");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  mgs_kernel<<<1, 1024, 0, st>>>(rows, rank, p, static_cast<double *>(workspace), p_hat, status);
+int gc_psgd_orthonormalize(int32_t tensors, int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace,
+                           int32_t *status, void *stream) {
+  GC_REQUIRE(tensors >= 1 && rows >= rank && rank >= 1 && rank <= kMaxRank && p && p_hat && workspace && status,
+             "invalid argument");
+  mgs_kernel<<<tensors, 1024, 0, static_cast<cudaStream_t>(stream)>>>(rows, rank, p, static_cast<double *>(workspace),
+                                                                     p_hat, status);
   GC_LAUNCH_CHECK("mgs_kernel");
   return GC_OK;
 }
 
-int gc_psgd_decode(int32_t workers, int32_t n, int64_t d, int64_t cols, int32_t rank, const float *p_hat,
-                   const float *q_workers, const float *q_sum, float *resid, int64_t ld, float *estimate,
+int gc_psgd_decode(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                   const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
                    void *stream) {
-  GC_REQUIRE(workers >= 1 && n >= 1 && d >= 1 && cols >= 1 && p_hat, "invalid argument");
+  if (int rc = check_batch(b)) return rc;
+  GC_REQUIRE(n >= 1 && d >= 1 && cols >= 1 && p_hat && q_workers && q_sum, "invalid argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  switch (rank) {
-    case 1: launch_decode<1>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 2: launch_decode<2>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 3: launch_decode<3>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 4: launch_decode<4>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 5: launch_decode<5>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 6: launch_decode<6>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 7: launch_decode<7>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 8: launch_decode<8>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    case 16: launch_decode<16>(workers, n, d, cols, p_hat, q_workers, q_sum, resid, ld, estimate, st); break;
-    default: gc_set_error("rank must be 1..8 or 16"); return GC_ERR_UNSUPPORTED;
-  }
+  const int64_t g = (d + 255) / 256;
+  GC_RANK_SWITCH(rank, ({
+    decode_kernel<R><<<dim3(grid_cap(g > 148 * 16 ? 148 * 16 : g), b->tensors), 256, 0, st>>>(
+        b->workers, n, d, cols, p_hat, q_workers, q_sum, resid, rows_of(b), estimate, b->est_offsets, rows);
+  }));
   GC_LAUNCH_CHECK("decode_kernel");
   return GC_OK;
 }
 
-int gc_psgd_gram(int64_t cols, int32_t rank, const float *q, double *gram, void *stream) {
-  GC_REQUIRE(cols >= 1 && rank >= 1 && rank <= kMaxRank && q && gram, "invalid argument");
-  gram_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(cols, rank, q, gram);
+int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                         const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
+                         void *stream) {
+  if (int rc = check_batch(b)) return rc;
+  GC_REQUIRE(n >= 1 && d >= 1 && p_hat && q_workers && q_sum, "invalid argument");
+  GC_REQUIRE(cols % 4 == 0 && b->rows_aligned, "decode_fused needs cols % 4 == 0 and 16-byte aligned rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  GC_RANK_SWITCH(rank, ({
+    decode_vec_kernel<R><<<dim3(grid_cap((cols + 1023) / 1024), grid_cap((rows + kDecRows - 1) / kDecRows),
+                               b->tensors), 256, 0, st>>>(b->workers, n, d, rows, cols, p_hat, q_workers, q_sum,
+                                                          resid, rows_of(b), estimate, b->est_offsets);
+  }));
+  GC_LAUNCH_CHECK("decode_vec_kernel");
+  return GC_OK;
+}
+
+int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, double *gram, void *stream) {
+  GC_REQUIRE(tensors >= 1 && cols >= 1 && rank >= 1 && rank <= kMaxRank && q && gram, "invalid argument");
+  gram_kernel<<<tensors, 256, 0, static_cast<cudaStream_t>(stream)>>>(cols, rank, q, gram);
   GC_LAUNCH_CHECK("gram_kernel");
   return GC_OK;
 }

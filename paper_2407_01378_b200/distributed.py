@@ -415,13 +415,22 @@ class _Chunked(_Base):
 class _PowerSgd(_Base):
     def __init__(self, cfg: PowerSgdConfig, pipe):
         super().__init__(pipe)
-        from .schemes import PowerSgdEngine
-        # reuse the simulated engine's seed / rank logic with the local worker count
-        self.local = PowerSgdEngine(cfg, self.L, self.dim, self.seeds, self.dev)
-        self.local.n = self.L
+        from .schemes import PowerSgdGroup
         self.cfg = cfg
-        self.rows, self.cols, self.r = self.local.rows, self.local.cols, cfg.rank
-        self.warm = None
+        self.bypass = self.dim < cfg.bypass_below
+        self.grp = None if self.bypass else PowerSgdGroup(cfg, self.n, self.L, self.dim, 1, self.seeds, self.dev)
+
+    @property
+    def warm(self):
+        return None if self.grp is None or self.grp.warm is None else self.grp.warm[0]
+
+    def _fold(self, kind, x, m):
+        """Gather every rank's factor rows, then fold them in the reference ring order."""
+        n = self.n
+        rows = self.comm.all_gather_rows(x.reshape(self.L, m))
+        out = torch.empty(1, m, dtype=torch.float32, device=self.dev)
+        _native.call("gc_float_fold", n, m, rows.data_ptr(), m, 0, -(-m // n), 0, 0, 0, out.data_ptr(), _sp())
+        return out
 
     def run(self, g, res, r, ledger, nmse):
         L, n, d = self.L, self.n, self.dim
@@ -430,46 +439,22 @@ class _PowerSgd(_Base):
         if res is not None:
             _native.call("gc_ef_apply", L, d, g.data_ptr(), res.data_ptr(), g.stride(0), res.data_ptr(),
                          res.stride(0), sp)
-            c = res
-        else:
-            c = g
-        ld = c.stride(0)
-        if self.local.bypass:
+        c = res if res is not None else g
+        if self.bypass:
             all_c = self.comm.all_gather_rows(c)
             _native.call("gc_float_fold", n, d, all_c.data_ptr(), d, 0, -(-d // n), 0, 0, n, est.data_ptr(), sp)
             if res is not None:
                 _native.call("gc_fill_zero", res.data_ptr(), res.numel() * 4, sp)
             ledger.charge_ring("dense-bypass", n, d, 32)
             return est, 32.0 * d, _simple_stats(None)
-        rows, cols, rk = self.rows, self.cols, self.r
-        self.local.warm = self.warm
-        q = self.local._seed_q(r)
-        p = torch.empty(L, rows, rk, dtype=torch.float32, device=self.dev)
-        _native.call("gc_psgd_mq", L, d, rows, cols, rk, c.data_ptr(), ld, q.data_ptr(), p.data_ptr(), sp)
-        all_p = self.comm.all_gather_rows(p)
-        L1 = rows * rk
-        p_sum = torch.empty(rows, rk, dtype=torch.float32, device=self.dev)
-        _native.call("gc_float_fold", n, L1, all_p.data_ptr(), L1, 0, -(-L1 // n), 0, 0, 0, p_sum.data_ptr(), sp)
-        p_hat = torch.empty(rows, rk, dtype=torch.float32, device=self.dev)
-        status = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        _native.call("gc_psgd_orthonormalize", rows, rk, p_sum.data_ptr(), p_hat.data_ptr(),
-                     self.local.mgs_ws.data_ptr(), status.data_ptr(), sp)
-        qw = torch.empty(L, cols, rk, dtype=torch.float32, device=self.dev)
-        _native.call("gc_psgd_mtp", L, d, rows, cols, rk, c.data_ptr(), ld, p_hat.data_ptr(), qw.data_ptr(),
-                     self.local.ws.data_ptr(), sp)
-        all_q = self.comm.all_gather_rows(qw)
-        L2 = cols * rk
-        q_sum = torch.empty(cols, rk, dtype=torch.float32, device=self.dev)
-        _native.call("gc_float_fold", n, L2, all_q.data_ptr(), L2, 0, -(-L2 // n), 0, 0, 0, q_sum.data_ptr(), sp)
-        _native.call("gc_psgd_decode", L, n, d, cols, rk, p_hat.data_ptr(), qw.data_ptr(), q_sum.data_ptr(),
-                     _ptr(res), ld, est.data_ptr(), sp)
-        warm = torch.empty(cols, rk, dtype=torch.float32, device=self.dev)
-        _native.call("gc_scale_div", L2, q_sum.data_ptr(), n, warm.data_ptr(), sp)
-        self.warm = warm
+        grp = self.grp
+        vec = bool(_native.lib().gc_psgd_vectorizable(grp.cols, c.data_ptr(), est.data_ptr(), c.stride(0)))
+        grp.set_ld(c.stride(0), vec)
+        grp.run(c.data_ptr(), _ptr(res), est.data_ptr(), r, vec=vec, fold=self._fold)
         self.launches += 11
-        ledger.charge_ring("left-factor", n, rows * rk, 32)
-        ledger.charge_ring("right-factor", n, cols * rk, 32)
-        return est, 32.0 * rk * (rows + cols), _simple_stats(None)
+        ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
+        ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)
+        return est, 32.0 * grp.rank * (grp.rows + grp.cols), _simple_stats(None)
 
 
 class _Dense(_Base):

@@ -353,59 +353,151 @@ class ChunkedEngine(Engine):
 
 
 # ----------------------------------------------------------------------------- PowerSGD
-class PowerSgdEngine(Engine):
-    """pipelines.py:324-368 (PowerSgdConfig), warm start and dense bypass included."""
+class PowerSgdGroup:
+    """T independent PowerSGD pipelines of the same length d (hence the same rows x cols),
+    L workers each, run as one batch of kernels (pipelines.py:338-368 per tensor).
+
+    The single-matrix reference path is T = 1 with rows at w * ld; the chunked mode of
+    cfg4(b) passes per-(tensor, worker) row offsets into the flat per-worker gradients."""
 
     RANKS = (1, 2, 3, 4, 5, 6, 7, 8, 16)
+
+    def __init__(self, cfg: PowerSgdConfig, n: int, L: int, d: int, T: int, seeds: SeedSpec, device,
+                 row_offsets=None, est_offsets=None, ld: int = 0):
+        self.cfg, self.n, self.L, self.d, self.T = cfg, n, L, d, T
+        self.seeds, self.device = seeds, device
+        self.rows, self.cols = matrix_shape_for(d)
+        self.rank = cfg.rank
+        if self.rank not in self.RANKS:
+            raise NotImplementedError(f"PowerSGD rank {self.rank} not compiled (supported: {self.RANKS})")
+        if self.rows < self.rank:
+            raise ValueError("need a tall matrix (rows >= cols)")
+        self.row_offsets, self.est_offsets = row_offsets, est_offsets
+        self.batch = _native.PsgdBatch(T, L, _ptr(row_offsets), ld, _ptr(est_offsets), 0)
+        ws = int(_native.lib().gc_psgd_workspace_bytes(T * L, self.rows, self.cols, self.rank))
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
+        self.mgs_ws = torch.empty(T * self.rows * self.rank, dtype=torch.float64, device=device)
+        self.warm = None          # [T][cols][r]
+        self.last = {}
+
+    def set_ld(self, ld: int, aligned: bool = False):
+        self.batch.ld = ld
+        self.batch.rows_aligned = 1 if aligned else 0
+
+    def _rank_ok(self, q_dev):
+        """Per tensor: np.linalg.matrix_rank(q) == rank (compressors.py:599), decided from the fp64
+        Gram eigenvalues computed on the device; near numpy's tolerance the exact numpy call on a
+        host copy decides."""
+        import numpy as np
+        T, r, cols = self.T, self.rank, self.cols
+        gram = torch.empty(T, r, r, dtype=torch.float64, device=self.device)
+        _native.call("gc_psgd_gram", T, cols, r, q_dev.data_ptr(), gram.data_ptr(), _sp())
+        ok = []
+        host = gram.cpu().numpy()
+        for t in range(T):
+            sig = np.sqrt(np.clip(np.linalg.eigvalsh(host[t]), 0.0, None))
+            tol = sig.max() * max(cols, r) * np.finfo(np.float32).eps
+            if np.all((sig > 2 * tol) | (sig < 0.5 * tol)):
+                ok.append(int(np.count_nonzero(sig > tol)) == r)
+            else:
+                ok.append(int(np.linalg.matrix_rank(q_dev[t].cpu().numpy())) == r)
+        return ok
+
+    def seed_q(self, round_index):
+        """Seed matrices with ensure_full_rank's redraws, one reference rng per tensor
+        (pipelines.py:341-346, compressors.py:591-603)."""
+        import numpy as np
+        from .configs import DegenerateMatrixError
+        T, cols, r = self.T, self.cols, self.rank
+        warm = self.cfg.warm_start and self.warm is not None
+        if warm:
+            q = self.warm.clone()
+            draws = [0] * T
+        else:
+            first = self.seeds.rng("lowrank-seed", round_index).standard_normal((cols, r)).astype(np.float32)
+            q = torch.from_numpy(first).to(self.device).unsqueeze(0).repeat(T, 1, 1).contiguous()
+            draws = [1] * T
+        for attempt in range(4):
+            ok = self._rank_ok(q)
+            if all(ok):
+                return q
+            if attempt == 3:
+                raise DegenerateMatrixError("seed matrix rank-deficient after redraws")
+            for t in range(T):
+                if not ok[t]:   # continue this tensor's own rng stream
+                    rng = self.seeds.rng("lowrank-seed", round_index)
+                    for _ in range(draws[t]):
+                        rng.standard_normal((cols, r))
+                    q[t] = torch.from_numpy(rng.standard_normal((cols, r)).astype(np.float32)).to(self.device)
+                    draws[t] += 1
+        return q
+
+    def run(self, c_ptr: int, resid_ptr, est_ptr: int, round_index: int, grads_ptr=None, vec=False, fold=None,
+            before_ef=None):
+        """One round for the batch.  c_ptr: corrected matrices (or raw gradients when grads_ptr is
+        given together with vec: ef_apply fused into P = M Q, corrected written over resid).
+        fold(kind, x [T*L][m], m) -> [T][m] sums in the reference ring order (simulated: local fold;
+        distributed: gather + fold).  before_ef() runs after the estimate, before the residuals
+        change (the nmse hook).  Returns warm Q [T][cols][r]."""
+        sp = _sp()
+        T, L, n, d, rows, cols, r = self.T, self.L, self.n, self.d, self.rows, self.cols, self.rank
+        dev = self.device
+        bref = ctypes.byref(self.batch)
+        q = self.seed_q(round_index)
+        p = torch.empty(T * L, rows, r, dtype=torch.float32, device=dev)
+        if vec and grads_ptr is not None:
+            _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, grads_ptr, resid_ptr, q.data_ptr(), p.data_ptr(),
+                         self.ws.data_ptr(), sp)
+        elif vec:
+            _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, c_ptr, None, q.data_ptr(), p.data_ptr(),
+                         self.ws.data_ptr(), sp)
+        else:
+            _native.call("gc_psgd_mq", bref, d, rows, cols, r, c_ptr, q.data_ptr(), p.data_ptr(), sp)
+        p_sum = fold("left-factor", p, rows * r).reshape(T, rows, r)
+        p_hat = torch.empty(T, rows, r, dtype=torch.float32, device=dev)
+        status = torch.zeros(T, dtype=torch.int32, device=dev)
+        _native.call("gc_psgd_orthonormalize", T, rows, r, p_sum.data_ptr(), p_hat.data_ptr(), self.mgs_ws.data_ptr(),
+                     status.data_ptr(), sp)
+        qw = torch.empty(T * L, cols, r, dtype=torch.float32, device=dev)
+        _native.call("gc_psgd_mtp", bref, d, rows, cols, r, c_ptr, p_hat.data_ptr(), qw.data_ptr(),
+                     self.ws.data_ptr(), sp)
+        q_sum = fold("right-factor", qw, cols * r).reshape(T, cols, r)
+        if vec and before_ef is None and resid_ptr is not None:
+            _native.call("gc_psgd_decode_fused", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
+                         q_sum.data_ptr(), resid_ptr, est_ptr, sp)
+        else:
+            _native.call("gc_psgd_decode", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
+                         q_sum.data_ptr(), None, est_ptr, sp)
+            if before_ef is not None:
+                before_ef()
+            if resid_ptr is not None:
+                _native.call("gc_psgd_decode", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
+                             q_sum.data_ptr(), resid_ptr, None, sp)
+        warm = torch.empty(T, cols, r, dtype=torch.float32, device=dev)
+        _native.call("gc_scale_div", T * cols * r, q_sum.data_ptr(), n, warm.data_ptr(), sp)   # pipelines.py:366
+        self.warm = warm
+        self.last = {"p_hat": p_hat, "q_sum": q_sum, "seed_q": q, "status": status, "qw": qw}
+        return warm
+
+
+class PowerSgdEngine(Engine):
+    """pipelines.py:324-368 (PowerSgdConfig), warm start and dense bypass included."""
 
     def __init__(self, cfg: PowerSgdConfig, n, dim, seeds, device):
         super().__init__(n, dim, seeds, device)
         self.cfg = cfg
-        self.rows, self.cols = matrix_shape_for(dim)
-        self.rank = cfg.rank
         self.bypass = dim < cfg.bypass_below
-        if not self.bypass:
-            if self.rank not in self.RANKS:
-                raise NotImplementedError(f"PowerSGD rank {self.rank} not compiled (supported: {self.RANKS})")
-            if self.rows < self.rank:
-                raise ValueError("need a tall matrix (rows >= cols)")
-            ws = int(_native.lib().gc_psgd_workspace_bytes(n, self.rows, self.cols, self.rank))
-            self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
-            self.mgs_ws = torch.empty(self.rows * self.rank, dtype=torch.float64, device=device)
-        self.warm = None
+        self.group = None if self.bypass else PowerSgdGroup(cfg, n, n, dim, 1, seeds, device)
 
     def warm_q(self):
-        return self.warm
+        return None if self.group is None or self.group.warm is None else self.group.warm[0]
 
-    def _rank_ok(self, q_dev) -> bool:
-        """np.linalg.matrix_rank(q) == rank (compressors.py:599), via the fp64 Gram matrix on the
-        device; near the numpy tolerance the exact numpy call on a host copy decides."""
-        import numpy as np
-        r, cols = self.rank, self.cols
-        gram = torch.empty(r, r, dtype=torch.float64, device=self.device)
-        _native.call("gc_psgd_gram", cols, r, q_dev.data_ptr(), gram.data_ptr(), _sp())
-        ev = np.clip(np.linalg.eigvalsh(gram.cpu().numpy()), 0.0, None)
-        sig = np.sqrt(ev)
-        tol = sig.max() * max(cols, r) * np.finfo(np.float32).eps
-        if np.all((sig > 2 * tol) | (sig < 0.5 * tol)):
-            return int(np.count_nonzero(sig > tol)) == r
-        return int(np.linalg.matrix_rank(q_dev.cpu().numpy())) == r
-
-    def _seed_q(self, round_index):
-        """Seed matrix with ensure_full_rank's redraws (pipelines.py:341-346, compressors.py:591-603)."""
-        import numpy as np
-        from .configs import DegenerateMatrixError
-        rng = self.seeds.rng("lowrank-seed", round_index)
-        if self.cfg.warm_start and self.warm is not None:
-            q = self.warm
-        else:
-            q = torch.from_numpy(rng.standard_normal((self.cols, self.rank)).astype(np.float32)).to(self.device)
-        for remaining in range(3, -1, -1):
-            if self._rank_ok(q):
-                return q.contiguous()
-            if remaining:
-                q = torch.from_numpy(rng.standard_normal((self.cols, self.rank)).astype(np.float32)).to(self.device)
-        raise DegenerateMatrixError("seed matrix rank-deficient after redraws")
+    def _fold(self, kind, x, m):
+        n = self.n
+        out = torch.empty(x.shape[0] // n, m, dtype=torch.float32, device=self.device)
+        _native.call("gc_float_fold_batched", x.shape[0] // n, n, m, x.data_ptr(), m, n * m, 0, 0, 0, out.data_ptr(),
+                     m, _sp())
+        return out
 
     def run(self, grads, res, round_index, ledger, nmse=True):
         n, d = self.n, self.dim
@@ -413,79 +505,48 @@ class PowerSgdEngine(Engine):
         dev = self.device
         est = torch.empty(d, dtype=torch.float32, device=dev)
         acc = torch.zeros(2, dtype=torch.float64, device=dev) if nmse else None
-        rows, cols, r = self.rows, self.cols, self.rank
-        lib = _native.lib()
-        vec = (not self.bypass and res is not None and
-               bool(lib.gc_psgd_vectorizable(cols, grads.data_ptr(), res.data_ptr(), grads.stride(0))) and
-               grads.stride(0) == res.stride(0))
-        if not vec:
-            if res is not None:   # corrected lives in r from here on
+        if self.bypass:   # dense fp32 ring (pipelines.py:326-336); own = corrected -> r_new = 0
+            if res is not None:
                 _native.call("gc_ef_apply", n, d, grads.data_ptr(), res.data_ptr(), grads.stride(0), res.data_ptr(),
                              res.stride(0), sp)
-                self.launches += 1
             c = res if res is not None else grads
-        else:
-            c = res
-        ld = c.stride(0)
-        if self.bypass:   # dense fp32 ring (pipelines.py:326-336); own = corrected -> r_new = 0
-            _native.call("gc_float_fold", n, d, c.data_ptr(), ld, 0, -(-d // n), 0, 0, n, est.data_ptr(), sp)
+            _native.call("gc_float_fold", n, d, c.data_ptr(), c.stride(0), 0, -(-d // n), 0, 0, n, est.data_ptr(), sp)
             if nmse:
                 self._nmse(c, None, est, acc)
             if res is not None:
                 _native.call("gc_fill_zero", res.data_ptr(), res.numel() * 4, sp)
-            self.launches += 3
+            self.launches += 4
             ledger.charge_ring("dense-bypass", n, d, 32)
             return est, 32.0 * d, _simple_stats(acc)
 
-        q = self._seed_q(round_index)
+        grp = self.group
+        lib = _native.lib()
+        fuse_ef = bool(res is not None and grads.stride(0) == res.stride(0) and
+                       lib.gc_psgd_vectorizable(grp.cols, grads.data_ptr(), res.data_ptr(), grads.stride(0)))
+        if fuse_ef:   # ef_apply fused into P = M Q
+            c, gptr = res, grads.data_ptr()
+        else:
+            if res is not None:
+                _native.call("gc_ef_apply", n, d, grads.data_ptr(), res.data_ptr(), grads.stride(0), res.data_ptr(),
+                             res.stride(0), sp)
+                self.launches += 1
+            c, gptr = (res if res is not None else grads), None
+        vec = bool(lib.gc_psgd_vectorizable(grp.cols, c.data_ptr(), est.data_ptr(), c.stride(0)))
+        grp.set_ld(c.stride(0), vec)
         ev = self._ev()
         if ev:
             ev[0].record()
-        p = torch.empty(n, rows, r, dtype=torch.float32, device=dev)
-        if vec:   # ef_apply fused into the P = M Q pass
-            _native.call("gc_psgd_mq_fused", n, d, rows, cols, r, grads.data_ptr(), res.data_ptr(), ld, q.data_ptr(),
-                         p.data_ptr(), self.ws.data_ptr(), sp)
-        else:
-            _native.call("gc_psgd_mq", n, d, rows, cols, r, c.data_ptr(), ld, q.data_ptr(), p.data_ptr(), sp)
-        p_sum = torch.empty(rows, r, dtype=torch.float32, device=dev)
-        L1 = rows * r
-        _native.call("gc_float_fold", n, L1, p.data_ptr(), L1, 0, -(-L1 // n), 0, 0, 0, p_sum.data_ptr(), sp)
-        p_hat = torch.empty(rows, r, dtype=torch.float32, device=dev)
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
-        _native.call("gc_psgd_orthonormalize", rows, r, p_sum.data_ptr(), p_hat.data_ptr(), self.mgs_ws.data_ptr(),
-                     status.data_ptr(), sp)
-        qw = torch.empty(n, cols, r, dtype=torch.float32, device=dev)
-        _native.call("gc_psgd_mtp", n, d, rows, cols, r, c.data_ptr(), ld, p_hat.data_ptr(), qw.data_ptr(),
-                     self.ws.data_ptr(), sp)
-        q_sum = torch.empty(cols, r, dtype=torch.float32, device=dev)
-        L2 = cols * r
-        _native.call("gc_float_fold", n, L2, qw.data_ptr(), L2, 0, -(-L2 // n), 0, 0, 0, q_sum.data_ptr(), sp)
-        if vec and not nmse:   # residual updates and the estimate in one pass
-            _native.call("gc_psgd_decode_fused", n, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
-                         q_sum.data_ptr(), res.data_ptr(), ld, est.data_ptr(), sp)
-            if ev:
-                ev[1].record()
-            self.launches += 9
-        else:
-            _native.call("gc_psgd_decode", n, n, d, cols, r, p_hat.data_ptr(), qw.data_ptr(), q_sum.data_ptr(), None,
-                         ld, est.data_ptr(), sp)
-            if ev:
-                ev[1].record()
-            if nmse:
-                self._nmse(c, None, est, acc)
-            if res is not None:
-                _native.call("gc_psgd_decode", n, n, d, cols, r, p_hat.data_ptr(), qw.data_ptr(),
-                             q_sum.data_ptr(), res.data_ptr(), ld, None, sp)
-            self.launches += 10
-        warm = torch.empty(cols, r, dtype=torch.float32, device=dev)
-        _native.call("gc_scale_div", L2, q_sum.data_ptr(), n, warm.data_ptr(), sp)   # pipelines.py:366
-        self.warm = warm
-        self.launches += 1
+        before = (lambda: self._nmse(c, None, est, acc)) if nmse else None
+        grp.run(c.data_ptr(), _ptr(res), est.data_ptr(), round_index, grads_ptr=gptr, vec=vec, fold=self._fold,
+                before_ef=before)
+        if ev:
+            ev[1].record()
+        self.launches += 10
         if self.capture:
-            self.last = {"p_hat": p_hat, "q_sum": q_sum, "seed_q": q, "status": status}
-        ledger.charge_ring("left-factor", n, rows * r, 32)
-        ledger.charge_ring("right-factor", n, cols * r, 32)
-        return est, 32.0 * r * (rows + cols), _simple_stats(acc)
+            self.last = {k: (v[0] if k not in ("status", "qw") else v) for k, v in grp.last.items()}
+        ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
+        ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)
+        return est, 32.0 * grp.rank * (grp.rows + grp.cols), _simple_stats(acc)
 
 
 def make_engine(cfg, n, dim, seeds, device, fused=True) -> Engine:
