@@ -168,6 +168,9 @@ class TensorListPipeline:
 
         sp = _sp()
         res = self._res
+        # seed matrices of every group first: their rank checks read a few bytes back to the host,
+        # so doing them before the heavy kernels keeps the device queue free of bubbles
+        qs = [grp.seed_q(round_index) for grp in self.groups]
         if res is not None:   # corrected vectors of every tensor, kept in r until the EF updates
             _native.call("gc_ef_apply", n, D, g.data_ptr(), res.data_ptr(), g.stride(0), res.data_ptr(),
                          res.stride(0), sp)
@@ -180,10 +183,13 @@ class TensorListPipeline:
             for t in self.bypass:
                 ledger.charge_ring("dense-bypass", n, self.sizes[t], 32)
                 bits += 32.0 * self.sizes[t]
-        # compressed tensors, batched by shape: estimates first, then (after nmse) the EF updates
-        for grp in self.groups:
+        # compressed tensors, batched by shape.  Without nmse the residual update rides in the
+        # decode pass; with nmse the estimates come first and the EF updates after it.
+        fuse_ef = res is not None and acc is None
+        for grp, q in zip(self.groups, qs):
             grp.set_ld(c.stride(0), grp.vec and c.data_ptr() % 16 == 0 and est.data_ptr() % 16 == 0)
-            grp.run(c.data_ptr(), None, est.data_ptr(), round_index, vec=bool(grp.batch.rows_aligned), fold=self._fold)
+            grp.run(c.data_ptr(), res.data_ptr() if fuse_ef else None, est.data_ptr(), round_index,
+                    vec=bool(grp.batch.rows_aligned), fold=self._fold, q=q)
             grp.saved = dict(grp.last)
             for t in grp.tensor_ids:
                 ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
@@ -195,7 +201,7 @@ class TensorListPipeline:
             if self.bypass:   # own == corrected: residual 0
                 _native.call("gc_segment_fold_ef", n, len(self.bypass), self.seg_off.data_ptr(),
                              self.seg_len.data_ptr(), c.data_ptr(), res.data_ptr(), c.stride(0), est.data_ptr(), sp)
-            for grp in self.groups:
+            for grp in ([] if fuse_ef else self.groups):
                 sv = grp.saved
                 _native.call("gc_psgd_decode", __import__("ctypes").byref(grp.batch), n, grp.d, grp.rows, grp.cols,
                              grp.rank, sv["p_hat"].data_ptr(), sv["qw"].data_ptr(), sv["q_sum"].data_ptr(),

@@ -433,7 +433,7 @@ class PowerSgdGroup:
         return q
 
     def run(self, c_ptr: int, resid_ptr, est_ptr: int, round_index: int, grads_ptr=None, vec=False, fold=None,
-            before_ef=None):
+            before_ef=None, q=None):
         """One round for the batch.  c_ptr: corrected matrices (or raw gradients when grads_ptr is
         given together with vec: ef_apply fused into P = M Q, corrected written over resid).
         fold(kind, x [T*L][m], m) -> [T][m] sums in the reference ring order (simulated: local fold;
@@ -443,7 +443,8 @@ class PowerSgdGroup:
         T, L, n, d, rows, cols, r = self.T, self.L, self.n, self.d, self.rows, self.cols, self.rank
         dev = self.device
         bref = ctypes.byref(self.batch)
-        q = self.seed_q(round_index)
+        if q is None:
+            q = self.seed_q(round_index)
         p = torch.empty(T * L, rows, r, dtype=torch.float32, device=dev)
         if vec and grads_ptr is not None:
             _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, grads_ptr, resid_ptr, q.data_ptr(), p.data_ptr(),

@@ -34,6 +34,7 @@ def main():
         ("topk_1pct_cfg3", gcb.TopKConfig(1_100_000), 110_000_000),
         ("topkc_1pct_cfg3", gcb.ChunkedTopKConfig(64, 17_187), 110_000_000),
         ("powersgd_r4_cfg4", gcb.PowerSgdConfig(4), 350_000_000),
+        ("powersgd_r4_gpt2m_chunked", gcb.PowerSgdConfig(4), "gpt2m"),
         ("dense16_cfg2", gcb.DenseConfig(16), 25_557_032),
         ("dense16_cfg4", gcb.DenseConfig(16), 350_000_000),
         ("dense32_cfg4", gcb.DenseConfig(32), 350_000_000),
@@ -43,13 +44,21 @@ def main():
         if only and not any(name.startswith(o) for o in only):
             continue
         torch.cuda.empty_cache()
-        g = torch.randn(n, d, device="cuda")
-        pipe = gcb.make_pipeline(cfg, n, d, gcb.SeedSpec(2024), validate=False, compute_nmse=False)
-        eng = pipe._engine
+        if d == "gpt2m":
+            from paper_2407_01378_b200.multitensor import TensorListPipeline, gpt2_medium_sizes
+            sizes = gpt2_medium_sizes()
+            d = sum(sizes)
+            g = torch.randn(n, d, device="cuda")
+            pipe = TensorListPipeline(cfg, n, sizes, gcb.SeedSpec(2024), validate=False, compute_nmse=False)
+            eng = pipe
+        else:
+            g = torch.randn(n, d, device="cuda")
+            pipe = gcb.make_pipeline(cfg, n, d, gcb.SeedSpec(2024), validate=False, compute_nmse=False)
+            eng = pipe._engine
         for r in range(2):
             pipe.run_round(g, r)
         torch.cuda.synchronize()
-        eng.kernel_events = []
+        eng.kernel_events = [] if hasattr(eng, "kernel_events") else None
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
         s.record()
         for r in range(a.steps):
@@ -57,7 +66,8 @@ def main():
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / a.steps
-        kms = sum(x.elapsed_time(y) for x, y in eng.kernel_events) / max(1, len(eng.kernel_events))
+        kev = getattr(eng, "kernel_events", None) or []
+        kms = sum(x.elapsed_time(y) for x, y in kev) / max(1, len(kev))
         b = alg_bytes(name, n, d, cfg)
         print(json.dumps({"case": name, "n": n, "d": d, "ms": round(ms, 4), "gelem_s": round(d / ms / 1e6, 3),
                           "core_ms": round(kms, 4), "alg_GB": round(b / 1e9, 3),
