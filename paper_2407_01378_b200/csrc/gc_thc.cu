@@ -370,22 +370,35 @@ __global__ void range_consensus_kernel(int L, int64_t nb, const float *in, float
   }
 }
 
+constexpr int kSignWordsPerThread = 8;   // one PCG jump amortised over 8 words (128 steps)
+
 __global__ void signs_kernel(gc_pcg64 stream, int64_t count, uint32_t *bits) {
-  // Sign i = top bit of u32 word i; u32 words are the low then high half of each
-  // next64 output (numpy buffered bounded uint32, Lemire with range 2).
+  // Sign i = top bit of u32 word i; u32 words are the low then high half of each next64 output
+  // (numpy buffered bounded uint32, Lemire with range 2).  Thread t writes words
+  // [t*8, t*8 + 8): 128 consecutive outputs after one jump.
   const int64_t words = (count + 31) / 32;
-  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < words;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t groups = (words + kSignWordsPerThread - 1) / kSignWordsPerThread;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < groups;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     gc::Pcg g;
     g.load(stream);
-    g.jump(static_cast<uint64_t>(k) * 16);
-    uint32_t word = 0;
-    for (int j = 0; j < 16; ++j) {
-      const uint64_t u = g.next();
-      word |= static_cast<uint32_t>((u >> 31) & 1u) << (2 * j);
-      word |= static_cast<uint32_t>((u >> 63) & 1u) << (2 * j + 1);
+    g.jump(static_cast<uint64_t>(t) * kSignWordsPerThread * 16);
+    uint32_t out[kSignWordsPerThread];
+#pragma unroll
+    for (int k = 0; k < kSignWordsPerThread; ++k) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint64_t u = g.next();
+        word |= static_cast<uint32_t>((u >> 31) & 1u) << (2 * j);
+        word |= static_cast<uint32_t>((u >> 63) & 1u) << (2 * j + 1);
+      }
+      out[k] = word;
     }
-    bits[k] = word;
+    const int64_t w0 = t * kSignWordsPerThread;
+#pragma unroll
+    for (int k = 0; k < kSignWordsPerThread; ++k)
+      if (w0 + k < words) bits[w0 + k] = out[k];
   }
 }
 
@@ -441,8 +454,8 @@ int gc_thc_signs(const gc_pcg64 *rotation_stream, int64_t count, uint32_t *bits,
   GC_REQUIRE(rotation_stream && bits, "null argument");
   GC_REQUIRE(count >= 0, "count must be non-negative");
   if (count == 0) return GC_OK;
-  const int64_t words = (count + 31) / 32;
-  signs_kernel<<<grid_for(words, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(*rotation_stream, count, bits);
+  const int64_t groups = ((count + 31) / 32 + kSignWordsPerThread - 1) / kSignWordsPerThread;
+  signs_kernel<<<grid_for(groups, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(*rotation_stream, count, bits);
   GC_LAUNCH_CHECK("signs_kernel");
   return GC_OK;
 }
