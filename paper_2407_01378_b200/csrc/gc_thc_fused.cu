@@ -333,6 +333,14 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
       v[4 * m + 3] = apply_sign(static_cast<double>(c.w), (my_sign_word >> (4 * m + 3)) & 1u);
     }
     wht_tile<K>(v, scratch, lane);
+    // lane's sign "column": bit j = sign of element 32j + lane (layout B), from 32 ballots over
+    // the row words the lanes already hold -- the own-decode epilogue then reads no shared memory
+    uint32_t sign_col = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      const uint32_t m = __ballot_sync(0xffffffffu, (my_sign_word >> b) & 1u);
+      sign_col = lane == b ? m : sign_col;
+    }
 
     // ---- x_rot = f32(v * B^-1/2), staged in layout B; per-block (min, max) (compressors.py:447-453)
     {
@@ -569,7 +577,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
       for (int j = 0; j < 32; ++j) {
         const int e = j * 32 + lane;
         const int64_t i = t0 + e;
-        const float own = static_cast<float>(apply_sign(v[j] * a.scale, (sgn[j] >> lane) & 1u));
+        const float own = static_cast<float>(apply_sign(v[j] * a.scale, (sign_col >> j) & 1u));
         if (i < a.dim) __stcs(rw + i, cbuf[cidx(e)] - own);
       }
     }
