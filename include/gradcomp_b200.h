@@ -187,6 +187,10 @@ int gc_ef_apply(int32_t workers, int64_t d, const float *grads, const float *res
  * pairwise fp64 order: norms [L][ceil(d/chunk)]. */
 int gc_chunk_norms(int32_t workers, int64_t d, int64_t chunk, const float *vals, int64_t ld, const int64_t *perm,
                    float *norms, void *stream);
+/* Same norms with ef_apply fused (no permutation, chunk % 8 == 0, chunk <= 128): corrected =
+ * f32(g + r) is written over resid (resid NULL: EF off, norms of g). */
+int gc_chunk_norms_ef(int32_t workers, int64_t d, int64_t chunk, const float *grads, float *resid, int64_t ld,
+                      float *norms, void *stream);
 /* chunk_values (compressors.py:417-430): packs[w][j*chunk + t] = fp16(work_w[sel[j]*chunk + t]). */
 int gc_chunk_pack(int32_t workers, int64_t d, int64_t chunk, int64_t selected, const int32_t *sel,
                   const float *vals, int64_t ld, const int64_t *perm, float *packs, void *stream);

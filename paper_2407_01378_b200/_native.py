@@ -91,6 +91,7 @@ SIGNATURES = {
     # TopK-Chunked
     "gc_ef_apply": (c_int, [I32, I64, P, P, I64, P, I64, P]),
     "gc_chunk_norms": (c_int, [I32, I64, I64, P, I64, P, P, P]),
+    "gc_chunk_norms_ef": (c_int, [I32, I64, I64, P, P, I64, P, P]),
     "gc_chunk_pack": (c_int, [I32, I64, I64, I64, P, P, I64, P, P, P]),
     "gc_chunk_scatter": (c_int, [I64, I64, I64, P, P, I32, P, P, P]),
     "gc_chunk_ef_update": (c_int, [I32, I64, I64, I64, P, P, P, P, I64, P]),

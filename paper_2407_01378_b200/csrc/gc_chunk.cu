@@ -70,10 +70,15 @@ __global__ void __launch_bounds__(kNT) norms_generic_kernel(int64_t d, int64_t C
 }
 
 // C % 8 == 0 and C <= 128: lane group of 8 per chunk, lane j owns accumulator r[j].
+// With grads != NULL (no permutation) ef_apply is fused: corrected = f32(g + r) is formed here and
+// written over r (vals == r then, or the corrected copy when r is NULL).
 __global__ void __launch_bounds__(kNT) norms_lanes_kernel(int64_t d, int C, int64_t nc, const float *vals,
-                                                          int64_t ld, const int64_t *perm, float *out) {
+                                                          int64_t ld, const int64_t *perm, float *out,
+                                                          const float *grads, float *resid) {
   const int w = blockIdx.y;
   const float *row = vals + w * ld;
+  const float *grow = grads ? grads + w * ld : nullptr;
+  float *rrow = resid ? resid + w * ld : nullptr;
   const int j = threadIdx.x & 7;
   const int group = (threadIdx.x & 31) >> 3;   // 4 chunks per warp
   const int64_t stride = static_cast<int64_t>(gridDim.x) * (kNT / 8);
@@ -83,8 +88,29 @@ __global__ void __launch_bounds__(kNT) norms_lanes_kernel(int64_t d, int C, int6
     double r = 0.0;
     if (live) {
       const int64_t i0 = c * C;
-      r = sq_at(row, perm, i0 + j, d);
-      for (int i = 8; i < C; i += 8) r += sq_at(row, perm, i0 + i + j, d);
+      if (grow) {   // fused ef_apply (compressors.py:624-626): all loads issued before any store
+        float gv[16], rv[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const int64_t x = i0 + t * 8 + j;
+          const bool ok = t * 8 < C && x < d;
+          gv[t] = ok ? __ldcs(grow + x) : 0.0f;
+          rv[t] = (ok && rrow) ? __ldcs(rrow + x) : 0.0f;
+        }
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          if (t * 8 < C) {
+            const int64_t x = i0 + t * 8 + j;
+            const float cv = rrow ? gv[t] + rv[t] : gv[t];
+            if (rrow && x < d) rrow[x] = cv;
+            const double v = static_cast<double>(cv);
+            r = (t == 0) ? v * v : r + v * v;
+          }
+        }
+      } else {
+        r = sq_at(row, perm, i0 + j, d);
+        for (int i = 8; i < C; i += 8) r += sq_at(row, perm, i0 + i + j, d);
+      }
     }
     r += __shfl_xor_sync(0xffffffffu, r, 1);   // (r0+r1), (r2+r3), ...
     r += __shfl_xor_sync(0xffffffffu, r, 2);   // ((r0+r1)+(r2+r3)), ...
@@ -140,8 +166,30 @@ __global__ void __launch_bounds__(kNT) chunk_ef_kernel(int64_t d, int64_t C, int
 }
 
 __global__ void __launch_bounds__(kNT) ef_apply_kernel(int64_t d, const float *g, const float *r, int64_t ld,
-                                                       float *out, int64_t ldo) {
+                                                       float *out, int64_t ldo, bool vec) {
   const int w = blockIdx.y;
+  if (vec) {   // float4 path (ld, ldo multiples of 4 and 16-byte aligned rows)
+    const int64_t d4 = d / 4;
+    const float4 *g4 = reinterpret_cast<const float4 *>(g + w * ld);
+    const float4 *r4 = r ? reinterpret_cast<const float4 *>(r + w * ld) : nullptr;
+    float4 *o4 = reinterpret_cast<float4 *>(out + w * ldo);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; i < d4;
+         i += static_cast<int64_t>(gridDim.x) * kNT) {
+      float4 c = __ldcs(g4 + i);
+      if (r4) {
+        const float4 rv = __ldcs(r4 + i);
+        c.x = c.x + rv.x; c.y = c.y + rv.y; c.z = c.z + rv.z; c.w = c.w + rv.w;
+      }
+      __stcs(o4 + i, c);
+    }
+    for (int64_t i = d4 * 4 + blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; i < d;
+         i += static_cast<int64_t>(gridDim.x) * kNT) {
+      float c = g[w * ld + i];
+      if (r) c = c + r[w * ld + i];
+      out[w * ldo + i] = c;
+    }
+    return;
+  }
   for (int64_t i = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; i < d;
        i += static_cast<int64_t>(gridDim.x) * kNT) {
     float c = g[w * ld + i];
@@ -158,8 +206,11 @@ int gc_ef_apply(int32_t workers, int64_t d, const float *grads, const float *res
                 int64_t ld_out, void *stream) {
   GC_REQUIRE(workers >= 1 && workers <= 65535 && d >= 1 && grads && out && ld >= d && ld_out >= d,
              "invalid argument");
-  ef_apply_kernel<<<dim3(grid_for(d), workers), kNT, 0, static_cast<cudaStream_t>(stream)>>>(d, grads, resid, ld,
-                                                                                           out, ld_out);
+  const bool vec = ld % 4 == 0 && ld_out % 4 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(grads) | reinterpret_cast<uintptr_t>(resid) |
+                     reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  ef_apply_kernel<<<dim3(grid_for(vec ? d / 4 + 1 : d), workers), kNT, 0, static_cast<cudaStream_t>(stream)>>>(
+      d, grads, resid, ld, out, ld_out, vec);
   GC_LAUNCH_CHECK("ef_apply_kernel");
   return GC_OK;
 }
@@ -172,11 +223,23 @@ int gc_chunk_norms(int32_t workers, int64_t d, int64_t chunk, const float *vals,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (chunk % 8 == 0 && chunk <= 128) {
     norms_lanes_kernel<<<dim3(grid_for(nc * 8), workers), kNT, 0, st>>>(d, static_cast<int>(chunk), nc, vals, ld,
-                                                                       perm, norms);
+                                                                       perm, norms, nullptr, nullptr);
   } else {
     norms_generic_kernel<<<dim3(grid_for(nc), workers), kNT, 0, st>>>(d, chunk, nc, vals, ld, perm, norms);
   }
   GC_LAUNCH_CHECK("chunk norms");
+  return GC_OK;
+}
+
+int gc_chunk_norms_ef(int32_t workers, int64_t d, int64_t chunk, const float *grads, float *resid, int64_t ld,
+                      float *norms, void *stream) {
+  GC_REQUIRE(workers >= 1 && workers <= 65535 && d >= 1 && chunk >= 1 && grads && norms && ld >= d,
+             "invalid argument");
+  GC_REQUIRE(chunk % 8 == 0 && chunk <= 128, "fused ef_apply + norms needs chunk % 8 == 0 and chunk <= 128");
+  const int64_t nc = (d + chunk - 1) / chunk;
+  norms_lanes_kernel<<<dim3(grid_for(nc * 8), workers), kNT, 0, static_cast<cudaStream_t>(stream)>>>(
+      d, static_cast<int>(chunk), nc, resid ? resid : grads, ld, nullptr, norms, grads, resid);
+  GC_LAUNCH_CHECK("norms_lanes_kernel");
   return GC_OK;
 }
 

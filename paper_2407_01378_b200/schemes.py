@@ -307,19 +307,22 @@ class ChunkedEngine(Engine):
         n, d, C, J, nc = self.n, self.dim, self.C, self.J, self.nc
         sp = _sp()
         dev = self.device
-        if res is not None:   # corrected = g + r, kept in r until the EF update
-            _native.call("gc_ef_apply", n, d, grads.data_ptr(), res.data_ptr(), grads.stride(0), res.data_ptr(),
-                         res.stride(0), sp)
-            work = res
-        else:
-            work = grads
         perm = self._perm(round_index) if self.cfg.permute else None
         pp = _ptr(perm)
+        fuse = perm is None and C % 8 == 0 and C <= 128 and (res is None or res.stride(0) == grads.stride(0))
+        if res is not None and not fuse:   # corrected = g + r, kept in r until the EF update
+            _native.call("gc_ef_apply", n, d, grads.data_ptr(), res.data_ptr(), grads.stride(0), res.data_ptr(),
+                         res.stride(0), sp)
+        work = res if res is not None else grads
         norms = torch.empty(n, nc, dtype=torch.float32, device=dev)
         ev = self._ev()
         if ev:
             ev[0].record()
-        _native.call("gc_chunk_norms", n, d, C, work.data_ptr(), work.stride(0), pp, norms.data_ptr(), sp)
+        if fuse:   # ef_apply fused into the chunk energies
+            _native.call("gc_chunk_norms_ef", n, d, C, grads.data_ptr(), _ptr(res), grads.stride(0), norms.data_ptr(),
+                         sp)
+        else:
+            _native.call("gc_chunk_norms", n, d, C, work.data_ptr(), work.stride(0), pp, norms.data_ptr(), sp)
         energy = torch.empty(nc, dtype=torch.float32, device=dev)
         _native.call("gc_float_fold", n, nc, norms.data_ptr(), nc, 0, -(-nc // n), 1, 0, 0, energy.data_ptr(), sp)
         sel = torch.empty(J, dtype=torch.int32, device=dev)
