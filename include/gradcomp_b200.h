@@ -266,6 +266,15 @@ int gc_fill_zero(void *ptr, int64_t bytes, void *stream);
 int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *grads, float *resid, int64_t ld,
                        const uint32_t *sign_bits, const gc_pcg64 *coin_streams, float *estimate,
                        int8_t *codes, int64_t *counters, double *nmse_acc, void *stream);
+/* The same round restricted to tiles [tile_begin, tile_end) of 1024 coordinates (tile_end < 0:
+ * to the end), with the residual read from resid_in and written to resid_out (equal pointers:
+ * in place).  Tiles are independent, so a host-fed round can stream: copy a segment of every
+ * worker's gradient, run its tiles, copy its estimate back -- and keep the previous residual
+ * intact until the whole round validated (pipelines.py:184-197 raises before any state change). */
+int gc_thc_round_fused_range(const gc_thc_geom *g, int32_t n, const float *grads, const float *resid_in,
+                             float *resid_out, int64_t ld, int64_t tile_begin, int64_t tile_end,
+                             const uint32_t *sign_bits, const gc_pcg64 *coin_streams, float *estimate,
+                             int8_t *codes, int64_t *counters, double *nmse_acc, void *stream);
 
 #ifdef __cplusplus
 }

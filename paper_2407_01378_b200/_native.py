@@ -77,6 +77,8 @@ SIGNATURES = {
     "gc_thc_decode_estimate": (c_int, [POINTER(ThcGeom), I32, P, I32, P, P, P, P, P]),
     "gc_thc_decode_ef": (c_int, [POINTER(ThcGeom), I32, P, P, P, P, P, I64, P, P]),
     "gc_thc_round_fused": (c_int, [POINTER(ThcGeom), I32, P, P, I64, P, POINTER(Pcg64), P, P, P, P, P]),
+    "gc_thc_round_fused_range": (c_int, [POINTER(ThcGeom), I32, P, P, P, I64, I64, I64, P, POINTER(Pcg64), P, P, P,
+                                          P, P]),
     # float folds
     "gc_float_fold": (c_int, [I32, I64, P, I64, I64, I64, I32, I32, I32, P, P]),
     "gc_float_fold_batched": (c_int, [I32, I32, I64, P, I64, I64, I32, I32, I32, P, I64, P]),

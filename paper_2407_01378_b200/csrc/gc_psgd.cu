@@ -20,6 +20,9 @@
 // the reference's canonical-basis completion of degenerate columns.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "gc_device.cuh"
 #include "gc_internal.h"
 
@@ -544,13 +547,21 @@ int gc_psgd_mq_fused(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t co
   GC_REQUIRE(cols % 4 == 0 && b->rows_aligned, "mq_fused needs cols % 4 == 0 and 16-byte aligned rows");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int L = b->tensors * b->workers;
-  const int slabs = static_cast<int>((cols + 1023) / 1024);
+  int slabs = static_cast<int>((cols + 1023) / 1024);
   double *partial = static_cast<double *>(workspace);
-  GC_RANK_SWITCH(rank, ({
-    mq_fused_kernel<R><<<dim3(slabs, grid_cap((rows + kMqRows - 1) / kMqRows), L), 256, 0, st>>>(
-        d, rows, cols, grads, resid, rows_of(b), q, partial, slabs);
-  }));
-  GC_LAUNCH_CHECK("mq_fused_kernel");
+  const char *impl = getenv("GC_PSGD_MQ");
+  if (impl && std::string(impl) == "cores") {
+    GC_RANK_SWITCH(rank, ({
+      mq_fused_kernel<R><<<dim3(slabs, grid_cap((rows + kMqRows - 1) / kMqRows), L), 256, 0, st>>>(
+          d, rows, cols, grads, resid, rows_of(b), q, partial, slabs);
+    }));
+    GC_LAUNCH_CHECK("mq_fused_kernel");
+  } else {
+    // tcgen05 (kind::tf32, 3xTF32) band GEMM fused with ef_apply (gc_psgd_umma.cu)
+    slabs = gc_psgd_mq_umma_launch(L, b->workers, b->row_offsets, b->ld, d, rows, cols, rank, grads, resid, q,
+                                   partial, st);
+    if (slabs < 0) return slabs;
+  }
   const int64_t total = static_cast<int64_t>(L) * rows * rank;
   mq_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(
       L, slabs, rows, rank, partial, p);

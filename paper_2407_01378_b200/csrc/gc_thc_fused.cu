@@ -42,11 +42,12 @@ constexpr int kMaxN = 16;
 constexpr int kLutMax = 256;   // doubles in the shared own-decode table
 
 struct FusedArgs {
-  int64_t dim, padded, active, tiles, ring_blk;
+  int64_t dim, padded, active, tile_begin, tiles, ring_blk;   // tiles = end of the tile range
   int n, k, q, bits;
   double scale;
   const float *g;
-  float *r;
+  const float *r;   // residual read (ef_apply)
+  float *rout;      // residual written (ef_update); == r for the in-place update
   int64_t ld;
   bool aligned;
   const uint32_t *signs;
@@ -162,6 +163,15 @@ struct Lcg {
     s2 = r2;
     s3 = r3;
   }
+  // the 64-bit XSL-RR output rotr64(hi ^ lo, hi >> 58) as two 32-bit halves
+  __device__ __forceinline__ void out(uint32_t &hi, uint32_t &lo) const {
+    const uint32_t xl = s0 ^ s2, xh = s1 ^ s3;
+    const uint32_t rot = s3 >> 26;
+    const bool swap = rot & 32u;
+    const uint32_t a = swap ? xh : xl, b = swap ? xl : xh;
+    lo = __funnelshift_r(a, b, rot);   // shift amount taken mod 32
+    hi = __funnelshift_r(b, a, rot);
+  }
   // coin = (next64 >> 11) * 2^-53 from the XSL-RR output rotr64(hi ^ lo, hi >> 58)
   __device__ __forceinline__ double coin() const {
     const uint32_t xl = s0 ^ s2, xh = s1 ^ s3;
@@ -219,6 +229,49 @@ __device__ __forceinline__ int quantize_one(double x, double mid, double step, d
   return static_cast<int>(low) + (up ? 1 : 0);
 }
 
+// coin_from: numpy's random() double (next64 >> 11) * 2^-53 from the two output halves.
+__device__ __forceinline__ double coin_from(uint32_t hi, uint32_t lo) {
+  const uint64_t u = (static_cast<uint64_t>(hi) << 32) | lo;
+  return static_cast<double>(u >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// The reference quantizer for one value, IEEE fp64 step by step (compressors.py:481-498):
+// the rare coordinates the fp32 screen below cannot decide come here.
+__device__ __noinline__ int quantize_ref(double x, double lo, double hi, double mid, double step, double bound,
+                                         double coin) {
+  x = fmin(fmax(x, lo), hi);
+  double t = (x - mid) / step;
+  t = fmin(fmax(t, -bound), bound);
+  double low = floor(t);
+  double frac = t - low;
+  if (frac > 1.0 - 1e-9) {
+    low += 1.0;
+    frac = 0.0;
+  } else if (frac < 1e-9) {
+    frac = 0.0;
+  }
+  const int z = static_cast<int>(low) + (coin < frac ? 1 : 0);
+  const int b = static_cast<int>(bound);
+  return z < -b ? -b : (z > b ? b : z);
+}
+
+// Per-block fp32 screen parameters {mid32, 1/step as f32, H, 1 - H}.  With t32 = (x - mid32) *
+// inv32 in fp32, |t32 - t| <= E = m + (bound + m) * 3.01 * 2^-24 (m = |mid| / step * 2^-24:
+// the rounding of mid to f32; the other terms: the f32 subtract, inv32 and the multiply).
+// H = E + 2^-22 also covers the 23-bit coin prefix (2^-23) and the f32 rounding of
+// frac = t32 - floor(t32) (2^-25).  A coordinate whose f32 frac lies in [H, 1 - H] and more
+// than H from the coin prefix has the reference's floor(t), no snapping and the same coin
+// comparison, so its code is decided in fp32; the rest (probability ~6H) take quantize_ref.
+// Degenerate blocks (step <= 0) always pass the screen (their code is forced to 0).
+__device__ __forceinline__ float4 screen_params(double mid, double step, double bound) {
+  if (!(step > 0.0)) return make_float4(0.0f, 0.0f, -1.0f, 2.0f);
+  const double m = fabs(mid) / step * 0x1p-24;
+  const double h = (m + (bound + m) * 3.01 * 0x1p-24 + 0x1p-40 + 0x1p-22) * 1.001;
+  if (!(h < 0x1p-8)) return make_float4(0.0f, 0.0f, 2.0f, -1.0f);   // never passes: exact path
+  return make_float4(static_cast<float>(mid), static_cast<float>(1.0 / step), static_cast<float>(h),
+                     static_cast<float>(1.0 - h));
+}
+
 template <int K, bool USE_LUT>
 __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -268,21 +321,22 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
   {
     gc::Pcg p;
     p.load(a.streams[w]);
-    p.jump(static_cast<uint64_t>(blockIdx.x) * kTileN + lane + 1);
+    p.jump(static_cast<uint64_t>(a.tile_begin + blockIdx.x) * kTileN + lane + 1);
     tile_state.set(static_cast<uint64_t>(p.state >> 64), static_cast<uint64_t>(p.state));
   }
 
   const float *gw = a.g + w * a.ld;
-  float *rw = a.r ? a.r + w * a.ld : nullptr;
+  const float *rw = a.r ? a.r + w * a.ld : nullptr;
+  float *ro = a.r ? a.rout + w * a.ld : nullptr;
   long long sz = 0, sz2 = 0, clips = 0;
   double nmse_num = 0.0, nmse_den = 0.0;
 
-  for (int64_t tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+  for (int64_t tile = a.tile_begin + blockIdx.x; tile < a.tiles; tile += gridDim.x) {
     const int64_t t0 = tile * kTileN;
-    uint32_t *sgn = sgn_all + ((tile / gridDim.x) & 1) * 32;
+    uint32_t *sgn = sgn_all + (((tile - a.tile_begin) / gridDim.x) & 1) * 32;
     {   // pull the next tile of this worker's g and r rows into L2 while this tile computes
       const int64_t tn = t0 + static_cast<int64_t>(gridDim.x) * kTileN;
-      if (lane < 2 && tn + kTileN <= a.dim && a.aligned) {
+      if (lane < 2 && tn + kTileN <= min(a.dim, a.tiles * kTileN) && a.aligned) {
         const float *src = lane == 0 ? gw + tn : (rw ? rw + tn : nullptr);
         if (src)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(kTileN * 4) : "memory");
@@ -383,6 +437,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
       bp[8 * lane + 3] = step;
       bp[8 * lane + 4] = step > 0.0 ? 1.0 / step : 0.0;   // degenerate: any finite value works
       bp[8 * lane + 5] = dhi > dlo ? step : 0.0;     // dequantize_sum's step (compressors.py:520)
+      *reinterpret_cast<float4 *>(bp + 8 * lane + 6) = screen_params((dlo + dhi) / 2.0, step, static_cast<double>(ibound));
     }
     __syncwarp();
     // dq(z, 1) table for the own decode (compressors.py:519-521), built cooperatively.
@@ -405,14 +460,42 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
       }
       for (int j = 0; j < 32; j += 4) {
         int z[4];
+        uint32_t hw[4], lw[4];
+        float xv[4];
+        bool safe = true;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int blk = (j + c) >> rpb_log;
-          const double *pb = bp + 8 * blk;
-          const double coin = ch[c].coin();
+          const float4 sp = *reinterpret_cast<const float4 *>(bp + 8 * blk + 6);
+          ch[c].out(hw[c], lw[c]);
           ch[c].step(m128, c128);
-          const int zq = quantize_one(static_cast<double>(xs[(j + c) * 32 + lane]), pb[2], pb[3], pb[4], coin);
-          z[c] = pb[3] > 0.0 ? zq : 0;   // degenerate block: code 0 (compressors.py:497)
+          xv[c] = xs[(j + c) * 32 + lane];
+          // fp32 screen: floor by the 1.5 * 2^23 magic constant (|t32| < 2^22), frac, 23-bit coin
+          const float tq = (xv[c] - sp.x) * sp.y;
+          const float sm = __fadd_rd(tq, 12582912.0f);
+          const float f = tq - (sm - 12582912.0f);
+          const float c23 = __uint_as_float(0x3f800000u | (hw[c] >> 9)) - 1.0f;
+          safe = safe && (f >= sp.z && f <= sp.w && fabsf(c23 - f) > sp.z);
+          z[c] = (__float_as_int(sm) - 0x4B400000) + (c23 < f ? 1 : 0);
+        }
+        if (__any_sync(0xffffffffu, !safe)) {   // warp-uniform: the exact path stays off the main line
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double *pb = bp + 8 * ((j + c) >> rpb_log);
+            const float4 sp = *reinterpret_cast<const float4 *>(pb + 6);
+            const float tq = (xv[c] - sp.x) * sp.y;
+            const float sm = __fadd_rd(tq, 12582912.0f);
+            const float f = tq - (sm - 12582912.0f);
+            const float c23 = __uint_as_float(0x3f800000u | (hw[c] >> 9)) - 1.0f;
+            if (!(f >= sp.z && f <= sp.w && fabsf(c23 - f) > sp.z))
+              z[c] = quantize_ref(static_cast<double>(xv[c]), pb[0], pb[1], pb[2], pb[3],
+                                  static_cast<double>(ibound), coin_from(hw[c], lw[c]));
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double *pb = bp + 8 * ((j + c) >> rpb_log);
+          z[c] = pb[3] > 0.0 ? z[c] : 0;   // degenerate block: code 0 (compressors.py:497)
           cod[(j + c) * 32 + lane] = static_cast<int8_t>(z[c]);
           sz += z[c];
           sz2 += z[c] * z[c];
@@ -543,7 +626,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
           const float f = static_cast<float>(apply_sign(e[t] * a.scale, (sgn[row] >> col) & 1u)) / nf;
           if (i < a.dim) {
             __stcs(a.est + i, f);
-            if (n == 1 && rw) __stcs(rw + i, cbuf[cidx(el)] - f);   // one worker: own == estimate
+            if (n == 1 && rw) __stcs(ro + i, cbuf[cidx(el)] - f);   // one worker: own == estimate
             if (a.nmse) {
               double ref = 0.0;
               for (int u = 0; u < n; ++u) ref += static_cast<double>(cbuf_all[u * (32 * kCRow) + cidx(el)]);
@@ -578,7 +661,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
         const int e = j * 32 + lane;
         const int64_t i = t0 + e;
         const float own = static_cast<float>(apply_sign(v[j] * a.scale, (sign_col >> j) & 1u));
-        if (i < a.dim) __stcs(rw + i, cbuf[cidx(e)] - own);
+        if (i < a.dim) __stcs(ro + i, cbuf[cidx(e)] - own);
       }
     }
     // (C) end of tile: only the nmse reduction needs it (it reads every warp's cbuf); all other
@@ -629,9 +712,12 @@ void host_jump(uint64_t delta, uint64_t out[4]) {
 
 }  // namespace
 
-extern "C" int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *grads, float *resid, int64_t ld,
-                                  const uint32_t *sign_bits, const gc_pcg64 *coin_streams, float *estimate,
-                                  int8_t *codes, int64_t *counters, double *nmse_acc, void *stream) {
+namespace {
+
+int launch_fused(const gc_thc_geom *g, int32_t n, const float *grads, const float *resid_in, float *resid_out,
+                 int64_t ld, int64_t tile_begin, int64_t tile_end, const uint32_t *sign_bits,
+                 const gc_pcg64 *coin_streams, float *estimate, int8_t *codes, int64_t *counters, double *nmse_acc,
+                 void *stream) {
   GC_REQUIRE(g != nullptr, "geometry is null");
   GC_REQUIRE(n >= 1 && n <= kMaxN, "fused THC round supports 1..16 workers");
   GC_REQUIRE(g->dim >= 1 && g->padded >= kTileN && (g->padded & (g->padded - 1)) == 0 && g->padded >= g->dim,
@@ -641,12 +727,18 @@ extern "C" int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *
   GC_REQUIRE(g->quant_bits >= 2 && g->quant_bits <= 8 && g->wire_bits >= g->quant_bits && g->wire_bits <= 32,
              "invalid quant/wire bits");
   GC_REQUIRE(grads && sign_bits && coin_streams && estimate && ld >= g->dim, "invalid argument");
+  GC_REQUIRE((resid_in == nullptr) == (resid_out == nullptr), "residual in/out must both be set or both NULL");
 
   FusedArgs a{};
   a.dim = g->dim;
   a.padded = g->padded;
   a.active = ((g->dim + g->block - 1) / g->block) * g->block;
-  a.tiles = (a.active + kTileN - 1) / kTileN;
+  const int64_t all_tiles = (a.active + kTileN - 1) / kTileN;
+  if (tile_end < 0 || tile_end > all_tiles) tile_end = all_tiles;
+  GC_REQUIRE(tile_begin >= 0 && tile_begin <= tile_end, "invalid tile range");
+  if (tile_begin == tile_end) return GC_OK;
+  a.tile_begin = tile_begin;
+  a.tiles = tile_end;
   a.ring_blk = (g->padded + n - 1) / n;
   a.n = n;
   int k = 0;
@@ -656,9 +748,11 @@ extern "C" int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *
   a.bits = g->wire_bits;
   a.scale = g->scale;
   a.g = grads;
-  a.r = resid;
+  a.r = resid_in;
+  a.rout = resid_out;
   a.ld = ld;
-  a.aligned = ((reinterpret_cast<uintptr_t>(grads) | reinterpret_cast<uintptr_t>(resid)) & 15) == 0 && (ld % 4) == 0;
+  a.aligned = ((reinterpret_cast<uintptr_t>(grads) | reinterpret_cast<uintptr_t>(resid_in) |
+                reinterpret_cast<uintptr_t>(resid_out)) & 15) == 0 && (ld % 4) == 0;
   a.signs = sign_bits;
   a.est = estimate;
   a.codes = codes;
@@ -692,9 +786,26 @@ extern "C" int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *
     return GC_ERR_UNSUPPORTED;
   }
   int64_t grid = static_cast<int64_t>(sms) * per_sm;
-  if (grid > a.tiles) grid = a.tiles;
+  if (grid > tile_end - tile_begin) grid = tile_end - tile_begin;
   host_jump(static_cast<uint64_t>(grid) * kTileN, a.tile_jump);
   fn<<<static_cast<unsigned>(grid), n * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
   GC_LAUNCH_CHECK("thc_fused_kernel");
   return GC_OK;
+}
+
+}  // namespace
+
+extern "C" int gc_thc_round_fused(const gc_thc_geom *g, int32_t n, const float *grads, float *resid, int64_t ld,
+                                  const uint32_t *sign_bits, const gc_pcg64 *coin_streams, float *estimate,
+                                  int8_t *codes, int64_t *counters, double *nmse_acc, void *stream) {
+  return launch_fused(g, n, grads, resid, resid, ld, 0, -1, sign_bits, coin_streams, estimate, codes, counters,
+                      nmse_acc, stream);
+}
+
+extern "C" int gc_thc_round_fused_range(const gc_thc_geom *g, int32_t n, const float *grads, const float *resid_in,
+                                        float *resid_out, int64_t ld, int64_t tile_begin, int64_t tile_end,
+                                        const uint32_t *sign_bits, const gc_pcg64 *coin_streams, float *estimate,
+                                        int8_t *codes, int64_t *counters, double *nmse_acc, void *stream) {
+  return launch_fused(g, n, grads, resid_in, resid_out, ld, tile_begin, tile_end, sign_bits, coin_streams, estimate,
+                      codes, counters, nmse_acc, stream);
 }

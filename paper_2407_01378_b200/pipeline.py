@@ -46,12 +46,20 @@ class RoundResult:
         self._dim = dim
         self._stats = stats
         self._estimate = None
+        self._est_host = None
 
     @property
     def estimate(self) -> GradientVector:
         if self._estimate is None:
-            self._estimate = GradientVector(tensor=self._est, logical_len=self._dim, padded_len=next_pow2(self._dim))
+            src = self._est_host if self._est_host is not None else self._est
+            self._estimate = GradientVector(tensor=src, logical_len=self._dim, padded_len=next_pow2(self._dim))
         return self._estimate
+
+    @property
+    def estimate_host(self) -> torch.Tensor | None:
+        """Pinned host copy of the estimate, already complete, when the round was fed from host
+        memory (the streamed path copies it back segment by segment); None otherwise."""
+        return self._est_host
 
     @property
     def estimate_tensor(self) -> torch.Tensor:
@@ -144,11 +152,61 @@ class GradientPipeline:
 
     # -- round entry (pipelines.py:147-182) ---------------------------------------------
     def run_round(self, worker_grads, round_index: int) -> RoundResult:
+        host_rows = self._host_rows(worker_grads)
+        if host_rows is not None:
+            return self._run_streamed(host_rows, round_index)
         grads = self._checked(worker_grads)
         ledger = TrafficLedger()
         est, input_bits, stats = self._engine.run(grads, self._res, round_index, ledger,
                                                   nmse=self.compute_nmse)
         return RoundResult(self.scheme, round_index, est, self.dim, ledger, input_bits, stats)
+
+    # -- host-fed THC round: PCIe in, kernel and PCIe out overlapped -----------------------
+    def _host_rows(self, worker_grads):
+        """The n gradients as 1-d CPU float32 tensors when every one is host memory and the scheme
+        streams (fused THC); None otherwise (the generic copy-then-run path)."""
+        eng = self._engine
+        if not (isinstance(eng, schemes.ThcEngine) and eng.fused) or eng.capture or torch.is_tensor(worker_grads):
+            return None
+        if len(worker_grads) != self.group.size:
+            raise ValueError("need exactly one gradient per worker")
+        rows = []
+        for x in worker_grads:
+            if isinstance(x, GradientVector):
+                x = x.tensor if x.tensor is not None else x.logical
+            if torch.is_tensor(x):
+                if x.is_cuda:
+                    return None
+                t = x
+            else:
+                t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+            if t.dim() != 1 or t.numel() != self.dim:
+                raise ValueError("gradient length does not match the pipeline dim")
+            rows.append(t.to(torch.float32).contiguous())
+        return rows
+
+    def _run_streamed(self, host_rows, round_index: int) -> RoundResult:
+        """run_round for host inputs: ThcEngine.run_streamed writes the new residual to a second
+        buffer, so a non-finite input (found by the per-segment checks) raises ValueError with the
+        EF state untouched, as pipelines.py:184-197 does before any state change."""
+        stage = self._stage_buffer()
+        res_in = self._res
+        res_out = None
+        if res_in is not None:
+            if getattr(self, "_res_alt", None) is None or self._res_alt.shape != res_in.shape:
+                self._res_alt = torch.empty_like(res_in)
+            res_out = self._res_alt
+        ledger = TrafficLedger()
+        est, est_host, input_bits, stats, bad = self._engine.run_streamed(
+            host_rows, stage, res_in, res_out, round_index, ledger, nmse=self.compute_nmse)
+        torch.cuda.current_stream().synchronize()   # a host caller reads the host estimate next
+        if self.validate and int(bad.item()):
+            raise ValueError("gradients must be finite")
+        if res_in is not None:
+            self._res, self._res_alt = res_out, res_in
+        result = RoundResult(self.scheme, round_index, est, self.dim, ledger, input_bits, stats)
+        result._est_host = est_host
+        return result
 
     def _checked(self, worker_grads) -> torch.Tensor:
         """pipelines.py:184-197: one finite 1-d gradient of length dim per worker -> [n, d] device."""

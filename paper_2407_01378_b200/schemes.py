@@ -189,6 +189,64 @@ class ThcEngine(Engine):
                 self.last = dict(b, signs=self.signs)
             self.launches += 5 + (n > 1) + bool(nmse) + (res is not None)
         # ledger + bits (pipelines.py:271-305, 321)
+        return self._round_meta(ledger, nmse)
+
+
+    def run_streamed(self, host_rows, stage, res_in, res_out, round_index, ledger: TrafficLedger, nmse=True,
+                     segments=16):
+        """Host-fed fused round (gc_thc_round_fused_range): segment s of every worker's gradient is
+        copied host -> device on one stream while segment s-1 is validated and runs its tiles on the
+        compute stream and segment s-2's estimate is copied device -> host on a third, so PCIe in,
+        the kernel and PCIe out overlap.  The residual is read from res_in and written to res_out;
+        the caller keeps res_in until the round validated (pipelines.py:184-197 raises first).
+        Returns (estimate_dev, estimate_host, input_bits, stats, nonfinite_count_dev)."""
+        n, d, T = self.n, self.dim, -(-self.active // self.TILE)
+        cur = torch.cuda.current_stream()
+        if getattr(self, "_h2d", None) is None:
+            self._h2d, self._d2h = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
+        h2d, d2h = self._h2d, self._d2h
+        sp = cur.cuda_stream
+        rot = self.seeds.pcg("rotation-signs", round_index)
+        _native.call("gc_thc_signs", ctypes.byref(rot), self.sign_count, self.signs.data_ptr(), sp)
+        coins = self.coin_streams(round_index)
+        self.est = torch.empty(d, dtype=torch.float32, device=self.device)
+        est_host = torch.empty(d, dtype=torch.float32, pin_memory=True)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self.nmse_acc = torch.zeros(2, dtype=torch.float64, device=self.device)
+        bad = torch.zeros(1, dtype=torch.int64, device=self.device)
+        h2d.wait_stream(cur)   # the stage buffer may still be read by the previous round
+        segments = max(1, min(segments, T))
+        ld = stage.stride(0)
+        ev = self._ev()
+        for s in range(segments):
+            tb, te = T * s // segments, T * (s + 1) // segments
+            a, b = tb * self.TILE, min(te * self.TILE, d)
+            if a >= b:
+                continue
+            with torch.cuda.stream(h2d):
+                for w in range(n):
+                    stage[w, a:b].copy_(host_rows[w][a:b], non_blocking=True)
+            cur.wait_stream(h2d)
+            if ev and s == 0:
+                ev[0].record()
+            _native.call("gc_check_finite", n, stage[:, a:].data_ptr(), ld, b - a, bad.data_ptr(), sp)
+            _native.call("gc_thc_round_fused_range", ctypes.byref(self.geom), n, stage.data_ptr(), _ptr(res_in),
+                         _ptr(res_out), ld, tb, te, self.signs.data_ptr(), coins, self.est.data_ptr(), None,
+                         self.counters.data_ptr(), self.nmse_acc.data_ptr() if nmse else None, sp)
+            if ev and s == segments - 1:
+                ev[1].record()
+            d2h.wait_stream(cur)
+            with torch.cuda.stream(d2h):
+                est_host[a:b].copy_(self.est[a:b], non_blocking=True)
+            self.launches += 2
+        cur.wait_stream(d2h)
+        self.est.record_stream(d2h)
+        stage.record_stream(h2d)
+        est, bits, stats = self._round_meta(ledger, nmse)
+        return est, est_host, bits, stats, bad
+
+    def _round_meta(self, ledger, nmse):
+        n, cfg = self.n, self.cfg
         num_blocks = self.P // self.B
         ledger.charge_ring("range-consensus", n, num_blocks, 32)
         ledger.charge_ring("range-consensus", n, num_blocks, 32)

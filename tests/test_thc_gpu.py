@@ -95,3 +95,46 @@ def test_thc_device_tensor_inputs_and_determinism():
     for x, y in zip(*outs):
         assert torch.equal(x, y)
     assert not torch.equal(outs[0][0], outs[0][1])
+
+
+@pytest.mark.parametrize("n,d", [(8, 3_000_017), (3, 70_001), (1, 5_000)])
+def test_thc_host_streamed_round_matches_device_round(n, d):
+    """Host inputs take the streamed path (PCIe in / kernel / PCIe out overlapped over tile
+    segments, residual double-buffered); results equal the device-input round bit for bit."""
+    import paper_2407_01378_b200 as gcb
+    seeds = gcb.SeedSpec(11)
+    grads = [[seeds.rng("grad-worker", r, w).standard_normal(d).astype(np.float32) for w in range(n)]
+             for r in range(3)]
+    host = gcb.make_pipeline(gcb.RotatedQuantConfig(4, 8), n, d, seeds)
+    dev = gcb.make_pipeline(gcb.RotatedQuantConfig(4, 8), n, d, seeds)
+    for r in range(3):
+        pinned = [torch.from_numpy(x).pin_memory() for x in grads[r]] if r == 1 else grads[r]
+        a = host.run_round(pinned, r)
+        b = dev.run_round(torch.from_numpy(np.stack(grads[r])).cuda(), r)
+        assert a.estimate_host is not None and b.estimate_host is None
+        assert np.array_equal(a.estimate.logical, b.estimate.logical), r
+        assert torch.equal(host.residuals_tensor, dev.residuals_tensor), r
+        assert a.overflow.clip_events == b.overflow.clip_events
+        assert a.overflow.code_sigma == b.overflow.code_sigma
+        assert a.nmse == pytest.approx(b.nmse, rel=1e-12)
+
+
+def test_thc_host_streamed_round_rejects_nonfinite_without_state_change():
+    """pipelines.py:184-197: a non-finite gradient raises ValueError before any EF state change,
+    even though the streamed round has already run tiles of earlier segments."""
+    import paper_2407_01378_b200 as gcb
+    n, d = 4, 2_000_000
+    seeds = gcb.SeedSpec(3)
+    pipe = gcb.make_pipeline(gcb.RotatedQuantConfig(4, 4), n, d, seeds)
+    g0 = [seeds.rng("grad-worker", 0, w).standard_normal(d).astype(np.float32) for w in range(n)]
+    pipe.run_round(g0, 0)
+    before = pipe.residuals_tensor.clone()
+    bad = [x.copy() for x in g0]
+    bad[2][d - 10] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        pipe.run_round(bad, 1)
+    assert torch.equal(pipe.residuals_tensor, before)
+    ref = gcb.make_pipeline(gcb.RotatedQuantConfig(4, 4), n, d, seeds)
+    ref.run_round(g0, 0)
+    a, b = pipe.run_round(g0, 1), ref.run_round(g0, 1)
+    assert np.array_equal(a.estimate.logical, b.estimate.logical)

@@ -10,10 +10,14 @@ data = [(int(r[0], 16), float(r[ix] or 0), float(r[isamp] or 0)) for r in rows[2
 base = min(a for a, _, _ in data)
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=tmp, capture_output=True)
-cubin = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cubin)], capture_output=True, text=True).stdout
-# map function name -> address->line
 want = sys.argv[4] if len(sys.argv) > 4 else None
+dis = ""
+for cubin in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):   # a .so holds one per .cu
+    text = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cubin)], capture_output=True, text=True).stdout
+    if want is None or want in text:
+        dis = text
+        break
+# map function name -> address->line
 lm = {}; cur = None; infn = False
 for line in dis.split("\n"):
     if line.startswith(".text."):
