@@ -310,13 +310,21 @@ __global__ void mq_reduce_kernel(int L, int slabs, int64_t rows, int R, const do
   }
 }
 
-// Q = M^T P_hat: a thread owns 4 consecutive columns (a CTA 1024), rows in 4-row steps.
+// Q = M^T P_hat: a thread owns 4 consecutive columns (a CTA 1024) and streams the rows of its
+// split.  Products accumulate in fp32 FMAs over 32-row groups that are folded into fp64
+// registers (per element: one float4 lane and 4 FFMA -- no fp32->fp64 conversions, which run
+// at a quarter of the FMA rate and capped the fp64 version at ~40% of HBM); the P_hat rows are
+// broadcast from shared memory as float4.  Accuracy: 32 fp32 terms per group, fp64 across
+// groups (~1e-7 relative, the reference itself is fp32 BLAS).
+constexpr int kMtpFold = 32;
+
 template <int R>
 __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, int64_t cols, const float *c,
                                                       Rows rw_, const float *ph, int64_t rows_per_split,
                                                       double *partial, int splits) {
   constexpr int kChunk = R <= 8 ? 512 : 256;
-  __shared__ float ps[kChunk * R];
+  constexpr int RP = R <= 4 ? 4 : (R <= 8 ? 8 : 16);   // P_hat rows padded for float4 reads
+  __shared__ __align__(16) float ps[kChunk * RP];
   const int w = blockIdx.z;
   const int s = blockIdx.y;
   const int64_t col = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * 4;
@@ -325,33 +333,53 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
   const float *cw = c + rw_.at(w);
   ph += static_cast<int64_t>(rw_.tensor(w)) * rows * R;
   double acc[4][R];
+  float a32[4][R];
 #pragma unroll
   for (int t = 0; t < 4; ++t)
 #pragma unroll
-    for (int b = 0; b < R; ++b) acc[t][b] = 0.0;
+    for (int b = 0; b < R; ++b) acc[t][b] = 0.0, a32[t][b] = 0.0f;
   for (int64_t i0 = r0; i0 < r1; i0 += kChunk) {
     const int ni = static_cast<int>(min(static_cast<int64_t>(kChunk), r1 - i0));
     __syncthreads();
-    for (int e = threadIdx.x; e < ni * R; e += 256) ps[e] = ph[i0 * R + e];
+    for (int e = threadIdx.x; e < ni * RP; e += 256) {
+      const int ii = e / RP, b = e - ii * RP;
+      ps[e] = b < R ? ph[(i0 + ii) * R + b] : 0.0f;
+    }
     __syncthreads();
     if (col < cols) {
+      for (int g0 = 0; g0 < ni; g0 += kMtpFold) {
+        const int g1 = min(ni, g0 + kMtpFold);
 #pragma unroll 8
-      for (int ii = 0; ii < ni; ++ii) {
-        const int64_t i = (i0 + ii) * cols + col;
-        float4 m;
-        if (i + 3 < d) {
-          m = __ldcs(reinterpret_cast<const float4 *>(cw + i));
-        } else {
-          float t4[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int ii = g0; ii < g1; ++ii) {
+          const int64_t i = (i0 + ii) * cols + col;
+          float4 m;
+          if (i + 3 < d) {
+            m = __ldcs(reinterpret_cast<const float4 *>(cw + i));
+          } else {
+            float t4[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int t = 0; t < 4; ++t)
+              if (i + t < d) t4[t] = cw[i + t];
+            m = make_float4(t4[0], t4[1], t4[2], t4[3]);
+          }
+          const float m4[4] = {m.x, m.y, m.z, m.w};
+          float pv[RP];
+#pragma unroll
+          for (int b4 = 0; b4 < RP; b4 += 4) {
+            const float4 p4 = *reinterpret_cast<const float4 *>(ps + ii * RP + b4);
+            pv[b4] = p4.x; pv[b4 + 1] = p4.y; pv[b4 + 2] = p4.z; pv[b4 + 3] = p4.w;
+          }
+#pragma unroll
           for (int t = 0; t < 4; ++t)
-            if (i + t < d) t4[t] = cw[i + t];
-          m = make_float4(t4[0], t4[1], t4[2], t4[3]);
+#pragma unroll
+            for (int b = 0; b < R; ++b) a32[t][b] = fmaf(m4[t], pv[b], a32[t][b]);
         }
-        const float m4[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
         for (int t = 0; t < 4; ++t)
 #pragma unroll
-          for (int b = 0; b < R; ++b) acc[t][b] += static_cast<double>(m4[t]) * static_cast<double>(ps[ii * R + b]);
+          for (int b = 0; b < R; ++b) {
+            acc[t][b] += static_cast<double>(a32[t][b]);
+            a32[t][b] = 0.0f;
+          }
       }
     }
   }
@@ -402,12 +430,15 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
       const int64_t i = (row0 + a) * cols + col;
       if (i >= d) break;
       float o4[4];
+      float pa[R];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        double v = 0.0;
+      for (int b = 0; b < R; ++b) pa[b] = ps[a * R + b];
 #pragma unroll
-        for (int b = 0; b < R; ++b) v += static_cast<double>(ps[a * R + b]) * static_cast<double>(qv[t][b]);
-        o4[t] = static_cast<float>(v);
+      for (int t = 0; t < 4; ++t) {   // fp32 FMAs, as the reference's fp32 p_hat @ q.T (K = r)
+        float v = pa[0] * qv[t][0];
+#pragma unroll
+        for (int b = 1; b < R; ++b) v = fmaf(pa[b], qv[t][b], v);
+        o4[t] = v;
       }
       if (i + 3 < d) {
         if (w < L) {

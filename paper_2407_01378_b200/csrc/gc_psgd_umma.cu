@@ -32,7 +32,7 @@ namespace {
 constexpr int kM = 128;          // UMMA M: rows per CTA
 constexpr int kN = 16;           // UMMA N: rank padded to 16
 constexpr int kKc = 32;          // columns per stage: one 128-byte swizzle atom of tf32
-constexpr int kStages = 4;
+constexpr int kStages = 2;
 constexpr int kThreads = 256;
 constexpr int kGroup = 16;       // chunks per TMEM partial (512 columns) before the fp64 fold
 constexpr int kATile = kM * kKc * 4;    // 16 KB
@@ -103,7 +103,7 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 }
 
 template <int R>
-__global__ void __launch_bounds__(kThreads, 1) mq_umma_kernel(int64_t d, int64_t rows, int64_t cols, const float *g,
+__global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t rows, int64_t cols, const float *g,
                                                               float *r, Rows rw_, const float *q, double *partial,
                                                               int splits, int64_t chunks_per_split) {
   extern __shared__ unsigned char smem_raw[];
@@ -176,9 +176,43 @@ __global__ void __launch_bounds__(kThreads, 1) mq_umma_kernel(int64_t d, int64_t
   };
 
   const int64_t nloc = c_end - c_begin;
+  // chunk kk's g and r in registers: thread t covers float4 f = t + 256u (row f / 8, chunk f % 8);
+  // the next chunk's loads are issued before this chunk's stores, so 8 float4 stay in flight
+  float4 pg[4], pr[4];
+  auto load_chunk = [&](int64_t kk) {
+    const int64_t col0 = (c_begin + kk) * kKc;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int f = tid + kThreads * u;
+      const int64_t grow = row0 + (f >> 3), col = col0 + 4 * (f & 7);
+      const int64_t i = grow * cols + col;
+      pg[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      pr[u] = pg[u];
+      if (grow < rows && col < cols) {
+        if (i + 3 < d) {
+          pg[u] = __ldcs(reinterpret_cast<const float4 *>(gw + i));
+          if (rw) pr[u] = __ldcs(reinterpret_cast<const float4 *>(rw + i));
+        } else {
+          float t[4] = {0.f, 0.f, 0.f, 0.f}, t2[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int e = 0; e < 4; ++e)
+            if (i + e < d) {
+              t[e] = gw[i + e];
+              if (rw) t2[e] = rw[i + e];
+            }
+          pg[u] = make_float4(t[0], t[1], t[2], t[3]);
+          pr[u] = make_float4(t2[0], t2[1], t2[2], t2[3]);
+        }
+      }
+    }
+  };
+  if (nloc > 0) load_chunk(0);
   for (int64_t k = 0; k < nloc; ++k) {
     const int s = static_cast<int>(k % kStages);
     const int64_t col0 = (c_begin + k) * kKc;
+    float4 cg[4], cr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cg[u] = pg[u], cr[u] = pr[u];
+    if (k + 1 < nloc) load_chunk(k + 1);
     if (k >= kStages) mbar_wait(empty_bar(s), static_cast<uint32_t>(((k / kStages) - 1) & 1));
     // ---- A: corrected = f32(g + r) for 128 rows x 32 columns, written back over r, split
 #pragma unroll
@@ -187,27 +221,17 @@ __global__ void __launch_bounds__(kThreads, 1) mq_umma_kernel(int64_t d, int64_t
       const int row = f >> 3, ch = f & 7;
       const int64_t grow = row0 + row, col = col0 + 4 * ch;
       const int64_t i = grow * cols + col;
-      float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (grow < rows && col < cols) {
-        if (i + 3 < d) {
-          c = __ldcs(reinterpret_cast<const float4 *>(gw + i));
-          if (rw) {
-            const float4 rv = __ldcs(reinterpret_cast<const float4 *>(rw + i));
-            c.x = c.x + rv.x; c.y = c.y + rv.y; c.z = c.z + rv.z; c.w = c.w + rv.w;
+      float4 c = cg[u];
+      if (rw) {
+        c.x = c.x + cr[u].x; c.y = c.y + cr[u].y; c.z = c.z + cr[u].z; c.w = c.w + cr[u].w;
+        if (grow < rows && col < cols) {
+          if (i + 3 < d) {
             __stcs(reinterpret_cast<float4 *>(rw + i), c);   // corrected kept in r for the later passes
+          } else {
+            const float cv[4] = {c.x, c.y, c.z, c.w};
+            for (int e = 0; e < 4; ++e)
+              if (i + e < d) rw[i + e] = cv[e];
           }
-        } else {
-          float t[4] = {0.f, 0.f, 0.f, 0.f};
-          for (int e = 0; e < 4; ++e)
-            if (i + e < d) {
-              float vv = gw[i + e];
-              if (rw) {
-                vv = vv + rw[i + e];
-                rw[i + e] = vv;
-              }
-              t[e] = vv;
-            }
-          c = make_float4(t[0], t[1], t[2], t[3]);
         }
       }
       float4 hb, hs;
