@@ -256,6 +256,11 @@ int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, do
 /* cudaMemsetAsync wrapper (residual reset of the dense bypass, pipelines.py:336). */
 int gc_fill_zero(void *ptr, int64_t bytes, void *stream);
 
+/* SparsePayload wire bytes (encode_payload, compressors.py:292-297) for each worker's TopK
+ * payload: out row w (stride >= 5 + 6k bytes) = <u8 1><u32 k><i32 idx[k]><f16 val[k]>, little endian. */
+int gc_encode_sparse_payloads(int32_t workers, int64_t k, const int32_t *idx, const float *val, uint8_t *out,
+                              int64_t stride, void *stream);
+
 /* Whole THC round for n workers simulated on one GPU, fused into one kernel per
  * rotation block (pipelines.py:260-322 + EF 148-151,168-170): every CTA owns one block of
  * all n workers, so range consensus, quantization, the ring-ordered saturating fold,

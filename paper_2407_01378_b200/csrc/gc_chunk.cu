@@ -119,6 +119,72 @@ __global__ void __launch_bounds__(kNT) norms_lanes_kernel(int64_t d, int C, int6
   }
 }
 
+// Fused ef_apply + chunk energies with float4 traffic (aligned rows, C % 8 == 0, C <= 128):
+// two lanes per chunk, lane half h owning numpy's accumulators 4h..4h+3 (elements 8t + 4h + q),
+// so one float4 of g and one of r per lane and 8-element step; corrected is written back over
+// r as float4.  In-lane ((r0+r1)+(r2+r3)), then one shuffle adds the other half: the same
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree as numpy.  x*x is exact in fp64, so
+// fma(x, x, r) == r + x*x bit for bit.  Chunks that cross d take the scalar path.
+__global__ void __launch_bounds__(kNT, 2) norms_ef_vec_kernel(int64_t d, int C, int64_t nc, const float *grads,
+                                                           float *resid, int64_t ld, float *out) {
+  const int w = blockIdx.y;
+  const float *grow = grads + w * ld;
+  float *rrow = resid ? resid + w * ld : nullptr;
+  const int half = threadIdx.x & 1;
+  const int nt = C >> 3;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * (kNT / 2);
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(kNT / 2) + (threadIdx.x >> 1); c - (threadIdx.x & 31) / 2 < nc;
+       c += stride) {
+    const bool live = c < nc;
+    const int64_t i0 = c * C + 4 * half;
+    double r[4] = {0.0, 0.0, 0.0, 0.0};
+    if (live && (c + 1) * C <= d) {
+      for (int t0 = 0; t0 < nt; t0 += 8) {   // 8 steps of loads in flight per lane
+        float4 gv[8], rv[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (t0 + t < nt) {
+            const int64_t x = i0 + 8 * (t0 + t);
+            gv[t] = __ldcs(reinterpret_cast<const float4 *>(grow + x));
+            rv[t] = rrow ? __ldcs(reinterpret_cast<const float4 *>(rrow + x)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (t0 + t < nt) {
+            float4 cv = gv[t];
+            if (rrow) {
+              cv.x = cv.x + rv[t].x; cv.y = cv.y + rv[t].y; cv.z = cv.z + rv[t].z; cv.w = cv.w + rv[t].w;
+              *reinterpret_cast<float4 *>(rrow + i0 + 8 * (t0 + t)) = cv;
+            }
+            const double a = cv.x, b = cv.y, e = cv.z, f = cv.w;
+            r[0] = fma(a, a, r[0]);
+            r[1] = fma(b, b, r[1]);
+            r[2] = fma(e, e, r[2]);
+            r[3] = fma(f, f, r[3]);
+          }
+      }
+    } else if (live) {
+      for (int t = 0; t < nt; ++t)
+        for (int q = 0; q < 4; ++q) {
+          const int64_t x = i0 + 8 * t + q;
+          float cv = 0.0f;
+          if (x < d) {
+            cv = grow[x];
+            if (rrow) {
+              cv = cv + rrow[x];
+              rrow[x] = cv;
+            }
+          }
+          const double v = cv;
+          r[q] = fma(v, v, r[q]);
+        }
+    }
+    double sum = (r[0] + r[1]) + (r[2] + r[3]);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);   // half 0: (r0..r3) + (r4..r7); same on half 1
+    if (live && half == 0) out[w * nc + c] = gc::fp16_round_trip(static_cast<float>(0.0 + sum));
+  }
+}
+
 // payload[w][jj*C + t] = fp16(work_w[sel[jj]*C + t]) (0 past d)  -- chunk_values.
 __global__ void __launch_bounds__(kNT) pack_kernel(int64_t d, int64_t C, int64_t J, const int32_t *sel,
                                                    const float *vals, int64_t ld, const int64_t *perm,
@@ -237,8 +303,14 @@ int gc_chunk_norms_ef(int32_t workers, int64_t d, int64_t chunk, const float *gr
              "invalid argument");
   GC_REQUIRE(chunk % 8 == 0 && chunk <= 128, "fused ef_apply + norms needs chunk % 8 == 0 and chunk <= 128");
   const int64_t nc = (d + chunk - 1) / chunk;
-  norms_lanes_kernel<<<dim3(grid_for(nc * 8), workers), kNT, 0, static_cast<cudaStream_t>(stream)>>>(
-      d, static_cast<int>(chunk), nc, resid ? resid : grads, ld, nullptr, norms, grads, resid);
+  const bool vec = (ld % 4) == 0 && ((reinterpret_cast<uintptr_t>(grads) | reinterpret_cast<uintptr_t>(resid)) & 15) == 0;
+  if (vec) {
+    norms_ef_vec_kernel<<<dim3(grid_for(nc * 2), workers), kNT, 0, static_cast<cudaStream_t>(stream)>>>(
+        d, static_cast<int>(chunk), nc, grads, resid, ld, norms);
+  } else {
+    norms_lanes_kernel<<<dim3(grid_for(nc * 8), workers), kNT, 0, static_cast<cudaStream_t>(stream)>>>(
+        d, static_cast<int>(chunk), nc, resid ? resid : grads, ld, nullptr, norms, grads, resid);
+  }
   GC_LAUNCH_CHECK("norms_lanes_kernel");
   return GC_OK;
 }

@@ -20,7 +20,7 @@
 // registers, alternating between two TMEM accumulators so the fold never stalls the MMA.  The
 // fp64 split-K partials go through the existing ordered reduction (deterministic).
 //
-// Precision: 3xTF32 drops only small * small (~2^-22 relative per product); fp32 accumulation
+// Precision: 3xTF32 drops small * small and the bits below small (~2^-20 relative per product); fp32 accumulation
 // spans at most 512 products before the fp64 fold.  Against the reference's fp32 BLAS the
 // factors agree to ~1e-6 relative (the contract is 1e-5).
 #include <cuda_runtime.h>
@@ -63,15 +63,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 16, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((kN >> 3) << 17) | ((kM >> 4) << 24);
 
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
+// 3xTF32 split by truncation: big keeps the top 10 mantissa bits (the tensor core reads a
+// tf32 operand as the f32 pattern with the low 13 bits ignored), small = c - big is exact in
+// f32 and is itself truncated to tf32.  c - (big + small) < 2^-20 |c|; two LOP3 + one FADD
+// per value (cvt.rna.tf32.f32 is a 4-instruction sequence on sm_100).
 __device__ __forceinline__ void split3(float c, float &big, float &small) {
-  big = tf32_rna(c);
-  small = tf32_rna(c - big);
+  big = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);
+  small = __uint_as_float(__float_as_uint(c - big) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {

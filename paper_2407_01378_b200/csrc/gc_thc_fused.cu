@@ -60,7 +60,7 @@ struct FusedArgs {
 };
 
 struct Layout {
-  int scratch, cbuf, cod, wr, bp, lut, sgn, total;
+  int scratch, cbuf, cod, wr, bp, lut, sgn, pcg, total;
 };
 
 constexpr int kScrRow = 33;   // fp64 transpose rows padded to 33: conflict-free, immediate offsets
@@ -68,16 +68,18 @@ constexpr int kCRow = 36;     // corrected-value rows padded to 36 floats (float
 constexpr int kScrBytes = 32 * kScrRow * 8;
 constexpr int kCBytes = 32 * kCRow * 4;
 
-__host__ __device__ inline Layout layout_for(int n, int nblk) {
+__host__ __device__ inline Layout layout_for(int n, int nblk, int q) {
   Layout L;
   L.scratch = 0;                        // n x 8.25 KB  fp64 transpose / x_rot staging
   L.cbuf = L.scratch + n * kScrBytes;   // n x 4.5 KB   corrected (f32, padded natural order)
   L.cod = L.cbuf + n * kCBytes;         // n x 1 KB     codes
   L.wr = L.cod + n * 1024;              // n x nblk x 2 f32   own block ranges
   L.bp = L.wr + ((n * nblk * 8 + 15) & ~15);   // n x nblk x 8 f64  consensus params (per warp)
-  L.lut = L.bp + n * nblk * 64;         // kLutMax f64  dq(z, 1) table
-  L.sgn = L.lut + kLutMax * 8;          // 2 x 32 u32 sign words (double-buffered by tile parity)
-  L.total = L.sgn + 256;
+  L.lut = L.bp + n * nblk * 64;         // nblk x (2^q - 1) f64 (<= kLutMax)  dq(z, 1) table
+  const int lut_n = nblk * ((1 << q) - 1);
+  L.sgn = L.lut + ((lut_n < kLutMax ? lut_n : kLutMax) * 8 + 15) / 16 * 16;          // 2 x 32 u32 sign words (double-buffered by tile parity)
+  L.pcg = L.sgn + 256;                  // n x 16 u32: the worker's 4-step and tile-step LCG jumps
+  L.total = L.pcg + n * 64;
   return L;
 }
 
@@ -262,7 +264,8 @@ __device__ __noinline__ int quantize_ref(double x, double lo, double hi, double 
 // frac = t32 - floor(t32) (2^-25).  A coordinate whose f32 frac lies in [H, 1 - H] and more
 // than H from the coin prefix has the reference's floor(t), no snapping and the same coin
 // comparison, so its code is decided in fp32; the rest (probability ~6H) take quantize_ref.
-// Degenerate blocks (step <= 0) always pass the screen (their code is forced to 0).
+// Degenerate blocks (step <= 0) always pass the screen with t32 = 0 and a coin test against
+// frac = 0 that never fires, i.e. code 0 as the reference forces (compressors.py:497).
 __device__ __forceinline__ float4 screen_params(double mid, double step, double bound) {
   if (!(step > 0.0)) return make_float4(0.0f, 0.0f, -1.0f, 2.0f);
   const double m = fabs(mid) / step * 0x1p-24;
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
   const int w = threadIdx.x >> 5;            // worker of this warp
   constexpr int k = K;                       // log2(rotation block), 5..10
   constexpr int nblk = kTileN >> K;
-  const Layout L = layout_for(n, nblk);
+  const Layout L = layout_for(n, nblk, a.q);
   double *scratch = reinterpret_cast<double *>(smem + L.scratch) + w * (32 * kScrRow);
   float *xs = reinterpret_cast<float *>(scratch);                  // x_rot staging (layout B)
   const float *cbuf_all = reinterpret_cast<const float *>(smem + L.cbuf);
@@ -304,18 +307,29 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
 
   // ---- PCG64 coin stream of worker w: four lane-strided chains (j mod 4), 128-step jumps.
   const uint64_t inc_h = a.streams[w].inc_hi, inc_l = a.streams[w].inc_lo;
-  uint32_t m32[4], c32[4], m128[4], c128[4], mt[4], ct[4];
+  // the per-step (128-step) jump stays in registers; the once-per-tile jumps live in shared
+  // memory (pcgw: {m32, c32, mt, ct}) to keep the quantizer loop free of spills
+  uint32_t m128[4], c128[4];
+  uint32_t *pcgw = reinterpret_cast<uint32_t *>(smem + L.pcg) + w * 16;
   {
     uint64_t h, l;
-    limbs(gc::kPcgJump[5][0], gc::kPcgJump[5][1], m32);
-    mul128(gc::kPcgJump[5][2], gc::kPcgJump[5][3], inc_h, inc_l, h, l);
-    limbs(h, l, c32);
+    uint32_t t4[4];
     limbs(gc::kPcgJump[7][0], gc::kPcgJump[7][1], m128);
     mul128(gc::kPcgJump[7][2], gc::kPcgJump[7][3], inc_h, inc_l, h, l);
     limbs(h, l, c128);
-    limbs(a.tile_jump[0], a.tile_jump[1], mt);
-    mul128(a.tile_jump[2], a.tile_jump[3], inc_h, inc_l, h, l);
-    limbs(h, l, ct);
+    if (lane == 0) {
+      limbs(gc::kPcgJump[5][0], gc::kPcgJump[5][1], t4);
+      for (int e = 0; e < 4; ++e) pcgw[e] = t4[e];
+      mul128(gc::kPcgJump[5][2], gc::kPcgJump[5][3], inc_h, inc_l, h, l);
+      limbs(h, l, t4);
+      for (int e = 0; e < 4; ++e) pcgw[4 + e] = t4[e];
+      limbs(a.tile_jump[0], a.tile_jump[1], t4);
+      for (int e = 0; e < 4; ++e) pcgw[8 + e] = t4[e];
+      mul128(a.tile_jump[2], a.tile_jump[3], inc_h, inc_l, h, l);
+      limbs(h, l, t4);
+      for (int e = 0; e < 4; ++e) pcgw[12 + e] = t4[e];
+    }
+    __syncwarp();
   }
   Lcg tile_state;
   {
@@ -331,8 +345,13 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
   long long sz = 0, sz2 = 0, clips = 0;
   double nmse_num = 0.0, nmse_den = 0.0;
 
+  // sign words of the next tile are loaded one tile ahead (the forward rotation needs them first)
+  uint32_t next_sign_word = 0;
+  if (a.tile_begin + blockIdx.x < a.tiles) next_sign_word = a.signs[((a.tile_begin + blockIdx.x) * kTileN >> 5) + lane];
   for (int64_t tile = a.tile_begin + blockIdx.x; tile < a.tiles; tile += gridDim.x) {
     const int64_t t0 = tile * kTileN;
+    const uint32_t my_sign_word = next_sign_word;
+    if (tile + gridDim.x < a.tiles) next_sign_word = a.signs[((tile + gridDim.x) * kTileN >> 5) + lane];
     uint32_t *sgn = sgn_all + (((tile - a.tile_begin) / gridDim.x) & 1) * 32;
     {   // pull the next tile of this worker's g and r rows into L2 while this tile computes
       const int64_t tn = t0 + static_cast<int64_t>(gridDim.x) * kTileN;
@@ -372,7 +391,6 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
       }
       *reinterpret_cast<float4 *>(cbuf + cidx(e4)) = c;
     }
-    const uint32_t my_sign_word = a.signs[(t0 >> 5) + lane];
     if (w == 0) sgn[lane] = my_sign_word;
     __syncwarp();
 
@@ -453,20 +471,28 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
     {
       Lcg ch[4];
       ch[0] = tile_state;
+      {
+        uint32_t m32[4], c32[4];
 #pragma unroll
-      for (int c = 1; c < 4; ++c) {
-        ch[c] = ch[c - 1];
-        ch[c].step(m32, c32);
+        for (int e = 0; e < 4; ++e) m32[e] = pcgw[e], c32[e] = pcgw[4 + e];
+#pragma unroll
+        for (int c = 1; c < 4; ++c) {
+          ch[c] = ch[c - 1];
+          ch[c].step(m32, c32);
+        }
       }
+      int tz = 0, tz2 = 0;   // per-tile code sums (|z| <= 127, 32 codes per lane: int32 is exact)
       for (int j = 0; j < 32; j += 4) {
         int z[4];
         uint32_t hw[4], lw[4];
         float xv[4];
         bool safe = true;
+        // screen parameters: one rotation block spans >= 4 registers when B >= 128
+        const float4 sp_j = *reinterpret_cast<const float4 *>(bp + 8 * (j >> rpb_log) + 6);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const int blk = (j + c) >> rpb_log;
-          const float4 sp = *reinterpret_cast<const float4 *>(bp + 8 * blk + 6);
+          const float4 sp =
+              rpb_log >= 2 ? sp_j : *reinterpret_cast<const float4 *>(bp + 8 * ((j + c) >> rpb_log) + 6);
           ch[c].out(hw[c], lw[c]);
           ch[c].step(m128, c128);
           xv[c] = xs[(j + c) * 32 + lane];
@@ -492,17 +518,23 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
                                   static_cast<double>(ibound), coin_from(hw[c], lw[c]));
           }
         }
+        // (degenerate blocks, compressors.py:497, come out as code 0 from their screen parameters)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const double *pb = bp + 8 * ((j + c) >> rpb_log);
-          z[c] = pb[3] > 0.0 ? z[c] : 0;   // degenerate block: code 0 (compressors.py:497)
           cod[(j + c) * 32 + lane] = static_cast<int8_t>(z[c]);
-          sz += z[c];
-          sz2 += z[c] * z[c];
+          tz += z[c];
+          tz2 += z[c] * z[c];
         }
       }
+      sz += tz;
+      sz2 += tz2;
     }
-    tile_state.step(mt, ct);
+    {
+      uint32_t mt[4], ct[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) mt[e] = pcgw[8 + e], ct[e] = pcgw[12 + e];
+      tile_state.step(mt, ct);
+    }
     __syncthreads();   // (B) all codes and the dq table of the tile are in shared memory
 
     if (a.codes && t0 + lane * 32 < a.active) {   // optional code dump (parity tests)
@@ -569,7 +601,10 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
         }
       }
     }
-    __syncthreads();   // (D) the tile's dequantized sums are complete
+    // (D) the tile's dequantized sums are complete.  With n = 8 the fold of warp w covers
+    // coordinates [128w, 128w + 128) = rows 4w..4w+3, exactly the rows its row phase below
+    // transforms, so the dependency is warp-local.
+    if (n == 8) __syncwarp(); else __syncthreads();
 
     // ---- estimate inverse rotation spread over all warps (transforms.py:120-126): a 32-lane
     // step covers 4 rows x 32 columns of the 32 x 32 tile, 4 elements per lane.  Row phase:
@@ -777,7 +812,7 @@ int launch_fused(const gc_thc_geom *g, int32_t n, const float *grads, const floa
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int smem = layout_for(n, nblk).total;
+  const int smem = layout_for(n, nblk, g->quant_bits).total;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, n * 32, smem);

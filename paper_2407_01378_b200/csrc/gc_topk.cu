@@ -7,14 +7,22 @@
 //
 // B200 design (HBM-bound integer work): keys are the f32 bit patterns with the sign
 // cleared (order-preserving for |x|, +-0 equal).  A three-level radix select (11 + 10 + 10
-// bits) finds the threshold key T and m = how many elements equal to T are taken; each
-// level is one coalesced histogram pass (shared-memory histograms, one global atomic per
-// bin) plus a one-CTA bin search.  Per 8192-element tile, counts of (key > T) and
-// (key == T) are scanned into output offsets and tie ranks; the write pass emits indices in
-// ascending order with warp ballots, so no sort is needed.  All L rows (workers) run in the
-// same launches (grid.y = worker).
+// bits) finds the threshold key T and m = how many elements equal to T are taken.  Only
+// three passes touch the whole row:
+//   1. level-0 histogram (float4 loads; fused with ef_apply, writing corrected over r);
+//   2. collect: per 4096-element tile the count of keys above the level-0 boundary bin, and
+//      the boundary bin's elements appended (key, index) to a per-worker candidate list
+//      (warp-aggregated atomics; typically < 1 % of the row) -- levels 1 and 2 and the tie
+//      counts then run on the candidates only;
+//   3. write: per tile, offsets from a scan of the (above, tie) counts; indices are emitted in
+//      ascending order with warp ballots, so no sort is needed.
+// If the boundary bin overflows the candidate capacity (degenerate inputs, e.g. a constant
+// row) the select falls back to full-row passes for levels 1-2 and the tile counts.  Every
+// count is an integer sum, so the result does not depend on the atomic order.  All L rows
+// (workers) run in the same launches (grid.y = worker).
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "gc_device.cuh"
@@ -34,6 +42,7 @@ struct RowState {  // per worker, lives in the workspace
   unsigned int thresh;     // final threshold key T
   unsigned int pad2;
   long long take_eq;       // m: number of T-keyed elements taken (lowest indices)
+  unsigned long long cand_count;   // boundary-bin elements collected (may exceed the capacity)
 };
 
 struct Work {
@@ -43,11 +52,19 @@ struct Work {
   unsigned int *tile_eq;        // [L][tiles]
   long long *tile_sel_off;      // [L][tiles]
   long long *tile_eq_off;       // [L][tiles]
+  unsigned int *cand_key;       // [L][cap]
+  unsigned int *cand_idx;       // [L][cap]
+  int64_t cap;
 };
+
+__host__ __device__ inline int64_t cand_cap_for(int64_t len) {
+  const int64_t c = len / 16 > (int64_t{1} << 16) ? len / 16 : (int64_t{1} << 16);
+  return c < len ? c : len;
+}
 
 __host__ __device__ inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t{255}; }
 
-__host__ __device__ inline Work carve(void *ws, int L, int64_t tiles) {
+__host__ __device__ inline Work carve(void *ws, int L, int64_t tiles, int64_t len) {
   char *p = static_cast<char *>(ws);
   Work w;
   w.state = reinterpret_cast<RowState *>(p);
@@ -61,12 +78,17 @@ __host__ __device__ inline Work carve(void *ws, int L, int64_t tiles) {
   w.tile_sel_off = reinterpret_cast<long long *>(p);
   p += align256(int64_t{8} * tiles * L);
   w.tile_eq_off = reinterpret_cast<long long *>(p);
+  p += align256(int64_t{8} * tiles * L);
+  w.cap = cand_cap_for(len);
+  w.cand_key = reinterpret_cast<unsigned int *>(p);
+  p += align256(int64_t{4} * w.cap * L);
+  w.cand_idx = reinterpret_cast<unsigned int *>(p);
   return w;
 }
 
-int64_t ws_bytes(int L, int64_t tiles) {
+int64_t ws_bytes(int L, int64_t tiles, int64_t len) {
   return align256(sizeof(RowState) * L) + align256(int64_t{4} * 2048 * L) + 2 * align256(int64_t{4} * tiles * L) +
-         2 * align256(int64_t{8} * tiles * L);
+         2 * align256(int64_t{8} * tiles * L) + 2 * align256(int64_t{4} * cand_cap_for(len) * L);
 }
 
 __device__ __forceinline__ unsigned int key_of(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
@@ -88,6 +110,7 @@ __global__ void __launch_bounds__(kNT) init_kernel(Work wk, int L, int64_t k) {
     s.gt = 0;
     s.thresh = 0;
     s.take_eq = 0;
+    s.cand_count = 0;
   }
 }
 
@@ -120,6 +143,212 @@ __global__ void __launch_bounds__(kNT) hist_kernel(Work wk, int level, int64_t l
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += kNT)
     if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
+}
+
+// Level 0 with float4 loads (aligned rows): a thread's 16 elements are 4 float4 at stride
+// 256, all loads issued before the shared-memory atomics.  grads != NULL fuses ef_apply.
+__global__ void __launch_bounds__(kNT) hist0_vec_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
+                                                        const float *grads, float *resid) {
+  __shared__ unsigned int h[2048];
+  const int w = blockIdx.y;
+  for (int i = threadIdx.x; i < 2048; i += kNT) h[i] = 0;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
+  float4 x[4];
+  const bool full = base + kTileE <= len;
+  if (full) {
+    const float *src = grads ? grads + w * ld : vals + w * ld;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = __ldcs(reinterpret_cast<const float4 *>(src + base) + threadIdx.x + kNT * u);
+    if (grads && resid) {
+      float4 *rr = reinterpret_cast<float4 *>(resid + w * ld + base);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 r4 = rr[threadIdx.x + kNT * u];
+        x[u].x = x[u].x + r4.x; x[u].y = x[u].y + r4.y; x[u].z = x[u].z + r4.z; x[u].w = x[u].w + r4.w;
+        rr[threadIdx.x + kNT * u] = x[u];
+      }
+    }
+  }
+  __syncthreads();
+  if (full) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      atomicAdd(&h[key_of(x[u].x) >> 20], 1u);
+      atomicAdd(&h[key_of(x[u].y) >> 20], 1u);
+      atomicAdd(&h[key_of(x[u].z) >> 20], 1u);
+      atomicAdd(&h[key_of(x[u].w) >> 20], 1u);
+    }
+  } else {
+    for (int64_t i = base + threadIdx.x; i < len; i += kNT) {
+      float v;
+      if (grads) {
+        v = grads[w * ld + i];
+        if (resid) {
+          v = v + resid[w * ld + i];
+          resid[w * ld + i] = v;
+        }
+      } else {
+        v = vals[w * ld + i];
+      }
+      atomicAdd(&h[key_of(v) >> 20], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += kNT)
+    if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
+}
+
+// Pass 2: per tile, count keys above the level-0 boundary bin p0 (tile_gt) and append the
+// boundary bin's (key, index) to the worker's candidate list; tile_eq starts at 0.  Slots are
+// reserved with one global atomic per CTA (warp scans + a CTA prefix), not per warp: the
+// per-warp version serialised on the worker's counter.
+__global__ void __launch_bounds__(kNT) collect_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
+                                                      int64_t tiles, int vec) {
+  __shared__ unsigned int s_wcnt[kNT / 32];
+  __shared__ unsigned long long s_base;
+  const int w = blockIdx.y;
+  RowState &st = wk.state[w];
+  const unsigned int p0 = st.prefix;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
+  const float *row = vals + w * ld;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned int keys[kSteps];
+  unsigned int cmask = 0, gt = 0;
+  const bool full_vec = vec && base + kTileE <= len;
+  if (full_vec) {   // element 4 * (tid + 256u) + q  <->  keys[4u + q]
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 x = __ldcs(reinterpret_cast<const float4 *>(row + base) + threadIdx.x + kNT * u);
+      keys[4 * u + 0] = key_of(x.x);
+      keys[4 * u + 1] = key_of(x.y);
+      keys[4 * u + 2] = key_of(x.z);
+      keys[4 * u + 3] = key_of(x.w);
+    }
+  } else {          // element s * 256 + tid  <->  keys[s]
+#pragma unroll
+    for (int s = 0; s < kSteps; ++s) {
+      const int64_t i = base + s * kNT + threadIdx.x;
+      keys[s] = i < len ? key_of(row[i]) : 0u;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < kSteps; ++s) {
+    const int64_t i = full_vec ? base + 4 * (threadIdx.x + kNT * (s >> 2)) + (s & 3) : base + s * kNT + threadIdx.x;
+    const bool valid = i < len;
+    const unsigned int b0 = keys[s] >> 20;
+    gt += valid && b0 > p0;
+    cmask |= (valid && b0 == p0) ? (1u << s) : 0u;
+  }
+  // slot reservation: warp-inclusive scan of the per-thread candidate counts, CTA prefix
+  const unsigned int mine = __popc(cmask);
+  unsigned int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wcnt[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int tot = 0;
+    for (int j = 0; j < kNT / 32; ++j) {
+      const unsigned int c = s_wcnt[j];
+      s_wcnt[j] = tot;
+      tot += c;
+    }
+    s_base = tot ? atomicAdd(&st.cand_count, static_cast<unsigned long long>(tot)) : 0ull;
+  }
+  __syncthreads();
+  if (cmask) {
+    unsigned long long pos = s_base + s_wcnt[warp] + (incl - mine);
+#pragma unroll
+    for (int s = 0; s < kSteps; ++s)
+      if ((cmask >> s) & 1u) {
+        const int64_t i = full_vec ? base + 4 * (threadIdx.x + kNT * (s >> 2)) + (s & 3) : base + s * kNT + threadIdx.x;
+        if (pos < static_cast<unsigned long long>(wk.cap)) {
+          wk.cand_key[w * wk.cap + pos] = keys[s];
+          wk.cand_idx[w * wk.cap + pos] = static_cast<unsigned int>(i);
+        }
+        ++pos;
+      }
+  }
+  using R = cub::BlockReduce<unsigned int, kNT>;
+  __shared__ typename R::TempStorage t1;
+  const unsigned int sgt = R(t1).Sum(gt);
+  if (threadIdx.x == 0) {
+    wk.tile_gt[w * tiles + blockIdx.x] = sgt;
+    wk.tile_eq[w * tiles + blockIdx.x] = 0;
+  }
+}
+
+// Levels 1 and 2 over the candidates (grid-stride); on overflow, over the whole row.
+__global__ void __launch_bounds__(kNT) cand_hist_kernel(Work wk, int level, int64_t len, const float *vals,
+                                                        int64_t ld) {
+  __shared__ unsigned int h[1024];
+  const int w = blockIdx.y;
+  for (int i = threadIdx.x; i < 1024; i += kNT) h[i] = 0;
+  __syncthreads();
+  const RowState &st = wk.state[w];
+  const unsigned int prefix = st.prefix;
+  const int64_t nc = static_cast<int64_t>(st.cand_count);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kNT;
+  if (nc <= wk.cap) {
+    const unsigned int *ck = wk.cand_key + w * wk.cap;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < nc; e += stride) {
+      const int b = bin_of(ck[e], level, prefix);
+      if (b >= 0) atomicAdd(&h[b], 1u);
+    }
+  } else {
+    const float *row = vals + w * ld;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; i < len; i += stride) {
+      const int b = bin_of(key_of(row[i]), level, prefix);
+      if (b >= 0) atomicAdd(&h[b], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 1024; i += kNT)
+    if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
+}
+
+// Tile counts of the candidates above / equal to T (tile_gt already holds the keys above the
+// boundary bin).  On overflow the counts are recomputed from the whole row.
+__global__ void __launch_bounds__(kNT) cand_tile_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
+                                                        int64_t tiles) {
+  const int w = blockIdx.y;
+  const RowState &st = wk.state[w];
+  const unsigned int T = st.thresh;
+  const int64_t nc = static_cast<int64_t>(st.cand_count);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kNT;
+  if (nc <= wk.cap) {
+    const unsigned int *ck = wk.cand_key + w * wk.cap, *ci = wk.cand_idx + w * wk.cap;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < nc; e += stride) {
+      const unsigned int key = ck[e];
+      if (key >= T) {
+        const int64_t t = ci[e] / kTileE;
+        atomicAdd(key > T ? &wk.tile_gt[w * tiles + t] : &wk.tile_eq[w * tiles + t], 1u);
+      }
+    }
+    return;
+  }
+  const float *row = vals + w * ld;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {   // overflow: one CTA per tile
+    const int64_t base = t * kTileE, end = min(base + kTileE, len);
+    unsigned int gt = 0, eq = 0;
+    for (int64_t i = base + threadIdx.x; i < end; i += kNT) {
+      const unsigned int key = key_of(row[i]);
+      gt += key > T;
+      eq += key == T;
+    }
+    using R = cub::BlockReduce<unsigned int, kNT>;
+    __shared__ typename R::TempStorage t1, t2;
+    const unsigned int sgt = R(t1).Sum(gt);
+    const unsigned int seq = R(t2).Sum(eq);
+    if (threadIdx.x == 0) {
+      wk.tile_gt[w * tiles + t] = sgt;
+      wk.tile_eq[w * tiles + t] = seq;
+    }
+    __syncthreads();
+  }
 }
 
 // One CTA per worker: find bin b (scanning bins from the top) with
@@ -168,38 +397,6 @@ __global__ void __launch_bounds__(1024) find_kernel(Work wk, int level) {
     }
   }
   for (int i = threadIdx.x; i < 2048; i += 1024) h[i] = 0;
-}
-
-__global__ void __launch_bounds__(kNT) tile_count_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
-                                                         int64_t tiles) {
-  const int w = blockIdx.y;
-  const unsigned int T = wk.state[w].thresh;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
-  const int64_t end = min(base + kTileE, len);
-  unsigned int gt = 0, eq = 0;
-  const float *row = vals + w * ld;
-  if (end - base == kTileE) {
-#pragma unroll 8
-    for (int s = 0; s < kSteps; ++s) {
-      const unsigned int key = key_of(__ldcs(row + base + s * kNT + threadIdx.x));
-      gt += key > T;
-      eq += key == T;
-    }
-  } else {
-    for (int64_t i = base + threadIdx.x; i < end; i += kNT) {
-      const unsigned int key = key_of(row[i]);
-      gt += key > T;
-      eq += key == T;
-    }
-  }
-  using R = cub::BlockReduce<unsigned int, kNT>;
-  __shared__ typename R::TempStorage t1, t2;
-  const unsigned int sgt = R(t1).Sum(gt);
-  const unsigned int seq = R(t2).Sum(eq);
-  if (threadIdx.x == 0) {
-    wk.tile_gt[w * tiles + blockIdx.x] = sgt;
-    wk.tile_eq[w * tiles + blockIdx.x] = seq;
-  }
 }
 
 // One CTA per worker: eq prefix (tie ranks) and selected-count prefix (output offsets).
@@ -323,6 +520,107 @@ __global__ void __launch_bounds__(kNT) write_kernel(Work wk, int64_t len, const 
   }
 }
 
+// write_kernel with float4 loads (aligned rows): a warp owns 512 consecutive elements as 4
+// steps of 128, lane l holding elements 128u + 4l .. 128u + 4l + 3 of step u (index order =
+// step, lane, element).  Tie ranks and output positions come from warp scans per step, skipped
+// (one ballot) when a step has no tie / no selected element.
+__device__ __forceinline__ unsigned int warp_excl_scan(unsigned int v, int lane, unsigned int &total) {
+  unsigned int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  total = __shfl_sync(0xffffffffu, incl, 31);
+  return incl - v;
+}
+
+__global__ void __launch_bounds__(kNT) write_vec_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
+                                                        int64_t tiles, int64_t k, int32_t *idx_out, float *val_out,
+                                                        int fp16_vals) {
+  __shared__ unsigned int s_eq[kNT / 32], s_sel[kNT / 32];
+  const int w = blockIdx.y;
+  const unsigned int T = wk.state[w].thresh;
+  const long long m = wk.state[w].take_eq;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTileE + warp * 512;
+  const float *row = vals + w * ld;
+  unsigned int keys[16];
+  if (wbase + 512 <= len) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 x = __ldcs(reinterpret_cast<const float4 *>(row + wbase + 128 * u) + lane);
+      keys[4 * u] = key_of(x.x); keys[4 * u + 1] = key_of(x.y); keys[4 * u + 2] = key_of(x.z); keys[4 * u + 3] = key_of(x.w);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int64_t i = wbase + 128 * (e >> 2) + 4 * lane + (e & 3);
+      keys[e] = i < len ? key_of(row[i]) : 0u;   // key 0 is never above T; never a tie past len
+    }
+  }
+  auto valid = [&](int e) { return wbase + 128 * (e >> 2) + 4 * lane + (e & 3) < len; };
+  unsigned int eqbits = 0, gtbits = 0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const bool v = valid(e);
+    eqbits |= (v && keys[e] == T) ? (1u << e) : 0u;
+    gtbits |= (v && keys[e] > T) ? (1u << e) : 0u;
+  }
+  unsigned int weq = __popc(eqbits);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) weq += __shfl_xor_sync(0xffffffffu, weq, o);
+  if (lane == 0) s_eq[warp] = weq;
+  __syncthreads();
+  long long eq_run = wk.tile_eq_off[w * tiles + blockIdx.x];
+  for (int j = 0; j < warp; ++j) eq_run += s_eq[j];
+  unsigned int selbits = gtbits;
+  if (__any_sync(0xffffffffu, eqbits != 0u)) {   // ties: the first m (index order) are taken
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned int eu = (eqbits >> (4 * u)) & 0xFu;
+      unsigned int tot;
+      const unsigned int ex = warp_excl_scan(__popc(eu), lane, tot);
+      long long rank = eq_run + ex;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if ((eu >> q) & 1u) {
+          if (rank < m) selbits |= 1u << (4 * u + q);
+          ++rank;
+        }
+      eq_run += tot;
+    }
+  }
+  unsigned int wsel = __popc(selbits);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) wsel += __shfl_xor_sync(0xffffffffu, wsel, o);
+  if (lane == 0) s_sel[warp] = wsel;
+  __syncthreads();
+  long long out = wk.tile_sel_off[w * tiles + blockIdx.x];
+  for (int j = 0; j < warp; ++j) out += s_sel[j];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const unsigned int su = (selbits >> (4 * u)) & 0xFu;
+    if (!__any_sync(0xffffffffu, su != 0u)) continue;
+    unsigned int tot;
+    long long pos = out + warp_excl_scan(__popc(su), lane, tot);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if ((su >> q) & 1u) {
+        const int64_t i = wbase + 128 * u + 4 * lane + q;
+        if (pos < k) {
+          idx_out[w * k + pos] = static_cast<int32_t>(i);
+          if (val_out) {
+            const float x = row[i];
+            val_out[w * k + pos] = fp16_vals ? gc::fp16_round_trip(x) : x;
+          }
+        }
+        ++pos;
+      }
+    out += tot;
+  }
+}
+
 // ---------------------------------------------------------------- sparse aggregation
 // estimate[idx] += val for one worker's payload (indices unique within a payload), launched
 // once per worker in worker order: the f32 sum per coordinate follows the reference's
@@ -343,6 +641,27 @@ __global__ void sparse_ef_kernel(int L, int64_t k, const int32_t *idx, const flo
   }
 }
 
+// SparsePayload wire bytes (compressors.py:294-297): <B 1><I k><i4 idx * k><f2 val * k>, one
+// row per worker; values are fp16-valued floats, so the half conversion is exact.
+__global__ void encode_sparse_kernel(int L, int64_t k, const int32_t *idx, const float *val, uint8_t *out,
+                                     int64_t stride) {
+  const int64_t total = static_cast<int64_t>(L) * k;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = e / k, j = e - w * k;
+    uint8_t *row = out + w * stride;
+    if (j == 0) {
+      row[0] = 1;
+      for (int b = 0; b < 4; ++b) row[1 + b] = static_cast<uint8_t>(static_cast<uint64_t>(k) >> (8 * b));
+    }
+    const uint32_t iv = static_cast<uint32_t>(idx[e]);
+    for (int b = 0; b < 4; ++b) row[5 + 4 * j + b] = static_cast<uint8_t>(iv >> (8 * b));
+    const unsigned short hv = __half_as_ushort(__float2half_rn(val[e]));
+    row[5 + 4 * k + 2 * j] = static_cast<uint8_t>(hv);
+    row[5 + 4 * k + 2 * j + 1] = static_cast<uint8_t>(hv >> 8);
+  }
+}
+
 int grid_for(int64_t work) {
   int64_t g = (work + kNT - 1) / kNT;
   if (g > 148 * 16) g = 148 * 16;
@@ -355,7 +674,7 @@ extern "C" {
 
 int64_t gc_topk_workspace_bytes(int32_t workers, int64_t len) {
   const int64_t tiles = (len + kTileE - 1) / kTileE;
-  return ws_bytes(workers, tiles);
+  return ws_bytes(workers, tiles, len);
 }
 
 int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld, int64_t k, const float *grads,
@@ -367,23 +686,36 @@ int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld
   GC_REQUIRE(workspace && idx_out && (values || grads), "null argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t tiles = (len + kTileE - 1) / kTileE;
-  Work wk = carve(workspace, workers, tiles);
+  Work wk = carve(workspace, workers, tiles, len);
   const dim3 grid(static_cast<unsigned>(tiles), workers);
+  const float *src = grads ? grads : values;
+  const bool vec = (ld % 4) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(resid)) & 15) == 0;
   init_kernel<<<grid_for(2048 * workers), kNT, 0, st>>>(wk, workers, k);
   GC_LAUNCH_CHECK("init_kernel");
-  // level 0 (optionally fused with ef_apply: values then live in resid, or in grads if EF is off)
-  hist_kernel<<<grid, kNT, 0, st>>>(wk, 0, len, values, ld, grads, resid);
+  // pass 1: level 0 (optionally fused with ef_apply: values then live in resid, or in grads if EF is off)
+  if (vec)
+    hist0_vec_kernel<<<grid, kNT, 0, st>>>(wk, len, values, ld, grads, resid);
+  else
+    hist_kernel<<<grid, kNT, 0, st>>>(wk, 0, len, values, ld, grads, resid);
   GC_LAUNCH_CHECK("hist_kernel");
   const float *vals = values ? values : (resid ? resid : grads);
+  const int vec_vals = (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
   find_kernel<<<workers, 1024, 0, st>>>(wk, 0);
+  // pass 2: tile counts above the boundary bin + the boundary bin's candidates
+  collect_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles, vec_vals);
+  const dim3 cgrid(static_cast<unsigned>(tiles < 4 * 148 ? tiles : 4 * 148), workers);
   for (int level = 1; level <= 2; ++level) {
-    hist_kernel<<<grid, kNT, 0, st>>>(wk, level, len, vals, ld, nullptr, nullptr);
+    cand_hist_kernel<<<cgrid, kNT, 0, st>>>(wk, level, len, vals, ld);
     find_kernel<<<workers, 1024, 0, st>>>(wk, level);
   }
   GC_LAUNCH_CHECK("radix select");
-  tile_count_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles);
+  cand_tile_kernel<<<cgrid, kNT, 0, st>>>(wk, len, vals, ld, tiles);
   tile_scan_kernel<<<workers, 1024, 0, st>>>(wk, tiles);
-  write_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles, k, idx_out, val_out, fp16_vals);
+  // pass 3: ordered emission
+  if (vec_vals)
+    write_vec_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles, k, idx_out, val_out, fp16_vals);
+  else
+    write_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles, k, idx_out, val_out, fp16_vals);
   GC_LAUNCH_CHECK("topk write");
   return GC_OK;
 }
@@ -397,6 +729,22 @@ int gc_sparse_accumulate(int32_t workers, int64_t k, const int32_t *idx, const f
     scatter_add_kernel<<<grid_for(k), kNT, 0, st>>>(k, idx + w * k, val + w * k, estimate);
   }
   GC_LAUNCH_CHECK("scatter_add_kernel");
+  return GC_OK;
+}
+
+int gc_encode_sparse_payloads(int32_t workers, int64_t k, const int32_t *idx, const float *val, uint8_t *out,
+                              int64_t stride, void *stream) {
+  GC_REQUIRE(workers >= 1 && k >= 0 && k <= 0xffffffffll && idx && val && out && stride >= 5 + 6 * k,
+             "invalid argument");
+  const int64_t total = static_cast<int64_t>(workers) * (k > 0 ? k : 1);
+  if (k == 0) {   // header only: <B 1><I 0>
+    cudaMemsetAsync(out, 0, static_cast<size_t>(stride) * workers, static_cast<cudaStream_t>(stream));
+    for (int w = 0; w < workers; ++w) cudaMemsetAsync(out + w * stride, 1, 1, static_cast<cudaStream_t>(stream));
+    return GC_OK;
+  }
+  encode_sparse_kernel<<<grid_for(total), kNT, 0, static_cast<cudaStream_t>(stream)>>>(workers, k, idx, val, out,
+                                                                                      stride);
+  GC_LAUNCH_CHECK("encode_sparse_kernel");
   return GC_OK;
 }
 

@@ -70,3 +70,27 @@ def test_topk_gaussian_large():
     res = pipe.run_round(grads[0], 0)
     assert np.array_equal(res.estimate.logical, o["estimate"])
     assert np.array_equal(np.stack(pipe.residuals), np.stack(o["residuals"]))
+
+
+@pytest.mark.parametrize("kind", ["const", "few_values"])
+def test_topk_candidate_overflow_fallback(kind):
+    """The boundary radix bin holds far more than the candidate capacity (len / 16): the select
+    falls back to full-row passes and must still match the reference tie-break bit for bit."""
+    import paper_2407_01378_b200 as gcb
+    n, d, k = 2, 2_000_000, 20_000
+    rng = np.random.default_rng(9)
+    if kind == "const":
+        grads = [[np.full(d, 0.5, np.float32) for _ in range(n)] for _ in range(2)]
+    else:
+        grads = [[rng.choice(np.array([0.5, -0.5, 0.25, 3.0], np.float32), d, p=[0.45, 0.45, 0.0999, 0.0001])
+                  for _ in range(n)] for _ in range(2)]
+    outs = oracle_rounds("topk", dict(k=k), grads, 9)
+    pipe = gcb.make_pipeline(gcb.TopKConfig(k), n, d, gcb.SeedSpec(9))
+    pipe._engine.capture = True
+    for r in range(2):
+        res = pipe.run_round(grads[r], r)
+        idx = pipe._engine.last["idx"].cpu().numpy()
+        for w in range(n):
+            assert np.array_equal(idx[w], outs[r]["payloads"][w][0]), (r, w)
+        assert np.array_equal(res.estimate.logical, outs[r]["estimate"])
+        assert np.array_equal(np.stack(pipe.residuals), np.stack(outs[r]["residuals"]))

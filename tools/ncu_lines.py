@@ -23,8 +23,10 @@ for line in dis.split("\n"):
     if line.startswith(".text."):
         infn = want is None or want in line
         continue
-    m = re.search(r'line (\d+)', line) if "//##" in line else None
-    if m: cur = int(m.group(1)); continue
+    m = re.search(r'File "([^"]+)", line (\d+)', line) if "//##" in line else None
+    if m:   # attribute only lines of the source file asked for (headers map to -1)
+        cur = int(m.group(2)) if os.path.basename(m.group(1)) == os.path.basename(srcf) else -1
+        continue
     m2 = re.search(r'/\*([0-9a-f]{4,})\*/', line)
     if m2 and cur and infn: lm[int(m2.group(1), 16)] = cur
 ci = collections.Counter(); cs = collections.Counter()

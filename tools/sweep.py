@@ -26,9 +26,22 @@ def main():
     ap.add_argument("--n", type=int, default=8)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--only", default="")
+    ap.add_argument("--dims", default="", help="cfg5: comma list of d (e.g. 1048576,...,1e9); every scheme at each d")
     a = ap.parse_args()
     n = a.n
-    cases = [
+    if a.dims:
+        dims = [int(float(x)) for x in a.dims.split(",")]
+        cases = []
+        for d in dims:
+            cases += [(f"thc_q4b8_d{d}", gcb.RotatedQuantConfig(4, 8), d),
+                      (f"thc_q4b4_d{d}", gcb.RotatedQuantConfig(4, 4), d),
+                      (f"topk_1pct_d{d}", gcb.TopKConfig(max(1, d // 100)), d),
+                      (f"topkc_1pct_d{d}", gcb.ChunkedTopKConfig(64, max(1, d // 6400)), d),
+                      (f"powersgd_r4_d{d}", gcb.PowerSgdConfig(4), d),
+                      (f"dense16_d{d}", gcb.DenseConfig(16), d),
+                      (f"dense32_d{d}", gcb.DenseConfig(32), d)]
+    else:
+      cases = [
         ("thc_q4b8_cfg2", gcb.RotatedQuantConfig(4, 8), 25_557_032),
         ("thc_q4b4_cfg2", gcb.RotatedQuantConfig(4, 4), 25_557_032),
         ("topk_1pct_cfg3", gcb.TopKConfig(1_100_000), 110_000_000),
