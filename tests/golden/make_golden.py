@@ -137,11 +137,43 @@ def chunk_norm_vectors():
     print("chunk norms ok")
 
 
+def payload_vectors():
+    """Reference encode_payload bytes (compressors.py:292-325) for one payload of every type,
+    built with the reference codec functions on seeded data."""
+    rng = np.random.default_rng(77)
+    x = rng.standard_normal(5000).astype(np.float32)
+    x[:3] = 1e6   # fp16 saturation in the sparse values
+    sp = comp.topk_compress(x, 200)
+    ids = comp.select_chunks(np.abs(x[:4992].reshape(-1, 64)).sum(axis=1).astype(np.float32), 5)
+    cs = comp.chunk_values(x, 64, ids)
+    xr = x[:4096].astype(np.float32)
+    ranges = comp.chunk_ranges(xr, 1024)
+    codes, _ = comp.quantize_stochastic(xr, ranges, 4, SeedSpec(1).rng("stochastic-round", 0, 0))
+    qp = comp.QuantPayload(codes, ranges, 0xDEADBEEFCAFE, 4, 1024)
+    lr = comp.LowRankPayload(rng.standard_normal((30, 3)).astype(np.float32),
+                             rng.standard_normal((20, 3)).astype(np.float32), (30, 20))
+    d16 = comp.DensePayload(x[:100], 16)
+    d32 = comp.DensePayload(x[:100], 32)
+    out = {}
+    for name, pl in (("sparse", sp), ("chunkset", cs), ("quant", qp), ("lowrank", lr), ("dense16", d16),
+                     ("dense32", d32)):
+        out[f"{name}_bytes"] = np.frombuffer(comp.encode_payload(pl), dtype=np.uint8)
+        out[f"{name}_bits"] = np.array(comp.payload_bits(pl), dtype=np.int64)
+    out["sparse_idx"], out["sparse_val"] = sp.indices, sp.values
+    out["chunk_ids"], out["chunk_vals"] = cs.chunk_ids, cs.values
+    out["quant_codes"], out["quant_ranges"] = qp.codes, qp.ranges
+    out["lr_left"], out["lr_right"] = lr.left, lr.right
+    out["dense_vals"] = x[:100]
+    np.savez_compressed(os.path.join(OUT, "payloads.npz"), **out)
+    print("payloads ok")
+
+
 def main():
     gauss = lambda rng, d, w: rng.standard_normal(d).astype(np.float32)  # noqa: E731
     quart = lambda rng, d, w: quarters(rng, d)  # noqa: E731
     seed_vectors()
     chunk_norm_vectors()
+    payload_vectors()
     thc_intermediates("thc_steps_a", 3, 3000, 1234, 0, 4, 4, 256)
     thc_intermediates("thc_steps_b", 4, 4096, 99, 2, 4, 8, 1024)
     thc_intermediates("thc_steps_c", 5, 20000, 5, 1, 3, 6, 1 << 15)
