@@ -5,10 +5,10 @@
 NVCC     ?= /usr/local/cuda/bin/nvcc
 PKG      := paper_2407_01378_b200
 SRC      := $(PKG)/csrc
-OBJDIR   := build/obj
-LIB      := $(PKG)/libgradcomp_b200.so
+OBJDIR   ?= build/obj
+LIB      ?= $(PKG)/libgradcomp_b200.so
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC) -Xptxas -v
+NVFLAGS  := $(ARCH) $(EXTRA) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC) -Xptxas -v
 EXACT    := -fmad=false
 
 CU_EXACT := gc_thc.cu gc_thc_fused.cu gc_util.cu gc_dense.cu gc_topk.cu gc_chunk.cu

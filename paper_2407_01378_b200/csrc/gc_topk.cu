@@ -656,7 +656,10 @@ __global__ void encode_sparse_kernel(int L, int64_t k, const int32_t *idx, const
     }
     const uint32_t iv = static_cast<uint32_t>(idx[e]);
     for (int b = 0; b < 4; ++b) row[5 + 4 * j + b] = static_cast<uint8_t>(iv >> (8 * b));
-    const unsigned short hv = __half_as_ushort(__float2half_rn(val[e]));
+    // fp16 bits straight from cvt: nvcc 12.9 folds uint8_t(__half_as_ushort(h)) into a saturating
+    // F2I.U8.F16 *value* conversion (also from a 16-bit cvt result), so the low byte would come out as 0 / 255
+    uint32_t hv;   // packed cvt: fp16(val) in the low half of a 32-bit register
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hv) : "f"(0.0f), "f"(val[e]));
     row[5 + 4 * k + 2 * j] = static_cast<uint8_t>(hv);
     row[5 + 4 * k + 2 * j + 1] = static_cast<uint8_t>(hv >> 8);
   }

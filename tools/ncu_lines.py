@@ -20,8 +20,8 @@ for cubin in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):   # a .
 # map function name -> address->line
 lm = {}; cur = None; infn = False
 for line in dis.split("\n"):
-    if line.startswith(".text."):
-        infn = want is None or want in line
+    if line.startswith(".text."):   # FN (env) narrows to one template instance's mangled name
+        infn = (want is None or want in line) and os.environ.get("FN", "") in line
         continue
     m = re.search(r'File "([^"]+)", line (\d+)', line) if "//##" in line else None
     if m:   # attribute only lines of the source file asked for (headers map to -1)

@@ -20,7 +20,7 @@ lines() {  # name, kernel regex, source file, cmd...  -> per-source-line shares 
   local name=$1 kre=$2 src=$3; shift 3
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$kre -c 1 \
       -o /tmp/prof/${tag}_${name}_one -f "$@" > /dev/null 2>&1
-  python tools/ncu_lines.py /tmp/prof/${tag}_${name}_one.ncu-rep paper_2407_01378_b200/libgradcomp_b200.so \
+  FN=${FN:-} python tools/ncu_lines.py /tmp/prof/${tag}_${name}_one.ncu-rep paper_2407_01378_b200/libgradcomp_b200.so \
       $src $kre > $out/${tag}_${name}_lines.txt 2>&1
 }
 for s in $schemes; do

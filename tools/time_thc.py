@@ -6,7 +6,7 @@ import paper_2407_01378_b200 as gcb
 
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 25_557_032
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-for fused in (True, False):
+for fused in ((True,) if os.environ.get("FUSED_ONLY") else (True, False)):
     for q, b in ((4, 8), (4, 4)):
         g = torch.randn(n, d, device="cuda")
         pipe = gcb.make_pipeline(gcb.RotatedQuantConfig(q, b), n, d, gcb.SeedSpec(2024), fused=fused, validate=False,
