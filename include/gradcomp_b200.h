@@ -161,12 +161,19 @@ int gc_fp16_round(int64_t len, const float *in, float *out, void *stream);
 /* ---------------------------------------------------------------- TopK
  * topk_indices / topk_compress (compressors.py:387-403): per row, the k largest |x| with the
  * lower index winning ties, emitted in ascending index order (idx_out [L][k] int32) with the
- * values (val_out [L][k], optional; fp16-rounded when fp16_vals != 0).
+ * values (val_out [L][k], optional; fp16-rounded with GC_TOPK_FP16_VALUES).
  * Values come from `values`, or when values is NULL from grads (+ resid): with resid != NULL the
- * selection is fused with ef_apply and the corrected vector f32(g + r) is written over resid. */
+ * selection is fused with ef_apply and the corrected vector f32(g + r) is written over resid.
+ * GC_TOPK_EF_UPDATE (needs grads + resid) also applies ef_update in place (compressors.py:629-631:
+ * resid[i] -= val at the selected i), so resid leaves as r_new and gc_sparse_ef_update is not needed.
+ * The workspace carries the previous call's boundary radix bin as a hint (zero it before first use;
+ * any content is safe): when a call's boundary bin is at or above (hint - 1), the candidate
+ * collection rides on the level-0 pass and the second full-row pass is skipped. */
+#define GC_TOPK_FP16_VALUES 1
+#define GC_TOPK_EF_UPDATE 2
 int64_t gc_topk_workspace_bytes(int32_t workers, int64_t len);
 int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld, int64_t k, const float *grads,
-                   float *resid, int32_t *idx_out, float *val_out, int32_t fp16_vals, void *workspace,
+                   float *resid, int32_t *idx_out, float *val_out, int32_t flags, void *workspace,
                    void *stream);
 /* TopK aggregation (pipelines.py:206-209): estimate = 0; estimate[idx_w] += val_w for w in
  * worker order (f32, the np.add.at order).  Dividing by n is gc_scale_div. */

@@ -18,6 +18,10 @@ GC_ERR_INVALID = -1
 GC_ERR_CUDA = -2
 GC_ERR_UNSUPPORTED = -3
 
+# gc_topk_select flags (include/gradcomp_b200.h)
+TOPK_FP16_VALUES = 1
+TOPK_EF_UPDATE = 2
+
 
 class Pcg64(ctypes.Structure):
     """gc_pcg64: numpy PCG64 state (128-bit state and increment)."""

@@ -67,9 +67,19 @@ __global__ void __launch_bounds__(kNT) segment_fold_kernel(int n, const int64_t 
 }
 
 __global__ void scale_div_kernel(int64_t len, const float *in, int divisor, float *out) {
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < len;
+  const float dv = static_cast<float>(divisor);
+  int64_t head = 0;
+  if (((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {   // float4 body
+    head = len & ~int64_t{3};
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; 4 * e < head;
+         e += static_cast<int64_t>(gridDim.x) * kNT) {
+      const float4 v = __ldcs(reinterpret_cast<const float4 *>(in) + e);
+      __stcs(reinterpret_cast<float4 *>(out) + e, make_float4(v.x / dv, v.y / dv, v.z / dv, v.w / dv));
+    }
+  }
+  for (int64_t e = head + blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < len;
        e += static_cast<int64_t>(gridDim.x) * kNT)
-    out[e] = in[e] / static_cast<float>(divisor);
+    out[e] = in[e] / dv;
 }
 
 __global__ void fp16_round_kernel(int64_t len, const float *in, float *out) {

@@ -347,20 +347,12 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
     }
     __syncthreads();
     if (col < cols) {
+      // rows whose 4 columns all lie below d load without per-row checks, so the unrolled loads
+      // of a fold group are all in flight together (a per-row branch serialised them)
+      const bool full = (i0 + ni - 1) * cols + col + 3 < d;
       for (int g0 = 0; g0 < ni; g0 += kMtpFold) {
         const int g1 = min(ni, g0 + kMtpFold);
-#pragma unroll 8
-        for (int ii = g0; ii < g1; ++ii) {
-          const int64_t i = (i0 + ii) * cols + col;
-          float4 m;
-          if (i + 3 < d) {
-            m = __ldcs(reinterpret_cast<const float4 *>(cw + i));
-          } else {
-            float t4[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int t = 0; t < 4; ++t)
-              if (i + t < d) t4[t] = cw[i + t];
-            m = make_float4(t4[0], t4[1], t4[2], t4[3]);
-          }
+        auto row_fma = [&](int ii, const float4 m) {
           const float m4[4] = {m.x, m.y, m.z, m.w};
           float pv[RP];
 #pragma unroll
@@ -372,6 +364,27 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
           for (int t = 0; t < 4; ++t)
 #pragma unroll
             for (int b = 0; b < R; ++b) a32[t][b] = fmaf(m4[t], pv[b], a32[t][b]);
+        };
+        if (full && g1 - g0 == kMtpFold) {
+          // branch-free group: all kMtpFold row loads are independent and issue back to back
+          const float *src = cw + (i0 + g0) * cols + col;
+#pragma unroll 8
+          for (int ii = 0; ii < kMtpFold; ++ii)
+            row_fma(g0 + ii, __ldcs(reinterpret_cast<const float4 *>(src + ii * cols)));
+        } else {
+          for (int ii = g0; ii < g1; ++ii) {
+            const int64_t i = (i0 + ii) * cols + col;
+            float4 m;
+            if (i + 3 < d) {
+              m = __ldcs(reinterpret_cast<const float4 *>(cw + i));
+            } else {
+              float t4[4] = {0.f, 0.f, 0.f, 0.f};
+              for (int t = 0; t < 4; ++t)
+                if (i + t < d) t4[t] = cw[i + t];
+              m = make_float4(t4[0], t4[1], t4[2], t4[3]);
+            }
+            row_fma(ii, m);
+          }
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t)
@@ -425,6 +438,42 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
     if (w < L && !resid) continue;
     if (w == L && !est) continue;
     float *dst = w < L ? resid + rw_.at(blockIdx.z * L + w) : est;
+    if ((row0 + nrows - 1) * cols + col + 3 < d) {   // whole block in range: branch-free
+      // rows go in batches of 8: the 8 loads of c are issued before any store (the compiler
+      // cannot prove that a store to row a does not alias the load of row a + 1)
+      const float nf = static_cast<float>(n);
+      for (int a0 = 0; a0 < nrows; a0 += 8) {
+        const int nb = min(8, nrows - a0);
+        float4 cv[8];
+        if (w < L) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (u < nb) cv[u] = __ldcs(reinterpret_cast<const float4 *>(dst + (row0 + a0 + u) * cols + col));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (u >= nb) break;
+          const int a = a0 + u;
+          float o4[4];
+          float pa[R];
+#pragma unroll
+          for (int b = 0; b < R; ++b) pa[b] = ps[a * R + b];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            float v = pa[0] * qv[t][0];
+#pragma unroll
+            for (int b = 1; b < R; ++b) v = fmaf(pa[b], qv[t][b], v);
+            o4[t] = v;
+          }
+          float4 *o = reinterpret_cast<float4 *>(dst + (row0 + a) * cols + col);
+          if (w < L)
+            __stcs(o, make_float4(cv[u].x - o4[0], cv[u].y - o4[1], cv[u].z - o4[2], cv[u].w - o4[3]));
+          else
+            __stcs(o, make_float4(o4[0] / nf, o4[1] / nf, o4[2] / nf, o4[3] / nf));
+        }
+      }
+      continue;
+    }
 #pragma unroll 8
     for (int a = 0; a < nrows; ++a) {
       const int64_t i = (row0 + a) * cols + col;

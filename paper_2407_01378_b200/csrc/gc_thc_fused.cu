@@ -35,9 +35,14 @@
 #include "gc_device.cuh"
 #include "gc_internal.h"
 
+#ifndef GC_THC_LOAD_BATCH
+#define GC_THC_LOAD_BATCH 2
+#endif
+
 namespace {
 
 constexpr int kTileN = 1024;
+constexpr int HALF = GC_THC_LOAD_BATCH;   // float4 loads of g (and r) in flight per batch
 constexpr int kMaxN = 16;
 constexpr int kLutMax = 256;   // doubles in the shared own-decode table
 
@@ -361,7 +366,32 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(kTileN * 4) : "memory");
       }
     }
-    // ---- corrected = f32(g + r) (compressors.py:624-626), coalesced loads -> cbuf
+    // ---- corrected = f32(g + r) (compressors.py:624-626), coalesced loads -> cbuf.  Full
+    // aligned tiles issue all 16 float4 loads before the first add, so the tile start pays one
+    // memory latency instead of eight (per-iteration bounds checks kept them serialised).
+    if (a.aligned && t0 + kTileN <= a.dim) {
+#pragma unroll
+      for (int h = 0; h < 8; h += HALF) {
+        float4 gv[HALF], rv[HALF];
+#pragma unroll
+        for (int m = 0; m < HALF; ++m)
+          gv[m] = __ldcs(reinterpret_cast<const float4 *>(gw + t0 + (lane + 32 * (h + m)) * 4));
+        if (rw) {
+#pragma unroll
+          for (int m = 0; m < HALF; ++m)
+            rv[m] = __ldcs(reinterpret_cast<const float4 *>(rw + t0 + (lane + 32 * (h + m)) * 4));
+#pragma unroll
+          for (int m = 0; m < HALF; ++m) {
+            gv[m].x = gv[m].x + rv[m].x;
+            gv[m].y = gv[m].y + rv[m].y;
+            gv[m].z = gv[m].z + rv[m].z;
+            gv[m].w = gv[m].w + rv[m].w;
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < HALF; ++m) *reinterpret_cast<float4 *>(cbuf + cidx((lane + 32 * (h + m)) * 4)) = gv[m];
+      }
+    } else
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const int e4 = (lane + 32 * m) * 4;

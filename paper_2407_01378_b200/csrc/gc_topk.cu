@@ -14,10 +14,14 @@
 //      the boundary bin's elements appended (key, index) to a per-worker candidate list
 //      (warp-aggregated atomics; typically < 1 % of the row) -- levels 1 and 2 and the tie
 //      counts then run on the candidates only;
-//   3. write: per tile, offsets from a scan of the (above, tie) counts; indices are emitted in
-//      ascending order with warp ballots, so no sort is needed.
-// If the boundary bin overflows the candidate capacity (degenerate inputs, e.g. a constant
-// row) the select falls back to full-row passes for levels 1-2 and the tile counts.  Every
+//   3. write: per tile, offsets from a scan of the (above, tie) counts.  The collect pass
+//      also appends every key above the boundary bin, so the candidate list holds all
+//      selected elements (raw f32 bits + index) in per-tile segments: the write pass reads
+//      only those segments (~ k + boundary-bin entries, not the row) and ranks each entry by
+//      index with two 4096-bit tile bitmaps (selected, ties), so no sort is needed.
+// If the candidates overflow the capacity (k above ~len/16, or degenerate inputs such as a
+// constant row) the select falls back to full-row passes for levels 1-2, the tile counts
+// and the write (ascending emission with warp ballots over the row).  Every
 // count is an integer sum, so the result does not depend on the atomic order.  All L rows
 // (workers) run in the same launches (grid.y = worker).
 #include <cub/block/block_reduce.cuh>
@@ -34,15 +38,19 @@ constexpr int kNT = 256;
 constexpr int kTileE = 4096;          // elements per tile (8 warps x 16 steps x 32 lanes)
 constexpr int kSteps = kTileE / kNT;  // 16
 
+constexpr unsigned int kNoGuess = 0xFFFFFFFFu;
+
 struct RowState {  // per worker, lives in the workspace
   unsigned int prefix;     // key bits fixed so far
-  unsigned int pad;
+  unsigned int hint;       // persists across calls: 1 + the previous call's level-0 boundary bin (0: none)
   long long k_rem;         // elements still to take at the current level
   long long gt;            // elements strictly above the current prefix
   unsigned int thresh;     // final threshold key T
-  unsigned int pad2;
+  unsigned int guess;      // candidate floor bin of pass 1 (kNoGuess: pass 1 collects nothing)
   long long take_eq;       // m: number of T-keyed elements taken (lowest indices)
-  unsigned long long cand_count;   // boundary-bin elements collected (may exceed the capacity)
+  unsigned long long cand_count;   // candidates appended (may exceed the capacity)
+  int spec_ok;             // pass 1's candidates are complete: the collect pass is skipped
+  int pad;
 };
 
 struct Work {
@@ -52,8 +60,10 @@ struct Work {
   unsigned int *tile_eq;        // [L][tiles]
   long long *tile_sel_off;      // [L][tiles]
   long long *tile_eq_off;       // [L][tiles]
-  unsigned int *cand_key;       // [L][cap]
+  unsigned int *cand_key;       // [L][cap]  raw f32 bits of the candidate (sign kept for the value)
   unsigned int *cand_idx;       // [L][cap]
+  unsigned long long *tile_cbase;   // [L][tiles] first candidate slot of the tile's segment
+  unsigned int *tile_ccnt;      // [L][tiles] candidates the tile appended
   int64_t cap;
 };
 
@@ -79,6 +89,10 @@ __host__ __device__ inline Work carve(void *ws, int L, int64_t tiles, int64_t le
   p += align256(int64_t{8} * tiles * L);
   w.tile_eq_off = reinterpret_cast<long long *>(p);
   p += align256(int64_t{8} * tiles * L);
+  w.tile_cbase = reinterpret_cast<unsigned long long *>(p);
+  p += align256(int64_t{8} * tiles * L);
+  w.tile_ccnt = reinterpret_cast<unsigned int *>(p);
+  p += align256(int64_t{4} * tiles * L);
   w.cap = cand_cap_for(len);
   w.cand_key = reinterpret_cast<unsigned int *>(p);
   p += align256(int64_t{4} * w.cap * L);
@@ -87,8 +101,8 @@ __host__ __device__ inline Work carve(void *ws, int L, int64_t tiles, int64_t le
 }
 
 int64_t ws_bytes(int L, int64_t tiles, int64_t len) {
-  return align256(sizeof(RowState) * L) + align256(int64_t{4} * 2048 * L) + 2 * align256(int64_t{4} * tiles * L) +
-         2 * align256(int64_t{8} * tiles * L) + 2 * align256(int64_t{4} * cand_cap_for(len) * L);
+  return align256(sizeof(RowState) * L) + align256(int64_t{4} * 2048 * L) + 3 * align256(int64_t{4} * tiles * L) +
+         3 * align256(int64_t{8} * tiles * L) + 2 * align256(int64_t{4} * cand_cap_for(len) * L);
 }
 
 __device__ __forceinline__ unsigned int key_of(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
@@ -101,10 +115,15 @@ __device__ __forceinline__ int bin_of(unsigned int key, int level, unsigned int 
   return (key >> 10) == prefix ? static_cast<int>(key & 1023u) : -1;
 }
 
-__global__ void __launch_bounds__(kNT) init_kernel(Work wk, int L, int64_t k) {
+__global__ void __launch_bounds__(kNT) init_kernel(Work wk, int L, int64_t k, int speculate) {
   for (int i = blockIdx.x * kNT + threadIdx.x; i < 2048 * L; i += gridDim.x * kNT) wk.hist[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x < L) {
-    RowState &s = wk.state[threadIdx.x];
+  for (int r = blockIdx.x * kNT + threadIdx.x; r < L; r += gridDim.x * kNT) {
+    RowState &s = wk.state[r];
+    // pass 1 collects the bins >= (previous boundary bin - 1): in steady EF rounds the new
+    // boundary bin is at or above it, so the collect pass is skipped (verified on the device)
+    const unsigned int h = s.hint;
+    s.guess = !speculate ? kNoGuess : ((h >= 2 && h <= 2048) ? h - 2 : (h == 1 ? 0u : kNoGuess));
+    s.spec_ok = 0;
     s.prefix = 0;
     s.k_rem = k;
     s.gt = 0;
@@ -145,102 +164,12 @@ __global__ void __launch_bounds__(kNT) hist_kernel(Work wk, int level, int64_t l
     if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
 }
 
-// Level 0 with float4 loads (aligned rows): a thread's 16 elements are 4 float4 at stride
-// 256, all loads issued before the shared-memory atomics.  grads != NULL fuses ef_apply.
-__global__ void __launch_bounds__(kNT) hist0_vec_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
-                                                        const float *grads, float *resid) {
-  __shared__ unsigned int h[2048];
-  const int w = blockIdx.y;
-  for (int i = threadIdx.x; i < 2048; i += kNT) h[i] = 0;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
-  float4 x[4];
-  const bool full = base + kTileE <= len;
-  if (full) {
-    const float *src = grads ? grads + w * ld : vals + w * ld;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = __ldcs(reinterpret_cast<const float4 *>(src + base) + threadIdx.x + kNT * u);
-    if (grads && resid) {
-      float4 *rr = reinterpret_cast<float4 *>(resid + w * ld + base);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float4 r4 = rr[threadIdx.x + kNT * u];
-        x[u].x = x[u].x + r4.x; x[u].y = x[u].y + r4.y; x[u].z = x[u].z + r4.z; x[u].w = x[u].w + r4.w;
-        rr[threadIdx.x + kNT * u] = x[u];
-      }
-    }
-  }
-  __syncthreads();
-  if (full) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      atomicAdd(&h[key_of(x[u].x) >> 20], 1u);
-      atomicAdd(&h[key_of(x[u].y) >> 20], 1u);
-      atomicAdd(&h[key_of(x[u].z) >> 20], 1u);
-      atomicAdd(&h[key_of(x[u].w) >> 20], 1u);
-    }
-  } else {
-    for (int64_t i = base + threadIdx.x; i < len; i += kNT) {
-      float v;
-      if (grads) {
-        v = grads[w * ld + i];
-        if (resid) {
-          v = v + resid[w * ld + i];
-          resid[w * ld + i] = v;
-        }
-      } else {
-        v = vals[w * ld + i];
-      }
-      atomicAdd(&h[key_of(v) >> 20], 1u);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 2048; i += kNT)
-    if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
-}
-
-// Pass 2: per tile, count keys above the level-0 boundary bin p0 (tile_gt) and append the
-// boundary bin's (key, index) to the worker's candidate list; tile_eq starts at 0.  Slots are
-// reserved with one global atomic per CTA (warp scans + a CTA prefix), not per warp: the
-// per-warp version serialised on the worker's counter.
-__global__ void __launch_bounds__(kNT) collect_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
-                                                      int64_t tiles, int vec) {
-  __shared__ unsigned int s_wcnt[kNT / 32];
-  __shared__ unsigned long long s_base;
-  const int w = blockIdx.y;
-  RowState &st = wk.state[w];
-  const unsigned int p0 = st.prefix;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
-  const float *row = vals + w * ld;
+// Reserve `mine` consecutive candidate slots per thread for a CTA (warp scans, one global atomic
+// per CTA) and return the thread's first slot; the CTA's segment base / size go to the tile.
+__device__ __forceinline__ unsigned long long reserve_slots(unsigned int mine, RowState &st, unsigned int *s_wcnt,
+                                                            unsigned long long *s_base, unsigned int *s_tot,
+                                                            unsigned long long *tile_cbase, unsigned int *tile_ccnt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned int keys[kSteps];
-  unsigned int cmask = 0, gt = 0;
-  const bool full_vec = vec && base + kTileE <= len;
-  if (full_vec) {   // element 4 * (tid + 256u) + q  <->  keys[4u + q]
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float4 x = __ldcs(reinterpret_cast<const float4 *>(row + base) + threadIdx.x + kNT * u);
-      keys[4 * u + 0] = key_of(x.x);
-      keys[4 * u + 1] = key_of(x.y);
-      keys[4 * u + 2] = key_of(x.z);
-      keys[4 * u + 3] = key_of(x.w);
-    }
-  } else {          // element s * 256 + tid  <->  keys[s]
-#pragma unroll
-    for (int s = 0; s < kSteps; ++s) {
-      const int64_t i = base + s * kNT + threadIdx.x;
-      keys[s] = i < len ? key_of(row[i]) : 0u;
-    }
-  }
-#pragma unroll
-  for (int s = 0; s < kSteps; ++s) {
-    const int64_t i = full_vec ? base + 4 * (threadIdx.x + kNT * (s >> 2)) + (s & 3) : base + s * kNT + threadIdx.x;
-    const bool valid = i < len;
-    const unsigned int b0 = keys[s] >> 20;
-    gt += valid && b0 > p0;
-    cmask |= (valid && b0 == p0) ? (1u << s) : 0u;
-  }
-  // slot reservation: warp-inclusive scan of the per-thread candidate counts, CTA prefix
-  const unsigned int mine = __popc(cmask);
   unsigned int incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -256,28 +185,152 @@ __global__ void __launch_bounds__(kNT) collect_kernel(Work wk, int64_t len, cons
       s_wcnt[j] = tot;
       tot += c;
     }
-    s_base = tot ? atomicAdd(&st.cand_count, static_cast<unsigned long long>(tot)) : 0ull;
+    const unsigned long long b = tot ? atomicAdd(&st.cand_count, static_cast<unsigned long long>(tot)) : 0ull;
+    *s_base = b;
+    *s_tot = tot;
+    *tile_cbase = b;
+    *tile_ccnt = tot;
   }
   __syncthreads();
-  if (cmask) {
-    unsigned long long pos = s_base + s_wcnt[warp] + (incl - mine);
+  return *s_base + s_wcnt[warp] + (incl - mine);
+}
+
+// Level 0 with float4 loads (aligned rows): a thread's 16 elements are 4 float4 at stride
+// 256 (element 4 * (tid + 256u) + q), all loads issued before the shared-memory atomics.
+// grads != NULL fuses ef_apply.  With a guess bin from the previous call, elements in bins >=
+// guess are appended to the candidate list as the tile's segment (pass 2 then only runs if the
+// guess turns out above the new boundary bin).
+__global__ void __launch_bounds__(kNT) hist0_vec_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
+                                                        const float *grads, float *resid, int64_t tiles) {
+  __shared__ unsigned int h[2048];
+  __shared__ unsigned int s_wcnt[kNT / 32];
+  __shared__ unsigned long long s_base;
+  __shared__ unsigned int s_tot;
+  const int w = blockIdx.y;
+  RowState &st = wk.state[w];
+  const unsigned int guess = st.guess;
+  for (int i = threadIdx.x; i < 2048; i += kNT) h[i] = 0;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
+  float4 x[4];
+  unsigned int valid = 0xFFFFu;
+  const float *src = grads ? grads + w * ld : vals + w * ld;
+  if (base + kTileE <= len) {
 #pragma unroll
-    for (int s = 0; s < kSteps; ++s)
-      if ((cmask >> s) & 1u) {
-        const int64_t i = full_vec ? base + 4 * (threadIdx.x + kNT * (s >> 2)) + (s & 3) : base + s * kNT + threadIdx.x;
-        if (pos < static_cast<unsigned long long>(wk.cap)) {
-          wk.cand_key[w * wk.cap + pos] = keys[s];
-          wk.cand_idx[w * wk.cap + pos] = static_cast<unsigned int>(i);
-        }
-        ++pos;
+    for (int u = 0; u < 4; ++u) x[u] = __ldcs(reinterpret_cast<const float4 *>(src + base) + threadIdx.x + kNT * u);
+    if (grads && resid) {
+      float4 *rr = reinterpret_cast<float4 *>(resid + w * ld + base);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 r4 = rr[threadIdx.x + kNT * u];
+        x[u].x = x[u].x + r4.x; x[u].y = x[u].y + r4.y; x[u].z = x[u].z + r4.z; x[u].w = x[u].w + r4.w;
+        rr[threadIdx.x + kNT * u] = x[u];
       }
+    }
+  } else {
+    valid = 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float t[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t i = base + 4 * (threadIdx.x + kNT * u) + q;
+        float v = 0.0f;
+        if (i < len) {
+          v = src[i];
+          if (grads && resid) {
+            v = v + resid[w * ld + i];
+            resid[w * ld + i] = v;
+          }
+          valid |= 1u << (4 * u + q);
+        }
+        t[q] = v;
+      }
+      x[u] = make_float4(t[0], t[1], t[2], t[3]);
+    }
   }
-  using R = cub::BlockReduce<unsigned int, kNT>;
-  __shared__ typename R::TempStorage t1;
-  const unsigned int sgt = R(t1).Sum(gt);
-  if (threadIdx.x == 0) {
-    wk.tile_gt[w * tiles + blockIdx.x] = sgt;
-    wk.tile_eq[w * tiles + blockIdx.x] = 0;
+  __syncthreads();
+  unsigned int bits[16];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    bits[4 * u] = __float_as_uint(x[u].x); bits[4 * u + 1] = __float_as_uint(x[u].y);
+    bits[4 * u + 2] = __float_as_uint(x[u].z); bits[4 * u + 3] = __float_as_uint(x[u].w);
+  }
+  unsigned int cmask = 0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const unsigned int b0 = (bits[e] & 0x7FFFFFFFu) >> 20;
+    if ((valid >> e) & 1u) {
+      atomicAdd(&h[b0], 1u);
+      cmask |= (b0 >= guess ? 1u : 0u) << e;
+    }
+  }
+  if (guess != kNoGuess) {   // grid-uniform
+    const unsigned int mine = __popc(cmask);
+    unsigned long long pos = reserve_slots(mine, st, s_wcnt, &s_base, &s_tot, &wk.tile_cbase[w * tiles + blockIdx.x],
+                                           &wk.tile_ccnt[w * tiles + blockIdx.x]);
+    while (cmask) {
+      const int e = __ffs(cmask) - 1;
+      cmask &= cmask - 1u;
+      if (pos < static_cast<unsigned long long>(wk.cap)) {
+        wk.cand_key[w * wk.cap + pos] = bits[e];
+        wk.cand_idx[w * wk.cap + pos] = static_cast<unsigned int>(base + 4 * (threadIdx.x + kNT * (e >> 2)) + (e & 3));
+      }
+      ++pos;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += kNT)
+    if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
+}
+
+// Pass 2 (skipped when pass 1's guess held): per tile, every element at or above the level-0
+// boundary bin p0 (raw bits, index) is appended to the worker's candidate list as the tile's
+// segment (tile_cbase / tile_ccnt).  Persistent CTAs walk the tiles.
+__global__ void __launch_bounds__(kNT) collect_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
+                                                      int64_t tiles, int vec) {
+  __shared__ unsigned int s_wcnt[kNT / 32];
+  __shared__ unsigned int s_tot;
+  __shared__ unsigned long long s_base;
+  const int w = blockIdx.y;
+  RowState &st = wk.state[w];
+  if (st.spec_ok) return;
+  const unsigned int p0 = st.prefix;
+  const float *row = vals + w * ld;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t base = tile * kTileE;
+    unsigned int keys[kSteps];   // raw f32 bits; element 4 * (tid + 256u) + q  <->  keys[4u + q]
+    unsigned int cmask = 0;
+    if (vec && base + kTileE <= len) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 x = __ldcs(reinterpret_cast<const float4 *>(row + base) + threadIdx.x + kNT * u);
+        keys[4 * u + 0] = __float_as_uint(x.x);
+        keys[4 * u + 1] = __float_as_uint(x.y);
+        keys[4 * u + 2] = __float_as_uint(x.z);
+        keys[4 * u + 3] = __float_as_uint(x.w);
+      }
+#pragma unroll
+      for (int e = 0; e < kSteps; ++e) cmask |= (((keys[e] & 0x7FFFFFFFu) >> 20) >= p0 ? 1u : 0u) << e;
+    } else {
+#pragma unroll
+      for (int e = 0; e < kSteps; ++e) {
+        const int64_t i = base + 4 * (threadIdx.x + kNT * (e >> 2)) + (e & 3);
+        keys[e] = i < len ? __float_as_uint(row[i]) : 0u;
+        cmask |= (i < len && ((keys[e] & 0x7FFFFFFFu) >> 20) >= p0 ? 1u : 0u) << e;
+      }
+    }
+    unsigned long long pos = reserve_slots(__popc(cmask), st, s_wcnt, &s_base, &s_tot,
+                                           &wk.tile_cbase[w * tiles + tile], &wk.tile_ccnt[w * tiles + tile]);
+    while (cmask) {
+      const int e = __ffs(cmask) - 1;
+      cmask &= cmask - 1u;
+      if (pos < static_cast<unsigned long long>(wk.cap)) {
+        wk.cand_key[w * wk.cap + pos] = keys[e];
+        wk.cand_idx[w * wk.cap + pos] = static_cast<unsigned int>(base + 4 * (threadIdx.x + kNT * (e >> 2)) + (e & 3));
+      }
+      ++pos;
+    }
+    __syncthreads();   // s_wcnt / s_base are reused by the next tile
   }
 }
 
@@ -295,7 +348,7 @@ __global__ void __launch_bounds__(kNT) cand_hist_kernel(Work wk, int level, int6
   if (nc <= wk.cap) {
     const unsigned int *ck = wk.cand_key + w * wk.cap;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < nc; e += stride) {
-      const int b = bin_of(ck[e], level, prefix);
+      const int b = bin_of(ck[e] & 0x7FFFFFFFu, level, prefix);
       if (b >= 0) atomicAdd(&h[b], 1u);
     }
   } else {
@@ -310,22 +363,35 @@ __global__ void __launch_bounds__(kNT) cand_hist_kernel(Work wk, int level, int6
     if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
 }
 
-// Tile counts of the candidates above / equal to T (tile_gt already holds the keys above the
-// boundary bin).  On overflow the counts are recomputed from the whole row.
+// Tile counts of the candidates above / equal to T: one warp per tile walks the tile's segment
+// (no atomics).  On overflow the counts come from the whole row.
 __global__ void __launch_bounds__(kNT) cand_tile_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
                                                         int64_t tiles) {
   const int w = blockIdx.y;
   const RowState &st = wk.state[w];
   const unsigned int T = st.thresh;
   const int64_t nc = static_cast<int64_t>(st.cand_count);
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * kNT;
   if (nc <= wk.cap) {
-    const unsigned int *ck = wk.cand_key + w * wk.cap, *ci = wk.cand_idx + w * wk.cap;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < nc; e += stride) {
-      const unsigned int key = ck[e];
-      if (key >= T) {
-        const int64_t t = ci[e] / kTileE;
-        atomicAdd(key > T ? &wk.tile_gt[w * tiles + t] : &wk.tile_eq[w * tiles + t], 1u);
+    const int lane = threadIdx.x & 31;
+    const unsigned int *ck = wk.cand_key + w * wk.cap;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(kNT / 32) + (threadIdx.x >> 5); t < tiles;
+         t += static_cast<int64_t>(gridDim.x) * (kNT / 32)) {
+      const unsigned long long cb = wk.tile_cbase[w * tiles + t];
+      const unsigned int cn = wk.tile_ccnt[w * tiles + t];
+      unsigned int gt = 0, eq = 0;
+      for (unsigned int e = lane; e < cn; e += 32) {
+        const unsigned int key = ck[cb + e] & 0x7FFFFFFFu;
+        gt += key > T;
+        eq += key == T;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        gt += __shfl_xor_sync(0xffffffffu, gt, o);
+        eq += __shfl_xor_sync(0xffffffffu, eq, o);
+      }
+      if (lane == 0) {
+        wk.tile_gt[w * tiles + t] = gt;
+        wk.tile_eq[w * tiles + t] = eq;
       }
     }
     return;
@@ -391,6 +457,12 @@ __global__ void __launch_bounds__(1024) find_kernel(Work wk, int level) {
     s.gt += static_cast<long long>(s_above);
     s.k_rem = static_cast<long long>(k_rem - s_above);
     s.prefix = (level == 0) ? b : ((s.prefix << 10) | b);
+    if (level == 0) {   // pass 1's candidates hold every bin >= guess: complete iff b >= guess
+      const bool ok = s.guess != kNoGuess && b >= s.guess && s.cand_count <= static_cast<unsigned long long>(wk.cap);
+      s.spec_ok = ok ? 1 : 0;
+      if (!ok) s.cand_count = 0;   // pass 2 rebuilds the list
+      s.hint = b + 1;
+    }
     if (level == 2) {
       s.thresh = s.prefix;
       s.take_eq = s.k_rem;
@@ -438,85 +510,94 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(Work wk, int64_t tiles)
 // 1 % density) costs one ballot.  Ties (key == T) are taken in index order up to m.
 __global__ void __launch_bounds__(kNT) write_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
                                                     int64_t tiles, int64_t k, int32_t *idx_out, float *val_out,
-                                                    int fp16_vals) {
+                                                    int fp16_vals, float *resid) {
   __shared__ unsigned int s_eq[kNT / 32], s_sel[kNT / 32];
-  const int w = blockIdx.y;
-  const unsigned int T = wk.state[w].thresh;
-  const long long m = wk.state[w].take_eq;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE + warp * (kSteps * 32);
-  const unsigned int lt_mask = (1u << lane) - 1u;
-  const float *row = vals + w * ld;
-  unsigned int keys[kSteps];
-  if (base + kSteps * 32 <= len) {
-#pragma unroll
-    for (int s = 0; s < kSteps; ++s) keys[s] = key_of(__ldcs(row + base + s * 32 + lane));
-  } else {
-#pragma unroll
-    for (int s = 0; s < kSteps; ++s) {
-      const int64_t i = base + s * 32 + lane;
-      keys[s] = i < len ? key_of(row[i]) : 0u;   // key 0 <= T: never selected past the end
-    }
-  }
-  // masks per group: ge (key >= T) and eq (key == T); padding lanes read key 0
-  unsigned int gem[kSteps], eqm[kSteps];
-  unsigned int eq_tot = 0;
-  const bool t_zero = T == 0u;
-#pragma unroll
-  for (int s = 0; s < kSteps; ++s) {
-    const bool valid = base + s * 32 + lane < len;
-    gem[s] = __ballot_sync(0xffffffffu, valid && keys[s] >= T);
-    eqm[s] = 0u;
-    if (gem[s]) {
-      eqm[s] = __ballot_sync(0xffffffffu, valid && keys[s] == T);
-      eq_tot += __popc(eqm[s]);
-    }
-  }
-  (void)t_zero;
-  if (lane == 0) s_eq[warp] = eq_tot;
-  __syncthreads();
-  long long eq_run = wk.tile_eq_off[w * tiles + blockIdx.x];
-  for (int j = 0; j < warp; ++j) eq_run += s_eq[j];
-  unsigned int sel_tot = 0;
-#pragma unroll
-  for (int s = 0; s < kSteps; ++s) {
-    unsigned int sm = gem[s] & ~eqm[s];   // strictly above T: always taken
-    if (eqm[s]) {
-      // ties: the first max(0, min(popc, m - eq_run)) set bits of eqm, in lane (= index) order
-      const long long room = m - eq_run;
-      const int take = room <= 0 ? 0 : (room >= 32 ? 32 : static_cast<int>(room));
-      unsigned int e = eqm[s];
-      for (int t = 0; t < take && e; ++t) {
-        const unsigned int lowbit = e & (0u - e);
-        sm |= lowbit;
-        e ^= lowbit;
-      }
-      eq_run += __popc(eqm[s]);
-    }
-    gem[s] = sm;   // reuse as the selected mask
-    sel_tot += __popc(sm);
-  }
-  if (lane == 0) s_sel[warp] = sel_tot;
-  __syncthreads();
-  long long out = wk.tile_sel_off[w * tiles + blockIdx.x];
-  for (int j = 0; j < warp; ++j) out += s_sel[j];
-#pragma unroll
-  for (int s = 0; s < kSteps; ++s) {
-    const unsigned int sm = gem[s];
-    if (sm) {
-      if ((sm >> lane) & 1u) {
-        const long long pos = out + __popc(sm & lt_mask);
+  // fallback only: the candidate write (cand_write_kernel) covers every row that fit the list
+  if (wk.state[blockIdx.y].cand_count <= static_cast<unsigned long long>(wk.cap)) return;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int w = blockIdx.y;
+    const unsigned int T = wk.state[w].thresh;
+    const long long m = wk.state[w].take_eq;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t base = static_cast<int64_t>(tile) * kTileE + warp * (kSteps * 32);
+    const unsigned int lt_mask = (1u << lane) - 1u;
+    const float *row = vals + w * ld;
+    unsigned int keys[kSteps];
+    if (base + kSteps * 32 <= len) {
+  #pragma unroll
+      for (int s = 0; s < kSteps; ++s) keys[s] = key_of(__ldcs(row + base + s * 32 + lane));
+    } else {
+  #pragma unroll
+      for (int s = 0; s < kSteps; ++s) {
         const int64_t i = base + s * 32 + lane;
-        if (pos < k) {
-          idx_out[w * k + pos] = static_cast<int32_t>(i);
-          if (val_out) {
-            const float x = row[i];
-            val_out[w * k + pos] = fp16_vals ? gc::fp16_round_trip(x) : x;
+        keys[s] = i < len ? key_of(row[i]) : 0u;   // key 0 <= T: never selected past the end
+      }
+    }
+    // masks per group: ge (key >= T) and eq (key == T); padding lanes read key 0
+    unsigned int gem[kSteps], eqm[kSteps];
+    unsigned int eq_tot = 0;
+    const bool t_zero = T == 0u;
+  #pragma unroll
+    for (int s = 0; s < kSteps; ++s) {
+      const bool valid = base + s * 32 + lane < len;
+      gem[s] = __ballot_sync(0xffffffffu, valid && keys[s] >= T);
+      eqm[s] = 0u;
+      if (gem[s]) {
+        eqm[s] = __ballot_sync(0xffffffffu, valid && keys[s] == T);
+        eq_tot += __popc(eqm[s]);
+      }
+    }
+    (void)t_zero;
+    if (lane == 0) s_eq[warp] = eq_tot;
+    __syncthreads();
+    long long eq_run = wk.tile_eq_off[w * tiles + tile];
+    for (int j = 0; j < warp; ++j) eq_run += s_eq[j];
+    unsigned int sel_tot = 0;
+  #pragma unroll
+    for (int s = 0; s < kSteps; ++s) {
+      unsigned int sm = gem[s] & ~eqm[s];   // strictly above T: always taken
+      if (eqm[s]) {
+        // ties: the first max(0, min(popc, m - eq_run)) set bits of eqm, in lane (= index) order
+        const long long room = m - eq_run;
+        const int take = room <= 0 ? 0 : (room >= 32 ? 32 : static_cast<int>(room));
+        unsigned int e = eqm[s];
+        for (int t = 0; t < take && e; ++t) {
+          const unsigned int lowbit = e & (0u - e);
+          sm |= lowbit;
+          e ^= lowbit;
+        }
+        eq_run += __popc(eqm[s]);
+      }
+      gem[s] = sm;   // reuse as the selected mask
+      sel_tot += __popc(sm);
+    }
+    if (lane == 0) s_sel[warp] = sel_tot;
+    __syncthreads();
+    long long out = wk.tile_sel_off[w * tiles + tile];
+    for (int j = 0; j < warp; ++j) out += s_sel[j];
+  #pragma unroll
+    for (int s = 0; s < kSteps; ++s) {
+      const unsigned int sm = gem[s];
+      if (sm) {
+        if ((sm >> lane) & 1u) {
+          const long long pos = out + __popc(sm & lt_mask);
+          const int64_t i = base + s * 32 + lane;
+          if (pos < k) {
+            idx_out[w * k + pos] = static_cast<int32_t>(i);
+            if (val_out) {
+              const float x = row[i];
+              val_out[w * k + pos] = fp16_vals ? gc::fp16_round_trip(x) : x;
+            }
+            if (resid) {   // fused ef_update (the corrected row is resid itself)
+              const float x = row[i];
+              resid[w * ld + i] = x - (fp16_vals ? gc::fp16_round_trip(x) : x);
+            }
           }
         }
+        out += __popc(sm);
       }
-      out += __popc(sm);
     }
+    __syncthreads();   // s_eq / s_sel are reused by the next tile
   }
 }
 
@@ -537,87 +618,189 @@ __device__ __forceinline__ unsigned int warp_excl_scan(unsigned int v, int lane,
 
 __global__ void __launch_bounds__(kNT) write_vec_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
                                                         int64_t tiles, int64_t k, int32_t *idx_out, float *val_out,
-                                                        int fp16_vals) {
+                                                        int fp16_vals, float *resid) {
   __shared__ unsigned int s_eq[kNT / 32], s_sel[kNT / 32];
-  const int w = blockIdx.y;
-  const unsigned int T = wk.state[w].thresh;
-  const long long m = wk.state[w].take_eq;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTileE + warp * 512;
-  const float *row = vals + w * ld;
-  unsigned int keys[16];
-  if (wbase + 512 <= len) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float4 x = __ldcs(reinterpret_cast<const float4 *>(row + wbase + 128 * u) + lane);
-      keys[4 * u] = key_of(x.x); keys[4 * u + 1] = key_of(x.y); keys[4 * u + 2] = key_of(x.z); keys[4 * u + 3] = key_of(x.w);
+  // fallback only: the candidate write (cand_write_kernel) covers every row that fit the list
+  if (wk.state[blockIdx.y].cand_count <= static_cast<unsigned long long>(wk.cap)) return;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int w = blockIdx.y;
+    const unsigned int T = wk.state[w].thresh;
+    const long long m = wk.state[w].take_eq;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t wbase = static_cast<int64_t>(tile) * kTileE + warp * 512;
+    const float *row = vals + w * ld;
+    unsigned int keys[16];
+    if (wbase + 512 <= len) {
+  #pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 x = __ldcs(reinterpret_cast<const float4 *>(row + wbase + 128 * u) + lane);
+        keys[4 * u] = key_of(x.x); keys[4 * u + 1] = key_of(x.y); keys[4 * u + 2] = key_of(x.z); keys[4 * u + 3] = key_of(x.w);
+      }
+    } else {
+  #pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int64_t i = wbase + 128 * (e >> 2) + 4 * lane + (e & 3);
+        keys[e] = i < len ? key_of(row[i]) : 0u;   // key 0 is never above T; never a tie past len
+      }
     }
-  } else {
-#pragma unroll
+    auto valid = [&](int e) { return wbase + 128 * (e >> 2) + 4 * lane + (e & 3) < len; };
+    unsigned int eqbits = 0, gtbits = 0;
+  #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      const int64_t i = wbase + 128 * (e >> 2) + 4 * lane + (e & 3);
-      keys[e] = i < len ? key_of(row[i]) : 0u;   // key 0 is never above T; never a tie past len
+      const bool v = valid(e);
+      eqbits |= (v && keys[e] == T) ? (1u << e) : 0u;
+      gtbits |= (v && keys[e] > T) ? (1u << e) : 0u;
     }
-  }
-  auto valid = [&](int e) { return wbase + 128 * (e >> 2) + 4 * lane + (e & 3) < len; };
-  unsigned int eqbits = 0, gtbits = 0;
-#pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    const bool v = valid(e);
-    eqbits |= (v && keys[e] == T) ? (1u << e) : 0u;
-    gtbits |= (v && keys[e] > T) ? (1u << e) : 0u;
-  }
-  unsigned int weq = __popc(eqbits);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) weq += __shfl_xor_sync(0xffffffffu, weq, o);
-  if (lane == 0) s_eq[warp] = weq;
-  __syncthreads();
-  long long eq_run = wk.tile_eq_off[w * tiles + blockIdx.x];
-  for (int j = 0; j < warp; ++j) eq_run += s_eq[j];
-  unsigned int selbits = gtbits;
-  if (__any_sync(0xffffffffu, eqbits != 0u)) {   // ties: the first m (index order) are taken
-#pragma unroll
+    unsigned int weq = __popc(eqbits);
+  #pragma unroll
+    for (int o = 16; o; o >>= 1) weq += __shfl_xor_sync(0xffffffffu, weq, o);
+    if (lane == 0) s_eq[warp] = weq;
+    __syncthreads();
+    long long eq_run = wk.tile_eq_off[w * tiles + tile];
+    for (int j = 0; j < warp; ++j) eq_run += s_eq[j];
+    unsigned int selbits = gtbits;
+    if (__any_sync(0xffffffffu, eqbits != 0u)) {   // ties: the first m (index order) are taken
+  #pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned int eu = (eqbits >> (4 * u)) & 0xFu;
+        unsigned int tot;
+        const unsigned int ex = warp_excl_scan(__popc(eu), lane, tot);
+        long long rank = eq_run + ex;
+  #pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if ((eu >> q) & 1u) {
+            if (rank < m) selbits |= 1u << (4 * u + q);
+            ++rank;
+          }
+        eq_run += tot;
+      }
+    }
+    unsigned int wsel = __popc(selbits);
+  #pragma unroll
+    for (int o = 16; o; o >>= 1) wsel += __shfl_xor_sync(0xffffffffu, wsel, o);
+    if (lane == 0) s_sel[warp] = wsel;
+    __syncthreads();
+    long long out = wk.tile_sel_off[w * tiles + tile];
+    for (int j = 0; j < warp; ++j) out += s_sel[j];
+  #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const unsigned int eu = (eqbits >> (4 * u)) & 0xFu;
+      const unsigned int su = (selbits >> (4 * u)) & 0xFu;
+      if (!__any_sync(0xffffffffu, su != 0u)) continue;
       unsigned int tot;
-      const unsigned int ex = warp_excl_scan(__popc(eu), lane, tot);
-      long long rank = eq_run + ex;
-#pragma unroll
+      long long pos = out + warp_excl_scan(__popc(su), lane, tot);
+  #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if ((eu >> q) & 1u) {
-          if (rank < m) selbits |= 1u << (4 * u + q);
+        if ((su >> q) & 1u) {
+          const int64_t i = wbase + 128 * u + 4 * lane + q;
+          if (pos < k) {
+            idx_out[w * k + pos] = static_cast<int32_t>(i);
+            if (val_out) {
+              const float x = row[i];
+              val_out[w * k + pos] = fp16_vals ? gc::fp16_round_trip(x) : x;
+            }
+            if (resid) {   // fused ef_update (the corrected row is resid itself)
+              const float x = row[i];
+              resid[w * ld + i] = x - (fp16_vals ? gc::fp16_round_trip(x) : x);
+            }
+          }
+          ++pos;
+        }
+      out += tot;
+    }
+    __syncthreads();   // s_eq / s_sel are reused by the next tile
+  }
+}
+
+// Pass 3 from the candidate segments, one warp per tile: tile t's selected elements are its
+// segment's entries with key > T plus its ties (key == T) whose global tie rank (tile_eq_off +
+// rank in the tile) is below m.  Index ranks come from two 4096-bit bitmaps per warp (ties,
+// selected; lane l owns words 4l..4l+3) and a warp prefix popcount, so no sort is needed.
+// With ef != 0 the own payload is subtracted in place: resid[i] = x - val (ef_update,
+// compressors.py:629-631; x is the corrected value the candidate carries).
+__global__ void __launch_bounds__(kNT) cand_write_kernel(Work wk, int64_t tiles, int64_t k, int32_t *idx_out,
+                                                         float *val_out, int fp16_vals, float *resid, int64_t ld) {
+  constexpr int kWords = kTileE / 32;   // 128
+  __shared__ unsigned int s_bits[kNT / 32][2][kWords];
+  const int w = blockIdx.y;
+  const RowState &st = wk.state[w];
+  if (st.cand_count > static_cast<unsigned long long>(wk.cap)) return;   // overflow: full-row write
+  const unsigned int T = st.thresh;
+  const long long m = st.take_eq;
+  const unsigned int *ck = wk.cand_key + w * wk.cap, *ci = wk.cand_idx + w * wk.cap;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  unsigned int *eqw = s_bits[wp][0], *selw = s_bits[wp][1];
+  for (int64_t tile = blockIdx.x * static_cast<int64_t>(kNT / 32) + wp; tile < tiles;
+       tile += static_cast<int64_t>(gridDim.x) * (kNT / 32)) {
+    const unsigned long long cb = wk.tile_cbase[w * tiles + tile];
+    const unsigned int cn = wk.tile_ccnt[w * tiles + tile];
+    if (cn == 0) continue;
+    const long long sel_off = wk.tile_sel_off[w * tiles + tile];
+    const long long eq_off = wk.tile_eq_off[w * tiles + tile];
+    const unsigned int tbase = static_cast<unsigned int>(tile * kTileE);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) eqw[4 * lane + j] = 0u, selw[4 * lane + j] = 0u;
+    __syncwarp();
+    for (unsigned int e = lane; e < cn; e += 32) {
+      const unsigned int key = ck[cb + e] & 0x7FFFFFFFu, pos = ci[cb + e] - tbase;
+      if (key > T) atomicOr(&selw[pos >> 5], 1u << (pos & 31));
+      else if (key == T) atomicOr(&eqw[pos >> 5], 1u << (pos & 31));
+    }
+    __syncwarp();
+    unsigned int ew[4], sw[4], ec = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ew[j] = eqw[4 * lane + j], sw[j] = selw[4 * lane + j], ec += __popc(ew[j]);
+    if (__any_sync(0xffffffffu, ec != 0u)) {   // ties in index order up to m
+      unsigned int incl = ec;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      long long rank = eq_off + (incl - ec);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        unsigned int e = ew[j];
+        while (e && rank < m) {
+          const unsigned int low = e & (0u - e);
+          sw[j] |= low;
+          e ^= low;
           ++rank;
         }
-      eq_run += tot;
-    }
-  }
-  unsigned int wsel = __popc(selbits);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) wsel += __shfl_xor_sync(0xffffffffu, wsel, o);
-  if (lane == 0) s_sel[warp] = wsel;
-  __syncthreads();
-  long long out = wk.tile_sel_off[w * tiles + blockIdx.x];
-  for (int j = 0; j < warp; ++j) out += s_sel[j];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const unsigned int su = (selbits >> (4 * u)) & 0xFu;
-    if (!__any_sync(0xffffffffu, su != 0u)) continue;
-    unsigned int tot;
-    long long pos = out + warp_excl_scan(__popc(su), lane, tot);
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if ((su >> q) & 1u) {
-        const int64_t i = wbase + 128 * u + 4 * lane + q;
-        if (pos < k) {
-          idx_out[w * k + pos] = static_cast<int32_t>(i);
-          if (val_out) {
-            const float x = row[i];
-            val_out[w * k + pos] = fp16_vals ? gc::fp16_round_trip(x) : x;
-          }
-        }
-        ++pos;
+        rank += __popc(e);
       }
-    out += tot;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) selw[4 * lane + j] = sw[j];
+    }
+    unsigned int sc = __popc(sw[0]) + __popc(sw[1]) + __popc(sw[2]) + __popc(sw[3]);
+    unsigned int incl = sc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    // exclusive prefix of selected bits before each of the lane's words, published in eqw
+    unsigned int ex = incl - sc;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      eqw[4 * lane + j] = ex;
+      ex += __popc(sw[j]);
+    }
+    __syncwarp();
+    for (unsigned int e = lane; e < cn; e += 32) {
+      const unsigned int pos = ci[cb + e] - tbase, wd = pos >> 5, bit = 1u << (pos & 31);
+      const unsigned int sword = selw[wd];
+      if (sword & bit) {
+        const long long o = sel_off + eqw[wd] + __popc(sword & (bit - 1u));
+        if (o < k) {
+          const float x = __uint_as_float(ck[cb + e]);
+          const float v = fp16_vals ? gc::fp16_round_trip(x) : x;
+          idx_out[w * k + o] = static_cast<int32_t>(tbase + pos);
+          if (val_out) val_out[w * k + o] = v;
+          if (resid) resid[w * ld + tbase + pos] = x - v;
+        }
+      }
+    }
+    __syncwarp();   // bitmaps are reused by the warp's next tile
   }
 }
 
@@ -681,8 +864,11 @@ int64_t gc_topk_workspace_bytes(int32_t workers, int64_t len) {
 }
 
 int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld, int64_t k, const float *grads,
-                   float *resid, int32_t *idx_out, float *val_out, int32_t fp16_vals, void *workspace,
+                   float *resid, int32_t *idx_out, float *val_out, int32_t flags, void *workspace,
                    void *stream) {
+  const int fp16_vals = flags & GC_TOPK_FP16_VALUES;
+  const bool ef = (flags & GC_TOPK_EF_UPDATE) != 0;
+  GC_REQUIRE(!ef || (grads && resid && !values), "GC_TOPK_EF_UPDATE needs grads and resid (fused ef_apply)");
   GC_REQUIRE(workers >= 1 && workers <= 65535 && len >= 1 && ld >= len, "invalid shape");
   GC_REQUIRE(k >= 1 && k <= len, "need 1 <= k <= len");
   GC_REQUIRE(len <= 0x7fffffff, "rows longer than 2^31-1 are not supported (int32 indices)");
@@ -693,11 +879,11 @@ int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld
   const dim3 grid(static_cast<unsigned>(tiles), workers);
   const float *src = grads ? grads : values;
   const bool vec = (ld % 4) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(resid)) & 15) == 0;
-  init_kernel<<<grid_for(2048 * workers), kNT, 0, st>>>(wk, workers, k);
+  init_kernel<<<grid_for(2048 * workers), kNT, 0, st>>>(wk, workers, k, vec ? 1 : 0);
   GC_LAUNCH_CHECK("init_kernel");
   // pass 1: level 0 (optionally fused with ef_apply: values then live in resid, or in grads if EF is off)
   if (vec)
-    hist0_vec_kernel<<<grid, kNT, 0, st>>>(wk, len, values, ld, grads, resid);
+    hist0_vec_kernel<<<grid, kNT, 0, st>>>(wk, len, values, ld, grads, resid, tiles);
   else
     hist_kernel<<<grid, kNT, 0, st>>>(wk, 0, len, values, ld, grads, resid);
   GC_LAUNCH_CHECK("hist_kernel");
@@ -705,7 +891,8 @@ int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld
   const int vec_vals = (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
   find_kernel<<<workers, 1024, 0, st>>>(wk, 0);
   // pass 2: tile counts above the boundary bin + the boundary bin's candidates
-  collect_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles, vec_vals);
+  const dim3 pgrid(static_cast<unsigned>(tiles < 8 * 148 ? tiles : 8 * 148), workers);
+  collect_kernel<<<pgrid, kNT, 0, st>>>(wk, len, vals, ld, tiles, vec_vals);
   const dim3 cgrid(static_cast<unsigned>(tiles < 4 * 148 ? tiles : 4 * 148), workers);
   for (int level = 1; level <= 2; ++level) {
     cand_hist_kernel<<<cgrid, kNT, 0, st>>>(wk, level, len, vals, ld);
@@ -714,11 +901,17 @@ int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld
   GC_LAUNCH_CHECK("radix select");
   cand_tile_kernel<<<cgrid, kNT, 0, st>>>(wk, len, vals, ld, tiles);
   tile_scan_kernel<<<workers, 1024, 0, st>>>(wk, tiles);
-  // pass 3: ordered emission
+  // pass 3: ordered emission from the candidate segments; rows whose candidates overflowed the
+  // list take the full-row write (each kernel returns at once for the other case)
+  const dim3 wgrid(static_cast<unsigned>(tiles < 16 * 148 ? tiles : 16 * 148), workers);
+  cand_write_kernel<<<wgrid, kNT, 0, st>>>(wk, tiles, k, idx_out, val_out, fp16_vals, ef ? resid : nullptr, ld);
+  const dim3 fgrid(static_cast<unsigned>(tiles < 4 * 148 ? tiles : 4 * 148), workers);
   if (vec_vals)
-    write_vec_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles, k, idx_out, val_out, fp16_vals);
+    write_vec_kernel<<<fgrid, kNT, 0, st>>>(wk, len, vals, ld, tiles, k, idx_out, val_out, fp16_vals,
+                                            ef ? resid : nullptr);
   else
-    write_kernel<<<grid, kNT, 0, st>>>(wk, len, vals, ld, tiles, k, idx_out, val_out, fp16_vals);
+    write_kernel<<<fgrid, kNT, 0, st>>>(wk, len, vals, ld, tiles, k, idx_out, val_out, fp16_vals,
+                                        ef ? resid : nullptr);
   GC_LAUNCH_CHECK("topk write");
   return GC_OK;
 }
@@ -737,7 +930,7 @@ int gc_sparse_accumulate(int32_t workers, int64_t k, const int32_t *idx, const f
 
 int gc_encode_sparse_payloads(int32_t workers, int64_t k, const int32_t *idx, const float *val, uint8_t *out,
                               int64_t stride, void *stream) {
-  GC_REQUIRE(workers >= 1 && k >= 0 && k <= 0xffffffffll && idx && val && out && stride >= 5 + 6 * k,
+  GC_REQUIRE(workers >= 1 && k >= 0 && k <= 0xffffffffll && (k == 0 || (idx && val)) && out && stride >= 5 + 6 * k,
              "invalid argument");
   const int64_t total = static_cast<int64_t>(workers) * (k > 0 ? k : 1);
   if (k == 0) {   // header only: <B 1><I 0>

@@ -341,23 +341,22 @@ class _TopK(_Base):
         super().__init__(pipe)
         self.k = cfg.k
         ws = int(_native.lib().gc_topk_workspace_bytes(self.L, self.dim))
-        self.ws = torch.empty(ws, dtype=torch.uint8, device=self.dev)
+        self.ws = torch.zeros(ws, dtype=torch.uint8, device=self.dev)   # zeroed: no threshold hint yet
 
     def run(self, g, res, r, ledger, nmse):
         L, k, d, n = self.L, self.k, self.dim, self.n
         sp = _sp()
         idx = torch.empty(L, k, dtype=torch.int32, device=self.dev)
         val = torch.empty(L, k, dtype=torch.float32, device=self.dev)
+        # ef_update fused into the select (own payload = the fp16 values at idx)
+        flags = _native.TOPK_FP16_VALUES | (_native.TOPK_EF_UPDATE if res is not None else 0)
         _native.call("gc_topk_select", L, d, None, g.stride(0), k, g.data_ptr(), _ptr(res), idx.data_ptr(),
-                     val.data_ptr(), 1, self.ws.data_ptr(), sp)
+                     val.data_ptr(), flags, self.ws.data_ptr(), sp)
         all_idx = self.comm.all_gather_rows(idx)     # all_gather (collectives.py:239-263)
         all_val = self.comm.all_gather_rows(val)
         est = torch.empty(d, dtype=torch.float32, device=self.dev)
         _native.call("gc_sparse_accumulate", n, k, all_idx.data_ptr(), all_val.data_ptr(), d, est.data_ptr(), sp)
         _native.call("gc_scale_div", d, est.data_ptr(), n, est.data_ptr(), sp)
-        if res is not None:
-            _native.call("gc_sparse_ef_update", L, k, idx.data_ptr(), val.data_ptr(), res.data_ptr(), res.stride(0),
-                         sp)
         self.launches += 11 + n
         ledger.charge_gather("sparse-gather", [48 * k] * n)
         return est, float(48 * k), _simple_stats(None)

@@ -307,7 +307,7 @@ class TopKEngine(Engine):
         super().__init__(n, dim, seeds, device)
         self.k = cfg.k
         ws = int(_native.lib().gc_topk_workspace_bytes(n, dim))
-        self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
+        self.ws = torch.zeros(ws, dtype=torch.uint8, device=device)   # zeroed: no threshold hint yet
 
     def run(self, grads, res, round_index, ledger, nmse=True):
         n, d, k = self.n, self.dim, self.k
@@ -317,9 +317,12 @@ class TopKEngine(Engine):
         ev = self._ev()
         if ev:
             ev[0].record()
-        # selection fused with ef_apply: the corrected vectors land in `res` (EF on)
+        # selection fused with ef_apply: the corrected vectors land in `res` (EF on); without the
+        # nmse diagnostic (which reads the corrected vectors) ef_update is fused in as well
+        fuse_ef = res is not None and not nmse
+        flags = _native.TOPK_FP16_VALUES | (_native.TOPK_EF_UPDATE if fuse_ef else 0)
         _native.call("gc_topk_select", n, d, None, grads.stride(0), k, grads.data_ptr(), _ptr(res),
-                     idx.data_ptr(), val.data_ptr(), 1, self.ws.data_ptr(), sp)
+                     idx.data_ptr(), val.data_ptr(), flags, self.ws.data_ptr(), sp)
         if ev:
             ev[1].record()
         est = torch.empty(d, dtype=torch.float32, device=self.device)
@@ -332,7 +335,7 @@ class TopKEngine(Engine):
             acc = torch.zeros(2, dtype=torch.float64, device=self.device)
             self._nmse(corrected, None, est, acc)
             self.launches += 1
-        if res is not None:
+        if res is not None and not fuse_ef:
             _native.call("gc_sparse_ef_update", n, k, idx.data_ptr(), val.data_ptr(), res.data_ptr(),
                          res.stride(0), sp)
             self.launches += 1

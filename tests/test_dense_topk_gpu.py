@@ -38,16 +38,17 @@ def test_dense_vs_oracle(bits, n, d):
     assert np.array_equal(res.estimate.logical, o["estimate"])
 
 
+@pytest.mark.parametrize("nmse", [True, False])   # False: ef_update fused into the select
 @pytest.mark.parametrize("n,d,k", [(8, 1_000_000, 10_000), (4, 300_001, 3), (3, 65_536, 65_536), (2, 5000, 1),
                                    (5, 123_457, 4321)])
-def test_topk_vs_oracle_multi_round(n, d, k):
+def test_topk_vs_oracle_multi_round(n, d, k, nmse):
     import paper_2407_01378_b200 as gcb
     seeds = gcb.SeedSpec(5)
     rng = np.random.default_rng(5)
     # quarter-valued inputs: heavy ties, exactly representable -> exercises the lower-index tie-break
     grads = [[(rng.integers(-40, 41, d) / 4.0).astype(np.float32) for _ in range(n)] for _ in range(3)]
     outs = oracle_rounds("topk", dict(k=k), grads, 5)
-    pipe = gcb.make_pipeline(gcb.TopKConfig(k), n, d, seeds)
+    pipe = gcb.make_pipeline(gcb.TopKConfig(k), n, d, seeds, compute_nmse=nmse)
     pipe._engine.capture = True
     for r in range(3):
         res = pipe.run_round(grads[r], r)
@@ -59,17 +60,26 @@ def test_topk_vs_oracle_multi_round(n, d, k):
 
 
 def test_topk_gaussian_large():
-    """BERT-like shape reduced: d = 11M, k = 1%, n = 2 (bit-exact indices, estimate and residuals)."""
+    """BERT-like shape reduced: d = 11M, k = 1%, n = 2 (bit-exact indices, estimate and residuals).
+    Rounds 1-3 run on the previous round's threshold hint (candidates collected in the level-0
+    pass); round 2's gradients cancel the carried residual, so its corrected vectors are ~100x
+    smaller, the boundary bin falls below the hint and the collect pass must run again."""
     import paper_2407_01378_b200 as gcb
     n, d = 2, 11_000_000
     k = d // 100
     seeds = gcb.SeedSpec(3)
-    grads = [[seeds.rng("grad-worker", 0, w).standard_normal(d).astype(np.float32) for w in range(n)]]
-    o = oracle_rounds("topk", dict(k=k), grads, 3)[0]
-    pipe = gcb.make_pipeline(gcb.TopKConfig(k), n, d, seeds)
-    res = pipe.run_round(grads[0], 0)
-    assert np.array_equal(res.estimate.logical, o["estimate"])
-    assert np.array_equal(np.stack(pipe.residuals), np.stack(o["residuals"]))
+    grads = [[seeds.rng("grad-worker", r, w).standard_normal(d).astype(np.float32) for w in range(n)]
+             for r in range(2)]
+    res1 = oracle_rounds("topk", dict(k=k), grads, 3)[-1]["residuals"]
+    grads.append([(0.01 * seeds.rng("grad-worker", 2, w).standard_normal(d) - res1[w]).astype(np.float32)
+                  for w in range(n)])
+    grads.append([seeds.rng("grad-worker", 3, w).standard_normal(d).astype(np.float32) for w in range(n)])
+    outs = oracle_rounds("topk", dict(k=k), grads, 3)
+    pipe = gcb.make_pipeline(gcb.TopKConfig(k), n, d, seeds, compute_nmse=False)
+    for r in range(4):
+        res = pipe.run_round(grads[r], r)
+        assert np.array_equal(res.estimate.logical, outs[r]["estimate"]), r
+        assert np.array_equal(np.stack(pipe.residuals), np.stack(outs[r]["residuals"])), r
 
 
 @pytest.mark.parametrize("kind", ["const", "few_values"])
@@ -85,7 +95,7 @@ def test_topk_candidate_overflow_fallback(kind):
         grads = [[rng.choice(np.array([0.5, -0.5, 0.25, 3.0], np.float32), d, p=[0.45, 0.45, 0.0999, 0.0001])
                   for _ in range(n)] for _ in range(2)]
     outs = oracle_rounds("topk", dict(k=k), grads, 9)
-    pipe = gcb.make_pipeline(gcb.TopKConfig(k), n, d, gcb.SeedSpec(9))
+    pipe = gcb.make_pipeline(gcb.TopKConfig(k), n, d, gcb.SeedSpec(9), compute_nmse=(kind == "const"))
     pipe._engine.capture = True
     for r in range(2):
         res = pipe.run_round(grads[r], r)
