@@ -32,7 +32,10 @@ namespace {
 constexpr int kM = 128;          // UMMA M: rows per CTA
 constexpr int kN = 16;           // UMMA N: rank padded to 16
 constexpr int kKc = 32;          // columns per stage: one 128-byte swizzle atom of tf32
-constexpr int kStages = 2;
+#ifndef GC_MQ_STAGES
+#define GC_MQ_STAGES 2
+#endif
+constexpr int kStages = GC_MQ_STAGES;   // smem ring depth (36 KB per stage)
 constexpr int kThreads = 256;
 constexpr int kGroup = 16;       // chunks per TMEM partial (512 columns) before the fp64 fold
 constexpr int kATile = kM * kKc * 4;    // 16 KB

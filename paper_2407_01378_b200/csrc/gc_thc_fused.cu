@@ -170,6 +170,18 @@ struct Lcg {
     s2 = r2;
     s3 = r3;
   }
+  // the high half of the XSL-RR output; (a, b, rot) let lo_of() rebuild the low half on demand
+  __device__ __forceinline__ uint32_t out_hi(uint32_t &a, uint32_t &b, uint32_t &rot) const {
+    const uint32_t xl = s0 ^ s2, xh = s1 ^ s3;
+    rot = s3 >> 26;
+    const bool swap = rot & 32u;
+    a = swap ? xh : xl;
+    b = swap ? xl : xh;
+    return __funnelshift_r(b, a, rot);
+  }
+  static __device__ __forceinline__ uint32_t lo_of(uint32_t a, uint32_t b, uint32_t rot) {
+    return __funnelshift_r(a, b, rot);
+  }
   // the 64-bit XSL-RR output rotr64(hi ^ lo, hi >> 58) as two 32-bit halves
   __device__ __forceinline__ void out(uint32_t &hi, uint32_t &lo) const {
     const uint32_t xl = s0 ^ s2, xh = s1 ^ s3;
@@ -309,6 +321,9 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
   constexpr bool use_lut = USE_LUT;
   const bool simd_fold = a.bits <= 8 && (256 % n) == 0 && (a.ring_blk % 4) == 0;
   constexpr int rpb_log = k - 5;   // layout-B registers per rotation block = 2^(k-5)
+  // B^-1/2 is a power of two for even log2(B): scaling the own-decode inputs by it is exact and
+  // commutes with every fp64 butterfly, so the per-element multiply after the WHT disappears
+  constexpr bool kPow2Scale = (K % 2) == 0;
 
   // ---- PCG64 coin stream of worker w: four lane-strided chains (j mod 4), 128-step jumps.
   const uint64_t inc_h = a.streams[w].inc_hi, inc_l = a.streams[w].inc_lo;
@@ -492,7 +507,9 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
     if (use_lut) {
       for (int e = threadIdx.x; e < nblk * lut_span; e += n * 32) {
         const int b = e / lut_span, z = e - b * lut_span - ibound;
-        lut[e] = static_cast<double>(static_cast<float>(1.0 * bp[8 * b + 2] + bp[8 * b + 5] * static_cast<double>(z)));
+        // pre-scaled by B^-1/2 when that is a power of two (exact, and the WHT commutes with it)
+        lut[e] = static_cast<double>(static_cast<float>(1.0 * bp[8 * b + 2] + bp[8 * b + 5] * static_cast<double>(z))) *
+                 (kPow2Scale ? a.scale : 1.0);
       }
     }
 
@@ -514,7 +531,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
       int tz = 0, tz2 = 0;   // per-tile code sums (|z| <= 127, 32 codes per lane: int32 is exact)
       for (int j = 0; j < 32; j += 4) {
         int z[4];
-        uint32_t hw[4], lw[4];
+        uint32_t hw[4], oa[4], ob[4], orot[4];
         float xv[4];
         bool safe = true;
         // screen parameters: one rotation block spans >= 4 registers when B >= 128
@@ -523,15 +540,16 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
         for (int c = 0; c < 4; ++c) {
           const float4 sp =
               rpb_log >= 2 ? sp_j : *reinterpret_cast<const float4 *>(bp + 8 * ((j + c) >> rpb_log) + 6);
-          ch[c].out(hw[c], lw[c]);
+          hw[c] = ch[c].out_hi(oa[c], ob[c], orot[c]);
           ch[c].step(m128, c128);
           xv[c] = xs[(j + c) * 32 + lane];
-          // fp32 screen: floor by the 1.5 * 2^23 magic constant (|t32| < 2^22), frac, 23-bit coin
+          // fp32 screen: floor by the 1.5 * 2^23 magic constant (|t32| < 2^22), frac, 23-bit coin;
+          // safe iff min(f, 1 - f, |c23 - f|) > H (1 - f is exact for f >= 1/2)
           const float tq = (xv[c] - sp.x) * sp.y;
           const float sm = __fadd_rd(tq, 12582912.0f);
           const float f = tq - (sm - 12582912.0f);
           const float c23 = __uint_as_float(0x3f800000u | (hw[c] >> 9)) - 1.0f;
-          safe = safe && (f >= sp.z && f <= sp.w && fabsf(c23 - f) > sp.z);
+          safe = safe && fminf(fminf(f, 1.0f - f), fabsf(c23 - f)) > sp.z;
           z[c] = (__float_as_int(sm) - 0x4B400000) + (c23 < f ? 1 : 0);
         }
         if (__any_sync(0xffffffffu, !safe)) {   // warp-uniform: the exact path stays off the main line
@@ -543,9 +561,9 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
             const float sm = __fadd_rd(tq, 12582912.0f);
             const float f = tq - (sm - 12582912.0f);
             const float c23 = __uint_as_float(0x3f800000u | (hw[c] >> 9)) - 1.0f;
-            if (!(f >= sp.z && f <= sp.w && fabsf(c23 - f) > sp.z))
-              z[c] = quantize_ref(static_cast<double>(xv[c]), pb[0], pb[1], pb[2], pb[3],
-                                  static_cast<double>(ibound), coin_from(hw[c], lw[c]));
+            if (!(fminf(fminf(f, 1.0f - f), fabsf(c23 - f)) > sp.z))
+              z[c] = quantize_ref(static_cast<double>(xv[c]), pb[0], pb[1], pb[2], pb[3], static_cast<double>(ibound),
+                                  coin_from(hw[c], Lcg::lo_of(oa[c], ob[c], orot[c])));
           }
         }
         // (degenerate blocks, compressors.py:497, come out as code 0 from their screen parameters)
@@ -718,15 +736,26 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int z = static_cast<int8_t>((zw[j >> 2] >> (8 * (j & 3))) & 0xff);
-        v[j] = use_lut ? tab[z] : static_cast<double>(static_cast<float>(1.0 * mid + step * static_cast<double>(z)));
+        v[j] = use_lut ? tab[z]
+                       : static_cast<double>(static_cast<float>(1.0 * mid + step * static_cast<double>(z))) *
+                             (kPow2Scale ? a.scale : 1.0);
       }
       wht_tile<K>(v, scratch, lane);
+      if (t0 + kTileN <= a.dim) {   // full tile: no bounds checks, immediate store offsets
+        float *rt = ro + t0 + lane;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int e = j * 32 + lane;
-        const int64_t i = t0 + e;
-        const float own = static_cast<float>(apply_sign(v[j] * a.scale, (sign_col >> j) & 1u));
-        if (i < a.dim) __stcs(ro + i, cbuf[cidx(e)] - own);
+        for (int j = 0; j < 32; ++j) {
+          const float own = static_cast<float>(apply_sign(kPow2Scale ? v[j] : v[j] * a.scale, (sign_col >> j) & 1u));
+          __stcs(rt + 32 * j, cbuf[cidx(j * 32 + lane)] - own);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int e = j * 32 + lane;
+          const int64_t i = t0 + e;
+          const float own = static_cast<float>(apply_sign(kPow2Scale ? v[j] : v[j] * a.scale, (sign_col >> j) & 1u));
+          if (i < a.dim) __stcs(ro + i, cbuf[cidx(e)] - own);
+        }
       }
     }
     // (C) end of tile: only the nmse reduction needs it (it reads every warp's cbuf); all other

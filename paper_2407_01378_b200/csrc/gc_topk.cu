@@ -37,6 +37,10 @@ namespace {
 constexpr int kNT = 256;
 constexpr int kTileE = 4096;          // elements per tile (8 warps x 16 steps x 32 lanes)
 constexpr int kSteps = kTileE / kNT;  // 16
+// radix digits of the 31-bit magnitude key: 13 + 10 + 8 bits.  The wide level-0 digit (32 bins
+// per octave) keeps the boundary bin -- and so the candidate list -- small even when EF piles
+// many magnitudes up just below the threshold.
+constexpr int kBins0 = 8192, kShift0 = 18, kShift1 = 8;
 
 constexpr unsigned int kNoGuess = 0xFFFFFFFFu;
 
@@ -50,12 +54,14 @@ struct RowState {  // per worker, lives in the workspace
   long long take_eq;       // m: number of T-keyed elements taken (lowest indices)
   unsigned long long cand_count;   // candidates appended (may exceed the capacity)
   int spec_ok;             // pass 1's candidates are complete: the collect pass is skipped
-  int pad;
+  unsigned int spec_fail;  // persists: consecutive calls whose speculation failed
+  unsigned int calls;      // persists: calls on this workspace
+  unsigned int pad3;
 };
 
 struct Work {
   RowState *state;              // [L]
-  unsigned int *hist;           // [L][2048]
+  unsigned int *hist;           // [L][kBins0]
   unsigned int *tile_gt;        // [L][tiles]
   unsigned int *tile_eq;        // [L][tiles]
   long long *tile_sel_off;      // [L][tiles]
@@ -80,7 +86,7 @@ __host__ __device__ inline Work carve(void *ws, int L, int64_t tiles, int64_t le
   w.state = reinterpret_cast<RowState *>(p);
   p += align256(sizeof(RowState) * L);
   w.hist = reinterpret_cast<unsigned int *>(p);
-  p += align256(int64_t{4} * 2048 * L);
+  p += align256(int64_t{4} * kBins0 * L);
   w.tile_gt = reinterpret_cast<unsigned int *>(p);
   p += align256(int64_t{4} * tiles * L);
   w.tile_eq = reinterpret_cast<unsigned int *>(p);
@@ -101,28 +107,34 @@ __host__ __device__ inline Work carve(void *ws, int L, int64_t tiles, int64_t le
 }
 
 int64_t ws_bytes(int L, int64_t tiles, int64_t len) {
-  return align256(sizeof(RowState) * L) + align256(int64_t{4} * 2048 * L) + 3 * align256(int64_t{4} * tiles * L) +
+  return align256(sizeof(RowState) * L) + align256(int64_t{4} * kBins0 * L) + 3 * align256(int64_t{4} * tiles * L) +
          3 * align256(int64_t{8} * tiles * L) + 2 * align256(int64_t{4} * cand_cap_for(len) * L);
 }
 
 __device__ __forceinline__ unsigned int key_of(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
 
-// level 0: bits 30..20 (2048 bins); level 1: bits 19..10 for keys with the level-0 prefix;
-// level 2: bits 9..0 for keys with the level-1 prefix.
+// level 0: bits 30..18 (8192 bins); level 1: bits 17..8 for keys with the level-0 prefix;
+// level 2: bits 7..0 for keys with the level-1 prefix.
 __device__ __forceinline__ int bin_of(unsigned int key, int level, unsigned int prefix) {
-  if (level == 0) return static_cast<int>(key >> 20);
-  if (level == 1) return (key >> 20) == prefix ? static_cast<int>((key >> 10) & 1023u) : -1;
-  return (key >> 10) == prefix ? static_cast<int>(key & 1023u) : -1;
+  if (level == 0) return static_cast<int>(key >> kShift0);
+  if (level == 1) return (key >> kShift0) == prefix ? static_cast<int>((key >> kShift1) & 1023u) : -1;
+  return (key >> kShift1) == prefix ? static_cast<int>(key & 255u) : -1;
 }
 
 __global__ void __launch_bounds__(kNT) init_kernel(Work wk, int L, int64_t k, int speculate) {
-  for (int i = blockIdx.x * kNT + threadIdx.x; i < 2048 * L; i += gridDim.x * kNT) wk.hist[i] = 0;
+  for (int i = blockIdx.x * kNT + threadIdx.x; i < kBins0 * L; i += gridDim.x * kNT) wk.hist[i] = 0;
   for (int r = blockIdx.x * kNT + threadIdx.x; r < L; r += gridDim.x * kNT) {
     RowState &s = wk.state[r];
     // pass 1 collects the bins >= (previous boundary bin - 1): in steady EF rounds the new
     // boundary bin is at or above it, so the collect pass is skipped (verified on the device)
     const unsigned int h = s.hint;
-    s.guess = !speculate ? kNoGuess : ((h >= 2 && h <= 2048) ? h - 2 : (h == 1 ? 0u : kNoGuess));
+    // guess = previous boundary bin - 2 (two 1/32-octave bins of margin).  After a failed
+    // speculation (threshold moving, or too many candidates) pass 1 stays plain except for a
+    // re-probe every 8th call, so a drifting workload pays little for the attempt.
+    const bool probe = s.spec_fail == 0 || (s.calls & 7u) == 0;
+    s.calls = s.calls + 1;
+    s.guess = !speculate || !probe || h == 0 || h > static_cast<unsigned int>(kBins0) ? kNoGuess
+                                                                                       : (h >= 3 ? h - 3 : 0u);
     s.spec_ok = 0;
     s.prefix = 0;
     s.k_rem = k;
@@ -137,9 +149,9 @@ __global__ void __launch_bounds__(kNT) init_kernel(Work wk, int L, int64_t k, in
 // compressors.py:624-626) while building the level-0 histogram of |corrected|.
 __global__ void __launch_bounds__(kNT) hist_kernel(Work wk, int level, int64_t len, const float *vals, int64_t ld,
                                                    const float *grads, float *resid) {
-  __shared__ unsigned int h[2048];
+  __shared__ unsigned int h[kBins0];
   const int w = blockIdx.y;
-  const int nb = level == 0 ? 2048 : 1024;
+  const int nb = level == 0 ? kBins0 : 1024;
   for (int i = threadIdx.x; i < nb; i += kNT) h[i] = 0;
   __syncthreads();
   const unsigned int prefix = wk.state[w].prefix;
@@ -161,7 +173,7 @@ __global__ void __launch_bounds__(kNT) hist_kernel(Work wk, int level, int64_t l
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += kNT)
-    if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
+    if (h[i]) atomicAdd(&wk.hist[w * kBins0 + i], h[i]);
 }
 
 // Reserve `mine` consecutive candidate slots per thread for a CTA (warp scans, one global atomic
@@ -195,92 +207,97 @@ __device__ __forceinline__ unsigned long long reserve_slots(unsigned int mine, R
   return *s_base + s_wcnt[warp] + (incl - mine);
 }
 
-// Level 0 with float4 loads (aligned rows): a thread's 16 elements are 4 float4 at stride
-// 256 (element 4 * (tid + 256u) + q), all loads issued before the shared-memory atomics.
-// grads != NULL fuses ef_apply.  With a guess bin from the previous call, elements in bins >=
-// guess are appended to the candidate list as the tile's segment (pass 2 then only runs if the
-// guess turns out above the new boundary bin).
+// Level 0 with float4 loads (aligned rows): persistent CTAs walk the tiles of their worker and
+// keep the 8192-bin histogram in shared memory (one flush per CTA).  Per tile a thread's 16
+// elements are 4 float4 at stride 256 (element 4 * (tid + 256u) + q), all loads issued before
+// the shared-memory atomics.  grads != NULL fuses ef_apply.  With a guess bin from the previous
+// call, elements in bins >= guess are appended to the candidate list as the tile's segment
+// (pass 2 then only runs if the guess turns out above the new boundary bin).
 __global__ void __launch_bounds__(kNT) hist0_vec_kernel(Work wk, int64_t len, const float *vals, int64_t ld,
                                                         const float *grads, float *resid, int64_t tiles) {
-  __shared__ unsigned int h[2048];
+  __shared__ unsigned int h[kBins0];
   __shared__ unsigned int s_wcnt[kNT / 32];
   __shared__ unsigned long long s_base;
   __shared__ unsigned int s_tot;
   const int w = blockIdx.y;
   RowState &st = wk.state[w];
   const unsigned int guess = st.guess;
-  for (int i = threadIdx.x; i < 2048; i += kNT) h[i] = 0;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileE;
-  float4 x[4];
-  unsigned int valid = 0xFFFFu;
+  for (int i = threadIdx.x; i < kBins0; i += kNT) h[i] = 0;
+  __syncthreads();
   const float *src = grads ? grads + w * ld : vals + w * ld;
-  if (base + kTileE <= len) {
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t base = tile * kTileE;
+    float4 x[4];
+    unsigned int valid = 0xFFFFu;
+    if (base + kTileE <= len) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = __ldcs(reinterpret_cast<const float4 *>(src + base) + threadIdx.x + kNT * u);
-    if (grads && resid) {
-      float4 *rr = reinterpret_cast<float4 *>(resid + w * ld + base);
+      for (int u = 0; u < 4; ++u) x[u] = __ldcs(reinterpret_cast<const float4 *>(src + base) + threadIdx.x + kNT * u);
+      if (grads && resid) {
+        float4 *rr = reinterpret_cast<float4 *>(resid + w * ld + base);
+        float4 r4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r4[u] = __ldcs(rr + threadIdx.x + kNT * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          x[u].x = x[u].x + r4[u].x; x[u].y = x[u].y + r4[u].y; x[u].z = x[u].z + r4[u].z; x[u].w = x[u].w + r4[u].w;
+          rr[threadIdx.x + kNT * u] = x[u];
+        }
+      }
+    } else {
+      valid = 0u;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float4 r4 = rr[threadIdx.x + kNT * u];
-        x[u].x = x[u].x + r4.x; x[u].y = x[u].y + r4.y; x[u].z = x[u].z + r4.z; x[u].w = x[u].w + r4.w;
-        rr[threadIdx.x + kNT * u] = x[u];
+        float t[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t i = base + 4 * (threadIdx.x + kNT * u) + q;
+          float v = 0.0f;
+          if (i < len) {
+            v = src[i];
+            if (grads && resid) {
+              v = v + resid[w * ld + i];
+              resid[w * ld + i] = v;
+            }
+            valid |= 1u << (4 * u + q);
+          }
+          t[q] = v;
+        }
+        x[u] = make_float4(t[0], t[1], t[2], t[3]);
       }
     }
-  } else {
-    valid = 0u;
+    unsigned int bits[16];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      float t[4];
+      bits[4 * u] = __float_as_uint(x[u].x); bits[4 * u + 1] = __float_as_uint(x[u].y);
+      bits[4 * u + 2] = __float_as_uint(x[u].z); bits[4 * u + 3] = __float_as_uint(x[u].w);
+    }
+    unsigned int cmask = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t i = base + 4 * (threadIdx.x + kNT * u) + q;
-        float v = 0.0f;
-        if (i < len) {
-          v = src[i];
-          if (grads && resid) {
-            v = v + resid[w * ld + i];
-            resid[w * ld + i] = v;
-          }
-          valid |= 1u << (4 * u + q);
+    for (int e = 0; e < 16; ++e) {
+      const unsigned int b0 = (bits[e] & 0x7FFFFFFFu) >> kShift0;
+      if ((valid >> e) & 1u) {
+        atomicAdd(&h[b0], 1u);
+        cmask |= (b0 >= guess ? 1u : 0u) << e;
+      }
+    }
+    if (guess != kNoGuess) {   // grid-uniform
+      unsigned long long pos = reserve_slots(__popc(cmask), st, s_wcnt, &s_base, &s_tot,
+                                             &wk.tile_cbase[w * tiles + tile], &wk.tile_ccnt[w * tiles + tile]);
+      while (cmask) {
+        const int e = __ffs(cmask) - 1;
+        cmask &= cmask - 1u;
+        if (pos < static_cast<unsigned long long>(wk.cap)) {
+          wk.cand_key[w * wk.cap + pos] = bits[e];
+          wk.cand_idx[w * wk.cap + pos] = static_cast<unsigned int>(base + 4 * (threadIdx.x + kNT * (e >> 2)) + (e & 3));
         }
-        t[q] = v;
+        ++pos;
       }
-      x[u] = make_float4(t[0], t[1], t[2], t[3]);
+      __syncthreads();   // s_wcnt / s_base are reused by the next tile
     }
   }
   __syncthreads();
-  unsigned int bits[16];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    bits[4 * u] = __float_as_uint(x[u].x); bits[4 * u + 1] = __float_as_uint(x[u].y);
-    bits[4 * u + 2] = __float_as_uint(x[u].z); bits[4 * u + 3] = __float_as_uint(x[u].w);
-  }
-  unsigned int cmask = 0;
-#pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    const unsigned int b0 = (bits[e] & 0x7FFFFFFFu) >> 20;
-    if ((valid >> e) & 1u) {
-      atomicAdd(&h[b0], 1u);
-      cmask |= (b0 >= guess ? 1u : 0u) << e;
-    }
-  }
-  if (guess != kNoGuess) {   // grid-uniform
-    const unsigned int mine = __popc(cmask);
-    unsigned long long pos = reserve_slots(mine, st, s_wcnt, &s_base, &s_tot, &wk.tile_cbase[w * tiles + blockIdx.x],
-                                           &wk.tile_ccnt[w * tiles + blockIdx.x]);
-    while (cmask) {
-      const int e = __ffs(cmask) - 1;
-      cmask &= cmask - 1u;
-      if (pos < static_cast<unsigned long long>(wk.cap)) {
-        wk.cand_key[w * wk.cap + pos] = bits[e];
-        wk.cand_idx[w * wk.cap + pos] = static_cast<unsigned int>(base + 4 * (threadIdx.x + kNT * (e >> 2)) + (e & 3));
-      }
-      ++pos;
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 2048; i += kNT)
-    if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
+  for (int i = threadIdx.x; i < kBins0; i += kNT)
+    if (h[i]) atomicAdd(&wk.hist[w * kBins0 + i], h[i]);
 }
 
 // Pass 2 (skipped when pass 1's guess held): per tile, every element at or above the level-0
@@ -310,13 +327,13 @@ __global__ void __launch_bounds__(kNT) collect_kernel(Work wk, int64_t len, cons
         keys[4 * u + 3] = __float_as_uint(x.w);
       }
 #pragma unroll
-      for (int e = 0; e < kSteps; ++e) cmask |= (((keys[e] & 0x7FFFFFFFu) >> 20) >= p0 ? 1u : 0u) << e;
+      for (int e = 0; e < kSteps; ++e) cmask |= (((keys[e] & 0x7FFFFFFFu) >> kShift0) >= p0 ? 1u : 0u) << e;
     } else {
 #pragma unroll
       for (int e = 0; e < kSteps; ++e) {
         const int64_t i = base + 4 * (threadIdx.x + kNT * (e >> 2)) + (e & 3);
         keys[e] = i < len ? __float_as_uint(row[i]) : 0u;
-        cmask |= (i < len && ((keys[e] & 0x7FFFFFFFu) >> 20) >= p0 ? 1u : 0u) << e;
+        cmask |= (i < len && ((keys[e] & 0x7FFFFFFFu) >> kShift0) >= p0 ? 1u : 0u) << e;
       }
     }
     unsigned long long pos = reserve_slots(__popc(cmask), st, s_wcnt, &s_base, &s_tot,
@@ -360,7 +377,7 @@ __global__ void __launch_bounds__(kNT) cand_hist_kernel(Work wk, int level, int6
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 1024; i += kNT)
-    if (h[i]) atomicAdd(&wk.hist[w * 2048 + i], h[i]);
+    if (h[i]) atomicAdd(&wk.hist[w * kBins0 + i], h[i]);
 }
 
 // Tile counts of the candidates above / equal to T: one warp per tile walks the tile's segment
@@ -426,17 +443,20 @@ __global__ void __launch_bounds__(1024) find_kernel(Work wk, int level) {
   __shared__ unsigned long long s_above, s_krem;
   const int w = blockIdx.x;
   RowState &s = wk.state[w];
-  const int nb = level == 0 ? 2048 : 1024;
-  const int per = nb / 1024;   // bins per thread, owned top-down
-  unsigned int *h = wk.hist + w * 2048;
+  const int nb = level == 0 ? kBins0 : (level == 1 ? 1024 : 256);
+  constexpr int kPerMax = kBins0 / 1024;
+  const int per = nb >= 1024 ? nb / 1024 : 1;   // bins per thread, owned top-down
   if (threadIdx.x == 0) {
     found = -1;
     s_krem = static_cast<unsigned long long>(s.k_rem);
   }
-  unsigned long long c[2] = {0, 0};
+  unsigned int *h = wk.hist + w * kBins0;
+  unsigned int c[kPerMax] = {};
   unsigned long long local = 0;
-  for (int j = 0; j < per; ++j) {
-    c[j] = h[nb - 1 - (threadIdx.x * per + j)];
+#pragma unroll
+  for (int j = 0; j < kPerMax; ++j) {
+    const int bi = threadIdx.x * per + j;
+    c[j] = (j < per && bi < nb) ? h[nb - 1 - bi] : 0u;
     local += c[j];
   }
   unsigned long long excl;
@@ -444,8 +464,9 @@ __global__ void __launch_bounds__(1024) find_kernel(Work wk, int level) {
   __syncthreads();
   const unsigned long long k_rem = s_krem;
   unsigned long long run = excl;
-  for (int j = 0; j < per; ++j) {
-    if (run < k_rem && k_rem <= run + c[j]) {   // exactly one bin qualifies
+#pragma unroll
+  for (int j = 0; j < kPerMax; ++j) {
+    if (j < per && run < k_rem && k_rem <= run + c[j]) {   // exactly one bin qualifies (c[j] > 0)
       found = nb - 1 - (threadIdx.x * per + j);
       s_above = run;
     }
@@ -456,10 +477,11 @@ __global__ void __launch_bounds__(1024) find_kernel(Work wk, int level) {
     const unsigned int b = static_cast<unsigned int>(found);
     s.gt += static_cast<long long>(s_above);
     s.k_rem = static_cast<long long>(k_rem - s_above);
-    s.prefix = (level == 0) ? b : ((s.prefix << 10) | b);
+    s.prefix = (level == 0) ? b : (level == 1 ? ((s.prefix << 10) | b) : ((s.prefix << 8) | b));
     if (level == 0) {   // pass 1's candidates hold every bin >= guess: complete iff b >= guess
       const bool ok = s.guess != kNoGuess && b >= s.guess && s.cand_count <= static_cast<unsigned long long>(wk.cap);
       s.spec_ok = ok ? 1 : 0;
+      if (s.guess != kNoGuess) s.spec_fail = ok ? 0u : s.spec_fail + 1u;
       if (!ok) s.cand_count = 0;   // pass 2 rebuilds the list
       s.hint = b + 1;
     }
@@ -468,7 +490,7 @@ __global__ void __launch_bounds__(1024) find_kernel(Work wk, int level) {
       s.take_eq = s.k_rem;
     }
   }
-  for (int i = threadIdx.x; i < 2048; i += 1024) h[i] = 0;
+  for (int i = threadIdx.x; i < kBins0; i += 1024) h[i] = 0;
 }
 
 // One CTA per worker: eq prefix (tie ranks) and selected-count prefix (output offsets).
@@ -879,11 +901,12 @@ int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld
   const dim3 grid(static_cast<unsigned>(tiles), workers);
   const float *src = grads ? grads : values;
   const bool vec = (ld % 4) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(resid)) & 15) == 0;
-  init_kernel<<<grid_for(2048 * workers), kNT, 0, st>>>(wk, workers, k, vec ? 1 : 0);
+  init_kernel<<<grid_for(kBins0 * workers), kNT, 0, st>>>(wk, workers, k, vec ? 1 : 0);
   GC_LAUNCH_CHECK("init_kernel");
   // pass 1: level 0 (optionally fused with ef_apply: values then live in resid, or in grads if EF is off)
   if (vec)
-    hist0_vec_kernel<<<grid, kNT, 0, st>>>(wk, len, values, ld, grads, resid, tiles);
+    hist0_vec_kernel<<<dim3(static_cast<unsigned>(tiles < 4 * 148 ? tiles : 4 * 148), workers), kNT, 0, st>>>(
+        wk, len, values, ld, grads, resid, tiles);
   else
     hist_kernel<<<grid, kNT, 0, st>>>(wk, 0, len, values, ld, grads, resid);
   GC_LAUNCH_CHECK("hist_kernel");
