@@ -153,6 +153,10 @@ int gc_float_fold_batched(int32_t batch, int32_t n, int64_t len, const float *in
  * or be NULL). */
 int gc_segment_fold_ef(int32_t n, int32_t nseg, const int64_t *seg_off, const int64_t *seg_len,
                        const float *corrected, float *resid, int64_t ld, float *estimate, void *stream);
+/* Same with ef_apply fused (compressors.py:624-626): corrected = f32(grads + resid) is formed in
+ * the kernel; resid (required) leaves as 0 on the segments. */
+int gc_segment_ef_fold(int32_t n, int32_t nseg, const int64_t *seg_off, const int64_t *seg_len,
+                       const float *grads, float *resid, int64_t ld, float *estimate, void *stream);
 /* out = in / divisor (f32, may alias). */
 int gc_scale_div(int64_t len, const float *in, int32_t divisor, float *out, void *stream);
 /* out = fp16_round_trip(in) (vectors.py:136-152; may alias). */
@@ -254,7 +258,8 @@ int gc_psgd_orthonormalize(int32_t tensors, int64_t rows, int32_t rank, const fl
 int gc_psgd_decode(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
                    const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
                    void *stream);
-/* Same, vectorised (cols % 4 == 0, aligned rows): both outputs in one pass. */
+/* The same entry (kept for the fused call sites): both outputs in one pass over the rows, float4
+ * accesses when cols % 4 == 0 and rows are 16-byte aligned, coalesced scalars otherwise. */
 int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
                          const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
                          void *stream);

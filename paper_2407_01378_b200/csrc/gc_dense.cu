@@ -45,8 +45,10 @@ __global__ void __launch_bounds__(kNT) float_fold_kernel(int n, int64_t len, con
 // Dense fp32 bypass of a batch of small tensors: segment blockIdx.y, ring block ceil(len/n).
 // c holds the corrected values; zero (may alias c) receives the new residual 0.
 __global__ void __launch_bounds__(kNT) segment_fold_kernel(int n, const int64_t *seg_off, const int64_t *seg_len,
-                                                           const float *g, float *r, int64_t ld, float *est) {
-  // g: corrected values, r: residual rows to zero (nullable)
+                                                           const float *g, float *r, int64_t ld, float *est,
+                                                           int apply_ef) {
+  // g: corrected values (apply_ef: raw gradients, corrected = f32(g + r)), r: residual rows to
+  // zero (nullable)
   const int64_t off = seg_off[blockIdx.y], len = seg_len[blockIdx.y];
   const int64_t blk = (len + n - 1) / n;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < len;
@@ -56,7 +58,7 @@ __global__ void __launch_bounds__(kNT) segment_fold_kernel(int n, const int64_t 
     float acc = 0.0f;
     int w = s;
     for (int k = 0; k < n; ++k) {
-      const float c = g[w * ld + i];
+      const float c = apply_ef ? g[w * ld + i] + r[w * ld + i] : g[w * ld + i];
       acc = (k == 0) ? c : acc + c;
       w = (w + 1 == n) ? 0 : w + 1;
     }
@@ -141,7 +143,18 @@ int gc_segment_fold_ef(int32_t n, int32_t nseg, const int64_t *seg_off, const in
              "invalid argument");
   if (nseg == 0) return GC_OK;
   segment_fold_kernel<<<dim3(4, nseg), kNT, 0, static_cast<cudaStream_t>(stream)>>>(n, seg_off, seg_len, grads, resid,
-                                                                                  ld, estimate);
+                                                                                  ld, estimate, 0);
+  GC_LAUNCH_CHECK("segment_fold_kernel");
+  return GC_OK;
+}
+
+int gc_segment_ef_fold(int32_t n, int32_t nseg, const int64_t *seg_off, const int64_t *seg_len, const float *grads,
+                       float *resid, int64_t ld, float *estimate, void *stream) {
+  GC_REQUIRE(n >= 1 && nseg >= 0 && nseg <= 65535 && (nseg == 0 || (seg_off && seg_len)) && grads && resid && estimate,
+             "invalid argument");
+  if (nseg == 0) return GC_OK;
+  segment_fold_kernel<<<dim3(4, nseg), kNT, 0, static_cast<cudaStream_t>(stream)>>>(n, seg_off, seg_len, grads, resid,
+                                                                                  ld, estimate, 1);
   GC_LAUNCH_CHECK("segment_fold_kernel");
   return GC_OK;
 }

@@ -12,10 +12,12 @@
 // ~1e-7 relative):
 //   * mq:  a CTA owns a band of 64 rows, stages Q in 1024-column chunks in shared memory
 //          (Q is read from L2 once per band), a warp accumulates 8 rows x r in registers;
-//   * mtp: a CTA owns 256 columns x a row range (thread = column, coalesced row reads, the
-//          P_hat rows broadcast from shared memory); row ranges are reduced in a fixed order;
-//   * decode: one pass per coordinate over all workers writes r_new = c - own and the
-//          estimate.
+//   * mtp: a CTA owns 1024 columns x a row range (thread = 4 columns, coalesced row reads,
+//          the P_hat rows broadcast from shared memory); row ranges are reduced in a fixed order;
+//   * decode: a CTA owns 1024 columns x 64 rows and writes r_new = c - own for every worker
+//          and the estimate in one pass.
+// mtp and decode use float4 accesses when cols % 4 == 0 and rows are 16-byte aligned, and the
+// same kernels with coalesced scalar accesses otherwise (e.g. GPT-2's 1774 x 1774 matrices).
 // MGS runs in one CTA in fp64 (column-by-column projections, block reductions), including
 // the reference's canonical-basis completion of degenerate columns.
 #include <cuda_runtime.h>
@@ -96,42 +98,6 @@ __global__ void __launch_bounds__(256) mq_kernel(int64_t d, int64_t rows, int64_
 
 // ------------------------------------------------------------------ Q = M^T P_hat
 // partial[w][s][col][R] over row range s; then reduced in order s = 0, 1, ...
-template <int R>
-__global__ void __launch_bounds__(256) mtp_kernel(int64_t d, int64_t rows, int64_t cols, const float *c, Rows rw_,
-                                                  const float *ph, int64_t rows_per_split, double *partial,
-                                                  int splits) {
-  constexpr int kChunk = R <= 8 ? 512 : 256;
-  __shared__ float ps[kChunk * R];
-  const int w = blockIdx.z;
-  const int s = blockIdx.y;
-  const int64_t col = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
-  const int64_t r0 = s * rows_per_split;
-  const int64_t r1 = min(rows, r0 + rows_per_split);
-  const float *cw = c + rw_.at(w);
-  ph += static_cast<int64_t>(rw_.tensor(w)) * rows * R;
-  double acc[R];
-#pragma unroll
-  for (int b = 0; b < R; ++b) acc[b] = 0.0;
-  for (int64_t i0 = r0; i0 < r1; i0 += kChunk) {
-    const int ni = static_cast<int>(min(static_cast<int64_t>(kChunk), r1 - i0));
-    __syncthreads();
-    for (int e = threadIdx.x; e < ni * R; e += 256) ps[e] = ph[i0 * R + e];
-    __syncthreads();
-    if (col < cols) {
-#pragma unroll 4
-      for (int ii = 0; ii < ni; ++ii) {
-        const int64_t i = (i0 + ii) * cols + col;
-        const double m = i < d ? static_cast<double>(__ldcs(cw + i)) : 0.0;
-#pragma unroll
-        for (int b = 0; b < R; ++b) acc[b] += m * static_cast<double>(ps[ii * R + b]);
-      }
-    }
-  }
-  if (col < cols) {
-#pragma unroll
-    for (int b = 0; b < R; ++b) partial[((static_cast<int64_t>(w) * splits + s) * cols + col) * R + b] = acc[b];
-  }
-}
 
 __global__ void mtp_reduce_kernel(int L, int splits, int64_t cols, int R, const double *partial, float *q) {
   const int64_t total = static_cast<int64_t>(L) * cols * R;
@@ -318,7 +284,28 @@ __global__ void mq_reduce_kernel(int L, int slabs, int64_t rows, int R, const do
 // groups (~1e-7 relative, the reference itself is fp32 BLAS).
 constexpr int kMtpFold = 32;
 
-template <int R>
+// A thread's 4 consecutive columns of one row: one float4 when rows are 16-byte aligned (A16),
+// else 4 coalesced scalar accesses guarded by nv = the columns left in the row (the last thread
+// of a row whose length is not a multiple of 4).
+template <bool A16>
+__device__ __forceinline__ float4 ld4(const float *p, int nv) {
+  if (A16) return __ldcs(reinterpret_cast<const float4 *>(p));
+  return make_float4(nv > 0 ? __ldcs(p) : 0.0f, nv > 1 ? __ldcs(p + 1) : 0.0f, nv > 2 ? __ldcs(p + 2) : 0.0f,
+                     nv > 3 ? __ldcs(p + 3) : 0.0f);
+}
+template <bool A16>
+__device__ __forceinline__ void st4(float *p, float4 v, int nv) {
+  if (A16) {
+    __stcs(reinterpret_cast<float4 *>(p), v);
+    return;
+  }
+  if (nv > 0) __stcs(p, v.x);
+  if (nv > 1) __stcs(p + 1, v.y);
+  if (nv > 2) __stcs(p + 2, v.z);
+  if (nv > 3) __stcs(p + 3, v.w);
+}
+
+template <int R, bool A16>
 __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, int64_t cols, const float *c,
                                                       Rows rw_, const float *ph, int64_t rows_per_split,
                                                       double *partial, int splits) {
@@ -350,6 +337,7 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
       // rows whose 4 columns all lie below d load without per-row checks, so the unrolled loads
       // of a fold group are all in flight together (a per-row branch serialised them)
       const bool full = (i0 + ni - 1) * cols + col + 3 < d;
+      const int nv = static_cast<int>(min(static_cast<int64_t>(4), cols - col));
       for (int g0 = 0; g0 < ni; g0 += kMtpFold) {
         const int g1 = min(ni, g0 + kMtpFold);
         auto row_fma = [&](int ii, const float4 m) {
@@ -370,17 +358,17 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
           const float *src = cw + (i0 + g0) * cols + col;
 #pragma unroll 8
           for (int ii = 0; ii < kMtpFold; ++ii)
-            row_fma(g0 + ii, __ldcs(reinterpret_cast<const float4 *>(src + ii * cols)));
+            row_fma(g0 + ii, ld4<A16>(src + ii * cols, nv));
         } else {
           for (int ii = g0; ii < g1; ++ii) {
             const int64_t i = (i0 + ii) * cols + col;
             float4 m;
             if (i + 3 < d) {
-              m = __ldcs(reinterpret_cast<const float4 *>(cw + i));
+              m = ld4<A16>(cw + i, nv);
             } else {
               float t4[4] = {0.f, 0.f, 0.f, 0.f};
               for (int t = 0; t < 4; ++t)
-                if (i + t < d) t4[t] = cw[i + t];
+                if (i + t < d && t < nv) t4[t] = cw[i + t];
               m = make_float4(t4[0], t4[1], t4[2], t4[3]);
             }
             row_fma(ii, m);
@@ -399,9 +387,11 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
   if (col < cols) {
 #pragma unroll
     for (int t = 0; t < 4; ++t)
+      if (col + t < cols) {
 #pragma unroll
-      for (int b = 0; b < R; ++b)
-        partial[((static_cast<int64_t>(w) * splits + s) * cols + col + t) * R + b] = acc[t][b];
+        for (int b = 0; b < R; ++b)
+          partial[((static_cast<int64_t>(w) * splits + s) * cols + col + t) * R + b] = acc[t][b];
+      }
   }
 }
 
@@ -410,7 +400,7 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
 // resid), then estimate = P_hat Q_sum^T / n.  Float4 loads/stores, Q read from L2 once per CTA.
 constexpr int kDecRows = 64;
 
-template <int R>
+template <int R, bool A16>
 __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d, int64_t rows, int64_t cols,
                                                          const float *ph, const float *qw, const float *qsum,
                                                          float *resid, Rows rw_, float *est, const int64_t *est_offs) {
@@ -428,6 +418,7 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
   for (int e = threadIdx.x; e < nrows * R; e += 256) ps[e] = ph[row0 * R + e];
   __syncthreads();
   if (col >= cols) return;
+  const int nv = static_cast<int>(min(static_cast<int64_t>(4), cols - col));   // columns of this thread
   for (int w = 0; w <= L; ++w) {   // w == L: the estimate with Q_sum
     const float *qsrc = w < L ? qw + static_cast<int64_t>(w) * cols * R : qsum;
     float qv[4][R];
@@ -448,7 +439,7 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
         if (w < L) {
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            if (u < nb) cv[u] = __ldcs(reinterpret_cast<const float4 *>(dst + (row0 + a0 + u) * cols + col));
+            if (u < nb) cv[u] = ld4<A16>(dst + (row0 + a0 + u) * cols + col, nv);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -465,11 +456,11 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
             for (int b = 1; b < R; ++b) v = fmaf(pa[b], qv[t][b], v);
             o4[t] = v;
           }
-          float4 *o = reinterpret_cast<float4 *>(dst + (row0 + a) * cols + col);
+          float *o = dst + (row0 + a) * cols + col;
           if (w < L)
-            __stcs(o, make_float4(cv[u].x - o4[0], cv[u].y - o4[1], cv[u].z - o4[2], cv[u].w - o4[3]));
+            st4<A16>(o, make_float4(cv[u].x - o4[0], cv[u].y - o4[1], cv[u].z - o4[2], cv[u].w - o4[3]), nv);
           else
-            __stcs(o, make_float4(o4[0] / nf, o4[1] / nf, o4[2] / nf, o4[3] / nf));
+            st4<A16>(o, make_float4(o4[0] / nf, o4[1] / nf, o4[2] / nf, o4[3] / nf), nv);
         }
       }
       continue;
@@ -489,7 +480,7 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
         for (int b = 1; b < R; ++b) v = fmaf(pa[b], qv[t][b], v);
         o4[t] = v;
       }
-      if (i + 3 < d) {
+      if (A16 && i + 3 < d) {
         if (w < L) {
           const float4 c = *reinterpret_cast<const float4 *>(dst + i);
           __stcs(reinterpret_cast<float4 *>(dst + i), make_float4(c.x - o4[0], c.y - o4[1], c.z - o4[2], c.w - o4[3]));
@@ -499,52 +490,13 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
         }
       } else {
         for (int t = 0; t < 4; ++t)
-          if (i + t < d) dst[i + t] = w < L ? dst[i + t] - o4[t] : o4[t] / static_cast<float>(n);
+          if (t < nv && i + t < d) dst[i + t] = w < L ? dst[i + t] - o4[t] : o4[t] / static_cast<float>(n);
       }
     }
   }
 }
 
 
-// ------------------------------------------------------------------ decode + EF
-// For flat index i < d: row = i / cols, col = i % cols.
-//   own_w = sum_b P_hat[row][b] * Q_w[col][b]      (p_hat @ r.T, pipelines.py:355)
-//   resid_w = c_w - own_w                          (ef_update, c_w held in resid)
-//   est = (sum_b P_hat[row][b] * Qsum[col][b]) / n (pipelines.py:365)
-template <int R>
-__global__ void __launch_bounds__(256) decode_kernel(int L, int n, int64_t d, int64_t cols, const float *ph,
-                                                     const float *qw, const float *qsum, float *resid, Rows rw_,
-                                                     float *est, const int64_t *est_offs, int64_t rows) {
-  {
-    const int t = blockIdx.y;
-    ph += static_cast<int64_t>(t) * rows * R;
-    qw += static_cast<int64_t>(t) * L * cols * R;
-    qsum += static_cast<int64_t>(t) * cols * R;
-    if (est) est += est_offs ? est_offs[t] : 0;
-  }
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < d;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t row = i / cols, col = i - row * cols;
-    float p[R];
-#pragma unroll
-    for (int b = 0; b < R; ++b) p[b] = ph[row * R + b];
-    if (resid) {
-      for (int w = 0; w < L; ++w) {
-        double own = 0.0;
-#pragma unroll
-        for (int b = 0; b < R; ++b) own += static_cast<double>(p[b]) * static_cast<double>(qw[(w * cols + col) * R + b]);
-        const int64_t o = rw_.at(blockIdx.y * L + w) + i;
-        resid[o] = resid[o] - static_cast<float>(own);
-      }
-    }
-    if (est) {
-      double e = 0.0;
-#pragma unroll
-      for (int b = 0; b < R; ++b) e += static_cast<double>(p[b]) * static_cast<double>(qsum[col * R + b]);
-      est[i] = static_cast<float>(e) / static_cast<float>(n);
-    }
-  }
-}
 
 // Gram matrix Q^T Q (fp64) for the rank check of ensure_full_rank (compressors.py:595-603).
 __global__ void __launch_bounds__(256) gram_kernel(int64_t cols, int R, const float *q, double *gram) {
@@ -661,13 +613,13 @@ int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, i
   const bool vec = cols % 4 == 0 && b->rows_aligned && (reinterpret_cast<uintptr_t>(c) & 15) == 0;
   if (vec) {
     GC_RANK_SWITCH(rank, ({
-      mtp_vec_kernel<R><<<dim3(grid_cap((cols + 1023) / 1024), splits, L), 256, 0, st>>>(
+      mtp_vec_kernel<R, true><<<dim3(grid_cap((cols + 1023) / 1024), splits, L), 256, 0, st>>>(
           d, rows, cols, c, rows_of(b), p_hat, per, partial, splits);
     }));
-  } else {
+  } else {   // unaligned rows: the same kernel with coalesced scalar loads
     GC_RANK_SWITCH(rank, ({
-      mtp_kernel<R><<<dim3(grid_cap((cols + 255) / 256), splits, L), 256, 0, st>>>(d, rows, cols, c, rows_of(b),
-                                                                                  p_hat, per, partial, splits);
+      mtp_vec_kernel<R, false><<<dim3(grid_cap((cols + 1023) / 1024), splits, L), 256, 0, st>>>(
+          d, rows, cols, c, rows_of(b), p_hat, per, partial, splits);
     }));
   }
   GC_LAUNCH_CHECK("mtp_kernel");
@@ -688,19 +640,15 @@ int gc_psgd_orthonormalize(int32_t tensors, int64_t rows, int32_t rank, const fl
   return GC_OK;
 }
 
+int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                         const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
+                         void *stream);
+
+// Either output may be NULL: estimate only, EF update only, or both in one pass.
 int gc_psgd_decode(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
                    const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
                    void *stream) {
-  if (int rc = check_batch(b)) return rc;
-  GC_REQUIRE(n >= 1 && d >= 1 && cols >= 1 && p_hat && q_workers && q_sum, "invalid argument");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t g = (d + 255) / 256;
-  GC_RANK_SWITCH(rank, ({
-    decode_kernel<R><<<dim3(grid_cap(g > 148 * 16 ? 148 * 16 : g), b->tensors), 256, 0, st>>>(
-        b->workers, n, d, cols, p_hat, q_workers, q_sum, resid, rows_of(b), estimate, b->est_offsets, rows);
-  }));
-  GC_LAUNCH_CHECK("decode_kernel");
-  return GC_OK;
+  return gc_psgd_decode_fused(b, n, d, rows, cols, rank, p_hat, q_workers, q_sum, resid, estimate, stream);
 }
 
 int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
@@ -708,12 +656,17 @@ int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t r
                          void *stream) {
   if (int rc = check_batch(b)) return rc;
   GC_REQUIRE(n >= 1 && d >= 1 && p_hat && q_workers && q_sum, "invalid argument");
-  GC_REQUIRE(cols % 4 == 0 && b->rows_aligned, "decode_fused needs cols % 4 == 0 and 16-byte aligned rows");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // float4 accesses need cols % 4 == 0 and 16-byte aligned rows; otherwise coalesced scalars
+  const bool a16 = cols % 4 == 0 && b->rows_aligned;
+  const dim3 grid(grid_cap((cols + 1023) / 1024), grid_cap((rows + kDecRows - 1) / kDecRows), b->tensors);
   GC_RANK_SWITCH(rank, ({
-    decode_vec_kernel<R><<<dim3(grid_cap((cols + 1023) / 1024), grid_cap((rows + kDecRows - 1) / kDecRows),
-                               b->tensors), 256, 0, st>>>(b->workers, n, d, rows, cols, p_hat, q_workers, q_sum,
-                                                          resid, rows_of(b), estimate, b->est_offsets);
+    if (a16)
+      decode_vec_kernel<R, true><<<grid, 256, 0, st>>>(b->workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid,
+                                                       rows_of(b), estimate, b->est_offsets);
+    else
+      decode_vec_kernel<R, false><<<grid, 256, 0, st>>>(b->workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid,
+                                                        rows_of(b), estimate, b->est_offsets);
   }));
   GC_LAUNCH_CHECK("decode_vec_kernel");
   return GC_OK;

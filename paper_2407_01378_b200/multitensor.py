@@ -171,25 +171,42 @@ class TensorListPipeline:
         # seed matrices of every group first: their rank checks read a few bytes back to the host,
         # so doing them before the heavy kernels keeps the device queue free of bubbles
         qs = [grp.seed_q(round_index) for grp in self.groups]
-        if res is not None:   # corrected vectors of every tensor, kept in r until the EF updates
+        # Without nmse, ef_apply rides in the first pass over each tensor (P = M Q for the
+        # compressed ones, the bypass fold for the small ones) and the residual update in the
+        # decode pass.  The nmse diagnostic needs every corrected vector before any residual
+        # changes, so then ef_apply runs as one pass up front and the EF updates come last.
+        fuse_ef = res is not None and acc is None
+        if res is not None and not fuse_ef:   # corrected vectors kept in r until the EF updates
             _native.call("gc_ef_apply", n, D, g.data_ptr(), res.data_ptr(), g.stride(0), res.data_ptr(),
                          res.stride(0), sp)
         c = res if res is not None else g
         bits = 0.0
         # dense-fp32 bypass of the small tensors (pipelines.py:326-336), one launch
         if self.bypass:
-            _native.call("gc_segment_fold_ef", n, len(self.bypass), self.seg_off.data_ptr(), self.seg_len.data_ptr(),
-                         c.data_ptr(), None, c.stride(0), est.data_ptr(), sp)
+            if fuse_ef:   # corrected = g + r formed in the fold; own == corrected, so r leaves as 0
+                _native.call("gc_segment_ef_fold", n, len(self.bypass), self.seg_off.data_ptr(),
+                             self.seg_len.data_ptr(), g.data_ptr(), res.data_ptr(), g.stride(0), est.data_ptr(), sp)
+            else:
+                _native.call("gc_segment_fold_ef", n, len(self.bypass), self.seg_off.data_ptr(),
+                             self.seg_len.data_ptr(), c.data_ptr(), None, c.stride(0), est.data_ptr(), sp)
             for t in self.bypass:
                 ledger.charge_ring("dense-bypass", n, self.sizes[t], 32)
                 bits += 32.0 * self.sizes[t]
-        # compressed tensors, batched by shape.  Without nmse the residual update rides in the
-        # decode pass; with nmse the estimates come first and the EF updates after it.
-        fuse_ef = res is not None and acc is None
         for grp, q in zip(self.groups, qs):
-            grp.set_ld(c.stride(0), grp.vec and c.data_ptr() % 16 == 0 and est.data_ptr() % 16 == 0)
-            grp.run(c.data_ptr(), res.data_ptr() if fuse_ef else None, est.data_ptr(), round_index,
-                    vec=bool(grp.batch.rows_aligned), fold=self._fold, q=q)
+            grp.set_ld(c.stride(0), grp.vec and c.data_ptr() % 16 == 0 and est.data_ptr() % 16 == 0
+                       and g.data_ptr() % 16 == 0 and g.stride(0) == c.stride(0))
+            if fuse_ef and grp.batch.rows_aligned:   # ef_apply inside the tcgen05 P = M Q pass
+                grp.run(c.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, grads_ptr=g.data_ptr(),
+                        vec=True, fold=self._fold, q=q, ef_resid_ptr=res.data_ptr())
+            elif fuse_ef:   # unaligned rows: ef_apply on the group's tensors, then the plain passes
+                for t in grp.tensor_ids:
+                    off = int(self.offsets[t])
+                    _native.call("gc_ef_apply", n, self.sizes[t], g.data_ptr() + 4 * off, res.data_ptr() + 4 * off,
+                                 g.stride(0), res.data_ptr() + 4 * off, res.stride(0), sp)
+                grp.run(c.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, vec=False, fold=self._fold, q=q)
+            else:
+                grp.run(c.data_ptr(), None, est.data_ptr(), round_index, vec=bool(grp.batch.rows_aligned),
+                        fold=self._fold, q=q)
             grp.saved = dict(grp.last)
             for t in grp.tensor_ids:
                 ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
@@ -197,7 +214,7 @@ class TensorListPipeline:
                 bits += 32.0 * grp.rank * (grp.rows + grp.cols)
         if acc is not None:
             _native.call("gc_nmse_accumulate", n, D, c.data_ptr(), None, c.stride(0), est.data_ptr(), acc.data_ptr(), sp)
-        if res is not None:
+        if res is not None and not fuse_ef:
             if self.bypass:   # own == corrected: residual 0
                 _native.call("gc_segment_fold_ef", n, len(self.bypass), self.seg_off.data_ptr(),
                              self.seg_len.data_ptr(), c.data_ptr(), res.data_ptr(), c.stride(0), est.data_ptr(), sp)

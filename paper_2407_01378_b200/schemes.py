@@ -497,12 +497,14 @@ class PowerSgdGroup:
         return q
 
     def run(self, c_ptr: int, resid_ptr, est_ptr: int, round_index: int, grads_ptr=None, vec=False, fold=None,
-            before_ef=None, q=None):
+            before_ef=None, q=None, ef_resid_ptr=None):
         """One round for the batch.  c_ptr: corrected matrices (or raw gradients when grads_ptr is
         given together with vec: ef_apply fused into P = M Q, corrected written over resid).
         fold(kind, x [T*L][m], m) -> [T][m] sums in the reference ring order (simulated: local fold;
         distributed: gather + fold).  before_ef() runs after the estimate, before the residuals
-        change (the nmse hook).  Returns warm Q [T][cols][r]."""
+        change (the nmse hook).  ef_resid_ptr (with grads_ptr and vec): ef_apply fused into
+        P = M Q, corrected written there (c_ptr must then point at it).  Returns warm Q
+        [T][cols][r]."""
         sp = _sp()
         T, L, n, d, rows, cols, r = self.T, self.L, self.n, self.d, self.rows, self.cols, self.rank
         dev = self.device
@@ -510,7 +512,10 @@ class PowerSgdGroup:
         if q is None:
             q = self.seed_q(round_index)
         p = torch.empty(T * L, rows, r, dtype=torch.float32, device=dev)
-        if vec and grads_ptr is not None:
+        if vec and ef_resid_ptr is not None:
+            _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, grads_ptr, ef_resid_ptr, q.data_ptr(),
+                         p.data_ptr(), self.ws.data_ptr(), sp)
+        elif vec and grads_ptr is not None:
             _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, grads_ptr, resid_ptr, q.data_ptr(), p.data_ptr(),
                          self.ws.data_ptr(), sp)
         elif vec:
@@ -527,7 +532,7 @@ class PowerSgdGroup:
         _native.call("gc_psgd_mtp", bref, d, rows, cols, r, c_ptr, p_hat.data_ptr(), qw.data_ptr(),
                      self.ws.data_ptr(), sp)
         q_sum = fold("right-factor", qw, cols * r).reshape(T, cols, r)
-        if vec and before_ef is None and resid_ptr is not None:
+        if before_ef is None and resid_ptr is not None:   # EF update and estimate in one pass
             _native.call("gc_psgd_decode_fused", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
                          q_sum.data_ptr(), resid_ptr, est_ptr, sp)
         else:

@@ -17,15 +17,16 @@ def _grads(n, D, rounds, seed):
     return [[rng.standard_normal(D).astype(np.float32) for _ in range(n)] for _ in range(rounds)]
 
 
+@pytest.mark.parametrize("nmse", [True, False])   # False: ef_apply fused into the first pass of each tensor
 @pytest.mark.parametrize("rank,warm", [(4, True), (2, False), (1, True)])
-def test_powersgd_per_tensor_matches_reference(rank, warm):
+def test_powersgd_per_tensor_matches_reference(rank, warm, nmse):
     import paper_2407_01378_b200 as gcb
     from paper_2407_01378_b200.multitensor import TensorListPipeline
     n, seed = 3, 51
     D = sum(SIZES)
     offs = np.concatenate([[0], np.cumsum(SIZES)[:-1]])
     grads = _grads(n, D, 3, seed)
-    pipe = TensorListPipeline(gcb.PowerSgdConfig(rank, warm), n, SIZES, gcb.SeedSpec(seed))
+    pipe = TensorListPipeline(gcb.PowerSgdConfig(rank, warm), n, SIZES, gcb.SeedSpec(seed), compute_nmse=nmse)
     results = [pipe.run_round(grads[r], r) for r in range(3)]
     for t, (off, s) in enumerate(zip(offs, SIZES)):
         outs = oracle_rounds("powersgd", dict(rank=rank, warm_start=warm),

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+python -m pytest tests/test_multitensor_gpu.py tests/test_chunked_psgd_gpu.py -q -m gpu -x > gpurun_out/pt12.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/gpt2m3_launches.csv python tools/prof_scheme.py psgd_gpt2m 0 8 2 > /dev/null 2>&1

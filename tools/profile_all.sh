@@ -26,7 +26,7 @@ lines() {  # name, kernel regex, source file, cmd...  -> per-source-line shares 
 for s in $schemes; do
   case $s in
     thc)     run thc     python tools/prof_thc.py ${THC_D:-25557032} 8 1 1
-             lines thc thc_fused paper_2407_01378_b200/csrc/gc_thc_fused.cu python tools/prof_thc.py 25557032 8 1 1 ;;
+             FN=${FN:-ILi10ELb1E} lines thc thc_fused paper_2407_01378_b200/csrc/gc_thc_fused.cu python tools/prof_thc.py 25557032 8 1 1 ;;
     topk)    run topk    python tools/prof_scheme.py topk 110000000 8 1 ;;
     topkc)   run topkc   python tools/prof_scheme.py topkc 110000000 8 1 ;;
     psgd)    run psgd    python tools/prof_scheme.py psgd 350000000 8 1 ;;
