@@ -41,6 +41,10 @@ constexpr int kSteps = kTileE / kNT;  // 16
 // per octave) keeps the boundary bin -- and so the candidate list -- small even when EF piles
 // many magnitudes up just below the threshold.
 constexpr int kBins0 = 8192, kShift0 = 18, kShift1 = 8;
+#ifndef GC_TOPK_H0_CTAS
+#define GC_TOPK_H0_CTAS 16
+#endif
+constexpr int kH0Ctas = GC_TOPK_H0_CTAS * 148;   // persistent level-0 CTAs per worker
 
 constexpr unsigned int kNoGuess = 0xFFFFFFFFu;
 
@@ -905,7 +909,7 @@ int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld
   GC_LAUNCH_CHECK("init_kernel");
   // pass 1: level 0 (optionally fused with ef_apply: values then live in resid, or in grads if EF is off)
   if (vec)
-    hist0_vec_kernel<<<dim3(static_cast<unsigned>(tiles < 4 * 148 ? tiles : 4 * 148), workers), kNT, 0, st>>>(
+    hist0_vec_kernel<<<dim3(static_cast<unsigned>(tiles < kH0Ctas ? tiles : kH0Ctas), workers), kNT, 0, st>>>(
         wk, len, values, ld, grads, resid, tiles);
   else
     hist_kernel<<<grid, kNT, 0, st>>>(wk, 0, len, values, ld, grads, resid);
