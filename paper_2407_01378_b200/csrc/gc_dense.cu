@@ -18,27 +18,93 @@ namespace {
 
 constexpr int kNT = 256;
 
-template <bool WIRE16, bool ROUND_IN>
+// MAXN: workers whose loads are issued up front (8 or 16; larger n: rolled loop)
+
+// One element's ordered fold over the n values x[0..n) already in registers, x[k] from worker
+// (s + k) mod n.
+template <bool WIRE16, bool ROUND_IN, int kMaxFold>
+__device__ __forceinline__ float fold_values(const float (&x)[kMaxFold], int n) {
+  float acc = ROUND_IN ? gc::fp16_round_trip(x[0]) : x[0];
+#pragma unroll
+  for (int k = 1; k < kMaxFold; ++k) {
+    if (k < n) {
+      const float v = ROUND_IN ? gc::fp16_round_trip(x[k]) : x[k];
+      const float sent = WIRE16 ? gc::fp16_round_trip(acc) : acc;
+      acc = sent + v;
+    }
+  }
+  if (WIRE16 && n > 1) acc = gc::fp16_round_trip(acc);
+  return acc;
+}
+
+template <bool WIRE16, bool ROUND_IN, int kMaxFold>
 __global__ void __launch_bounds__(kNT) float_fold_kernel(int n, int64_t len, const float *in, int64_t ld,
                                                          int64_t offset, int64_t ring_block, int divisor,
-                                                         float *out, int64_t in_stride, int64_t out_stride) {
+                                                         float *out, int64_t in_stride, int64_t out_stride,
+                                                         int vec) {
   in += blockIdx.y * in_stride;   // batch of independent folds
   out += blockIdx.y * out_stride;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < len;
-       e += static_cast<int64_t>(gridDim.x) * kNT) {
-    const int s = static_cast<int>((offset + e) / ring_block);
-    float acc = in[s * ld + e];
-    if (ROUND_IN) acc = gc::fp16_round_trip(acc);
-    int w = s;
-    for (int k = 1; k < n; ++k) {
-      w = (w + 1 == n) ? 0 : w + 1;
-      float x = in[w * ld + e];
-      if (ROUND_IN) x = gc::fp16_round_trip(x);
-      const float sent = WIRE16 ? gc::fp16_round_trip(acc) : acc;
-      acc = sent + x;
+  const float dv = static_cast<float>(divisor);
+  // vec: 4 elements per thread with float4 rows (ld, in, out 16-byte aligned); a group that
+  // straddles a ring-block boundary folds its elements one by one.  All n row loads of a group
+  // are issued before the fold (n <= kMaxFold), so each thread keeps n loads in flight.
+  const int64_t groups = vec ? (len + 3) / 4 : len;
+  for (int64_t gi = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; gi < groups;
+       gi += static_cast<int64_t>(gridDim.x) * kNT) {
+    const int64_t e0 = vec ? 4 * gi : gi;
+    const int s = static_cast<int>((offset + e0) / ring_block);
+    if (n <= kMaxFold && vec && e0 + 3 < len && (offset + e0 + 3) / ring_block == s) {
+      float4 x4[kMaxFold];
+      int w = s;
+#pragma unroll
+      for (int k = 0; k < kMaxFold; ++k) {
+        if (k < n) {
+          x4[k] = __ldcs(reinterpret_cast<const float4 *>(in + w * ld + e0));
+          w = (w + 1 == n) ? 0 : w + 1;
+        }
+      }
+      float r[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float x[kMaxFold];
+#pragma unroll
+        for (int k = 0; k < kMaxFold; ++k) x[k] = c == 0 ? x4[k].x : (c == 1 ? x4[k].y : (c == 2 ? x4[k].z : x4[k].w));
+        const float acc = fold_values<WIRE16, ROUND_IN, kMaxFold>(x, n);
+        r[c] = divisor > 0 ? acc / dv : acc;
+      }
+      __stcs(reinterpret_cast<float4 *>(out + e0), make_float4(r[0], r[1], r[2], r[3]));
+      continue;
     }
-    if (WIRE16 && n > 1) acc = gc::fp16_round_trip(acc);
-    out[e] = divisor > 0 ? acc / static_cast<float>(divisor) : acc;
+    const int64_t e1 = vec ? min(e0 + 4, len) : e0 + 1;
+    for (int64_t e = e0; e < e1; ++e) {
+      const int se = static_cast<int>((offset + e) / ring_block);
+      float acc;
+      if (n <= kMaxFold) {
+        float x[kMaxFold];
+        int w = se;
+#pragma unroll
+        for (int k = 0; k < kMaxFold; ++k) {
+          if (k < n) {
+            x[k] = in[w * ld + e];
+            w = (w + 1 == n) ? 0 : w + 1;
+          }
+        }
+        acc = fold_values<WIRE16, ROUND_IN, kMaxFold>(x, n);
+      } else {
+        acc = in[se * ld + e];
+        if (ROUND_IN) acc = gc::fp16_round_trip(acc);
+        int w = se;
+        for (int k = 1; k < n; ++k) {
+          w = (w + 1 == n) ? 0 : w + 1;
+          float x = in[w * ld + e];
+          if (ROUND_IN) x = gc::fp16_round_trip(x);
+          const float sent = WIRE16 ? gc::fp16_round_trip(acc) : acc;
+          acc = sent + x;
+        }
+        if (WIRE16 && n > 1) acc = gc::fp16_round_trip(acc);
+      }
+      out[e] = divisor > 0 ? acc / dv : acc;
+    }
   }
 }
 
@@ -99,19 +165,28 @@ int grid_for(int64_t work) {
 int fold_launch(int32_t batch, int32_t n, int64_t len, const float *inputs, int64_t ld, int64_t in_stride,
                 int64_t offset, int64_t ring_block, int32_t wire_fp16, int32_t round_inputs, int32_t divisor,
                 float *out, int64_t out_stride, cudaStream_t st) {
-  const dim3 g(grid_for(len), batch);
-  if (wire_fp16 && round_inputs)
-    float_fold_kernel<true, true><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out, in_stride,
-                                                     out_stride);
-  else if (wire_fp16)
-    float_fold_kernel<true, false><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out,
-                                                      in_stride, out_stride);
-  else if (round_inputs)
-    float_fold_kernel<false, true><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out,
-                                                      in_stride, out_stride);
-  else
-    float_fold_kernel<false, false><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out,
-                                                       in_stride, out_stride);
+  const int vec = (ld % 4) == 0 && (in_stride % 4) == 0 && (out_stride % 4) == 0 &&
+                  ((reinterpret_cast<uintptr_t>(inputs) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const dim3 g(grid_for(vec ? (len + 3) / 4 : len), batch);
+#define GC_FOLD(W, R, M)                                                                                 \
+  float_fold_kernel<W, R, M><<<g, kNT, 0, st>>>(n, len, inputs, ld, offset, ring_block, divisor, out, in_stride, \
+                                                out_stride, vec)
+#define GC_FOLD_N(W, R) \
+  if (n <= 8)           \
+    GC_FOLD(W, R, 8);   \
+  else                  \
+    GC_FOLD(W, R, 16);
+  if (wire_fp16 && round_inputs) {
+    GC_FOLD_N(true, true)
+  } else if (wire_fp16) {
+    GC_FOLD_N(true, false)
+  } else if (round_inputs) {
+    GC_FOLD_N(false, true)
+  } else {
+    GC_FOLD_N(false, false)
+  }
+#undef GC_FOLD_N
+#undef GC_FOLD
   GC_LAUNCH_CHECK("float_fold_kernel");
   return GC_OK;
 }
