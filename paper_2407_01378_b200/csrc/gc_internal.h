@@ -22,7 +22,7 @@ void gc_set_error(const std::string &msg);
 // tcgen05 P = M Q pass (gc_psgd_umma.cu): fp64 split-K partials; returns the split count.
 int gc_psgd_mq_umma_launch(int32_t L, int32_t workers, const int64_t *row_offsets, int64_t ld, int64_t d,
                            int64_t rows, int64_t cols, int32_t rank, const float *grads, float *resid, const float *q,
-                           double *partial, cudaStream_t st);
+                           double *partial, int a16, cudaStream_t st);
 #define GC_LAUNCH_CHECK(what)                                                     \
   do {                                                                            \
     cudaError_t e_ = cudaGetLastError();                                          \

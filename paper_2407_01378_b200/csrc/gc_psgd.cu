@@ -290,8 +290,9 @@ constexpr int kMtpFold = 32;
 template <bool A16>
 __device__ __forceinline__ float4 ld4(const float *p, int nv) {
   if (A16) return __ldcs(reinterpret_cast<const float4 *>(p));
-  return make_float4(nv > 0 ? __ldcs(p) : 0.0f, nv > 1 ? __ldcs(p + 1) : 0.0f, nv > 2 ? __ldcs(p + 2) : 0.0f,
-                     nv > 3 ? __ldcs(p + 3) : 0.0f);
+  // plain (L1-allocating) loads: the 4 scalar instructions of a warp touch the same sectors, so
+  // the second to fourth are L1 hits instead of 4x the L2 traffic of evict-first loads
+  return make_float4(nv > 0 ? p[0] : 0.0f, nv > 1 ? p[1] : 0.0f, nv > 2 ? p[2] : 0.0f, nv > 3 ? p[3] : 0.0f);
 }
 template <bool A16>
 __device__ __forceinline__ void st4(float *p, float4 v, int nv) {
@@ -299,10 +300,10 @@ __device__ __forceinline__ void st4(float *p, float4 v, int nv) {
     __stcs(reinterpret_cast<float4 *>(p), v);
     return;
   }
-  if (nv > 0) __stcs(p, v.x);
-  if (nv > 1) __stcs(p + 1, v.y);
-  if (nv > 2) __stcs(p + 2, v.z);
-  if (nv > 3) __stcs(p + 3, v.w);
+  if (nv > 0) p[0] = v.x;
+  if (nv > 1) p[1] = v.y;
+  if (nv > 2) p[2] = v.z;
+  if (nv > 3) p[3] = v.w;
 }
 
 template <int R, bool A16>
@@ -576,13 +577,13 @@ int gc_psgd_mq_fused(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t co
                      float *resid, const float *q, float *p, void *workspace, void *stream) {
   if (int rc = check_batch(b)) return rc;
   GC_REQUIRE(d >= 1 && rows * cols >= d && grads && q && p && workspace, "invalid argument");
-  GC_REQUIRE(cols % 4 == 0 && b->rows_aligned, "mq_fused needs cols % 4 == 0 and 16-byte aligned rows");
+  const bool a16 = cols % 4 == 0 && b->rows_aligned;   // else the masked-scalar producer
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int L = b->tensors * b->workers;
   int slabs = static_cast<int>((cols + 1023) / 1024);
   double *partial = static_cast<double *>(workspace);
   const char *impl = getenv("GC_PSGD_MQ");
-  if (impl && std::string(impl) == "cores") {
+  if (impl && std::string(impl) == "cores" && a16) {
     GC_RANK_SWITCH(rank, ({
       mq_fused_kernel<R><<<dim3(slabs, grid_cap((rows + kMqRows - 1) / kMqRows), L), 256, 0, st>>>(
           d, rows, cols, grads, resid, rows_of(b), q, partial, slabs);
@@ -591,7 +592,7 @@ int gc_psgd_mq_fused(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t co
   } else {
     // tcgen05 (kind::tf32, 3xTF32) band GEMM fused with ef_apply (gc_psgd_umma.cu)
     slabs = gc_psgd_mq_umma_launch(L, b->workers, b->row_offsets, b->ld, d, rows, cols, rank, grads, resid, q,
-                                   partial, st);
+                                   partial, a16 ? 1 : 0, st);
     if (slabs < 0) return slabs;
   }
   const int64_t total = static_cast<int64_t>(L) * rows * rank;

@@ -103,7 +103,10 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                : "memory");
 }
 
-template <int R>
+// A16: rows are 16-byte aligned and cols % 4 == 0 (float4 accesses); otherwise every thread's 4
+// columns go as plain (L1-allocating) scalars masked to the row (nv = columns left in the row
+// and before d): the 4 scalar instructions of a warp share sectors, so L1 absorbs the repeats.
+template <int R, bool A16>
 __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t rows, int64_t cols, const float *g,
                                                               float *r, Rows rw_, const float *q, double *partial,
                                                               int splits, int64_t chunks_per_split) {
@@ -189,7 +192,18 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
       const int64_t i = grow * cols + col;
       pg[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       pr[u] = pg[u];
-      if (grow < rows && col < cols) {
+      if (!A16 && grow < rows && col < cols) {
+        const int nv = static_cast<int>(min(min(static_cast<int64_t>(4), cols - col), d - i));
+        float t[4] = {0.f, 0.f, 0.f, 0.f}, t2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (e < nv) {
+            t[e] = gw[i + e];
+            if (rw) t2[e] = rw[i + e];
+          }
+        pg[u] = make_float4(t[0], t[1], t[2], t[3]);
+        pr[u] = make_float4(t2[0], t2[1], t2[2], t2[3]);
+      } else if (A16 && grow < rows && col < cols) {
         if (i + 3 < d) {
           pg[u] = __ldcs(reinterpret_cast<const float4 *>(gw + i));
           if (rw) pr[u] = __ldcs(reinterpret_cast<const float4 *>(rw + i));
@@ -225,7 +239,13 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
       float4 c = cg[u];
       if (rw) {
         c.x = c.x + cr[u].x; c.y = c.y + cr[u].y; c.z = c.z + cr[u].z; c.w = c.w + cr[u].w;
-        if (grow < rows && col < cols) {
+        if (!A16 && grow < rows && col < cols) {
+          const int nv = static_cast<int>(min(min(static_cast<int64_t>(4), cols - col), d - i));
+          const float cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e < nv) rw[i + e] = cv[e];
+        } else if (A16 && grow < rows && col < cols) {
           if (i + 3 < d) {
             __stcs(reinterpret_cast<float4 *>(rw + i), c);   // corrected kept in r for the later passes
           } else {
@@ -308,7 +328,7 @@ int grid_cap(int64_t g) { return static_cast<int>(g < 1 ? 1 : (g > 65535 ? 65535
 // workspace the caller sized) or a negative status.
 int gc_psgd_mq_umma_launch(int32_t L, int32_t workers, const int64_t *row_offsets, int64_t ld, int64_t d,
                            int64_t rows, int64_t cols, int32_t rank, const float *grads, float *resid, const float *q,
-                           double *partial, cudaStream_t st) {
+                           double *partial, int a16, cudaStream_t st) {
   const int64_t row_blocks = (rows + kM - 1) / kM;
   const int64_t nchunks = (cols + kKc - 1) / kKc;
   const int64_t max_splits = (cols + 1023) / 1024;
@@ -319,11 +339,17 @@ int gc_psgd_mq_umma_launch(int32_t L, int32_t workers, const int64_t *row_offset
   splits = (nchunks + per - 1) / per;
   Rows rw{row_offsets, ld, workers};
   const dim3 grid(grid_cap(row_blocks), static_cast<unsigned>(splits), static_cast<unsigned>(L));
-#define GC_UMMA_CASE(RR)                                                                                  \
-  case RR:                                                                                                \
-    cudaFuncSetAttribute(mq_umma_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);   \
-    mq_umma_kernel<RR><<<grid, kThreads, kSmemBytes, st>>>(d, rows, cols, grads, resid, rw, q, partial,   \
-                                                           static_cast<int>(splits), per);                \
+#define GC_UMMA_LAUNCH(RR, AA)                                                                             \
+  cudaFuncSetAttribute(mq_umma_kernel<RR, AA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);   \
+  mq_umma_kernel<RR, AA><<<grid, kThreads, kSmemBytes, st>>>(d, rows, cols, grads, resid, rw, q, partial,   \
+                                                             static_cast<int>(splits), per);
+#define GC_UMMA_CASE(RR)        \
+  case RR:                      \
+    if (a16) {                  \
+      GC_UMMA_LAUNCH(RR, true)  \
+    } else {                    \
+      GC_UMMA_LAUNCH(RR, false) \
+    }                           \
     break;
   switch (rank) {
     GC_UMMA_CASE(1) GC_UMMA_CASE(2) GC_UMMA_CASE(3) GC_UMMA_CASE(4) GC_UMMA_CASE(5) GC_UMMA_CASE(6)
@@ -333,6 +359,7 @@ int gc_psgd_mq_umma_launch(int32_t L, int32_t workers, const int64_t *row_offset
       return GC_ERR_UNSUPPORTED;
   }
 #undef GC_UMMA_CASE
+#undef GC_UMMA_LAUNCH
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     gc_set_error(std::string("mq_umma_kernel: ") + cudaGetErrorString(e));

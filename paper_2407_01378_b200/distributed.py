@@ -369,7 +369,7 @@ class _Chunked(_Base):
         self.C, self.J = cfg.chunk_size, cfg.chunks_selected
         self.nc = -(-self.dim // self.C)
         ws = int(_native.lib().gc_topk_workspace_bytes(1, self.nc))
-        self.ws = torch.empty(ws, dtype=torch.uint8, device=self.dev)
+        self.ws = torch.zeros(ws, dtype=torch.uint8, device=self.dev)   # zeroed: no threshold hint yet
 
     def run(self, g, res, r, ledger, nmse):
         L, n, d, C, J, nc = self.L, self.n, self.dim, self.C, self.J, self.nc

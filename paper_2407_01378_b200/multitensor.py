@@ -20,7 +20,7 @@ from . import _native
 from .configs import PowerSgdConfig, matrix_shape_for, scheme_label
 from .ledger import TrafficLedger, WorkerGroup
 from .pipeline import RoundResult
-from .schemes import PowerSgdGroup, RoundStats, _simple_stats, make_engine, nmse_from
+from .schemes import PowerSgdGroup, RoundStats, _simple_stats, make_engine, nmse_from, umma_unaligned
 from .vectors import GradientVector, SeedSpec
 
 
@@ -195,9 +195,9 @@ class TensorListPipeline:
         for grp, q in zip(self.groups, qs):
             grp.set_ld(c.stride(0), grp.vec and c.data_ptr() % 16 == 0 and est.data_ptr() % 16 == 0
                        and g.data_ptr() % 16 == 0 and g.stride(0) == c.stride(0))
-            if fuse_ef and grp.batch.rows_aligned:   # ef_apply inside the tcgen05 P = M Q pass
+            if fuse_ef and (grp.batch.rows_aligned or umma_unaligned()):   # ef_apply inside the tcgen05 P = M Q
                 grp.run(c.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, grads_ptr=g.data_ptr(),
-                        vec=True, fold=self._fold, q=q, ef_resid_ptr=res.data_ptr())
+                        vec=bool(grp.batch.rows_aligned), fold=self._fold, q=q, ef_resid_ptr=res.data_ptr())
             elif fuse_ef:   # unaligned rows: ef_apply on the group's tensors, then the plain passes
                 for t in grp.tensor_ids:
                     off = int(self.offsets[t])

@@ -9,6 +9,7 @@ RoundStats) and charges the round's closed-form traffic to the ledger.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 
 import torch
@@ -356,7 +357,7 @@ class ChunkedEngine(Engine):
         self.J = cfg.chunks_selected
         self.nc = -(-dim // self.C)
         ws = int(_native.lib().gc_topk_workspace_bytes(1, self.nc))
-        self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
+        self.ws = torch.zeros(ws, dtype=torch.uint8, device=device)   # zeroed: no threshold hint yet
         self._work = None
 
     def _perm(self, round_index):
@@ -417,6 +418,12 @@ class ChunkedEngine(Engine):
 
 
 # ----------------------------------------------------------------------------- PowerSGD
+def umma_unaligned() -> bool:
+    """P = M Q for unaligned rows on the tcgen05 kernel (masked scalar producer, ef_apply fused)
+    rather than ef_apply + the fp64 CUDA-core kernel; GC_PSGD_MQ_UNALIGNED=cores selects the latter."""
+    return os.environ.get("GC_PSGD_MQ_UNALIGNED", "umma") != "cores"
+
+
 class PowerSgdGroup:
     """T independent PowerSGD pipelines of the same length d (hence the same rows x cols),
     L workers each, run as one batch of kernels (pipelines.py:338-368 per tensor).
@@ -512,13 +519,15 @@ class PowerSgdGroup:
         if q is None:
             q = self.seed_q(round_index)
         p = torch.empty(T * L, rows, r, dtype=torch.float32, device=dev)
-        if vec and ef_resid_ptr is not None:
+        # P = M Q on tcgen05: float4 producer for aligned rows, masked scalars otherwise
+        umma = vec or umma_unaligned()
+        if umma and ef_resid_ptr is not None:
             _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, grads_ptr, ef_resid_ptr, q.data_ptr(),
                          p.data_ptr(), self.ws.data_ptr(), sp)
-        elif vec and grads_ptr is not None:
+        elif umma and grads_ptr is not None:
             _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, grads_ptr, resid_ptr, q.data_ptr(), p.data_ptr(),
                          self.ws.data_ptr(), sp)
-        elif vec:
+        elif umma:
             _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, c_ptr, None, q.data_ptr(), p.data_ptr(),
                          self.ws.data_ptr(), sp)
         else:
@@ -592,7 +601,8 @@ class PowerSgdEngine(Engine):
         grp = self.group
         lib = _native.lib()
         fuse_ef = bool(res is not None and grads.stride(0) == res.stride(0) and
-                       lib.gc_psgd_vectorizable(grp.cols, grads.data_ptr(), res.data_ptr(), grads.stride(0)))
+                       (umma_unaligned() or
+                        lib.gc_psgd_vectorizable(grp.cols, grads.data_ptr(), res.data_ptr(), grads.stride(0))))
         if fuse_ef:   # ef_apply fused into P = M Q
             c, gptr = res, grads.data_ptr()
         else:
