@@ -284,26 +284,39 @@ __global__ void mq_reduce_kernel(int L, int slabs, int64_t rows, int R, const do
 // groups (~1e-7 relative, the reference itself is fp32 BLAS).
 constexpr int kMtpFold = 32;
 
-// A thread's 4 consecutive columns of one row: one float4 when rows are 16-byte aligned (A16),
-// else 4 coalesced scalar accesses guarded by nv = the columns left in the row (the last thread
-// of a row whose length is not a multiple of 4).
+// A thread's 4 columns of one row.  A16 (cols % 4 == 0, 16-byte aligned rows): 4 consecutive
+// columns as one float4.  Otherwise columns base + 256k (k = 0..3), so every scalar access of a
+// warp covers 32 consecutive columns (coalesced); vm bit k = column k exists.
 template <bool A16>
-__device__ __forceinline__ float4 ld4(const float *p, int nv) {
+__device__ __forceinline__ int64_t col_off(int k) { return A16 ? k : 256 * k; }
+template <bool A16>
+__device__ __forceinline__ float4 ldc(const float *p, unsigned vm) {
   if (A16) return __ldcs(reinterpret_cast<const float4 *>(p));
-  // plain (L1-allocating) loads: the 4 scalar instructions of a warp touch the same sectors, so
-  // the second to fourth are L1 hits instead of 4x the L2 traffic of evict-first loads
-  return make_float4(nv > 0 ? p[0] : 0.0f, nv > 1 ? p[1] : 0.0f, nv > 2 ? p[2] : 0.0f, nv > 3 ? p[3] : 0.0f);
+  return make_float4(vm & 1u ? __ldcs(p) : 0.0f, vm & 2u ? __ldcs(p + 256) : 0.0f, vm & 4u ? __ldcs(p + 512) : 0.0f,
+                     vm & 8u ? __ldcs(p + 768) : 0.0f);
 }
 template <bool A16>
-__device__ __forceinline__ void st4(float *p, float4 v, int nv) {
+__device__ __forceinline__ void stc(float *p, float4 v, unsigned vm) {
   if (A16) {
     __stcs(reinterpret_cast<float4 *>(p), v);
     return;
   }
-  if (nv > 0) p[0] = v.x;
-  if (nv > 1) p[1] = v.y;
-  if (nv > 2) p[2] = v.z;
-  if (nv > 3) p[3] = v.w;
+  if (vm & 1u) __stcs(p, v.x);
+  if (vm & 2u) __stcs(p + 256, v.y);
+  if (vm & 4u) __stcs(p + 512, v.z);
+  if (vm & 8u) __stcs(p + 768, v.w);
+}
+// the thread's first column, its valid-column mask and the offset of its last valid column
+template <bool A16>
+__device__ __forceinline__ int64_t thread_cols(int64_t cols, unsigned &vm, int64_t &last) {
+  const int64_t col = A16 ? (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * 4
+                          : static_cast<int64_t>(blockIdx.x) * 1024 + threadIdx.x;
+  vm = 0;
+  last = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (col + col_off<A16>(k) < cols) vm |= 1u << k, last = col_off<A16>(k);
+  return col;
 }
 
 template <int R, bool A16>
@@ -315,7 +328,9 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
   __shared__ __align__(16) float ps[kChunk * RP];
   const int w = blockIdx.z;
   const int s = blockIdx.y;
-  const int64_t col = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * 4;
+  unsigned vm;
+  int64_t lastoff;
+  const int64_t col = thread_cols<A16>(cols, vm, lastoff);
   const int64_t r0 = s * rows_per_split;
   const int64_t r1 = min(rows, r0 + rows_per_split);
   const float *cw = c + rw_.at(w);
@@ -334,11 +349,10 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
       ps[e] = b < R ? ph[(i0 + ii) * R + b] : 0.0f;
     }
     __syncthreads();
-    if (col < cols) {
-      // rows whose 4 columns all lie below d load without per-row checks, so the unrolled loads
+    if (vm) {
+      // rows whose columns all lie below d load without per-row checks, so the unrolled loads
       // of a fold group are all in flight together (a per-row branch serialised them)
-      const bool full = (i0 + ni - 1) * cols + col + 3 < d;
-      const int nv = static_cast<int>(min(static_cast<int64_t>(4), cols - col));
+      const bool full = (i0 + ni - 1) * cols + col + lastoff < d;
       for (int g0 = 0; g0 < ni; g0 += kMtpFold) {
         const int g1 = min(ni, g0 + kMtpFold);
         auto row_fma = [&](int ii, const float4 m) {
@@ -359,17 +373,17 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
           const float *src = cw + (i0 + g0) * cols + col;
 #pragma unroll 8
           for (int ii = 0; ii < kMtpFold; ++ii)
-            row_fma(g0 + ii, ld4<A16>(src + ii * cols, nv));
+            row_fma(g0 + ii, ldc<A16>(src + ii * cols, vm));
         } else {
           for (int ii = g0; ii < g1; ++ii) {
             const int64_t i = (i0 + ii) * cols + col;
             float4 m;
-            if (i + 3 < d) {
-              m = ld4<A16>(cw + i, nv);
+            if (i + lastoff < d) {
+              m = ldc<A16>(cw + i, vm);
             } else {
               float t4[4] = {0.f, 0.f, 0.f, 0.f};
               for (int t = 0; t < 4; ++t)
-                if (i + t < d && t < nv) t4[t] = cw[i + t];
+                if (((vm >> t) & 1u) && i + col_off<A16>(t) < d) t4[t] = cw[i + col_off<A16>(t)];
               m = make_float4(t4[0], t4[1], t4[2], t4[3]);
             }
             row_fma(ii, m);
@@ -385,15 +399,13 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
       }
     }
   }
-  if (col < cols) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (col + t < cols) {
+  for (int t = 0; t < 4; ++t)
+    if ((vm >> t) & 1u) {
 #pragma unroll
-        for (int b = 0; b < R; ++b)
-          partial[((static_cast<int64_t>(w) * splits + s) * cols + col + t) * R + b] = acc[t][b];
-      }
-  }
+      for (int b = 0; b < R; ++b)
+        partial[((static_cast<int64_t>(w) * splits + s) * cols + col + col_off<A16>(t)) * R + b] = acc[t][b];
+    }
 }
 
 // Decode with a CTA per (1024-column slab, 64-row chunk): a thread keeps the Q rows of its 4
@@ -413,24 +425,25 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
     qsum += static_cast<int64_t>(t) * cols * R;
     if (est) est += est_offs ? est_offs[t] : 0;
   }
-  const int64_t col = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * 4;
+  unsigned vm;
+  int64_t lastoff;
+  const int64_t col = thread_cols<A16>(cols, vm, lastoff);
   const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kDecRows;
   const int nrows = static_cast<int>(min(static_cast<int64_t>(kDecRows), rows - row0));
   for (int e = threadIdx.x; e < nrows * R; e += 256) ps[e] = ph[row0 * R + e];
   __syncthreads();
-  if (col >= cols) return;
-  const int nv = static_cast<int>(min(static_cast<int64_t>(4), cols - col));   // columns of this thread
+  if (!vm) return;
   for (int w = 0; w <= L; ++w) {   // w == L: the estimate with Q_sum
     const float *qsrc = w < L ? qw + static_cast<int64_t>(w) * cols * R : qsum;
     float qv[4][R];
 #pragma unroll
     for (int t = 0; t < 4; ++t)
 #pragma unroll
-      for (int b = 0; b < R; ++b) qv[t][b] = col + t < cols ? qsrc[(col + t) * R + b] : 0.0f;
+      for (int b = 0; b < R; ++b) qv[t][b] = ((vm >> t) & 1u) ? qsrc[(col + col_off<A16>(t)) * R + b] : 0.0f;
     if (w < L && !resid) continue;
     if (w == L && !est) continue;
     float *dst = w < L ? resid + rw_.at(blockIdx.z * L + w) : est;
-    if ((row0 + nrows - 1) * cols + col + 3 < d) {   // whole block in range: branch-free
+    if ((row0 + nrows - 1) * cols + col + lastoff < d) {   // whole block in range: branch-free
       // rows go in batches of 8: the 8 loads of c are issued before any store (the compiler
       // cannot prove that a store to row a does not alias the load of row a + 1)
       const float nf = static_cast<float>(n);
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
         if (w < L) {
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            if (u < nb) cv[u] = ld4<A16>(dst + (row0 + a0 + u) * cols + col, nv);
+            if (u < nb) cv[u] = ldc<A16>(dst + (row0 + a0 + u) * cols + col, vm);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -459,9 +472,9 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
           }
           float *o = dst + (row0 + a) * cols + col;
           if (w < L)
-            st4<A16>(o, make_float4(cv[u].x - o4[0], cv[u].y - o4[1], cv[u].z - o4[2], cv[u].w - o4[3]), nv);
+            stc<A16>(o, make_float4(cv[u].x - o4[0], cv[u].y - o4[1], cv[u].z - o4[2], cv[u].w - o4[3]), vm);
           else
-            st4<A16>(o, make_float4(o4[0] / nf, o4[1] / nf, o4[2] / nf, o4[3] / nf), nv);
+            stc<A16>(o, make_float4(o4[0] / nf, o4[1] / nf, o4[2] / nf, o4[3] / nf), vm);
         }
       }
       continue;
@@ -490,8 +503,10 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
           __stcs(reinterpret_cast<float4 *>(dst + i), make_float4(o4[0] / nf, o4[1] / nf, o4[2] / nf, o4[3] / nf));
         }
       } else {
-        for (int t = 0; t < 4; ++t)
-          if (t < nv && i + t < d) dst[i + t] = w < L ? dst[i + t] - o4[t] : o4[t] / static_cast<float>(n);
+        for (int t = 0; t < 4; ++t) {
+          const int64_t it = i + col_off<A16>(t);
+          if (((vm >> t) & 1u) && it < d) dst[it] = w < L ? dst[it] - o4[t] : o4[t] / static_cast<float>(n);
+        }
       }
     }
   }
