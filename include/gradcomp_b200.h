@@ -183,6 +183,12 @@ int gc_topk_select(int32_t workers, int64_t len, const float *values, int64_t ld
  * worker order (f32, the np.add.at order).  Dividing by n is gc_scale_div. */
 int gc_sparse_accumulate(int32_t workers, int64_t k, const int32_t *idx, const float *val, int64_t dim,
                          float *estimate, void *stream);
+/* The same aggregation with the mean in one dense pass: estimate = (worker-order f32 sums) /
+ * divisor, every coordinate written once (pipelines.py:204-211).  idx ascending per worker (as
+ * gc_topk_select emits); workspace: gc_sparse_mean_workspace_bytes (per-tile entry starts). */
+int64_t gc_sparse_mean_workspace_bytes(int32_t workers, int64_t dim);
+int gc_sparse_mean(int32_t workers, int64_t k, const int32_t *idx, const float *val, int64_t dim, int32_t divisor,
+                   float *estimate, void *workspace, void *stream);
 /* ef_update with a sparse own payload (compressors.py:629-631, 406-409): resid[w][idx] -= val. */
 int gc_sparse_ef_update(int32_t workers, int64_t k, const int32_t *idx, const float *val, float *resid, int64_t ld,
                         void *stream);

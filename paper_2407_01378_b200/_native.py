@@ -95,6 +95,8 @@ SIGNATURES = {
     "gc_topk_select": (c_int, [I32, I64, P, I64, I64, P, P, P, P, I32, P, P]),
     "gc_encode_sparse_payloads": (c_int, [I32, I64, P, P, P, I64, P]),
     "gc_sparse_accumulate": (c_int, [I32, I64, P, P, I64, P, P]),
+    "gc_sparse_mean_workspace_bytes": (c_int64, [I32, I64]),
+    "gc_sparse_mean": (c_int, [I32, I64, P, P, I64, I32, P, P, P]),
     "gc_sparse_ef_update": (c_int, [I32, I64, P, P, P, I64, P]),
     # TopK-Chunked
     "gc_ef_apply": (c_int, [I32, I64, P, P, I64, P, I64, P]),

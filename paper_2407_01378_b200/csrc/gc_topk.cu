@@ -840,6 +840,49 @@ __global__ void scatter_add_kernel(int64_t k, const int32_t *idx, const float *v
     acc[idx[e]] += val[e];
 }
 
+// Tiled sparse mean (pipelines.py:204-211 + the / n): estimate tile t (4096 coordinates) is
+// built in shared memory from each worker's entries in [start[w][t], start[w][t+1]) -- worker by
+// worker, so every coordinate sees the np.add.at order -- and written once, divided by n.  The
+// payload indices are ascending per worker, so the tile starts come from one pass over them.
+__global__ void sparse_tile_starts_kernel(int L, int64_t k, const int32_t *idx, int64_t tiles, int32_t *start) {
+  const int w = blockIdx.y;
+  const int32_t *iw = idx + w * k;
+  int32_t *sw = start + w * (tiles + 1);
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; j <= k;
+       j += static_cast<int64_t>(gridDim.x) * kNT) {
+    // entry j opens tiles (tile(idx[j-1]), tile(idx[j])]; j == k closes the list
+    const int64_t lo = j == 0 ? -1 : iw[j - 1] / kTileE;
+    const int64_t hi = j == k ? tiles : iw[j] / kTileE;
+    for (int64_t t = lo + 1; t <= hi; ++t) sw[t] = static_cast<int32_t>(j);
+  }
+}
+
+__global__ void __launch_bounds__(kNT) sparse_mean_kernel(int L, int64_t k, const int32_t *idx, const float *val,
+                                                          int64_t dim, int64_t tiles, const int32_t *start,
+                                                          int divisor, float *est) {
+  __shared__ __align__(16) float acc[kTileE];
+  const float dv = static_cast<float>(divisor);
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t base = t * kTileE;
+    for (int i = threadIdx.x; i < kTileE; i += kNT) acc[i] = 0.0f;
+    __syncthreads();
+    for (int w = 0; w < L; ++w) {   // worker order; indices are unique within a worker
+      const int32_t j0 = start[w * (tiles + 1) + t], j1 = start[w * (tiles + 1) + t + 1];
+      for (int32_t j = j0 + threadIdx.x; j < j1; j += kNT) acc[idx[w * k + j] - base] += val[w * k + j];
+      __syncthreads();
+    }
+    if (base + kTileE <= dim && (reinterpret_cast<uintptr_t>(est) & 15) == 0) {
+      for (int i = threadIdx.x; i < kTileE / 4; i += kNT) {
+        const float4 a = reinterpret_cast<const float4 *>(acc)[i];
+        __stcs(reinterpret_cast<float4 *>(est + base) + i, make_float4(a.x / dv, a.y / dv, a.z / dv, a.w / dv));
+      }
+    } else {
+      for (int i = threadIdx.x; i < kTileE && base + i < dim; i += kNT) est[base + i] = acc[i] / dv;
+    }
+    __syncthreads();
+  }
+}
+
 // resid[idx] = resid[idx] - val (ef_update at the selected coordinates; elsewhere own = 0).
 __global__ void sparse_ef_kernel(int L, int64_t k, const int32_t *idx, const float *val, float *resid, int64_t ld) {
   const int w = blockIdx.y;
@@ -952,6 +995,25 @@ int gc_sparse_accumulate(int32_t workers, int64_t k, const int32_t *idx, const f
     scatter_add_kernel<<<grid_for(k), kNT, 0, st>>>(k, idx + w * k, val + w * k, estimate);
   }
   GC_LAUNCH_CHECK("scatter_add_kernel");
+  return GC_OK;
+}
+
+int64_t gc_sparse_mean_workspace_bytes(int32_t workers, int64_t dim) {
+  return static_cast<int64_t>(workers) * ((dim + kTileE - 1) / kTileE + 1) * 4;
+}
+
+int gc_sparse_mean(int32_t workers, int64_t k, const int32_t *idx, const float *val, int64_t dim, int32_t divisor,
+                   float *estimate, void *workspace, void *stream) {
+  GC_REQUIRE(workers >= 1 && workers <= 65535 && k >= 0 && k <= 0x7fffffff && dim >= 1 && dim <= 0x7fffffff &&
+                 divisor >= 1 && estimate && workspace && (k == 0 || (idx && val)),
+             "invalid argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t tiles = (dim + kTileE - 1) / kTileE;
+  int32_t *start = static_cast<int32_t *>(workspace);
+  sparse_tile_starts_kernel<<<dim3(grid_for(k + 1), workers), kNT, 0, st>>>(workers, k, idx, tiles, start);
+  sparse_mean_kernel<<<static_cast<unsigned>(tiles < 16 * 148 ? tiles : 16 * 148), kNT, 0, st>>>(
+      workers, k, idx, val, dim, tiles, start, divisor, estimate);
+  GC_LAUNCH_CHECK("sparse_mean_kernel");
   return GC_OK;
 }
 

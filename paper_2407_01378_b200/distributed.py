@@ -342,6 +342,8 @@ class _TopK(_Base):
         self.k = cfg.k
         ws = int(_native.lib().gc_topk_workspace_bytes(self.L, self.dim))
         self.ws = torch.zeros(ws, dtype=torch.uint8, device=self.dev)   # zeroed: no threshold hint yet
+        mws = int(_native.lib().gc_sparse_mean_workspace_bytes(self.n, self.dim))
+        self.mean_ws = torch.empty(mws, dtype=torch.uint8, device=self.dev)
 
     def run(self, g, res, r, ledger, nmse):
         L, k, d, n = self.L, self.k, self.dim, self.n
@@ -355,8 +357,8 @@ class _TopK(_Base):
         all_idx = self.comm.all_gather_rows(idx)     # all_gather (collectives.py:239-263)
         all_val = self.comm.all_gather_rows(val)
         est = torch.empty(d, dtype=torch.float32, device=self.dev)
-        _native.call("gc_sparse_accumulate", n, k, all_idx.data_ptr(), all_val.data_ptr(), d, est.data_ptr(), sp)
-        _native.call("gc_scale_div", d, est.data_ptr(), n, est.data_ptr(), sp)
+        _native.call("gc_sparse_mean", n, k, all_idx.data_ptr(), all_val.data_ptr(), d, n, est.data_ptr(),
+                     self.mean_ws.data_ptr(), sp)
         self.launches += 11 + n
         ledger.charge_gather("sparse-gather", [48 * k] * n)
         return est, float(48 * k), _simple_stats(None)

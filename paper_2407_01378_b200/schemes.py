@@ -309,6 +309,8 @@ class TopKEngine(Engine):
         self.k = cfg.k
         ws = int(_native.lib().gc_topk_workspace_bytes(n, dim))
         self.ws = torch.zeros(ws, dtype=torch.uint8, device=device)   # zeroed: no threshold hint yet
+        mws = int(_native.lib().gc_sparse_mean_workspace_bytes(n, dim))
+        self.mean_ws = torch.empty(mws, dtype=torch.uint8, device=device)
 
     def run(self, grads, res, round_index, ledger, nmse=True):
         n, d, k = self.n, self.dim, self.k
@@ -327,8 +329,8 @@ class TopKEngine(Engine):
         if ev:
             ev[1].record()
         est = torch.empty(d, dtype=torch.float32, device=self.device)
-        _native.call("gc_sparse_accumulate", n, k, idx.data_ptr(), val.data_ptr(), d, est.data_ptr(), sp)
-        _native.call("gc_scale_div", d, est.data_ptr(), n, est.data_ptr(), sp)
+        _native.call("gc_sparse_mean", n, k, idx.data_ptr(), val.data_ptr(), d, n, est.data_ptr(),
+                     self.mean_ws.data_ptr(), sp)
         self.launches += 10 + n
         acc = None
         corrected = res if res is not None else grads

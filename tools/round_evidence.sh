@@ -1,4 +1,5 @@
-# round-end evidence: full GPU tests, smoke, bench (both arms), sweep, launch list, per-scheme ncu
+# round-end evidence on one B200 (run under gpurun): full GPU tests, smoke, bench (both arms), sweep, launch list,
+# per-scheme ncu (tools/profile_all.sh); then `bash tools/collect_profiles.sh` here copies the summaries to profiles/
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q > gpurun_out/final_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/final_pytest.log
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final_smoke.log 2>&1
