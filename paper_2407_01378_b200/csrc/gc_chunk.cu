@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kNT) scatter_kernel(int64_t d, int64_t C, int6
        e += static_cast<int64_t>(gridDim.x) * kNT) {
     const int64_t jj = e / C, t = e - jj * C;
     const int64_t i = static_cast<int64_t>(sel[jj]) * C + t;
-    if (i < d) est[perm ? perm[i] : i] = summed[e] / static_cast<float>(divisor);
+    if (i < d) est[perm ? perm[i] : i] = gc::DivN(divisor)(summed[e]);
   }
 }
 

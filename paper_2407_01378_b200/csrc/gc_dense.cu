@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(kNT) float_fold_kernel(int n, int64_t len, con
                                                          int vec) {
   in += blockIdx.y * in_stride;   // batch of independent folds
   out += blockIdx.y * out_stride;
-  const float dv = static_cast<float>(divisor);
+  const gc::DivN dv(divisor > 0 ? divisor : 1);
   // vec: 4 elements per thread with float4 rows (ld, in, out 16-byte aligned); a group that
   // straddles a ring-block boundary folds its elements one by one.  All n row loads of a group
   // are issued before the fold (n <= kMaxFold), so each thread keeps n loads in flight.
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kNT) float_fold_kernel(int n, int64_t len, con
 #pragma unroll
         for (int k = 0; k < kMaxFold; ++k) x[k] = c == 0 ? x4[k].x : (c == 1 ? x4[k].y : (c == 2 ? x4[k].z : x4[k].w));
         const float acc = fold_values<WIRE16, ROUND_IN, kMaxFold>(x, n);
-        r[c] = divisor > 0 ? acc / dv : acc;
+        r[c] = divisor > 0 ? dv(acc) : acc;
       }
       __stcs(reinterpret_cast<float4 *>(out + e0), make_float4(r[0], r[1], r[2], r[3]));
       continue;
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kNT) float_fold_kernel(int n, int64_t len, con
         }
         if (WIRE16 && n > 1) acc = gc::fp16_round_trip(acc);
       }
-      out[e] = divisor > 0 ? acc / dv : acc;
+      out[e] = divisor > 0 ? dv(acc) : acc;
     }
   }
 }
@@ -128,26 +128,26 @@ __global__ void __launch_bounds__(kNT) segment_fold_kernel(int n, const int64_t 
       acc = (k == 0) ? c : acc + c;
       w = (w + 1 == n) ? 0 : w + 1;
     }
-    est[i] = acc / static_cast<float>(n);
+    est[i] = gc::DivN(n)(acc);
     if (r)
       for (int u = 0; u < n; ++u) r[u * ld + i] = 0.0f;   // corrected - own with own = corrected
   }
 }
 
 __global__ void scale_div_kernel(int64_t len, const float *in, int divisor, float *out) {
-  const float dv = static_cast<float>(divisor);
+  const gc::DivN dv(divisor);
   int64_t head = 0;
   if (((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {   // float4 body
     head = len & ~int64_t{3};
     for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; 4 * e < head;
          e += static_cast<int64_t>(gridDim.x) * kNT) {
       const float4 v = __ldcs(reinterpret_cast<const float4 *>(in) + e);
-      __stcs(reinterpret_cast<float4 *>(out) + e, make_float4(v.x / dv, v.y / dv, v.z / dv, v.w / dv));
+      __stcs(reinterpret_cast<float4 *>(out) + e, make_float4(dv(v.x), dv(v.y), dv(v.z), dv(v.w)));
     }
   }
   for (int64_t e = head + blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < len;
        e += static_cast<int64_t>(gridDim.x) * kNT)
-    out[e] = in[e] / dv;
+    out[e] = dv(in[e]);
 }
 
 __global__ void fp16_round_kernel(int64_t len, const float *in, float *out) {

@@ -84,6 +84,16 @@ __device__ __forceinline__ bool sign_positive(const uint32_t *bits, int64_t i) {
   return (bits[i >> 5] >> (i & 31)) & 1u;
 }
 
+// x / n in f32 with the IEEE quotient the reference computes: for a power-of-two n the product
+// with the exact reciprocal is the same correctly rounded value (no division sequence).
+struct DivN {
+  float n, inv;
+  bool pow2;
+  __device__ __forceinline__ explicit DivN(int d) : n(static_cast<float>(d)), inv(1.0f / static_cast<float>(d)),
+                                                    pow2(d > 0 && (d & (d - 1)) == 0) {}
+  __device__ __forceinline__ float operator()(float x) const { return pow2 ? x * inv : x / n; }
+};
+
 // Order-preserving float <-> uint encoding for atomic min/max.
 __device__ __forceinline__ unsigned int float_to_ordered(float f) {
   const unsigned int u = __float_as_uint(f);

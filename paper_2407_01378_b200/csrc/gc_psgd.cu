@@ -412,6 +412,10 @@ __global__ void __launch_bounds__(256) mtp_vec_kernel(int64_t d, int64_t rows, i
 // columns in registers and streams its rows -- per worker r_new = c - P_hat Q_w^T (c held in
 // resid), then estimate = P_hat Q_sum^T / n.  Float4 loads/stores, Q read from L2 once per CTA.
 constexpr int kDecRows = 64;
+#ifndef GC_PSGD_DEC_BATCH
+#define GC_PSGD_DEC_BATCH 8
+#endif
+constexpr int kDecBatch = GC_PSGD_DEC_BATCH;   // rows whose loads are in flight together
 
 template <int R, bool A16>
 __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d, int64_t rows, int64_t cols,
@@ -433,6 +437,7 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
   for (int e = threadIdx.x; e < nrows * R; e += 256) ps[e] = ph[row0 * R + e];
   __syncthreads();
   if (!vm) return;
+  const gc::DivN dn(n);
   for (int w = 0; w <= L; ++w) {   // w == L: the estimate with Q_sum
     const float *qsrc = w < L ? qw + static_cast<int64_t>(w) * cols * R : qsum;
     float qv[4][R];
@@ -446,17 +451,16 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
     if ((row0 + nrows - 1) * cols + col + lastoff < d) {   // whole block in range: branch-free
       // rows go in batches of 8: the 8 loads of c are issued before any store (the compiler
       // cannot prove that a store to row a does not alias the load of row a + 1)
-      const float nf = static_cast<float>(n);
-      for (int a0 = 0; a0 < nrows; a0 += 8) {
-        const int nb = min(8, nrows - a0);
-        float4 cv[8];
+      for (int a0 = 0; a0 < nrows; a0 += kDecBatch) {
+        const int nb = min(kDecBatch, nrows - a0);
+        float4 cv[kDecBatch];
         if (w < L) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < kDecBatch; ++u)
             if (u < nb) cv[u] = ldc<A16>(dst + (row0 + a0 + u) * cols + col, vm);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kDecBatch; ++u) {
           if (u >= nb) break;
           const int a = a0 + u;
           float o4[4];
@@ -474,7 +478,7 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
           if (w < L)
             stc<A16>(o, make_float4(cv[u].x - o4[0], cv[u].y - o4[1], cv[u].z - o4[2], cv[u].w - o4[3]), vm);
           else
-            stc<A16>(o, make_float4(o4[0] / nf, o4[1] / nf, o4[2] / nf, o4[3] / nf), vm);
+            stc<A16>(o, make_float4(dn(o4[0]), dn(o4[1]), dn(o4[2]), dn(o4[3])), vm);
         }
       }
       continue;
@@ -499,13 +503,12 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
           const float4 c = *reinterpret_cast<const float4 *>(dst + i);
           __stcs(reinterpret_cast<float4 *>(dst + i), make_float4(c.x - o4[0], c.y - o4[1], c.z - o4[2], c.w - o4[3]));
         } else {
-          const float nf = static_cast<float>(n);
-          __stcs(reinterpret_cast<float4 *>(dst + i), make_float4(o4[0] / nf, o4[1] / nf, o4[2] / nf, o4[3] / nf));
+          __stcs(reinterpret_cast<float4 *>(dst + i), make_float4(dn(o4[0]), dn(o4[1]), dn(o4[2]), dn(o4[3])));
         }
       } else {
         for (int t = 0; t < 4; ++t) {
           const int64_t it = i + col_off<A16>(t);
-          if (((vm >> t) & 1u) && it < d) dst[it] = w < L ? dst[it] - o4[t] : o4[t] / static_cast<float>(n);
+          if (((vm >> t) & 1u) && it < d) dst[it] = w < L ? dst[it] - o4[t] : dn(o4[t]);
         }
       }
     }

@@ -840,10 +840,13 @@ __global__ void scatter_add_kernel(int64_t k, const int32_t *idx, const float *v
     acc[idx[e]] += val[e];
 }
 
-// Tiled sparse mean (pipelines.py:204-211 + the / n): estimate tile t (4096 coordinates) is
-// built in shared memory from each worker's entries in [start[w][t], start[w][t+1]) -- worker by
-// worker, so every coordinate sees the np.add.at order -- and written once, divided by n.  The
-// payload indices are ascending per worker, so the tile starts come from one pass over them.
+// Tiled sparse mean (pipelines.py:204-211 + the / n): one warp builds the estimate of a
+// 1024-coordinate tile in shared memory from each worker's entries in [start[w][t],
+// start[w][t+1]) -- worker by worker (__syncwarp between), so every coordinate sees the
+// np.add.at order -- and writes it once, divided by n.  The payload indices are ascending per
+// worker, so the tile starts come from one pass over them.
+constexpr int kMeanTile = 1024;
+
 __global__ void sparse_tile_starts_kernel(int L, int64_t k, const int32_t *idx, int64_t tiles, int32_t *start) {
   const int w = blockIdx.y;
   const int32_t *iw = idx + w * k;
@@ -851,8 +854,8 @@ __global__ void sparse_tile_starts_kernel(int L, int64_t k, const int32_t *idx, 
   for (int64_t j = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; j <= k;
        j += static_cast<int64_t>(gridDim.x) * kNT) {
     // entry j opens tiles (tile(idx[j-1]), tile(idx[j])]; j == k closes the list
-    const int64_t lo = j == 0 ? -1 : iw[j - 1] / kTileE;
-    const int64_t hi = j == k ? tiles : iw[j] / kTileE;
+    const int64_t lo = j == 0 ? -1 : iw[j - 1] / kMeanTile;
+    const int64_t hi = j == k ? tiles : iw[j] / kMeanTile;
     for (int64_t t = lo + 1; t <= hi; ++t) sw[t] = static_cast<int32_t>(j);
   }
 }
@@ -860,26 +863,74 @@ __global__ void sparse_tile_starts_kernel(int L, int64_t k, const int32_t *idx, 
 __global__ void __launch_bounds__(kNT) sparse_mean_kernel(int L, int64_t k, const int32_t *idx, const float *val,
                                                           int64_t dim, int64_t tiles, const int32_t *start,
                                                           int divisor, float *est) {
-  __shared__ __align__(16) float acc[kTileE];
-  const float dv = static_cast<float>(divisor);
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const int64_t base = t * kTileE;
-    for (int i = threadIdx.x; i < kTileE; i += kNT) acc[i] = 0.0f;
-    __syncthreads();
-    for (int w = 0; w < L; ++w) {   // worker order; indices are unique within a worker
-      const int32_t j0 = start[w * (tiles + 1) + t], j1 = start[w * (tiles + 1) + t + 1];
-      for (int32_t j = j0 + threadIdx.x; j < j1; j += kNT) acc[idx[w * k + j] - base] += val[w * k + j];
-      __syncthreads();
+  __shared__ __align__(16) float acc_all[kNT / 32][kMeanTile];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  float *acc = acc_all[wp];
+  const gc::DivN dv(divisor);
+  const bool a16 = (reinterpret_cast<uintptr_t>(est) & 15) == 0;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(kNT / 32) + wp; t < tiles;
+       t += static_cast<int64_t>(gridDim.x) * (kNT / 32)) {
+    const int64_t base = t * kMeanTile;
+#pragma unroll
+    for (int i = 0; i < kMeanTile / 128; ++i)
+      reinterpret_cast<float4 *>(acc)[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+    // one round trip for the tile's entry ranges of all workers (lane w < L), then the entries
+    // of the concatenated worker-ordered list loaded in chunks of 32 * kE ahead of their adds
+    for (int w0 = 0; w0 < L; w0 += 32) {   // groups of 32 workers
+      const int nw = min(32, L - w0);
+      int32_t my0 = 0, mycnt = 0;
+      if (lane < nw) {
+        my0 = start[(w0 + lane) * (tiles + 1) + t];
+        mycnt = start[(w0 + lane) * (tiles + 1) + t + 1] - my0;
+      }
+      int32_t incl = mycnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      const int32_t excl = incl - mycnt;
+      constexpr int kE = 4;
+      for (int32_t q0 = 0; q0 < total; q0 += 32 * kE) {
+        int wq[kE];
+        int32_t iq[kE];
+        float vq[kE];
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+          const int32_t q = q0 + lane + 32 * e;
+          int ww = 0;   // the worker whose [excl, excl + cnt) holds q (all lanes shuffle)
+          for (int u = 1; u < nw; ++u)
+            if (q >= __shfl_sync(0xffffffffu, excl, u)) ww = u;
+          const int32_t j = __shfl_sync(0xffffffffu, my0, ww) + (q - __shfl_sync(0xffffffffu, excl, ww));
+          wq[e] = q < total ? ww : -1;
+          iq[e] = 0;
+          vq[e] = 0.0f;
+          if (q < total) {
+            iq[e] = idx[(w0 + ww) * k + j];
+            vq[e] = val[(w0 + ww) * k + j];
+          }
+        }
+        for (int ww = 0; ww < nw; ++ww) {   // worker order; indices unique within a worker
+#pragma unroll
+          for (int e = 0; e < kE; ++e)
+            if (wq[e] == ww) acc[iq[e] - base] += vq[e];
+          __syncwarp();
+        }
+      }
     }
-    if (base + kTileE <= dim && (reinterpret_cast<uintptr_t>(est) & 15) == 0) {
-      for (int i = threadIdx.x; i < kTileE / 4; i += kNT) {
-        const float4 a = reinterpret_cast<const float4 *>(acc)[i];
-        __stcs(reinterpret_cast<float4 *>(est + base) + i, make_float4(a.x / dv, a.y / dv, a.z / dv, a.w / dv));
+    if (a16 && base + kMeanTile <= dim) {
+#pragma unroll
+      for (int i = 0; i < kMeanTile / 128; ++i) {
+        const float4 a = reinterpret_cast<const float4 *>(acc)[lane + 32 * i];
+        __stcs(reinterpret_cast<float4 *>(est + base) + lane + 32 * i,
+               make_float4(dv(a.x), dv(a.y), dv(a.z), dv(a.w)));
       }
     } else {
-      for (int i = threadIdx.x; i < kTileE && base + i < dim; i += kNT) est[base + i] = acc[i] / dv;
+      for (int i = lane; i < kMeanTile && base + i < dim; i += 32) est[base + i] = dv(acc[i]);
     }
-    __syncthreads();
+    __syncwarp();   // the tile buffer is reused by the warp's next tile
   }
 }
 
@@ -999,7 +1050,7 @@ int gc_sparse_accumulate(int32_t workers, int64_t k, const int32_t *idx, const f
 }
 
 int64_t gc_sparse_mean_workspace_bytes(int32_t workers, int64_t dim) {
-  return static_cast<int64_t>(workers) * ((dim + kTileE - 1) / kTileE + 1) * 4;
+  return static_cast<int64_t>(workers) * ((dim + kMeanTile - 1) / kMeanTile + 1) * 4;
 }
 
 int gc_sparse_mean(int32_t workers, int64_t k, const int32_t *idx, const float *val, int64_t dim, int32_t divisor,
@@ -1008,10 +1059,11 @@ int gc_sparse_mean(int32_t workers, int64_t k, const int32_t *idx, const float *
                  divisor >= 1 && estimate && workspace && (k == 0 || (idx && val)),
              "invalid argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t tiles = (dim + kTileE - 1) / kTileE;
+  const int64_t tiles = (dim + kMeanTile - 1) / kMeanTile;
   int32_t *start = static_cast<int32_t *>(workspace);
   sparse_tile_starts_kernel<<<dim3(grid_for(k + 1), workers), kNT, 0, st>>>(workers, k, idx, tiles, start);
-  sparse_mean_kernel<<<static_cast<unsigned>(tiles < 16 * 148 ? tiles : 16 * 148), kNT, 0, st>>>(
+  const int64_t ctas = (tiles + kNT / 32 - 1) / (kNT / 32);
+  sparse_mean_kernel<<<static_cast<unsigned>(ctas < 6 * 148 ? ctas : 6 * 148), kNT, 0, st>>>(
       workers, k, idx, val, dim, tiles, start, divisor, estimate);
   GC_LAUNCH_CHECK("sparse_mean_kernel");
   return GC_OK;
