@@ -118,10 +118,11 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
   auto a_small = [&](int s) { return base + s * kStageBytes + kATile; };
   auto b_big = [&](int s) { return base + s * kStageBytes + 2 * kATile; };
   auto b_small = [&](int s) { return base + s * kStageBytes + 2 * kATile + kBTile; };
-  const uint32_t bars = base + kStages * kStageBytes;   // empty[kStages], acc[2], tmem slot
+  const uint32_t bars = base + kStages * kStageBytes;   // empty[kStages], acc[2], full[kStages], tmem slot
   auto empty_bar = [&](int s) { return bars + 8 * s; };
   auto acc_bar = [&](int a) { return bars + 8 * (kStages + a); };
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + kStages * kStageBytes + 8 * (kStages + 2));
+  auto full_bar = [&](int s) { return bars + 8 * (kStages + 2 + s); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + kStages * kStageBytes + 8 * (2 * kStages + 2));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int v = blockIdx.z;                      // (tensor, worker) row of the batch
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(empty_bar(s), 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(full_bar(s), kThreads);   // every producer arrives
     mbar_init(acc_bar(0), 1);
     mbar_init(acc_bar(1), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -282,11 +284,14 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
       *reinterpret_cast<float4 *>(sm + (b_big(s) - base) + off) = hb;
       *reinterpret_cast<float4 *>(sm + (b_small(s) - base) + off) = hs;
     }
-    // the generic-proxy stores must be visible to the tensor core (async proxy)
+    // the generic-proxy stores must be visible to the tensor core (async proxy).  Producers
+    // publish the stage on a full barrier instead of a CTA-wide barrier: only the issuing
+    // thread waits for all of them, the other warps run ahead to the next chunk
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full_bar(s)) : "memory");
     const int64_t gi = k / kGroup;
     if (tid == 0) {
+      mbar_wait(full_bar(s), static_cast<uint32_t>((k / kStages) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t dcol = tmem + static_cast<uint32_t>((gi & 1) * kN);
 #pragma unroll
