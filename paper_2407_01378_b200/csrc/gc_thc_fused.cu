@@ -35,6 +35,9 @@
 #include "gc_device.cuh"
 #include "gc_internal.h"
 
+#ifndef GC_THC_LCG_U128
+#define GC_THC_LCG_U128 0
+#endif
 #ifndef GC_THC_LOAD_BATCH
 #define GC_THC_LOAD_BATCH 2
 #endif
@@ -170,6 +173,24 @@ struct Lcg {
     s2 = r2;
     s3 = r3;
   }
+#if GC_THC_LCG_U128
+  // the same step written with unsigned __int128 (ptxas schedules the carry chain itself)
+  __device__ __forceinline__ void step(const uint32_t (&m)[4], const uint32_t (&c)[4], int) {
+    using u128 = unsigned __int128;
+    const u128 sv = (static_cast<u128>((static_cast<uint64_t>(s3) << 32) | s2) << 64) |
+                    ((static_cast<uint64_t>(s1) << 32) | s0);
+    const u128 mv = (static_cast<u128>((static_cast<uint64_t>(m[3]) << 32) | m[2]) << 64) |
+                    ((static_cast<uint64_t>(m[1]) << 32) | m[0]);
+    const u128 cv = (static_cast<u128>((static_cast<uint64_t>(c[3]) << 32) | c[2]) << 64) |
+                    ((static_cast<uint64_t>(c[1]) << 32) | c[0]);
+    const u128 r = sv * mv + cv;
+    const uint64_t lo = static_cast<uint64_t>(r), hi = static_cast<uint64_t>(r >> 64);
+    s0 = static_cast<uint32_t>(lo);
+    s1 = static_cast<uint32_t>(lo >> 32);
+    s2 = static_cast<uint32_t>(hi);
+    s3 = static_cast<uint32_t>(hi >> 32);
+  }
+#endif
   // the high half of the XSL-RR output; (a, b, rot) let lo_of() rebuild the low half on demand
   __device__ __forceinline__ uint32_t out_hi(uint32_t &a, uint32_t &b, uint32_t &rot) const {
     const uint32_t xl = s0 ^ s2, xh = s1 ^ s3;
@@ -541,7 +562,11 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
           const float4 sp =
               rpb_log >= 2 ? sp_j : *reinterpret_cast<const float4 *>(bp + 8 * ((j + c) >> rpb_log) + 6);
           hw[c] = ch[c].out_hi(oa[c], ob[c], orot[c]);
+#if GC_THC_LCG_U128
+          ch[c].step(m128, c128, 0);
+#else
           ch[c].step(m128, c128);
+#endif
           xv[c] = xs[(j + c) * 32 + lane];
           // fp32 screen: floor by the 1.5 * 2^23 magic constant (|t32| < 2^22), frac, 23-bit coin;
           // safe iff min(f, 1 - f, |c23 - f|) > H (1 - f is exact for f >= 1/2)
