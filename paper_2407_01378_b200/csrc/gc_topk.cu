@@ -60,7 +60,7 @@ struct RowState {  // per worker, lives in the workspace
   int spec_ok;             // pass 1's candidates are complete: the collect pass is skipped
   unsigned int spec_fail;  // persists: consecutive calls whose speculation failed
   unsigned int calls;      // persists: calls on this workspace
-  unsigned int pad3;
+  unsigned int hint2;      // persists: the hint of the call before (trend of the boundary bin)
 };
 
 struct Work {
@@ -129,16 +129,22 @@ __global__ void __launch_bounds__(kNT) init_kernel(Work wk, int L, int64_t k, in
   for (int i = blockIdx.x * kNT + threadIdx.x; i < kBins0 * L; i += gridDim.x * kNT) wk.hist[i] = 0;
   for (int r = blockIdx.x * kNT + threadIdx.x; r < L; r += gridDim.x * kNT) {
     RowState &s = wk.state[r];
-    // pass 1 collects the bins >= (previous boundary bin - 1): in steady EF rounds the new
-    // boundary bin is at or above it, so the collect pass is skipped (verified on the device)
+    // pass 1 collects the bins >= guess = previous boundary bin - 2 (two 1/32-octave bins of
+    // margin) + the bin's last upward step: when the new boundary bin is at or above the guess
+    // the collect pass is skipped (verified on the device).  After a failed speculation
+    // (threshold falling, or too many candidates) pass 1 stays plain except for a re-probe every
+    // 8th call, so an unpredictable workload pays little for the attempt.
     const unsigned int h = s.hint;
-    // guess = previous boundary bin - 2 (two 1/32-octave bins of margin).  After a failed
-    // speculation (threshold moving, or too many candidates) pass 1 stays plain except for a
-    // re-probe every 8th call, so a drifting workload pays little for the attempt.
     const bool probe = s.spec_fail == 0 || (s.calls & 7u) == 0;
     s.calls = s.calls + 1;
-    s.guess = !speculate || !probe || h == 0 || h > static_cast<unsigned int>(kBins0) ? kNoGuess
-                                                                                       : (h >= 3 ? h - 3 : 0u);
+    // a boundary bin that moved up since the call before is expected to keep moving (gradient
+    // scales drift over training; EF residuals grow): the guess follows the last step
+    const unsigned int h2 = s.hint2;
+    const int trend = (h2 >= 1 && h2 <= static_cast<unsigned int>(kBins0) && h > h2) ? static_cast<int>(h - h2) : 0;
+    const int g0 = static_cast<int>(h) - 3 + trend;
+    s.guess = !speculate || !probe || h == 0 || h > static_cast<unsigned int>(kBins0)
+                  ? kNoGuess
+                  : static_cast<unsigned int>(g0 > 0 ? (g0 < kBins0 ? g0 : kBins0 - 1) : 0);
     s.spec_ok = 0;
     s.prefix = 0;
     s.k_rem = k;
@@ -487,6 +493,7 @@ __global__ void __launch_bounds__(1024) find_kernel(Work wk, int level) {
       s.spec_ok = ok ? 1 : 0;
       if (s.guess != kNoGuess) s.spec_fail = ok ? 0u : s.spec_fail + 1u;
       if (!ok) s.cand_count = 0;   // pass 2 rebuilds the list
+      s.hint2 = s.hint;
       s.hint = b + 1;
     }
     if (level == 2) {
