@@ -19,9 +19,11 @@
 // (this file is compiled with -fmad=false), so codes are bit-exact with the reference.
 //
 // Coins: numpy PCG64 "stochastic-round" stream of worker w; coordinate i uses output
-// i+1.  Lane l of layout B consumes positions t0+l+1+32j: two interleaved LCG chains
-// (even / odd j, 64-step jumps) keep the 128-bit multiply chain short; tiles advance by a
-// host-precomputed gridDim*1024-step jump.
+// i+1.  Lane l of layout B consumes positions t0+l+1+32j: four interleaved LCG chains
+// (j mod 4, 128-step jumps) keep four independent 128-bit multiply chains in flight; tiles
+// advance by a host-precomputed gridDim*1024-step jump.  The quantizer decides a code from
+// the top 23 bits of the coin in fp32 (see screen_params); the rare undecidable coordinates
+// rebuild the full 53-bit coin and run the reference's fp64 formula.
 //
 // In-pipeline simplifications that are exact (not approximations):
 //  * the value clamp of quantize_stochastic (compressors.py:482-483) is the identity: the
@@ -35,9 +37,6 @@
 #include "gc_device.cuh"
 #include "gc_internal.h"
 
-#ifndef GC_THC_LCG_U128
-#define GC_THC_LCG_U128 0
-#endif
 #ifndef GC_THC_LOAD_BATCH
 #define GC_THC_LOAD_BATCH 2
 #endif
@@ -173,24 +172,7 @@ struct Lcg {
     s2 = r2;
     s3 = r3;
   }
-#if GC_THC_LCG_U128
-  // the same step written with unsigned __int128 (ptxas schedules the carry chain itself)
-  __device__ __forceinline__ void step(const uint32_t (&m)[4], const uint32_t (&c)[4], int) {
-    using u128 = unsigned __int128;
-    const u128 sv = (static_cast<u128>((static_cast<uint64_t>(s3) << 32) | s2) << 64) |
-                    ((static_cast<uint64_t>(s1) << 32) | s0);
-    const u128 mv = (static_cast<u128>((static_cast<uint64_t>(m[3]) << 32) | m[2]) << 64) |
-                    ((static_cast<uint64_t>(m[1]) << 32) | m[0]);
-    const u128 cv = (static_cast<u128>((static_cast<uint64_t>(c[3]) << 32) | c[2]) << 64) |
-                    ((static_cast<uint64_t>(c[1]) << 32) | c[0]);
-    const u128 r = sv * mv + cv;
-    const uint64_t lo = static_cast<uint64_t>(r), hi = static_cast<uint64_t>(r >> 64);
-    s0 = static_cast<uint32_t>(lo);
-    s1 = static_cast<uint32_t>(lo >> 32);
-    s2 = static_cast<uint32_t>(hi);
-    s3 = static_cast<uint32_t>(hi >> 32);
-  }
-#endif
+
   // the high half of the XSL-RR output; (a, b, rot) let lo_of() rebuild the low half on demand
   __device__ __forceinline__ uint32_t out_hi(uint32_t &a, uint32_t &b, uint32_t &rot) const {
     const uint32_t xl = s0 ^ s2, xh = s1 ^ s3;
@@ -202,26 +184,6 @@ struct Lcg {
   }
   static __device__ __forceinline__ uint32_t lo_of(uint32_t a, uint32_t b, uint32_t rot) {
     return __funnelshift_r(a, b, rot);
-  }
-  // the 64-bit XSL-RR output rotr64(hi ^ lo, hi >> 58) as two 32-bit halves
-  __device__ __forceinline__ void out(uint32_t &hi, uint32_t &lo) const {
-    const uint32_t xl = s0 ^ s2, xh = s1 ^ s3;
-    const uint32_t rot = s3 >> 26;
-    const bool swap = rot & 32u;
-    const uint32_t a = swap ? xh : xl, b = swap ? xl : xh;
-    lo = __funnelshift_r(a, b, rot);   // shift amount taken mod 32
-    hi = __funnelshift_r(b, a, rot);
-  }
-  // coin = (next64 >> 11) * 2^-53 from the XSL-RR output rotr64(hi ^ lo, hi >> 58)
-  __device__ __forceinline__ double coin() const {
-    const uint32_t xl = s0 ^ s2, xh = s1 ^ s3;
-    const uint32_t rot = s3 >> 26;
-    const bool swap = rot & 32u;
-    const uint32_t a = swap ? xh : xl, b = swap ? xl : xh;
-    const uint32_t lo = __funnelshift_r(a, b, rot);   // shift amount taken mod 32
-    const uint32_t hi = __funnelshift_r(b, a, rot);
-    const uint64_t u = (static_cast<uint64_t>(hi) << 32) | lo;
-    return static_cast<double>(u >> 11) * (1.0 / 9007199254740992.0);
   }
 };
 
@@ -236,37 +198,6 @@ __device__ __forceinline__ void mul128(uint64_t ah, uint64_t al, uint64_t bh, ui
                                        uint64_t &rl) {
   rl = al * bl;
   rh = __umul64hi(al, bl) + al * bh + ah * bl;
-}
-
-// quantize one value (compressors.py:485-498 with the exact in-pipeline simplifications).
-// t = (x - mid) / step is formed with one Markstein correction from inv = RN(1/step): the
-// result is within 1 ulp of the IEEE quotient, i.e. within 2^-46 since |t| <= 127.  The
-// code depends on t only through floor(t) and comparisons of frac with the coin and the
-// 1e-9 snap thresholds; a change of t across an integer is absorbed by the snapping, so
-// the code can only differ from the reference when frac lies within 2^-44 of the coin or
-// of a threshold.  Those (probability ~1e-13) recompute t with the IEEE division.
-__device__ __noinline__ double ieee_quotient(double a, double b) { return a / b; }
-
-__device__ __forceinline__ int quantize_one(double x, double mid, double step, double inv, double coin) {
-  const double a = x - mid;
-  const double q0 = a * inv;
-  double t = fma(fma(-q0, step, a), inv, q0);
-  double low = floor(t);
-  double frac = t - low;
-  constexpr double kLo = 1e-9, kHi = 1.0 - 1e-9, kGuard = 0x1p-44;
-  // |frac - 0.5| is within 2^-53 of 0.5 - 1e-9 exactly when frac is near either snap threshold
-  const bool danger = fabs(frac - coin) < kGuard || fabs(fabs(frac - 0.5) - (0.5 - 1e-9)) < 2 * kGuard;
-  // warp-uniform branch around the (practically never taken) exact path keeps it out of the
-  // straight-line code
-  if (__any_sync(0xffffffffu, danger)) {
-    if (danger) {
-      t = ieee_quotient(a, step);
-      low = floor(t);
-      frac = t - low;
-    }
-  }
-  const bool up = frac > kHi || (frac >= kLo && coin < frac);
-  return static_cast<int>(low) + (up ? 1 : 0);
 }
 
 // coin_from: numpy's random() double (next64 >> 11) * 2^-53 from the two output halves.
@@ -562,11 +493,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
           const float4 sp =
               rpb_log >= 2 ? sp_j : *reinterpret_cast<const float4 *>(bp + 8 * ((j + c) >> rpb_log) + 6);
           hw[c] = ch[c].out_hi(oa[c], ob[c], orot[c]);
-#if GC_THC_LCG_U128
-          ch[c].step(m128, c128, 0);
-#else
           ch[c].step(m128, c128);
-#endif
           xv[c] = xs[(j + c) * 32 + lane];
           // fp32 screen: floor by the 1.5 * 2^23 magic constant (|t32| < 2^22), frac, 23-bit coin;
           // safe iff min(f, 1 - f, |c23 - f|) > H (1 - f is exact for f >= 1/2)
