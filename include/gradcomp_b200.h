@@ -189,6 +189,15 @@ int gc_sparse_accumulate(int32_t workers, int64_t k, const int32_t *idx, const f
 int64_t gc_sparse_mean_workspace_bytes(int32_t workers, int64_t dim);
 int gc_sparse_mean(int32_t workers, int64_t k, const int32_t *idx, const float *val, int64_t dim, int32_t divisor,
                    float *estimate, void *workspace, void *stream);
+/* QuantPayload wire bytes (compressors.py:305-317) for L workers: row w = <B 3><B quant_bits>
+ * <I block_size><I num_codes><I num_blocks> codes[w] (int8, num_codes; entries past codes_len are 0)
+ * ranges (f32 [num_blocks][2], shared; blocks past ranges_len are (0, 0)) <Q rotation_id>.
+ * Rows are gc_quant_payload_nbytes(num_codes, num_blocks) bytes at `stride`. */
+int64_t gc_quant_payload_nbytes(int64_t num_codes, int64_t num_blocks);
+int gc_encode_quant_payloads(int32_t workers, int32_t quant_bits, int64_t block_size, int64_t num_codes,
+                             const int8_t *codes, int64_t codes_ld, int64_t codes_len, int64_t num_blocks,
+                             const float *ranges, int64_t ranges_len, uint64_t rotation_id, uint8_t *out,
+                             int64_t stride, void *stream);
 /* ef_update with a sparse own payload (compressors.py:629-631, 406-409): resid[w][idx] -= val. */
 int gc_sparse_ef_update(int32_t workers, int64_t k, const int32_t *idx, const float *val, float *resid, int64_t ld,
                         void *stream);

@@ -96,6 +96,8 @@ SIGNATURES = {
     "gc_encode_sparse_payloads": (c_int, [I32, I64, P, P, P, I64, P]),
     "gc_sparse_accumulate": (c_int, [I32, I64, P, P, I64, P, P]),
     "gc_sparse_mean_workspace_bytes": (c_int64, [I32, I64]),
+    "gc_quant_payload_nbytes": (c_int64, [I64, I64]),
+    "gc_encode_quant_payloads": (c_int, [I32, I32, I64, I64, P, I64, I64, I64, P, I64, c_uint64, P, I64, P]),
     "gc_sparse_mean": (c_int, [I32, I64, P, P, I64, I32, P, P, P]),
     "gc_sparse_ef_update": (c_int, [I32, I64, P, P, P, I64, P]),
     # TopK-Chunked

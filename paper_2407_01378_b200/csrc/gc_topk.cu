@@ -975,6 +975,42 @@ __global__ void encode_sparse_kernel(int L, int64_t k, const int32_t *idx, const
   }
 }
 
+// QuantPayload wire bytes (compressors.py:305-317): <B 3><B q><I block><I num_codes><I num_blocks>
+// <i1 codes * num_codes><f4 ranges * 2 num_blocks><Q rotation_id>, one row per worker.  Codes /
+// ranges past the given lengths (the all-zero padded tail the engine skips) are zero.  One thread
+// per output byte: the row is HBM-bound byte traffic, the header costs nothing.
+__global__ void encode_quant_kernel(int L, int q, int64_t block, int64_t num_codes, const int8_t *codes,
+                                    int64_t codes_ld, int64_t codes_len, int64_t num_blocks, const float *ranges,
+                                    int64_t ranges_len, unsigned long long rot, uint8_t *out, int64_t stride,
+                                    int64_t row_bytes) {
+  const int64_t total = static_cast<int64_t>(L) * row_bytes;
+  const int64_t c0 = 14, r0 = c0 + num_codes, t0 = r0 + 8 * num_blocks;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = e / row_bytes, p = e - w * row_bytes;
+    uint8_t b;
+    if (p >= c0 && p < r0) {
+      const int64_t i = p - c0;
+      b = i < codes_len ? static_cast<uint8_t>(codes[w * codes_ld + i]) : 0;
+    } else if (p >= r0 && p < t0) {
+      const int64_t j = (p - r0) >> 2;   // float index into ranges [num_blocks][2]
+      const uint32_t bits = j < 2 * ranges_len ? __float_as_uint(ranges[j]) : 0u;
+      b = static_cast<uint8_t>(bits >> (8 * ((p - r0) & 3)));
+    } else if (p >= t0) {
+      b = static_cast<uint8_t>(rot >> (8 * (p - t0)));
+    } else if (p == 0) {
+      b = 3;
+    } else if (p == 1) {
+      b = static_cast<uint8_t>(q);
+    } else {   // bytes 2..13: block, num_codes, num_blocks as little-endian u32
+      const int64_t f = (p - 2) >> 2;
+      const uint32_t v = static_cast<uint32_t>(f == 0 ? block : (f == 1 ? num_codes : num_blocks));
+      b = static_cast<uint8_t>(v >> (8 * ((p - 2) & 3)));
+    }
+    out[w * stride + p] = b;
+  }
+}
+
 int grid_for(int64_t work) {
   int64_t g = (work + kNT - 1) / kNT;
   if (g > 148 * 16) g = 148 * 16;
@@ -1089,6 +1125,26 @@ int gc_encode_sparse_payloads(int32_t workers, int64_t k, const int32_t *idx, co
   encode_sparse_kernel<<<grid_for(total), kNT, 0, static_cast<cudaStream_t>(stream)>>>(workers, k, idx, val, out,
                                                                                       stride);
   GC_LAUNCH_CHECK("encode_sparse_kernel");
+  return GC_OK;
+}
+
+int64_t gc_quant_payload_nbytes(int64_t num_codes, int64_t num_blocks) { return 14 + num_codes + 8 * num_blocks + 8; }
+
+int gc_encode_quant_payloads(int32_t workers, int32_t quant_bits, int64_t block_size, int64_t num_codes,
+                             const int8_t *codes, int64_t codes_ld, int64_t codes_len, int64_t num_blocks,
+                             const float *ranges, int64_t ranges_len, uint64_t rotation_id, uint8_t *out,
+                             int64_t stride, void *stream) {
+  const int64_t row = gc_quant_payload_nbytes(num_codes, num_blocks);
+  GC_REQUIRE(workers >= 1 && quant_bits >= 2 && quant_bits <= 8 && block_size >= 1 && num_codes >= 0 &&
+                 num_codes <= 0xffffffffll && num_blocks >= 0 && num_blocks * block_size == num_codes &&
+                 codes_len >= 0 && codes_len <= num_codes && ranges_len >= 0 && ranges_len <= num_blocks &&
+                 (codes_len == 0 || (codes && codes_ld >= codes_len)) && (ranges_len == 0 || ranges) && out &&
+                 stride >= row,
+             "invalid argument");
+  encode_quant_kernel<<<grid_for(workers * row), kNT, 0, static_cast<cudaStream_t>(stream)>>>(
+      workers, quant_bits, block_size, num_codes, codes, codes_ld, codes_len, num_blocks, ranges, ranges_len,
+      static_cast<unsigned long long>(rotation_id), out, stride, row);
+  GC_LAUNCH_CHECK("encode_quant_kernel");
   return GC_OK;
 }
 

@@ -249,3 +249,30 @@ def encode_sparse_payloads_device(idx: torch.Tensor, val: torch.Tensor) -> torch
     _native.call("gc_encode_sparse_payloads", L, k, idx.data_ptr(), val.data_ptr(), out.data_ptr(),
                  out.stride(0), torch.cuda.current_stream().cuda_stream)
     return out
+
+
+def quant_payload_nbytes(num_codes: int, num_blocks: int) -> int:
+    """Bytes of one encoded QuantPayload (compressors.py:305-317)."""
+    return 14 + num_codes + 8 * num_blocks + 8
+
+
+def encode_quant_payloads_device(codes: torch.Tensor, ranges: torch.Tensor, quant_bits: int, block_size: int,
+                                 num_codes: int, rotation_id: int = 0) -> torch.Tensor:
+    """Wire bytes of L QuantPayloads straight from a THC round's device buffers.
+
+    codes: int8 [L, active] (the engine's codes over the non-zero prefix); ranges: float32
+    [active_blocks, 2] (the shared consensus grid); num_codes: the padded length P.  Codes and
+    ranges past the given prefix are the zeros of the padded tail.  Returns uint8 [L, nbytes];
+    row w equals encode_payload(QuantPayload(codes_w padded, ranges padded, rotation_id, q, B))."""
+    if codes.dim() != 2 or codes.dtype != torch.int8 or ranges.dim() != 2 or ranges.shape[1] != 2 \
+            or ranges.dtype != torch.float32 or num_codes % block_size:
+        raise ValueError("need int8 codes [workers, n] and float32 ranges [blocks, 2], num_codes % block_size == 0")
+    L = codes.shape[0]
+    codes, ranges = codes.contiguous(), ranges.contiguous()
+    nblocks = num_codes // block_size
+    out = torch.empty(L, quant_payload_nbytes(num_codes, nblocks), dtype=torch.uint8, device=codes.device)
+    _native.call("gc_encode_quant_payloads", L, quant_bits, block_size, num_codes, codes.data_ptr(),
+                 codes.stride(0), codes.shape[1], nblocks, ranges.data_ptr(), ranges.shape[0],
+                 rotation_id & ((1 << 64) - 1), out.data_ptr(), out.stride(0),
+                 torch.cuda.current_stream().cuda_stream)
+    return out

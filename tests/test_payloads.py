@@ -83,3 +83,33 @@ def test_device_sparse_payload_bytes_match_host_codec():
         assert dev[w].tobytes() == host, w
     empty = pl.encode_sparse_payloads_device(idx[:, :0].contiguous(), val[:, :0].contiguous()).cpu().numpy()
     assert all(row.tobytes() == pl.encode_payload(pl.SparsePayload(np.zeros(0), np.zeros(0))) for row in empty)
+
+
+@pytest.mark.gpu
+@needs_gpu
+@pytest.mark.parametrize("d,q,b,blk", [(300_001, 4, 8, 1024), (5000, 3, 4, 256)])
+def test_device_quant_payload_bytes_match_host_codec(d, q, b, blk):
+    """THC round on the GPU (multi-kernel path, codes and consensus ranges captured) -> QuantPayload
+    wire bytes built on the device == encode_payload of the padded payload (zero tail included)."""
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200 import payloads as pl
+    n = 3
+    seeds = gcb.SeedSpec(21)
+    grads = [seeds.rng("grad-worker", 0, w).standard_normal(d).astype(np.float32) for w in range(n)]
+    pipe = gcb.make_pipeline(gcb.RotatedQuantConfig(q, b, blk), n, d, seeds, fused=False)
+    pipe._engine.capture = True
+    pipe.run_round(grads, 0)
+    eng = pipe._engine
+    codes, shared = eng.last["codes"], eng.last["shared"].float().reshape(-1, 2)
+    P, B = eng.P, eng.B
+    rot = 0x1234_5678_9ABC_DEF0
+    dev = pl.encode_quant_payloads_device(codes, shared, q, B, P, rot).cpu().numpy()
+    for w in range(n):
+        full = np.zeros(P, np.int8)
+        full[: codes.shape[1]] = codes[w].cpu().numpy()
+        rng = np.zeros((P // B, 2), np.float32)
+        rng[: shared.shape[0]] = shared.cpu().numpy()
+        host = pl.encode_payload(pl.QuantPayload(full, rng, rot, q, B))
+        assert dev[w].tobytes() == host, w
+        back = pl.decode_payload(dev[w].tobytes())
+        assert np.array_equal(back.codes, full) and np.array_equal(back.ranges, rng)
