@@ -282,6 +282,10 @@ int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t r
 int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, double *gram, void *stream);
 /* cudaMemsetAsync wrapper (residual reset of the dense bypass, pipelines.py:336). */
 int gc_fill_zero(void *ptr, int64_t bytes, void *stream);
+/* rows x row_bytes strided copy in either direction (cudaMemcpy2DAsync): one PCIe transfer for the
+ * same segment of all n worker rows of a host-fed round (pinned [n][d] host gradients). */
+int gc_copy_rows_async(void *dst, int64_t dst_pitch, const void *src, int64_t src_pitch, int64_t row_bytes,
+                       int64_t rows, void *stream);
 
 /* SparsePayload wire bytes (encode_payload, compressors.py:292-297) for each worker's TopK
  * payload: out row w (stride >= 5 + 6k bytes) = <u8 1><u32 k><i32 idx[k]><f16 val[k]>, little endian. */

@@ -80,4 +80,19 @@ int gc_nmse_accumulate(int32_t n, int64_t d, const float *grads, const float *re
   return GC_OK;
 }
 
+int gc_copy_rows_async(void *dst, int64_t dst_pitch, const void *src, int64_t src_pitch, int64_t row_bytes,
+                       int64_t rows, void *stream) {
+  GC_REQUIRE(rows >= 0 && row_bytes >= 0 && dst_pitch >= row_bytes && src_pitch >= row_bytes &&
+                 (rows * row_bytes == 0 || (dst && src)),
+             "invalid argument");
+  if (rows * row_bytes == 0) return GC_OK;
+  if (cudaMemcpy2DAsync(dst, static_cast<size_t>(dst_pitch), src, static_cast<size_t>(src_pitch),
+                        static_cast<size_t>(row_bytes), static_cast<size_t>(rows), cudaMemcpyDefault,
+                        static_cast<cudaStream_t>(stream)) != cudaSuccess) {
+    gc_set_error("cudaMemcpy2DAsync failed");
+    return GC_ERR_CUDA;
+  }
+  return GC_OK;
+}
+
 }  // extern "C"

@@ -51,13 +51,23 @@ def _ptr(t):
 
 
 class Comm:
-    """Collectives used by the exchange plan (NCCL on CUDA tensors, gloo with host staging)."""
+    """Collectives used by the exchange plan (NCCL on CUDA tensors, gloo with host staging).
+
+    `sent` counts, per ledger phase, the payload bytes this rank delivers to the other ranks:
+    (world-1) x own bytes for an all-gather, the off-rank chunks of an all-to-all, and
+    2 (world-1) / world x bytes for an all-reduce (the ring's reduce-scatter + all-gather) --
+    the quantities the reference's TrafficLedger meters per worker (collectives.py:209-262)."""
 
     def __init__(self, group=None):
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.stage = dist.get_backend(group) != "nccl"
+        self.sent: dict[str, int] = {}
+
+    def _count(self, phase, nbytes):
+        if phase is not None and self.world > 1:
+            self.sent[phase] = self.sent.get(phase, 0) + int(nbytes)
 
     def _run(self, fn, out, *ins):
         if self.stage and out.is_cuda:
@@ -68,11 +78,12 @@ class Comm:
             fn(out, *ins)
         return out
 
-    def all_gather_rows(self, x: torch.Tensor) -> torch.Tensor:
+    def all_gather_rows(self, x: torch.Tensor, phase: str | None = None) -> torch.Tensor:
         """[L, ...] per rank -> [world * L, ...] in rank order (global worker order).
 
         Pure data movement, done on a byte view (int16 sums are not an NCCL / gloo type)."""
         x = x.contiguous()
+        self._count(phase, (self.world - 1) * x.numel() * x.element_size())
         out = torch.empty((self.world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         if self.world == 1:
             out.copy_(x)
@@ -81,9 +92,10 @@ class Comm:
                   out.view(-1).view(torch.uint8), x.view(-1).view(torch.uint8))
         return out
 
-    def all_to_all(self, send: torch.Tensor) -> torch.Tensor:
+    def all_to_all(self, send: torch.Tensor, phase: str | None = None) -> torch.Tensor:
         """send [world, ...]: chunk r goes to rank r; returns recv [world, ...], chunk r from rank r."""
         send = send.contiguous()
+        self._count(phase, (self.world - 1) * (send.numel() // self.world) * send.element_size())
         recv = torch.empty_like(send)
         if self.world == 1:
             recv.copy_(send)
@@ -92,7 +104,8 @@ class Comm:
                   recv.view(-1).view(torch.uint8), send.view(-1).view(torch.uint8))
         return recv
 
-    def all_reduce(self, t: torch.Tensor, op) -> torch.Tensor:
+    def all_reduce(self, t: torch.Tensor, op, phase: str | None = None) -> torch.Tensor:
+        self._count(phase, 2 * (self.world - 1) * t.numel() * t.element_size() // self.world)
         if self.world == 1:
             return t
         if self.stage and t.is_cuda:
@@ -112,7 +125,7 @@ def fold_slices(active: int, world: int, align: int = 256):
 
 
 def exchange_fold(codes: torch.Tensor, comm: Comm, n: int, active: int, slice_len: int, fold_fn, out_dtype,
-                  send: torch.Tensor | None = None) -> torch.Tensor:
+                  send: torch.Tensor | None = None, phase: str | None = None) -> torch.Tensor:
     """Saturating code sums over all n workers, reference ring order (collectives.py:215-235).
 
     codes: this rank's [L, active] int8 codes (global workers rank*L .. rank*L+L-1).  Slice
@@ -126,13 +139,13 @@ def exchange_fold(codes: torch.Tensor, comm: Comm, n: int, active: int, slice_le
         lo, hi = dst * slice_len, min(active, (dst + 1) * slice_len)
         if hi > lo:
             send[dst, :, : hi - lo].copy_(codes[:, lo:hi])
-    recv = comm.all_to_all(send).reshape(n, slice_len)
+    recv = comm.all_to_all(send, phase).reshape(n, slice_len)
     s0 = comm.rank * slice_len
     my_len = max(0, min(slice_len, active - s0))
     sums = torch.zeros(slice_len, dtype=out_dtype, device=codes.device)
     if my_len:
         fold_fn(recv, my_len, s0, sums)
-    return comm.all_gather_rows(sums.reshape(1, -1)).reshape(-1)
+    return comm.all_gather_rows(sums.reshape(1, -1), phase).reshape(-1)
 
 
 class DistributedGradientPipeline:
@@ -200,8 +213,11 @@ class DistributedGradientPipeline:
     def run_round(self, local_grads, round_index: int) -> RoundResult:
         g = self._checked(local_grads)
         ledger = TrafficLedger()
+        self.comm.sent = {}
         est, bits, stats = self._engine.run(g, self._res, round_index, ledger, self.compute_nmse)
-        return RoundResult(self.scheme, round_index, est, self.dim, ledger, bits, stats)
+        res = RoundResult(self.scheme, round_index, est, self.dim, ledger, bits, stats)
+        res.wire_bytes = dict(self.comm.sent)   # bytes this rank sent per ledger phase
+        return res
 
     def _checked(self, local_grads) -> torch.Tensor:
         L, d = self.L, self.dim
@@ -296,7 +312,7 @@ class _Thc(_Base):
         _native.call("gc_range_consensus", L, self.nb, self.ranges.data_ptr(), shared.data_ptr(), sp)
         # ElemMin / ElemMax ring (pipelines.py:271-288) as one all-reduce MAX of (-lo, hi)
         shared[:, 0].neg_()
-        comm.all_reduce(shared, dist.ReduceOp.MAX)
+        comm.all_reduce(shared, dist.ReduceOp.MAX, "range-consensus")
         shared[:, 0].neg_()
         counters = torch.zeros(4, dtype=torch.int64, device=self.dev)
         _native.call("gc_thc_quantize", geom, L, self.x_rot.data_ptr(), shared.data_ptr(), coins,
@@ -310,7 +326,8 @@ class _Thc(_Base):
             else:
                 out[:length].copy_(rows[0, :length])
 
-        sums = exchange_fold(self.codes, comm, n, self.active, self.S, fold, self.sum_dtype, self.send)
+        sums = exchange_fold(self.codes, comm, n, self.active, self.S, fold, self.sum_dtype, self.send,
+                             "code-aggregate")
         est = torch.empty(self.dim, dtype=torch.float32, device=self.dev)
         _native.call("gc_thc_decode_estimate", geom, n, sums.data_ptr(), self.sum_bytes, shared.data_ptr(),
                      self.signs.data_ptr(), est.data_ptr(), _ptr(self.ws), sp)
@@ -354,8 +371,9 @@ class _TopK(_Base):
         flags = _native.TOPK_FP16_VALUES | (_native.TOPK_EF_UPDATE if res is not None else 0)
         _native.call("gc_topk_select", L, d, None, g.stride(0), k, g.data_ptr(), _ptr(res), idx.data_ptr(),
                      val.data_ptr(), flags, self.ws.data_ptr(), sp)
-        all_idx = self.comm.all_gather_rows(idx)     # all_gather (collectives.py:239-263)
-        all_val = self.comm.all_gather_rows(val)
+        # all_gather (collectives.py:239-263) of the SparsePayload wire: int32 indices + fp16 values
+        all_idx = self.comm.all_gather_rows(idx, "sparse-gather")
+        all_val = self.comm.all_gather_rows(val.half(), "sparse-gather").float()
         est = torch.empty(d, dtype=torch.float32, device=self.dev)
         _native.call("gc_sparse_mean", n, k, all_idx.data_ptr(), all_val.data_ptr(), d, n, est.data_ptr(),
                      self.mean_ws.data_ptr(), sp)
@@ -389,7 +407,7 @@ class _Chunked(_Base):
         pp = _ptr(perm)
         norms = torch.empty(L, nc, dtype=torch.float32, device=self.dev)
         _native.call("gc_chunk_norms", L, d, C, work.data_ptr(), work.stride(0), pp, norms.data_ptr(), sp)
-        all_norms = self.comm.all_gather_rows(norms)
+        all_norms = self.comm.all_gather_rows(norms.half(), "norm-consensus").float()   # fp16-valued: exact
         energy = torch.empty(nc, dtype=torch.float32, device=self.dev)
         _native.call("gc_float_fold", n, nc, all_norms.data_ptr(), nc, 0, -(-nc // n), 1, 0, 0, energy.data_ptr(), sp)
         sel = torch.empty(J, dtype=torch.int32, device=self.dev)
@@ -399,7 +417,7 @@ class _Chunked(_Base):
         packs = torch.empty(L, Lc, dtype=torch.float32, device=self.dev)
         _native.call("gc_chunk_pack", L, d, C, J, sel.data_ptr(), work.data_ptr(), work.stride(0), pp,
                      packs.data_ptr(), sp)
-        all_packs = self.comm.all_gather_rows(packs)
+        all_packs = self.comm.all_gather_rows(packs.half(), "chunk-aggregate").float()   # fp16-valued: exact
         summed = torch.empty(Lc, dtype=torch.float32, device=self.dev)
         _native.call("gc_float_fold", n, Lc, all_packs.data_ptr(), Lc, 0, -(-Lc // n), 1, 0, 0, summed.data_ptr(), sp)
         est = torch.empty(d, dtype=torch.float32, device=self.dev)
@@ -428,7 +446,7 @@ class _PowerSgd(_Base):
     def _fold(self, kind, x, m):
         """Gather every rank's factor rows, then fold them in the reference ring order."""
         n = self.n
-        rows = self.comm.all_gather_rows(x.reshape(self.L, m))
+        rows = self.comm.all_gather_rows(x.reshape(self.L, m), kind)
         out = torch.empty(1, m, dtype=torch.float32, device=self.dev)
         _native.call("gc_float_fold", n, m, rows.data_ptr(), m, 0, -(-m // n), 0, 0, 0, out.data_ptr(), _sp())
         return out
@@ -442,7 +460,7 @@ class _PowerSgd(_Base):
                          res.stride(0), sp)
         c = res if res is not None else g
         if self.bypass:
-            all_c = self.comm.all_gather_rows(c)
+            all_c = self.comm.all_gather_rows(c, "dense-bypass")
             _native.call("gc_float_fold", n, d, all_c.data_ptr(), d, 0, -(-d // n), 0, 0, n, est.data_ptr(), sp)
             if res is not None:
                 _native.call("gc_fill_zero", res.data_ptr(), res.numel() * 4, sp)
@@ -474,10 +492,10 @@ class _Dense(_Base):
         _native.call("gc_float_fold", L, d, g.data_ptr(), g.stride(0), 0, d, w16, w16, 0, local.data_ptr(), sp)
         if self.bits == 16:
             wire = local.half()
-            self.comm.all_reduce(wire, dist.ReduceOp.SUM)
+            self.comm.all_reduce(wire, dist.ReduceOp.SUM, "dense")
             total = wire.float()
         else:
-            total = self.comm.all_reduce(local, dist.ReduceOp.SUM)
+            total = self.comm.all_reduce(local, dist.ReduceOp.SUM, "dense")
         est = torch.empty(d, dtype=torch.float32, device=self.dev)
         _native.call("gc_scale_div", d, total.data_ptr(), n, est.data_ptr(), sp)
         self.launches += 2

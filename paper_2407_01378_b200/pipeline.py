@@ -166,8 +166,17 @@ class GradientPipeline:
         """The n gradients as 1-d CPU float32 tensors when every one is host memory and the scheme
         streams (fused THC); None otherwise (the generic copy-then-run path)."""
         eng = self._engine
-        if not (isinstance(eng, schemes.ThcEngine) and eng.fused) or eng.capture or torch.is_tensor(worker_grads):
+        if not (isinstance(eng, schemes.ThcEngine) and eng.fused) or eng.capture:
             return None
+        if isinstance(worker_grads, np.ndarray) and worker_grads.ndim == 2:
+            worker_grads = torch.from_numpy(np.ascontiguousarray(worker_grads, dtype=np.float32))
+        if torch.is_tensor(worker_grads):
+            # one [n, d] host tensor: every segment of all n rows is one strided PCIe copy
+            if worker_grads.is_cuda or worker_grads.dim() != 2:
+                return None
+            if tuple(worker_grads.shape) != (self.group.size, self.dim):
+                raise ValueError("need [num_workers, dim] gradients")
+            return worker_grads.to(torch.float32).contiguous()
         if len(worker_grads) != self.group.size:
             raise ValueError("need exactly one gradient per worker")
         rows = []

@@ -194,7 +194,7 @@ class ThcEngine(Engine):
 
 
     def run_streamed(self, host_rows, stage, res_in, res_out, round_index, ledger: TrafficLedger, nmse=True,
-                     segments=16):
+                     segments=None):
         """Host-fed fused round (gc_thc_round_fused_range): segment s of every worker's gradient is
         copied host -> device on one stream while segment s-1 is validated and runs its tiles on the
         compute stream and segment s-2's estimate is copied device -> host on a third, so PCIe in,
@@ -216,6 +216,11 @@ class ThcEngine(Engine):
         self.nmse_acc = torch.zeros(2, dtype=torch.float64, device=self.device)
         bad = torch.zeros(1, dtype=torch.int64, device=self.device)
         h2d.wait_stream(cur)   # the stage buffer may still be read by the previous round
+        if segments is None:
+            # measured on B200: one strided copy per segment ([n, d] block) overlaps best at 16
+            # segments; per-row copies pay a launch per row and segment, so 8 fewer-larger ones win
+            env = os.environ.get("GC_THC_SEGMENTS")
+            segments = int(env) if env else (16 if torch.is_tensor(host_rows) else 8)
         segments = max(1, min(segments, T))
         ld = stage.stride(0)
         ev = self._ev()
@@ -225,8 +230,13 @@ class ThcEngine(Engine):
             if a >= b:
                 continue
             with torch.cuda.stream(h2d):
-                for w in range(n):
-                    stage[w, a:b].copy_(host_rows[w][a:b], non_blocking=True)
+                if torch.is_tensor(host_rows):   # [n, d] host block: one strided copy per segment
+                    _native.call("gc_copy_rows_async", stage[0, a:].data_ptr(), stage.stride(0) * 4,
+                                 host_rows[0, a:].data_ptr(), host_rows.stride(0) * 4, (b - a) * 4, n,
+                                 h2d.cuda_stream)
+                else:
+                    for w in range(n):
+                        stage[w, a:b].copy_(host_rows[w][a:b], non_blocking=True)
             cur.wait_stream(h2d)
             if ev and s == 0:
                 ev[0].record()

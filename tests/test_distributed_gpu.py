@@ -65,3 +65,39 @@ def test_two_ranks_match_reference(scheme, params, exact):
             tol = 1e-3 if params.get("bits") == 16 else 1e-5
             err = np.linalg.norm(e0.astype(np.float64) - ref) / np.linalg.norm(ref)
             assert err <= tol, (scheme, r, err)
+
+
+def _wire_rank(rank, world, scheme, params, d):
+    import torch
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.distributed import DistributedGradientPipeline
+    from tests.gpu_util import config_for
+    torch.cuda.set_device(0)
+    ef = None if scheme != "dense" else False
+    pipe = DistributedGradientPipeline(config_for(scheme, params), world, d, gcb.SeedSpec(SEED), ef)
+    g = np.random.default_rng(rank).standard_normal(d).astype(np.float32)
+    res = pipe.run_round([g], 0)
+    led = {ph: res.ledger.bits_sent(worker=rank, phase=ph) for ph in res.ledger.phases()}
+    return res.wire_bytes, led
+
+
+@pytest.mark.parametrize("scheme,params", [
+    ("rotated_quant", dict(quant_bits=4, wire_bits=8, rotation_block=1024)),
+    ("topk", dict(k=1000)),
+    ("chunked_topk", dict(chunk_size=64, chunks_selected=50)),
+    ("powersgd", dict(rank=4)),
+    ("dense", dict(bits=16)),
+    ("dense", dict(bits=32)),
+])
+def test_wire_bytes_match_reference_ledger(scheme, params):
+    """One worker per rank (n = world = 2, d = 2^17): the bytes each rank actually hands to the
+    transport, per phase, equal the reference TrafficLedger's bits / 8 for that worker
+    (collectives.py:209-262) -- the ring's reduce-scatter + all-gather volume for the all-reduce
+    phases and (n - 1) x payload for the gathers."""
+    d = 1 << 17
+    out = run_world(_wire_rank, 2, (scheme, params, d))
+    for rank in range(2):
+        wire, led = out[rank]
+        assert set(wire) == set(led), (wire, led)
+        for ph, bits in led.items():
+            assert wire[ph] * 8 == bits, (scheme, ph, wire[ph] * 8, bits)

@@ -107,10 +107,14 @@ def test_thc_host_streamed_round_matches_device_round(n, d):
              for r in range(3)]
     host = gcb.make_pipeline(gcb.RotatedQuantConfig(4, 8), n, d, seeds)
     dev = gcb.make_pipeline(gcb.RotatedQuantConfig(4, 8), n, d, seeds)
-    for r in range(3):
-        pinned = [torch.from_numpy(x).pin_memory() for x in grads[r]] if r == 1 else grads[r]
-        a = host.run_round(pinned, r)
-        b = dev.run_round(torch.from_numpy(np.stack(grads[r])).cuda(), r)
+    for r in range(4):
+        gr = grads[r % 3]
+        # round 0: list of numpy rows; 1: pinned rows; 2: one pinned [n, d] tensor (strided segment
+        # copies); 3: one [n, d] numpy array
+        feed = {0: gr, 1: [torch.from_numpy(x).pin_memory() for x in gr],
+                2: torch.from_numpy(np.stack(gr)).pin_memory(), 3: np.stack(gr)}[r]
+        a = host.run_round(feed, r)
+        b = dev.run_round(torch.from_numpy(np.stack(gr)).cuda(), r)
         assert a.estimate_host is not None and b.estimate_host is None
         assert np.array_equal(a.estimate.logical, b.estimate.logical), r
         assert torch.equal(host.residuals_tensor, dev.residuals_tensor), r
