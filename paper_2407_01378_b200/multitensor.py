@@ -20,7 +20,8 @@ from . import _native
 from .configs import PowerSgdConfig, matrix_shape_for, scheme_label
 from .ledger import TrafficLedger, WorkerGroup
 from .pipeline import RoundResult
-from .schemes import PowerSgdGroup, RoundStats, _simple_stats, make_engine, nmse_from, umma_unaligned
+from .schemes import (PowerSgdGroup, RoundStats, _simple_stats, make_engine, nmse_from, seed_q_groups,
+                      umma_unaligned)
 from .vectors import GradientVector, SeedSpec
 
 
@@ -170,7 +171,7 @@ class TensorListPipeline:
         res = self._res
         # seed matrices of every group first: their rank checks read a few bytes back to the host,
         # so doing them before the heavy kernels keeps the device queue free of bubbles
-        qs = [grp.seed_q(round_index) for grp in self.groups]
+        qs = seed_q_groups(self.groups, round_index)
         # Without nmse, ef_apply rides in the first pass over each tensor (P = M Q for the
         # compressed ones, the bypass fold for the small ones) and the residual update in the
         # decode pass.  The nmse diagnostic needs every corrected vector before any residual

@@ -430,6 +430,32 @@ class ChunkedEngine(Engine):
 
 
 # ----------------------------------------------------------------------------- PowerSGD
+def seed_q_groups(groups, round_index):
+    """Seed matrices of several PowerSGD groups with one device -> host round trip: all Gram
+    matrices are computed, copied back together and decided with batched eigvalsh; only the
+    (rare) rejected tensors loop through ensure_full_rank's redraws (compressors.py:591-603)."""
+    from .configs import DegenerateMatrixError
+    state = [grp.seed_start(round_index) for grp in groups]
+    pending = list(range(len(groups)))
+    for attempt in range(4):
+        grams = [groups[i]._gram(state[i][0]) for i in pending]
+        host = torch.cat([x.reshape(-1) for x in grams]).cpu().numpy()   # one synchronisation
+        off, still = 0, []
+        for i, gm in zip(pending, grams):
+            grp = groups[i]
+            ok = grp._rank_ok_host(host[off:off + gm.numel()].reshape(gm.shape), state[i][0])
+            off += gm.numel()
+            if not all(ok):
+                if attempt == 3:
+                    raise DegenerateMatrixError("seed matrix rank-deficient after redraws")
+                grp.seed_redraw(state[i][0], ok, state[i][1], round_index)
+                still.append(i)
+        if not still:
+            break
+        pending = still
+    return [q for q, _ in state]
+
+
 def umma_unaligned() -> bool:
     """P = M Q for unaligned rows on the tcgen05 kernel (masked scalar producer, ef_apply fused)
     rather than ef_apply + the fp64 CUDA-core kernel; GC_PSGD_MQ_UNALIGNED=cores selects the latter."""
@@ -467,53 +493,53 @@ class PowerSgdGroup:
         self.batch.ld = ld
         self.batch.rows_aligned = 1 if aligned else 0
 
-    def _rank_ok(self, q_dev):
+    def _gram(self, q_dev):
+        gram = torch.empty(self.T, self.rank, self.rank, dtype=torch.float64, device=self.device)
+        _native.call("gc_psgd_gram", self.T, self.cols, self.rank, q_dev.data_ptr(), gram.data_ptr(), _sp())
+        return gram
+
+    def _rank_ok_host(self, host_gram, q_dev):
         """Per tensor: np.linalg.matrix_rank(q) == rank (compressors.py:599), decided from the fp64
-        Gram eigenvalues computed on the device; near numpy's tolerance the exact numpy call on a
-        host copy decides."""
+        Gram eigenvalues (one batched eigvalsh for all T tensors); near numpy's tolerance the exact
+        numpy call on a host copy decides."""
         import numpy as np
-        T, r, cols = self.T, self.rank, self.cols
-        gram = torch.empty(T, r, r, dtype=torch.float64, device=self.device)
-        _native.call("gc_psgd_gram", T, cols, r, q_dev.data_ptr(), gram.data_ptr(), _sp())
-        ok = []
-        host = gram.cpu().numpy()
-        for t in range(T):
-            sig = np.sqrt(np.clip(np.linalg.eigvalsh(host[t]), 0.0, None))
-            tol = sig.max() * max(cols, r) * np.finfo(np.float32).eps
-            if np.all((sig > 2 * tol) | (sig < 0.5 * tol)):
-                ok.append(int(np.count_nonzero(sig > tol)) == r)
-            else:
-                ok.append(int(np.linalg.matrix_rank(q_dev[t].cpu().numpy())) == r)
-        return ok
+        r, cols = self.rank, self.cols
+        sig = np.sqrt(np.clip(np.linalg.eigvalsh(host_gram), 0.0, None))           # [T, r]
+        tol = sig.max(axis=1, keepdims=True) * max(cols, r) * np.finfo(np.float32).eps
+        clear = np.all((sig > 2 * tol) | (sig < 0.5 * tol), axis=1)
+        ok = np.count_nonzero(sig > tol, axis=1) == r
+        for t in np.nonzero(~clear)[0]:
+            ok[t] = int(np.linalg.matrix_rank(q_dev[t].cpu().numpy())) == r
+        return [bool(x) for x in ok]
+
+    def _rank_ok(self, q_dev):
+        return self._rank_ok_host(self._gram(q_dev).cpu().numpy(), q_dev)
+
+    def seed_start(self, round_index):
+        """The round's candidate seed matrices (warm Q or the first draw) and the draw counts."""
+        import numpy as np
+        T, cols, r = self.T, self.cols, self.rank
+        if self.cfg.warm_start and self.warm is not None:
+            return self.warm.clone(), [0] * T
+        first = self.seeds.rng("lowrank-seed", round_index).standard_normal((cols, r)).astype(np.float32)
+        return torch.from_numpy(first).to(self.device).unsqueeze(0).repeat(T, 1, 1).contiguous(), [1] * T
+
+    def seed_redraw(self, q, ok, draws, round_index):
+        """ensure_full_rank's redraw of every rejected tensor from its own rng stream."""
+        import numpy as np
+        cols, r = self.cols, self.rank
+        for t in range(self.T):
+            if not ok[t]:   # continue this tensor's own rng stream
+                rng = self.seeds.rng("lowrank-seed", round_index)
+                for _ in range(draws[t]):
+                    rng.standard_normal((cols, r))
+                q[t] = torch.from_numpy(rng.standard_normal((cols, r)).astype(np.float32)).to(self.device)
+                draws[t] += 1
 
     def seed_q(self, round_index):
         """Seed matrices with ensure_full_rank's redraws, one reference rng per tensor
         (pipelines.py:341-346, compressors.py:591-603)."""
-        import numpy as np
-        from .configs import DegenerateMatrixError
-        T, cols, r = self.T, self.cols, self.rank
-        warm = self.cfg.warm_start and self.warm is not None
-        if warm:
-            q = self.warm.clone()
-            draws = [0] * T
-        else:
-            first = self.seeds.rng("lowrank-seed", round_index).standard_normal((cols, r)).astype(np.float32)
-            q = torch.from_numpy(first).to(self.device).unsqueeze(0).repeat(T, 1, 1).contiguous()
-            draws = [1] * T
-        for attempt in range(4):
-            ok = self._rank_ok(q)
-            if all(ok):
-                return q
-            if attempt == 3:
-                raise DegenerateMatrixError("seed matrix rank-deficient after redraws")
-            for t in range(T):
-                if not ok[t]:   # continue this tensor's own rng stream
-                    rng = self.seeds.rng("lowrank-seed", round_index)
-                    for _ in range(draws[t]):
-                        rng.standard_normal((cols, r))
-                    q[t] = torch.from_numpy(rng.standard_normal((cols, r)).astype(np.float32)).to(self.device)
-                    draws[t] += 1
-        return q
+        return seed_q_groups([self], round_index)[0]
 
     def run(self, c_ptr: int, resid_ptr, est_ptr: int, round_index: int, grads_ptr=None, vec=False, fold=None,
             before_ef=None, q=None, ef_resid_ptr=None):
