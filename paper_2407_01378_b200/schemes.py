@@ -438,13 +438,28 @@ def seed_q_groups(groups, round_index):
     state = [grp.seed_start(round_index) for grp in groups]
     pending = list(range(len(groups)))
     for attempt in range(4):
-        grams = [groups[i]._gram(state[i][0]) for i in pending]
-        host = torch.cat([x.reshape(-1) for x in grams]).cpu().numpy()   # one synchronisation
+        # warm Q of the previous round: its Gram is already on the host once that event fired
+        ready = {}
+        if attempt == 0:
+            for i in pending:
+                grp = groups[i]
+                pg = grp._pending_gram
+                if pg is not None and pg[0] is grp.warm and grp.cfg.warm_start:
+                    pg[1].synchronize()
+                    ready[i] = grp._gram_host.numpy().copy()
+        todo = [i for i in pending if i not in ready]
+        grams = [groups[i]._gram(state[i][0]) for i in todo]
+        host = torch.cat([x.reshape(-1) for x in grams]).cpu().numpy() if grams else None   # one sync
         off, still = 0, []
-        for i, gm in zip(pending, grams):
+        for i in pending:
             grp = groups[i]
-            ok = grp._rank_ok_host(host[off:off + gm.numel()].reshape(gm.shape), state[i][0])
-            off += gm.numel()
+            if i in ready:
+                hg = ready[i]
+            else:
+                gm = grams[todo.index(i)]
+                hg = host[off:off + gm.numel()].reshape(gm.shape)
+                off += gm.numel()
+            ok = grp._rank_ok_host(hg, state[i][0])
             if not all(ok):
                 if attempt == 3:
                     raise DegenerateMatrixError("seed matrix rank-deficient after redraws")
@@ -488,6 +503,8 @@ class PowerSgdGroup:
         self.mgs_ws = torch.empty(T * self.rows * self.rank, dtype=torch.float64, device=device)
         self.warm = None          # [T][cols][r]
         self.last = {}
+        self._gram_host = None    # pinned [T][r][r]: Gram of the warm Q, filled behind an event
+        self._pending_gram = None
 
     def set_ld(self, ld: int, aligned: bool = False):
         self.batch.ld = ld
@@ -579,6 +596,19 @@ class PowerSgdGroup:
         _native.call("gc_psgd_mtp", bref, d, rows, cols, r, c_ptr, p_hat.data_ptr(), qw.data_ptr(),
                      self.ws.data_ptr(), sp)
         q_sum = fold("right-factor", qw, cols * r).reshape(T, cols, r)
+        # warm Q (pipelines.py:366) before the decode, and its Gram copied to pinned host memory
+        # behind an event: the next round's rank check (ensure_full_rank) then reads it without
+        # draining the device, so that round's kernels queue while this round's decode runs
+        warm = torch.empty(T, cols, r, dtype=torch.float32, device=dev)
+        _native.call("gc_scale_div", T * cols * r, q_sum.data_ptr(), n, warm.data_ptr(), sp)
+        self.warm = warm
+        if self.cfg.warm_start:
+            if self._gram_host is None:
+                self._gram_host = torch.empty(T, r, r, dtype=torch.float64, pin_memory=True)
+            self._gram_host.copy_(self._gram(warm), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pending_gram = (warm, ev)
         if before_ef is None and resid_ptr is not None:   # EF update and estimate in one pass
             _native.call("gc_psgd_decode_fused", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
                          q_sum.data_ptr(), resid_ptr, est_ptr, sp)
@@ -590,9 +620,6 @@ class PowerSgdGroup:
             if resid_ptr is not None:
                 _native.call("gc_psgd_decode", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
                              q_sum.data_ptr(), resid_ptr, None, sp)
-        warm = torch.empty(T, cols, r, dtype=torch.float32, device=dev)
-        _native.call("gc_scale_div", T * cols * r, q_sum.data_ptr(), n, warm.data_ptr(), sp)   # pipelines.py:366
-        self.warm = warm
         self.last = {"p_hat": p_hat, "q_sum": q_sum, "seed_q": q, "status": status, "qw": qw}
         return warm
 
