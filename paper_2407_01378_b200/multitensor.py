@@ -87,7 +87,9 @@ class TensorListPipeline:
             if s >= cfg.bypass_below:
                 groups.setdefault(s, []).append(t)
         self.groups = []
-        for s, ts in groups.items():
+        # smallest batches first: the round ends with the longest decode, behind which the host
+        # reads the warm-Q Gram events and queues the next round (groups are independent)
+        for s, ts in sorted(groups.items(), key=lambda kv: kv[0] * len(kv[1])):
             rows = [w * D + int(self.offsets[t]) for t in ts for w in range(n)]
             ro = torch.tensor(rows, dtype=torch.int64, device=dev)
             eo = torch.tensor([int(self.offsets[t]) for t in ts], dtype=torch.int64, device=dev)
