@@ -16,7 +16,9 @@ if name == "psgd_gpt2m":
     pipe = TensorListPipeline(gcb.PowerSgdConfig(4), n, sizes, gcb.SeedSpec(2024), validate=False, compute_nmse=False)
 else:
     d, cfg = {"topk": (110_000_000, gcb.TopKConfig(1_100_000)), "thc": (25_557_032, gcb.RotatedQuantConfig(4, 8)),
-              "psgd": (350_000_000, gcb.PowerSgdConfig(4))}[name]
+              "psgd": (350_000_000, gcb.PowerSgdConfig(4)),
+              "topkc": (110_000_000, gcb.ChunkedTopKConfig(64, 17_187)),
+              "dense16": (25_557_032, gcb.DenseConfig(16))}[name]
     pipe = gcb.make_pipeline(cfg, n, d, gcb.SeedSpec(2024), validate=False, compute_nmse=False)
 g = torch.randn(n, d, device="cuda")
 for r in range(3):
