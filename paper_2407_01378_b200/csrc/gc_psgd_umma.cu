@@ -29,15 +29,22 @@
 
 namespace {
 
-constexpr int kM = 128;          // UMMA M: rows per CTA
+#ifndef GC_MQ_M64
+#define GC_MQ_M64 0
+#endif
+// M64: UMMA M = 64 rows per CTA with 64-column (two 128-byte swizzle atoms) stages -- the same
+// shared memory per stage, 256-byte row segments per load and half the concurrent row streams
+constexpr int kM = GC_MQ_M64 ? 64 : 128;   // UMMA M: rows per CTA
 constexpr int kN = 16;           // UMMA N: rank padded to 16
-constexpr int kKc = 32;          // columns per stage: one 128-byte swizzle atom of tf32
+constexpr int kKc = GC_MQ_M64 ? 64 : 32;   // columns per stage: 128-byte swizzle atoms of tf32
+constexpr int kAtoms = kKc / 32;           // swizzle atoms along K per stage
+constexpr int kF4Row = kKc / 4;            // float4 per row of a chunk
 #ifndef GC_MQ_STAGES
 #define GC_MQ_STAGES 2
 #endif
 constexpr int kStages = GC_MQ_STAGES;   // smem ring depth (36 KB per stage)
 constexpr int kThreads = 256;
-constexpr int kGroup = 16;       // chunks per TMEM partial (512 columns) before the fp64 fold
+constexpr int kGroup = 512 / kKc;   // chunks per TMEM partial (512 columns) before the fp64 fold
 constexpr int kATile = kM * kKc * 4;    // 16 KB
 constexpr int kBTile = kN * kKc * 4;    // 2 KB
 constexpr int kStageBytes = 2 * kATile + 2 * kBTile;
@@ -54,6 +61,11 @@ struct Rows {
 // byte offset of (row, 16-byte chunk) in a K-major SWIZZLE_128B tile (1024-byte aligned)
 __device__ __forceinline__ uint32_t sw128(int row, int chunk) {
   return static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4));
+}
+// (row, 16-byte chunk ch of the stage's kKc columns) in a tile of `rows` rows stored atom-major:
+// swizzle atom ch / 8 occupies rows * 128 bytes
+__device__ __forceinline__ uint32_t tile_off(int rows, int row, int ch) {
+  return static_cast<uint32_t>((ch >> 3) * rows * 128) + sw128(row, ch & 7);
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B between 8-row groups,
@@ -175,8 +187,11 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
             "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // M = 128: lane = row 32 warp + lane; M = 64: rows 16 warp + lane live in lanes 0-15
+      if (kM == 128 || lane < 16) {
 #pragma unroll
-      for (int b = 0; b < R; ++b) acc64[b] += static_cast<double>(__uint_as_float(x[b]));
+        for (int b = 0; b < R; ++b) acc64[b] += static_cast<double>(__uint_as_float(x[b]));
+      }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     }
   };
@@ -190,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int f = tid + kThreads * u;
-      const int64_t grow = row0 + (f >> 3), col = col0 + 4 * (f & 7);
+      const int64_t grow = row0 + f / kF4Row, col = col0 + 4 * (f % kF4Row);
       const int64_t i = grow * cols + col;
       pg[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       pr[u] = pg[u];
@@ -235,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int f = tid + kThreads * u;
-      const int row = f >> 3, ch = f & 7;
+      const int row = f / kF4Row, ch = f % kF4Row;
       const int64_t grow = row0 + row, col = col0 + 4 * ch;
       const int64_t i = grow * cols + col;
       float4 c = cg[u];
@@ -262,13 +277,13 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
       split3(c.y, hb.y, hs.y);
       split3(c.z, hb.z, hs.z);
       split3(c.w, hb.w, hs.w);
-      const uint32_t off = sw128(row, ch);
+      const uint32_t off = tile_off(kM, row, ch);
       *reinterpret_cast<float4 *>(sm + (a_big(s) - base) + off) = hb;
       *reinterpret_cast<float4 *>(sm + (a_small(s) - base) + off) = hs;
     }
     // ---- B = Q^T for the chunk (rows n < R; 8 threads per row, 4 columns each)
-    if (tid < R * 8) {
-      const int n = tid >> 3, ch = tid & 7;
+    if (tid < R * kF4Row) {
+      const int n = tid / kF4Row, ch = tid % kF4Row;
       float t[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -280,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
       split3(t[1], hb.y, hs.y);
       split3(t[2], hb.z, hs.z);
       split3(t[3], hb.w, hs.w);
-      const uint32_t off = sw128(n, ch);
+      const uint32_t off = tile_off(kN, n, ch);
       *reinterpret_cast<float4 *>(sm + (b_big(s) - base) + off) = hb;
       *reinterpret_cast<float4 *>(sm + (b_small(s) - base) + off) = hs;
     }
@@ -296,8 +311,9 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
       const uint32_t dcol = tmem + static_cast<uint32_t>((gi & 1) * kN);
 #pragma unroll
       for (int kk = 0; kk < kKc / 8; ++kk) {
-        const uint64_t ab = sdesc(a_big(s) + 32 * kk), as = sdesc(a_small(s) + 32 * kk);
-        const uint64_t bb = sdesc(b_big(s) + 32 * kk), bs = sdesc(b_small(s) + 32 * kk);
+        const uint32_t ao = (kk >> 2) * kM * 128 + 32 * (kk & 3), bo = (kk >> 2) * kN * 128 + 32 * (kk & 3);
+        const uint64_t ab = sdesc(a_big(s) + ao), as = sdesc(a_small(s) + ao);
+        const uint64_t bb = sdesc(b_big(s) + bo), bs = sdesc(b_small(s) + bo);
         const uint32_t accum = (k % kGroup != 0 || kk != 0) ? 1u : 0u;
         umma_tf32(dcol, as, bb, accum);
         umma_tf32(dcol, ab, bs, 1u);
@@ -311,8 +327,8 @@ __global__ void __launch_bounds__(kThreads, 2) mq_umma_kernel(int64_t d, int64_t
   }
   if (nloc > 0) fold_group((nloc - 1) / kGroup);
 
-  if (warp < 4) {
-    const int64_t grow = row0 + warp * 32 + lane;
+  if (warp < 4 && (kM == 128 || lane < 16)) {
+    const int64_t grow = row0 + warp * (kM / 4) + lane;
     if (grow < rows) {
 #pragma unroll
       for (int b = 0; b < R; ++b)
