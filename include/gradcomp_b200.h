@@ -109,6 +109,11 @@ int gc_thc_quantize(const gc_thc_geom *g, int32_t workers, const float *x_rot,
                     const float *shared_ranges, const gc_pcg64 *coin_streams, int8_t *codes,
                     int64_t *counters, void *stream);
 
+/* Nibble wire of the distributed THC exchange for wire_bits <= 4 (codes and saturated sums in
+ * [-7, 7]): two values per byte, element 2i low nibble, 2i+1 high; len even.  The transport then
+ * carries the ledger's b = 4 bits per coordinate (collectives.py:209-233). */
+int gc_pack_nibbles(int64_t len, const int8_t *codes, uint8_t *packed, void *stream);
+int gc_unpack_nibbles(int64_t len, const uint8_t *packed, int8_t *codes, void *stream);
 /* Ordered saturating fold (SatIntSum.combine in ring order, collectives.py:123-143,215-226):
  * for element e (global index offset+e) start worker s = floor((offset+e)/ring_block);
  * acc = z[s]; acc = clip(acc + z[(s+k)%n], +-(2^(bits-1)-1)) for k=1..n-1.

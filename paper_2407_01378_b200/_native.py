@@ -119,6 +119,8 @@ SIGNATURES = {
     "gc_psgd_decode_fused": (c_int, [POINTER(PsgdBatch), I32, I64, I64, I64, I32, P, P, P, P, P, P]),
     "gc_psgd_gram": (c_int, [I32, I64, I32, P, P, P]),
     "gc_fill_zero": (c_int, [P, I64, P]),
+    "gc_pack_nibbles": (c_int, [I64, P, P, P]),
+    "gc_unpack_nibbles": (c_int, [I64, P, P, P]),
     "gc_copy_rows_async": (c_int, [P, I64, P, I64, I64, I64, P]),
 }
 

@@ -434,9 +434,47 @@ ThcArgs base_args(const gc_thc_geom *g, int mode, int workers) {
   return a;
 }
 
+// Nibble wire for b <= 4: codes and saturated sums lie in [-7, 7], two per byte (element 2i in
+// the low nibble, 2i + 1 in the high one; unpacking sign-extends).
+__global__ void pack_nibbles_kernel(int64_t pairs, const int8_t *in, uint8_t *out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < pairs;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<uint8_t>((static_cast<uint8_t>(in[2 * i]) & 0xFu) | (static_cast<uint8_t>(in[2 * i + 1]) << 4));
+}
+
+__global__ void unpack_nibbles_kernel(int64_t pairs, const uint8_t *in, int8_t *out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < pairs;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int v = in[i];
+    out[2 * i] = static_cast<int8_t>(static_cast<int8_t>(v << 4) >> 4);
+    out[2 * i + 1] = static_cast<int8_t>(static_cast<int8_t>(v) >> 4);
+  }
+}
+
+int nibble_grid(int64_t pairs) {
+  const int64_t g = (pairs + 255) / 256;
+  return static_cast<int>(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
+}
+
 }  // namespace
 
 extern "C" {
+
+int gc_pack_nibbles(int64_t len, const int8_t *codes, uint8_t *packed, void *stream) {
+  GC_REQUIRE(len >= 0 && len % 2 == 0 && (len == 0 || (codes && packed)), "need an even length and buffers");
+  if (len == 0) return GC_OK;
+  pack_nibbles_kernel<<<nibble_grid(len / 2), 256, 0, static_cast<cudaStream_t>(stream)>>>(len / 2, codes, packed);
+  GC_LAUNCH_CHECK("pack_nibbles_kernel");
+  return GC_OK;
+}
+
+int gc_unpack_nibbles(int64_t len, const uint8_t *packed, int8_t *codes, void *stream) {
+  GC_REQUIRE(len >= 0 && len % 2 == 0 && (len == 0 || (codes && packed)), "need an even length and buffers");
+  if (len == 0) return GC_OK;
+  unpack_nibbles_kernel<<<nibble_grid(len / 2), 256, 0, static_cast<cudaStream_t>(stream)>>>(len / 2, packed, codes);
+  GC_LAUNCH_CHECK("unpack_nibbles_kernel");
+  return GC_OK;
+}
 
 int64_t gc_thc_active_len(const gc_thc_geom *g) {
   if (!g || g->block < 1) return 0;

@@ -124,8 +124,20 @@ def fold_slices(active: int, world: int, align: int = 256):
     return s
 
 
+def _nibbles(x: torch.Tensor, pack: bool) -> torch.Tensor:
+    """int8 [.., 2m] <-> uint8 [.., m] nibble pairs on the device (gc_pack_nibbles)."""
+    x = x.contiguous()
+    if pack:
+        out = torch.empty(x.shape[:-1] + (x.shape[-1] // 2,), dtype=torch.uint8, device=x.device)
+        _native.call("gc_pack_nibbles", x.numel(), x.data_ptr(), out.data_ptr(), _sp())
+    else:
+        out = torch.empty(x.shape[:-1] + (x.shape[-1] * 2,), dtype=torch.int8, device=x.device)
+        _native.call("gc_unpack_nibbles", out.numel(), x.data_ptr(), out.data_ptr(), _sp())
+    return out
+
+
 def exchange_fold(codes: torch.Tensor, comm: Comm, n: int, active: int, slice_len: int, fold_fn, out_dtype,
-                  send: torch.Tensor | None = None, phase: str | None = None) -> torch.Tensor:
+                  send: torch.Tensor | None = None, phase: str | None = None, nibble: bool = False) -> torch.Tensor:
     """Saturating code sums over all n workers, reference ring order (collectives.py:215-235).
 
     codes: this rank's [L, active] int8 codes (global workers rank*L .. rank*L+L-1).  Slice
@@ -139,12 +151,17 @@ def exchange_fold(codes: torch.Tensor, comm: Comm, n: int, active: int, slice_le
         lo, hi = dst * slice_len, min(active, (dst + 1) * slice_len)
         if hi > lo:
             send[dst, :, : hi - lo].copy_(codes[:, lo:hi])
-    recv = comm.all_to_all(send, phase).reshape(n, slice_len)
+    if nibble:   # wire_bits <= 4: codes and sums travel as packed nibbles (the ledger's b bits)
+        recv = _nibbles(comm.all_to_all(_nibbles(send, True), phase), False).reshape(n, slice_len)
+    else:
+        recv = comm.all_to_all(send, phase).reshape(n, slice_len)
     s0 = comm.rank * slice_len
     my_len = max(0, min(slice_len, active - s0))
     sums = torch.zeros(slice_len, dtype=out_dtype, device=codes.device)
     if my_len:
         fold_fn(recv, my_len, s0, sums)
+    if nibble:
+        return _nibbles(comm.all_gather_rows(_nibbles(sums.reshape(1, -1), True), phase), False).reshape(-1)
     return comm.all_gather_rows(sums.reshape(1, -1), phase).reshape(-1)
 
 
@@ -327,7 +344,7 @@ class _Thc(_Base):
                 out[:length].copy_(rows[0, :length])
 
         sums = exchange_fold(self.codes, comm, n, self.active, self.S, fold, self.sum_dtype, self.send,
-                             "code-aggregate")
+                             "code-aggregate", nibble=cfg.wire_bits <= 4)
         est = torch.empty(self.dim, dtype=torch.float32, device=self.dev)
         _native.call("gc_thc_decode_estimate", geom, n, sums.data_ptr(), self.sum_bytes, shared.data_ptr(),
                      self.signs.data_ptr(), est.data_ptr(), _ptr(self.ws), sp)

@@ -83,6 +83,7 @@ def _wire_rank(rank, world, scheme, params, d):
 
 @pytest.mark.parametrize("scheme,params", [
     ("rotated_quant", dict(quant_bits=4, wire_bits=8, rotation_block=1024)),
+    ("rotated_quant", dict(quant_bits=4, wire_bits=4, rotation_block=1024)),   # packed nibble wire
     ("topk", dict(k=1000)),
     ("chunked_topk", dict(chunk_size=64, chunks_selected=50)),
     ("powersgd", dict(rank=4)),
