@@ -506,33 +506,55 @@ __global__ void __launch_bounds__(1024) find_kernel(Work wk, int level) {
 
 // One CTA per worker: eq prefix (tie ranks) and selected-count prefix (output offsets).
 __global__ void __launch_bounds__(1024) tile_scan_kernel(Work wk, int64_t tiles) {
-  using Scan = cub::BlockScan<long long, 1024>;
+  // kItems consecutive tiles per thread: a thread-local scan plus one block scan per 4096 tiles
+  // (the block scans are the serial part: 7 steps instead of 27 at cfg3's 27K tiles).  Counts
+  // and offsets fit int32: rows are shorter than 2^31 (gc_topk_select checks it).
+  constexpr int kItems = 4;
+  using Scan = cub::BlockScan<int, 1024>;
   __shared__ typename Scan::TempStorage tmp;
-  __shared__ long long carry_eq, carry_sel;
+  __shared__ int carry_eq, carry_sel;
   const int w = blockIdx.x;
-  const long long m = wk.state[w].take_eq;
+  const int m = static_cast<int>(wk.state[w].take_eq);
   if (threadIdx.x == 0) carry_eq = carry_sel = 0;
   __syncthreads();
-  for (int64_t t0 = 0; t0 < tiles; t0 += 1024) {
-    const int64_t t = t0 + threadIdx.x;
-    const long long eq = t < tiles ? wk.tile_eq[w * tiles + t] : 0;
-    long long eq_ex;
-    Scan(tmp).ExclusiveSum(eq, eq_ex);
+  for (int64_t t0 = 0; t0 < tiles; t0 += 1024 * kItems) {
+    const int64_t tb = t0 + static_cast<int64_t>(threadIdx.x) * kItems;
+    int eq[kItems], gt[kItems], eq_local = 0;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const int64_t t = tb + j;
+      eq[j] = t < tiles ? static_cast<int>(wk.tile_eq[w * tiles + t]) : 0;
+      gt[j] = t < tiles ? static_cast<int>(wk.tile_gt[w * tiles + t]) : 0;
+      eq_local += eq[j];
+    }
+    int eq_ex;
+    Scan(tmp).ExclusiveSum(eq_local, eq_ex);
     __syncthreads();
-    eq_ex += carry_eq;
-    long long take = m - eq_ex;
-    take = take < 0 ? 0 : (take > eq ? eq : take);
-    const long long sel = (t < tiles ? wk.tile_gt[w * tiles + t] : 0) + take;
-    long long sel_ex;
-    long long sel_tot;
-    Scan(tmp).ExclusiveSum(sel, sel_ex, sel_tot);
+    int eq_run = eq_ex + carry_eq, sel_local = 0, sel[kItems], eq_ofs[kItems];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      eq_ofs[j] = eq_run;
+      int take = m - eq_run;
+      take = take < 0 ? 0 : (take > eq[j] ? eq[j] : take);
+      sel[j] = gt[j] + take;
+      sel_local += sel[j];
+      eq_run += eq[j];
+    }
+    int sel_ex, sel_tot;
+    Scan(tmp).ExclusiveSum(sel_local, sel_ex, sel_tot);
     __syncthreads();
-    if (t < tiles) {
-      wk.tile_eq_off[w * tiles + t] = eq_ex;
-      wk.tile_sel_off[w * tiles + t] = sel_ex + carry_sel;
+    int sel_run = sel_ex + carry_sel;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const int64_t t = tb + j;
+      if (t < tiles) {
+        wk.tile_eq_off[w * tiles + t] = eq_ofs[j];
+        wk.tile_sel_off[w * tiles + t] = sel_run;
+      }
+      sel_run += sel[j];
     }
     __syncthreads();
-    if (threadIdx.x == 1023) carry_eq = eq_ex + eq;
+    if (threadIdx.x == 1023) carry_eq = eq_run;
     if (threadIdx.x == 0) carry_sel += sel_tot;
     __syncthreads();
   }
