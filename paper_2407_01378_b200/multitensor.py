@@ -67,6 +67,7 @@ class TensorListPipeline:
         n, D = num_workers, self.dim
         self._res = torch.zeros(n, D, dtype=torch.float32, device=self.device) if self.error_feedback else None
         self._stage = None
+        self._fold_out = {}
         self.batched = isinstance(config, PowerSgdConfig)
         self.launches = 0
         if self.batched:
@@ -100,7 +101,10 @@ class TensorListPipeline:
 
     def _fold(self, kind, x, m):
         n = self.group.size
-        out = torch.empty(x.shape[0] // n, m, dtype=torch.float32, device=self.device)
+        key = (kind, x.data_ptr(), x.shape[0] // n, m)   # one reused output per group input buffer
+        out = self._fold_out.get(key)
+        if out is None:
+            out = self._fold_out[key] = torch.empty(x.shape[0] // n, m, dtype=torch.float32, device=self.device)
         _native.call("gc_float_fold_batched", x.shape[0] // n, n, m, x.data_ptr(), m, n * m, 0, 0, 0, out.data_ptr(),
                      m, _sp())
         return out

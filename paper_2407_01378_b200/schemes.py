@@ -505,6 +505,13 @@ class PowerSgdGroup:
         self.last = {}
         self._gram_host = None    # pinned [T][r][r]: Gram of the warm Q, filled behind an event
         self._pending_gram = None
+        self._bufs = {}           # per-round device buffers, allocated once (no allocator traffic)
+
+    def _buf(self, name, shape, dtype=torch.float32):
+        b = self._bufs.get(name)
+        if b is None or tuple(b.shape) != tuple(shape) or b.dtype != dtype:
+            b = self._bufs[name] = torch.empty(shape, dtype=dtype, device=self.device)
+        return b
 
     def set_ld(self, ld: int, aligned: bool = False):
         self.batch.ld = ld
@@ -573,7 +580,7 @@ class PowerSgdGroup:
         bref = ctypes.byref(self.batch)
         if q is None:
             q = self.seed_q(round_index)
-        p = torch.empty(T * L, rows, r, dtype=torch.float32, device=dev)
+        p = self._buf("p", (T * L, rows, r))
         # P = M Q on tcgen05: float4 producer for aligned rows, masked scalars otherwise
         umma = vec or umma_unaligned()
         if umma and ef_resid_ptr is not None:
@@ -588,18 +595,18 @@ class PowerSgdGroup:
         else:
             _native.call("gc_psgd_mq", bref, d, rows, cols, r, c_ptr, q.data_ptr(), p.data_ptr(), sp)
         p_sum = fold("left-factor", p, rows * r).reshape(T, rows, r)
-        p_hat = torch.empty(T, rows, r, dtype=torch.float32, device=dev)
-        status = torch.zeros(T, dtype=torch.int32, device=dev)
+        p_hat = self._buf("p_hat", (T, rows, r))
+        status = self._buf("status", (T,), torch.int32).zero_()
         _native.call("gc_psgd_orthonormalize", T, rows, r, p_sum.data_ptr(), p_hat.data_ptr(), self.mgs_ws.data_ptr(),
                      status.data_ptr(), sp)
-        qw = torch.empty(T * L, cols, r, dtype=torch.float32, device=dev)
+        qw = self._buf("qw", (T * L, cols, r))
         _native.call("gc_psgd_mtp", bref, d, rows, cols, r, c_ptr, p_hat.data_ptr(), qw.data_ptr(),
                      self.ws.data_ptr(), sp)
         q_sum = fold("right-factor", qw, cols * r).reshape(T, cols, r)
         # warm Q (pipelines.py:366) before the decode, and its Gram copied to pinned host memory
         # behind an event: the next round's rank check (ensure_full_rank) then reads it without
         # draining the device, so that round's kernels queue while this round's decode runs
-        warm = torch.empty(T, cols, r, dtype=torch.float32, device=dev)
+        warm = self._buf("warm", (T, cols, r))   # the next round clones it before overwriting
         _native.call("gc_scale_div", T * cols * r, q_sum.data_ptr(), n, warm.data_ptr(), sp)
         self.warm = warm
         if self.cfg.warm_start:
