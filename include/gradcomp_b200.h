@@ -268,6 +268,16 @@ int gc_psgd_mq_fused(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t co
 /* Q_w = M_w^T P_hat (pipelines.py:354). */
 int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                 const float *p_hat, float *q, void *workspace, void *stream);
+/* Q_w = M_w^T P_hat (pipelines.py:354) fused with the EF update r_w = c_w - P_hat Q_w^T
+ * (pipelines.py:357-361, the own-decode half of gc_psgd_decode): resid holds the corrected
+ * matrices on entry and the residuals on return, q receives Q_w.  One read and one write of M
+ * (a 16-CTA cluster per 32-column strip, partial Q summed over distributed shared memory).
+ * GC_ERR_UNSUPPORTED unless gc_psgd_mtp_ef_supported(rows, cols, rank, rows_aligned).
+ * Moves the algorithmic bytes only, but measured slower than gc_psgd_mtp + gc_psgd_decode on
+ * B200 (strided 128-byte segments); the host uses it only with GC_PSGD_MTP_EF=1. */
+int gc_psgd_mtp_ef_supported(int64_t rows, int64_t cols, int32_t rank, int32_t rows_aligned);
+int gc_psgd_mtp_ef(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, float *resid,
+                   const float *p_hat, float *q, void *stream);
 /* orthonormalize (compressors.py:555-588) for T tensors: fp64 modified Gram-Schmidt with
  * canonical-basis completion; status[t] = 1 if completion failed (DegenerateMatrixError).
  * workspace: T*rows*rank doubles. */

@@ -20,6 +20,7 @@
 // same kernels with coalesced scalar accesses otherwise (e.g. GPT-2's 1774 x 1774 matrices).
 // MGS runs in one CTA in fp64 (column-by-column projections, block reductions), including
 // the reference's canonical-basis completion of degenerate columns.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -515,7 +516,155 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
   }
 }
 
+// Q_w = M_w^T P_hat fused with the EF update r_w = c_w - P_hat Q_w^T: one read and one write of
+// M instead of mtp's read plus decode's read-modify-write.  A cluster of kEfCta CTAs owns a
+// kEfCols-column strip of one worker's matrix; each CTA stages its rows of the strip in shared
+// memory (cp.async, all loads in flight), forms its partial Q in fp32 FMAs folded to fp64, the
+// cluster sums the partials over distributed shared memory in rank order, and every CTA then
+// writes its rows' residuals straight from shared memory.  Aligned shapes (cols % 4 == 0,
+// 16-byte rows) whose strip fits the shared-memory budget; the estimate stays in decode.
+// Opt-in: exactly the algorithmic DRAM bytes, but the strided 128-byte segments run at ~1.7 TB/s.
+constexpr int kEfCta = 16;          // CTAs per cluster (row slices of a strip)
+#ifndef GC_PSGD_EF_COLS
+#define GC_PSGD_EF_COLS 32
+#endif
+constexpr int kEfCols = GC_PSGD_EF_COLS;   // strip width (kEfQ float4 per row)
+constexpr int kEfQ = kEfCols / 4;
+constexpr int kEfThreads = 256;            // kEfThreads / kEfQ rows per sweep
+constexpr int64_t kEfSmemRows = 196608 / (kEfCols * 4);   // rows a CTA stages (192 KB)
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+template <int R>
+__global__ void __launch_bounds__(kEfThreads) mtp_ef_kernel(int64_t d, int64_t rows, int64_t cols, float *resid,
+                                                            Rows rw_, const float *ph, float *qw,
+                                                            int64_t rows_per_cta) {
+  namespace cgr = cooperative_groups;
+  cgr::cluster_group cl = cgr::this_cluster();
+  extern __shared__ __align__(16) unsigned char ef_smem[];
+  double *qp = reinterpret_cast<double *>(ef_smem);               // [kEfCols][R] CTA partial
+  double *wred = qp + kEfCols * R;                                 // [8 warps][kEfCols][R]
+  float *qf = reinterpret_cast<float *>(wred + 8 * kEfCols * R);   // [kEfCols][R] Q_w strip
+  float4 *ms = reinterpret_cast<float4 *>(qf + kEfCols * R);       // [rows_per_cta][kEfQ]
+  const int crank = static_cast<int>(cl.block_rank());
+  const int v = blockIdx.y;
+  const int64_t col0 = static_cast<int64_t>(blockIdx.x / kEfCta) * kEfCols;
+  const int64_t r0 = crank * rows_per_cta;
+  const int64_t r1 = min(rows, r0 + rows_per_cta);
+  const int nr = r1 > r0 ? static_cast<int>(r1 - r0) : 0;
+  float *cw = resid + rw_.at(v);
+  ph += static_cast<int64_t>(rw_.tensor(v)) * rows * R;
+  constexpr int kSweep = kEfThreads / kEfQ;
+  const int qd = threadIdx.x % kEfQ, rg = threadIdx.x / kEfQ;
+  const int64_t col = col0 + 4 * qd;
+  const bool colok = col < cols;
+  // stage: element (i, col..col+3) of the padded matrix; entries at flat index >= d are zero
+  for (int a = rg; a < nr; a += kSweep) {
+    const int64_t i = (r0 + a) * cols + col;
+    float4 *dst = ms + a * kEfQ + qd;
+    if (colok && i + 3 < d) {
+      cp_async16(dst, cw + i);
+    } else {
+      float t4[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) t4[t] = colok && i + t < d ? cw[i + t] : 0.0f;
+      *dst = make_float4(t4[0], t4[1], t4[2], t4[3]);
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  // partial Q over this CTA's rows: fp32 FMAs per thread, folded to fp64
+  double acc[4][R];
+  {
+    float a32[4][R];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b) a32[t][b] = 0.0f;
+    for (int a = rg; a < nr; a += kSweep) {
+      const float4 m = ms[a * kEfQ + qd];
+      const float m4[4] = {m.x, m.y, m.z, m.w};
+      const float *pr = ph + (r0 + a) * R;
+      float pv[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) pv[b] = __ldg(pr + b);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int b = 0; b < R; ++b) a32[t][b] = fmaf(m4[t], pv[b], a32[t][b]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[t][b] = static_cast<double>(a32[t][b]);
+  }
+  // lanes sharing qd (lane bits 2..4) -> warp sums -> CTA partial in warp order
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      double s = acc[t][b];
+      for (int o = kEfQ; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      acc[t][b] = s;
+    }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane < kEfQ) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b) wred[(warp * kEfCols + 4 * lane + t) * R + b] = acc[t][b];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kEfCols * R; e += kEfThreads) {
+    double s = 0.0;
+    for (int wp = 0; wp < kEfThreads / 32; ++wp) s += wred[wp * kEfCols * R + e];
+    qp[e] = s;
+  }
+  cl.sync();
+  // Q_w strip: the cluster's partials summed in rank order (identical in every CTA)
+  for (int e = threadIdx.x; e < kEfCols * R; e += kEfThreads) {
+    double s = 0.0;
+    for (int k = 0; k < kEfCta; ++k) s += cl.map_shared_rank(qp, k)[e];
+    qf[e] = static_cast<float>(s);
+    if (crank == 0 && col0 + e / R < cols) qw[(static_cast<int64_t>(v) * cols + col0) * R + e] = qf[e];
+  }
+  cl.sync();   // no CTA leaves while a peer may still read its partial
+  if (!colok) return;
+  float qv[4][R];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) qv[t][b] = qf[(4 * qd + t) * R + b];
+  // r = c - P_hat Q_w^T in fp32 FMAs (the decode's formula), c from shared memory
+  for (int a = rg; a < nr; a += kSweep) {
+    const int64_t i = (r0 + a) * cols + col;
+    if (i >= d) break;
+    const float4 m = ms[a * kEfQ + qd];
+    const float *pr = ph + (r0 + a) * R;
+    float pa[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) pa[b] = __ldg(pr + b);
+    float o4[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      float x = pa[0] * qv[t][0];
+#pragma unroll
+      for (int b = 1; b < R; ++b) x = fmaf(pa[b], qv[t][b], x);
+      o4[t] = x;
+    }
+    const float4 out = make_float4(m.x - o4[0], m.y - o4[1], m.z - o4[2], m.w - o4[3]);
+    if (i + 3 < d) {
+      __stcs(reinterpret_cast<float4 *>(cw + i), out);
+    } else {
+      const float o[4] = {out.x, out.y, out.z, out.w};
+      for (int t = 0; t < 4; ++t)
+        if (i + t < d) cw[i + t] = o[t];
+    }
+  }
+}
 
 // Gram matrix Q^T Q (fp64) for the rank check of ensure_full_rank (compressors.py:595-603).
 __global__ void __launch_bounds__(256) gram_kernel(int64_t cols, int R, const float *q, double *gram) {
@@ -646,6 +795,57 @@ int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, i
   mtp_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(
       L, splits, cols, rank, partial, q);
   GC_LAUNCH_CHECK("mtp_reduce_kernel");
+  return GC_OK;
+}
+
+int gc_psgd_mtp_ef_supported(int64_t rows, int64_t cols, int32_t rank, int32_t rows_aligned) {
+  return rows_aligned && cols % 4 == 0 && rank >= 1 && rank <= 8 && rows >= kEfCta &&
+         (rows + kEfCta - 1) / kEfCta <= kEfSmemRows;
+}
+
+// Q_w = M_w^T P_hat and r_w = c_w - P_hat Q_w^T in one pass over M (c held in resid).
+int gc_psgd_mtp_ef(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, float *resid,
+                   const float *p_hat, float *q, void *stream) {
+  if (int rc = check_batch(b)) return rc;
+  GC_REQUIRE(d >= 1 && rows * cols >= d && resid && p_hat && q, "invalid argument");
+  if (!gc_psgd_mtp_ef_supported(rows, cols, rank, b->rows_aligned) || (reinterpret_cast<uintptr_t>(resid) & 15)) {
+    gc_set_error("gc_psgd_mtp_ef: shape not supported (see gc_psgd_mtp_ef_supported)");
+    return GC_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int L = b->tensors * b->workers;
+  const int64_t per = (rows + kEfCta - 1) / kEfCta;
+  const int64_t strips = (cols + kEfCols - 1) / kEfCols;
+  GC_REQUIRE(strips * kEfCta < (int64_t{1} << 31) && L <= 65535, "invalid argument");
+  cudaError_t err = cudaSuccess;
+  GC_RANK_SWITCH(rank, ({
+    const size_t smem = kEfCols * R * (8 + 64 + 4) + static_cast<size_t>(per) * kEfCols * 4;
+    static bool attr_done = false;
+    if (!attr_done) {
+      cudaFuncSetAttribute(mtp_ef_kernel<R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(mtp_ef_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kEfCols * R * 76 + kEfSmemRows * kEfCols * 4));
+      attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(strips * kEfCta), static_cast<unsigned>(L), 1);
+    cfg.blockDim = dim3(kEfThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kEfCta;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    err = cudaLaunchKernelEx(&cfg, mtp_ef_kernel<R>, d, rows, cols, resid, rows_of(b), p_hat, q, per);
+  }));
+  if (err != cudaSuccess) {
+    gc_set_error(std::string("mtp_ef_kernel launch: ") + cudaGetErrorString(err));
+    return GC_ERR_CUDA;
+  }
+  GC_LAUNCH_CHECK("mtp_ef_kernel");
   return GC_OK;
 }
 

@@ -565,6 +565,14 @@ class PowerSgdGroup:
         (pipelines.py:341-346, compressors.py:591-603)."""
         return seed_q_groups([self], round_index)[0]
 
+    def _mtp_ef_ok(self):
+        # opt-in (GC_PSGD_MTP_EF=1): the fused pass moves exactly the algorithmic bytes but its
+        # 128-byte column-strip segments run at ~1.7 TB/s, slower than mtp + decode (DESIGN.md)
+        if getattr(self, "_mtp_ef_cache", None) is None:
+            self._mtp_ef_cache = os.environ.get("GC_PSGD_MTP_EF", "0") == "1"
+        return self._mtp_ef_cache and bool(
+            _native.lib().gc_psgd_mtp_ef_supported(self.rows, self.cols, self.rank, self.batch.rows_aligned))
+
     def run(self, c_ptr: int, resid_ptr, est_ptr: int, round_index: int, grads_ptr=None, vec=False, fold=None,
             before_ef=None, q=None, ef_resid_ptr=None):
         """One round for the batch.  c_ptr: corrected matrices (or raw gradients when grads_ptr is
@@ -600,8 +608,14 @@ class PowerSgdGroup:
         _native.call("gc_psgd_orthonormalize", T, rows, r, p_sum.data_ptr(), p_hat.data_ptr(), self.mgs_ws.data_ptr(),
                      status.data_ptr(), sp)
         qw = self._buf("qw", (T * L, cols, r))
-        _native.call("gc_psgd_mtp", bref, d, rows, cols, r, c_ptr, p_hat.data_ptr(), qw.data_ptr(),
-                     self.ws.data_ptr(), sp)
+        # Q_w and the EF update in one pass over M when nothing reads the corrected matrices
+        # between them (no nmse hook; corrected held in resid); the estimate stays in decode
+        mtp_ef = before_ef is None and resid_ptr is not None and c_ptr == resid_ptr and self._mtp_ef_ok()
+        if mtp_ef:
+            _native.call("gc_psgd_mtp_ef", bref, d, rows, cols, r, resid_ptr, p_hat.data_ptr(), qw.data_ptr(), sp)
+        else:
+            _native.call("gc_psgd_mtp", bref, d, rows, cols, r, c_ptr, p_hat.data_ptr(), qw.data_ptr(),
+                         self.ws.data_ptr(), sp)
         q_sum = fold("right-factor", qw, cols * r).reshape(T, cols, r)
         # warm Q (pipelines.py:366) before the decode, and its Gram copied to pinned host memory
         # behind an event: the next round's rank check (ensure_full_rank) then reads it without
@@ -616,7 +630,10 @@ class PowerSgdGroup:
             ev = torch.cuda.Event()
             ev.record()
             self._pending_gram = (warm, ev)
-        if before_ef is None and resid_ptr is not None:   # EF update and estimate in one pass
+        if mtp_ef:
+            _native.call("gc_psgd_decode", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
+                         q_sum.data_ptr(), None, est_ptr, sp)
+        elif before_ef is None and resid_ptr is not None:   # EF update and estimate in one pass
             _native.call("gc_psgd_decode_fused", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
                          q_sum.data_ptr(), resid_ptr, est_ptr, sp)
         else:

@@ -81,6 +81,33 @@ def test_psgd_vs_oracle_multi_round(n, d, rank):
         assert_close_fp32(np.stack(pipe.residuals), np.stack(outs[r]["residuals"]), f"round {r} residuals")
 
 
+@pytest.mark.parametrize("n,d,rank", [(4, 1_000_000, 4), (3, 999_997, 8), (2, 350_001, 1), (8, 4096, 2),
+                                      (2, 50_000, 16), (3, 100_003, 3)])
+def test_psgd_mtp_ef_vs_oracle(n, d, rank):
+    """Without the nmse hook Q_w and the EF update run fused (gc_psgd_mtp_ef) where the shape allows:
+    estimate, residuals and warm Q against the oracle over rounds, and against the unfused kernels."""
+    import paper_2407_01378_b200 as gcb
+    seeds = gcb.SeedSpec(37)
+    grads = [[seeds.rng("grad-worker", r, w).standard_normal(d).astype(np.float32) for w in range(n)]
+             for r in range(3)]
+    outs = oracle_rounds("powersgd", dict(rank=rank), grads, 37)
+    pipe = gcb.make_pipeline(gcb.PowerSgdConfig(rank), n, d, seeds, compute_nmse=False)
+    ref = gcb.make_pipeline(gcb.PowerSgdConfig(rank), n, d, seeds, compute_nmse=False)
+    for r in range(3):
+        if r == 0:
+            pipe._engine.group._mtp_ef_cache = True    # opt-in path under test
+            ref._engine.group._mtp_ef_cache = False
+        res = pipe.run_round(grads[r], r)
+        alt = ref.run_round(grads[r], r)
+        assert_close_fp32(res.estimate.logical, outs[r]["estimate"], f"round {r}")
+        assert_close_fp32(np.stack(pipe.residuals), np.stack(outs[r]["residuals"]), f"round {r} residuals")
+        assert_close_fp32(res.estimate.logical, alt.estimate.logical, f"round {r} vs unfused")
+        assert_close_fp32(np.stack(pipe.residuals), np.stack(ref.residuals), f"round {r} residuals vs unfused")
+    grp = pipe._engine.group
+    if grp.rank <= 8 and grp.rows >= 16 and grp.cols % 4 == 0 and grp.batch.rows_aligned:
+        assert grp._mtp_ef_ok()
+
+
 def test_psgd_zero_gradients_complete_basis_and_redraw():
     """All-zero gradients: MGS completes with canonical vectors; round 1's warm Q is zero and is redrawn."""
     import paper_2407_01378_b200 as gcb
