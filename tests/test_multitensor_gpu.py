@@ -17,9 +17,11 @@ def _grads(n, D, rounds, seed):
     return [[rng.standard_normal(D).astype(np.float32) for _ in range(n)] for _ in range(rounds)]
 
 
-@pytest.mark.parametrize("nmse", [True, False])   # False: ef_apply fused into the first pass of each tensor
+@pytest.mark.parametrize("nmse,mtp_ef", [(True, False), (False, False), (False, True)])
 @pytest.mark.parametrize("rank,warm", [(4, True), (2, False), (1, True)])
-def test_powersgd_per_tensor_matches_reference(rank, warm, nmse):
+def test_powersgd_per_tensor_matches_reference(rank, warm, nmse, mtp_ef):
+    """nmse False: ef_apply fused into the first pass of each tensor; mtp_ef: Q_w and the EF update
+    in one pass (gc_psgd_mtp_ef, opt-in) for the batched groups whose shapes allow it."""
     import paper_2407_01378_b200 as gcb
     from paper_2407_01378_b200.multitensor import TensorListPipeline
     n, seed = 3, 51
@@ -27,6 +29,9 @@ def test_powersgd_per_tensor_matches_reference(rank, warm, nmse):
     offs = np.concatenate([[0], np.cumsum(SIZES)[:-1]])
     grads = _grads(n, D, 3, seed)
     pipe = TensorListPipeline(gcb.PowerSgdConfig(rank, warm), n, SIZES, gcb.SeedSpec(seed), compute_nmse=nmse)
+    if mtp_ef:
+        for grp in pipe.groups:
+            grp._mtp_ef_cache = True
     results = [pipe.run_round(grads[r], r) for r in range(3)]
     for t, (off, s) in enumerate(zip(offs, SIZES)):
         outs = oracle_rounds("powersgd", dict(rank=rank, warm_start=warm),
@@ -41,6 +46,8 @@ def test_powersgd_per_tensor_matches_reference(rank, warm, nmse):
         assert np.max(np.abs(res_got - res_ref)) <= 1e-5 * max(np.max(np.abs(res_ref)), 1e-30), t
         if s >= 4096 and warm:
             assert np.max(np.abs(pipe.warm_q(t) - outs[2]["warm_q"])) <= 1e-5 * np.max(np.abs(outs[2]["warm_q"]))
+    if mtp_ef:   # the fused pass ran for the aligned groups (64 x 64 batch of three, 100 x 100)
+        assert sum(bool(grp._mtp_ef_ok()) for grp in pipe.groups) >= 2
 
 
 def test_topk_per_tensor_bit_exact():
