@@ -52,3 +52,74 @@ def test_ddp_hook_matches_reference_round(scheme):
         assert np.array_equal(log0[s][1], log1[s][1])                    # same estimate on both ranks
         assert np.array_equal(log0[s][1], outs[s]["estimate"]), s        # = the reference round
         assert np.array_equal(log0[s][2], np.sort(outs[s]["estimate"]))  # and DDP applied it
+
+
+class _FakeBucket:
+    """GradBucket stand-in: index(), buffer() (the parameters' gradients packed in order), parameters()."""
+
+    def __init__(self, index, params, grads):
+        import torch
+        self._i, self._p = index, params
+        self._buf = torch.cat([g.reshape(-1) for g in grads]).cuda()
+
+    def index(self):
+        return self._i
+
+    def buffer(self):
+        return self._buf
+
+    def parameters(self):
+        return self._p
+
+
+def _rebuild(rank, world, nonfinite):
+    import torch
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.ddp import CompressionHookState, compression_hook
+    torch.cuda.set_device(0)
+    sizes = [3000, 1000, 2000]
+    params = [torch.nn.Parameter(torch.zeros(s)) for s in sizes]
+    state = CompressionHookState(gcb.RotatedQuantConfig(4, 8, 256), gcb.SeedSpec(9))
+    rng = np.random.default_rng(10 + rank)
+    layouts = [[[0, 1], [2]], [[0], [1, 2]], [[0], [1, 2]]]    # DDP's rebuild after step 0
+    inputs, outs = [], []
+    for step, layout in enumerate(layouts):
+        g = [rng.standard_normal(s).astype(np.float32) for s in sizes]
+        if nonfinite and step == 1 and rank == 1:
+            g[2][5] = np.inf
+        inputs.append(g)
+        est = []
+        for bi, ids in enumerate(layout):
+            b = _FakeBucket(bi, [params[i] for i in ids], [torch.from_numpy(g[i]) for i in ids])
+            est.append(compression_hook(state, b).value().cpu().numpy())
+        outs.append(est)
+    return inputs, outs, state.skipped_rounds
+
+
+@pytest.mark.parametrize("nonfinite", [False, True])
+def test_ddp_bucket_rebuild_carries_residuals(nonfinite):
+    """Buckets are re-laid out after step 0: every parameter keeps its own EF residual, so each
+    bucket's round equals the reference round started from the residuals its parameters carried.
+    A non-finite bucket yields NaN on every rank and leaves every residual untouched."""
+    from oracle import gradcomp_oracle as orc
+    (in0, out0, sk0), (in1, out1, sk1) = run_world(_rebuild, 2, (nonfinite,))
+    sizes = [3000, 1000, 2000]
+    layouts = [[[0, 1], [2]], [[0], [1, 2]], [[0], [1, 2]]]
+    params = dict(quant_bits=4, wire_bits=8, rotation_block=256)
+    resid = [[np.zeros(s, np.float32) for s in sizes] for _ in range(2)]   # [rank][param]
+    for step, layout in enumerate(layouts):
+        for bi, ids in enumerate(layout):
+            got0, got1 = out0[step][bi], out1[step][bi]
+            if nonfinite and step == 1:
+                assert np.isnan(got0).all() and np.isnan(got1).all()
+                continue
+            grads = [np.concatenate([inp[step][i] for i in ids]) for inp in (in0, in1)]
+            st = orc.OracleState([np.concatenate([resid[w][i] for i in ids]) for w in range(2)])
+            ref = orc.run_round("rotated_quant", params, st, grads, 9, step)
+            assert np.array_equal(got0, ref["estimate"]) and np.array_equal(got1, ref["estimate"]), (step, bi)
+            for w in range(2):
+                o = 0
+                for i in ids:
+                    resid[w][i] = st.residuals[w][o:o + sizes[i]].copy()
+                    o += sizes[i]
+    assert sk0 == sk1 == ([1] if nonfinite else [])
