@@ -164,6 +164,13 @@ int gc_segment_ef_fold(int32_t n, int32_t nseg, const int64_t *seg_off, const in
                        const float *grads, float *resid, int64_t ld, float *estimate, void *stream);
 /* out = in / divisor (f32, may alias). */
 int gc_scale_div(int64_t len, const float *in, int32_t divisor, float *out, void *stream);
+/* FP16 bar across ranks (pipelines.py:370-393 with NCCL's half sum standing in for the ring):
+ * gc_fold_to_half folds this rank's L rows [L][ld] with fp16 inputs and fp16 wire per hop into
+ * binary16 (out_half: uint16 [len]); after the NCCL half all-reduce, gc_half_mean_sat maps the
+ * sums back to f32 / divisor, saturating partial sums that overflowed to +-inf to +-65504 as the
+ * reference's fp16 wire does (vectors.py:136-152). */
+int gc_fold_to_half(int32_t L, int64_t len, const float *inputs, int64_t ld, void *out_half, void *stream);
+int gc_half_mean_sat(int64_t len, const void *in_half, int32_t divisor, float *out, void *stream);
 /* out = fp16_round_trip(in) (vectors.py:136-152; may alias). */
 int gc_fp16_round(int64_t len, const float *in, float *out, void *stream);
 

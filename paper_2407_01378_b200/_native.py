@@ -90,6 +90,8 @@ SIGNATURES = {
     "gc_segment_ef_fold": (c_int, [I32, I32, P, P, P, P, I64, P, P]),
     "gc_scale_div": (c_int, [I64, P, I32, P, P]),
     "gc_fp16_round": (c_int, [I64, P, P, P]),
+    "gc_fold_to_half": (c_int, [I32, I64, P, I64, P, P]),
+    "gc_half_mean_sat": (c_int, [I64, P, I32, P, P]),
     # TopK
     "gc_topk_workspace_bytes": (c_int64, [I32, I64]),
     "gc_topk_select": (c_int, [I32, I64, P, I64, I64, P, P, P, P, I32, P, P]),

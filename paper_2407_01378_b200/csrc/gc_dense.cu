@@ -9,6 +9,7 @@
 //  * divisor > 0: the folded value is divided by it in f32 (estimate = summed / n).
 // One thread per element reads the n worker rows coalesced: HBM traffic = 4n + 4 bytes per
 // element, the bound for this op.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "gc_device.cuh"
@@ -156,6 +157,46 @@ __global__ void fp16_round_kernel(int64_t len, const float *in, float *out) {
     out[e] = gc::fp16_round_trip(in[e]);
 }
 
+
+// FP16 bar across ranks, the local half: fold this rank's L rows with fp16 inputs and wire
+// (as float_fold_kernel<true, true>) and emit the binary16 bits the NCCL half all-reduce sends.
+__global__ void __launch_bounds__(kNT) fold_to_half_kernel(int L, int64_t len, const float *in, int64_t ld,
+                                                           __half *out) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; 2 * e < len;
+       e += static_cast<int64_t>(gridDim.x) * kNT) {
+    float acc[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t i = 2 * e + c;
+      float a = 0.0f;
+      if (i < len) {
+        a = gc::fp16_round_trip(in[i]);
+        for (int w = 1; w < L; ++w) a = gc::fp16_round_trip(gc::fp16_round_trip(a) + gc::fp16_round_trip(in[w * ld + i]));
+      }
+      acc[c] = a;
+    }
+    if (2 * e + 1 < len && (reinterpret_cast<uintptr_t>(out) & 3) == 0)
+      *reinterpret_cast<__half2 *>(out + 2 * e) = __floats2half2_rn(acc[0], acc[1]);
+    else {
+      out[2 * e] = __float2half_rn(acc[0]);
+      if (2 * e + 1 < len) out[2 * e + 1] = __float2half_rn(acc[1]);
+    }
+  }
+}
+
+// ... and the other half: the all-reduced binary16 sums -> f32 estimate = sum / n, with the
+// fp16 wire's +-65504 saturation (vectors.py:136-152) applied to partial sums that overflowed
+// to +-inf inside NCCL's half adds.
+__global__ void __launch_bounds__(kNT) half_mean_kernel(int64_t len, const __half *in, int divisor, float *out) {
+  const gc::DivN dv(divisor);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(kNT) + threadIdx.x; e < len;
+       e += static_cast<int64_t>(gridDim.x) * kNT) {
+    float x = __half2float(in[e]);
+    if (isinf(x)) x = copysignf(65504.0f, x);
+    out[e] = dv(x);
+  }
+}
+
 int grid_for(int64_t work) {
   int64_t g = (work + kNT - 1) / kNT;
   if (g > 148 * 16) g = 148 * 16;
@@ -247,6 +288,24 @@ int gc_fp16_round(int64_t len, const float *in, float *out, void *stream) {
   if (len == 0) return GC_OK;
   fp16_round_kernel<<<grid_for(len), kNT, 0, static_cast<cudaStream_t>(stream)>>>(len, in, out);
   GC_LAUNCH_CHECK("fp16_round_kernel");
+  return GC_OK;
+}
+
+int gc_fold_to_half(int32_t L, int64_t len, const float *inputs, int64_t ld, void *out_half, void *stream) {
+  GC_REQUIRE(L >= 1 && len >= 0 && ld >= len && inputs && out_half, "invalid argument");
+  if (len == 0) return GC_OK;
+  fold_to_half_kernel<<<grid_for((len + 1) / 2), kNT, 0, static_cast<cudaStream_t>(stream)>>>(
+      L, len, inputs, ld, static_cast<__half *>(out_half));
+  GC_LAUNCH_CHECK("fold_to_half_kernel");
+  return GC_OK;
+}
+
+int gc_half_mean_sat(int64_t len, const void *in_half, int32_t divisor, float *out, void *stream) {
+  GC_REQUIRE(len >= 0 && divisor >= 1 && in_half && out, "invalid argument");
+  if (len == 0) return GC_OK;
+  half_mean_kernel<<<grid_for(len), kNT, 0, static_cast<cudaStream_t>(stream)>>>(
+      len, static_cast<const __half *>(in_half), divisor, out);
+  GC_LAUNCH_CHECK("half_mean_kernel");
   return GC_OK;
 }
 

@@ -175,6 +175,8 @@ class DistributedGradientPipeline:
 
     def __init__(self, config, num_workers: int, dim: int, seeds: SeedSpec, error_feedback: bool | None = None, *,
                  group=None, device=None, validate: bool = True, compute_nmse: bool = False):
+        """compute_nmse=True fills RoundResult.nmse as the reference does (an fp64 all-reduce of the
+        corrected gradients per round); off by default, in which case nmse is NaN."""
         if num_workers < 1:
             raise ValueError("num_workers must be positive")
         if dim < 1:
@@ -231,10 +233,29 @@ class DistributedGradientPipeline:
         g = self._checked(local_grads)
         ledger = TrafficLedger()
         self.comm.sent = {}
+        ref = self._nmse_reference(g) if self.compute_nmse else None
         est, bits, stats = self._engine.run(g, self._res, round_index, ledger, self.compute_nmse)
+        if ref is not None:
+            stats = _NmseStats(stats, self._nmse_acc(est, ref))
         res = RoundResult(self.scheme, round_index, est, self.dim, ledger, bits, stats)
         res.wire_bytes = dict(self.comm.sent)   # bytes this rank sent per ledger phase
         return res
+
+    def _nmse_reference(self, g) -> torch.Tensor:
+        """The reference's nmse target (pipelines.py:176-181): the fp64 mean of every worker's
+        corrected gradient, summed over the ranks (an fp64 all-reduce of d values: the opt-in
+        diagnostic's cost).  Taken before the round overwrites the residuals."""
+        c = g.double()
+        if self._res is not None:
+            c += self._res.double()
+        total = c.sum(0)
+        self.comm.all_reduce(total, dist.ReduceOp.SUM)
+        return total / self.group.size
+
+    def _nmse_acc(self, est, ref) -> torch.Tensor:
+        """[sum (est - ref)^2, sum ref^2] in fp64 (metrics.py:32-37)."""
+        e = est.double() - ref
+        return torch.stack([torch.dot(e, e), torch.dot(ref, ref)])
 
     def _checked(self, local_grads) -> torch.Tensor:
         L, d = self.L, self.dim
@@ -268,6 +289,24 @@ class DistributedGradientPipeline:
         if self._stage is None:
             self._stage = torch.empty(self.L, self.dim, dtype=torch.float32, device=self.device)
         return self._stage
+
+
+class _NmseStats:
+    """An engine's RoundStats with the nmse taken from the distributed fp64 accumulators."""
+
+    def __init__(self, stats, acc):
+        self._s, self._acc, self._nmse = stats, acc, None
+
+    def nmse(self) -> float:
+        if self._nmse is None:
+            self._nmse = nmse_from(self._acc.cpu().tolist())
+        return self._nmse
+
+    def overflow(self):
+        return self._s.overflow()
+
+    def range_clips(self) -> int:
+        return self._s.range_clips()
 
 
 # ======================================================================================
@@ -499,22 +538,25 @@ class _Dense(_Base):
     def __init__(self, cfg: DenseConfig, pipe):
         super().__init__(pipe)
         self.bits = cfg.bits
+        self._wire = None
 
     def run(self, g, res, r, ledger, nmse):
         L, n, d = self.L, self.n, self.dim
         sp = _sp()
-        local = torch.empty(d, dtype=torch.float32, device=self.dev)
-        w16 = 1 if self.bits == 16 else 0
-        # local workers first (fp16 inputs and wire for the FP16 bar), then the NCCL sum
-        _native.call("gc_float_fold", L, d, g.data_ptr(), g.stride(0), 0, d, w16, w16, 0, local.data_ptr(), sp)
-        if self.bits == 16:
-            wire = local.half()
-            self.comm.all_reduce(wire, dist.ReduceOp.SUM, "dense")
-            total = wire.float()
-        else:
-            total = self.comm.all_reduce(local, dist.ReduceOp.SUM, "dense")
         est = torch.empty(d, dtype=torch.float32, device=self.dev)
-        _native.call("gc_scale_div", d, total.data_ptr(), n, est.data_ptr(), sp)
+        if self.bits == 16:
+            # local workers folded with fp16 inputs / wire straight into binary16, NCCL half sum,
+            # then f32 mean with the fp16 wire's +-65504 saturation (no eager casts)
+            if self._wire is None:
+                self._wire = torch.empty(d, dtype=torch.float16, device=self.dev)
+            _native.call("gc_fold_to_half", L, d, g.data_ptr(), g.stride(0), self._wire.data_ptr(), sp)
+            self.comm.all_reduce(self._wire, dist.ReduceOp.SUM, "dense")
+            _native.call("gc_half_mean_sat", d, self._wire.data_ptr(), n, est.data_ptr(), sp)
+        else:
+            local = torch.empty(d, dtype=torch.float32, device=self.dev)
+            _native.call("gc_float_fold", L, d, g.data_ptr(), g.stride(0), 0, d, 0, 0, 0, local.data_ptr(), sp)
+            total = self.comm.all_reduce(local, dist.ReduceOp.SUM, "dense")
+            _native.call("gc_scale_div", d, total.data_ptr(), n, est.data_ptr(), sp)
         self.launches += 2
         ledger.charge_ring("dense", n, d, self.bits)
         return est, float(self.bits) * d, _simple_stats(None)

@@ -163,6 +163,13 @@ class TensorListPipeline:
         acc = torch.zeros(2, dtype=torch.float64, device=self.device) if self.compute_nmse else None
         if not self.batched:
             bits = 0.0
+            ref = None
+            if acc is not None:   # nmse target: fp64 mean of the corrected vectors, before EF updates
+                c = g.double()
+                if self._res is not None:
+                    c += self._res.double()
+                ref = c.mean(0)
+                del c
             for t, eng in enumerate(self.engines):
                 off, s = int(self.offsets[t]), self.sizes[t]
                 gv = g[:, off:off + s]
@@ -171,7 +178,10 @@ class TensorListPipeline:
                 est[off:off + s].copy_(e)
                 bits += b
             self.launches += sum(e.launches for e in self.engines)
-            return RoundResult(self.scheme, round_index, est, D, ledger, bits, _simple_stats(None))
+            if ref is not None:
+                e = est.double() - ref
+                acc = torch.stack([torch.dot(e, e), torch.dot(ref, ref)])
+            return RoundResult(self.scheme, round_index, est, D, ledger, bits, _simple_stats(acc))
 
         sp = _sp()
         res = self._res

@@ -102,3 +102,49 @@ def test_wire_bytes_match_reference_ledger(scheme, params):
         assert set(wire) == set(led), (wire, led)
         for ph, bits in led.items():
             assert wire[ph] * 8 == bits, (scheme, ph, wire[ph] * 8, bits)
+
+
+def _nmse_rank(rank, world, scheme, params):
+    import torch
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.distributed import DistributedGradientPipeline
+    from tests.gpu_util import config_for
+    torch.cuda.set_device(0)
+    L = N // world
+    ef = None if scheme != "dense" else False
+    pipe = DistributedGradientPipeline(config_for(scheme, params), N, D, gcb.SeedSpec(SEED), ef, compute_nmse=True)
+    return [pipe.run_round(_grads(r)[rank * L:(rank + 1) * L], r).nmse for r in range(2)]
+
+
+@pytest.mark.parametrize("scheme,params", [
+    ("rotated_quant", dict(quant_bits=4, wire_bits=8, rotation_block=1024)),
+    ("topk", dict(k=1000)),
+    ("dense", dict(bits=16)),
+])
+def test_distributed_nmse_matches_reference(scheme, params):
+    """compute_nmse=True: RoundResult.nmse against the fp64 mean of every worker's corrected
+    gradient (pipelines.py:176-181), identical on both ranks."""
+    out = run_world(_nmse_rank, 2, (scheme, params))
+    ref = oracle_rounds(scheme, params, [_grads(r) for r in range(2)], SEED, ef=scheme != "dense")
+    for r in range(2):
+        assert out[0][r] == out[1][r]
+        assert abs(out[0][r] - ref[r]["nmse"]) <= 1e-9 + 1e-6 * abs(ref[r]["nmse"]), (r, out[0][r], ref[r]["nmse"])
+
+
+def _fp16_sat_rank(rank, world):
+    import torch
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.distributed import DistributedGradientPipeline
+    torch.cuda.set_device(0)
+    pipe = DistributedGradientPipeline(gcb.DenseConfig(16), world, 8, gcb.SeedSpec(1), False)
+    g = np.array([40000, -40000, 60000, 1.5, -70000, 30000, 1e-3, 65504], np.float32)
+    return pipe.run_round([g], 0).estimate.logical.copy()
+
+
+def test_fp16_bar_saturates_like_the_reference_wire():
+    """Partial sums past 65504 saturate (vectors.py:136-152) instead of becoming inf."""
+    out = run_world(_fp16_sat_rank, 2)
+    g = np.array([40000, -40000, 60000, 1.5, -70000, 30000, 1e-3, 65504], np.float32)
+    ref = oracle_rounds("dense", dict(bits=16), [[g, g]], 1, ef=False)[0]["estimate"]
+    assert np.all(np.isfinite(out[0])) and np.array_equal(out[0], out[1])
+    assert np.array_equal(out[0], ref), (out[0], ref)

@@ -65,6 +65,18 @@ def test_topk_per_tensor_bit_exact():
         for r in range(2):
             assert np.array_equal(results[r].estimate.logical[off:off + s], outs[r]["estimate"])
         assert np.array_equal(np.stack(pipe.residuals)[:, off:off + s], np.stack(outs[1]["residuals"]))
+    # nmse of the flat vector against the fp64 mean of the corrected gradients (pipelines.py:176-181)
+    res0 = np.zeros((n, D), np.float32)
+    for r in range(2):
+        corrected = np.stack(grads[r]) + res0
+        ref = corrected.astype(np.float64).mean(axis=0)
+        est = results[r].estimate.logical.astype(np.float64)
+        want = np.sum((est - ref) ** 2) / np.sum(ref ** 2)
+        assert abs(results[r].nmse - want) <= 1e-9 * want, (r, results[r].nmse, want)
+        if r == 0:
+            res0 = np.stack([np.concatenate([oracle_rounds("topk", dict(k=50), [[g[o:o + s] for g in grads[0]]],
+                                                           seed)[0]["residuals"][w] for o, s in zip(offs, sizes)])
+                             for w in range(n)])
 
 
 def test_gpt2_medium_layout():
