@@ -63,6 +63,9 @@ class Comm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.stage = dist.get_backend(group) != "nccl"
+        # a one-rank gloo group needs no transport; a one-rank NCCL group still issues every
+        # collective (local copies), so the per-rank NCCL path runs as it does at N ranks
+        self.local_only = self.world == 1 and self.stage
         self.sent: dict[str, int] = {}
 
     def _count(self, phase, nbytes):
@@ -85,7 +88,7 @@ class Comm:
         x = x.contiguous()
         self._count(phase, (self.world - 1) * x.numel() * x.element_size())
         out = torch.empty((self.world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
-        if self.world == 1:
+        if self.local_only:
             out.copy_(x)
             return out
         self._run(lambda o, i: dist.all_gather_into_tensor(o, i, group=self.group),
@@ -97,7 +100,7 @@ class Comm:
         send = send.contiguous()
         self._count(phase, (self.world - 1) * (send.numel() // self.world) * send.element_size())
         recv = torch.empty_like(send)
-        if self.world == 1:
+        if self.local_only:
             recv.copy_(send)
             return recv
         self._run(lambda o, i: dist.all_to_all_single(o, i, group=self.group),
@@ -106,7 +109,7 @@ class Comm:
 
     def all_reduce(self, t: torch.Tensor, op, phase: str | None = None) -> torch.Tensor:
         self._count(phase, 2 * (self.world - 1) * t.numel() * t.element_size() // self.world)
-        if self.world == 1:
+        if self.local_only:
             return t
         if self.stage and t.is_cuda:
             h = t.cpu()

@@ -15,11 +15,16 @@ def _free_port():
     return port
 
 
-def _entry(rank, world, port, fn, args, outdir):
+def _entry(rank, world, port, fn, args, outdir, backend="gloo"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        import torch
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    else:
+        dist.init_process_group(backend, rank=rank, world_size=world)
     try:
         out = fn(rank, world, *args)
     finally:
@@ -28,10 +33,11 @@ def _entry(rank, world, port, fn, args, outdir):
         pickle.dump(out, f)
 
 
-def run_world(fn, world=2, args=()):
-    """Run fn(rank, world, *args) in `world` gloo processes; return the per-rank results."""
+def run_world(fn, world=2, args=(), backend="gloo"):
+    """Run fn(rank, world, *args) in `world` processes (gloo, or nccl with one GPU per rank);
+    return the per-rank results."""
     outdir = tempfile.mkdtemp()
-    mp.spawn(_entry, args=(world, _free_port(), fn, args, outdir), nprocs=world, join=True)
+    mp.spawn(_entry, args=(world, _free_port(), fn, args, outdir, backend), nprocs=world, join=True)
     res = []
     for r in range(world):
         with open(os.path.join(outdir, f"rank{r}.pkl"), "rb") as f:

@@ -168,10 +168,24 @@ def payload_vectors():
     print("payloads ok")
 
 
+def synthetic_vectors():
+    """trainbench.synthetic_round (trainbench.py:31-113) at small sizes: pins oracle/synthetic.py."""
+    from gradcomp.trainbench import SyntheticGradSpec, synthetic_round
+    out, meta = {}, []
+    for i, (d, kw, seed, r, n) in enumerate([(1000, {}, 2024, 0, 3), (4099, dict(rho=0.0), 5, 2, 2),
+                                             (20000, dict(rho=0.5, spike_density=0.3, divergence=0.0), 9, 1, 2),
+                                             (30000, {}, 2024, 3, 4)]):
+        out[f"g_{i}"] = np.stack(synthetic_round(SyntheticGradSpec(dim=d, **kw), SeedSpec(seed), r, n))
+        meta.append({"d": d, "kw": kw, "seed": seed, "round": r, "n": n})
+    np.savez_compressed(os.path.join(OUT, "synthetic.npz"), meta=json.dumps(meta), **out)
+    print("synthetic ok")
+
+
 def main():
     gauss = lambda rng, d, w: rng.standard_normal(d).astype(np.float32)  # noqa: E731
     quart = lambda rng, d, w: quarters(rng, d)  # noqa: E731
     seed_vectors()
+    synthetic_vectors()
     chunk_norm_vectors()
     payload_vectors()
     thc_intermediates("thc_steps_a", 3, 3000, 1234, 0, 4, 4, 256)
