@@ -11,7 +11,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) $(EXTRA) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC) -Xptxas -v
 EXACT    := -fmad=false
 
-CU_EXACT := gc_thc.cu gc_thc_fused.cu gc_util.cu gc_dense.cu gc_topk.cu gc_chunk.cu
+CU_EXACT := gc_thc.cu gc_thc_fused.cu gc_thc_rank.cu gc_util.cu gc_dense.cu gc_topk.cu gc_chunk.cu
 CU_FAST  := gc_psgd.cu gc_psgd_umma.cu
 CPP      := gc_host.cpp
 

@@ -137,6 +137,38 @@ int gc_thc_decode_ef(const gc_thc_geom *g, int32_t workers, const int8_t *codes,
                      float *resid, int64_t ld, void *workspace, void *stream);
 
 
+/* Per-rank THC round of the distributed pipeline (one rank's L local workers), split at the
+ * reference round's two exchange points (pipelines.py:260-322).  Tiles are 1024 coordinates;
+ * [tile_begin, tile_end) restricts a call to a segment (tile_end < 0: to the end), so the host
+ * can run K1 of segment s+1 while segment s's range all-reduce is in flight and K2 of segment s
+ * re-reads g and r from L2.  Requires 32 <= B <= 1024, 1 <= L <= 16.
+ *
+ * K1 gc_thc_rank_ranges: corrected = f32(g + r), signs, fp64 WHT, per-block (min, max) stored as
+ *    (-lo, hi) pairs: neg_ranges [L][nb][2] (nb = active / B), ready for one MAX all-reduce
+ *    (ElemMin/ElemMax consensus, pipelines.py:271-288).  gc_thc_merge_ranges folds L tables.
+ * K2 gc_thc_rank_quant: with the consensus table shared_neg_ranges [nb][2] (-lo, hi): the same
+ *    rotation again, quantize_stochastic with worker l's coin stream coin_streams[l]
+ *    (compressors.py:456-498), codes written straight into the all-to-all send buffer
+ *    [W][L][slice] (slice a multiple of 1024; nibble != 0: packed nibbles, element 2i low, for
+ *    wire_bits <= 4), then own decode + ef_update: resid_out = corrected - inv_WHT(dq(z, 1))
+ *    (pipelines.py:312-318, 168-170; resid_in/out may alias; both NULL = EF off).
+ *    counters[1] += sum z, counters[2] += sum z^2.
+ * K3 gc_thc_rank_decode: estimate = f32(inv_WHT(f32(n mid + step z_sum)) * signs) / n
+ *    (dequantize_sum + rht_inverse + / n, pipelines.py:307-311) from the all-gathered saturated
+ *    sums (sum_bytes 1, 2 or 4; >= ceil(active/1024)*1024 entries, 16-byte aligned).
+ * All three reproduce the reference bit for bit (codes, sums, residuals, estimate). */
+int gc_thc_rank_ranges(const gc_thc_geom *g, int32_t L, const float *grads, const float *resid, int64_t ld,
+                       int64_t tile_begin, int64_t tile_end, const uint32_t *sign_bits, float *neg_ranges,
+                       void *stream);
+int gc_thc_merge_ranges(int32_t L, int64_t num_blocks, const float *neg_ranges_in, float *neg_ranges_out,
+                        void *stream);
+int gc_thc_rank_quant(const gc_thc_geom *g, int32_t L, const float *grads, const float *resid_in, float *resid_out,
+                      int64_t ld, int64_t tile_begin, int64_t tile_end, const uint32_t *sign_bits,
+                      const float *shared_neg_ranges, const gc_pcg64 *coin_streams, int8_t *send, int64_t slice,
+                      int32_t nibble, int64_t *counters, void *stream);
+int gc_thc_rank_decode(const gc_thc_geom *g, int32_t n, const void *sums, int32_t sum_bytes,
+                       const float *shared_neg_ranges, const uint32_t *sign_bits, float *estimate, void *stream);
+
 /* ---------------------------------------------------------------- float ring folds
  * FloatSum ring_all_reduce (collectives.py:112-120, 177-236) as an ordered fold per element:
  * element e (global index offset+e) starts at worker (offset+e)/ring_block and folds in ring

@@ -80,6 +80,11 @@ SIGNATURES = {
     "gc_sat_fold": (c_int, [I32, I64, P, I64, I64, I64, I32, P, P, P]),
     "gc_thc_decode_estimate": (c_int, [POINTER(ThcGeom), I32, P, I32, P, P, P, P, P]),
     "gc_thc_decode_ef": (c_int, [POINTER(ThcGeom), I32, P, P, P, P, P, I64, P, P]),
+    "gc_thc_rank_ranges": (c_int, [POINTER(ThcGeom), I32, P, P, I64, I64, I64, P, P, P]),
+    "gc_thc_merge_ranges": (c_int, [I32, I64, P, P, P]),
+    "gc_thc_rank_quant": (c_int, [POINTER(ThcGeom), I32, P, P, P, I64, I64, I64, P, P, POINTER(Pcg64), P, I64, I32,
+                                  P, P]),
+    "gc_thc_rank_decode": (c_int, [POINTER(ThcGeom), I32, P, I32, P, P, P, P]),
     "gc_thc_round_fused": (c_int, [POINTER(ThcGeom), I32, P, P, I64, P, POINTER(Pcg64), P, P, P, P, P]),
     "gc_thc_round_fused_range": (c_int, [POINTER(ThcGeom), I32, P, P, P, I64, I64, I64, P, POINTER(Pcg64), P, P, P,
                                           P, P]),

@@ -43,8 +43,9 @@ class CompressionHookState:
         self._seen: set[int] = set()
         self.last_results = {}
         self.skipped_rounds = []     # rounds whose bucket was non-finite (state untouched)
-        self.record = record        # keep each bucket's input (tests / debugging)
+        self.record = record        # keep each bucket's input and layout (tests / debugging)
         self.last_inputs = {}
+        self.last_layouts = {}
 
     @staticmethod
     def layout(bucket):
@@ -101,6 +102,7 @@ def compression_hook(state: CompressionHookState, bucket) -> torch.futures.Futur
         flat = buf.reshape(1, -1).to(torch.float32).contiguous()
         if state.record:
             state.last_inputs[idx] = flat.detach().clone()
+            state.last_layouts[idx] = state.layout(bucket)
         fut = torch.futures.Future()
         try:
             res = pipe.run_round(flat, state.round_index)

@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -107,6 +108,19 @@ class Comm:
                   recv.view(-1).view(torch.uint8), send.view(-1).view(torch.uint8))
         return recv
 
+    def all_reduce_async(self, t: torch.Tensor, op, phase: str | None = None):
+        """In-place all-reduce of a contiguous tensor; returns a work handle to wait() on before
+        the result is used (NCCL: the current stream waits), or None when already complete."""
+        self._count(phase, 2 * (self.world - 1) * t.numel() * t.element_size() // self.world)
+        if self.local_only or t.numel() == 0:
+            return None
+        if self.stage and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, op=op, group=self.group)
+            t.copy_(h)
+            return None
+        return dist.all_reduce(t, op=op, group=self.group, async_op=True)
+
     def all_reduce(self, t: torch.Tensor, op, phase: str | None = None) -> torch.Tensor:
         self._count(phase, 2 * (self.world - 1) * t.numel() * t.element_size() // self.world)
         if self.local_only:
@@ -120,7 +134,7 @@ class Comm:
         return t
 
 
-def fold_slices(active: int, world: int, align: int = 256):
+def fold_slices(active: int, world: int, align: int = 256) -> int:
     """Length of the equal per-rank slices of the code vector for the all-to-all fold."""
     s = -(-active // world)
     s = -(-s // align) * align
@@ -137,6 +151,25 @@ def _nibbles(x: torch.Tensor, pack: bool) -> torch.Tensor:
         out = torch.empty(x.shape[:-1] + (x.shape[-1] * 2,), dtype=torch.int8, device=x.device)
         _native.call("gc_unpack_nibbles", out.numel(), x.data_ptr(), out.data_ptr(), _sp())
     return out
+
+
+def exchange_sums(send: torch.Tensor, comm: Comm, n: int, active: int, slice_len: int, fold_fn, out_dtype,
+                  phase: str | None = None, nibble: bool = False) -> torch.Tensor:
+    """The code exchange for a send buffer already in the all-to-all layout [W][L][S] (int8, or
+    packed nibbles [W][L][S/2] when nibble): all-to-all, ordered saturating fold of this rank's
+    slice over the n worker rows, all-gather of the summed slices (collectives.py:215-235)."""
+    recv = comm.all_to_all(send, phase)
+    if nibble:
+        recv = _nibbles(recv, False)
+    recv = recv.reshape(n, slice_len)
+    s0 = comm.rank * slice_len
+    my_len = max(0, min(slice_len, active - s0))
+    sums = torch.zeros(slice_len, dtype=out_dtype, device=send.device)
+    if my_len:
+        fold_fn(recv, my_len, s0, sums)
+    if nibble:
+        return _nibbles(comm.all_gather_rows(_nibbles(sums.reshape(1, -1), True), phase), False).reshape(-1)
+    return comm.all_gather_rows(sums.reshape(1, -1), phase).reshape(-1)
 
 
 def exchange_fold(codes: torch.Tensor, comm: Comm, n: int, active: int, slice_len: int, fold_fn, out_dtype,
@@ -330,6 +363,21 @@ class _Base:
 
 
 class _Thc(_Base):
+    """RotatedQuantConfig round (pipelines.py:260-322) for this rank's L workers.
+
+    Rotation blocks 32..1024 (the paper's settings) run the fused per-rank kernels of
+    gc_thc_rank.cu over L2-sized segments of tiles:
+
+        K1(s)  ranges of segment s                       (reads g, r; they stay in L2)
+        AR(s)  NCCL MAX all-reduce of segment s's (-lo, hi) pairs, async -- K1(s+1) runs meanwhile
+        K2(s)  quantize + codes into the all-to-all send buffer + own decode + EF (g, r from L2)
+
+    then one all-to-all of the codes, the ring-ordered saturating fold of this rank's slice, one
+    all-gather of the sums and K3, the estimate decode.  Other block sizes use the generic
+    multi-kernel path (gc_thc_rotate / quantize / decode)."""
+
+    SEG_TILES = 4096   # tiles (of 1024 coordinates) per segment: L * 32 MB of g + r
+
     def __init__(self, cfg: RotatedQuantConfig, pipe):
         super().__init__(pipe)
         self.cfg = cfg
@@ -341,62 +389,86 @@ class _Thc(_Base):
         self.active = int(_native.lib().gc_thc_active_len(ctypes.byref(self.geom)))
         self.nb = self.active // B
         self.ring_blk = -(-P // self.n)
-        self.S = fold_slices(self.active, self.comm.world)
         self.sum_bytes = 1 if cfg.wire_bits <= 8 else (2 if cfg.wire_bits <= 16 else 4)
         self.sum_dtype = {1: torch.int8, 2: torch.int16, 4: torch.int32}[self.sum_bytes]
-        ws = int(_native.lib().gc_thc_workspace_bytes(ctypes.byref(self.geom), self.L))
-        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=self.dev) if ws else None
+        self.nibble = cfg.wire_bits <= 4
         L, W = self.L, self.comm.world
-        self.signs = torch.empty(-(-self.active // 32), dtype=torch.int32, device=self.dev)
-        self.x_rot = torch.empty(L, self.active, dtype=torch.float32, device=self.dev)
-        self.ranges = torch.empty(L, self.nb, 2, dtype=torch.float32, device=self.dev)
-        self.codes = torch.empty(L, self.active, dtype=torch.int8, device=self.dev)
-        self.send = torch.zeros(W, L, self.S, dtype=torch.int8, device=self.dev)
+        self.fused = P >= 1024 and 32 <= B <= 1024 and L <= 16
+        i32 = dict(dtype=torch.int32, device=self.dev)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=self.dev)
+        if self.fused:
+            self.tiles = -(-self.active // 1024)
+            self.S = fold_slices(self.active, W, align=1024)
+            self.signs = torch.empty(self.tiles * 32, **i32)
+            self.neg = torch.empty(L, self.nb, 2, dtype=torch.float32, device=self.dev)
+            self.shared = self.neg[0] if L == 1 else torch.empty(self.nb, 2, dtype=torch.float32, device=self.dev)
+            if self.nibble:
+                self.send = torch.zeros(W, L, self.S // 2, dtype=torch.uint8, device=self.dev)
+            else:
+                self.send = torch.zeros(W, L, self.S, dtype=torch.int8, device=self.dev)
+            env = os.environ.get("GC_THC_RANK_SEG_TILES")
+            self.seg_tiles = max(1, int(env)) if env else self.SEG_TILES
+            # bench roofline: the whole per-rank round, algorithmic bytes per SURVEY §8(d) (g, r in,
+            # r_new and codes out, summed codes in, estimate out)
+            w = 0.5 if self.nibble else 1
+            self.timed_kernel = "thc per-rank round (K1 + K2 + exchange + K3)"
+            self.timed_kernel_bytes = int((12 * L + 4 + w * (L + 1)) * d)
+        else:
+            self.S = fold_slices(self.active, W)
+            ws = int(_native.lib().gc_thc_workspace_bytes(ctypes.byref(self.geom), L))
+            self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=self.dev) if ws else None
+            self.signs = torch.empty(-(-self.active // 32), **i32)
+            self.x_rot = torch.empty(L, self.active, dtype=torch.float32, device=self.dev)
+            self.ranges = torch.empty(L, self.nb, 2, dtype=torch.float32, device=self.dev)
+            self.codes = torch.empty(L, self.active, dtype=torch.int8, device=self.dev)
+            self.send = torch.zeros(W, L, self.S, dtype=torch.int8, device=self.dev)
+
+    def _coins(self, r):
+        coins = (_native.Pcg64 * self.L)()
+        for l in range(self.L):
+            coins[l] = self.seeds.pcg("stochastic-round", r, self.w0 + l)   # pipelines.py:293
+        return coins
+
+    def _fold(self, counters):
+        cfg, n = self.cfg, self.n
+
+        def fold(rows, length, offset, out):
+            if n > 1:
+                _native.call("gc_sat_fold", n, length, rows.data_ptr(), rows.stride(0), offset, self.ring_blk,
+                             cfg.wire_bits, out.data_ptr(), counters[3:].data_ptr(), _sp())
+            else:
+                out[:length].copy_(rows[0, :length])
+        return fold
 
     def run(self, g, res, r, ledger, nmse):
         n, L, cfg, comm = self.n, self.L, self.cfg, self.comm
         sp = _sp()
         geom = ctypes.byref(self.geom)
-        rot = self.seeds.pcg("rotation-signs", r)
-        _native.call("gc_thc_signs", ctypes.byref(rot), self.active, self.signs.data_ptr(), sp)
-        coins = (_native.Pcg64 * L)()
-        for l in range(L):
-            coins[l] = self.seeds.pcg("stochastic-round", r, self.w0 + l)
+        rot = self.seeds.pcg("rotation-signs", r)                            # transforms.py:80-82
+        _native.call("gc_thc_signs", ctypes.byref(rot), self.signs.numel() * 32, self.signs.data_ptr(), sp)
+        coins = self._coins(r)
+        counters = self.counters = torch.zeros(4, dtype=torch.int64, device=self.dev)
         ev = self._ev()
         if ev:
             ev[0].record()
-        _native.call("gc_thc_rotate", geom, L, g.data_ptr(), _ptr(res), g.stride(0), self.signs.data_ptr(),
-                     self.x_rot.data_ptr(), self.ranges.data_ptr(), _ptr(self.ws), sp)
-        shared = torch.empty(self.nb, 2, dtype=torch.float32, device=self.dev)
-        _native.call("gc_range_consensus", L, self.nb, self.ranges.data_ptr(), shared.data_ptr(), sp)
-        # ElemMin / ElemMax ring (pipelines.py:271-288) as one all-reduce MAX of (-lo, hi)
-        shared[:, 0].neg_()
-        comm.all_reduce(shared, dist.ReduceOp.MAX, "range-consensus")
-        shared[:, 0].neg_()
-        counters = torch.zeros(4, dtype=torch.int64, device=self.dev)
-        _native.call("gc_thc_quantize", geom, L, self.x_rot.data_ptr(), shared.data_ptr(), coins,
-                     self.codes.data_ptr(), counters.data_ptr(), sp)
-        # codes -> per-destination slices -> all-to-all -> ordered saturating fold -> all-gather
-
-        def fold(rows, length, offset, out):
-            if n > 1:
-                _native.call("gc_sat_fold", n, length, rows.data_ptr(), rows.stride(0), offset, self.ring_blk,
-                             cfg.wire_bits, out.data_ptr(), counters[3:].data_ptr(), sp)
-            else:
-                out[:length].copy_(rows[0, :length])
-
-        sums = exchange_fold(self.codes, comm, n, self.active, self.S, fold, self.sum_dtype, self.send,
-                             "code-aggregate", nibble=cfg.wire_bits <= 4)
+        if self.fused:
+            sums = self._run_fused(g, res, coins, counters, geom, sp)
+            shared = self.shared
+        else:
+            sums, shared = self._run_generic(g, res, coins, counters, geom, sp)
         est = torch.empty(self.dim, dtype=torch.float32, device=self.dev)
-        _native.call("gc_thc_decode_estimate", geom, n, sums.data_ptr(), self.sum_bytes, shared.data_ptr(),
-                     self.signs.data_ptr(), est.data_ptr(), _ptr(self.ws), sp)
-        if res is not None:
-            _native.call("gc_thc_decode_ef", geom, L, self.codes.data_ptr(), shared.data_ptr(), self.signs.data_ptr(),
-                         g.data_ptr(), res.data_ptr(), res.stride(0), _ptr(self.ws), sp)
+        if self.fused:
+            _native.call("gc_thc_rank_decode", geom, n, sums.data_ptr(), self.sum_bytes, shared.data_ptr(),
+                         self.signs.data_ptr(), est.data_ptr(), sp)
+        else:
+            _native.call("gc_thc_decode_estimate", geom, n, sums.data_ptr(), self.sum_bytes, shared.data_ptr(),
+                         self.signs.data_ptr(), est.data_ptr(), _ptr(self.ws), sp)
+            if res is not None:
+                _native.call("gc_thc_decode_ef", geom, L, self.codes.data_ptr(), shared.data_ptr(),
+                             self.signs.data_ptr(), g.data_ptr(), res.data_ptr(), res.stride(0), _ptr(self.ws), sp)
         if ev:
             ev[1].record()
         comm.all_reduce(counters, dist.ReduceOp.SUM)   # clamp count, sum z, sum z^2, clips
-        self.launches += 7
         num_blocks = self.P // self.B
         ledger.charge_ring("range-consensus", n, num_blocks, 32)
         ledger.charge_ring("range-consensus", n, num_blocks, 32)
@@ -410,6 +482,54 @@ class _Thc(_Base):
                     "overflow": OverflowStats(int(c[3]), int(total_adds), math.sqrt(max(var, 0.0)))}
 
         return est, float(cfg.wire_bits * self.P + 64 * num_blocks), RoundStats(counters, None, finalize)
+
+    def _run_fused(self, g, res, coins, counters, geom, sp):
+        L, comm, B = self.L, self.comm, self.B
+        seg = self.seg_tiles
+        bounds = [(t, min(t + seg, self.tiles)) for t in range(0, self.tiles, seg)]
+        pending = []
+
+        def k2(tb, te, work):
+            if work is not None:
+                work.wait()
+            _native.call("gc_thc_rank_quant", geom, L, g.data_ptr(), _ptr(res), _ptr(res), g.stride(0), tb, te,
+                         self.signs.data_ptr(), self.shared.data_ptr(), coins, self.send.data_ptr(), self.S,
+                         int(self.nibble), counters.data_ptr(), sp)
+            self.launches += 1
+
+        for tb, te in bounds:
+            _native.call("gc_thc_rank_ranges", geom, L, g.data_ptr(), _ptr(res), g.stride(0), tb, te,
+                         self.signs.data_ptr(), self.neg.data_ptr(), sp)
+            b0, b1 = tb * 1024 // B, min(te * 1024 // B, self.nb)
+            if L > 1:   # this rank's L tables -> one, rows b0..b1
+                part = self.neg[:, b0:b1].contiguous()
+                _native.call("gc_thc_merge_ranges", L, b1 - b0, part.data_ptr(), self.shared[b0:b1].data_ptr(), sp)
+            self.launches += 1 + (L > 1)
+            # ElemMin / ElemMax ring (pipelines.py:271-288) as one MAX all-reduce of (-lo, hi)
+            work = comm.all_reduce_async(self.shared[b0:b1], dist.ReduceOp.MAX, "range-consensus")
+            pending.append((tb, te, work))
+            if len(pending) > 1:
+                k2(*pending.pop(0))
+        while pending:
+            k2(*pending.pop(0))
+        return exchange_sums(self.send, comm, self.n, self.active, self.S, self._fold(counters), self.sum_dtype,
+                             "code-aggregate", nibble=self.nibble)
+
+    def _run_generic(self, g, res, coins, counters, geom, sp):
+        L, comm, cfg = self.L, self.comm, self.cfg
+        _native.call("gc_thc_rotate", geom, L, g.data_ptr(), _ptr(res), g.stride(0), self.signs.data_ptr(),
+                     self.x_rot.data_ptr(), self.ranges.data_ptr(), _ptr(self.ws), sp)
+        shared = torch.empty(self.nb, 2, dtype=torch.float32, device=self.dev)
+        _native.call("gc_range_consensus", L, self.nb, self.ranges.data_ptr(), shared.data_ptr(), sp)
+        shared[:, 0].neg_()
+        comm.all_reduce(shared, dist.ReduceOp.MAX, "range-consensus")
+        shared[:, 0].neg_()
+        _native.call("gc_thc_quantize", geom, L, self.x_rot.data_ptr(), shared.data_ptr(), coins,
+                     self.codes.data_ptr(), counters.data_ptr(), sp)
+        sums = exchange_fold(self.codes, comm, self.n, self.active, self.S, self._fold(counters), self.sum_dtype,
+                             self.send, "code-aggregate", nibble=cfg.wire_bits <= 4)
+        self.launches += 7
+        return sums, shared
 
 
 class _TopK(_Base):

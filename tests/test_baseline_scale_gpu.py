@@ -160,3 +160,33 @@ def test_cfg4_powersgd_matches_reference(case):
                 _close(wq, z[key], f"{case} warm Q tensor {t} r{r}")
         if len(sizes) == 1:
             assert res.nmse == pytest.approx(rec["nmse"], rel=1e-4)
+
+
+def _rank_cfg2(rank, world, case):
+    import torch
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.distributed import DistributedGradientPipeline
+    from tests.test_baseline_scale_gpu import _check_exact, _check_inputs, _dev, _gaussian, _meta
+    m = _meta(case)
+    q, b = (4, 8) if case.endswith("q4b8") else (4, 4)
+    pipe = DistributedGradientPipeline(gcb.RotatedQuantConfig(q, b, 1024), m["n"], m["d"], gcb.SeedSpec(SEED),
+                                       device=torch.device("cuda", rank))
+    assert pipe._engine.fused
+    for rec in m["rounds"]:
+        r = rec["round"]
+        grads = _gaussian(m["d"], m["n"], r)
+        _check_inputs(grads, rec)
+        res = pipe.run_round(_dev(grads), r)
+        _check_exact(res, pipe, rec, f"{case}/per-rank round {r}")
+        assert res.overflow.clip_events == rec["clip_events"] and res.overflow.total_adds == rec["total_adds"]
+        assert res.overflow.code_sigma == pytest.approx(rec["code_sigma"], rel=1e-12)
+    return True
+
+
+@pytest.mark.parametrize("case", ["cfg2_thc_q4b8", "cfg2_thc_q4b4"])
+def test_cfg2_thc_per_rank_path_matches_reference(case):
+    """The distributed pipeline's per-rank path (K1 ranges / NCCL range all-reduce / K2 quantize +
+    own decode + EF into the send layout / all-to-all + fold + all-gather / K3 decode) on a one-rank
+    NCCL group holding all 8 workers, at cfg2's full size, against the reference's hashes."""
+    from tests.dist_util import run_world
+    assert run_world(_rank_cfg2, 1, (case,), backend="nccl") == [True]

@@ -37,21 +37,34 @@ def _train(rank, world, scheme):
         local = state.last_inputs[0].reshape(-1).cpu().numpy()          # what DDP handed to the hook
         est = state.last_results[0].estimate_tensor.cpu().numpy()      # what the hook returned
         applied = np.sort(torch.cat([p.grad.reshape(-1) for p in model.parameters()]).cpu().numpy())
-        log.append((local, est, applied))
+        ids, offs, numels = state.last_layouts[0]                       # parameter order in the bucket
+        pidx = {id(p): i for i, p in enumerate(model.parameters())}
+        log.append((local, est, applied, [(pidx[i], o, m) for i, o, m in zip(ids, offs, numels)]))
         opt.step()
     return log, params
 
 
 @pytest.mark.parametrize("scheme", ["rotated_quant", "topk"])
 def test_ddp_hook_matches_reference_round(scheme):
+    """DDP may re-lay the bucket out after step 0 (parameters in gradient-ready order): the
+    reference round of every step then starts from the residual each parameter carried."""
+    from oracle import gradcomp_oracle as orc
     res = run_world(_train, 2, (scheme,))
     (log0, params), (log1, _) = res
-    grads = [[log0[s][0], log1[s][0]] for s in range(3)]
-    outs = oracle_rounds(scheme, params, grads, 5)
+    resid = [{}, {}]   # [rank][param index] -> residual
     for s in range(3):
+        layout = log0[s][3]
+        assert layout == log1[s][3]
+        grads = [log0[s][0], log1[s][0]]
+        st = orc.OracleState([np.concatenate([resid[w].get(i, np.zeros(m, np.float32)) for i, o, m in layout])
+                              for w in range(2)])
+        out = orc.run_round(scheme, params, st, grads, 5, s)
+        for w in range(2):
+            for i, o, m in layout:
+                resid[w][i] = st.residuals[w][o:o + m].copy()
         assert np.array_equal(log0[s][1], log1[s][1])                    # same estimate on both ranks
-        assert np.array_equal(log0[s][1], outs[s]["estimate"]), s        # = the reference round
-        assert np.array_equal(log0[s][2], np.sort(outs[s]["estimate"]))  # and DDP applied it
+        assert np.array_equal(log0[s][1], out["estimate"]), s            # = the reference round
+        assert np.array_equal(log0[s][2], np.sort(out["estimate"]))      # and DDP applied it
 
 
 class _FakeBucket:

@@ -28,7 +28,10 @@ def _grads(n, r):
     return [orc.stream_rng(SEED, "grad-worker", r, w).standard_normal(D).astype(np.float32) for w in range(n)]
 
 
-def _rank(rank, world, scheme, params, n):
+def _rank(rank, world, scheme, params, n, seg_tiles=None):
+    import os
+    if seg_tiles:
+        os.environ["GC_THC_RANK_SEG_TILES"] = str(seg_tiles)
     import torch
     import torch.distributed as dist
     import paper_2407_01378_b200 as gcb
@@ -79,3 +82,19 @@ def test_nccl_round_matches_reference(scheme, params, exact, per_rank):
             tol = 1e-3 if params.get("bits") == 16 else 1e-5
             err = np.linalg.norm(got.astype(np.float64) - want) / np.linalg.norm(want)
             assert err <= tol, (scheme, r, err)
+
+
+@pytest.mark.parametrize("params", [dict(quant_bits=4, wire_bits=8, rotation_block=1024),
+                                    dict(quant_bits=4, wire_bits=4, rotation_block=128),
+                                    dict(quant_bits=5, wire_bits=16, rotation_block=32)])
+@pytest.mark.parametrize("per_rank", [1, 3])
+def test_nccl_thc_segments(params, per_rank):
+    """The per-rank THC round over 5-tile segments (K1 / async range all-reduce / K2 pipelined)."""
+    world = _world()
+    n = per_rank * world
+    out = run_world(_rank, world, ("rotated_quant", params, n, 5), backend="nccl")
+    ref = oracle_rounds("rotated_quant", params, [_grads(n, r) for r in range(2)], SEED)
+    for r in range(2):
+        assert np.array_equal(out[0][r]["est"], ref[r]["estimate"]), r
+        assert np.array_equal(np.stack(sum((o[r]["res"] for o in out), [])), np.stack(ref[r]["residuals"]))
+        assert out[0][r]["clips"] == ref[r]["clip_events"]
