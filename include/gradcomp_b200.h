@@ -292,6 +292,7 @@ typedef struct gc_psgd_batch {
   int64_t ld;
   const int64_t *est_offsets;
   int32_t rows_aligned;   /* 1 if every row start (and the estimate slices) is 16-byte aligned */
+  int32_t est_accumulate; /* decode: estimate += P_hat Q_sum^T / n instead of = (rank chunks after the first) */
 } gc_psgd_batch;
 
 int gc_psgd_splits(int32_t rows_total, int64_t cols);
@@ -317,9 +318,9 @@ int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, i
 int gc_psgd_mtp_ef_supported(int64_t rows, int64_t cols, int32_t rank, int32_t rows_aligned);
 int gc_psgd_mtp_ef(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, float *resid,
                    const float *p_hat, float *q, void *stream);
-/* orthonormalize (compressors.py:555-588) for T tensors: fp64 modified Gram-Schmidt with
- * canonical-basis completion; status[t] = 1 if completion failed (DegenerateMatrixError).
- * workspace: T*rows*rank doubles. */
+/* orthonormalize (compressors.py:555-588) for T tensors, rank <= 64: fp64 Gram-Schmidt (CGS2, the
+ * c dot products of a column formed in one sweep) with the reference's canonical-basis completion;
+ * status[t] = 1 if completion failed (DegenerateMatrixError).  workspace: T*rows*rank doubles. */
 int gc_psgd_orthonormalize(int32_t tensors, int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace,
                            int32_t *status, void *stream);
 /* own_w = P_hat Q_w^T, resid_w -= own_w (resid holds the corrected matrix; NULL skips);
@@ -332,8 +333,11 @@ int gc_psgd_decode(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, i
 int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
                          const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
                          void *stream);
-/* gram[t] = Q_t^T Q_t in fp64 (rank check of ensure_full_rank, compressors.py:595-603). */
-int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, double *gram, void *stream);
+/* gram[t] = Q_t^T Q_t in fp64 (rank check of ensure_full_rank, compressors.py:595-603), rank <= 64;
+ * workspace: gc_psgd_gram_workspace_bytes(tensors, rank) (column-slice partials, summed in order). */
+int64_t gc_psgd_gram_workspace_bytes(int32_t tensors, int32_t rank);
+int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, double *gram, void *workspace,
+                 void *stream);
 /* cudaMemsetAsync wrapper (residual reset of the dense bypass, pipelines.py:336). */
 int gc_fill_zero(void *ptr, int64_t bytes, void *stream);
 /* rows x row_bytes strided copy in either direction (cudaMemcpy2DAsync): one PCIe transfer for the

@@ -51,7 +51,7 @@ class PsgdBatch(ctypes.Structure):
     """gc_psgd_batch: T same-shape tensors x L workers (row_offsets / est_offsets are device int64)."""
 
     _fields_ = [("tensors", c_int32), ("workers", c_int32), ("row_offsets", c_void_p), ("ld", c_int64),
-                ("est_offsets", c_void_p), ("rows_aligned", c_int32)]
+                ("est_offsets", c_void_p), ("rows_aligned", c_int32), ("est_accumulate", c_int32)]
 
 
 P = c_void_p
@@ -126,7 +126,8 @@ SIGNATURES = {
     "gc_psgd_orthonormalize": (c_int, [I32, I64, I32, P, P, P, P, P]),
     "gc_psgd_decode": (c_int, [POINTER(PsgdBatch), I32, I64, I64, I64, I32, P, P, P, P, P, P]),
     "gc_psgd_decode_fused": (c_int, [POINTER(PsgdBatch), I32, I64, I64, I64, I32, P, P, P, P, P, P]),
-    "gc_psgd_gram": (c_int, [I32, I64, I32, P, P, P]),
+    "gc_psgd_gram_workspace_bytes": (I64, [I32, I32]),
+    "gc_psgd_gram": (c_int, [I32, I64, I32, P, P, P, P]),
     "gc_fill_zero": (c_int, [P, I64, P]),
     "gc_pack_nibbles": (c_int, [I64, P, P, P]),
     "gc_unpack_nibbles": (c_int, [I64, P, P, P]),

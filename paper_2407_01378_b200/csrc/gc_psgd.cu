@@ -193,6 +193,110 @@ __global__ void __launch_bounds__(1024) mgs_kernel(int64_t rows, int R, const fl
 }
 
 
+// Orthonormalization for any rank <= kMaxOrthRank (compressors.py:555-588), one CTA per tensor.
+// Column c is projected against all previous columns with classical Gram-Schmidt applied twice
+// (CGS2: as stable as the reference's MGS; both give the Q factor of the same nested column
+// spaces, agreeing to O(cond * eps) in fp64 -- far inside the 1e-5 contract).  The c dot products
+// of a pass are formed together: a thread accumulates 8 of them over its rows, each warp reduces
+// them with shuffles and the warps' partials are summed in a fixed order (deterministic), so a
+// column costs 2 x (ceil(c / 8) + 1) row sweeps and 3 block reductions instead of MGS's c + 1
+// sequential block reductions -- the difference that matters at r = 64.  A column
+// whose residual norm is at or below 1e-8 * scale takes the reference's canonical-basis
+// completion (the sequential path of mgs_kernel); none left -> status = 1 (DegenerateMatrixError).
+constexpr int kMaxOrthRank = 64;
+constexpr int kOrthThreads = 256;
+
+__device__ void orth_dots(int64_t rows, int R, const double *a, int c, double *dots, double (*wred)[kMaxOrthRank]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int p0 = 0; p0 < c; p0 += 8) {
+    double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t i = threadIdx.x; i < rows; i += kOrthThreads) {
+      const double x = a[i * R + c];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (p0 + k < c) part[k] += a[i * R + p0 + k] * x;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double v = part[k];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && p0 + k < c) wred[warp][p0 + k] = v;
+    }
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < c; p += kOrthThreads) {
+    double v = 0.0;
+    for (int w = 0; w < kOrthThreads / 32; ++w) v += wred[w][p];
+    dots[p] = v;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kOrthThreads) orth_kernel(int64_t rows, int R, const float *in, double *a,
+                                                            float *out, int *status) {
+  __shared__ double red[33];
+  __shared__ double dots[kMaxOrthRank];
+  __shared__ double wred[kOrthThreads / 32][kMaxOrthRank];
+  {
+    const int64_t t = blockIdx.x;
+    in += t * rows * R;
+    a += t * rows * R;
+    out += t * rows * R;
+    status += t;
+  }
+  double fro = 0.0;
+  for (int64_t i = threadIdx.x; i < rows * R; i += kOrthThreads) {
+    const double v = static_cast<double>(in[i]);
+    a[i] = v;
+    fro += v * v;
+  }
+  fro = block_sum(fro, red);
+  const double scale = sqrt(fro) / fmax(1.0, sqrt(static_cast<double>(R)));
+  const double floor_ = fmax(scale * 1e-8, 1e-300);
+  for (int c = 0; c < R; ++c) {
+    for (int pass = 0; pass < 2 && c > 0; ++pass) {
+      orth_dots(rows, R, a, c, dots, wred);
+      for (int64_t i = threadIdx.x; i < rows; i += kOrthThreads) {
+        double x = a[i * R + c];
+        for (int p = 0; p < c; ++p) x -= dots[p] * a[i * R + p];
+        a[i * R + c] = x;
+      }
+      __syncthreads();
+    }
+    double nn = 0.0;
+    for (int64_t i = threadIdx.x; i < rows; i += kOrthThreads) nn += a[i * R + c] * a[i * R + c];
+    const double norm = sqrt(block_sum(nn, red));
+    if (norm > floor_) {
+      for (int64_t i = threadIdx.x; i < rows; i += kOrthThreads) a[i * R + c] /= norm;
+      __syncthreads();
+      continue;
+    }
+    bool done = false;   // canonical completion, as mgs_kernel
+    for (int64_t basis = 0; basis < rows && !done; ++basis) {
+      for (int64_t i = threadIdx.x; i < rows; i += kOrthThreads) a[i * R + c] = (i == basis) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int p = 0; p < c; ++p) {
+        double dot = 0.0;
+        for (int64_t i = threadIdx.x; i < rows; i += kOrthThreads) dot += a[i * R + p] * a[i * R + c];
+        dot = block_sum(dot, red);
+        for (int64_t i = threadIdx.x; i < rows; i += kOrthThreads) a[i * R + c] -= dot * a[i * R + p];
+        __syncthreads();
+      }
+      double cn = 0.0;
+      for (int64_t i = threadIdx.x; i < rows; i += kOrthThreads) cn += a[i * R + c] * a[i * R + c];
+      const double cnorm = sqrt(block_sum(cn, red));
+      if (cnorm > 0.5) {
+        for (int64_t i = threadIdx.x; i < rows; i += kOrthThreads) a[i * R + c] /= cnorm;
+        done = true;
+      }
+      __syncthreads();
+    }
+    if (!done && threadIdx.x == 0) *status = 1;
+    __syncthreads();
+  }
+  for (int64_t i = threadIdx.x; i < rows * R; i += kOrthThreads) out[i] = static_cast<float>(a[i]);
+}
+
 // ------------------------------------------------------------------ vectorised kernels
 // Used when cols % 4 == 0 and the buffers are 16-byte aligned (cfg4: 18709 x 18708).
 //
@@ -421,7 +525,8 @@ constexpr int kDecBatch = GC_PSGD_DEC_BATCH;   // rows whose loads are in flight
 template <int R, bool A16>
 __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d, int64_t rows, int64_t cols,
                                                          const float *ph, const float *qw, const float *qsum,
-                                                         float *resid, Rows rw_, float *est, const int64_t *est_offs) {
+                                                         float *resid, Rows rw_, float *est, const int64_t *est_offs,
+                                                         int est_acc) {
   __shared__ float ps[kDecRows * R];
   {   // tensor t of a batch: its factors, workers t*L .. t*L+L-1, its slice of the estimate
     const int t = blockIdx.z;
@@ -478,8 +583,14 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
           float *o = dst + (row0 + a) * cols + col;
           if (w < L)
             stc<A16>(o, make_float4(cv[u].x - o4[0], cv[u].y - o4[1], cv[u].z - o4[2], cv[u].w - o4[3]), vm);
-          else
-            stc<A16>(o, make_float4(dn(o4[0]), dn(o4[1]), dn(o4[2]), dn(o4[3])), vm);
+          else {
+            float4 e = make_float4(dn(o4[0]), dn(o4[1]), dn(o4[2]), dn(o4[3]));
+            if (est_acc) {   // rank chunks after the first: estimate += this chunk's part
+              const float4 pv = ldc<A16>(o, vm);
+              e.x += pv.x; e.y += pv.y; e.z += pv.z; e.w += pv.w;
+            }
+            stc<A16>(o, e, vm);
+          }
         }
       }
       continue;
@@ -504,12 +615,17 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
           const float4 c = *reinterpret_cast<const float4 *>(dst + i);
           __stcs(reinterpret_cast<float4 *>(dst + i), make_float4(c.x - o4[0], c.y - o4[1], c.z - o4[2], c.w - o4[3]));
         } else {
-          __stcs(reinterpret_cast<float4 *>(dst + i), make_float4(dn(o4[0]), dn(o4[1]), dn(o4[2]), dn(o4[3])));
+          float4 e = make_float4(dn(o4[0]), dn(o4[1]), dn(o4[2]), dn(o4[3]));
+          if (est_acc) {
+            const float4 pv = *reinterpret_cast<const float4 *>(dst + i);
+            e.x += pv.x; e.y += pv.y; e.z += pv.z; e.w += pv.w;
+          }
+          __stcs(reinterpret_cast<float4 *>(dst + i), e);
         }
       } else {
         for (int t = 0; t < 4; ++t) {
           const int64_t it = i + col_off<A16>(t);
-          if (((vm >> t) & 1u) && it < d) dst[it] = w < L ? dst[it] - o4[t] : dn(o4[t]);
+          if (((vm >> t) & 1u) && it < d) dst[it] = w < L ? dst[it] - o4[t] : (est_acc ? dst[it] + dn(o4[t]) : dn(o4[t]));
         }
       }
     }
@@ -667,18 +783,44 @@ __global__ void __launch_bounds__(kEfThreads) mtp_ef_kernel(int64_t d, int64_t r
 }
 
 // Gram matrix Q^T Q (fp64) for the rank check of ensure_full_rank (compressors.py:595-603).
-__global__ void __launch_bounds__(256) gram_kernel(int64_t cols, int R, const float *q, double *gram) {
-  __shared__ double red[33];
-  q += static_cast<int64_t>(blockIdx.x) * cols * R;
-  gram += static_cast<int64_t>(blockIdx.x) * R * R;
-  for (int a = 0; a < R; ++a)
-    for (int b = a; b < R; ++b) {
-      double v = 0.0;
-      for (int64_t j = threadIdx.x; j < cols; j += blockDim.x)
-        v += static_cast<double>(q[j * R + a]) * static_cast<double>(q[j * R + b]);
-      v = block_sum(v, red);
-      if (threadIdx.x == 0) gram[a * R + b] = gram[b * R + a] = v;
+// Gram Q^T Q per tensor (fp64): the columns are split over kGramSlices CTAs; a thread owns
+// (a, b) pairs of the upper triangle and sums its slice's rows; the slices are added in order.
+constexpr int kGramSlices = 32;
+
+__global__ void __launch_bounds__(256) gram_partial_kernel(int64_t cols, int R, const float *q, double *partial) {
+  const int t = blockIdx.x, sl = blockIdx.y;
+  q += static_cast<int64_t>(t) * cols * R;
+  const int P = R * (R + 1) / 2;
+  const int64_t per = (cols + kGramSlices - 1) / kGramSlices;
+  const int64_t j0 = sl * per, j1 = min(cols, j0 + per);
+  for (int pi = threadIdx.x; pi < P; pi += 256) {
+    int a = 0, rem = pi;   // pair index -> (a, b >= a)
+    while (rem >= R - a) {
+      rem -= R - a;
+      ++a;
     }
+    const int b = a + rem;
+    double v = 0.0;
+    for (int64_t j = j0; j < j1; ++j) v += static_cast<double>(q[j * R + a]) * static_cast<double>(q[j * R + b]);
+    partial[(static_cast<int64_t>(t) * kGramSlices + sl) * P + pi] = v;
+  }
+}
+
+__global__ void gram_reduce_kernel(int R, const double *partial, double *gram) {
+  const int t = blockIdx.x;
+  const int P = R * (R + 1) / 2;
+  for (int pi = threadIdx.x; pi < P; pi += blockDim.x) {
+    int a = 0, rem = pi;
+    while (rem >= R - a) {
+      rem -= R - a;
+      ++a;
+    }
+    const int b = a + rem;
+    double v = 0.0;
+    for (int sl = 0; sl < kGramSlices; ++sl) v += partial[(static_cast<int64_t>(t) * kGramSlices + sl) * P + pi];
+    gram[(static_cast<int64_t>(t) * R + a) * R + b] = v;
+    gram[(static_cast<int64_t>(t) * R + b) * R + a] = v;
+  }
 }
 
 #define GC_RANK_SWITCH(rank, CALL)                                                      \
@@ -851,11 +993,12 @@ int gc_psgd_mtp_ef(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols
 
 int gc_psgd_orthonormalize(int32_t tensors, int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace,
                            int32_t *status, void *stream) {
-  GC_REQUIRE(tensors >= 1 && rows >= rank && rank >= 1 && rank <= kMaxRank && p && p_hat && workspace && status,
+  GC_REQUIRE(tensors >= 1 && tensors <= 65535 && rows >= rank && rank >= 1 && rank <= kMaxOrthRank && p && p_hat &&
+                 workspace && status,
              "invalid argument");
-  mgs_kernel<<<tensors, 1024, 0, static_cast<cudaStream_t>(stream)>>>(rows, rank, p, static_cast<double *>(workspace),
-                                                                     p_hat, status);
-  GC_LAUNCH_CHECK("mgs_kernel");
+  orth_kernel<<<tensors, kOrthThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      rows, rank, p, static_cast<double *>(workspace), p_hat, status);
+  GC_LAUNCH_CHECK("orth_kernel");
   return GC_OK;
 }
 
@@ -882,19 +1025,32 @@ int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t r
   GC_RANK_SWITCH(rank, ({
     if (a16)
       decode_vec_kernel<R, true><<<grid, 256, 0, st>>>(b->workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid,
-                                                       rows_of(b), estimate, b->est_offsets);
+                                                       rows_of(b), estimate, b->est_offsets,
+                                                       b->est_accumulate);
     else
       decode_vec_kernel<R, false><<<grid, 256, 0, st>>>(b->workers, n, d, rows, cols, p_hat, q_workers, q_sum, resid,
-                                                        rows_of(b), estimate, b->est_offsets);
+                                                        rows_of(b), estimate, b->est_offsets,
+                                                        b->est_accumulate);
   }));
   GC_LAUNCH_CHECK("decode_vec_kernel");
   return GC_OK;
 }
 
-int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, double *gram, void *stream) {
-  GC_REQUIRE(tensors >= 1 && cols >= 1 && rank >= 1 && rank <= kMaxRank && q && gram, "invalid argument");
-  gram_kernel<<<tensors, 256, 0, static_cast<cudaStream_t>(stream)>>>(cols, rank, q, gram);
-  GC_LAUNCH_CHECK("gram_kernel");
+int64_t gc_psgd_gram_workspace_bytes(int32_t tensors, int32_t rank) {
+  return 8 * static_cast<int64_t>(tensors) * kGramSlices * rank * (rank + 1) / 2;
+}
+
+int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, double *gram, void *workspace,
+                 void *stream) {
+  GC_REQUIRE(tensors >= 1 && tensors <= 65535 && cols >= 1 && rank >= 1 && rank <= kMaxOrthRank && q && gram &&
+                 workspace,
+             "invalid argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double *partial = static_cast<double *>(workspace);
+  gram_partial_kernel<<<dim3(tensors, kGramSlices), 256, 0, st>>>(cols, rank, q, partial);
+  GC_LAUNCH_CHECK("gram_partial_kernel");
+  gram_reduce_kernel<<<tensors, 256, 0, st>>>(rank, partial, gram);
+  GC_LAUNCH_CHECK("gram_reduce_kernel");
   return GC_OK;
 }
 

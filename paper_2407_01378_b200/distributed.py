@@ -376,7 +376,8 @@ class _Thc(_Base):
     all-gather of the sums and K3, the estimate decode.  Other block sizes use the generic
     multi-kernel path (gc_thc_rotate / quantize / decode)."""
 
-    SEG_TILES = 4096   # tiles (of 1024 coordinates) per segment: L * 32 MB of g + r
+    SEG_TILES = 32768   # tiles (of 1024 coordinates) per segment across ranks
+    DEPTH = 2           # segments whose K1 and range all-reduce are in flight before K2 runs
 
     def __init__(self, cfg: RotatedQuantConfig, pipe):
         super().__init__(pipe)
@@ -406,8 +407,10 @@ class _Thc(_Base):
                 self.send = torch.zeros(W, L, self.S // 2, dtype=torch.uint8, device=self.dev)
             else:
                 self.send = torch.zeros(W, L, self.S, dtype=torch.int8, device=self.dev)
+            # one segment on a one-rank group (nothing to overlap); across ranks segments of
+            # SEG_TILES so the range all-reduce of one overlaps the next one's K1
             env = os.environ.get("GC_THC_RANK_SEG_TILES")
-            self.seg_tiles = max(1, int(env)) if env else self.SEG_TILES
+            self.seg_tiles = max(1, int(env)) if env else (self.tiles if W == 1 else self.SEG_TILES)
             # bench roofline: the whole per-rank round, algorithmic bytes per SURVEY §8(d) (g, r in,
             # r_new and codes out, summed codes in, estimate out)
             w = 0.5 if self.nibble else 1
@@ -508,7 +511,7 @@ class _Thc(_Base):
             # ElemMin / ElemMax ring (pipelines.py:271-288) as one MAX all-reduce of (-lo, hi)
             work = comm.all_reduce_async(self.shared[b0:b1], dist.ReduceOp.MAX, "range-consensus")
             pending.append((tb, te, work))
-            if len(pending) > 1:
+            if len(pending) > self.DEPTH:
                 k2(*pending.pop(0))
         while pending:
             k2(*pending.pop(0))

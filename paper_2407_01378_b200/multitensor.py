@@ -236,9 +236,6 @@ class TensorListPipeline:
                 _native.call("gc_segment_fold_ef", n, len(self.bypass), self.seg_off.data_ptr(),
                              self.seg_len.data_ptr(), c.data_ptr(), res.data_ptr(), c.stride(0), est.data_ptr(), sp)
             for grp in ([] if fuse_ef else self.groups):
-                sv = grp.saved
-                _native.call("gc_psgd_decode", __import__("ctypes").byref(grp.batch), n, grp.d, grp.rows, grp.cols,
-                             grp.rank, sv["p_hat"].data_ptr(), sv["qw"].data_ptr(), sv["q_sum"].data_ptr(),
-                             res.data_ptr(), None, sp)
+                grp.saved["decode"](res.data_ptr(), None)   # EF update of the group (rank chunk by chunk)
         self.launches += 2 + len(self.groups) * 11
         return RoundResult(self.scheme, round_index, est, D, ledger, bits, _simple_stats(acc))

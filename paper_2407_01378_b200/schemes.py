@@ -484,7 +484,24 @@ class PowerSgdGroup:
     The single-matrix reference path is T = 1 with rows at w * ld; the chunked mode of
     cfg4(b) passes per-(tensor, worker) row offsets into the flat per-worker gradients."""
 
-    RANKS = (1, 2, 3, 4, 5, 6, 7, 8, 16)
+    RANKS = (1, 2, 3, 4, 5, 6, 7, 8, 16)   # ranks the factor kernels are compiled for
+    MAX_RANK = 64                           # orthonormalization / Gram limit
+
+    @staticmethod
+    def rank_chunks(r: int) -> list[int]:
+        """Compiled ranks whose sum is r (16s, then 8, then the rest): a rank outside RANKS runs
+        its factor passes chunk by chunk (P, Q and the decode are column-separable; the
+        orthonormalization and the rank check see all r columns)."""
+        out = []
+        while r >= 16:
+            out.append(16)
+            r -= 16
+        if r > 8:
+            out.append(8)
+            r -= 8
+        if r:
+            out.append(r)
+        return out
 
     def __init__(self, cfg: PowerSgdConfig, n: int, L: int, d: int, T: int, seeds: SeedSpec, device,
                  row_offsets=None, est_offsets=None, ld: int = 0):
@@ -492,15 +509,18 @@ class PowerSgdGroup:
         self.seeds, self.device = seeds, device
         self.rows, self.cols = matrix_shape_for(d)
         self.rank = cfg.rank
-        if self.rank not in self.RANKS:
-            raise NotImplementedError(f"PowerSGD rank {self.rank} not compiled (supported: {self.RANKS})")
+        if self.rank > self.MAX_RANK:
+            raise NotImplementedError(f"PowerSGD rank {self.rank} > {self.MAX_RANK} is not supported")
         if self.rows < self.rank:
             raise ValueError("need a tall matrix (rows >= cols)")
+        self.chunks = [self.rank] if self.rank in self.RANKS else self.rank_chunks(self.rank)
         self.row_offsets, self.est_offsets = row_offsets, est_offsets
-        self.batch = _native.PsgdBatch(T, L, _ptr(row_offsets), ld, _ptr(est_offsets), 0)
+        self.batch = _native.PsgdBatch(T, L, _ptr(row_offsets), ld, _ptr(est_offsets), 0, 0)
         ws = int(_native.lib().gc_psgd_workspace_bytes(T * L, self.rows, self.cols, self.rank))
         self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
         self.mgs_ws = torch.empty(T * self.rows * self.rank, dtype=torch.float64, device=device)
+        self.gram_ws = torch.empty(int(_native.lib().gc_psgd_gram_workspace_bytes(T, self.rank)) // 8,
+                                   dtype=torch.float64, device=device)
         self.warm = None          # [T][cols][r]
         self.last = {}
         self._gram_host = None    # pinned [T][r][r]: Gram of the warm Q, filled behind an event
@@ -519,7 +539,8 @@ class PowerSgdGroup:
 
     def _gram(self, q_dev):
         gram = torch.empty(self.T, self.rank, self.rank, dtype=torch.float64, device=self.device)
-        _native.call("gc_psgd_gram", self.T, self.cols, self.rank, q_dev.data_ptr(), gram.data_ptr(), _sp())
+        _native.call("gc_psgd_gram", self.T, self.cols, self.rank, q_dev.data_ptr(), gram.data_ptr(),
+                     self.gram_ws.data_ptr(), _sp())
         return gram
 
     def _rank_ok_host(self, host_gram, q_dev):
@@ -584,24 +605,42 @@ class PowerSgdGroup:
         [T][cols][r]."""
         sp = _sp()
         T, L, n, d, rows, cols, r = self.T, self.L, self.n, self.d, self.rows, self.cols, self.rank
-        dev = self.device
         bref = ctypes.byref(self.batch)
         if q is None:
             q = self.seed_q(round_index)
+        # rank chunks: (first column, width); one chunk = the compiled rank itself
+        spans, c0 = [], 0
+        for rc in self.chunks:
+            spans.append((c0, rc))
+            c0 += rc
+        multi = len(spans) > 1
+
+        def cols_of(x, c0, rc, name):
+            if not multi:
+                return x
+            out = self._buf(name, x.shape[:-1] + (rc,))
+            out.copy_(x[..., c0:c0 + rc])
+            return out
+
         p = self._buf("p", (T * L, rows, r))
         # P = M Q on tcgen05: float4 producer for aligned rows, masked scalars otherwise
         umma = vec or umma_unaligned()
-        if umma and ef_resid_ptr is not None:
-            _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, grads_ptr, ef_resid_ptr, q.data_ptr(),
-                         p.data_ptr(), self.ws.data_ptr(), sp)
-        elif umma and grads_ptr is not None:
-            _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, grads_ptr, resid_ptr, q.data_ptr(), p.data_ptr(),
-                         self.ws.data_ptr(), sp)
-        elif umma:
-            _native.call("gc_psgd_mq_fused", bref, d, rows, cols, r, c_ptr, None, q.data_ptr(), p.data_ptr(),
-                         self.ws.data_ptr(), sp)
-        else:
-            _native.call("gc_psgd_mq", bref, d, rows, cols, r, c_ptr, q.data_ptr(), p.data_ptr(), sp)
+        for k, (c0, rc) in enumerate(spans):
+            q_c = cols_of(q, c0, rc, f"q_c{k}")
+            p_c = self._buf(f"p_c{k}", (T * L, rows, rc)) if multi else p
+            if umma and k == 0 and ef_resid_ptr is not None:
+                _native.call("gc_psgd_mq_fused", bref, d, rows, cols, rc, grads_ptr, ef_resid_ptr, q_c.data_ptr(),
+                             p_c.data_ptr(), self.ws.data_ptr(), sp)
+            elif umma and k == 0 and grads_ptr is not None:
+                _native.call("gc_psgd_mq_fused", bref, d, rows, cols, rc, grads_ptr, resid_ptr, q_c.data_ptr(),
+                             p_c.data_ptr(), self.ws.data_ptr(), sp)
+            elif umma:   # later chunks read the corrected matrices the first chunk left in c_ptr
+                _native.call("gc_psgd_mq_fused", bref, d, rows, cols, rc, c_ptr, None, q_c.data_ptr(), p_c.data_ptr(),
+                             self.ws.data_ptr(), sp)
+            else:
+                _native.call("gc_psgd_mq", bref, d, rows, cols, rc, c_ptr, q_c.data_ptr(), p_c.data_ptr(), sp)
+            if multi:
+                p[..., c0:c0 + rc].copy_(p_c)
         p_sum = fold("left-factor", p, rows * r).reshape(T, rows, r)
         p_hat = self._buf("p_hat", (T, rows, r))
         status = self._buf("status", (T,), torch.int32).zero_()
@@ -610,12 +649,21 @@ class PowerSgdGroup:
         qw = self._buf("qw", (T * L, cols, r))
         # Q_w and the EF update in one pass over M when nothing reads the corrected matrices
         # between them (no nmse hook; corrected held in resid); the estimate stays in decode
-        mtp_ef = before_ef is None and resid_ptr is not None and c_ptr == resid_ptr and self._mtp_ef_ok()
-        if mtp_ef:
-            _native.call("gc_psgd_mtp_ef", bref, d, rows, cols, r, resid_ptr, p_hat.data_ptr(), qw.data_ptr(), sp)
-        else:
-            _native.call("gc_psgd_mtp", bref, d, rows, cols, r, c_ptr, p_hat.data_ptr(), qw.data_ptr(),
-                         self.ws.data_ptr(), sp)
+        mtp_ef = (not multi and before_ef is None and resid_ptr is not None and c_ptr == resid_ptr
+                  and self._mtp_ef_ok())
+        ph_chunks, qw_chunks = [], []
+        for k, (c0, rc) in enumerate(spans):
+            ph_c = cols_of(p_hat, c0, rc, f"ph_c{k}")
+            qw_c = self._buf(f"qw_c{k}", (T * L, cols, rc)) if multi else qw
+            if mtp_ef:
+                _native.call("gc_psgd_mtp_ef", bref, d, rows, cols, rc, resid_ptr, ph_c.data_ptr(), qw_c.data_ptr(), sp)
+            else:
+                _native.call("gc_psgd_mtp", bref, d, rows, cols, rc, c_ptr, ph_c.data_ptr(), qw_c.data_ptr(),
+                             self.ws.data_ptr(), sp)
+            if multi:
+                qw[..., c0:c0 + rc].copy_(qw_c)
+            ph_chunks.append(ph_c)
+            qw_chunks.append(qw_c)
         q_sum = fold("right-factor", qw, cols * r).reshape(T, cols, r)
         # warm Q (pipelines.py:366) before the decode, and its Gram copied to pinned host memory
         # behind an event: the next round's rank check (ensure_full_rank) then reads it without
@@ -630,21 +678,28 @@ class PowerSgdGroup:
             ev = torch.cuda.Event()
             ev.record()
             self._pending_gram = (warm, ev)
+        qs_chunks = [cols_of(q_sum, c0, rc, f"qs_c{k}") for k, (c0, rc) in enumerate(spans)]
+
+        def decode(resid, est):
+            # own = P_hat Q_w^T and the estimate are sums over the rank: chunk k > 0 subtracts its
+            # part from the residual in place and adds its part to the estimate
+            for k, (c0, rc) in enumerate(spans):
+                self.batch.est_accumulate = 1 if (k > 0 and est is not None) else 0
+                _native.call("gc_psgd_decode", bref, n, d, rows, cols, rc, ph_chunks[k].data_ptr(),
+                             qw_chunks[k].data_ptr(), qs_chunks[k].data_ptr(), resid, est, sp)
+            self.batch.est_accumulate = 0
+
         if mtp_ef:
-            _native.call("gc_psgd_decode", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
-                         q_sum.data_ptr(), None, est_ptr, sp)
+            decode(None, est_ptr)
         elif before_ef is None and resid_ptr is not None:   # EF update and estimate in one pass
-            _native.call("gc_psgd_decode_fused", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
-                         q_sum.data_ptr(), resid_ptr, est_ptr, sp)
+            decode(resid_ptr, est_ptr)
         else:
-            _native.call("gc_psgd_decode", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
-                         q_sum.data_ptr(), None, est_ptr, sp)
+            decode(None, est_ptr)
             if before_ef is not None:
                 before_ef()
             if resid_ptr is not None:
-                _native.call("gc_psgd_decode", bref, n, d, rows, cols, r, p_hat.data_ptr(), qw.data_ptr(),
-                             q_sum.data_ptr(), resid_ptr, None, sp)
-        self.last = {"p_hat": p_hat, "q_sum": q_sum, "seed_q": q, "status": status, "qw": qw}
+                decode(resid_ptr, None)
+        self.last = {"p_hat": p_hat, "q_sum": q_sum, "seed_q": q, "status": status, "qw": qw, "decode": decode}
         return warm
 
 

@@ -66,15 +66,22 @@ def test_psgd_golden_within_tolerance(name):
         assert _ledger(res, pipe.group.size) == st["ledger"]
 
 
+@pytest.mark.parametrize("nmse", [True, False])
 @pytest.mark.parametrize("n,d,rank", [(4, 1_000_000, 4), (2, 350_001, 1), (3, 100_000, 8), (8, 4096, 2),
-                                      (2, 50_000, 16)])
-def test_psgd_vs_oracle_multi_round(n, d, rank):
+                                      (2, 50_000, 16), (2, 60_001, 9), (3, 100_000, 20), (2, 100_003, 32),
+                                      (2, 200_000, 64)])
+def test_psgd_vs_oracle_multi_round(n, d, rank, nmse):
+    """Every rank the reference accepts (compressors.py:100-112): ranks outside the compiled set run
+    their factor passes in rank chunks (16s, 8, rest); nmse=True decodes estimate and EF update
+    separately, nmse=False in one pass."""
     import paper_2407_01378_b200 as gcb
     seeds = gcb.SeedSpec(31)
     grads = [[seeds.rng("grad-worker", r, w).standard_normal(d).astype(np.float32) for w in range(n)]
              for r in range(3)]
     outs = oracle_rounds("powersgd", dict(rank=rank), grads, 31)
-    pipe = gcb.make_pipeline(gcb.PowerSgdConfig(rank), n, d, seeds)
+    pipe = gcb.make_pipeline(gcb.PowerSgdConfig(rank), n, d, seeds, compute_nmse=nmse)
+    if rank in (20, 64):
+        assert pipe._engine.group.chunks == ([16, 4] if rank == 20 else [16, 16, 16, 16])
     for r in range(3):
         res = pipe.run_round(grads[r], r)
         assert_close_fp32(res.estimate.logical, outs[r]["estimate"], f"round {r}")
@@ -108,10 +115,11 @@ def test_psgd_mtp_ef_vs_oracle(n, d, rank):
         assert grp._mtp_ef_ok()
 
 
-def test_psgd_zero_gradients_complete_basis_and_redraw():
+@pytest.mark.parametrize("rank", [4, 20])
+def test_psgd_zero_gradients_complete_basis_and_redraw(rank):
     """All-zero gradients: MGS completes with canonical vectors; round 1's warm Q is zero and is redrawn."""
     import paper_2407_01378_b200 as gcb
-    n, d, rank = 2, 10_000, 4
+    n, d = 2, 10_000
     grads = [[np.zeros(d, np.float32) for _ in range(n)] for _ in range(2)]
     outs = oracle_rounds("powersgd", dict(rank=rank), grads, 41)
     pipe = gcb.make_pipeline(gcb.PowerSgdConfig(rank), n, d, gcb.SeedSpec(41))

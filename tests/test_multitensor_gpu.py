@@ -18,7 +18,7 @@ def _grads(n, D, rounds, seed):
 
 
 @pytest.mark.parametrize("nmse,mtp_ef", [(True, False), (False, False), (False, True)])
-@pytest.mark.parametrize("rank,warm", [(4, True), (2, False), (1, True)])
+@pytest.mark.parametrize("rank,warm", [(4, True), (2, False), (1, True), (12, True)])
 def test_powersgd_per_tensor_matches_reference(rank, warm, nmse, mtp_ef):
     """nmse False: ef_apply fused into the first pass of each tensor; mtp_ef: Q_w and the EF update
     in one pass (gc_psgd_mtp_ef, opt-in) for the batched groups whose shapes allow it."""
