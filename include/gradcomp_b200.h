@@ -305,6 +305,20 @@ int gc_psgd_mq(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, in
  * written over resid (when non-NULL) in the same pass; split-K partials in the workspace. */
 int gc_psgd_mq_fused(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
                      float *resid, const float *q, float *p, void *workspace, void *stream);
+/* TMA-fed tcgen05 P = M Q with ef_apply, and the previous round's EF update deferred into it
+ * (pipelines.py:348 with compressors.py:624-631).  With ef_p_hat / ef_q_workers NULL: resid holds
+ * the residuals r and corrected f32(g + r) is written over them (as gc_psgd_mq_fused).  With the
+ * previous round's factors: resid holds that round's corrected matrices c_prev, and the pass uses
+ * r = f32(c_prev - P_hat_prev Q_w_prev^T) (gc_psgd_decode's arithmetic, bit for bit) -- the
+ * decode then only writes the estimate (gc_psgd_decode with resid NULL), and a residual read in
+ * between materialises r with gc_psgd_decode(..., resid, NULL).  One tensor (row_offsets NULL),
+ * cols % 4 == 0, ld % 4 == 0, 16-byte aligned rows, d >= cols, rank 1..8 or 16:
+ * gc_psgd_mq_tma_supported; GC_ERR_UNSUPPORTED otherwise. */
+int gc_psgd_mq_tma_supported(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                             const void *grads, const void *resid);
+int gc_psgd_mq_deferred(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
+                        float *resid, const float *q, const float *ef_p_hat, const float *ef_q_workers, float *p,
+                        void *workspace, void *stream);
 /* Q_w = M_w^T P_hat (pipelines.py:354). */
 int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                 const float *p_hat, float *q, void *workspace, void *stream);
@@ -318,9 +332,13 @@ int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, i
 int gc_psgd_mtp_ef_supported(int64_t rows, int64_t cols, int32_t rank, int32_t rows_aligned);
 int gc_psgd_mtp_ef(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, float *resid,
                    const float *p_hat, float *q, void *stream);
-/* orthonormalize (compressors.py:555-588) for T tensors, rank <= 64: fp64 Gram-Schmidt (CGS2, the
- * c dot products of a column formed in one sweep) with the reference's canonical-basis completion;
- * status[t] = 1 if completion failed (DegenerateMatrixError).  workspace: T*rows*rank doubles. */
+/* orthonormalize (compressors.py:555-588) for T tensors, rank <= 64.  Ranks 1..8 and 16 first try
+ * the Cholesky-QR fast path (fp64 Gram of P over the whole GPU, R = chol(G) whose pivots are MGS's
+ * residual norms, P_hat = P R^-1) and keep it only when every pivot is far from the degeneracy
+ * floor and from cancellation; every other tensor runs fp64 Gram-Schmidt (CGS2, the c dot products
+ * of a column formed in one sweep) with the reference's canonical-basis completion; status[t] = 1
+ * if completion failed (DegenerateMatrixError).  workspace: gc_psgd_orth_workspace_bytes. */
+int64_t gc_psgd_orth_workspace_bytes(int32_t tensors, int64_t rows, int32_t rank);
 int gc_psgd_orthonormalize(int32_t tensors, int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace,
                            int32_t *status, void *stream);
 /* own_w = P_hat Q_w^T, resid_w -= own_w (resid holds the corrected matrix; NULL skips);

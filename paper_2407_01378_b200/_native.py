@@ -120,10 +120,13 @@ SIGNATURES = {
     "gc_psgd_vectorizable": (c_int, [I64, P, P, I64]),
     "gc_psgd_mq": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P]),
     "gc_psgd_mq_fused": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P, P, P]),
+    "gc_psgd_mq_tma_supported": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P]),
+    "gc_psgd_mq_deferred": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P, P, P, P, P]),
     "gc_psgd_mtp": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P, P]),
     "gc_psgd_mtp_ef_supported": (c_int, [I64, I64, I32, I32]),
     "gc_psgd_mtp_ef": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P]),
     "gc_psgd_orthonormalize": (c_int, [I32, I64, I32, P, P, P, P, P]),
+    "gc_psgd_orth_workspace_bytes": (I64, [I32, I64, I32]),
     "gc_psgd_decode": (c_int, [POINTER(PsgdBatch), I32, I64, I64, I64, I32, P, P, P, P, P, P]),
     "gc_psgd_decode_fused": (c_int, [POINTER(PsgdBatch), I32, I64, I64, I64, I32, P, P, P, P, P, P]),
     "gc_psgd_gram_workspace_bytes": (I64, [I32, I32]),

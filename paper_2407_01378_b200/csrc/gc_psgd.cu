@@ -233,10 +233,11 @@ __device__ void orth_dots(int64_t rows, int R, const double *a, int c, double *d
 }
 
 __global__ void __launch_bounds__(kOrthThreads) orth_kernel(int64_t rows, int R, const float *in, double *a,
-                                                            float *out, int *status) {
+                                                            float *out, int *status, const int *fast) {
   __shared__ double red[33];
   __shared__ double dots[kMaxOrthRank];
   __shared__ double wred[kOrthThreads / 32][kMaxOrthRank];
+  if (fast && fast[blockIdx.x]) return;   // the Cholesky path already wrote this tensor's P_hat
   {
     const int64_t t = blockIdx.x;
     in += t * rows * R;
@@ -295,6 +296,124 @@ __global__ void __launch_bounds__(kOrthThreads) orth_kernel(int64_t rows, int R,
     __syncthreads();
   }
   for (int64_t i = threadIdx.x; i < rows * R; i += kOrthThreads) out[i] = static_cast<float>(a[i]);
+}
+
+// Fast path of the orthonormalization for tall factors (rank <= 16).  In exact arithmetic the
+// reference's MGS (compressors.py:555-588) produces the Q factor of P = Q R with a positive
+// diagonal, and R is the Cholesky factor of the Gram matrix G = P^T P; column c's residual norm
+// after projection is R[c][c].  So: (A) G in fp64 from row slices spread over the GPU, (B) per
+// tensor the slices summed in a fixed order, R = chol(G) and R^-1, (C) P_hat = P R^-1 row by row.
+// (B) takes the fast path only when every pivot is far from the reference's degeneracy floor
+// (R[c][c] > 1e3 * floor) and from cancellation (R[c][c] > 1e-4 * |p_c|, so the fp64 result is
+// within ~1e-8 of MGS's); otherwise the tensor's flag stays 0 and orth_kernel (CGS2 with the
+// canonical completion) runs it.  One pass over P instead of 2 r + 2 single-CTA sweeps.
+constexpr int kOrthSlicesMax = 148;
+
+template <int R>
+__global__ void __launch_bounds__(256) tall_gram_kernel(int64_t rows, const float *p, double *partial, int slices) {
+  constexpr int NP = R * (R + 1) / 2;
+  __shared__ double red[8][NP];
+  const int t = blockIdx.y, sl = blockIdx.x;
+  p += static_cast<int64_t>(t) * rows * R;
+  double acc[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) acc[k] = 0.0;
+  for (int64_t i = static_cast<int64_t>(sl) * 256 + threadIdx.x; i < rows; i += static_cast<int64_t>(slices) * 256) {
+    double x[R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) x[a] = static_cast<double>(p[i * R + a]);
+    int k = 0;
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = a; b < R; ++b) acc[k++] += x[a] * x[b];
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < NP; k += 256) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w][k];
+    partial[(static_cast<int64_t>(t) * slices + sl) * NP + k] = v;
+  }
+}
+
+// one thread per tensor: G from the slices (fixed order), Cholesky, pivot checks, R^-1
+__global__ void orth_chol_kernel(int T, int R, int slices, const double *partial, double *rinv, int *fast) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int NP = R * (R + 1) / 2;
+  double g[16][16], r[16][16], ri[16][16];
+  for (int a = 0, k = 0; a < R; ++a)
+    for (int b = a; b < R; ++b, ++k) {
+      double v = 0.0;
+      for (int sl = 0; sl < slices; ++sl) v += partial[(static_cast<int64_t>(t) * slices + sl) * NP + k];
+      g[a][b] = v;
+      g[b][a] = v;
+    }
+  double fro2 = 0.0;
+  for (int a = 0; a < R; ++a) fro2 += g[a][a];
+  const double scale = sqrt(fro2) / fmax(1.0, sqrt(static_cast<double>(R)));
+  const double floor_ = fmax(scale * 1e-8, 1e-300);
+  bool ok = true;
+  for (int c = 0; c < R && ok; ++c) {
+    for (int p = 0; p < c; ++p) {
+      double v = g[p][c];
+      for (int k = 0; k < p; ++k) v -= r[k][p] * r[k][c];
+      r[p][c] = v / r[p][p];
+    }
+    double dd = g[c][c];
+    for (int k = 0; k < c; ++k) dd -= r[k][c] * r[k][c];
+    if (!(dd > 0.0)) {
+      ok = false;
+      break;
+    }
+    r[c][c] = sqrt(dd);
+    if (!(r[c][c] > 1e3 * floor_) || !(r[c][c] > 1e-4 * sqrt(g[c][c]))) ok = false;
+  }
+  if (ok) {   // upper-triangular inverse, column by column
+    for (int b = 0; b < R; ++b) {
+      for (int a = R - 1; a >= 0; --a) {
+        double v = a == b ? 1.0 : 0.0;
+        for (int k = a + 1; k <= b; ++k) v -= r[a][k] * ri[k][b];
+        ri[a][b] = a <= b ? v / r[a][a] : 0.0;
+      }
+    }
+    for (int a = 0; a < R; ++a)
+      for (int b = 0; b < R; ++b) rinv[(static_cast<int64_t>(t) * R + a) * R + b] = a <= b ? ri[a][b] : 0.0;
+  }
+  fast[t] = ok ? 1 : 0;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) orth_apply_kernel(int64_t rows, const float *p, const double *rinv,
+                                                         const int *fast, float *out) {
+  const int t = blockIdx.y;
+  if (!fast[t]) return;
+  __shared__ double ri[R * R];
+  for (int e = threadIdx.x; e < R * R; e += 256) ri[e] = rinv[static_cast<int64_t>(t) * R * R + e];
+  __syncthreads();
+  p += static_cast<int64_t>(t) * rows * R;
+  out += static_cast<int64_t>(t) * rows * R;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < rows;
+       i += static_cast<int64_t>(gridDim.x) * 256) {
+    double x[R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) x[a] = static_cast<double>(p[i * R + a]);
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      double y = 0.0;
+#pragma unroll
+      for (int a = 0; a <= b; ++a) y += x[a] * ri[a * R + b];
+      out[i * R + b] = static_cast<float>(y);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ vectorised kernels
@@ -575,7 +694,7 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
           for (int b = 0; b < R; ++b) pa[b] = ps[a * R + b];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            float v = pa[0] * qv[t][0];
+            float v = __fmul_rn(pa[0], qv[t][0]);   // no contraction into the subtraction below
 #pragma unroll
             for (int b = 1; b < R; ++b) v = fmaf(pa[b], qv[t][b], v);
             o4[t] = v;
@@ -605,7 +724,7 @@ __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d
       for (int b = 0; b < R; ++b) pa[b] = ps[a * R + b];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {   // fp32 FMAs, as the reference's fp32 p_hat @ q.T (K = r)
-        float v = pa[0] * qv[t][0];
+        float v = __fmul_rn(pa[0], qv[t][0]);   // no contraction into the subtraction below
 #pragma unroll
         for (int b = 1; b < R; ++b) v = fmaf(pa[b], qv[t][b], v);
         o4[t] = v;
@@ -911,6 +1030,37 @@ int gc_psgd_mq_fused(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t co
   return GC_OK;
 }
 
+int gc_psgd_mq_tma_supported(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                             const void *grads, const void *resid) {
+  if (b == nullptr || d < 1 || rows * cols < d) return 0;
+  return gc_psgd_mq_tma_supported_impl(b->tensors, b->workers, b->row_offsets, b->ld, d, rows, cols, rank, grads,
+                                       resid);
+}
+
+int gc_psgd_mq_deferred(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
+                        float *resid, const float *q, const float *ef_p_hat, const float *ef_q_workers, float *p,
+                        void *workspace, void *stream) {
+  if (int rc = check_batch(b)) return rc;
+  GC_REQUIRE(d >= 1 && rows * cols >= d && grads && q && p && workspace, "invalid argument");
+  GC_REQUIRE((ef_p_hat == nullptr) == (ef_q_workers == nullptr), "deferred EF needs both factors or neither");
+  GC_REQUIRE(ef_p_hat == nullptr || resid != nullptr, "deferred EF needs the residual buffer");
+  if (!gc_psgd_mq_tma_supported(b, d, rows, cols, rank, grads, resid)) {
+    gc_set_error("TMA P = M Q needs one tensor (no row offsets), cols % 4 == 0, ld % 4 == 0, 16-byte aligned "
+                 "rows, d >= cols and a compiled rank");
+    return GC_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int L = b->tensors * b->workers;
+  const int slabs = gc_psgd_mq_tma_launch(L, b->ld, d, rows, cols, rank, grads, resid, q, ef_p_hat, ef_q_workers,
+                                          static_cast<double *>(workspace), (cols + 1023) / 1024, st);
+  if (slabs < 0) return slabs;
+  const int64_t total = static_cast<int64_t>(L) * rows * rank;
+  mq_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(
+      L, slabs, rows, rank, static_cast<const double *>(workspace), p);
+  GC_LAUNCH_CHECK("mq_reduce_kernel");
+  return GC_OK;
+}
+
 int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                 const float *p_hat, float *q, void *workspace, void *stream) {
   if (int rc = check_batch(b)) return rc;
@@ -991,13 +1141,40 @@ int gc_psgd_mtp_ef(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols
   return GC_OK;
 }
 
+int64_t gc_psgd_orth_workspace_bytes(int32_t tensors, int64_t rows, int32_t rank) {
+  const int64_t np = static_cast<int64_t>(rank) * (rank + 1) / 2;
+  return 8 * (static_cast<int64_t>(tensors) * rows * rank + static_cast<int64_t>(tensors) * kOrthSlicesMax * np +
+              static_cast<int64_t>(tensors) * rank * rank) +
+         4 * static_cast<int64_t>(tensors) + 64;
+}
+
 int gc_psgd_orthonormalize(int32_t tensors, int64_t rows, int32_t rank, const float *p, float *p_hat, void *workspace,
                            int32_t *status, void *stream) {
   GC_REQUIRE(tensors >= 1 && tensors <= 65535 && rows >= rank && rank >= 1 && rank <= kMaxOrthRank && p && p_hat &&
                  workspace && status,
              "invalid argument");
-  orth_kernel<<<tensors, kOrthThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      rows, rank, p, static_cast<double *>(workspace), p_hat, status);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double *a = static_cast<double *>(workspace);
+  const int *fast = nullptr;
+  if (rank <= 8 || rank == 16) {   // Cholesky fast path (flags per tensor), CGS2 kernel for the rest
+    const int64_t np = static_cast<int64_t>(rank) * (rank + 1) / 2;
+    double *partial = a + static_cast<int64_t>(tensors) * rows * rank;
+    double *rinv = partial + static_cast<int64_t>(tensors) * kOrthSlicesMax * np;
+    int *flags = reinterpret_cast<int *>(rinv + static_cast<int64_t>(tensors) * rank * rank);
+    int64_t slices = (rows + 2047) / 2048;
+    if (slices > kOrthSlicesMax) slices = kOrthSlicesMax;
+    const int sl = static_cast<int>(slices);
+    const dim3 g2(sl, tensors);
+    GC_RANK_SWITCH(rank, ({ tall_gram_kernel<R><<<g2, 256, 0, st>>>(rows, p, partial, sl); }));
+    GC_LAUNCH_CHECK("tall_gram_kernel");
+    orth_chol_kernel<<<(tensors + 63) / 64, 64, 0, st>>>(tensors, rank, sl, partial, rinv, flags);
+    GC_LAUNCH_CHECK("orth_chol_kernel");
+    const dim3 g3(grid_cap((rows + 255) / 256 > 148 ? 148 : (rows + 255) / 256), tensors);
+    GC_RANK_SWITCH(rank, ({ orth_apply_kernel<R><<<g3, 256, 0, st>>>(rows, p, rinv, flags, p_hat); }));
+    GC_LAUNCH_CHECK("orth_apply_kernel");
+    fast = flags;
+  }
+  orth_kernel<<<tensors, kOrthThreads, 0, st>>>(rows, rank, p, a, p_hat, status, fast);
   GC_LAUNCH_CHECK("orth_kernel");
   return GC_OK;
 }
@@ -1047,8 +1224,14 @@ int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, do
              "invalid argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double *partial = static_cast<double *>(workspace);
-  gram_partial_kernel<<<dim3(tensors, kGramSlices), 256, 0, st>>>(cols, rank, q, partial);
-  GC_LAUNCH_CHECK("gram_partial_kernel");
+  if (rank <= 8 || rank == 16) {   // row-parallel: every thread sums all pairs of its rows
+    const dim3 g2(kGramSlices, tensors);
+    GC_RANK_SWITCH(rank, ({ tall_gram_kernel<R><<<g2, 256, 0, st>>>(cols, q, partial, kGramSlices); }));
+    GC_LAUNCH_CHECK("tall_gram_kernel");
+  } else {
+    gram_partial_kernel<<<dim3(tensors, kGramSlices), 256, 0, st>>>(cols, rank, q, partial);
+    GC_LAUNCH_CHECK("gram_partial_kernel");
+  }
   gram_reduce_kernel<<<tensors, 256, 0, st>>>(rank, partial, gram);
   GC_LAUNCH_CHECK("gram_reduce_kernel");
   return GC_OK;

@@ -1,0 +1,514 @@
+// PowerSGD P = M Q on tcgen05 with TMA-fed operands and the error-feedback update folded in
+// (single-matrix layout: worker w's matrix at w * ld, cols % 4 == 0, 16-byte aligned rows).
+//
+// Reference: P_w = M_w @ Q (pipelines.py:348), M_w = to_matrix(corrected_w) (compressors.py:530-548),
+// corrected_w = f32(g_w + r_w) (ef_apply, compressors.py:624-626), and the previous round's
+// r_w = f32(c_w - own_w), own_w = P_hat Q_w^T (pipelines.py:357-361, ef_update compressors.py:629-631).
+//
+// Deferred error feedback.  The previous round left its corrected matrix c_prev in the residual
+// buffer together with its factors (P_hat_prev, Q_w_prev) instead of materialising
+// r = c_prev - P_hat_prev Q_w_prev^T (that materialisation was a read-modify-write of M).  This
+// pass forms, per element, own = P_hat_prev[i,:] . Q_w_prev[j,:] in the decode kernel's fp32 order
+// (product, then FMAs), r = f32(c_prev - own), corrected = f32(g + r) -- the values the three-pass
+// schedule produces, bit for bit -- so a round moves g and c_prev in, corrected out (12 B per
+// element here), Mᵀ P_hat (4 B) and the estimate (4 B): 20 B per element instead of 28.
+//
+// B200 design.  One CTA (256 threads) per SM owns a 128-row band and a range of 32-column
+// chunks.  The control thread (thread 0) keeps a 3-stage ring full with TMA: per chunk a
+// 128 x 32 fp32 box of g and of the residual buffer (SWIZZLE_128B, i.e. already in the canonical
+// K-major UMMA layout) plus the chunk's 32 x r rows of Q (and of Q_w_prev) by 1-D bulk copies, all
+// on one mbarrier with expect-tx.  The producers (all 256 threads) turn the boxes into operands in
+// place: corrected c into the residual box -- the TMA store source and, as is, A_big (kind::tf32
+// reads the top 19 bits of an fp32 pattern: tf32(c) by truncation) -- and small = tf32(c - big)
+// over the consumed g box; Q^T split into big / small 16 x 32 B tiles.  Two 16 KB boxes per stage
+// let five stages (four chunks of loads in flight) share the SM.  The
+// control thread then issues D += A_big B_big + A_big B_small + A_small B_big (kind::tf32,
+// M = 128, N = 16) into TMEM, commits the stage's release, and TMA-stores the corrected box back
+// over the residual buffer.  Every 512 columns the fp32 TMEM partial is folded into fp64
+// registers (two accumulators alternate), as in gc_psgd_umma.cu.  A row that is only partly
+// inside d (the zero-padded tail of to_matrix) is left to a one-row fix-up kernel; rows past it
+// are zero padding.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "gc_internal.h"
+
+namespace {
+
+constexpr int kM = 128;        // UMMA M: rows per CTA
+constexpr int kN = 16;         // UMMA N: rank padded to 16
+constexpr int kKc = 32;        // columns per stage: one 128-byte swizzle atom of fp32
+constexpr int kThreads = 256;
+#ifndef GC_MQT_STAGES
+#define GC_MQT_STAGES 5
+#endif
+constexpr int kStages = GC_MQT_STAGES;
+constexpr int kGroup = 512 / kKc;          // chunks per TMEM partial before the fp64 fold
+constexpr int kTile = kM * kKc * 4;        // 16 KB
+constexpr int kBTile = kN * kKc * 4;       // 2 KB
+constexpr int kRaw = kKc * 16 * 4;         // 2 KB: 32 rows of Q (or Q_w_prev), rank <= 16
+// stage: G (g box -> small = tf32(c - tf32(c))) | C (residual box -> corrected c, which is also A_big:
+// kind::tf32 reads an fp32 pattern's top 19 bits, i.e. tf32(c) by truncation) | Bb | Bs | Qraw | Wraw
+constexpr int kOffG = 0, kOffC = kTile, kOffBb = 2 * kTile, kOffBs = 2 * kTile + kBTile,
+              kOffQ = 2 * kTile + 2 * kBTile, kOffW = 2 * kTile + 2 * kBTile + kRaw;
+constexpr int kStageBytes = 2 * kTile + 2 * kBTile + 2 * kRaw;
+constexpr int kPhBytes = kM * 16 * 4;      // P_hat_prev rows of the band, rank <= 16
+constexpr int kSmemBytes = kStages * kStageBytes + kPhBytes + 256 /*barriers*/ + 1024 /*alignment*/;
+
+__device__ __forceinline__ uint32_t sw128(int row, int chunk) {
+  return static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((kN >> 3) << 17) | ((kM >> 4) << 24);
+
+__device__ __forceinline__ void split3(float c, float &big, float &small) {
+  big = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);
+  small = __uint_as_float(__float_as_uint(c - big) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+struct TmaArgs {
+  int64_t d, rows, cols, rows_full;
+  const float *q;          // [cols][R] (one tensor)
+  const float *ef_ph;      // deferred EF: P_hat_prev [rows][R] or NULL
+  const float *ef_qw;      // deferred EF: Q_w_prev [L][cols][R]
+  double *partial;         // [L][splits][rows][R]
+  int splits;
+  int64_t chunks_per_split;
+  int has_resid;
+};
+
+// own = P_hat_prev[i,:] . Q_w_prev[j,:] exactly as decode_vec_kernel forms it (fp32 product then
+// FMAs in rank order), so r = f32(c_prev - own) is the residual the three-pass schedule stores
+template <int R>
+__device__ __forceinline__ float own_of(const float *pa, const float *qv) {
+  float v = __fmul_rn(pa[0], qv[0]);
+#pragma unroll
+  for (int b = 1; b < R; ++b) v = fmaf(pa[b], qv[b], v);
+  return v;
+}
+
+template <int R, bool DEF>
+__global__ void __launch_bounds__(kThreads, 1)
+    mq_tma_kernel(const __grid_constant__ CUtensorMap map_g, const __grid_constant__ CUtensorMap map_r,
+                  const __grid_constant__ TmaArgs a) {
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char *sm = smem_raw + (base - raw);
+  auto stage = [&](int s) { return base + static_cast<uint32_t>(s * kStageBytes); };
+  float *ph_s = reinterpret_cast<float *>(sm + kStages * kStageBytes);
+  const uint32_t bars = base + kStages * kStageBytes + kPhBytes;   // loaded[S], empty[S], full[S], acc[2]
+  auto loaded_bar = [&](int s) { return bars + 8 * s; };
+  auto empty_bar = [&](int s) { return bars + 8 * (kStages + s); };
+  auto full_bar = [&](int s) { return bars + 8 * (2 * kStages + s); };
+  auto acc_bar = [&](int x) { return bars + 8 * (3 * kStages + x); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + kStages * kStageBytes + kPhBytes + 8 * (3 * kStages + 2));
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int v = blockIdx.z;   // worker
+  const int split = blockIdx.y;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kM;
+  const int64_t nchunks_all = (a.cols + kKc - 1) / kKc;
+  const int64_t c_begin = split * a.chunks_per_split;
+  const int64_t c_end = min(nchunks_all, c_begin + a.chunks_per_split);
+  const int64_t nloc = c_end - c_begin;
+  const float *qw_prev = DEF ? a.ef_qw + static_cast<int64_t>(v) * a.cols * R : nullptr;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(loaded_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+      mbar_init(full_bar(s), kThreads);
+    }
+    mbar_init(acc_bar(0), 1);
+    mbar_init(acc_bar(1), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot)))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // B tiles: rows >= R stay zero (rank padded to N = 16)
+  for (int e = tid; e < kStages * 2 * kBTile / 16; e += kThreads) {
+    const int s = e / (2 * kBTile / 16), o = e - s * (2 * kBTile / 16);
+    *reinterpret_cast<uint4 *>(sm + s * kStageBytes + kOffBb + o * 16) = make_uint4(0, 0, 0, 0);
+  }
+  if (DEF) {   // the band's P_hat_prev rows (rows past d's matrix are never used)
+    for (int e = tid; e < kM * R; e += kThreads) {
+      const int64_t i = row0 + e / R;
+      ph_s[e] = i < a.rows ? a.ef_ph[i * R + e % R] : 0.0f;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  const uint32_t tx_bytes_box = static_cast<uint32_t>(kTile) * (a.has_resid ? 2u : 1u);
+  // control thread: fill stage s with chunk k
+  auto issue_load = [&](int64_t k) {
+    const int s = static_cast<int>(k % kStages);
+    const int64_t col0 = (c_begin + k) * kKc;
+    const int64_t ncol = min(static_cast<int64_t>(kKc), a.cols - col0);
+    const uint32_t qbytes = static_cast<uint32_t>(ncol * R * 4);
+    mbar_expect_tx(loaded_bar(s), tx_bytes_box + qbytes * (DEF ? 2u : 1u));
+    tma_load_3d(stage(s) + kOffG, &map_g, static_cast<int>(col0), static_cast<int>(row0), v, loaded_bar(s));
+    if (a.has_resid)
+      tma_load_3d(stage(s) + kOffC, &map_r, static_cast<int>(col0), static_cast<int>(row0), v, loaded_bar(s));
+    bulk_load(stage(s) + kOffQ, a.q + col0 * R, qbytes, loaded_bar(s));
+    if (DEF) bulk_load(stage(s) + kOffW, qw_prev + col0 * R, qbytes, loaded_bar(s));
+  };
+  if (tid == 0) {
+    for (int64_t k = 0; k < min(static_cast<int64_t>(kStages), nloc); ++k) issue_load(k);
+  }
+
+  double acc64[R];
+#pragma unroll
+  for (int b = 0; b < R; ++b) acc64[b] = 0.0;
+  auto fold_group = [&](int64_t gi) {
+    if (warp < 4) {
+      mbar_wait(acc_bar(static_cast<int>(gi & 1)), static_cast<uint32_t>((gi >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t x[16];
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>((gi & 1) * kN);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
+            "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc64[b] += static_cast<double>(__uint_as_float(x[b]));
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+  };
+
+  const int ch = tid & 7;   // the thread's 16-byte chunk of a row (4 columns): the same in every pass
+  for (int64_t k = 0; k < nloc; ++k) {
+    const int s = static_cast<int>(k % kStages);
+    const int64_t col0 = (c_begin + k) * kKc;
+    unsigned char *st = sm + s * kStageBytes;
+    const float *qraw = reinterpret_cast<const float *>(st + kOffQ);
+    mbar_wait(loaded_bar(s), static_cast<uint32_t>((k / kStages) & 1));
+    // this thread's 4 columns; columns past cols are zero in the boxes (TMA fill) and stay zero
+    const int64_t cbase = col0 + 4 * ch;
+    float wq[4][R];
+    if (DEF) {
+      const float *wraw = reinterpret_cast<const float *>(st + kOffW);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int b = 0; b < R; ++b) wq[e][b] = wraw[(4 * ch + e) * R + b];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int row = (tid >> 3) + 32 * u;
+      const uint32_t off = sw128(row, ch);
+      float4 gv = *reinterpret_cast<const float4 *>(st + kOffG + off);
+      float4 c = gv;
+      if (a.has_resid) {
+        float4 rv = *reinterpret_cast<const float4 *>(st + kOffC + off);
+        if (DEF) {
+          float pa[R];
+#pragma unroll
+          for (int b = 0; b < R; ++b) pa[b] = ph_s[row * R + b];
+          const bool live = row0 + row < a.rows_full;   // the partial row is the fix-up kernel's
+          rv.x = live && cbase + 0 < a.cols ? rv.x - own_of<R>(pa, wq[0]) : 0.0f;
+          rv.y = live && cbase + 1 < a.cols ? rv.y - own_of<R>(pa, wq[1]) : 0.0f;
+          rv.z = live && cbase + 2 < a.cols ? rv.z - own_of<R>(pa, wq[2]) : 0.0f;
+          rv.w = live && cbase + 3 < a.cols ? rv.w - own_of<R>(pa, wq[3]) : 0.0f;
+        }
+        c.x = gv.x + rv.x;
+        c.y = gv.y + rv.y;
+        c.z = gv.z + rv.z;
+        c.w = gv.w + rv.w;
+      }
+      float4 hb, hs;
+      split3(c.x, hb.x, hs.x);
+      split3(c.y, hb.y, hs.y);
+      split3(c.z, hb.z, hs.z);
+      split3(c.w, hb.w, hs.w);
+      *reinterpret_cast<float4 *>(st + kOffC + off) = c;    // A_big (truncated by the MMA) and the store source
+      *reinterpret_cast<float4 *>(st + kOffG + off) = hs;   // A_small over the consumed g box
+    }
+    if (tid < R * 8) {   // B = Q^T of the chunk: row n (< R), 4 columns per thread
+      const int n = tid >> 3;
+      float t[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) t[e] = cbase + e < a.cols ? qraw[(4 * ch + e) * R + n] : 0.0f;
+      float4 hb, hs;
+      split3(t[0], hb.x, hs.x);
+      split3(t[1], hb.y, hs.y);
+      split3(t[2], hb.z, hs.z);
+      split3(t[3], hb.w, hs.w);
+      const uint32_t off = sw128(n, ch);
+      *reinterpret_cast<float4 *>(st + kOffBb + off) = hb;
+      *reinterpret_cast<float4 *>(st + kOffBs + off) = hs;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full_bar(s)) : "memory");
+    const int64_t gi = k / kGroup;
+    if (tid == 0) {
+      mbar_wait(full_bar(s), static_cast<uint32_t>((k / kStages) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dcol = tmem + static_cast<uint32_t>((gi & 1) * kN);
+#pragma unroll
+      for (int kk = 0; kk < kKc / 8; ++kk) {
+        const uint64_t ab = sdesc(stage(s) + kOffC + 32 * kk), as = sdesc(stage(s) + kOffG + 32 * kk);
+        const uint64_t bb = sdesc(stage(s) + kOffBb + 32 * kk), bs = sdesc(stage(s) + kOffBs + 32 * kk);
+        const uint32_t accum = (k % kGroup != 0 || kk != 0) ? 1u : 0u;
+        umma_tf32(dcol, as, bb, accum);
+        umma_tf32(dcol, ab, bs, 1u);
+        umma_tf32(dcol, ab, bb, 1u);
+      }
+      umma_commit(empty_bar(s));
+      if (k % kGroup == kGroup - 1 || k == nloc - 1) umma_commit(acc_bar(static_cast<int>(gi & 1)));
+      if (a.has_resid) {   // corrected box back over the residual buffer (clipped to the map)
+        tma_store_3d(&map_r, stage(s) + kOffC, static_cast<int>(col0), static_cast<int>(row0), v);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      // refill the stage of chunk k - 1 with chunk k - 1 + S once its MMAs and store are done
+      if (k >= 1 && k - 1 + kStages < nloc) {
+        const int sp = static_cast<int>((k - 1) % kStages);
+        mbar_wait(empty_bar(sp), static_cast<uint32_t>(((k - 1) / kStages) & 1));
+        if (a.has_resid) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        issue_load(k - 1 + kStages);
+      }
+    }
+    if (k % kGroup == 0 && gi >= 1) fold_group(gi - 1);
+  }
+  if (nloc > 0) fold_group((nloc - 1) / kGroup);
+  if (tid == 0 && a.has_resid) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+
+  if (warp < 4) {
+    const int64_t grow = row0 + warp * 32 + lane;
+    if (grow < a.rows) {
+#pragma unroll
+      for (int b = 0; b < R; ++b)
+        a.partial[((static_cast<int64_t>(v) * a.splits + split) * a.rows + grow) * R + b] = acc64[b];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+}
+
+// The row of the matrix that is only partly inside d (to_matrix's zero padding starts in it):
+// corrected values written, P row summed in fp64 (split 0; the other splits' partials zeroed).
+template <int R, bool DEF>
+__global__ void __launch_bounds__(256) mq_tail_row_kernel(const float *g, float *resid, int64_t ld, TmaArgs a) {
+  __shared__ double red[8][R];
+  const int v = blockIdx.x;
+  const int64_t i = a.rows_full;
+  const int64_t n_valid = a.d - i * a.cols;
+  const float *gw = g + v * ld + i * a.cols;
+  float *rw = resid ? resid + v * ld + i * a.cols : nullptr;
+  const float *qw_prev = DEF ? a.ef_qw + static_cast<int64_t>(v) * a.cols * R : nullptr;
+  float pa[R];
+  if (DEF) {
+#pragma unroll
+    for (int b = 0; b < R; ++b) pa[b] = a.ef_ph[i * R + b];
+  }
+  double acc[R];
+#pragma unroll
+  for (int b = 0; b < R; ++b) acc[b] = 0.0;
+  for (int64_t j = threadIdx.x; j < n_valid; j += 256) {
+    float c = gw[j];
+    if (rw) {
+      float r = rw[j];
+      if (DEF) {
+        float qv[R];
+#pragma unroll
+        for (int b = 0; b < R; ++b) qv[b] = qw_prev[j * R + b];
+        r = r - own_of<R>(pa, qv);
+      }
+      c = c + r;
+      rw[j] = c;
+    }
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc[b] += static_cast<double>(c) * static_cast<double>(a.q[j * R + b]);
+  }
+#pragma unroll
+  for (int b = 0; b < R; ++b) {
+    double x = acc[b];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][b] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double x = 0.0;
+    for (int w = 0; w < 8; ++w) x += red[w][threadIdx.x];
+    for (int s = 0; s < a.splits; ++s)
+      a.partial[((static_cast<int64_t>(v) * a.splits + s) * a.rows + i) * R + threadIdx.x] = s == 0 ? x : 0.0;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// [L][rows_full][cols] fp32 view of worker rows at base + w * ld, 32 x 128 boxes, SWIZZLE_128B
+bool make_map(CUtensorMap *m, const float *base, int64_t L, int64_t rows_full, int64_t cols, int64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows_full), static_cast<cuuint64_t>(L)};
+  // one worker: the worker stride is never used, any multiple of 16 bytes will do
+  const int64_t ld_map = L == 1 ? (ld + 3) / 4 * 4 : ld;
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols * 4), static_cast<cuuint64_t>(ld_map * 4)};
+  cuuint32_t box[3] = {kKc, kM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int grid_cap(int64_t g) { return static_cast<int>(g < 1 ? 1 : (g > 65535 ? 65535 : g)); }
+
+}  // namespace
+
+int gc_psgd_mq_tma_supported_impl(int32_t tensors, int32_t workers, const int64_t *row_offsets, int64_t ld, int64_t d,
+                                  int64_t rows, int64_t cols, int32_t rank, const void *grads, const void *resid) {
+  if (tensors != 1 || row_offsets != nullptr) return 0;
+  if (cols % 4 != 0 || (workers > 1 && ld % 4 != 0) || cols > (int64_t{1} << 31) - 1 ||
+      rows > (int64_t{1} << 31) - 1)
+    return 0;
+  if (d / cols < 1) return 0;
+  if ((reinterpret_cast<uintptr_t>(grads) | reinterpret_cast<uintptr_t>(resid)) & 15) return 0;
+  switch (rank) {
+    case 1: case 2: case 3: case 4: case 5: case 6: case 7: case 8: case 16: break;
+    default: return 0;
+  }
+  return encode_fn() != nullptr ? 1 : 0;
+}
+
+// TMA-fed tcgen05 P = M Q with ef_apply (and, with ef_ph / ef_qw, the previous round's deferred
+// EF update).  fp64 split-K partials partial[w][split][row][R]; returns the split count or a
+// negative status.
+int gc_psgd_mq_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank,
+                          const float *grads, float *resid, const float *q, const float *ef_ph, const float *ef_qw,
+                          double *partial, int64_t max_splits, cudaStream_t st) {
+  const int64_t rows_full = d / cols;
+  const int64_t row_blocks = (rows + kM - 1) / kM;
+  const int64_t nchunks = (cols + kKc - 1) / kKc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t splits = sms / (row_blocks * L);
+  if (splits > max_splits) splits = max_splits;
+  if (splits < 1) splits = 1;
+  const int64_t per = (nchunks + splits - 1) / splits;
+  splits = (nchunks + per - 1) / per;
+  CUtensorMap mg, mr;
+  std::memset(&mr, 0, sizeof(mr));
+  if (!make_map(&mg, grads, L, rows_full, cols, ld) || (resid && !make_map(&mr, resid, L, rows_full, cols, ld))) {
+    gc_set_error("cuTensorMapEncodeTiled failed for the P = M Q operands");
+    return GC_ERR_CUDA;
+  }
+  TmaArgs a{};
+  a.d = d;
+  a.rows = rows;
+  a.cols = cols;
+  a.rows_full = rows_full;
+  a.q = q;
+  a.ef_ph = ef_ph;
+  a.ef_qw = ef_qw;
+  a.partial = partial;
+  a.splits = static_cast<int>(splits);
+  a.chunks_per_split = per;
+  a.has_resid = resid != nullptr;
+  const bool def = resid != nullptr && ef_ph != nullptr && ef_qw != nullptr;
+  const dim3 grid(grid_cap(row_blocks), static_cast<unsigned>(splits), static_cast<unsigned>(L));
+  const bool tail = rows_full < rows && d > rows_full * cols;
+#define GC_TMA_LAUNCH(RR, DD)                                                                              \
+  cudaFuncSetAttribute(mq_tma_kernel<RR, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);    \
+  mq_tma_kernel<RR, DD><<<grid, kThreads, kSmemBytes, st>>>(mg, mr, a);                                    \
+  if (tail) mq_tail_row_kernel<RR, DD><<<L, 256, 0, st>>>(grads, resid, ld, a);
+#define GC_TMA_CASE(RR)        \
+  case RR:                     \
+    if (def) {                 \
+      GC_TMA_LAUNCH(RR, true)  \
+    } else {                   \
+      GC_TMA_LAUNCH(RR, false) \
+    }                          \
+    break;
+  switch (rank) {
+    GC_TMA_CASE(1) GC_TMA_CASE(2) GC_TMA_CASE(3) GC_TMA_CASE(4) GC_TMA_CASE(5) GC_TMA_CASE(6)
+    GC_TMA_CASE(7) GC_TMA_CASE(8) GC_TMA_CASE(16)
+    default:
+      gc_set_error("rank must be 1..8 or 16");
+      return GC_ERR_UNSUPPORTED;
+  }
+#undef GC_TMA_CASE
+#undef GC_TMA_LAUNCH
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    gc_set_error(std::string("mq_tma_kernel: ") + cudaGetErrorString(e));
+    return GC_ERR_CUDA;
+  }
+  return static_cast<int>(splits);
+}

@@ -370,7 +370,7 @@ __global__ void range_consensus_kernel(int L, int64_t nb, const float *in, float
   }
 }
 
-constexpr int kSignWordsPerThread = 8;   // one PCG jump amortised over 8 words (128 steps)
+constexpr int kSignWordsPerThread = 64;   // one PCG jump amortised over 64 words (1024 steps)
 
 __global__ void signs_kernel(gc_pcg64 stream, int64_t count, uint32_t *bits) {
   // Sign i = top bit of u32 word i; u32 words are the low then high half of each next64 output
@@ -383,9 +383,10 @@ __global__ void signs_kernel(gc_pcg64 stream, int64_t count, uint32_t *bits) {
     gc::Pcg g;
     g.load(stream);
     g.jump(static_cast<uint64_t>(t) * kSignWordsPerThread * 16);
-    uint32_t out[kSignWordsPerThread];
-#pragma unroll
-    for (int k = 0; k < kSignWordsPerThread; ++k) {
+    const int64_t w0 = t * kSignWordsPerThread;
+    const int nw = static_cast<int>(min(static_cast<int64_t>(kSignWordsPerThread), words - w0));
+#pragma unroll 2
+    for (int k = 0; k < nw; ++k) {
       uint32_t word = 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -393,12 +394,8 @@ __global__ void signs_kernel(gc_pcg64 stream, int64_t count, uint32_t *bits) {
         word |= static_cast<uint32_t>((u >> 31) & 1u) << (2 * j);
         word |= static_cast<uint32_t>((u >> 63) & 1u) << (2 * j + 1);
       }
-      out[k] = word;
+      bits[w0 + k] = word;
     }
-    const int64_t w0 = t * kSignWordsPerThread;
-#pragma unroll
-    for (int k = 0; k < kSignWordsPerThread; ++k)
-      if (w0 + k < words) bits[w0 + k] = out[k];
   }
 }
 

@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kWarps * 32) rank_decode_kernel(const __grid_c
   if (!warp_run(a, l, t_lo, t_hi)) return;
   const double levels = static_cast<double>((1 << a.q) - 2);
   const double nd = static_cast<double>(a.n);
-  const float nf = static_cast<float>(a.n);
+  const gc::DivN dn(a.n);   // / n: an exact reciprocal product for power-of-two n
   for (int64_t t = t_lo; t < t_hi; ++t) {
     const int64_t t0 = t * kTileN;
     const uint32_t sw = a.signs[(t0 >> 5) + lane];
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(kWarps * 32) rank_decode_kernel(const __grid_c
     for (int j = 0; j < 32; ++j) {
       const int64_t i = t0 + 32 * j + lane;
       // rht_inverse (transforms.py:120-126) then / n (pipelines.py:308-311)
-      const float f = static_cast<float>(apply_sign(v[j] * a.scale, (sign_col >> j) & 1u)) / nf;
+      const float f = dn(static_cast<float>(apply_sign(v[j] * a.scale, (sign_col >> j) & 1u)));
       if (i < a.dim) __stcs(a.est + i, f);
     }
     __syncwarp();

@@ -164,9 +164,14 @@ def exchange_sums(send: torch.Tensor, comm: Comm, n: int, active: int, slice_len
     recv = recv.reshape(n, slice_len)
     s0 = comm.rank * slice_len
     my_len = max(0, min(slice_len, active - s0))
-    sums = torch.zeros(slice_len, dtype=out_dtype, device=send.device)
-    if my_len:
-        fold_fn(recv, my_len, s0, sums)
+    if n == 1 and out_dtype == recv.dtype:   # one worker: its codes are the sums (tail already zero)
+        sums = recv[0]
+    else:
+        sums = torch.empty(slice_len, dtype=out_dtype, device=send.device)
+        if my_len < slice_len:
+            sums[my_len:].zero_()
+        if my_len:
+            fold_fn(recv, my_len, s0, sums)
     if nibble:
         return _nibbles(comm.all_gather_rows(_nibbles(sums.reshape(1, -1), True), phase), False).reshape(-1)
     return comm.all_gather_rows(sums.reshape(1, -1), phase).reshape(-1)
@@ -252,11 +257,14 @@ class DistributedGradientPipeline:
     def residuals(self):
         if self._res is None:
             return None
+        self._engine.sync_residuals(self._res)
         h = self._res.cpu().numpy()
         return [h[i].copy() for i in range(self.L)]
 
     @property
     def residuals_tensor(self):
+        if self._res is not None:
+            self._engine.sync_residuals(self._res)
         return self._res
 
     @property
@@ -283,6 +291,7 @@ class DistributedGradientPipeline:
         diagnostic's cost).  Taken before the round overwrites the residuals."""
         c = g.double()
         if self._res is not None:
+            self._engine.sync_residuals(self._res)
             c += self._res.double()
         total = c.sum(0)
         self.comm.all_reduce(total, dist.ReduceOp.SUM)
@@ -360,6 +369,12 @@ class _Base:
         e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         self.kernel_events.append(e)
         return e
+
+    def sync_residuals(self, res):
+        """Materialise an EF update deferred into the next round (PowerSGD)."""
+
+    def drop_deferred(self):
+        pass
 
 
 class _Thc(_Base):
@@ -625,6 +640,14 @@ class _PowerSgd(_Base):
     def warm(self):
         return None if self.grp is None or self.grp.warm is None else self.grp.warm[0]
 
+    def sync_residuals(self, res):
+        if self.grp is not None:
+            self.grp.materialize(_ptr(res))
+
+    def drop_deferred(self):
+        if self.grp is not None:
+            self.grp.pending = None
+
     def _fold(self, kind, x, m):
         """Gather every rank's factor rows, then fold them in the reference ring order."""
         n = self.n
@@ -637,6 +660,22 @@ class _PowerSgd(_Base):
         L, n, d = self.L, self.n, self.dim
         sp = _sp()
         est = torch.empty(d, dtype=torch.float32, device=self.dev)
+        grp = self.grp
+        if grp is not None and res is not None and g.stride(0) == res.stride(0):
+            # ef_apply (and the previous round's deferred EF update) fused into P = M Q when the
+            # TMA pass takes this layout (pipelines.py:338-368 with ef_apply / ef_update)
+            vec = bool(_native.lib().gc_psgd_vectorizable(grp.cols, g.data_ptr(), res.data_ptr(), g.stride(0)))
+            grp.set_ld(g.stride(0), vec)
+            if vec and _native.lib().gc_psgd_mq_tma_supported(ctypes.byref(grp.batch), d, grp.rows, grp.cols,
+                                                              grp.rank, g.data_ptr(), res.data_ptr()):
+                grp.run(res.data_ptr(), res.data_ptr(), est.data_ptr(), r, grads_ptr=g.data_ptr(), vec=True,
+                        fold=self._fold)
+                self.launches += 6
+                ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
+                ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)
+                return est, 32.0 * grp.rank * (grp.rows + grp.cols), _simple_stats(None)
+        if grp is not None:
+            grp.materialize(_ptr(res))
         if res is not None:
             _native.call("gc_ef_apply", L, d, g.data_ptr(), res.data_ptr(), g.stride(0), res.data_ptr(),
                          res.stride(0), sp)
@@ -648,7 +687,6 @@ class _PowerSgd(_Base):
                 _native.call("gc_fill_zero", res.data_ptr(), res.numel() * 4, sp)
             ledger.charge_ring("dense-bypass", n, d, 32)
             return est, 32.0 * d, _simple_stats(None)
-        grp = self.grp
         vec = bool(_native.lib().gc_psgd_vectorizable(grp.cols, c.data_ptr(), est.data_ptr(), c.stride(0)))
         grp.set_ld(c.stride(0), vec)
         grp.run(c.data_ptr(), _ptr(res), est.data_ptr(), r, vec=vec, fold=self._fold)

@@ -125,11 +125,13 @@ class GradientPipeline:
     def residuals(self):
         if self._res is None:
             return None
+        self._engine.sync_residuals(self._res)
         host = self._res.cpu().numpy()
         return [host[i].copy() for i in range(self.group.size)]
 
     @residuals.setter
     def residuals(self, value):
+        self._engine.drop_deferred()
         if value is None:
             self._res = None
             self.error_feedback = False
@@ -143,6 +145,8 @@ class GradientPipeline:
 
     @property
     def residuals_tensor(self) -> torch.Tensor | None:
+        if self._res is not None:
+            self._engine.sync_residuals(self._res)
         return self._res
 
     @property

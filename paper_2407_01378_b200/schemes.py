@@ -83,6 +83,12 @@ class Engine:
     def warm_q(self):
         return None
 
+    def sync_residuals(self, res):
+        """Materialise any error-feedback update the engine deferred into the next round (PowerSGD)."""
+
+    def drop_deferred(self):
+        """Forget a deferred EF update (the caller replaced the residual buffer)."""
+
     def _nmse(self, grads, res, est, acc):
         _native.call("gc_nmse_accumulate", self.n, self.dim, grads.data_ptr(), _ptr(res) or None,
                      grads.stride(0), est.data_ptr(), acc.data_ptr(), _sp())
@@ -518,7 +524,8 @@ class PowerSgdGroup:
         self.batch = _native.PsgdBatch(T, L, _ptr(row_offsets), ld, _ptr(est_offsets), 0, 0)
         ws = int(_native.lib().gc_psgd_workspace_bytes(T * L, self.rows, self.cols, self.rank))
         self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
-        self.mgs_ws = torch.empty(T * self.rows * self.rank, dtype=torch.float64, device=device)
+        self.mgs_ws = torch.empty(int(_native.lib().gc_psgd_orth_workspace_bytes(T, self.rows, self.rank)),
+                                  dtype=torch.uint8, device=device)
         self.gram_ws = torch.empty(int(_native.lib().gc_psgd_gram_workspace_bytes(T, self.rank)) // 8,
                                    dtype=torch.float64, device=device)
         self.warm = None          # [T][cols][r]
@@ -526,6 +533,10 @@ class PowerSgdGroup:
         self._gram_host = None    # pinned [T][r][r]: Gram of the warm Q, filled behind an event
         self._pending_gram = None
         self._bufs = {}           # per-round device buffers, allocated once (no allocator traffic)
+        # deferred EF: (residual buffer ptr, P_hat, Q_w) of the last round when that buffer still holds
+        # the round's corrected matrices (r = c - P_hat Q_w^T not yet materialised, see materialize)
+        self.pending = None
+        self.defer = os.environ.get("GC_PSGD_DEFER", "1") != "0"
 
     def _buf(self, name, shape, dtype=torch.float32):
         b = self._bufs.get(name)
@@ -586,6 +597,19 @@ class PowerSgdGroup:
         (pipelines.py:341-346, compressors.py:591-603)."""
         return seed_q_groups([self], round_index)[0]
 
+    def materialize(self, resid_ptr):
+        """Write the deferred residuals r = c - P_hat Q_w^T (pipelines.py:357-361, ef_update) into the
+        buffer that holds the last round's corrected matrices -- before anything but the next round's
+        TMA P = M Q pass reads them.  A no-op when nothing is deferred."""
+        if self.pending is None:
+            return
+        rp, ph, qw = self.pending
+        self.pending = None
+        if resid_ptr is None or rp != resid_ptr:   # the caller replaced the EF state
+            return
+        _native.call("gc_psgd_decode", ctypes.byref(self.batch), self.n, self.d, self.rows, self.cols, self.rank,
+                     ph.data_ptr(), qw.data_ptr(), qw.data_ptr(), resid_ptr, None, _sp())
+
     def _mtp_ef_ok(self):
         # opt-in (GC_PSGD_MTP_EF=1): the fused pass moves exactly the algorithmic bytes but its
         # 128-byte column-strip segments run at ~1.7 TB/s, slower than mtp + decode (DESIGN.md)
@@ -623,9 +647,22 @@ class PowerSgdGroup:
             return out
 
         p = self._buf("p", (T * L, rows, r))
-        # P = M Q on tcgen05: float4 producer for aligned rows, masked scalars otherwise
+        # P = M Q on tcgen05: TMA-fed when the layout allows it (then the previous round's EF update
+        # rides along: deferred EF), float4 producer for aligned rows, masked scalars otherwise
         umma = vec or umma_unaligned()
+        rp = ef_resid_ptr if ef_resid_ptr is not None else resid_ptr
+        tma = (not multi and grads_ptr is not None and rp is not None and
+               bool(_native.lib().gc_psgd_mq_tma_supported(bref, d, rows, cols, r, grads_ptr, rp)))
+        if self.pending is not None and not (tma and self.pending[0] == rp):
+            self.materialize(rp)
+        if tma:
+            pend, self.pending = self.pending, None
+            _native.call("gc_psgd_mq_deferred", bref, d, rows, cols, r, grads_ptr, rp, q.data_ptr(),
+                         pend[1].data_ptr() if pend else None, pend[2].data_ptr() if pend else None, p.data_ptr(),
+                         self.ws.data_ptr(), sp)
         for k, (c0, rc) in enumerate(spans):
+            if tma:
+                break
             q_c = cols_of(q, c0, rc, f"q_c{k}")
             p_c = self._buf(f"p_c{k}", (T * L, rows, rc)) if multi else p
             if umma and k == 0 and ef_resid_ptr is not None:
@@ -691,6 +728,13 @@ class PowerSgdGroup:
 
         if mtp_ef:
             decode(None, est_ptr)
+        elif tma and self.defer and resid_ptr is not None and rp == resid_ptr:
+            # deferred EF: the estimate only; r = c - P_hat Q_w^T is folded into the next round's
+            # P = M Q pass (or materialised when the residuals are read first)
+            decode(None, est_ptr)
+            if before_ef is not None:
+                before_ef()
+            self.pending = (rp, p_hat, qw)
         elif before_ef is None and resid_ptr is not None:   # EF update and estimate in one pass
             decode(resid_ptr, est_ptr)
         else:
@@ -714,6 +758,14 @@ class PowerSgdEngine(Engine):
 
     def warm_q(self):
         return None if self.group is None or self.group.warm is None else self.group.warm[0]
+
+    def sync_residuals(self, res):
+        if self.group is not None:
+            self.group.materialize(_ptr(res))
+
+    def drop_deferred(self):
+        if self.group is not None:
+            self.group.pending = None
 
     def _fold(self, kind, x, m):
         n = self.n
@@ -750,6 +802,7 @@ class PowerSgdEngine(Engine):
         if fuse_ef:   # ef_apply fused into P = M Q
             c, gptr = res, grads.data_ptr()
         else:
+            grp.materialize(_ptr(res))
             if res is not None:
                 _native.call("gc_ef_apply", n, d, grads.data_ptr(), res.data_ptr(), grads.stride(0), res.data_ptr(),
                              res.stride(0), sp)
@@ -767,7 +820,7 @@ class PowerSgdEngine(Engine):
             ev[1].record()
         self.launches += 10
         if self.capture:
-            self.last = {k: (v[0] if k not in ("status", "qw") else v) for k, v in grp.last.items()}
+            self.last = {k: (v[0] if k not in ("status", "qw") else v) for k, v in grp.last.items() if not callable(v)}
         ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
         ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)
         return est, 32.0 * grp.rank * (grp.rows + grp.cols), _simple_stats(acc)

@@ -1,0 +1,152 @@
+"""PowerSGD with the TMA-fed tcgen05 P = M Q pass and the deferred error-feedback update.
+
+The deferred schedule keeps the corrected matrices in the residual buffer and folds
+r = c - P_hat Q_w^T (pipelines.py:357-361) into the next round's P = M Q pass
+(gc_psgd_mq_deferred).  It must give the same rounds, bit for bit, as the eager schedule
+(decode writes r each round) and match the reference within the fp32 contract (1e-5)."""
+import numpy as np
+import pytest
+import torch
+
+from tests.gpu_util import needs_gpu, oracle_rounds
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+
+def _dims(step=4):
+    """(d with a partly filled last matrix row, d filling whole rows) whose cols % 4 == 0 (the TMA
+    pass's row pitch); d % 4 == 0 too with step 4 (the worker pitch of an [n, d] batch)."""
+    from paper_2407_01378_b200.configs import matrix_shape_for
+    partial = full = None
+    for d in range(40_000, 90_000, step):
+        rows, cols = matrix_shape_for(d)
+        if cols % 4:
+            continue
+        if partial is None and d % cols and d // cols >= rows - 1:
+            partial = d
+        if full is None and d % cols == 0:
+            full = d
+        if partial and full:
+            return partial, full
+    raise AssertionError("no suitable dims")
+
+
+def _grads(n, d, rounds, seed):
+    rng = np.random.default_rng(seed)
+    return [[rng.standard_normal(d).astype(np.float32) for _ in range(n)] for _ in range(rounds)]
+
+
+def _run(n, d, rank, grads, defer, read_every=False, seed=5):
+    import paper_2407_01378_b200 as gcb
+    pipe = gcb.make_pipeline(gcb.PowerSgdConfig(rank), n, d, gcb.SeedSpec(seed), compute_nmse=False)
+    grp = pipe._engine.group
+    grp.defer = defer
+    ests, res = [], []
+    for r, g in enumerate(grads):
+        out = pipe.run_round(torch.from_numpy(np.stack(g)).cuda(), r)
+        ests.append(out.estimate.logical.copy())
+        if read_every:
+            res.append(np.stack(pipe.residuals))
+    return pipe, ests, res
+
+
+@pytest.mark.parametrize("rank", [1, 4, 8, 16])
+@pytest.mark.parametrize("which", ["partial", "full"])
+def test_deferred_equals_eager_bitwise(rank, which):
+    d = dict(zip(("partial", "full"), _dims()))[which]
+    n = 3
+    grads = _grads(n, d, 4, 11)
+    p0, e0, _ = _run(n, d, rank, grads, defer=False)
+    p1, e1, _ = _run(n, d, rank, grads, defer=True)
+    assert p1._engine.group.pending is not None, "the deferred schedule did not engage"
+    for r in range(4):
+        assert np.array_equal(e0[r], e1[r]), r
+    assert np.array_equal(np.stack(p0.residuals), np.stack(p1.residuals))
+    assert p1._engine.group.pending is None   # reading the residuals materialised them
+
+
+def test_deferred_one_worker_odd_dim():
+    """One worker (the per-rank layout): the TMA pass needs no worker pitch, so d % 4 != 0 works."""
+    d, _ = _dims(step=7)
+    assert d % 4
+    grads = _grads(1, d, 3, 14)
+    p0, e0, _ = _run(1, d, 4, grads, defer=False)
+    p1, e1, _ = _run(1, d, 4, grads, defer=True)
+    assert p1._engine.group.pending is not None
+    for r in range(3):
+        assert np.array_equal(e0[r], e1[r]), r
+    assert np.array_equal(np.stack(p0.residuals), np.stack(p1.residuals))
+
+
+@pytest.mark.parametrize("rank", [2, 4])
+def test_deferred_matches_reference(rank):
+    d, _ = _dims()
+    n, seed = 2, 5
+    grads = _grads(n, d, 3, 12)
+    pipe, ests, _ = _run(n, d, rank, grads, defer=True, seed=seed)
+    outs = oracle_rounds("powersgd", dict(rank=rank), grads, seed)
+    for r in range(3):
+        ref = outs[r]["estimate"].astype(np.float64)
+        assert np.max(np.abs(ests[r] - ref)) <= 1e-5 * np.max(np.abs(ref)), r
+    res_ref = np.stack(outs[2]["residuals"])
+    assert np.max(np.abs(np.stack(pipe.residuals) - res_ref)) <= 1e-5 * np.max(np.abs(res_ref))
+
+
+def test_residual_reads_and_writes_between_rounds():
+    """Reading the residuals mid-run materialises them; assigning new residuals drops the deferred
+    update (the reference's _one_shot pattern, pipelines.py:436-439)."""
+    d, _ = _dims()
+    n = 2
+    grads = _grads(n, d, 3, 13)
+    _, e_eager, r_eager = _run(n, d, 4, grads, defer=False, read_every=True)
+    _, e_def, r_def = _run(n, d, 4, grads, defer=True, read_every=True)
+    for r in range(3):
+        assert np.array_equal(e_eager[r], e_def[r])
+        assert np.array_equal(r_eager[r], r_def[r])
+    import paper_2407_01378_b200 as gcb
+    pipe = gcb.make_pipeline(gcb.PowerSgdConfig(4), n, d, gcb.SeedSpec(5), compute_nmse=False)
+    pipe.run_round(torch.from_numpy(np.stack(grads[0])).cuda(), 0)
+    assert pipe._engine.group.pending is not None
+    zeros = [np.zeros(d, np.float32) for _ in range(n)]
+    pipe.residuals = zeros
+    assert pipe._engine.group.pending is None
+    assert not np.any(np.stack(pipe.residuals))
+
+
+def test_tma_pass_matches_register_pass():
+    """P = M Q from the TMA-fed kernel against the register-fed tcgen05 kernel: same 3xTF32 split
+    and fold cadence, so the factors agree to far inside the 1e-5 contract."""
+    import ctypes
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200 import _native
+    from paper_2407_01378_b200.configs import matrix_shape_for
+    d, _ = _dims()
+    rows, cols = matrix_shape_for(d)
+    n, r = 2, 4
+    g = torch.randn(n, d, device="cuda")
+    res = torch.randn(n, d, device="cuda")
+    q = torch.randn(cols, r, device="cuda")
+    batch = _native.PsgdBatch(1, n, None, d, None, 1, 0)
+    ws = torch.empty(int(_native.lib().gc_psgd_workspace_bytes(n, rows, cols, r)), dtype=torch.uint8, device="cuda")
+    p1 = torch.empty(n, rows, r, device="cuda")
+    p2 = torch.empty(n, rows, r, device="cuda")
+    r1, r2 = res.clone(), res.clone()
+    sp = torch.cuda.current_stream().cuda_stream
+    assert _native.lib().gc_psgd_mq_tma_supported(ctypes.byref(batch), d, rows, cols, r, g.data_ptr(), r1.data_ptr())
+    _native.call("gc_psgd_mq_deferred", ctypes.byref(batch), d, rows, cols, r, g.data_ptr(), r1.data_ptr(),
+                 q.data_ptr(), None, None, p1.data_ptr(), ws.data_ptr(), sp)
+    _native.call("gc_psgd_mq_fused", ctypes.byref(batch), d, rows, cols, r, g.data_ptr(), r2.data_ptr(),
+                 q.data_ptr(), p2.data_ptr(), ws.data_ptr(), sp)
+    torch.cuda.synchronize()
+    assert torch.equal(r1, r2)                       # corrected = f32(g + r) written over r
+    assert torch.equal(r1, g + res)
+    # rows wholly inside d: the same 3xTF32 products in the same order -- identical only if the
+    # tensor core truncates the raw fp32 A_big operand to tf32 exactly as the register kernel's mask
+    rf = d // cols
+    assert torch.equal(p1[:, :rf], p2[:, :rf])
+    m = torch.zeros(n, rows * cols, dtype=torch.float64, device="cuda")
+    m[:, :d] = (g + res).double()
+    ref = torch.einsum("wij,jb->wib", m.reshape(n, rows, cols), q.double())
+    scale = ref.abs().max().item()
+    assert (p1.double() - ref).abs().max().item() <= 1e-5 * scale
+    assert (p2.double() - ref).abs().max().item() <= 1e-5 * scale

@@ -1,0 +1,52 @@
+"""Small rounds of the kernels with mbarrier / TMEM / DSMEM / cluster / shared-memory protocols,
+for compute-sanitizer (memcheck, racecheck, synccheck):
+
+    compute-sanitizer --tool racecheck python tools/sanitize_cases.py [case ...]
+
+cases: thc_fused (n = 8, B = 1024, 2 rounds), thc_rank (per-rank K1/K2/K3 on a one-rank gloo
+group), psgd_umma (tcgen05 P = M Q), psgd_mtp_ef (cluster / DSMEM Q + EF pass), topk, topkc."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2407_01378_b200 as gcb
+
+cases = sys.argv[1:] or ["thc_fused", "thc_rank", "psgd_umma", "psgd_mtp_ef", "topk", "topkc"]
+torch.cuda.set_device(0)
+S = gcb.SeedSpec(7)
+
+
+def rounds(pipe, g, k=2):
+    for r in range(k):
+        pipe.run_round(g, r)
+    torch.cuda.synchronize()
+
+
+for c in cases:
+    if c == "thc_fused":
+        n, d = 8, (1 << 15) + 77
+        rounds(gcb.make_pipeline(gcb.RotatedQuantConfig(4, 8), n, d, S, fused=True), torch.randn(n, d, device="cuda"))
+    elif c == "thc_rank":
+        import torch.distributed as dist
+        from paper_2407_01378_b200.distributed import DistributedGradientPipeline
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        if not dist.is_initialized():
+            dist.init_process_group("gloo", rank=0, world_size=1)
+        d = (1 << 15) + 77
+        rounds(DistributedGradientPipeline(gcb.RotatedQuantConfig(4, 8), 1, d, S), torch.randn(1, d, device="cuda"))
+    elif c == "psgd_umma":
+        n, d = 2, 300 * 257
+        rounds(gcb.make_pipeline(gcb.PowerSgdConfig(4), n, d, S), torch.randn(n, d, device="cuda"))
+    elif c == "psgd_mtp_ef":
+        os.environ["GC_PSGD_MTP_EF"] = "1"
+        n, d = 2, 256 * 256
+        pipe = gcb.make_pipeline(gcb.PowerSgdConfig(4), n, d, S, compute_nmse=False)
+        rounds(pipe, torch.randn(n, d, device="cuda"))
+        os.environ["GC_PSGD_MTP_EF"] = "0"
+    elif c == "topk":
+        n, d = 2, 1 << 16
+        rounds(gcb.make_pipeline(gcb.TopKConfig(d // 100), n, d, S), torch.randn(n, d, device="cuda"))
+    elif c == "topkc":
+        n, d = 2, 1 << 16
+        rounds(gcb.make_pipeline(gcb.ChunkedTopKConfig(64, 10), n, d, S), torch.randn(n, d, device="cuda"))
+    print("case ok:", c, flush=True)
