@@ -29,6 +29,8 @@ int gc_psgd_mq_tma_supported_impl(int32_t tensors, int32_t workers, const int64_
 int gc_psgd_mq_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank,
                           const float *grads, float *resid, const float *q, const float *ef_ph, const float *ef_qw,
                           double *partial, int64_t max_splits, cudaStream_t st);
+int gc_psgd_mtp_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
+                           const float *p_hat, double *partial, int64_t max_splits, cudaStream_t st);
 #define GC_LAUNCH_CHECK(what)                                                     \
   do {                                                                            \
     cudaError_t e_ = cudaGetLastError();                                          \

@@ -1067,11 +1067,17 @@ int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, i
   GC_REQUIRE(d >= 1 && rows * cols >= d && c && p_hat && q && workspace, "invalid argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int L = b->tensors * b->workers;
-  const int splits = gc_psgd_splits(L, cols);
+  int splits = gc_psgd_splits(L, cols);
   const int64_t per = (rows + splits - 1) / splits;
   double *partial = static_cast<double *>(workspace);
   const bool vec = cols % 4 == 0 && b->rows_aligned && (reinterpret_cast<uintptr_t>(c) & 15) == 0;
-  if (vec) {
+  const char *impl = getenv("GC_PSGD_MTP");
+  if ((impl == nullptr || std::string(impl) != "cores") &&
+      gc_psgd_mq_tma_supported_impl(b->tensors, b->workers, b->row_offsets, b->ld, d, rows, cols, rank, c, c)) {
+    // TMA-fed column slabs (gc_psgd_tma.cu); the same split-K partials and ordered reduction
+    splits = gc_psgd_mtp_tma_launch(L, b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);
+    if (splits < 0) return splits;
+  } else if (vec) {
     GC_RANK_SWITCH(rank, ({
       mtp_vec_kernel<R, true><<<dim3(grid_cap((cols + 1023) / 1024), splits, L), 256, 0, st>>>(
           d, rows, cols, c, rows_of(b), p_hat, per, partial, splits);

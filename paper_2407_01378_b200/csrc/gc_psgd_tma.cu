@@ -43,7 +43,12 @@ namespace {
 constexpr int kM = 128;        // UMMA M: rows per CTA
 constexpr int kN = 16;         // UMMA N: rank padded to 16
 constexpr int kKc = 32;        // columns per stage: one 128-byte swizzle atom of fp32
-constexpr int kThreads = 256;
+constexpr int kProducers = 512;            // 16 producer warps (2 float4 of a 128 x 32 box each)
+constexpr int kThreads = kProducers + 32;  // + the control warp (TMA loads / MMA issue / TMA stores)
+#ifndef GC_MQT_PAIR
+#define GC_MQT_PAIR 0
+#endif
+constexpr int kPair = GC_MQT_PAIR ? 2 : 1;   // stages refilled together: 256-byte row bursts for DRAM
 #ifndef GC_MQT_STAGES
 #define GC_MQT_STAGES 5
 #endif
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kStages; ++s) {
       mbar_init(loaded_bar(s), 1);
       mbar_init(empty_bar(s), 1);
-      mbar_init(full_bar(s), kThreads);
+      mbar_init(full_bar(s), kProducers);
     }
     mbar_init(acc_bar(0), 1);
     mbar_init(acc_bar(1), 1);
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   const uint32_t tx_bytes_box = static_cast<uint32_t>(kTile) * (a.has_resid ? 2u : 1u);
-  // control thread: fill stage s with chunk k
+  // control warp: fill stage s with chunk k
   auto issue_load = [&](int64_t k) {
     const int s = static_cast<int>(k % kStages);
     const int64_t col0 = (c_begin + k) * kKc;
@@ -214,9 +219,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     bulk_load(stage(s) + kOffQ, a.q + col0 * R, qbytes, loaded_bar(s));
     if (DEF) bulk_load(stage(s) + kOffW, qw_prev + col0 * R, qbytes, loaded_bar(s));
   };
-  if (tid == 0) {
-    for (int64_t k = 0; k < min(static_cast<int64_t>(kStages), nloc); ++k) issue_load(k);
-  }
 
   double acc64[R];
 #pragma unroll
@@ -239,102 +241,120 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
 
-  const int ch = tid & 7;   // the thread's 16-byte chunk of a row (4 columns): the same in every pass
-  for (int64_t k = 0; k < nloc; ++k) {
-    const int s = static_cast<int>(k % kStages);
-    const int64_t col0 = (c_begin + k) * kKc;
-    unsigned char *st = sm + s * kStageBytes;
-    const float *qraw = reinterpret_cast<const float *>(st + kOffQ);
-    mbar_wait(loaded_bar(s), static_cast<uint32_t>((k / kStages) & 1));
-    // this thread's 4 columns; columns past cols are zero in the boxes (TMA fill) and stay zero
-    const int64_t cbase = col0 + 4 * ch;
-    float wq[4][R];
-    if (DEF) {
-      const float *wraw = reinterpret_cast<const float *>(st + kOffW);
+  if (warp == kProducers / 32) {
+    // ---- control warp (one elected lane): TMA ring, MMA issue, TMA stores.  It never produces, so
+    // the producers' chunk time is not serialised behind the issue path.
+    if (lane == 0) {
+      for (int64_t k = 0; k < min(static_cast<int64_t>(kStages), nloc); ++k) issue_load(k);
+      int64_t next = kStages;   // next chunk to load
+      for (int64_t k = 0; k < nloc; ++k) {
+        const int s = static_cast<int>(k % kStages);
+        const int64_t col0 = (c_begin + k) * kKc;
+        const int64_t gi = k / kGroup;
+        mbar_wait(full_bar(s), static_cast<uint32_t>((k / kStages) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dcol = tmem + static_cast<uint32_t>((gi & 1) * kN);
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-#pragma unroll
-        for (int b = 0; b < R; ++b) wq[e][b] = wraw[(4 * ch + e) * R + b];
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int row = (tid >> 3) + 32 * u;
-      const uint32_t off = sw128(row, ch);
-      float4 gv = *reinterpret_cast<const float4 *>(st + kOffG + off);
-      float4 c = gv;
-      if (a.has_resid) {
-        float4 rv = *reinterpret_cast<const float4 *>(st + kOffC + off);
-        if (DEF) {
-          float pa[R];
-#pragma unroll
-          for (int b = 0; b < R; ++b) pa[b] = ph_s[row * R + b];
-          const bool live = row0 + row < a.rows_full;   // the partial row is the fix-up kernel's
-          rv.x = live && cbase + 0 < a.cols ? rv.x - own_of<R>(pa, wq[0]) : 0.0f;
-          rv.y = live && cbase + 1 < a.cols ? rv.y - own_of<R>(pa, wq[1]) : 0.0f;
-          rv.z = live && cbase + 2 < a.cols ? rv.z - own_of<R>(pa, wq[2]) : 0.0f;
-          rv.w = live && cbase + 3 < a.cols ? rv.w - own_of<R>(pa, wq[3]) : 0.0f;
+        for (int kk = 0; kk < kKc / 8; ++kk) {
+          const uint64_t ab = sdesc(stage(s) + kOffC + 32 * kk), as = sdesc(stage(s) + kOffG + 32 * kk);
+          const uint64_t bb = sdesc(stage(s) + kOffBb + 32 * kk), bs = sdesc(stage(s) + kOffBs + 32 * kk);
+          const uint32_t accum = (k % kGroup != 0 || kk != 0) ? 1u : 0u;
+          umma_tf32(dcol, as, bb, accum);
+          umma_tf32(dcol, ab, bs, 1u);
+          umma_tf32(dcol, ab, bb, 1u);
         }
-        c.x = gv.x + rv.x;
-        c.y = gv.y + rv.y;
-        c.z = gv.z + rv.z;
-        c.w = gv.w + rv.w;
+        umma_commit(empty_bar(s));
+        if (k % kGroup == kGroup - 1 || k == nloc - 1) umma_commit(acc_bar(static_cast<int>(gi & 1)));
+        if (a.has_resid) {   // corrected box back over the residual buffer (clipped to the map)
+          tma_store_3d(&map_r, stage(s) + kOffC, static_cast<int>(col0), static_cast<int>(row0), v);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        // refill the stages of chunks next - S .. next - S + kPair - 1 (all older than k) once their
+        // MMAs and stores are done, kPair at a time so each row's adjacent segments go out together
+        if (next < nloc && next - kStages + kPair - 1 <= k - 1) {
+          const int64_t batch = min(static_cast<int64_t>(kPair), nloc - next);
+          for (int64_t pp = 0; pp < batch; ++pp) {
+            const int64_t old = next + pp - kStages;
+            mbar_wait(empty_bar(static_cast<int>(old % kStages)), static_cast<uint32_t>((old / kStages) & 1));
+          }
+          if (a.has_resid) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          for (int64_t pp = 0; pp < batch; ++pp) issue_load(next + pp);
+          next += batch;
+        }
       }
-      float4 hb, hs;
-      split3(c.x, hb.x, hs.x);
-      split3(c.y, hb.y, hs.y);
-      split3(c.z, hb.z, hs.z);
-      split3(c.w, hb.w, hs.w);
-      *reinterpret_cast<float4 *>(st + kOffC + off) = c;    // A_big (truncated by the MMA) and the store source
-      *reinterpret_cast<float4 *>(st + kOffG + off) = hs;   // A_small over the consumed g box
+      if (a.has_resid) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
-    if (tid < R * 8) {   // B = Q^T of the chunk: row n (< R), 4 columns per thread
-      const int n = tid >> 3;
-      float t[4];
+  } else {
+    // ---- producers: boxes -> operands (and the corrected values) in place
+    const int ch = tid & 7;   // the thread's 16-byte chunk of a row (4 columns): the same in every pass
+    for (int64_t k = 0; k < nloc; ++k) {
+      const int s = static_cast<int>(k % kStages);
+      const int64_t col0 = (c_begin + k) * kKc;
+      unsigned char *st = sm + s * kStageBytes;
+      const float *qraw = reinterpret_cast<const float *>(st + kOffQ);
+      mbar_wait(loaded_bar(s), static_cast<uint32_t>((k / kStages) & 1));
+      // this thread's 4 columns; columns past cols are zero in the boxes (TMA fill) and stay zero
+      const int64_t cbase = col0 + 4 * ch;
+      float wq[4][R];
+      if (DEF) {
+        const float *wraw = reinterpret_cast<const float *>(st + kOffW);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) t[e] = cbase + e < a.cols ? qraw[(4 * ch + e) * R + n] : 0.0f;
-      float4 hb, hs;
-      split3(t[0], hb.x, hs.x);
-      split3(t[1], hb.y, hs.y);
-      split3(t[2], hb.z, hs.z);
-      split3(t[3], hb.w, hs.w);
-      const uint32_t off = sw128(n, ch);
-      *reinterpret_cast<float4 *>(st + kOffBb + off) = hb;
-      *reinterpret_cast<float4 *>(st + kOffBs + off) = hs;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full_bar(s)) : "memory");
-    const int64_t gi = k / kGroup;
-    if (tid == 0) {
-      mbar_wait(full_bar(s), static_cast<uint32_t>((k / kStages) & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t dcol = tmem + static_cast<uint32_t>((gi & 1) * kN);
+        for (int e = 0; e < 4; ++e)
 #pragma unroll
-      for (int kk = 0; kk < kKc / 8; ++kk) {
-        const uint64_t ab = sdesc(stage(s) + kOffC + 32 * kk), as = sdesc(stage(s) + kOffG + 32 * kk);
-        const uint64_t bb = sdesc(stage(s) + kOffBb + 32 * kk), bs = sdesc(stage(s) + kOffBs + 32 * kk);
-        const uint32_t accum = (k % kGroup != 0 || kk != 0) ? 1u : 0u;
-        umma_tf32(dcol, as, bb, accum);
-        umma_tf32(dcol, ab, bs, 1u);
-        umma_tf32(dcol, ab, bb, 1u);
+          for (int b = 0; b < R; ++b) wq[e][b] = wraw[(4 * ch + e) * R + b];
       }
-      umma_commit(empty_bar(s));
-      if (k % kGroup == kGroup - 1 || k == nloc - 1) umma_commit(acc_bar(static_cast<int>(gi & 1)));
-      if (a.has_resid) {   // corrected box back over the residual buffer (clipped to the map)
-        tma_store_3d(&map_r, stage(s) + kOffC, static_cast<int>(col0), static_cast<int>(row0), v);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#pragma unroll
+      for (int u = 0; u < kM * 8 / kProducers; ++u) {
+        const int row = (tid >> 3) + (kProducers / 8) * u;
+        const uint32_t off = sw128(row, ch);
+        float4 gv = *reinterpret_cast<const float4 *>(st + kOffG + off);
+        float4 c = gv;
+        if (a.has_resid) {
+          float4 rv = *reinterpret_cast<const float4 *>(st + kOffC + off);
+          if (DEF) {
+            float pa[R];
+#pragma unroll
+            for (int b = 0; b < R; ++b) pa[b] = ph_s[row * R + b];
+            const bool live = row0 + row < a.rows_full;   // the partial row is the fix-up kernel's
+            rv.x = live && cbase + 0 < a.cols ? rv.x - own_of<R>(pa, wq[0]) : 0.0f;
+            rv.y = live && cbase + 1 < a.cols ? rv.y - own_of<R>(pa, wq[1]) : 0.0f;
+            rv.z = live && cbase + 2 < a.cols ? rv.z - own_of<R>(pa, wq[2]) : 0.0f;
+            rv.w = live && cbase + 3 < a.cols ? rv.w - own_of<R>(pa, wq[3]) : 0.0f;
+          }
+          c.x = gv.x + rv.x;
+          c.y = gv.y + rv.y;
+          c.z = gv.z + rv.z;
+          c.w = gv.w + rv.w;
+        }
+        float4 hb, hs;
+        split3(c.x, hb.x, hs.x);
+        split3(c.y, hb.y, hs.y);
+        split3(c.z, hb.z, hs.z);
+        split3(c.w, hb.w, hs.w);
+        *reinterpret_cast<float4 *>(st + kOffC + off) = c;    // A_big (truncated by the MMA) and the store source
+        *reinterpret_cast<float4 *>(st + kOffG + off) = hs;   // A_small over the consumed g box
       }
-      // refill the stage of chunk k - 1 with chunk k - 1 + S once its MMAs and store are done
-      if (k >= 1 && k - 1 + kStages < nloc) {
-        const int sp = static_cast<int>((k - 1) % kStages);
-        mbar_wait(empty_bar(sp), static_cast<uint32_t>(((k - 1) / kStages) & 1));
-        if (a.has_resid) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        issue_load(k - 1 + kStages);
+      if (tid < R * 8) {   // B = Q^T of the chunk: row n (< R), 4 columns per thread
+        const int n = tid >> 3;
+        float t[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) t[e] = cbase + e < a.cols ? qraw[(4 * ch + e) * R + n] : 0.0f;
+        float4 hb, hs;
+        split3(t[0], hb.x, hs.x);
+        split3(t[1], hb.y, hs.y);
+        split3(t[2], hb.z, hs.z);
+        split3(t[3], hb.w, hs.w);
+        const uint32_t off = sw128(n, ch);
+        *reinterpret_cast<float4 *>(st + kOffBb + off) = hb;
+        *reinterpret_cast<float4 *>(st + kOffBs + off) = hs;
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full_bar(s)) : "memory");
+      const int64_t gi = k / kGroup;
+      if (k % kGroup == 0 && gi >= 1) fold_group(gi - 1);
     }
-    if (k % kGroup == 0 && gi >= 1) fold_group(gi - 1);
+    if (nloc > 0) fold_group((nloc - 1) / kGroup);
   }
-  if (nloc > 0) fold_group((nloc - 1) / kGroup);
-  if (tid == 0 && a.has_resid) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 
   if (warp < 4) {
     const int64_t grow = row0 + warp * 32 + lane;
@@ -351,9 +371,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // The row of the matrix that is only partly inside d (to_matrix's zero padding starts in it):
 // corrected values written, P row summed in fp64 (split 0; the other splits' partials zeroed).
+constexpr int kTailThreads = 1024;
+
 template <int R, bool DEF>
-__global__ void __launch_bounds__(256) mq_tail_row_kernel(const float *g, float *resid, int64_t ld, TmaArgs a) {
-  __shared__ double red[8][R];
+__global__ void __launch_bounds__(kTailThreads) mq_tail_row_kernel(const float *g, float *resid, int64_t ld,
+                                                                  TmaArgs a) {
+  __shared__ double red[kTailThreads / 32][R];
   const int v = blockIdx.x;
   const int64_t i = a.rows_full;
   const int64_t n_valid = a.d - i * a.cols;
@@ -368,7 +391,7 @@ __global__ void __launch_bounds__(256) mq_tail_row_kernel(const float *g, float 
   double acc[R];
 #pragma unroll
   for (int b = 0; b < R; ++b) acc[b] = 0.0;
-  for (int64_t j = threadIdx.x; j < n_valid; j += 256) {
+  for (int64_t j = threadIdx.x; j < n_valid; j += kTailThreads) {
     float c = gw[j];
     if (rw) {
       float r = rw[j];
@@ -394,9 +417,114 @@ __global__ void __launch_bounds__(256) mq_tail_row_kernel(const float *g, float 
   __syncthreads();
   if (threadIdx.x < R) {
     double x = 0.0;
-    for (int w = 0; w < 8; ++w) x += red[w][threadIdx.x];
+    for (int w = 0; w < kTailThreads / 32; ++w) x += red[w][threadIdx.x];
     for (int s = 0; s < a.splits; ++s)
       a.partial[((static_cast<int64_t>(v) * a.splits + s) * a.rows + i) * R + threadIdx.x] = s == 0 ? x : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------ Q_w = M_w^T P_hat (pipelines.py:354)
+// Same TMA boxes (128 rows x 32 columns of M, SWIZZLE_128B) streamed by a producer warp; a CTA owns a
+// 32-column slab and a range of rows: consumer thread (column c, row group g) accumulates
+// sum_i M[i,c] P_hat[i,:] over its rows in fp32 FMAs, folded into fp64 after every box (16 rows,
+// the CUDA-core pass folds every 32), the 8 row groups reduced in order through shared memory and
+// the split-K partials written as gc_psgd_mtp's, so the same ordered reduction finishes Q_w.
+constexpr int kMtpStages = 4;
+constexpr int kMtpConsumers = 256;
+constexpr int kMtpThreads = kMtpConsumers + 32;
+constexpr int kMtpSmem = kMtpStages * kTile + 64 + 1024;
+
+struct MtpArgs {
+  int64_t d, rows, cols, rows_full, ld;
+  const float *c;          // corrected matrices (the partial row is read from here)
+  const float *ph;         // P_hat [rows][R]
+  double *partial;         // [L][splits][cols][R]
+  int splits;
+  int64_t rows_per_split;  // multiple of kM
+};
+
+template <int R>
+__global__ void __launch_bounds__(kMtpThreads, 2) mtp_tma_kernel(const __grid_constant__ CUtensorMap map_c,
+                                                                const __grid_constant__ MtpArgs a) {
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char *sm = smem_raw + (base - raw);
+  const uint32_t bars = base + kMtpStages * kTile;   // loaded[S], empty[S]
+  __shared__ double red[kMtpConsumers / 32][32][R];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int v = blockIdx.z, split = blockIdx.y;
+  const int64_t col0 = static_cast<int64_t>(blockIdx.x) * kKc;
+  const int64_t r_begin = split * a.rows_per_split;
+  const int64_t r_end = min(a.rows_full, r_begin + a.rows_per_split);
+  const int64_t nbox = r_end > r_begin ? (r_end - r_begin + kM - 1) / kM : 0;
+  if (tid == 0) {
+    for (int s = 0; s < kMtpStages; ++s) {
+      mbar_init(bars + 8 * s, 1);
+      mbar_init(bars + 8 * (kMtpStages + s), kMtpConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kMtpConsumers / 32) {   // producer warp: the TMA ring
+    if (lane == 0) {
+      for (int64_t b = 0; b < nbox; ++b) {
+        const int s = static_cast<int>(b % kMtpStages);
+        if (b >= kMtpStages)
+          mbar_wait(bars + 8 * (kMtpStages + s), static_cast<uint32_t>(((b / kMtpStages) - 1) & 1));
+        mbar_expect_tx(bars + 8 * s, kTile);
+        tma_load_3d(base + s * kTile, &map_c, static_cast<int>(col0), static_cast<int>(r_begin + b * kM), v,
+                    bars + 8 * s);
+      }
+    }
+    return;
+  }
+  const int c = lane, g = warp;   // column of the slab, row group
+  double acc64[R];
+#pragma unroll
+  for (int b = 0; b < R; ++b) acc64[b] = 0.0;
+  for (int64_t bx = 0; bx < nbox; ++bx) {
+    const int s = static_cast<int>(bx % kMtpStages);
+    const int64_t i0 = r_begin + bx * kM;
+    mbar_wait(bars + 8 * s, static_cast<uint32_t>((bx / kMtpStages) & 1));
+    const unsigned char *st = sm + s * kTile;
+    float acc[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc[b] = 0.0f;
+#pragma unroll 4
+    for (int rr = 0; rr < kM / 8; ++rr) {
+      const int row = g + 8 * rr;
+      const float m = *reinterpret_cast<const float *>(st + sw128(row, c >> 2) + (c & 3) * 4);
+      const int64_t i = i0 + row;
+      if (i < r_end) {   // rows past the slab's range are zero-filled or another split's
+        const float *pr = a.ph + i * R;
+#pragma unroll
+        for (int b = 0; b < R; ++b) acc[b] = fmaf(m, __ldg(pr + b), acc[b]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc64[b] += static_cast<double>(acc[b]);
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bars + 8 * (kMtpStages + s)) : "memory");
+  }
+  // the row that is only partly inside d belongs to the last split (plain loads, fp64)
+  if (g == 0 && split == a.splits - 1 && a.rows_full < a.rows && col0 + c < a.cols) {
+    const int64_t off = a.rows_full * a.cols + col0 + c;
+    if (off < a.d) {
+      const double m = static_cast<double>(a.c[v * a.ld + off]);
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc64[b] += m * static_cast<double>(a.ph[a.rows_full * R + b]);
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < R; ++b) red[g][c][b] = acc64[b];
+  asm volatile("bar.sync 1, %0;" ::"r"(kMtpConsumers) : "memory");   // consumers only
+  for (int e = tid; e < 32 * R; e += kMtpConsumers) {
+    const int cc = e / R, b = e - cc * R;
+    double x = 0.0;
+#pragma unroll
+    for (int w = 0; w < kMtpConsumers / 32; ++w) x += red[w][cc][b];
+    if (col0 + cc < a.cols)
+      a.partial[((static_cast<int64_t>(v) * a.splits + split) * a.cols + col0 + cc) * R + b] = x;
   }
 }
 
@@ -446,6 +574,59 @@ int gc_psgd_mq_tma_supported_impl(int32_t tensors, int32_t workers, const int64_
   return encode_fn() != nullptr ? 1 : 0;
 }
 
+// TMA-fed Q_w = M_w^T P_hat: fp64 split-K partials partial[w][split][col][R] (max_splits slots
+// sized by the caller); returns the split count or a negative status.
+int gc_psgd_mtp_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
+                           const float *p_hat, double *partial, int64_t max_splits, cudaStream_t st) {
+  const int64_t rows_full = d / cols;
+  const int64_t slabs = (cols + kKc - 1) / kKc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t boxes = (rows_full + kM - 1) / kM;
+  int64_t splits = (2 * sms + slabs * L - 1) / (slabs * L);
+  if (splits > max_splits) splits = max_splits;
+  if (splits > boxes) splits = boxes;
+  if (splits < 1) splits = 1;
+  const int64_t per = (boxes + splits - 1) / splits;
+  splits = (boxes + per - 1) / per;
+  CUtensorMap mc;
+  if (!make_map(&mc, c, L, rows_full, cols, ld)) {
+    gc_set_error("cuTensorMapEncodeTiled failed for the Q = M^T P_hat operand");
+    return GC_ERR_CUDA;
+  }
+  MtpArgs a{};
+  a.d = d;
+  a.rows = rows;
+  a.cols = cols;
+  a.rows_full = rows_full;
+  a.ld = ld;
+  a.c = c;
+  a.ph = p_hat;
+  a.partial = partial;
+  a.splits = static_cast<int>(splits);
+  a.rows_per_split = per * kM;
+  const dim3 grid(static_cast<unsigned>(slabs), static_cast<unsigned>(splits), static_cast<unsigned>(L));
+#define GC_MTPT(RR)                                                                                  \
+  case RR:                                                                                           \
+    cudaFuncSetAttribute(mtp_tma_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMtpSmem); \
+    mtp_tma_kernel<RR><<<grid, kMtpThreads, kMtpSmem, st>>>(mc, a);                                 \
+    break;
+  switch (rank) {
+    GC_MTPT(1) GC_MTPT(2) GC_MTPT(3) GC_MTPT(4) GC_MTPT(5) GC_MTPT(6) GC_MTPT(7) GC_MTPT(8) GC_MTPT(16)
+    default:
+      gc_set_error("rank must be 1..8 or 16");
+      return GC_ERR_UNSUPPORTED;
+  }
+#undef GC_MTPT
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    gc_set_error(std::string("mtp_tma_kernel: ") + cudaGetErrorString(e));
+    return GC_ERR_CUDA;
+  }
+  return static_cast<int>(splits);
+}
+
 // TMA-fed tcgen05 P = M Q with ef_apply (and, with ef_ph / ef_qw, the previous round's deferred
 // EF update).  fp64 split-K partials partial[w][split][row][R]; returns the split count or a
 // negative status.
@@ -487,7 +668,7 @@ int gc_psgd_mq_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_
 #define GC_TMA_LAUNCH(RR, DD)                                                                              \
   cudaFuncSetAttribute(mq_tma_kernel<RR, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);    \
   mq_tma_kernel<RR, DD><<<grid, kThreads, kSmemBytes, st>>>(mg, mr, a);                                    \
-  if (tail) mq_tail_row_kernel<RR, DD><<<L, 256, 0, st>>>(grads, resid, ld, a);
+  if (tail) mq_tail_row_kernel<RR, DD><<<L, kTailThreads, 0, st>>>(grads, resid, ld, a);
 #define GC_TMA_CASE(RR)        \
   case RR:                     \
     if (def) {                 \

@@ -150,3 +150,35 @@ def test_tma_pass_matches_register_pass():
     scale = ref.abs().max().item()
     assert (p1.double() - ref).abs().max().item() <= 1e-5 * scale
     assert (p2.double() - ref).abs().max().item() <= 1e-5 * scale
+
+
+@pytest.mark.parametrize("which", ["partial", "full"])
+@pytest.mark.parametrize("r", [1, 4, 16])
+def test_mtp_tma_matches_cuda_core_pass(which, r, monkeypatch):
+    """Q_w = M_w^T P_hat from the TMA-fed slab kernel against the CUDA-core pass (GC_PSGD_MTP=cores)
+    and an fp64 reference: both within far less than the 1e-5 contract."""
+    import ctypes
+    from paper_2407_01378_b200 import _native
+    from paper_2407_01378_b200.configs import matrix_shape_for
+    d = dict(zip(("partial", "full"), _dims()))[which]
+    rows, cols = matrix_shape_for(d)
+    n = 2
+    c = torch.randn(n, d, device="cuda")
+    ph = torch.randn(rows, r, device="cuda")
+    batch = _native.PsgdBatch(1, n, None, d, None, 1, 0)
+    ws = torch.empty(int(_native.lib().gc_psgd_workspace_bytes(n, rows, cols, r)), dtype=torch.uint8, device="cuda")
+    q1 = torch.empty(n, cols, r, device="cuda")
+    q2 = torch.empty(n, cols, r, device="cuda")
+    sp = torch.cuda.current_stream().cuda_stream
+    _native.call("gc_psgd_mtp", ctypes.byref(batch), d, rows, cols, r, c.data_ptr(), ph.data_ptr(), q1.data_ptr(),
+                 ws.data_ptr(), sp)
+    monkeypatch.setenv("GC_PSGD_MTP", "cores")
+    _native.call("gc_psgd_mtp", ctypes.byref(batch), d, rows, cols, r, c.data_ptr(), ph.data_ptr(), q2.data_ptr(),
+                 ws.data_ptr(), sp)
+    torch.cuda.synchronize()
+    m = torch.zeros(n, rows * cols, dtype=torch.float64, device="cuda")
+    m[:, :d] = c.double()
+    ref = torch.einsum("wij,ib->wjb", m.reshape(n, rows, cols), ph.double())
+    scale = ref.abs().max().item()
+    assert (q1.double() - ref).abs().max().item() <= 1e-6 * scale
+    assert (q2.double() - ref).abs().max().item() <= 1e-6 * scale

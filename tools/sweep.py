@@ -1,8 +1,16 @@
 """Time every scheme at its SURVEY §8(d) config, n simulated workers on one B200.
 
-python tools/sweep.py [--n 8] [--steps 10] [--only thc,topk,...]
+python tools/sweep.py [--n 8] [--steps 10] [--only thc,topk,...] [--synthetic] [--nmse R]
 Prints one JSON line per scheme: ms/round, Gelem/s (d / T), algorithmic HBM bytes and the
-fraction of the measured HBM bandwidth those bytes imply."""
+fraction of the measured HBM bandwidth those bytes imply.
+
+--synthetic: SyntheticGradSpec-model gradients (paper_2407_01378_b200.synthetic, trainbench.py:31-113
+structure), a fresh round for every warm-up and timed step (pre-generated outside the timed
+region), so data-dependent paths (TopK's threshold hint) see real round-to-round drift.
+--nmse R: the nmse sweep of cli.py:279-333 instead of timing: R rounds per scheme on synthetic
+gradients with compute_nmse, one `round,scheme,nmse,bits_per_coord,overflow_rate` row per round and
+a mean line per scheme (the reference's rounds.csv / nmse_summary.csv columns, minus the
+TimeModel's simulated_ms)."""
 import argparse, json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -21,6 +29,24 @@ def alg_bytes(name, n, d, cfg):
     return 12 * n * d + 4 * d
 
 
+def nmse_sweep(name, cfg, n, d, rounds, seed=2024):
+    """cli.py:279-333: R rounds of one scheme on synthetic gradients, nmse per round."""
+    from paper_2407_01378_b200.ledger import overflow_rate
+    from paper_2407_01378_b200.synthetic import SyntheticGradients
+    gen = SyntheticGradients(d, gcb.SeedSpec(seed))
+    pipe = gcb.make_pipeline(cfg, n, d, gcb.SeedSpec(seed), validate=False, compute_nmse=True)
+    nmses, rates = [], []
+    for r in range(rounds):
+        res = pipe.run_round(gen.round(r, n), r)
+        nmses.append(res.nmse)
+        rates.append(overflow_rate(res.overflow))
+        print(f"{r},{name},{res.nmse!r},{res.input_bits_per_coord!r},{rates[-1]!r}", flush=True)
+    print(json.dumps({"scheme": name, "n": n, "d": d, "rounds": rounds, "bits_per_coord": res.input_bits_per_coord,
+                      "mean_nmse": sum(nmses) / rounds, "mean_overflow_rate": sum(rates) / rounds}), flush=True)
+    del pipe, gen
+    torch.cuda.empty_cache()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=8)
@@ -28,6 +54,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=12)
     ap.add_argument("--only", default="")
     ap.add_argument("--dims", default="", help="cfg5: comma list of d (e.g. 1048576,...,1e9); every scheme at each d")
+    ap.add_argument("--synthetic", action="store_true", help="fresh SyntheticGradSpec-model gradients every round")
+    ap.add_argument("--nmse", type=int, default=0, help="nmse sweep: R rounds per scheme, no timing")
     a = ap.parse_args()
     n = a.n
     if a.dims:
@@ -65,20 +93,31 @@ def main():
             g = torch.randn(n, d, device="cuda")
             pipe = TensorListPipeline(cfg, n, sizes, gcb.SeedSpec(2024), validate=False, compute_nmse=False)
             eng = pipe
+            pool = [g]
+        elif a.nmse:
+            nmse_sweep(name, cfg, n, d, a.nmse)
+            continue
         else:
-            g = torch.randn(n, d, device="cuda")
             pipe = gcb.make_pipeline(cfg, n, d, gcb.SeedSpec(2024), validate=False, compute_nmse=False)
             eng = pipe._engine
-        # warm-up rounds: the inputs repeat every round, so EF residuals grow until the TopK
-        # threshold settles; time the steady state
+            if a.synthetic:   # a distinct round of gradients per step, generated before timing
+                from paper_2407_01378_b200.synthetic import SyntheticGradients
+                gen = SyntheticGradients(d, gcb.SeedSpec(2024))
+                pool = [gen.round(r, n) for r in range(a.warmup + a.steps)]
+                del gen
+            else:
+                pool = [torch.randn(n, d, device="cuda")]
+            g = pool[0]
+        # warm-up rounds (repeated Gaussian inputs: EF residuals grow until the TopK threshold
+        # settles; synthetic: fresh rounds), then the timed steady state
         for r in range(a.warmup):
-            pipe.run_round(g, r)
+            pipe.run_round(pool[r % len(pool)], r)
         torch.cuda.synchronize()
         eng.kernel_events = [] if hasattr(eng, "kernel_events") else None
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
         s.record()
         for r in range(a.steps):
-            pipe.run_round(g, a.warmup + r)
+            pipe.run_round(pool[(a.warmup + r) % len(pool)], a.warmup + r)
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / a.steps
@@ -87,8 +126,10 @@ def main():
         b = alg_bytes(name, n, d, cfg)
         print(json.dumps({"case": name, "n": n, "d": d, "ms": round(ms, 4), "gelem_s": round(d / ms / 1e6, 3),
                           "core_ms": round(kms, 4), "alg_GB": round(b / 1e9, 3),
-                          "hbm_frac": round(b / (ms * 1e-3) / HBM, 4)}), flush=True)
-        del pipe, g, eng
+                          "hbm_frac": round(b / (ms * 1e-3) / HBM, 4),
+                          "inputs": "synthetic, fresh per round" if a.synthetic else "gaussian, repeated"}),
+              flush=True)
+        del pipe, g, eng, pool
         torch.cuda.empty_cache()
 
 
