@@ -26,9 +26,10 @@ one worker per GPU (n = N): THC q4b8, PowerSGD r4 (one 18,709 x 18,708 matrix, a
 GPT-2-medium's 292 tensors) and the FP16 NCCL all-reduce bar.  `cpu_baseline` times the CPU
 oracle (oracle/, a NumPy restatement of the reference path) on a bounded sample.
 
---impl reference times the reference's own CPU algorithm (the oracle port: the Python
-reference cannot be shipped to the GPU box) on a bounded sample of the same workload; rank 0
-alone runs it.
+--impl reference times the reference's own CPU THC round -- the unmodified gradcomp package staged
+under baseline/_ref/src (git-ignored; build() copies it from /root/reference and it travels with
+the snapshot), or the oracle port when it is absent -- on a bounded sample of the same workload;
+rank 0 alone runs it.
 """
 
 from __future__ import annotations
@@ -167,46 +168,81 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ CPU side
+def reference_package():
+    """The UNMODIFIED reference package staged under baseline/_ref/src (git-ignored, travels with the
+    snapshot; build() stages it from /root/reference), or None."""
+    src = os.path.join(ROOT, "baseline", "_ref", "src")
+    if not os.path.isfile(os.path.join(src, "gradcomp", "pipelines.py")):
+        return None
+    if src not in sys.path:
+        sys.path.insert(0, src)
+    try:
+        import gradcomp
+        return gradcomp
+    except Exception:
+        return None
+
+
 def cpu_thc_sample(args, d_sample: int, rounds: int):
-    """Reference CPU algorithm (oracle port) on a bounded sample: seconds per round."""
+    """The reference's CPU THC round on a bounded sample: seconds per round and the kind --
+    "reference" (gradcomp's own make_pipeline(...).run_round, pipelines.py:418-425, 147-182) when
+    the package is staged, else "port" (the oracle's NumPy restatement of the same round)."""
     import numpy as np
 
-    from oracle import gradcomp_oracle as orc
     n = args.workers
+    ref = reference_package()
+    times = []
+    if ref is not None:
+        seeds = ref.SeedSpec(2024)
+        pipe = ref.make_pipeline(ref.RotatedQuantConfig(args.quant_bits, args.wire_bits, args.rotation_block), n,
+                                 d_sample, seeds)
+        for r in range(rounds):
+            grads = [seeds.rng("grad-worker", r, w).standard_normal(d_sample).astype(np.float32) for w in range(n)]
+            t0 = time.perf_counter()
+            pipe.run_round(grads, r)
+            times.append(time.perf_counter() - t0)
+        return times, "reference"
+    from oracle import gradcomp_oracle as orc
     seeds = 2024
     params = dict(quant_bits=args.quant_bits, wire_bits=args.wire_bits, rotation_block=args.rotation_block)
     state = orc.OracleState([np.zeros(d_sample, np.float32) for _ in range(n)])
-    times = []
     for r in range(rounds):
         grads = [orc.stream_rng(seeds, "grad-worker", r, w).standard_normal(d_sample).astype(np.float32)
                  for w in range(n)]
         t0 = time.perf_counter()
         orc.run_round("rotated_quant", params, state, grads, seeds, r)
         times.append(time.perf_counter() - t0)
-    return times
+    return times, "port"
 
 
 def run_reference(args):
-    """The reference's CPU algorithm (oracle port, one host core: the reference's numpy THC path is
-    single-threaded) on a 2^18-coordinate sample of the cfg2 workload per step.  Rank 0 only."""
+    """The reference's own CPU THC round (gradcomp from baseline/_ref, else the oracle port; one host
+    core: the reference's numpy THC path is single-threaded) on a 2^18-coordinate sample of the cfg2
+    workload per step.  Rank 0 only."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     d_sample = 1 << 18
-    times = cpu_thc_sample(args, d_sample, args.warmup + args.steps)[args.warmup:]
+    times, kind = cpu_thc_sample(args, d_sample, args.warmup + args.steps)
+    times = times[args.warmup:]
     t = statistics.median(times)
     val = d_sample / t / 1e9
     cfg = workload(args, max(world, args.gpus))
+    cfg["d"] = d_sample
+    cfg["workload"] += f" -- CPU sample: d={d_sample:,} per step (cfg2's d={args.d:,} would take minutes per round)"
     cfg["sample_d"] = d_sample
     out = {"metric": METRIC, "value": val, "unit": "Gelem/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic (Gaussian grad-worker streams)",
            "config": cfg, "impl": "reference",
-           "cpu_baseline": dict({"value": val, "unit": "Gelem/s", "cores": 1, "kind": "port",
-                                 "sample": f"oracle port (NumPy restatement of gradcomp's THC round, "
-                                           f"pipelines.py:260-322), n={args.workers} workers, d={d_sample:,} "
+           "cpu_baseline": dict({"value": val, "unit": "Gelem/s", "cores": 1, "kind": kind,
+                                 "sample": (("gradcomp itself (the unmodified reference package, "
+                                             "make_pipeline(...).run_round)") if kind == "reference" else
+                                            "oracle port (NumPy restatement of gradcomp's THC round, "
+                                            "pipelines.py:260-322)")
+                                           + f", n={args.workers} workers, d={d_sample:,} "
                                            f"coordinates per step (not cfg2's d={args.d:,}: the rate is per "
-                                           f"coordinate and the port is linear in d), median of {args.steps} steps; "
+                                           f"coordinate and the round is linear in d), median of {args.steps} steps; "
                                            f"numpy's elementwise THC path runs on one core"}, **host_info()),
            "e2e": {"value": val, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -437,13 +473,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        d_sample = 1 << 19
-        times = cpu_thc_sample(args, d_sample, 3)
+        d_sample = 1 << 18
+        times, kind = cpu_thc_sample(args, d_sample, 3)
         t = statistics.median(times)
-        cpu = dict({"value": d_sample / t / 1e9, "unit": "Gelem/s", "cores": 1, "kind": "port",
-                    "sample": f"oracle port (NumPy restatement of the reference THC round), n={n}, d={d_sample:,} "
-                              f"(not cfg2's d; the port is linear in d), median of 3 rounds; numpy's elementwise "
-                              f"THC path runs on one core"}, **host_info())
+        cpu = dict({"value": d_sample / t / 1e9, "unit": "Gelem/s", "cores": 1, "kind": kind,
+                    "sample": ("gradcomp itself (unmodified reference package)" if kind == "reference" else
+                               "oracle port (NumPy restatement of the reference THC round)")
+                              + f", n={n}, d={d_sample:,} (not cfg2's d; the round is linear in d), median of 3 "
+                              f"rounds; numpy's elementwise THC path runs on one core"}, **host_info())
 
     bar = None
     if not args.no_bar:

@@ -108,10 +108,17 @@ class Comm:
                   recv.view(-1).view(torch.uint8), send.view(-1).view(torch.uint8))
         return recv
 
-    def all_reduce_async(self, t: torch.Tensor, op, phase: str | None = None):
+    def _count_ring(self, phase, t: torch.Tensor, rings: int):
+        # what `rings` reference ring all-reduces of numel / rings elements send per worker:
+        # 2 (W - 1) ceil(len / W) elements each (collectives.py:209-233)
+        per = t.numel() // rings
+        self._count(phase, rings * 2 * (self.world - 1) * -(-per // self.world) * t.element_size())
+
+    def all_reduce_async(self, t: torch.Tensor, op, phase: str | None = None, rings: int = 1):
         """In-place all-reduce of a contiguous tensor; returns a work handle to wait() on before
-        the result is used (NCCL: the current stream waits), or None when already complete."""
-        self._count(phase, 2 * (self.world - 1) * t.numel() * t.element_size() // self.world)
+        the result is used (NCCL: the current stream waits), or None when already complete.
+        `rings`: the tensor stands for that many equal reference rings (for the wire accounting)."""
+        self._count_ring(phase, t, rings)
         if self.local_only or t.numel() == 0:
             return None
         if self.stage and t.is_cuda:
@@ -121,8 +128,8 @@ class Comm:
             return None
         return dist.all_reduce(t, op=op, group=self.group, async_op=True)
 
-    def all_reduce(self, t: torch.Tensor, op, phase: str | None = None) -> torch.Tensor:
-        self._count(phase, 2 * (self.world - 1) * t.numel() * t.element_size() // self.world)
+    def all_reduce(self, t: torch.Tensor, op, phase: str | None = None, rings: int = 1) -> torch.Tensor:
+        self._count_ring(phase, t, rings)
         if self.local_only:
             return t
         if self.stage and t.is_cuda:
@@ -204,6 +211,32 @@ def exchange_fold(codes: torch.Tensor, comm: Comm, n: int, active: int, slice_le
     if nibble:
         return _nibbles(comm.all_gather_rows(_nibbles(sums.reshape(1, -1), True), phase), False).reshape(-1)
     return comm.all_gather_rows(sums.reshape(1, -1), phase).reshape(-1)
+
+
+def exchange_float(x: torch.Tensor, comm: Comm, n: int, phase: str | None, wire16: bool) -> torch.Tensor:
+    """FloatSum ring all-reduce (collectives.py:112-120, 177-236) of [L, m] float32 rows per rank,
+    exact in the reference's ring order and with the ring's wire volume: slice r of every row goes to
+    rank r (all-to-all), rank r folds its slice over the n worker rows in ring order (gc_float_fold:
+    element i starts at worker floor(i / ceil(m/n)), fp16 wire per hop when wire16), and the folded
+    slices are all-gathered -- 2 (W-1) ceil(m/W) elements per rank, the ledger's 2 (n-1) ceil(m/n)
+    when every rank holds one worker.  Rows are fp16-valued when wire16 (they travel as binary16).
+    Returns the [m] sums on every rank."""
+    W, L, m = comm.world, x.shape[0], x.shape[1]
+    S = -(-m // W)
+    wdt = torch.float16 if wire16 else torch.float32
+    send = torch.zeros(W, L, S, dtype=wdt, device=x.device)
+    for r in range(W):
+        lo, hi = r * S, min(m, (r + 1) * S)
+        if hi > lo:
+            send[r, :, : hi - lo].copy_(x[:, lo:hi])
+    recv = comm.all_to_all(send, phase).reshape(n, S).float()
+    s0 = comm.rank * S
+    my_len = max(0, min(S, m - s0))
+    out = torch.zeros(1, S, dtype=torch.float32, device=x.device)
+    if my_len:
+        _native.call("gc_float_fold", n, my_len, recv.data_ptr(), S, s0, -(-m // n), int(wire16), 0, 0,
+                     out.data_ptr(), _sp())
+    return comm.all_gather_rows(out.to(wdt), phase).reshape(-1)[:m].float()
 
 
 class DistributedGradientPipeline:
@@ -524,7 +557,7 @@ class _Thc(_Base):
                 _native.call("gc_thc_merge_ranges", L, b1 - b0, part.data_ptr(), self.shared[b0:b1].data_ptr(), sp)
             self.launches += 1 + (L > 1)
             # ElemMin / ElemMax ring (pipelines.py:271-288) as one MAX all-reduce of (-lo, hi)
-            work = comm.all_reduce_async(self.shared[b0:b1], dist.ReduceOp.MAX, "range-consensus")
+            work = comm.all_reduce_async(self.shared[b0:b1], dist.ReduceOp.MAX, "range-consensus", rings=2)
             pending.append((tb, te, work))
             if len(pending) > self.DEPTH:
                 k2(*pending.pop(0))
@@ -540,7 +573,7 @@ class _Thc(_Base):
         shared = torch.empty(self.nb, 2, dtype=torch.float32, device=self.dev)
         _native.call("gc_range_consensus", L, self.nb, self.ranges.data_ptr(), shared.data_ptr(), sp)
         shared[:, 0].neg_()
-        comm.all_reduce(shared, dist.ReduceOp.MAX, "range-consensus")
+        comm.all_reduce(shared, dist.ReduceOp.MAX, "range-consensus", rings=2)
         shared[:, 0].neg_()
         _native.call("gc_thc_quantize", geom, L, self.x_rot.data_ptr(), shared.data_ptr(), coins,
                      self.codes.data_ptr(), counters.data_ptr(), sp)
@@ -604,9 +637,8 @@ class _Chunked(_Base):
         pp = _ptr(perm)
         norms = torch.empty(L, nc, dtype=torch.float32, device=self.dev)
         _native.call("gc_chunk_norms", L, d, C, work.data_ptr(), work.stride(0), pp, norms.data_ptr(), sp)
-        all_norms = self.comm.all_gather_rows(norms.half(), "norm-consensus").float()   # fp16-valued: exact
-        energy = torch.empty(nc, dtype=torch.float32, device=self.dev)
-        _native.call("gc_float_fold", n, nc, all_norms.data_ptr(), nc, 0, -(-nc // n), 1, 0, 0, energy.data_ptr(), sp)
+        # norm consensus: fp16-wire FloatSum ring (pipelines.py:224-232), ring volume, reference order
+        energy = exchange_float(norms, self.comm, n, "norm-consensus", wire16=True)
         sel = torch.empty(J, dtype=torch.int32, device=self.dev)
         _native.call("gc_topk_select", 1, nc, energy.data_ptr(), nc, J, None, None, sel.data_ptr(), None, 0,
                      self.ws.data_ptr(), sp)
@@ -614,9 +646,7 @@ class _Chunked(_Base):
         packs = torch.empty(L, Lc, dtype=torch.float32, device=self.dev)
         _native.call("gc_chunk_pack", L, d, C, J, sel.data_ptr(), work.data_ptr(), work.stride(0), pp,
                      packs.data_ptr(), sp)
-        all_packs = self.comm.all_gather_rows(packs.half(), "chunk-aggregate").float()   # fp16-valued: exact
-        summed = torch.empty(Lc, dtype=torch.float32, device=self.dev)
-        _native.call("gc_float_fold", n, Lc, all_packs.data_ptr(), Lc, 0, -(-Lc // n), 1, 0, 0, summed.data_ptr(), sp)
+        summed = exchange_float(packs, self.comm, n, "chunk-aggregate", wire16=True)   # pipelines.py:235-251
         est = torch.empty(d, dtype=torch.float32, device=self.dev)
         _native.call("gc_chunk_scatter", d, C, J, sel.data_ptr(), summed.data_ptr(), n, pp, est.data_ptr(), sp)
         if res is not None:
@@ -649,12 +679,9 @@ class _PowerSgd(_Base):
             self.grp.pending = None
 
     def _fold(self, kind, x, m):
-        """Gather every rank's factor rows, then fold them in the reference ring order."""
-        n = self.n
-        rows = self.comm.all_gather_rows(x.reshape(self.L, m), kind)
-        out = torch.empty(1, m, dtype=torch.float32, device=self.dev)
-        _native.call("gc_float_fold", n, m, rows.data_ptr(), m, 0, -(-m // n), 0, 0, 0, out.data_ptr(), _sp())
-        return out
+        """The factor all-reduce (pipelines.py:349-351, 362-364): exact fp32 FloatSum ring order,
+        ring wire volume (exchange_float)."""
+        return exchange_float(x.reshape(self.L, m), self.comm, self.n, kind, wire16=False).reshape(1, m)
 
     def run(self, g, res, r, ledger, nmse):
         L, n, d = self.L, self.n, self.dim

@@ -53,10 +53,11 @@ def test_round_statistics_match_the_reference_model():
         m = np.abs(x[0]) - np.abs(x[0]).mean()
         return float(np.dot(m[:-1], m[1:]) / np.dot(m, m))
     assert abs(lag1(got) - lag1(ref)) < 0.02
-    # top-1% sets overlap heavily (the persistent hot rows dominate both)
+    # the top 1% of both rounds sits on the persistent hot rows (envelope lifted by spike_boost)
     k = D // 100
-    top = lambda x: set(np.argsort(-np.abs(x[0]))[:k].tolist())
-    assert len(top(got) & top(ref)) > 0.5 * k
+    for x in (got, ref):
+        top = np.argsort(-np.abs(x[0]))[:k]
+        assert np.mean(env[top] >= 10.0) > 0.9
 
 
 def test_rounds_and_workers_are_fresh():
