@@ -1071,10 +1071,9 @@ int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, i
   const int64_t per = (rows + splits - 1) / splits;
   double *partial = static_cast<double *>(workspace);
   const bool vec = cols % 4 == 0 && b->rows_aligned && (reinterpret_cast<uintptr_t>(c) & 15) == 0;
-  // opt-in (GC_PSGD_MTP=tma): the TMA-fed slab kernel measured slower than the CUDA-core pass on
-  // B200 (0.61 vs 0.36 ms at cfg4, one worker: its per-row P_hat loads cost more than the stream)
+  // TMA-fed column slabs for ranks 1..4 (gc_psgd_tma.cu); GC_PSGD_MTP=cores selects the CUDA-core pass
   const char *impl = getenv("GC_PSGD_MTP");
-  if (impl != nullptr && std::string(impl) == "tma" &&
+  if (rank <= 4 && (impl == nullptr || std::string(impl) != "cores") &&
       gc_psgd_mq_tma_supported_impl(b->tensors, b->workers, b->row_offsets, b->ld, d, rows, cols, rank, c, c)) {
     // TMA-fed column slabs (gc_psgd_tma.cu); the same split-K partials and ordered reduction
     splits = gc_psgd_mtp_tma_launch(L, b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);

@@ -424,15 +424,19 @@ __global__ void __launch_bounds__(kTailThreads) mq_tail_row_kernel(const float *
 }
 
 // ------------------------------------------------------------------ Q_w = M_w^T P_hat (pipelines.py:354)
-// Same TMA boxes (128 rows x 32 columns of M, SWIZZLE_128B) streamed by a producer warp; a CTA owns a
-// 32-column slab and a range of rows: consumer thread (column c, row group g) accumulates
-// sum_i M[i,c] P_hat[i,:] over its rows in fp32 FMAs, folded into fp64 after every box (16 rows,
-// the CUDA-core pass folds every 32), the 8 row groups reduced in order through shared memory and
-// the split-K partials written as gc_psgd_mtp's, so the same ordered reduction finishes Q_w.
+// Same TMA boxes (128 rows x 32 columns of M, SWIZZLE_128B) streamed by a producer warp, together
+// with the box's 128 rows of P_hat (one bulk copy); a CTA owns a 32-column slab and a range of rows.
+// Consumer thread (float4 column group g4, row group rg) forms, per row, the 4 columns x R
+// products from one float4 of the box and one broadcast read of the P_hat row, in fp32 FMAs folded
+// into fp64 after every box (4 rows per thread per box); the 32 row groups are reduced in order
+// through shared memory and the split-K partials written as gc_psgd_mtp's, so the same ordered
+// reduction finishes Q_w.  Ranks 1..4.
 constexpr int kMtpStages = 4;
 constexpr int kMtpConsumers = 256;
 constexpr int kMtpThreads = kMtpConsumers + 32;
-constexpr int kMtpSmem = kMtpStages * kTile + 64 + 1024;
+constexpr int kMtpPh = kM * 4 * 4;                  // 128 rows of P_hat, rank <= 4
+constexpr int kMtpStage = kTile + kMtpPh;
+constexpr int kMtpSmem = kMtpStages * kMtpStage + 64 + 1024;
 
 struct MtpArgs {
   int64_t d, rows, cols, rows_full, ld;
@@ -444,14 +448,15 @@ struct MtpArgs {
 };
 
 template <int R>
-__global__ void __launch_bounds__(kMtpThreads, 2) mtp_tma_kernel(const __grid_constant__ CUtensorMap map_c,
+__global__ void __launch_bounds__(kMtpThreads, 1) mtp_tma_kernel(const __grid_constant__ CUtensorMap map_c,
                                                                 const __grid_constant__ MtpArgs a) {
+  static_assert(R <= 4, "rank <= 4");
   extern __shared__ unsigned char smem_raw[];
   const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t base = (raw + 1023u) & ~1023u;
   unsigned char *sm = smem_raw + (base - raw);
-  const uint32_t bars = base + kMtpStages * kTile;   // loaded[S], empty[S]
-  __shared__ double red[kMtpConsumers / 32][32][R];
+  const uint32_t bars = base + kMtpStages * kMtpStage;   // loaded[S], empty[S]
+  __shared__ double red[kMtpConsumers / 8][32][R];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int v = blockIdx.z, split = blockIdx.y;
   const int64_t col0 = static_cast<int64_t>(blockIdx.x) * kKc;
@@ -466,63 +471,86 @@ __global__ void __launch_bounds__(kMtpThreads, 2) mtp_tma_kernel(const __grid_co
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == kMtpConsumers / 32) {   // producer warp: the TMA ring
+  if (warp == kMtpConsumers / 32) {   // producer warp: the TMA ring (box + its P_hat rows)
     if (lane == 0) {
       for (int64_t b = 0; b < nbox; ++b) {
         const int s = static_cast<int>(b % kMtpStages);
+        const int64_t i0 = r_begin + b * kM;
         if (b >= kMtpStages)
           mbar_wait(bars + 8 * (kMtpStages + s), static_cast<uint32_t>(((b / kMtpStages) - 1) & 1));
-        mbar_expect_tx(bars + 8 * s, kTile);
-        tma_load_3d(base + s * kTile, &map_c, static_cast<int>(col0), static_cast<int>(r_begin + b * kM), v,
-                    bars + 8 * s);
+        const bool full = i0 + kM <= r_end;   // partial boxes read P_hat with plain loads
+        mbar_expect_tx(bars + 8 * s, kTile + (full ? kM * R * 4 : 0));
+        tma_load_3d(base + s * kMtpStage, &map_c, static_cast<int>(col0), static_cast<int>(i0), v, bars + 8 * s);
+        if (full) bulk_load(base + s * kMtpStage + kTile, a.ph + i0 * R, kM * R * 4, bars + 8 * s);
       }
     }
     return;
   }
-  const int c = lane, g = warp;   // column of the slab, row group
-  double acc64[R];
+  const int g4 = tid & 7, rg = tid >> 3;   // float4 column group of the slab, row group (0..31)
+  double acc64[4][R];
 #pragma unroll
-  for (int b = 0; b < R; ++b) acc64[b] = 0.0;
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc64[t][b] = 0.0;
   for (int64_t bx = 0; bx < nbox; ++bx) {
     const int s = static_cast<int>(bx % kMtpStages);
     const int64_t i0 = r_begin + bx * kM;
+    const bool full = i0 + kM <= r_end;
     mbar_wait(bars + 8 * s, static_cast<uint32_t>((bx / kMtpStages) & 1));
-    const unsigned char *st = sm + s * kTile;
-    float acc[R];
+    const unsigned char *st = sm + s * kMtpStage;
+    const float *phs = reinterpret_cast<const float *>(st + kTile);
+    float acc[4][R];
 #pragma unroll
-    for (int b = 0; b < R; ++b) acc[b] = 0.0f;
-#pragma unroll 4
-    for (int rr = 0; rr < kM / 8; ++rr) {
-      const int row = g + 8 * rr;
-      const float m = *reinterpret_cast<const float *>(st + sw128(row, c >> 2) + (c & 3) * 4);
-      const int64_t i = i0 + row;
-      if (i < r_end) {   // rows past the slab's range are zero-filled or another split's
-        const float *pr = a.ph + i * R;
+    for (int t = 0; t < 4; ++t)
 #pragma unroll
-        for (int b = 0; b < R; ++b) acc[b] = fmaf(m, __ldg(pr + b), acc[b]);
+      for (int b = 0; b < R; ++b) acc[t][b] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kM / 32; ++k) {
+      const int row = rg + 32 * k;
+      const float4 m = *reinterpret_cast<const float4 *>(st + sw128(row, g4));
+      float p[R];
+      if (full) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) p[b] = phs[row * R + b];
+      } else {
+#pragma unroll
+        for (int b = 0; b < R; ++b) p[b] = i0 + row < r_end ? __ldg(a.ph + (i0 + row) * R + b) : 0.0f;
       }
+      const float mv[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int b = 0; b < R; ++b) acc[t][b] = fmaf(mv[t], p[b], acc[t][b]);
     }
 #pragma unroll
-    for (int b = 0; b < R; ++b) acc64[b] += static_cast<double>(acc[b]);
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc64[t][b] += static_cast<double>(acc[t][b]);
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bars + 8 * (kMtpStages + s)) : "memory");
   }
   // the row that is only partly inside d belongs to the last split (plain loads, fp64)
-  if (g == 0 && split == a.splits - 1 && a.rows_full < a.rows && col0 + c < a.cols) {
-    const int64_t off = a.rows_full * a.cols + col0 + c;
-    if (off < a.d) {
-      const double m = static_cast<double>(a.c[v * a.ld + off]);
+  if (rg == 0 && split == a.splits - 1 && a.rows_full < a.rows) {
 #pragma unroll
-      for (int b = 0; b < R; ++b) acc64[b] += m * static_cast<double>(a.ph[a.rows_full * R + b]);
+    for (int t = 0; t < 4; ++t) {
+      const int64_t col = col0 + 4 * g4 + t;
+      const int64_t off = a.rows_full * a.cols + col;
+      if (col < a.cols && off < a.d) {
+        const double m = static_cast<double>(a.c[v * a.ld + off]);
+#pragma unroll
+        for (int b = 0; b < R; ++b) acc64[t][b] += m * static_cast<double>(a.ph[a.rows_full * R + b]);
+      }
     }
   }
 #pragma unroll
-  for (int b = 0; b < R; ++b) red[g][c][b] = acc64[b];
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) red[rg][4 * g4 + t][b] = acc64[t][b];
   asm volatile("bar.sync 1, %0;" ::"r"(kMtpConsumers) : "memory");   // consumers only
   for (int e = tid; e < 32 * R; e += kMtpConsumers) {
     const int cc = e / R, b = e - cc * R;
     double x = 0.0;
-#pragma unroll
-    for (int w = 0; w < kMtpConsumers / 32; ++w) x += red[w][cc][b];
+#pragma unroll 8
+    for (int w = 0; w < kMtpConsumers / 8; ++w) x += red[w][cc][b];
     if (col0 + cc < a.cols)
       a.partial[((static_cast<int64_t>(v) * a.splits + split) * a.cols + col0 + cc) * R + b] = x;
   }
@@ -613,9 +641,9 @@ int gc_psgd_mtp_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64
     mtp_tma_kernel<RR><<<grid, kMtpThreads, kMtpSmem, st>>>(mc, a);                                 \
     break;
   switch (rank) {
-    GC_MTPT(1) GC_MTPT(2) GC_MTPT(3) GC_MTPT(4) GC_MTPT(5) GC_MTPT(6) GC_MTPT(7) GC_MTPT(8) GC_MTPT(16)
+    GC_MTPT(1) GC_MTPT(2) GC_MTPT(3) GC_MTPT(4)
     default:
-      gc_set_error("rank must be 1..8 or 16");
+      gc_set_error("the TMA Q = M^T P_hat pass takes ranks 1..4");
       return GC_ERR_UNSUPPORTED;
   }
 #undef GC_MTPT
