@@ -224,15 +224,19 @@ def exchange_float(x: torch.Tensor, comm: Comm, n: int, phase: str | None, wire1
     W, L, m = comm.world, x.shape[0], x.shape[1]
     S = -(-m // W)
     wdt = torch.float16 if wire16 else torch.float32
-    send = torch.zeros(W, L, S, dtype=wdt, device=x.device)
+    send = torch.empty(W, L, S, dtype=wdt, device=x.device)
     for r in range(W):
         lo, hi = r * S, min(m, (r + 1) * S)
         if hi > lo:
             send[r, :, : hi - lo].copy_(x[:, lo:hi])
+        if hi - lo < S:   # the padded tail of the last slices (never folded; zero on the wire)
+            send[r, :, max(0, hi - lo):].zero_()
     recv = comm.all_to_all(send, phase).reshape(n, S).float()
     s0 = comm.rank * S
     my_len = max(0, min(S, m - s0))
-    out = torch.zeros(1, S, dtype=torch.float32, device=x.device)
+    out = torch.empty(1, S, dtype=torch.float32, device=x.device)
+    if my_len < S:
+        out[:, my_len:].zero_()
     if my_len:
         _native.call("gc_float_fold", n, my_len, recv.data_ptr(), S, s0, -(-m // n), int(wire16), 0, 0,
                      out.data_ptr(), _sp())
