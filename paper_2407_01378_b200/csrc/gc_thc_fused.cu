@@ -83,7 +83,7 @@ __host__ __device__ inline Layout layout_for(int n, int nblk, int q) {
   const int lut_n = nblk * ((1 << q) - 1);
   L.sgn = L.lut + ((lut_n < kLutMax ? lut_n : kLutMax) * 8 + 15) / 16 * 16;          // 2 x 32 u32 sign words (double-buffered by tile parity)
   L.pcg = L.sgn + 256;                  // n x 16 u32: the worker's 4-step and tile-step LCG jumps
-  L.total = L.pcg + n * 64;
+  L.total = L.pcg + n * 64 + 32 + n * 16;   // + loop invariants (8 ints) + per-warp counters (4 ints)
   return L;
 }
 
@@ -163,11 +163,40 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
   // sign words of the next tile are loaded one tile ahead (the forward rotation needs them first)
   uint32_t next_sign_word = 0;
   if (a.tile_begin + blockIdx.x < a.tiles) next_sign_word = a.signs[((a.tile_begin + blockIdx.x) * kTileN >> 5) + lane];
-  for (int64_t tile = a.tile_begin + blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+  // loop-carried tile bookkeeping instead of per-tile 64-bit divisions: the estimate warp
+  // (tile mod n), the sign-buffer parity, and the ring block of the tile start (t0 / ring_blk with
+  // its remainder; a tile crosses at most one ring-block boundary when ring_blk >= 1024)
+  const int64_t first_tile = a.tile_begin + blockIdx.x;
+  const int64_t stride_elems = static_cast<int64_t>(gridDim.x) * kTileN;
+  // (32-bit: ring_blk = ceil(P / n) <= 2^30 and the quotient is a worker index)
+  const bool ring_incr = a.ring_blk >= kTileN && a.ring_blk < (int64_t{1} << 31);
+  const int rb = static_cast<int>(a.ring_blk);
+  // loop invariants and the per-warp tile counters live in shared memory (registers are at the
+  // 128 cap): inv[0..3] = gridDim % n, ring quotient / remainder steps, fold share per warp;
+  // wst = {estimate warp, ring block of the tile start, its remainder, sign-buffer parity}
+  int *inv = reinterpret_cast<int *>(smem + L.pcg) + n * 16;
+  int *wst = inv + 8 + 4 * w;
+  if (threadIdx.x == 0) {
+    inv[0] = static_cast<int>(gridDim.x % n);
+    inv[1] = ring_incr ? static_cast<int>(stride_elems / a.ring_blk) : 0;
+    inv[2] = ring_incr ? static_cast<int>(stride_elems % a.ring_blk) : 0;
+    inv[3] = (kTileN + n - 1) / n;
+    inv[4] = rb;
+    inv[5] = ring_incr ? 1 : 0;
+  }
+  if (lane == 0) {
+    const int q0 = ring_incr ? static_cast<int>((first_tile * kTileN) / a.ring_blk) : 0;
+    wst[0] = static_cast<int>(first_tile % n);
+    wst[1] = q0;
+    wst[2] = ring_incr ? static_cast<int>(first_tile * kTileN - static_cast<int64_t>(q0) * a.ring_blk) : 0;
+    wst[3] = 0;
+  }
+  __syncthreads();
+  for (int64_t tile = first_tile; tile < a.tiles; tile += gridDim.x) {
     const int64_t t0 = tile * kTileN;
     const uint32_t my_sign_word = next_sign_word;
     if (tile + gridDim.x < a.tiles) next_sign_word = a.signs[((tile + gridDim.x) * kTileN >> 5) + lane];
-    uint32_t *sgn = sgn_all + (((tile - a.tile_begin) / gridDim.x) & 1) * 32;
+    uint32_t *sgn = sgn_all + wst[3] * 32;
     {   // pull the next tile of this worker's g and r rows into L2 while this tile computes
       const int64_t tn = t0 + static_cast<int64_t>(gridDim.x) * kTileN;
       if (lane < 2 && tn + kTileN <= min(a.dim, a.tiles * kTileN) && a.aligned) {
@@ -247,12 +276,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
     wht_tile<K>(v, scratch, lane);
     // lane's sign "column": bit j = sign of element 32j + lane (layout B), from 32 ballots over
     // the row words the lanes already hold -- the own-decode epilogue then reads no shared memory
-    uint32_t sign_col = 0;
-#pragma unroll
-    for (int b = 0; b < 32; ++b) {
-      const uint32_t m = __ballot_sync(0xffffffffu, (my_sign_word >> b) & 1u);
-      sign_col = lane == b ? m : sign_col;
-    }
+    const uint32_t sign_col = bit_transpose32(my_sign_word, lane);
 
     // ---- x_rot = f32(v * B^-1/2), staged in layout B; per-block (min, max) (compressors.py:447-453)
     {
@@ -336,7 +360,11 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
           const float4 sp =
               rpb_log >= 2 ? sp_j : *reinterpret_cast<const float4 *>(bp + 8 * ((j + c) >> rpb_log) + 6);
           hw[c] = ch[c].out_hi(oa[c], ob[c], orot[c]);
+#if GC_THC_IMM
+          ch[c].step128(c128);
+#else
           ch[c].step(m128, c128);
+#endif
           xv[c] = xs[(j + c) * 32 + lane];
           // fp32 screen: floor by the 1.5 * 2^23 magic constant (|t32| < 2^22), frac, 23-bit coin;
           // safe iff min(f, 1 - f, |c23 - f|) > H (1 - f is exact for f >= 1/2)
@@ -389,16 +417,17 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
 
     // ---- ring-ordered saturating fold (SatIntSum, collectives.py:123-143, 215-226), split
     // over all warps; dequantize_sum(., n) lands in the estimate warp's transpose rows.
-    const int ew = static_cast<int>(tile % n);
+
+    const int ew = wst[0];
     double *escr = reinterpret_cast<double *>(smem + L.scratch) + ew * (32 * kScrRow);
     {
       const double nd = static_cast<double>(n);
-      const int per = (kTileN + n - 1) / n;
+      const int per = inv[3];
       const int e_end = min(kTileN, (w + 1) * per);
       if (simd_fold) {
         // four coordinates per lane as packed int8 (ring blocks are 4-aligned here)
         for (int e = w * per + lane * 4; e < e_end; e += 128) {
-          const int s0 = static_cast<int>((t0 + e) / a.ring_blk);
+          const int s0 = inv[5] ? wst[1] + (wst[2] + e >= inv[4] ? 1 : 0) : static_cast<int>((t0 + e) / a.ring_blk);
           uint32_t acc = *reinterpret_cast<const uint32_t *>(cod_all + s0 * 1024 + e);
           int u = s0;
           for (int m = 1; m < n; ++m) {
@@ -428,7 +457,8 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
       } else {
         for (int e = w * per + lane; e < e_end; e += 32) {
           const int64_t i = t0 + e;
-          const int s0 = static_cast<int>(i / a.ring_blk);   // ring block j starts at worker j
+          // ring block j starts at worker j
+          const int s0 = inv[5] ? wst[1] + (wst[2] + e >= inv[4] ? 1 : 0) : static_cast<int>(i / a.ring_blk);
           long long acc = cod_all[s0 * 1024 + e];
           int u = s0;
           for (int m = 1; m < n; ++m) {
@@ -556,6 +586,22 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
     // (C) end of tile: only the nmse reduction needs it (it reads every warp's cbuf); all other
     // buffers are protected by barriers A / B / D of the next tile (sign words double-buffered).
     if (a.nmse) __syncthreads();
+    __syncwarp();   // every lane of the warp is done with this tile's counters
+    if (lane == 0) {
+      int e2 = wst[0] + inv[0];
+      wst[0] = e2 >= n ? e2 - n : e2;
+      if (inv[5]) {
+        int q = wst[1] + inv[1], r = wst[2] + inv[2];
+        if (r >= inv[4]) {
+          r -= inv[4];
+          ++q;
+        }
+        wst[1] = q;
+        wst[2] = r;
+      }
+      wst[3] ^= 1;
+    }
+    __syncwarp();
   }
 
 #pragma unroll

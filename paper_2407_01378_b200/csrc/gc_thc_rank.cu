@@ -151,13 +151,7 @@ __device__ __forceinline__ void forward(double (&v)[32], const float *cbuf, uint
 
 // lane's sign "column" in layout B: bit j = sign of element 32j + lane
 __device__ __forceinline__ uint32_t sign_column(uint32_t sign_word, int lane) {
-  uint32_t col = 0;
-#pragma unroll
-  for (int b = 0; b < 32; ++b) {
-    const uint32_t m = __ballot_sync(0xffffffffu, (sign_word >> b) & 1u);
-    col = lane == b ? m : col;
-  }
-  return col;
+  return bit_transpose32(sign_word, lane);
 }
 
 // ---------------------------------------------------------------- K1: ranges
@@ -309,7 +303,11 @@ __global__ void __launch_bounds__(kWarps * 32, 4) rank_quant_kernel(const __grid
         for (int c = 0; c < 4; ++c) {
           const float4 sp = rpb_log >= 2 ? sp_j : *reinterpret_cast<const float4 *>(bp + 8 * ((j + c) >> rpb_log) + 6);
           hw[c] = ch[c].out_hi(oa[c], ob[c], orot[c]);
+#if GC_THC_IMM
+          ch[c].step128(c128);
+#else
           ch[c].step(m128, c128);
+#endif
           xv[c] = xs[(j + c) * 32 + lane];
           const float tq = (xv[c] - sp.x) * sp.y;
           const float sm = __fadd_rd(tq, 12582912.0f);

@@ -11,6 +11,10 @@
 
 #include "gc_device.cuh"
 
+#ifndef GC_THC_IMM
+#define GC_THC_IMM 1
+#endif
+
 namespace thc {
 
 constexpr int kTileN = 1024;
@@ -65,6 +69,21 @@ __device__ __forceinline__ double apply_sign(double x, uint32_t positive) {
   return __longlong_as_double(__double_as_longlong(x) ^ (static_cast<long long>(positive ^ 1u) << 63));
 }
 
+// 32 x 32 bit-matrix transpose across the warp (row = lane, column = bit): returns the word whose
+// bit j is bit `lane` of lane j's w.  Five shuffle stages swapping the off-diagonal blocks
+// (16, 8, 4, 2, 1) instead of 32 ballots; used for the layout-B sign "column" of a tile.
+__device__ __forceinline__ uint32_t bit_transpose32(uint32_t x, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int sft = 16 >> k;
+    const uint32_t m = masks[k];
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, sft);
+    x = (lane & sft) ? ((x & ~m) | ((y >> sft) & m)) : ((x & m) | ((y << sft) & ~m));
+  }
+  return x;
+}
+
 // PCG64 state as four 32-bit limbs (s0 least significant).  step(): s = s * m + c mod 2^128 as
 // a schoolbook column product with PTX carry chains (17 IMADs); output(): numpy's XSL-RR.
 struct Lcg {
@@ -101,6 +120,36 @@ struct Lcg {
     s2 = r2;
     s3 = r3;
   }
+
+#if GC_THC_IMM
+  // s = s * A^128 + c with the 128-step jump multiplier as instruction immediates
+  // (kPcgJump[7] mult = 0x602167331d86cf56'84fe009a6d09de01); c stays per-stream.
+  __device__ __forceinline__ void step128(const uint32_t (&c)[4]) {
+    uint32_t r0, r1, r2, r3;
+    asm("mad.lo.cc.u32  %0, %4, 0x6d09de01, %8;\n\t"
+        "madc.hi.cc.u32 %1, %4, 0x6d09de01, %9;\n\t"
+        "madc.hi.cc.u32 %2, %4, 0x84fe009a, %10;\n\t"
+        "madc.hi.u32    %3, %4, 0x1d86cf56, %11;\n\t"
+        "mad.lo.cc.u32  %1, %4, 0x84fe009a, %1;\n\t"
+        "madc.lo.cc.u32 %2, %4, 0x1d86cf56, %2;\n\t"
+        "madc.lo.u32    %3, %4, 0x60216733, %3;\n\t"
+        "mad.lo.cc.u32  %1, %5, 0x6d09de01, %1;\n\t"
+        "madc.hi.cc.u32 %2, %5, 0x6d09de01, %2;\n\t"
+        "madc.hi.u32    %3, %5, 0x84fe009a, %3;\n\t"
+        "mad.lo.cc.u32  %2, %5, 0x84fe009a, %2;\n\t"
+        "madc.lo.u32    %3, %5, 0x1d86cf56, %3;\n\t"
+        "mad.lo.cc.u32  %2, %6, 0x6d09de01, %2;\n\t"
+        "madc.hi.u32    %3, %6, 0x6d09de01, %3;\n\t"
+        "mad.lo.u32     %3, %6, 0x84fe009a, %3;\n\t"
+        "mad.lo.u32     %3, %7, 0x6d09de01, %3;"
+        : "=&r"(r0), "=&r"(r1), "=&r"(r2), "=&r"(r3)
+        : "r"(s0), "r"(s1), "r"(s2), "r"(s3), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]));
+    s0 = r0;
+    s1 = r1;
+    s2 = r2;
+    s3 = r3;
+  }
+#endif
 
   // the high half of the XSL-RR output; (a, b, rot) let lo_of() rebuild the low half on demand
   __device__ __forceinline__ uint32_t out_hi(uint32_t &a, uint32_t &b, uint32_t &rot) const {
