@@ -319,6 +319,15 @@ int gc_psgd_mq_tma_supported(const gc_psgd_batch *b, int64_t d, int64_t rows, in
 int gc_psgd_mq_deferred(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
                         float *resid, const float *q, const float *ef_p_hat, const float *ef_q_workers, float *p,
                         void *workspace, void *stream);
+/* The same for a batch of T same-shape tensors (chunked PowerSGD: one group per matrix shape; row
+ * v = t * workers + w at row_offsets[v] = w * ld + host_tensor_offsets[t]): one tensor map per
+ * tensor (the host needs the tensor offsets, host_tensor_offsets[T]; each a multiple of 4). */
+int gc_psgd_mq_tma_supported_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offsets, int64_t d,
+                                     int64_t rows, int64_t cols, int32_t rank, const void *grads, const void *resid);
+int gc_psgd_mq_deferred_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offsets, int64_t d, int64_t rows,
+                                int64_t cols, int32_t rank, const float *grads, float *resid, const float *q,
+                                const float *ef_p_hat, const float *ef_q_workers, float *p, void *workspace,
+                                void *stream);
 /* Q_w = M_w^T P_hat (pipelines.py:354). */
 int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                 const float *p_hat, float *q, void *workspace, void *stream);

@@ -1032,33 +1032,55 @@ int gc_psgd_mq_fused(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t co
 
 int gc_psgd_mq_tma_supported(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank,
                              const void *grads, const void *resid) {
+  if (b == nullptr || d < 1 || rows * cols < d || b->tensors != 1 || b->row_offsets != nullptr) return 0;
+  return gc_psgd_mq_tma_supported_impl(1, b->workers, nullptr, b->ld, d, rows, cols, rank, grads, resid);
+}
+
+int gc_psgd_mq_tma_supported_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offsets, int64_t d,
+                                     int64_t rows, int64_t cols, int32_t rank, const void *grads, const void *resid) {
   if (b == nullptr || d < 1 || rows * cols < d) return 0;
-  return gc_psgd_mq_tma_supported_impl(b->tensors, b->workers, b->row_offsets, b->ld, d, rows, cols, rank, grads,
+  // a batch with row offsets needs the host copy of its tensor offsets (one tensor map per tensor)
+  if ((b->tensors > 1 || b->row_offsets != nullptr) && (host_tensor_offsets == nullptr || b->row_offsets == nullptr))
+    return 0;
+  return gc_psgd_mq_tma_supported_impl(b->tensors, b->workers, host_tensor_offsets, b->ld, d, rows, cols, rank, grads,
                                        resid);
 }
 
-int gc_psgd_mq_deferred(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
-                        float *resid, const float *q, const float *ef_p_hat, const float *ef_q_workers, float *p,
-                        void *workspace, void *stream) {
+int gc_psgd_mq_deferred_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offsets, int64_t d, int64_t rows,
+                                int64_t cols, int32_t rank, const float *grads, float *resid, const float *q,
+                                const float *ef_p_hat, const float *ef_q_workers, float *p, void *workspace,
+                                void *stream) {
   if (int rc = check_batch(b)) return rc;
   GC_REQUIRE(d >= 1 && rows * cols >= d && grads && q && p && workspace, "invalid argument");
   GC_REQUIRE((ef_p_hat == nullptr) == (ef_q_workers == nullptr), "deferred EF needs both factors or neither");
   GC_REQUIRE(ef_p_hat == nullptr || resid != nullptr, "deferred EF needs the residual buffer");
-  if (!gc_psgd_mq_tma_supported(b, d, rows, cols, rank, grads, resid)) {
-    gc_set_error("TMA P = M Q needs one tensor (no row offsets), cols % 4 == 0, ld % 4 == 0, 16-byte aligned "
-                 "rows, d >= cols and a compiled rank");
+  if (!gc_psgd_mq_tma_supported_batched(b, host_tensor_offsets, d, rows, cols, rank, grads, resid)) {
+    gc_set_error("TMA P = M Q needs cols % 4 == 0, ld % 4 == 0, 16-byte aligned tensor starts (host offsets for a "
+                 "batch of tensors), d >= cols and a compiled rank");
     return GC_ERR_UNSUPPORTED;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int L = b->tensors * b->workers;
-  const int slabs = gc_psgd_mq_tma_launch(L, b->ld, d, rows, cols, rank, grads, resid, q, ef_p_hat, ef_q_workers,
-                                          static_cast<double *>(workspace), (cols + 1023) / 1024, st);
+  const int slabs = gc_psgd_mq_tma_launch(b->tensors, b->workers, host_tensor_offsets, b->row_offsets, b->ld, d, rows,
+                                          cols, rank, grads, resid, q, ef_p_hat,
+                                          ef_q_workers, static_cast<double *>(workspace), (cols + 1023) / 1024, st);
   if (slabs < 0) return slabs;
   const int64_t total = static_cast<int64_t>(L) * rows * rank;
   mq_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(
       L, slabs, rows, rank, static_cast<const double *>(workspace), p);
   GC_LAUNCH_CHECK("mq_reduce_kernel");
   return GC_OK;
+}
+
+int gc_psgd_mq_deferred(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
+                        float *resid, const float *q, const float *ef_p_hat, const float *ef_q_workers, float *p,
+                        void *workspace, void *stream) {
+  if (b != nullptr && (b->tensors != 1 || b->row_offsets != nullptr)) {
+    gc_set_error("gc_psgd_mq_deferred takes one tensor without row offsets; see gc_psgd_mq_deferred_batched");
+    return GC_ERR_UNSUPPORTED;
+  }
+  return gc_psgd_mq_deferred_batched(b, nullptr, d, rows, cols, rank, grads, resid, q, ef_p_hat, ef_q_workers, p,
+                                     workspace, stream);
 }
 
 int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
@@ -1073,8 +1095,9 @@ int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, i
   const bool vec = cols % 4 == 0 && b->rows_aligned && (reinterpret_cast<uintptr_t>(c) & 15) == 0;
   // TMA-fed column slabs for ranks 1..4 (gc_psgd_tma.cu); GC_PSGD_MTP=cores selects the CUDA-core pass
   const char *impl = getenv("GC_PSGD_MTP");
-  if (rank <= 4 && (impl == nullptr || std::string(impl) != "cores") &&
-      gc_psgd_mq_tma_supported_impl(b->tensors, b->workers, b->row_offsets, b->ld, d, rows, cols, rank, c, c)) {
+  if (rank <= 4 && (impl == nullptr || std::string(impl) != "cores") && b->tensors == 1 &&
+      b->row_offsets == nullptr &&
+      gc_psgd_mq_tma_supported_impl(1, b->workers, nullptr, b->ld, d, rows, cols, rank, c, c)) {
     // TMA-fed column slabs (gc_psgd_tma.cu); the same split-K partials and ordered reduction
     splits = gc_psgd_mtp_tma_launch(L, b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);
     if (splits < 0) return splits;

@@ -125,8 +125,19 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                : "memory");
 }
 
+// A batch of T same-shape tensors (the chunked PowerSGD of a model: one group per matrix shape):
+// one 3-D tensor map [L workers][rows_full][cols] per tensor in each direction.
+constexpr int kMaxMapT = 48;
+struct MapSet {
+  CUtensorMap g[kMaxMapT];
+  CUtensorMap r[kMaxMapT];
+};
+
 struct TmaArgs {
   int64_t d, rows, cols, rows_full;
+  int L;                   // workers per tensor: virtual row v = t * L + w
+  int v_base;              // first virtual row of this launch (tensor chunks of <= kMaxMapT)
+  const int64_t *row_start;   // device [T * L] element offset of each virtual row (tail-row kernel)
   const float *q;          // [cols][R] (one tensor)
   const float *ef_ph;      // deferred EF: P_hat_prev [rows][R] or NULL
   const float *ef_qw;      // deferred EF: Q_w_prev [L][cols][R]
@@ -148,8 +159,7 @@ __device__ __forceinline__ float own_of(const float *pa, const float *qv) {
 
 template <int R, bool DEF>
 __global__ void __launch_bounds__(kThreads, 1)
-    mq_tma_kernel(const __grid_constant__ CUtensorMap map_g, const __grid_constant__ CUtensorMap map_r,
-                  const __grid_constant__ TmaArgs a) {
+    mq_tma_kernel(const __grid_constant__ MapSet maps, const __grid_constant__ TmaArgs a) {
   extern __shared__ unsigned char smem_raw[];
   const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -164,7 +174,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + kStages * kStageBytes + kPhBytes + 8 * (3 * kStages + 2));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int v = blockIdx.z;   // worker
+  const int vl = blockIdx.z;                 // virtual row within this launch
+  const int v = a.v_base + vl;               // (tensor, worker) row of the batch
+  const int tl = vl / a.L, w = vl - tl * a.L;   // tensor within the launch, worker
+  const int t = v / a.L;                     // tensor within the batch
+  const CUtensorMap *map_g = &maps.g[tl];
+  const CUtensorMap *map_r = &maps.r[tl];
+  const float *qt = a.q + static_cast<int64_t>(t) * a.cols * R;
+  const float *pht = DEF ? a.ef_ph + static_cast<int64_t>(t) * a.rows * R : nullptr;
   const int split = blockIdx.y;
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kM;
   const int64_t nchunks_all = (a.cols + kKc - 1) / kKc;
@@ -197,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (DEF) {   // the band's P_hat_prev rows (rows past d's matrix are never used)
     for (int e = tid; e < kM * R; e += kThreads) {
       const int64_t i = row0 + e / R;
-      ph_s[e] = i < a.rows ? a.ef_ph[i * R + e % R] : 0.0f;
+      ph_s[e] = i < a.rows ? pht[i * R + e % R] : 0.0f;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -213,10 +230,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t ncol = min(static_cast<int64_t>(kKc), a.cols - col0);
     const uint32_t qbytes = static_cast<uint32_t>(ncol * R * 4);
     mbar_expect_tx(loaded_bar(s), tx_bytes_box + qbytes * (DEF ? 2u : 1u));
-    tma_load_3d(stage(s) + kOffG, &map_g, static_cast<int>(col0), static_cast<int>(row0), v, loaded_bar(s));
+    tma_load_3d(stage(s) + kOffG, map_g, static_cast<int>(col0), static_cast<int>(row0), w, loaded_bar(s));
     if (a.has_resid)
-      tma_load_3d(stage(s) + kOffC, &map_r, static_cast<int>(col0), static_cast<int>(row0), v, loaded_bar(s));
-    bulk_load(stage(s) + kOffQ, a.q + col0 * R, qbytes, loaded_bar(s));
+      tma_load_3d(stage(s) + kOffC, map_r, static_cast<int>(col0), static_cast<int>(row0), w, loaded_bar(s));
+    bulk_load(stage(s) + kOffQ, qt + col0 * R, qbytes, loaded_bar(s));
     if (DEF) bulk_load(stage(s) + kOffW, qw_prev + col0 * R, qbytes, loaded_bar(s));
   };
 
@@ -266,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(empty_bar(s));
         if (k % kGroup == kGroup - 1 || k == nloc - 1) umma_commit(acc_bar(static_cast<int>(gi & 1)));
         if (a.has_resid) {   // corrected box back over the residual buffer (clipped to the map)
-          tma_store_3d(&map_r, stage(s) + kOffC, static_cast<int>(col0), static_cast<int>(row0), v);
+          tma_store_3d(map_r, stage(s) + kOffC, static_cast<int>(col0), static_cast<int>(row0), w);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         // refill the stages of chunks next - S .. next - S + kPair - 1 (all older than k) once their
@@ -377,16 +394,19 @@ template <int R, bool DEF>
 __global__ void __launch_bounds__(kTailThreads) mq_tail_row_kernel(const float *g, float *resid, int64_t ld,
                                                                   TmaArgs a) {
   __shared__ double red[kTailThreads / 32][R];
-  const int v = blockIdx.x;
+  const int v = a.v_base + blockIdx.x;
+  const int t = v / a.L;
   const int64_t i = a.rows_full;
   const int64_t n_valid = a.d - i * a.cols;
-  const float *gw = g + v * ld + i * a.cols;
-  float *rw = resid ? resid + v * ld + i * a.cols : nullptr;
+  const int64_t rs = a.row_start ? a.row_start[v] : static_cast<int64_t>(v) * ld;
+  const float *gw = g + rs + i * a.cols;
+  float *rw = resid ? resid + rs + i * a.cols : nullptr;
   const float *qw_prev = DEF ? a.ef_qw + static_cast<int64_t>(v) * a.cols * R : nullptr;
+  const float *qt = a.q + static_cast<int64_t>(t) * a.cols * R;
   float pa[R];
   if (DEF) {
 #pragma unroll
-    for (int b = 0; b < R; ++b) pa[b] = a.ef_ph[i * R + b];
+    for (int b = 0; b < R; ++b) pa[b] = a.ef_ph[(static_cast<int64_t>(t) * a.rows + i) * R + b];
   }
   double acc[R];
 #pragma unroll
@@ -405,7 +425,7 @@ __global__ void __launch_bounds__(kTailThreads) mq_tail_row_kernel(const float *
       rw[j] = c;
     }
 #pragma unroll
-    for (int b = 0; b < R; ++b) acc[b] += static_cast<double>(c) * static_cast<double>(a.q[j * R + b]);
+    for (int b = 0; b < R; ++b) acc[b] += static_cast<double>(c) * static_cast<double>(qt[j * R + b]);
   }
 #pragma unroll
   for (int b = 0; b < R; ++b) {
@@ -587,14 +607,18 @@ int grid_cap(int64_t g) { return static_cast<int>(g < 1 ? 1 : (g > 65535 ? 65535
 
 }  // namespace
 
-int gc_psgd_mq_tma_supported_impl(int32_t tensors, int32_t workers, const int64_t *row_offsets, int64_t ld, int64_t d,
-                                  int64_t rows, int64_t cols, int32_t rank, const void *grads, const void *resid) {
-  if (tensors != 1 || row_offsets != nullptr) return 0;
-  if (cols % 4 != 0 || (workers > 1 && ld % 4 != 0) || cols > (int64_t{1} << 31) - 1 ||
+int gc_psgd_mq_tma_supported_impl(int32_t tensors, int32_t workers, const int64_t *host_tensor_offsets, int64_t ld,
+                                  int64_t d, int64_t rows, int64_t cols, int32_t rank, const void *grads,
+                                  const void *resid) {
+  if (tensors < 1 || (tensors > 1 && host_tensor_offsets == nullptr)) return 0;
+  if (cols % 4 != 0 || ((workers > 1 || tensors > 1) && ld % 4 != 0) || cols > (int64_t{1} << 31) - 1 ||
       rows > (int64_t{1} << 31) - 1)
     return 0;
   if (d / cols < 1) return 0;
   if ((reinterpret_cast<uintptr_t>(grads) | reinterpret_cast<uintptr_t>(resid)) & 15) return 0;
+  if (host_tensor_offsets)
+    for (int t = 0; t < tensors; ++t)
+      if (host_tensor_offsets[t] % 4 != 0) return 0;
   switch (rank) {
     case 1: case 2: case 3: case 4: case 5: case 6: case 7: case 8: case 16: break;
     default: return 0;
@@ -658,31 +682,28 @@ int gc_psgd_mtp_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64
 // TMA-fed tcgen05 P = M Q with ef_apply (and, with ef_ph / ef_qw, the previous round's deferred
 // EF update).  fp64 split-K partials partial[w][split][row][R]; returns the split count or a
 // negative status.
-int gc_psgd_mq_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank,
-                          const float *grads, float *resid, const float *q, const float *ef_ph, const float *ef_qw,
-                          double *partial, int64_t max_splits, cudaStream_t st) {
+int gc_psgd_mq_tma_launch(int32_t T, int32_t L, const int64_t *host_tensor_offsets, const int64_t *row_start,
+                          int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
+                          float *resid, const float *q, const float *ef_ph, const float *ef_qw, double *partial,
+                          int64_t max_splits, cudaStream_t st) {
   const int64_t rows_full = d / cols;
   const int64_t row_blocks = (rows + kM - 1) / kM;
   const int64_t nchunks = (cols + kKc - 1) / kKc;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t splits = sms / (row_blocks * L);
+  int64_t splits = sms / (row_blocks * L * T);
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
   const int64_t per = (nchunks + splits - 1) / splits;
   splits = (nchunks + per - 1) / per;
-  CUtensorMap mg, mr;
-  std::memset(&mr, 0, sizeof(mr));
-  if (!make_map(&mg, grads, L, rows_full, cols, ld) || (resid && !make_map(&mr, resid, L, rows_full, cols, ld))) {
-    gc_set_error("cuTensorMapEncodeTiled failed for the P = M Q operands");
-    return GC_ERR_CUDA;
-  }
   TmaArgs a{};
   a.d = d;
   a.rows = rows;
   a.cols = cols;
   a.rows_full = rows_full;
+  a.L = L;
+  a.row_start = row_start;
   a.q = q;
   a.ef_ph = ef_ph;
   a.ef_qw = ef_qw;
@@ -691,12 +712,25 @@ int gc_psgd_mq_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_
   a.chunks_per_split = per;
   a.has_resid = resid != nullptr;
   const bool def = resid != nullptr && ef_ph != nullptr && ef_qw != nullptr;
-  const dim3 grid(grid_cap(row_blocks), static_cast<unsigned>(splits), static_cast<unsigned>(L));
   const bool tail = rows_full < rows && d > rows_full * cols;
+  MapSet maps;   // the launch's tensor maps, copied into the kernel parameter buffer at launch
+  for (int t0 = 0; t0 < T; t0 += kMaxMapT) {
+    const int tc = T - t0 < kMaxMapT ? T - t0 : kMaxMapT;
+    std::memset(&maps, 0, sizeof(maps));
+    for (int k = 0; k < tc; ++k) {
+      const int64_t off = host_tensor_offsets ? host_tensor_offsets[t0 + k] : 0;
+      if (!make_map(&maps.g[k], grads + off, L, rows_full, cols, ld) ||
+          (resid && !make_map(&maps.r[k], resid + off, L, rows_full, cols, ld))) {
+        gc_set_error("cuTensorMapEncodeTiled failed for the P = M Q operands");
+        return GC_ERR_CUDA;
+      }
+    }
+    a.v_base = t0 * L;
+    const dim3 grid(grid_cap(row_blocks), static_cast<unsigned>(splits), static_cast<unsigned>(tc * L));
 #define GC_TMA_LAUNCH(RR, DD)                                                                              \
   cudaFuncSetAttribute(mq_tma_kernel<RR, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);    \
-  mq_tma_kernel<RR, DD><<<grid, kThreads, kSmemBytes, st>>>(mg, mr, a);                                    \
-  if (tail) mq_tail_row_kernel<RR, DD><<<L, kTailThreads, 0, st>>>(grads, resid, ld, a);
+  mq_tma_kernel<RR, DD><<<grid, kThreads, kSmemBytes, st>>>(maps, a);                                      \
+  if (tail) mq_tail_row_kernel<RR, DD><<<tc * L, kTailThreads, 0, st>>>(grads, resid, ld, a);
 #define GC_TMA_CASE(RR)        \
   case RR:                     \
     if (def) {                 \
@@ -705,15 +739,16 @@ int gc_psgd_mq_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_
       GC_TMA_LAUNCH(RR, false) \
     }                          \
     break;
-  switch (rank) {
-    GC_TMA_CASE(1) GC_TMA_CASE(2) GC_TMA_CASE(3) GC_TMA_CASE(4) GC_TMA_CASE(5) GC_TMA_CASE(6)
-    GC_TMA_CASE(7) GC_TMA_CASE(8) GC_TMA_CASE(16)
-    default:
-      gc_set_error("rank must be 1..8 or 16");
-      return GC_ERR_UNSUPPORTED;
-  }
+    switch (rank) {
+      GC_TMA_CASE(1) GC_TMA_CASE(2) GC_TMA_CASE(3) GC_TMA_CASE(4) GC_TMA_CASE(5) GC_TMA_CASE(6)
+      GC_TMA_CASE(7) GC_TMA_CASE(8) GC_TMA_CASE(16)
+      default:
+        gc_set_error("rank must be 1..8 or 16");
+        return GC_ERR_UNSUPPORTED;
+    }
 #undef GC_TMA_CASE
 #undef GC_TMA_LAUNCH
+  }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     gc_set_error(std::string("mq_tma_kernel: ") + cudaGetErrorString(e));

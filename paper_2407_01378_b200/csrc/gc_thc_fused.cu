@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
         rowp[0] = e[0]; rowp[1] = e[1]; rowp[2] = e[2]; rowp[3] = e[3];
       }
       __syncthreads();   // (E) row stages done
-      const float nf = static_cast<float>(n);
+      const gc::DivN dn(n);   // / n (pipelines.py:308-311): exact reciprocal product for power-of-two n
       const double nd = static_cast<double>(n);
 #pragma unroll 1
       for (int gi = w; gi < 8; gi += n) {
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kMaxN * 32, 1) thc_fused_kernel(const __grid_c
           const int row = q4 + t;
           const int el = row * 32 + col;
           const int64_t i = t0 + el;
-          const float f = static_cast<float>(apply_sign(e[t] * a.scale, (sgn[row] >> col) & 1u)) / nf;
+          const float f = dn(static_cast<float>(apply_sign(e[t] * a.scale, (sgn[row] >> col) & 1u)));
           if (i < a.dim) {
             __stcs(a.est + i, f);
             if (n == 1 && rw) __stcs(ro + i, cbuf[cidx(el)] - f);   // one worker: own == estimate

@@ -94,7 +94,8 @@ class TensorListPipeline:
             rows = [w * D + int(self.offsets[t]) for t in ts for w in range(n)]
             ro = torch.tensor(rows, dtype=torch.int64, device=dev)
             eo = torch.tensor([int(self.offsets[t]) for t in ts], dtype=torch.int64, device=dev)
-            grp = PowerSgdGroup(cfg, n, n, s, len(ts), self.seeds, dev, row_offsets=ro, est_offsets=eo, ld=D)
+            grp = PowerSgdGroup(cfg, n, n, s, len(ts), self.seeds, dev, row_offsets=ro, est_offsets=eo, ld=D,
+                                host_offsets=[int(self.offsets[t]) for t in ts])
             grp.tensor_ids = ts
             grp.vec = grp.cols % 4 == 0 and all(x % 4 == 0 for x in rows) and D % 4 == 0
             self.groups.append(grp)
@@ -114,12 +115,20 @@ class TensorListPipeline:
     def residuals(self):
         if self._res is None:
             return None
+        self._sync_residuals()
         h = self._res.cpu().numpy()
         return [h[i].copy() for i in range(self.group.size)]
 
     @property
     def residuals_tensor(self):
+        if self._res is not None:
+            self._sync_residuals()
         return self._res
+
+    def _sync_residuals(self):
+        """Materialise the EF updates the PowerSGD groups deferred into their next P = M Q pass."""
+        for grp in getattr(self, "groups", []):
+            grp.materialize(self._res.data_ptr())
 
     def warm_q(self, tensor: int):
         """The warm-start Q of one tensor (pipelines.py:366), or None."""
@@ -193,6 +202,8 @@ class TensorListPipeline:
         # decode pass.  The nmse diagnostic needs every corrected vector before any residual
         # changes, so then ef_apply runs as one pass up front and the EF updates come last.
         fuse_ef = res is not None and acc is None
+        if res is not None and not fuse_ef:
+            self._sync_residuals()
         if res is not None and not fuse_ef:   # corrected vectors kept in r until the EF updates
             _native.call("gc_ef_apply", n, D, g.data_ptr(), res.data_ptr(), g.stride(0), res.data_ptr(),
                          res.stride(0), sp)
@@ -216,6 +227,7 @@ class TensorListPipeline:
                 grp.run(c.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, grads_ptr=g.data_ptr(),
                         vec=bool(grp.batch.rows_aligned), fold=self._fold, q=q, ef_resid_ptr=res.data_ptr())
             elif fuse_ef:   # unaligned rows: ef_apply on the group's tensors, then the plain passes
+                grp.materialize(res.data_ptr())
                 for t in grp.tensor_ids:
                     off = int(self.offsets[t])
                     _native.call("gc_ef_apply", n, self.sizes[t], g.data_ptr() + 4 * off, res.data_ptr() + 4 * off,

@@ -510,7 +510,7 @@ class PowerSgdGroup:
         return out
 
     def __init__(self, cfg: PowerSgdConfig, n: int, L: int, d: int, T: int, seeds: SeedSpec, device,
-                 row_offsets=None, est_offsets=None, ld: int = 0):
+                 row_offsets=None, est_offsets=None, ld: int = 0, host_offsets=None):
         self.cfg, self.n, self.L, self.d, self.T = cfg, n, L, d, T
         self.seeds, self.device = seeds, device
         self.rows, self.cols = matrix_shape_for(d)
@@ -521,6 +521,7 @@ class PowerSgdGroup:
             raise ValueError("need a tall matrix (rows >= cols)")
         self.chunks = [self.rank] if self.rank in self.RANKS else self.rank_chunks(self.rank)
         self.row_offsets, self.est_offsets = row_offsets, est_offsets
+        self.host_offsets = host_offsets   # [T] tensor offsets within a worker row (batched layout)
         self.batch = _native.PsgdBatch(T, L, _ptr(row_offsets), ld, _ptr(est_offsets), 0, 0)
         ws = int(_native.lib().gc_psgd_workspace_bytes(T * L, self.rows, self.cols, self.rank))
         self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
@@ -597,6 +598,15 @@ class PowerSgdGroup:
         (pipelines.py:341-346, compressors.py:591-603)."""
         return seed_q_groups([self], round_index)[0]
 
+    def host_offsets_arg(self):
+        """ctypes array of the batch's tensor offsets (element offset of tensor t in a worker row), or
+        None for the single-matrix layout -- the TMA pass builds one tensor map per tensor."""
+        if self.host_offsets is None:
+            return None
+        if getattr(self, "_hoffs", None) is None:
+            self._hoffs = (ctypes.c_int64 * len(self.host_offsets))(*[int(x) for x in self.host_offsets])
+        return self._hoffs
+
     def materialize(self, resid_ptr):
         """Write the deferred residuals r = c - P_hat Q_w^T (pipelines.py:357-361, ef_update) into the
         buffer that holds the last round's corrected matrices -- before anything but the next round's
@@ -651,13 +661,14 @@ class PowerSgdGroup:
         # rides along: deferred EF), float4 producer for aligned rows, masked scalars otherwise
         umma = vec or umma_unaligned()
         rp = ef_resid_ptr if ef_resid_ptr is not None else resid_ptr
-        tma = (not multi and grads_ptr is not None and rp is not None and
-               bool(_native.lib().gc_psgd_mq_tma_supported(bref, d, rows, cols, r, grads_ptr, rp)))
+        hoffs = self.host_offsets_arg()
+        tma = (not multi and grads_ptr is not None and rp is not None and os.environ.get("GC_PSGD_TMA", "1") != "0"
+               and bool(_native.lib().gc_psgd_mq_tma_supported_batched(bref, hoffs, d, rows, cols, r, grads_ptr, rp)))
         if self.pending is not None and not (tma and self.pending[0] == rp):
             self.materialize(rp)
         if tma:
             pend, self.pending = self.pending, None
-            _native.call("gc_psgd_mq_deferred", bref, d, rows, cols, r, grads_ptr, rp, q.data_ptr(),
+            _native.call("gc_psgd_mq_deferred_batched", bref, hoffs, d, rows, cols, r, grads_ptr, rp, q.data_ptr(),
                          pend[1].data_ptr() if pend else None, pend[2].data_ptr() if pend else None, p.data_ptr(),
                          self.ws.data_ptr(), sp)
         for k, (c0, rc) in enumerate(spans):

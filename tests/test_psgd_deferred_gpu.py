@@ -184,3 +184,29 @@ def test_mtp_tma_matches_cuda_core_pass(which, r, monkeypatch):
     scale = ref.abs().max().item()
     assert (q1.double() - ref).abs().max().item() <= 1e-6 * scale
     assert (q2.double() - ref).abs().max().item() <= 1e-6 * scale
+
+
+def test_batched_groups_defer_bitwise():
+    """Chunked PowerSGD (one pipeline per tensor, batched per shape): the TMA pass with one tensor
+    map per tensor and the deferred EF update give the eager schedule's rounds bit for bit."""
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.multitensor import TensorListPipeline
+    sizes = [64 * 64, 4096, 128 * 128, 64 * 64, 100, 200 * 200, 128 * 128]   # groups of 1..3, one bypass
+    n, D = 2, sum(sizes)
+    rng = np.random.default_rng(21)
+    grads = [torch.from_numpy(rng.standard_normal((n, D)).astype(np.float32)).cuda() for _ in range(4)]
+
+    def run(defer):
+        pipe = TensorListPipeline(gcb.PowerSgdConfig(4), n, sizes, gcb.SeedSpec(9), compute_nmse=False)
+        for grp in pipe.groups:
+            grp.defer = defer
+        ests = [pipe.run_round(g, r).estimate.logical.copy() for r, g in enumerate(grads)]
+        engaged = any(grp.pending is not None for grp in pipe.groups)
+        return ests, np.stack(pipe.residuals), engaged
+
+    e0, r0, _ = run(False)
+    e1, r1, engaged = run(True)
+    assert engaged, "no batched group took the TMA / deferred path"
+    for r in range(4):
+        assert np.array_equal(e0[r], e1[r]), r
+    assert np.array_equal(r0, r1)
