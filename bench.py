@@ -439,12 +439,17 @@ def main():
                 tr = json.load(f)
             key = f"{kname}:n={local_n}:d={d}:q={args.quant_bits}:b={args.wire_bits}:B={args.rotation_block}"
             traffic = tr.get(key, tr.get(key.replace("thc_fused_kernel", "thc_fused")))
+            issue = tr.get("issue:" + key)
         except (OSError, ValueError):
-            pass
+            issue = None
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": kname, "kernel_ms": kernel_ms,
                 "kernel_share_of_step": kernel_ms / ms, "algorithmic_bytes_per_launch": alg_bytes,
                 "peak_source": peak_src}
+        if issue:   # what actually bounds the bit-exact THC kernel: instruction issue (ncu capture)
+            roof["issue"] = dict(issue, achieved_warp_inst_per_s=issue["warp_instructions_per_launch"] / (kernel_ms * 1e-3),
+                                 frac_of_issue_peak=issue["warp_instructions_per_launch"] / (kernel_ms * 1e-3)
+                                 / issue["peak_warp_inst_per_s"])
 
     # end to end through the public API from pinned host memory
     e2e = None

@@ -61,10 +61,13 @@ struct WarpSmem {
 
 __host__ __device__ inline WarpSmem warp_smem(int nblk, int q) {
   WarpSmem S;
-  S.scratch = 0;                               // fp64 transpose / x_rot staging
+  S.scratch = 0;                               // fp64 transpose / x_rot staging (f32 [32][32])
   S.cbuf = S.scratch + kScrBytes;              // corrected, natural order (padded rows)
-  S.cod = S.cbuf + kCBytes;                    // codes of the tile
-  S.bp = S.cod + 1024;                         // nblk x 8 doubles: block parameters
+  // the tile's codes share the scratch rows behind x_rot: both live only between the forward and
+  // the own-decode transposes (the codes are read into registers before that transpose), so the
+  // warp needs 13 KB and four 4-warp CTAs fit an SM
+  S.cod = S.scratch + kTileN * 4;
+  S.bp = S.cbuf + kCBytes;                     // nblk x 8 doubles: block parameters
   S.lut = S.bp + nblk * 64;                    // dq(z, 1) table
   const int lut_n = nblk * ((1 << q) - 1);
   S.total = S.lut + ((lut_n < kLutMax ? lut_n : kLutMax) * 8 + 15) / 16 * 16;

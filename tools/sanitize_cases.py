@@ -4,13 +4,16 @@ for compute-sanitizer (memcheck, racecheck, synccheck):
     compute-sanitizer --tool racecheck python tools/sanitize_cases.py [case ...]
 
 cases: thc_fused (n = 8, B = 1024, 2 rounds), thc_rank (per-rank K1/K2/K3 on a one-rank gloo
-group), psgd_umma (tcgen05 P = M Q), psgd_mtp_ef (cluster / DSMEM Q + EF pass), topk, topkc."""
+group), psgd_umma (register-fed tcgen05 P = M Q), psgd_tma (TMA-fed tcgen05 P = M Q with the
+deferred EF update, TMA Q = M^T P_hat, Cholesky orthonormalization; 3 rounds), psgd_batched (one
+tensor map per tensor of a shape group), psgd_mtp_ef (cluster / DSMEM Q + EF pass), topk, topkc."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2407_01378_b200 as gcb
 
-cases = sys.argv[1:] or ["thc_fused", "thc_rank", "psgd_umma", "psgd_mtp_ef", "topk", "topkc"]
+cases = sys.argv[1:] or ["thc_fused", "thc_rank", "psgd_umma", "psgd_tma", "psgd_batched", "psgd_mtp_ef", "topk",
+                         "topkc"]
 torch.cuda.set_device(0)
 S = gcb.SeedSpec(7)
 
@@ -37,6 +40,17 @@ for c in cases:
     elif c == "psgd_umma":
         n, d = 2, 300 * 257
         rounds(gcb.make_pipeline(gcb.PowerSgdConfig(4), n, d, S), torch.randn(n, d, device="cuda"))
+    elif c == "psgd_tma":
+        n, d = 2, 40004   # 201 x 200: TMA boxes, a partly filled last row (tail kernel), deferred EF
+        pipe = gcb.make_pipeline(gcb.PowerSgdConfig(4), n, d, S, compute_nmse=False)
+        rounds(pipe, torch.randn(n, d, device="cuda"), 3)
+        pipe.residuals
+    elif c == "psgd_batched":
+        from paper_2407_01378_b200.multitensor import TensorListPipeline
+        sizes = [64 * 64, 4096, 128 * 128, 100, 200 * 200]
+        pipe = TensorListPipeline(gcb.PowerSgdConfig(4), 2, sizes, S, compute_nmse=False)
+        rounds(pipe, torch.randn(2, sum(sizes), device="cuda"), 3)
+        pipe.residuals
     elif c == "psgd_mtp_ef":
         os.environ["GC_PSGD_MTP_EF"] = "1"
         n, d = 2, 256 * 256
