@@ -367,6 +367,8 @@ def main():
     import paper_2407_01378_b200 as gcb
 
     n_gpus = world
+    if os.environ.get("GC_BENCH_ONE_DEVICE") == "1":   # test hook: N gloo ranks sharing one GPU
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     distributed = world > 1 or args.distributed

@@ -370,21 +370,26 @@ __global__ void range_consensus_kernel(int L, int64_t nb, const float *in, float
   }
 }
 
-constexpr int kSignWordsPerThread = 64;   // one PCG jump amortised over 64 words (1024 steps)
+// words per thread: one PCG jump amortised over 8..64 words (128..1024 steps), as many as keeps
+// ~2 threads per core busy (small vectors need the threads more than the amortisation)
+inline int sign_words_per_thread(int64_t words) {
+  int64_t w = words / (148 * 2048);
+  return static_cast<int>(w < 8 ? 8 : (w > 64 ? 64 : w));
+}
 
-__global__ void signs_kernel(gc_pcg64 stream, int64_t count, uint32_t *bits) {
+__global__ void signs_kernel(gc_pcg64 stream, int64_t count, uint32_t *bits, int wpt) {
   // Sign i = top bit of u32 word i; u32 words are the low then high half of each next64 output
   // (numpy buffered bounded uint32, Lemire with range 2).  Thread t writes words
   // [t*8, t*8 + 8): 128 consecutive outputs after one jump.
   const int64_t words = (count + 31) / 32;
-  const int64_t groups = (words + kSignWordsPerThread - 1) / kSignWordsPerThread;
+  const int64_t groups = (words + wpt - 1) / wpt;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < groups;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     gc::Pcg g;
     g.load(stream);
-    g.jump(static_cast<uint64_t>(t) * kSignWordsPerThread * 16);
-    const int64_t w0 = t * kSignWordsPerThread;
-    const int nw = static_cast<int>(min(static_cast<int64_t>(kSignWordsPerThread), words - w0));
+    g.jump(static_cast<uint64_t>(t) * wpt * 16);
+    const int64_t w0 = t * wpt;
+    const int nw = static_cast<int>(min(static_cast<int64_t>(wpt), words - w0));
 #pragma unroll 2
     for (int k = 0; k < nw; ++k) {
       uint32_t word = 0;
@@ -489,8 +494,11 @@ int gc_thc_signs(const gc_pcg64 *rotation_stream, int64_t count, uint32_t *bits,
   GC_REQUIRE(rotation_stream && bits, "null argument");
   GC_REQUIRE(count >= 0, "count must be non-negative");
   if (count == 0) return GC_OK;
-  const int64_t groups = ((count + 31) / 32 + kSignWordsPerThread - 1) / kSignWordsPerThread;
-  signs_kernel<<<grid_for(groups, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(*rotation_stream, count, bits);
+  const int64_t words = (count + 31) / 32;
+  const int wpt = sign_words_per_thread(words);
+  const int64_t groups = (words + wpt - 1) / wpt;
+  signs_kernel<<<grid_for(groups, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(*rotation_stream, count, bits,
+                                                                                       wpt);
   GC_LAUNCH_CHECK("signs_kernel");
   return GC_OK;
 }

@@ -39,7 +39,7 @@
 #include "gc_thc_tile.cuh"
 
 #ifndef GC_THC_LOAD_BATCH
-#define GC_THC_LOAD_BATCH 2
+#define GC_THC_LOAD_BATCH 8
 #endif
 
 namespace {

@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) rank_quant_kernel(const __grid
                        : static_cast<double>(static_cast<float>(1.0 * mid + step * static_cast<double>(z))) *
                              (kPow2Scale ? a.scale : 1.0);
       }
+      __syncwarp();   // every lane has read the tile's codes: the transpose rows below overlay them
       wht_tile<K>(v, scr, lane);
       if (t0 + kTileN <= a.dim) {
         float *rt = ro + t0 + lane;

@@ -13,7 +13,7 @@ cp ${o}_bench_launches.csv $p/${r}_bench_launches.csv
 { echo "ncu --metrics gpu__time_duration.sum --clock-control none  python bench.py --steps 3 --warmup 3 (cold-cache, serialised launches)";
   python tools/launch_summary.py ${o}_bench_launches.csv; } > $p/${r}_bench_launch_summary.txt
 python tools/ncu_summary.py ${o}_thc_fused.ncu-rep > $p/${r}_thc_fused_ncu_full.txt 2>&1
-FN=ILi10ELb1E python tools/ncu_lines.py ${o}_thc_fused.ncu-rep paper_2407_01378_b200/libgradcomp_b200.so \
+FN=ILi10ELb1E python tools/ncu_lines.py ${o}_thc_fused.ncu-rep ${EVIDENCE_LIB:-paper_2407_01378_b200/libgradcomp_b200.so} \
   paper_2407_01378_b200/csrc/gc_thc_fused.cu thc_fused > $p/${r}_thc_fused_lines.txt 2>&1
 python tools/ncu_summary.py ${o}_psgd_tma.ncu-rep > $p/${r}_psgd_tma_ncu_full.txt 2>&1
 python tools/ncu_summary.py ${o}_thc_rank.ncu-rep > $p/${r}_thc_rank_ncu_full.txt 2>&1

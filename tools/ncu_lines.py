@@ -24,16 +24,23 @@ for line in dis.split("\n"):
         infn = (want is None or want in line) and os.environ.get("FN", "") in line
         continue
     m = re.search(r'File "([^"]+)", line (\d+)', line) if "//##" in line else None
-    if m:   # attribute only lines of the source file asked for (headers map to -1)
-        cur = int(m.group(2)) if os.path.basename(m.group(1)) == os.path.basename(srcf) else -1
+    if m:   # (file, line): the source file asked for and the headers it inlines
+        cur = (os.path.basename(m.group(1)), int(m.group(2)))
         continue
     m2 = re.search(r'/\*([0-9a-f]{4,})\*/', line)
     if m2 and cur and infn: lm[int(m2.group(1), 16)] = cur
 ci = collections.Counter(); cs = collections.Counter()
 for a, c, s in data:
-    l = lm.get(a - base, -1); ci[l] += c; cs[l] += s
+    l = lm.get(a - base, ("?", -1)); ci[l] += c; cs[l] += s
 ti, ts = sum(ci.values()), sum(cs.values())
-src = open(srcf).read().split("\n")
+srcdir = os.path.dirname(os.path.abspath(srcf))
+cache = {}
+def text(f, l):
+    if f not in cache:
+        path = os.path.join(srcdir, f)
+        cache[f] = open(path).read().split("\n") if os.path.exists(path) else []
+    lines = cache[f]
+    return lines[l - 1].strip()[:80] if 0 < l <= len(lines) else "?"
 print(f"{kname[:80]}: {ti:.3g} warp-instr, {ts:.3g} samples")
-for l, c in ci.most_common(int(os.environ.get("TOP", 30))):
-    print(f"{l:4d} inst {c/ti*100:5.1f}%  stall {cs[l]/ts*100:5.1f}%  {src[l-1].strip()[:90] if l > 0 else '?'}")
+for (f, l), c in ci.most_common(int(os.environ.get("TOP", 30))):
+    print(f"{f[:18]:18s}:{l:4d} inst {c/ti*100:5.1f}%  stall {cs[(f, l)]/ts*100:5.1f}%  {text(f, l)}")
