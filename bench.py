@@ -22,7 +22,7 @@ the CUDA-event time of the K steps / K.  `e2e` runs the same step through the pu
 from pinned host buffers (H2D of the gradients and D2H of the estimate inside the timed
 region).  `roofline` reports the dominant kernel against the measured HBM copy bandwidth
 with algorithmic bytes per launch.  `north_star` times north_star's 350M-element vector with
-one worker per GPU (n = N): THC q4b8, PowerSGD r4 (one 18,709 x 18,708 matrix, and at N = 1
+one worker per GPU (n = N): THC q4b8, PowerSGD r4 (one 18,709 x 18,708 matrix, and chunked over
 GPT-2-medium's 292 tensors) and the FP16 NCCL all-reduce bar.  `cpu_baseline` times the CPU
 oracle (oracle/, a NumPy restatement of the reference path) on a bounded sample.
 
@@ -309,7 +309,7 @@ def make_pipe(gcb, cfg, n, d, seeds, distributed, **kw):
 def north_star_block(gcb, args, world, rank, dev, gen, barrier):
     """north_star's 350M-element vector, one worker per GPU (n = N, weak per GPU): per-rank
     DistributedGradientPipeline rounds over NCCL for THC q4b8, PowerSGD r4 (one 18,709 x 18,708
-    matrix) and the FP16 all-reduce bar; at N = 1 also PowerSGD over GPT-2-medium's 292 tensors."""
+    matrix), chunked PowerSGD r4 over GPT-2-medium's 292 tensors, and the FP16 all-reduce bar."""
     import torch
     seeds = gcb.SeedSpec(2024)
     n, d = world, D_NORTH
@@ -328,18 +328,21 @@ def north_star_block(gcb, args, world, rank, dev, gen, barrier):
         except Exception as exc:   # a failing extra case must not cost the contract line
             out[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         torch.cuda.empty_cache()
-    if world == 1:
-        from paper_2407_01378_b200.multitensor import TensorListPipeline, gpt2_medium_sizes
+    try:   # chunked PowerSGD: one reference pipeline per GPT-2-medium tensor, one worker per GPU
+        from paper_2407_01378_b200.distributed import DistributedTensorListPipeline
+        from paper_2407_01378_b200.multitensor import gpt2_medium_sizes
         sizes = gpt2_medium_sizes()
         D = sum(sizes)
         del pool
         torch.cuda.empty_cache()
         pool = [torch.randn(1, D, device=dev, generator=gen) for _ in range(2)]
-        pipe = TensorListPipeline(gcb.PowerSgdConfig(4), 1, sizes, seeds, validate=False, compute_nmse=False)
+        pipe = DistributedTensorListPipeline(gcb.PowerSgdConfig(4), n, sizes, seeds, device=dev, validate=False)
         ms = timed_rounds(pipe, pool, warm, steps, world, dev, barrier)
         out["powersgd_r4_gpt2m"] = {"ms_per_step": ms, "value": D / (ms * 1e-3) / 1e9, "unit": "Gelem/s", "d": D,
                                     "tensors": len(sizes)}
         del pipe
+    except Exception as exc:
+        out["powersgd_r4_gpt2m"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     bar = out.get("fp16_bar", {}).get("ms_per_step")
     for name in ("thc_q4b8", "powersgd_r4", "powersgd_r4_gpt2m"):
         if bar and "ms_per_step" in out.get(name, {}):

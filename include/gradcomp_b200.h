@@ -184,6 +184,12 @@ int gc_float_fold(int32_t n, int64_t len, const float *inputs, int64_t ld, int64
 int gc_float_fold_batched(int32_t batch, int32_t n, int64_t len, const float *inputs, int64_t ld, int64_t in_stride,
                           int32_t wire_fp16, int32_t round_inputs, int32_t divisor, float *out, int64_t out_stride,
                           void *stream);
+/* The batched fold of a slice: elements [offset, offset + len) of B same-length ring reductions
+ * whose ring blocks are ring_block long (element i starts at worker floor(i / ring_block)); inputs
+ * hold only the slice.  The per-tensor factor exchange of chunked PowerSGD across ranks. */
+int gc_float_fold_batched_slice(int32_t batch, int32_t n, int64_t len, const float *inputs, int64_t ld,
+                                int64_t in_stride, int64_t offset, int64_t ring_block, int32_t wire_fp16,
+                                int32_t round_inputs, int32_t divisor, float *out, int64_t out_stride, void *stream);
 /* Dense-fp32 bypass of many small tensors in one launch (pipelines.py:326-336): for segment s
  * (offsets/lengths device int64 [nseg]) of the flat [n][ld] corrected vectors, estimate =
  * ring-ordered fp32 sum / n, and resid = 0 there (own == corrected; resid may alias corrected

@@ -91,6 +91,7 @@ SIGNATURES = {
     # float folds
     "gc_float_fold": (c_int, [I32, I64, P, I64, I64, I64, I32, I32, I32, P, P]),
     "gc_float_fold_batched": (c_int, [I32, I32, I64, P, I64, I64, I32, I32, I32, P, I64, P]),
+    "gc_float_fold_batched_slice": (c_int, [I32, I32, I64, P, I64, I64, I64, I64, I32, I32, I32, P, I64, P]),
     "gc_segment_fold_ef": (c_int, [I32, I32, P, P, P, P, I64, P, P]),
     "gc_segment_ef_fold": (c_int, [I32, I32, P, P, P, P, I64, P, P]),
     "gc_scale_div": (c_int, [I64, P, I32, P, P]),

@@ -303,6 +303,17 @@ int gc_float_fold_batched(int32_t batch, int32_t n, int64_t len, const float *in
                      out, out_stride, static_cast<cudaStream_t>(stream));
 }
 
+int gc_float_fold_batched_slice(int32_t batch, int32_t n, int64_t len, const float *inputs, int64_t ld,
+                                int64_t in_stride, int64_t offset, int64_t ring_block, int32_t wire_fp16,
+                                int32_t round_inputs, int32_t divisor, float *out, int64_t out_stride, void *stream) {
+  GC_REQUIRE(batch >= 1 && batch <= 65535 && n >= 1 && len >= 0 && ld >= len && offset >= 0 && ring_block >= 1 &&
+                 inputs && out,
+             "invalid argument");
+  if (len == 0) return GC_OK;
+  return fold_launch(batch, n, len, inputs, ld, in_stride, offset, ring_block, wire_fp16, round_inputs, divisor, out,
+                     out_stride, static_cast<cudaStream_t>(stream));
+}
+
 int gc_segment_fold_ef(int32_t n, int32_t nseg, const int64_t *seg_off, const int64_t *seg_len, const float *grads,
                        float *resid, int64_t ld, float *estimate, void *stream) {
   GC_REQUIRE(n >= 1 && nseg >= 0 && nseg <= 65535 && (nseg == 0 || (seg_off && seg_len)) && grads && estimate,

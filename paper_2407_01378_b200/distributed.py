@@ -769,3 +769,173 @@ def _make(cfg, pipe):
     if isinstance(cfg, DenseConfig):
         return _Dense(cfg, pipe)
     raise TypeError(f"unknown config type {type(cfg).__name__}")
+
+
+def exchange_float_batched(x: torch.Tensor, comm: Comm, n: int, T: int, m: int, phase: str | None) -> torch.Tensor:
+    """T independent fp32 FloatSum rings of length m at once (one per tensor of a shape group):
+    x [T * L, m] (row t * L + l = tensor t, local worker l) -> [T, m] sums in the reference ring
+    order of each tensor (collectives.py:177-236), one all-to-all + one all-gather for the group."""
+    W, L = comm.world, x.shape[0] // T
+    S = -(-m // W)
+    xv = x.reshape(T, L, m)
+    send = torch.empty(W, T, L, S, dtype=torch.float32, device=x.device)
+    for r in range(W):
+        lo, hi = r * S, min(m, (r + 1) * S)
+        if hi > lo:
+            send[r, :, :, : hi - lo].copy_(xv[:, :, lo:hi])
+        if hi - lo < S:
+            send[r, :, :, max(0, hi - lo):].zero_()
+    recv = comm.all_to_all(send, phase)                         # [W][T][L][S]: rank r's workers
+    rows = recv.permute(1, 0, 2, 3).reshape(T, n, S).contiguous()   # [T][worker][S]
+    s0 = comm.rank * S
+    my_len = max(0, min(S, m - s0))
+    out = torch.empty(T, S, dtype=torch.float32, device=x.device)
+    if my_len < S:
+        out[:, my_len:].zero_()
+    if my_len:
+        _native.call("gc_float_fold_batched_slice", T, n, my_len, rows.data_ptr(), S, n * S, s0, -(-m // n), 0, 0, 0,
+                     out.data_ptr(), S, _sp())
+    gathered = comm.all_gather_rows(out.reshape(1, T * S), phase)    # [W][T * S]
+    return gathered.reshape(W, T, S).permute(1, 0, 2).reshape(T, W * S)[:, :m].contiguous()
+
+
+class DistributedTensorListPipeline:
+    """Chunked PowerSGD across ranks: one reference pipeline per tensor of a flat gradient
+    (pipelines.py:324-368 per tensor), this rank's L = n / world workers.
+
+    The tensors below bypass_below go through the dense-fp32 ring (pipelines.py:326-336): their
+    corrected values are gathered from all ranks and folded per tensor in ring order
+    (gc_segment_fold_ef), residual 0.  The compressed tensors are batched by shape as in
+    TensorListPipeline (TMA P = M Q with the deferred EF update where the row pitch allows); each
+    group's factor all-reduces are one exchange_float_batched (all-to-all + per-tensor ring-order
+    fold + all-gather) per phase, so a round issues 4 collectives per shape group instead of 4 per
+    tensor."""
+
+    def __init__(self, config: PowerSgdConfig, num_workers: int, sizes, seeds: SeedSpec,
+                 error_feedback: bool | None = None, *, group=None, device=None, validate: bool = True):
+        from collections import OrderedDict
+        from .schemes import PowerSgdGroup
+        if not isinstance(config, PowerSgdConfig):
+            raise TypeError("DistributedTensorListPipeline runs PowerSGD (chunked); use DistributedGradientPipeline")
+        self.comm = Comm(group)
+        W = self.comm.world
+        if num_workers < 1 or num_workers % W:
+            raise ValueError("num_workers must be a positive multiple of the world size")
+        if not sizes or min(sizes) < 1:
+            raise ValueError("need positive tensor sizes")
+        self.config, self.scheme = config, scheme_label(config)
+        self.group = WorkerGroup(num_workers)
+        self.L = num_workers // W
+        self.sizes = [int(x) for x in sizes]
+        self.offsets = np.concatenate([[0], np.cumsum(self.sizes)[:-1]]).astype(np.int64)
+        self.dim = D = int(sum(self.sizes))
+        self.seeds, self.validate = seeds, validate
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.error_feedback = True if error_feedback is None else bool(error_feedback)
+        dev, L, n = self.device, self.L, num_workers
+        self._res = torch.zeros(L, D, dtype=torch.float32, device=dev) if self.error_feedback else None
+        self.bypass = [t for t, s in enumerate(self.sizes) if s < config.bypass_below]
+        if self.bypass:
+            idx = np.concatenate([np.arange(self.offsets[t], self.offsets[t] + self.sizes[t]) for t in self.bypass])
+            self.byp_idx = torch.from_numpy(idx.astype(np.int64)).to(dev)
+            lens = [self.sizes[t] for t in self.bypass]
+            self.byp_off = torch.tensor(np.concatenate([[0], np.cumsum(lens)[:-1]]), dtype=torch.int64, device=dev)
+            self.byp_len = torch.tensor(lens, dtype=torch.int64, device=dev)
+        groups = OrderedDict()
+        for t, s in enumerate(self.sizes):
+            if s >= config.bypass_below:
+                groups.setdefault(s, []).append(t)
+        self.groups = []
+        for s, ts in sorted(groups.items(), key=lambda kv: kv[0] * len(kv[1])):
+            rows = [l * D + int(self.offsets[t]) for t in ts for l in range(L)]
+            ro = torch.tensor(rows, dtype=torch.int64, device=dev)
+            eo = torch.tensor([int(self.offsets[t]) for t in ts], dtype=torch.int64, device=dev)
+            grp = PowerSgdGroup(config, n, L, s, len(ts), seeds, dev, row_offsets=ro, est_offsets=eo, ld=D,
+                                host_offsets=[int(self.offsets[t]) for t in ts])
+            grp.tensor_ids = ts
+            grp.vec = grp.cols % 4 == 0 and all(x % 4 == 0 for x in rows) and D % 4 == 0
+            self.groups.append(grp)
+        self.launches = 0
+
+    @property
+    def residuals(self):
+        if self._res is None:
+            return None
+        self._sync()
+        h = self._res.cpu().numpy()
+        return [h[i].copy() for i in range(self.L)]
+
+    @property
+    def residuals_tensor(self):
+        if self._res is not None:
+            self._sync()
+        return self._res
+
+    def _sync(self):
+        for grp in self.groups:
+            grp.materialize(self._res.data_ptr())
+
+    def _fold(self, kind, x, m):
+        T = x.shape[0] // self.L
+        return exchange_float_batched(x, self.comm, self.group.size, T, m, kind)
+
+    def run_round(self, local_grads, round_index: int) -> RoundResult:
+        from .schemes import seed_q_groups, umma_unaligned
+        L, D, n = self.L, self.dim, self.group.size
+        if not (torch.is_tensor(local_grads) and tuple(local_grads.shape) == (L, D)):
+            raise ValueError("need [local_workers, dim] gradients")
+        g = local_grads if (local_grads.is_cuda and local_grads.is_contiguous()
+                            and local_grads.dtype == torch.float32) else local_grads.to(self.device, torch.float32).contiguous()
+        if self.validate:
+            bad = torch.zeros(1, dtype=torch.int64, device=self.device)
+            _native.call("gc_check_finite", L, g.data_ptr(), g.stride(0), D, bad.data_ptr(), _sp())
+            self.comm.all_reduce(bad, dist.ReduceOp.SUM)
+            if int(bad.item()):
+                raise ValueError("gradients must be finite")
+        sp = _sp()
+        res = self._res
+        ledger = TrafficLedger()
+        est = torch.empty(D, dtype=torch.float32, device=self.device)
+        bits = 0.0
+        qs = seed_q_groups(self.groups, round_index)
+        if self.bypass:   # dense fp32 ring per small tensor (pipelines.py:326-336): own = corrected, r -> 0
+            c = g.index_select(1, self.byp_idx)
+            if res is not None:
+                c += res.index_select(1, self.byp_idx)
+                res.index_fill_(1, self.byp_idx, 0.0)
+            allc = self.comm.all_gather_rows(c, "dense-bypass")            # [n, Dbyp], worker order
+            packed = torch.empty(allc.shape[1], dtype=torch.float32, device=self.device)
+            _native.call("gc_segment_fold_ef", n, len(self.bypass), self.byp_off.data_ptr(), self.byp_len.data_ptr(),
+                         allc.data_ptr(), None, allc.stride(0), packed.data_ptr(), sp)
+            est.index_copy_(0, self.byp_idx, packed)
+            for t in self.bypass:
+                ledger.charge_ring("dense-bypass", n, self.sizes[t], 32)
+                bits += 32.0 * self.sizes[t]
+        for grp, q in zip(self.groups, qs):
+            aligned = grp.vec and g.data_ptr() % 16 == 0 and est.data_ptr() % 16 == 0
+            if res is not None:
+                grp.set_ld(D, aligned and res.data_ptr() % 16 == 0)
+                if grp.batch.rows_aligned or umma_unaligned():   # ef_apply inside the tcgen05 P = M Q
+                    grp.run(res.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, grads_ptr=g.data_ptr(),
+                            vec=bool(grp.batch.rows_aligned), fold=self._fold, q=q, ef_resid_ptr=res.data_ptr())
+                else:
+                    grp.materialize(res.data_ptr())
+                    for t in grp.tensor_ids:
+                        off = int(self.offsets[t])
+                        _native.call("gc_ef_apply", L, self.sizes[t], g.data_ptr() + 4 * off, res.data_ptr() + 4 * off,
+                                     D, res.data_ptr() + 4 * off, D, sp)
+                    grp.run(res.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, vec=False, fold=self._fold,
+                            q=q)
+            else:
+                grp.set_ld(D, aligned)
+                grp.run(g.data_ptr(), None, est.data_ptr(), round_index, vec=bool(grp.batch.rows_aligned),
+                        fold=self._fold, q=q)
+            for t in grp.tensor_ids:
+                ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
+                ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)
+                bits += 32.0 * grp.rank * (grp.rows + grp.cols)
+        self.launches += 4 + len(self.groups) * 11
+        result = RoundResult(self.scheme, round_index, est, D, ledger, bits, _simple_stats(None))
+        result.wire_bytes = dict(self.comm.sent)
+        self.comm.sent = {}
+        return result

@@ -162,3 +162,58 @@ def test_fp16_bar_saturates_like_the_reference_wire():
     ref = oracle_rounds("dense", dict(bits=16), [[g, g]], 1, ef=False)[0]["estimate"]
     assert np.all(np.isfinite(out[0])) and np.array_equal(out[0], out[1])
     assert np.array_equal(out[0], ref), (out[0], ref)
+
+
+CHUNK_SIZES = [6000, 64, 3 * 4096, 192, 4096, 64 * 64, 10_000, 128 * 128]
+
+
+def _chunked_rank(rank, world, n):
+    import torch
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.distributed import DistributedTensorListPipeline
+    torch.cuda.set_device(0)
+    L, D = n // world, sum(CHUNK_SIZES)
+    pipe = DistributedTensorListPipeline(gcb.PowerSgdConfig(4), n, CHUNK_SIZES, gcb.SeedSpec(SEED),
+                                         device=torch.device("cuda", 0))
+    out = []
+    for r in range(3):
+        g = np.stack(_chunk_grads(n, D, r)[rank * L:(rank + 1) * L])
+        res = pipe.run_round(torch.from_numpy(g).cuda(), r)
+        out.append({"est": res.estimate.logical.copy(), "wire": res.wire_bytes,
+                    "led": {ph: res.ledger.bits_sent(worker=rank * L, phase=ph) for ph in res.ledger.phases()}})
+    out[-1]["res"] = pipe.residuals
+    return out
+
+
+def _chunk_grads(n, D, r):
+    rng = np.random.default_rng(1000 + r)
+    return [rng.standard_normal(D).astype(np.float32) for _ in range(n)]
+
+
+@pytest.mark.parametrize("world,n", [(2, 2), (2, 4), (4, 4)])
+def test_chunked_powersgd_across_ranks(world, n):
+    """Chunked PowerSGD (one reference pipeline per tensor) over `world` ranks: every tensor's
+    estimate and residuals within the fp32 contract of the reference, the dense bypass bit for bit,
+    the factor phases' wire bytes equal to the ledger's ring volume (one worker per rank)."""
+    out = run_world(_chunked_rank, world, (n,))
+    D = sum(CHUNK_SIZES)
+    offs = np.concatenate([[0], np.cumsum(CHUNK_SIZES)[:-1]])
+    grads = [_chunk_grads(n, D, r) for r in range(3)]
+    for t, (off, s) in enumerate(zip(offs, CHUNK_SIZES)):
+        ref = oracle_rounds("powersgd", dict(rank=4), [[g[off:off + s] for g in grads[r]] for r in range(3)], SEED)
+        for r in range(3):
+            e0 = out[0][r]["est"][off:off + s]
+            for k in range(1, world):
+                assert np.array_equal(e0, out[k][r]["est"][off:off + s]), "ranks disagree"
+            want = ref[r]["estimate"]
+            if s < 4096:
+                assert np.array_equal(e0, want), (t, r)
+            else:
+                assert np.max(np.abs(e0 - want)) <= 1e-5 * max(np.max(np.abs(want)), 1e-30), (t, r)
+        mine = np.stack(sum((out[k][2]["res"] for k in range(world)), []))[:, off:off + s]
+        theirs = np.stack(ref[2]["residuals"])
+        assert np.max(np.abs(mine - theirs)) <= 1e-5 * max(np.max(np.abs(theirs)), 1e-30), t
+    if n == world:
+        for k in range(world):
+            for ph in ("left-factor", "right-factor"):
+                assert out[k][0]["wire"][ph] * 8 == out[k][0]["led"][ph], (ph, out[k][0]["wire"], out[k][0]["led"])
