@@ -11,7 +11,9 @@ set of parameters from one step to the next.  Error-feedback residuals are per p
 layout appears for the first time, its pipeline starts from the residuals every parameter
 carried in the layout it came from (the reference keeps a residual per coordinate,
 pipelines.py:129-133, 168-170); the PowerSGD warm start (pipelines.py:366) is tied to the bucket's
-matrix shape and restarts from a fresh seed matrix.
+matrix shape and restarts from a fresh seed matrix.  With `chunked=True` (PowerSGD) every parameter
+is its own reference pipeline (DistributedTensorListPipeline: per-layer matrices, as PowerSGD is
+used in practice); residuals carry over per parameter the same way.
 
 A non-finite bucket (e.g. an fp16 GradScaler overflow step) is detected on every rank (the
 pipeline's finite check is all-reduced), raises nothing inside autograd and leaves every
@@ -27,13 +29,18 @@ the step everywhere, as the reference rejects non-finite gradients before any st
 import torch
 import torch.distributed as dist
 
-from .distributed import DistributedGradientPipeline
+from .configs import PowerSgdConfig
+from .distributed import DistributedGradientPipeline, DistributedTensorListPipeline
 from .vectors import SeedSpec
 
 
 class CompressionHookState:
-    def __init__(self, config, seeds: SeedSpec, *, group=None, validate: bool = True, record: bool = False):
+    def __init__(self, config, seeds: SeedSpec, *, group=None, validate: bool = True, record: bool = False,
+                 chunked: bool = False):
         self.config = config
+        # chunked=True with PowerSgdConfig: one reference pipeline per parameter (per-layer matrices,
+        # the paper's and PyTorch's PowerSGD practice) instead of one matrix per bucket
+        self.chunked = bool(chunked) and isinstance(config, PowerSgdConfig)
         self.seeds = seeds
         self.group = group
         self.validate = validate
@@ -69,8 +76,12 @@ class CompressionHookState:
         buf = bucket.buffer()
         world = dist.get_world_size(self.group)
         with torch.cuda.device(buf.device):
-            pipe = DistributedGradientPipeline(self.config, world, buf.numel(), self.seeds, group=self.group,
-                                               device=buf.device, validate=self.validate)
+            if self.chunked:
+                pipe = DistributedTensorListPipeline(self.config, world, numels, self.seeds, group=self.group,
+                                                     device=buf.device, validate=self.validate)
+            else:
+                pipe = DistributedGradientPipeline(self.config, world, buf.numel(), self.seeds, group=self.group,
+                                                   device=buf.device, validate=self.validate)
             if pipe.residuals_tensor is not None:   # carry every parameter's residual over
                 dst = pipe.residuals_tensor[0]
                 for pid, o, m in zip(ids, offs, numels):

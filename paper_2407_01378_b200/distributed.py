@@ -774,28 +774,33 @@ def _make(cfg, pipe):
 def exchange_float_batched(x: torch.Tensor, comm: Comm, n: int, T: int, m: int, phase: str | None) -> torch.Tensor:
     """T independent fp32 FloatSum rings of length m at once (one per tensor of a shape group):
     x [T * L, m] (row t * L + l = tensor t, local worker l) -> [T, m] sums in the reference ring
-    order of each tensor (collectives.py:177-236), one all-to-all + one all-gather for the group."""
+    order of each tensor (collectives.py:177-236), one all-to-all + one all-gather for the group.
+    Few launches: the send layout [W][T][L][S] is one permuted copy of x padded to W * S columns;
+    with one worker per rank the fold reads the received rows in place."""
     W, L = comm.world, x.shape[0] // T
     S = -(-m // W)
     xv = x.reshape(T, L, m)
-    send = torch.empty(W, T, L, S, dtype=torch.float32, device=x.device)
-    for r in range(W):
-        lo, hi = r * S, min(m, (r + 1) * S)
-        if hi > lo:
-            send[r, :, :, : hi - lo].copy_(xv[:, :, lo:hi])
-        if hi - lo < S:
-            send[r, :, :, max(0, hi - lo):].zero_()
-    recv = comm.all_to_all(send, phase)                         # [W][T][L][S]: rank r's workers
-    rows = recv.permute(1, 0, 2, 3).reshape(T, n, S).contiguous()   # [T][worker][S]
+    if W * S != m:
+        xp = torch.zeros(T, L, W * S, dtype=torch.float32, device=x.device)
+        xp[:, :, :m].copy_(xv)
+        xv = xp
+    send = xv.reshape(T, L, W, S).permute(2, 0, 1, 3).contiguous()   # [W][T][L][S]
+    recv = comm.all_to_all(send, phase)                              # [W][T][L][S]: rank r's workers
+    if L == 1:   # worker r's row of tensor t at (r * T + t) * S
+        rows, ld, stride = recv, T * S, S
+    else:
+        rows, ld, stride = recv.permute(1, 0, 2, 3).reshape(T, n, S).contiguous(), S, n * S
     s0 = comm.rank * S
     my_len = max(0, min(S, m - s0))
     out = torch.empty(T, S, dtype=torch.float32, device=x.device)
     if my_len < S:
         out[:, my_len:].zero_()
     if my_len:
-        _native.call("gc_float_fold_batched_slice", T, n, my_len, rows.data_ptr(), S, n * S, s0, -(-m // n), 0, 0, 0,
-                     out.data_ptr(), S, _sp())
+        _native.call("gc_float_fold_batched_slice", T, n, my_len, rows.data_ptr(), ld, stride, s0, -(-m // n), 0, 0,
+                     0, out.data_ptr(), S, _sp())
     gathered = comm.all_gather_rows(out.reshape(1, T * S), phase)    # [W][T * S]
+    if W == 1:
+        return gathered.reshape(T, S)
     return gathered.reshape(W, T, S).permute(1, 0, 2).reshape(T, W * S)[:, :m].contiguous()
 
 

@@ -136,3 +136,56 @@ def test_ddp_bucket_rebuild_carries_residuals(nonfinite):
                     resid[w][i] = st.residuals[w][o:o + sizes[i]].copy()
                     o += sizes[i]
     assert sk0 == sk1 == ([1] if nonfinite else [])
+
+
+def _train_chunked(rank, world):
+    import torch
+    import torch.nn as nn
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.ddp import CompressionHookState, compression_hook
+    torch.cuda.set_device(0)
+    torch.manual_seed(0)
+    model = nn.Sequential(nn.Linear(64, 128), nn.ReLU(), nn.Linear(128, 64), nn.ReLU(), nn.Linear(64, 10)).cuda()
+    ddp = nn.parallel.DistributedDataParallel(model, device_ids=[0], bucket_cap_mb=1000)
+    state = CompressionHookState(gcb.PowerSgdConfig(2), gcb.SeedSpec(5), record=True, chunked=True)
+    ddp.register_comm_hook(state, compression_hook)
+    opt = torch.optim.SGD(ddp.parameters(), lr=0.1)
+    log = []
+    for step in range(3):
+        g = torch.Generator().manual_seed(100 * step + rank)
+        x = torch.randn(32, 64, generator=g).cuda()
+        y = torch.randint(0, 10, (32,), generator=g).cuda()
+        opt.zero_grad()
+        nn.functional.cross_entropy(ddp(x), y).backward()
+        torch.cuda.synchronize()
+        local = state.last_inputs[0].reshape(-1).cpu().numpy()
+        est = state.last_results[0].estimate_tensor.cpu().numpy()
+        ids, offs, numels = state.last_layouts[0]
+        pidx = {id(p): i for i, p in enumerate(model.parameters())}
+        log.append((local, est, [(pidx[i], o, m) for i, o, m in zip(ids, offs, numels)]))
+        opt.step()
+    return log
+
+
+def test_ddp_hook_chunked_powersgd_per_parameter():
+    """chunked=True: every parameter is its own reference PowerSGD pipeline (per-layer matrices;
+    the 64x128 and 128x64 weights compressed, biases through the dense bypass), EF carried per
+    parameter across DDP's bucket re-layout; estimates within the fp32 contract of the reference."""
+    from oracle import gradcomp_oracle as orc
+    log0, log1 = run_world(_train_chunked, 2, ())
+    states = {}   # param index -> OracleState (both workers) of its own pipeline
+    prev = None
+    for s in range(3):
+        layout = log0[s][2]
+        assert layout == log1[s][2]
+        if prev is not None and layout != prev:   # a re-laid-out bucket is a new pipeline: EF carried,
+            for st in states.values():            # the warm start restarts (ddp.py)
+                st.warm_q = None
+        prev = layout
+        assert np.array_equal(log0[s][1], log1[s][1])
+        for i, o, m in layout:
+            st = states.setdefault(i, orc.OracleState([np.zeros(m, np.float32) for _ in range(2)]))
+            out = orc.run_round("powersgd", dict(rank=2), st, [log0[s][0][o:o + m], log1[s][0][o:o + m]], 5, s)
+            want = out["estimate"].astype(np.float64)
+            got = log0[s][1][o:o + m].astype(np.float64)
+            assert np.max(np.abs(got - want)) <= 1e-5 * max(np.max(np.abs(want)), 1e-30), (s, i)

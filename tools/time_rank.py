@@ -39,10 +39,15 @@ def make():
         from paper_2407_01378_b200.multitensor import TensorListPipeline, gpt2_medium_sizes
         return TensorListPipeline(gcb.PowerSgdConfig(a.rank), a.n, gpt2_medium_sizes(), gcb.SeedSpec(2024),
                                   validate=False, compute_nmse=False)
+    if a.scheme == "psgd_gpt2_dist":
+        from paper_2407_01378_b200.distributed import DistributedTensorListPipeline
+        from paper_2407_01378_b200.multitensor import gpt2_medium_sizes
+        return DistributedTensorListPipeline(gcb.PowerSgdConfig(a.rank), a.n, gpt2_medium_sizes(), gcb.SeedSpec(2024),
+                                             validate=False)
     raise SystemExit(a.scheme)
 
 
-if a.scheme == "psgd_gpt2":
+if a.scheme.startswith("psgd_gpt2"):
     from paper_2407_01378_b200.multitensor import gpt2_medium_sizes
     a.d = sum(gpt2_medium_sizes())
 g = [torch.randn(a.n, a.d, device="cuda") for _ in range(2)]
