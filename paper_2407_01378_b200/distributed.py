@@ -35,7 +35,7 @@ import torch.distributed as dist
 
 from . import _native
 from .configs import (
-    ChunkedTopKConfig, DenseConfig, PowerSgdConfig, RotatedQuantConfig, TopKConfig, matrix_shape_for, scheme_label,
+    ChunkedTopKConfig, DenseConfig, PowerSgdConfig, RotatedQuantConfig, TopKConfig, scheme_label,
 )
 from .ledger import OverflowStats, TrafficLedger, WorkerGroup
 from .pipeline import RoundResult

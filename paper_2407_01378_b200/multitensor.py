@@ -17,12 +17,11 @@ import numpy as np
 import torch
 
 from . import _native
-from .configs import PowerSgdConfig, matrix_shape_for, scheme_label
+from .configs import PowerSgdConfig, scheme_label
 from .ledger import TrafficLedger, WorkerGroup
 from .pipeline import RoundResult
-from .schemes import (PowerSgdGroup, RoundStats, _simple_stats, make_engine, nmse_from, seed_q_groups,
-                      umma_unaligned)
-from .vectors import GradientVector, SeedSpec
+from .schemes import PowerSgdGroup, _simple_stats, make_engine, seed_q_groups, umma_unaligned
+from .vectors import SeedSpec
 
 
 def _sp() -> int:
