@@ -961,6 +961,9 @@ int check_batch(const gc_psgd_batch *b) {
   GC_REQUIRE(b->tensors >= 1 && b->workers >= 1 && static_cast<int64_t>(b->tensors) * b->workers <= 65535,
              "batch must have 1..65535 (tensor, worker) rows");
   GC_REQUIRE(b->row_offsets != nullptr || b->ld >= 1, "need row_offsets or ld");
+  GC_REQUIRE(!b->rows_aligned || b->row_offsets != nullptr || static_cast<int64_t>(b->tensors) * b->workers == 1 ||
+                 b->ld % 4 == 0,
+             "rows_aligned is set but the row pitch ld is not a multiple of 4 floats");
   return GC_OK;
 }
 
@@ -1093,12 +1096,18 @@ int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, i
   const int64_t per = (rows + splits - 1) / splits;
   double *partial = static_cast<double *>(workspace);
   const bool vec = cols % 4 == 0 && b->rows_aligned && (reinterpret_cast<uintptr_t>(c) & 15) == 0;
-  // TMA-fed column slabs for ranks 1..4 (gc_psgd_tma.cu); GC_PSGD_MTP=cores selects the CUDA-core pass
-  const char *impl = getenv("GC_PSGD_MTP");
-  if (rank <= 4 && (impl == nullptr || std::string(impl) != "cores") && b->tensors == 1 &&
-      b->row_offsets == nullptr &&
-      gc_psgd_mq_tma_supported_impl(1, b->workers, nullptr, b->ld, d, rows, cols, rank, c, c)) {
-    // TMA-fed column slabs (gc_psgd_tma.cu); the same split-K partials and ordered reduction
+  // TMA-fed passes (gc_psgd_tma.cu), the same split-K partials and ordered reduction.  Default:
+  // ranks 5..16 on tcgen05 (MN-major A straight from the TMA boxes; 2.3x the CUDA-core pass at
+  // ranks 8 and 16), ranks 1..4 on the CUDA-core TMA slabs (the 3xTF32 MMAs' shared-memory
+  // traffic costs more than rank-4 FFMA).  GC_PSGD_MTP=umma | slab | cores forces a path.
+  const char *impl_env = getenv("GC_PSGD_MTP");
+  const std::string impl = impl_env ? impl_env : "";
+  const bool tma_ok = b->tensors == 1 && b->row_offsets == nullptr &&
+                      gc_psgd_mq_tma_supported_impl(1, b->workers, nullptr, b->ld, d, rows, cols, rank, c, c);
+  if (tma_ok && (impl == "umma" || (impl.empty() && rank > 4))) {
+    splits = gc_psgd_mtp_umma_launch(L, b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);
+    if (splits < 0) return splits;
+  } else if (tma_ok && rank <= 4 && impl != "cores") {
     splits = gc_psgd_mtp_tma_launch(L, b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);
     if (splits < 0) return splits;
   } else if (vec) {

@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -465,6 +466,7 @@ struct MtpArgs {
   double *partial;         // [L][splits][cols][R]
   int splits;
   int64_t rows_per_split;  // multiple of kM
+  int stages, slots, stage_bytes, op_bytes;   // mtp_umma_kernel's rings
 };
 
 template <int R>
@@ -576,6 +578,258 @@ __global__ void __launch_bounds__(kMtpThreads, 1) mtp_tma_kernel(const __grid_co
   }
 }
 
+// ------------------------------------------------------------------ Q_w = M_w^T P_hat on tcgen05
+// D[cols x r] = M^T P_hat with A = M^T MN-major, straight from the TMA boxes of M: a box is 32 rows
+// (K) x 32 columns (MN, 128 bytes), loaded with the 128-byte swizzle of 32-byte atoms that MN-major
+// tf32 operands require (descriptor layout type 1, 4 K-rows per 512-byte atom), and four boxes side
+// by side are A for UMMA M = 128 columns (LBO = 4 KB between boxes, SBO = 512 B between K-row
+// quads).  kind::tf32 reads the raw fp32 box as A_big (truncation); the producers write
+// A_small = tf32(c - tf32(c)) at the same offsets and the K-major B tiles (P_hat^T of the chunk's
+// 32 rows, split in two; the rows arrive by bulk copy with the box).  D += A_small B_big +
+// A_big B_small + A_big B_big into TMEM, folded to fp64 every 512 rows.  A CTA owns 128 columns
+// and a range of rows; its two producer halves take alternate chunks.
+constexpr int kQtM = 128;                 // columns per CTA (UMMA M)
+constexpr int kQtK = 32;                  // rows per chunk (4 k-steps of 8)
+constexpr int kQtBox = kQtK * 128;        // one 32-row x 32-column box: 4 KB
+constexpr int kQtA = 4 * kQtBox;          // 16 KB: the four column boxes
+// load ring (held from the TMA issue to the chunk's MMAs): the raw boxes (= A_big) and the P_hat
+// rows; operand slots (held from production to the chunk's MMAs): A_small and B.  One CTA per SM;
+// the ring depths are launch arguments sized to fill shared memory (gc_psgd_mtp_umma_launch).
+constexpr int kQtOffP = kQtA;                      // [32][R] fp32 P_hat rows
+constexpr int kQtOffSmall = 0, kQtOffB = kQtA;
+constexpr int kQtProducers = 256, kQtHalf = kQtProducers / 2;
+constexpr int kQtThreads = kQtProducers + 64;   // + the TMA warp + the MMA warp
+constexpr int kQtGroup = 512 / kQtK;      // chunks per TMEM partial
+constexpr int kQtFoldLag = 4;             // group g-1 is folded at chunk 16 g + 4 (long retired)
+constexpr int kQtBarBytes = 512;
+// B = [P_hat_big^T ; P_hat_small^T]: rows 0..H-1 the tf32 heads, rows H..2H-1 the remainders
+// (H = 8, or 16 for rank 16), so one MMA gives A x both halves: two MMAs per k-step for 3xTF32.
+template <int R> struct QtShape {
+  static constexpr int H = R <= 8 ? 8 : 16;
+  static constexpr int N = 2 * H;
+  static constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) /*A MN-major*/ |
+                                    ((N >> 3) << 17) | ((kQtM >> 4) << 24);
+};
+static_assert(kQtFoldLag % 2 == 0 && kQtGroup % 2 == 0, "folds run on the even-chunk half (warps 0..3)");
+
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(kQtBox >> 4) << 16) |
+         (static_cast<uint64_t>(512 >> 4) << 32) | (1ull << 46) | (1ull << 61);
+}
+
+__device__ __forceinline__ void umma_tf32_desc(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+struct RingPos {   // position k of a ring of n slots: idx = k mod n, phase = (k / n) & 1
+  int idx;
+  uint32_t phase;
+  __device__ __forceinline__ void step(int n) {
+    if (++idx == n) {
+      idx = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+template <int R>
+__global__ void __launch_bounds__(kQtThreads, 1) mtp_umma_kernel(const __grid_constant__ CUtensorMap map_c,
+                                                                 const __grid_constant__ MtpArgs a) {
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char *sm = smem_raw + (base - raw);
+  const int kQtStages = a.stages, kQtSlots = a.slots, kQtStage = a.stage_bytes, kQtOp = a.op_bytes;
+  auto stage = [&](int s) { return base + static_cast<uint32_t>(s * kQtStage); };
+  auto op = [&](int h) { return base + static_cast<uint32_t>(kQtStages * kQtStage + h * kQtOp); };
+  constexpr int H = QtShape<R>::H, N = QtShape<R>::N;
+  const uint32_t bars = op(kQtSlots);   // loaded[S], empty[S], full[S], acc[2], op_free[slots]
+  auto loaded_bar = [&](int s) { return bars + 8 * s; };
+  auto empty_bar = [&](int s) { return bars + 8 * (kQtStages + s); };
+  auto full_bar = [&](int s) { return bars + 8 * (2 * kQtStages + s); };
+  auto acc_bar = [&](int x) { return bars + 8 * (3 * kQtStages + x); };
+  auto op_bar = [&](int h) { return bars + 8 * (3 * kQtStages + 2 + h); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + (bars - base) + 8 * (3 * kQtStages + 2 + kQtSlots));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int v = blockIdx.z, split = blockIdx.y;
+  const int64_t col0 = static_cast<int64_t>(blockIdx.x) * kQtM;
+  const int64_t r_begin = split * a.rows_per_split;
+  const int64_t r_end = min(a.rows_full, r_begin + a.rows_per_split);
+  const int64_t nk = r_end > r_begin ? (r_end - r_begin + kQtK - 1) / kQtK : 0;
+  if (tid == 0) {
+    for (int s = 0; s < kQtStages; ++s) {
+      mbar_init(loaded_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+      mbar_init(full_bar(s), kQtHalf);
+    }
+    for (int x = 0; x < 2; ++x) mbar_init(acc_bar(x), 1);
+    for (int x = 0; x < kQtSlots; ++x) mbar_init(op_bar(x), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot)))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int e = tid; e < kQtSlots * N * 8; e += kQtThreads) {   // padding rows of B stay zero
+    const int h = e / (N * 8), o = e - h * (N * 8);
+    *reinterpret_cast<uint4 *>(sm + (op(h) - base) + kQtOffB + o * 16) = make_uint4(0, 0, 0, 0);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  auto chunk_full = [&](int64_t k) { return r_begin + (k + 1) * kQtK <= r_end; };
+  auto issue_load = [&](int64_t k, int s) {
+    const int64_t row = r_begin + k * kQtK;
+    const bool full = chunk_full(k);   // a partial chunk reads its P_hat rows with plain loads
+    mbar_expect_tx(loaded_bar(s), kQtA + (full ? kQtK * R * 4 : 0));
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      tma_load_3d(stage(s) + j * kQtBox, &map_c, static_cast<int>(col0 + 32 * j), static_cast<int>(row),
+                  v, loaded_bar(s));
+    if (full) bulk_load(stage(s) + kQtOffP, a.ph + row * R, kQtK * R * 4, loaded_bar(s));
+  };
+  double acc64[R];
+#pragma unroll
+  for (int b = 0; b < R; ++b) acc64[b] = 0.0;
+  auto fold_group = [&](int64_t gi) {   // warps 0..3: TMEM lanes = the CTA's 128 columns
+    mbar_wait(acc_bar(static_cast<int>(gi & 1)), static_cast<uint32_t>((gi >> 1) & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>((gi & 1) * N);
+#pragma unroll
+    for (int part = 0; part < N / 16; ++part) {   // columns 16 part .. 16 part + 15
+      uint32_t x[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
+            "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15])
+          : "r"(taddr + 16 * part));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {   // column c = 16 part + j is rank c mod H (head or remainder)
+        const int b = (16 * part + j) % H;
+        if (b < R) acc64[b] += static_cast<double>(__uint_as_float(x[j]));
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  };
+
+  if (warp == kQtProducers / 32) {   // TMA warp: the load ring
+    if (lane == 0) {
+      RingPos rs{0, 0};   // ring positions by counting: no runtime divisions in the loops
+      for (int64_t k = 0; k < nk; ++k, rs.step(kQtStages)) {
+        if (k >= kQtStages) mbar_wait(empty_bar(rs.idx), rs.phase ^ 1u);
+        issue_load(k, rs.idx);
+      }
+    }
+  } else if (warp == kQtProducers / 32 + 1) {   // MMA warp: one elected lane issues
+    if (lane == 0) {
+      RingPos rs{0, 0}, ro{0, 0};
+      for (int64_t k = 0; k < nk; ++k, rs.step(kQtStages), ro.step(kQtSlots)) {
+        const int s = rs.idx;
+        const int64_t gi = k / kQtGroup;
+        mbar_wait(full_bar(s), rs.phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dcol = tmem + static_cast<uint32_t>((gi & 1) * N);
+        const uint32_t o = op(ro.idx);
+#pragma unroll
+        for (int ks = 0; ks < kQtK / 8; ++ks) {
+          const uint64_t ab = sdesc_mn(stage(s) + 1024 * ks), as = sdesc_mn(o + kQtOffSmall + 1024 * ks);
+          const uint64_t bd = sdesc(o + kQtOffB + 32 * ks);
+          const uint32_t accum = (k % kQtGroup != 0 || ks != 0) ? 1u : 0u;
+          umma_tf32_desc(dcol, as, bd, QtShape<R>::idesc, accum);   // A_small [B_big B_small]
+          umma_tf32_desc(dcol, ab, bd, QtShape<R>::idesc, 1u);      // A_big   [B_big B_small]
+        }
+        umma_commit(empty_bar(s));
+        umma_commit(op_bar(ro.idx));
+        if (k % kQtGroup == kQtGroup - 1 || k == nk - 1) umma_commit(acc_bar(static_cast<int>(gi & 1)));
+      }
+    }
+  } else {
+    const int half = tid / kQtHalf, ht = tid - half * kQtHalf;
+    int64_t folded = 0;   // groups folded so far (warps 0..3)
+    RingPos rs{0, 0}, ro{0, 0};
+    if (half) {
+      rs.step(kQtStages);
+      ro.step(kQtSlots);
+    }
+    for (int64_t k = half; k < nk; k += 2, rs.step(kQtStages), rs.step(kQtStages), ro.step(kQtSlots), ro.step(kQtSlots)) {
+      const int s = rs.idx;
+      const int64_t k0 = r_begin + k * kQtK;
+      unsigned char *st = sm + s * kQtStage;
+      const int slot = ro.idx;
+      unsigned char *ot = sm + (op(slot) - base);
+      mbar_wait(loaded_bar(s), rs.phase);
+      if (k >= kQtSlots)   // the slot's previous chunk (k - slots) has been consumed by its MMAs
+        mbar_wait(op_bar(slot), ro.phase ^ 1u);
+#pragma unroll
+      for (int u = 0; u < kQtA / 16 / kQtHalf; ++u) {   // A_small at the raw box's offsets
+        const int f = ht + kQtHalf * u;
+        const float4 c = *reinterpret_cast<const float4 *>(st + 16 * f);
+        float4 hb, hs;
+        split3(c.x, hb.x, hs.x);
+        split3(c.y, hb.y, hs.y);
+        split3(c.z, hb.z, hs.z);
+        split3(c.w, hb.w, hs.w);
+        *reinterpret_cast<float4 *>(ot + kQtOffSmall + 16 * f) = hs;
+      }
+      if (ht < R * 8) {   // B = P_hat^T of the chunk's rows: row n (< R), 4 k per thread
+        const int n = ht >> 3, ch = ht & 7;
+        const float *prow = reinterpret_cast<const float *>(st + kQtOffP);
+        const bool full = chunk_full(k);
+        float t[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int kk = 4 * ch + e;
+          t[e] = full ? prow[kk * R + n] : (k0 + kk < r_end ? __ldg(a.ph + (k0 + kk) * R + n) : 0.0f);
+        }
+        float4 hb, hs;
+        split3(t[0], hb.x, hs.x);
+        split3(t[1], hb.y, hs.y);
+        split3(t[2], hb.z, hs.z);
+        split3(t[3], hb.w, hs.w);
+        *reinterpret_cast<float4 *>(ot + kQtOffB + sw128(n, ch)) = hb;
+        *reinterpret_cast<float4 *>(ot + kQtOffB + sw128(H + n, ch)) = hs;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full_bar(s)) : "memory");
+      if (warp < 4 && k % kQtGroup == kQtFoldLag && k >= kQtGroup) {
+        fold_group(k / kQtGroup - 1);
+        folded = k / kQtGroup;
+      }
+    }
+    if (warp < 4) {
+      for (int64_t g = folded; nk > 0 && g <= (nk - 1) / kQtGroup; ++g) fold_group(g);
+      const int64_t col = col0 + warp * 32 + lane;
+      if (split == a.splits - 1 && a.rows_full < a.rows && col < a.cols) {   // the partly filled row, fp64
+        const int64_t off = a.rows_full * a.cols + col;
+        if (off < a.d) {
+          const double m = static_cast<double>(a.c[v * a.ld + off]);
+#pragma unroll
+          for (int b = 0; b < R; ++b) acc64[b] += m * static_cast<double>(a.ph[a.rows_full * R + b]);
+        }
+      }
+      if (col < a.cols) {
+#pragma unroll
+        for (int b = 0; b < R; ++b)
+          a.partial[((static_cast<int64_t>(v) * a.splits + split) * a.cols + col) * R + b] = acc64[b];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -589,17 +843,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // [L][rows_full][cols] fp32 view of worker rows at base + w * ld, 32 x 128 boxes, SWIZZLE_128B
-bool make_map(CUtensorMap *m, const float *base, int64_t L, int64_t rows_full, int64_t cols, int64_t ld) {
+bool make_map(CUtensorMap *m, const float *base, int64_t L, int64_t rows_full, int64_t cols, int64_t ld,
+              uint32_t box_rows = kM, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows_full), static_cast<cuuint64_t>(L)};
   // one worker: the worker stride is never used, any multiple of 16 bytes will do
   const int64_t ld_map = L == 1 ? (ld + 3) / 4 * 4 : ld;
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols * 4), static_cast<cuuint64_t>(ld_map * 4)};
-  cuuint32_t box[3] = {kKc, kM, 1};
+  cuuint32_t box[3] = {kKc, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -674,6 +929,74 @@ int gc_psgd_mtp_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     gc_set_error(std::string("mtp_tma_kernel: ") + cudaGetErrorString(e));
+    return GC_ERR_CUDA;
+  }
+  return static_cast<int>(splits);
+}
+
+// tcgen05 Q_w = M_w^T P_hat (MN-major A from the TMA boxes): fp64 split-K partials
+// partial[w][split][col][R]; returns the split count or a negative status.
+int gc_psgd_mtp_umma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
+                            const float *p_hat, double *partial, int64_t max_splits, cudaStream_t st) {
+  const int64_t rows_full = d / cols;
+  const int64_t cblocks = (cols + kQtM - 1) / kQtM;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t chunks = (rows_full + kQtK - 1) / kQtK;
+  int64_t splits = sms / (cblocks * L);
+  if (splits > max_splits) splits = max_splits;
+  if (splits > chunks) splits = chunks;
+  if (splits < 1) splits = 1;
+  const int64_t per = (chunks + splits - 1) / splits;
+  splits = (chunks + per - 1) / per;
+  CUtensorMap mc;
+  if (!make_map(&mc, c, L, rows_full, cols, ld, kQtK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+    gc_set_error("cuTensorMapEncodeTiled failed for the Q = M^T P_hat operand");
+    return GC_ERR_CUDA;
+  }
+  MtpArgs a{};
+  a.d = d;
+  a.rows = rows;
+  a.cols = cols;
+  a.rows_full = rows_full;
+  a.ld = ld;
+  a.c = c;
+  a.ph = p_hat;
+  a.partial = partial;
+  a.splits = static_cast<int>(splits);
+  a.rows_per_split = per * kQtK;
+  const dim3 grid(static_cast<unsigned>(cblocks), static_cast<unsigned>(splits), static_cast<unsigned>(L));
+  // rings: operand slots first (the producers wait on them), then as many load stages as fit
+  const int n_cols = rank <= 8 ? 16 : 32;
+  a.stage_bytes = kQtA + (kQtK * rank * 4 + 1023) / 1024 * 1024;
+  a.op_bytes = kQtA + n_cols * 128;
+  const char *e_slots = getenv("GC_MTPU_SLOTS");
+  a.slots = e_slots ? atoi(e_slots) : (rank <= 8 ? 6 : 4);
+  const int smem_cap = 232448 - 1024 - kQtBarBytes;
+  a.stages = (smem_cap - a.slots * a.op_bytes) / a.stage_bytes;
+  if (const char *e_st = getenv("GC_MTPU_STAGES")) a.stages = std::min(a.stages, atoi(e_st));
+  if (a.stages > 16) a.stages = 16;
+  if (a.slots < 2 || a.slots > 16 || a.stages < 2) {
+    gc_set_error("mtp_umma_kernel: ring sizes do not fit shared memory");
+    return GC_ERR_UNSUPPORTED;
+  }
+  const int smem = a.stages * a.stage_bytes + a.slots * a.op_bytes + kQtBarBytes + 1024;
+#define GC_MTPU(RR)                                                                                 \
+  case RR:                                                                                          \
+    cudaFuncSetAttribute(mtp_umma_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
+    mtp_umma_kernel<RR><<<grid, kQtThreads, smem, st>>>(mc, a);                                    \
+    break;
+  switch (rank) {
+    GC_MTPU(1) GC_MTPU(2) GC_MTPU(3) GC_MTPU(4) GC_MTPU(5) GC_MTPU(6) GC_MTPU(7) GC_MTPU(8) GC_MTPU(16)
+    default:
+      gc_set_error("rank must be 1..8 or 16");
+      return GC_ERR_UNSUPPORTED;
+  }
+#undef GC_MTPU
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    gc_set_error(std::string("mtp_umma_kernel: ") + cudaGetErrorString(e));
     return GC_ERR_CUDA;
   }
   return static_cast<int>(splits);

@@ -153,11 +153,11 @@ def test_tma_pass_matches_register_pass():
 
 
 @pytest.mark.parametrize("which", ["partial", "full"])
-@pytest.mark.parametrize("r", [1, 3, 4, 8])
+@pytest.mark.parametrize("r", [1, 3, 4, 5, 8, 16])
 def test_mtp_tma_matches_cuda_core_pass(which, r, monkeypatch):
-    """Q_w = M_w^T P_hat from the TMA-fed slab kernel (ranks 1..4; larger ranks take the CUDA-core
-    pass either way) against the CUDA-core pass (GC_PSGD_MTP=cores) and an fp64 reference: both
-    within far less than the 1e-5 contract."""
+    """Q_w = M_w^T P_hat from every path -- the default (TMA slabs for ranks 1..4, tcgen05 above),
+    the CUDA-core pass (GC_PSGD_MTP=cores) and the tcgen05 pass at any rank (GC_PSGD_MTP=umma) --
+    against an fp64 reference: all within far less than the 1e-5 contract."""
     import ctypes
     from paper_2407_01378_b200 import _native
     from paper_2407_01378_b200.configs import matrix_shape_for
@@ -177,6 +177,10 @@ def test_mtp_tma_matches_cuda_core_pass(which, r, monkeypatch):
     monkeypatch.setenv("GC_PSGD_MTP", "cores")
     _native.call("gc_psgd_mtp", ctypes.byref(batch), d, rows, cols, r, c.data_ptr(), ph.data_ptr(), q2.data_ptr(),
                  ws.data_ptr(), sp)
+    q3 = torch.empty(n, cols, r, device="cuda")
+    monkeypatch.setenv("GC_PSGD_MTP", "umma")      # tcgen05, MN-major A from the TMA boxes
+    _native.call("gc_psgd_mtp", ctypes.byref(batch), d, rows, cols, r, c.data_ptr(), ph.data_ptr(), q3.data_ptr(),
+                 ws.data_ptr(), sp)
     torch.cuda.synchronize()
     m = torch.zeros(n, rows * cols, dtype=torch.float64, device="cuda")
     m[:, :d] = c.double()
@@ -184,6 +188,7 @@ def test_mtp_tma_matches_cuda_core_pass(which, r, monkeypatch):
     scale = ref.abs().max().item()
     assert (q1.double() - ref).abs().max().item() <= 1e-6 * scale
     assert (q2.double() - ref).abs().max().item() <= 1e-6 * scale
+    assert (q3.double() - ref).abs().max().item() <= 1e-6 * scale
 
 
 def test_batched_groups_defer_bitwise():

@@ -6,14 +6,16 @@ for compute-sanitizer (memcheck, racecheck, synccheck):
 cases: thc_fused (n = 8, B = 1024, 2 rounds), thc_rank (per-rank K1/K2/K3 on a one-rank gloo
 group), psgd_umma (register-fed tcgen05 P = M Q), psgd_tma (TMA-fed tcgen05 P = M Q with the
 deferred EF update, TMA Q = M^T P_hat, Cholesky orthonormalization; 3 rounds), psgd_batched (one
-tensor map per tensor of a shape group), psgd_mtp_ef (cluster / DSMEM Q + EF pass), topk, topkc."""
+tensor map per tensor of a shape group), psgd_mtp_ef (cluster / DSMEM Q + EF pass), psgd_mtp_umma
+(tcgen05 Q = M^T P_hat at ranks 4 / 8 / 16: several TMEM fold groups, a partial chunk and row),
+topk, topkc."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2407_01378_b200 as gcb
 
-cases = sys.argv[1:] or ["thc_fused", "thc_rank", "psgd_umma", "psgd_tma", "psgd_batched", "psgd_mtp_ef", "topk",
-                         "topkc"]
+cases = sys.argv[1:] or ["thc_fused", "thc_rank", "psgd_umma", "psgd_tma", "psgd_batched", "psgd_mtp_ef",
+                         "psgd_mtp_umma", "topk", "topkc"]
 torch.cuda.set_device(0)
 S = gcb.SeedSpec(7)
 
@@ -57,6 +59,23 @@ for c in cases:
         pipe = gcb.make_pipeline(gcb.PowerSgdConfig(4), n, d, S, compute_nmse=False)
         rounds(pipe, torch.randn(n, d, device="cuda"))
         os.environ["GC_PSGD_MTP_EF"] = "0"
+    elif c == "psgd_mtp_umma":
+        import ctypes
+        from paper_2407_01378_b200 import _native
+        os.environ["GC_PSGD_MTP"] = "umma"
+        rows, cols = 1100, 260          # 35 chunks of 32 rows: three fold groups, a partial chunk
+        d = rows * cols - 40            # and a partly filled last row (d % 4 == 0: aligned worker rows)
+        for r in (4, 8, 16):
+            c = torch.randn(2, d, device="cuda")
+            ph = torch.randn(rows, r, device="cuda")
+            batch = _native.PsgdBatch(1, 2, None, d, None, 1, 0)
+            ws = torch.empty(int(_native.lib().gc_psgd_workspace_bytes(2, rows, cols, r)), dtype=torch.uint8,
+                             device="cuda")
+            q = torch.empty(2, cols, r, device="cuda")
+            _native.call("gc_psgd_mtp", ctypes.byref(batch), d, rows, cols, r, c.data_ptr(), ph.data_ptr(),
+                         q.data_ptr(), ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        del os.environ["GC_PSGD_MTP"]
     elif c == "topk":
         n, d = 2, 1 << 16
         rounds(gcb.make_pipeline(gcb.TopKConfig(d // 100), n, d, S), torch.randn(n, d, device="cuda"))
