@@ -12,7 +12,7 @@ NVFLAGS  := $(ARCH) $(EXTRA) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude
 EXACT    := -fmad=false
 
 CU_EXACT := gc_thc.cu gc_thc_fused.cu gc_thc_rank.cu gc_util.cu gc_dense.cu gc_topk.cu gc_chunk.cu
-CU_FAST  := gc_psgd.cu gc_psgd_umma.cu gc_psgd_tma.cu
+CU_FAST  := gc_psgd.cu gc_psgd_umma.cu gc_psgd_tma.cu gc_psgd_async.cu
 CPP      := gc_host.cpp
 
 OBJS := $(patsubst %.cu,$(OBJDIR)/%.o,$(CU_EXACT) $(CU_FAST)) $(patsubst %.cpp,$(OBJDIR)/%.o,$(CPP))

@@ -334,6 +334,12 @@ int gc_psgd_mq_deferred_batched(const gc_psgd_batch *b, const int64_t *host_tens
                                 int64_t cols, int32_t rank, const float *grads, float *resid, const float *q,
                                 const float *ef_p_hat, const float *ef_q_workers, float *p, void *workspace,
                                 void *stream);
+/* 1 when gc_psgd_mq_deferred_batched accepts the layout: TMA-fed as above, or -- for row pitches a
+ * tensor map cannot describe (cols % 4 != 0, unaligned tensor starts) -- fed by 4-byte cp.async
+ * (any 4-byte aligned grads / resid, row_offsets or ld, rank 1..8 or 16; host_tensor_offsets may
+ * then be NULL).  Same arithmetic, same outputs. */
+int gc_psgd_mq_deferred_supported(const gc_psgd_batch *b, const int64_t *host_tensor_offsets, int64_t d,
+                                  int64_t rows, int64_t cols, int32_t rank, const void *grads, const void *resid);
 /* Q_w = M_w^T P_hat (pipelines.py:354). */
 int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                 const float *p_hat, float *q, void *workspace, void *stream);

@@ -967,6 +967,11 @@ int check_batch(const gc_psgd_batch *b) {
   return GC_OK;
 }
 
+std::string getenv_str(const char *name) {
+  const char *v = getenv(name);
+  return v ? v : "";
+}
+
 Rows rows_of(const gc_psgd_batch *b) { return Rows{b->row_offsets, b->ld, b->workers}; }
 
 }  // namespace
@@ -1049,6 +1054,14 @@ int gc_psgd_mq_tma_supported_batched(const gc_psgd_batch *b, const int64_t *host
                                        resid);
 }
 
+int gc_psgd_mq_deferred_supported(const gc_psgd_batch *b, const int64_t *host_tensor_offsets, int64_t d,
+                                  int64_t rows, int64_t cols, int32_t rank, const void *grads, const void *resid) {
+  if (b == nullptr || d < 1 || rows * cols < d || d < cols) return 0;
+  if (gc_psgd_mq_tma_supported_batched(b, host_tensor_offsets, d, rows, cols, rank, grads, resid)) return 1;
+  if (b->tensors > 1 && b->row_offsets == nullptr) return 0;
+  return gc_psgd_mq_async_supported_impl(rank, grads, resid);
+}
+
 int gc_psgd_mq_deferred_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offsets, int64_t d, int64_t rows,
                                 int64_t cols, int32_t rank, const float *grads, float *resid, const float *q,
                                 const float *ef_p_hat, const float *ef_q_workers, float *p, void *workspace,
@@ -1057,16 +1070,22 @@ int gc_psgd_mq_deferred_batched(const gc_psgd_batch *b, const int64_t *host_tens
   GC_REQUIRE(d >= 1 && rows * cols >= d && grads && q && p && workspace, "invalid argument");
   GC_REQUIRE((ef_p_hat == nullptr) == (ef_q_workers == nullptr), "deferred EF needs both factors or neither");
   GC_REQUIRE(ef_p_hat == nullptr || resid != nullptr, "deferred EF needs the residual buffer");
-  if (!gc_psgd_mq_tma_supported_batched(b, host_tensor_offsets, d, rows, cols, rank, grads, resid)) {
-    gc_set_error("TMA P = M Q needs cols % 4 == 0, ld % 4 == 0, 16-byte aligned tensor starts (host offsets for a "
-                 "batch of tensors), d >= cols and a compiled rank");
+  if (!gc_psgd_mq_deferred_supported(b, host_tensor_offsets, d, rows, cols, rank, grads, resid)) {
+    gc_set_error("deferred P = M Q needs 4-byte aligned buffers, d >= cols and a compiled rank");
     return GC_ERR_UNSUPPORTED;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int L = b->tensors * b->workers;
-  const int slabs = gc_psgd_mq_tma_launch(b->tensors, b->workers, host_tensor_offsets, b->row_offsets, b->ld, d, rows,
-                                          cols, rank, grads, resid, q, ef_p_hat,
-                                          ef_q_workers, static_cast<double *>(workspace), (cols + 1023) / 1024, st);
+  // TMA boxes when a tensor map describes the rows, else the cp.async-fed pass (gc_psgd_async.cu)
+  const bool tma = gc_psgd_mq_tma_supported_batched(b, host_tensor_offsets, d, rows, cols, rank, grads, resid) &&
+                   getenv_str("GC_PSGD_MQ_FEED") != "async";
+  const int slabs =
+      tma ? gc_psgd_mq_tma_launch(b->tensors, b->workers, host_tensor_offsets, b->row_offsets, b->ld, d, rows, cols,
+                                  rank, grads, resid, q, ef_p_hat, ef_q_workers, static_cast<double *>(workspace),
+                                  (cols + 1023) / 1024, st)
+          : gc_psgd_mq_async_launch(b->tensors, b->workers, b->row_offsets, host_tensor_offsets, b->ld, d, rows, cols,
+                                    rank, grads, resid, q, ef_p_hat, ef_q_workers, static_cast<double *>(workspace),
+                                    (cols + 1023) / 1024, st);
   if (slabs < 0) return slabs;
   const int64_t total = static_cast<int64_t>(L) * rows * rank;
   mq_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(

@@ -697,9 +697,9 @@ class _PowerSgd(_Base):
             # TMA pass takes this layout (pipelines.py:338-368 with ef_apply / ef_update)
             vec = bool(_native.lib().gc_psgd_vectorizable(grp.cols, g.data_ptr(), res.data_ptr(), g.stride(0)))
             grp.set_ld(g.stride(0), vec)
-            if vec and _native.lib().gc_psgd_mq_tma_supported(ctypes.byref(grp.batch), d, grp.rows, grp.cols,
-                                                              grp.rank, g.data_ptr(), res.data_ptr()):
-                grp.run(res.data_ptr(), res.data_ptr(), est.data_ptr(), r, grads_ptr=g.data_ptr(), vec=True,
+            if _native.lib().gc_psgd_mq_deferred_supported(ctypes.byref(grp.batch), None, d, grp.rows, grp.cols,
+                                                           grp.rank, g.data_ptr(), res.data_ptr()):
+                grp.run(res.data_ptr(), res.data_ptr(), est.data_ptr(), r, grads_ptr=g.data_ptr(), vec=vec,
                         fold=self._fold)
                 self.launches += 6
                 ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)

@@ -657,13 +657,15 @@ class PowerSgdGroup:
             return out
 
         p = self._buf("p", (T * L, rows, r))
-        # P = M Q on tcgen05: TMA-fed when the layout allows it (then the previous round's EF update
-        # rides along: deferred EF), float4 producer for aligned rows, masked scalars otherwise
+        # P = M Q on tcgen05 with the previous round's EF update riding along (deferred EF): TMA-fed
+        # when a tensor map describes the rows, cp.async-fed otherwise (gc_psgd_mq_deferred_batched).
+        # GC_PSGD_TMA=0: the register-fed pass (float4 producer for aligned rows, masked scalars
+        # otherwise) with eager EF
         umma = vec or umma_unaligned()
         rp = ef_resid_ptr if ef_resid_ptr is not None else resid_ptr
         hoffs = self.host_offsets_arg()
         tma = (not multi and grads_ptr is not None and rp is not None and os.environ.get("GC_PSGD_TMA", "1") != "0"
-               and bool(_native.lib().gc_psgd_mq_tma_supported_batched(bref, hoffs, d, rows, cols, r, grads_ptr, rp)))
+               and bool(_native.lib().gc_psgd_mq_deferred_supported(bref, hoffs, d, rows, cols, r, grads_ptr, rp)))
         if self.pending is not None and not (tma and self.pending[0] == rp):
             self.materialize(rp)
         if tma:

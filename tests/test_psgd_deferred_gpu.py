@@ -215,3 +215,85 @@ def test_batched_groups_defer_bitwise():
     for r in range(4):
         assert np.array_equal(e0[r], e1[r]), r
     assert np.array_equal(r0, r1)
+
+
+def test_unaligned_groups_defer_bitwise():
+    """Row pitches no tensor map can describe (cols % 4 != 0, odd tensor offsets, a partly filled
+    last row): the cp.async-fed P = M Q pass with the deferred EF update gives the eager schedule's
+    rounds bit for bit, and the residuals read back through the API match."""
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200.configs import matrix_shape_for
+    from paper_2407_01378_b200.multitensor import TensorListPipeline
+    sizes = [150 * 150, 77 * 77, 150 * 150 - 7, 111 * 111, 77 * 77, 100, 150 * 150]
+    assert all(matrix_shape_for(s)[1] % 4 for s in sizes if s >= 4096)
+    n, D = 2, sum(sizes)
+    rng = np.random.default_rng(23)
+    grads = [torch.from_numpy(rng.standard_normal((n, D)).astype(np.float32)).cuda() for _ in range(4)]
+
+    def run(defer):
+        pipe = TensorListPipeline(gcb.PowerSgdConfig(4), n, sizes, gcb.SeedSpec(9), compute_nmse=False)
+        for grp in pipe.groups:
+            grp.defer = defer
+        ests = [pipe.run_round(g, r).estimate.logical.copy() for r, g in enumerate(grads)]
+        engaged = sum(grp.pending is not None for grp in pipe.groups)
+        return ests, np.stack(pipe.residuals), engaged
+
+    e0, r0, _ = run(False)
+    e1, r1, engaged = run(True)
+    assert engaged >= 3, "the unaligned groups did not take the deferred path"
+    for r in range(4):
+        assert np.array_equal(e0[r], e1[r]), r
+    assert np.array_equal(r0, r1)
+
+
+@pytest.mark.parametrize("r", [1, 4, 8, 16])
+@pytest.mark.parametrize("layout", ["unaligned", "even", "aligned_forced"])
+def test_async_mq_pass(r, layout, monkeypatch):
+    """gc_psgd_mq_deferred_batched on the cp.async feed: corrected = f32(g + r) written over the
+    residuals bit for bit, P = M Q within 1e-5 of fp64 (3xTF32 with B halves packed along N), with
+    a batch of T = 3 tensors at odd offsets (unaligned) or forced on a TMA-capable layout."""
+    import ctypes
+    from paper_2407_01378_b200 import _native
+    from paper_2407_01378_b200.configs import matrix_shape_for
+    # unaligned: odd tensor offsets (4-byte copies); even: cols % 4 == 2 with even offsets (8-byte
+    # copies, GPT-2's case); aligned_forced: a TMA-capable layout on the cp.async feed
+    d = {"unaligned": 150 * 150 - 7, "even": 150 * 150 - 8, "aligned_forced": 200 * 200 - 8}[layout]
+    rows, cols = matrix_shape_for(d)
+    T, L = 3, 2
+    pad = {"unaligned": 1, "even": 2, "aligned_forced": 0}[layout]
+    ld = T * (d + pad) + 3 * pad
+    offs_t = [t * (d + pad) + pad for t in range(T)]
+    row_offs = torch.tensor([w * ld + offs_t[t] for t in range(T) for w in range(L)], dtype=torch.int64,
+                            device="cuda")
+    if layout == "aligned_forced":
+        monkeypatch.setenv("GC_PSGD_MQ_FEED", "async")
+    g = torch.randn(L, ld, device="cuda")
+    res = torch.randn(L, ld, device="cuda")
+    q = torch.randn(T, cols, r, device="cuda")
+    batch = _native.PsgdBatch(T, L, row_offs.data_ptr(), ld, None, 0, 0)
+    hoffs = (ctypes.c_int64 * T)(*offs_t)
+    lib = _native.lib()
+    assert lib.gc_psgd_mq_deferred_supported(ctypes.byref(batch), hoffs, d, rows, cols, r, g.data_ptr(),
+                                             res.data_ptr())
+    assert bool(lib.gc_psgd_mq_tma_supported_batched(ctypes.byref(batch), hoffs, d, rows, cols, r, g.data_ptr(),
+                                                     res.data_ptr())) == (layout == "aligned_forced")
+    ws = torch.empty(int(lib.gc_psgd_workspace_bytes(T * L, rows, cols, r)), dtype=torch.uint8, device="cuda")
+    p = torch.empty(T * L, rows, r, device="cuda")
+    want_c = g + res
+    r_before = res.clone()
+    _native.call("gc_psgd_mq_deferred_batched", ctypes.byref(batch), hoffs, d, rows, cols, r, g.data_ptr(),
+                 res.data_ptr(), q.data_ptr(), None, None, p.data_ptr(), ws.data_ptr(),
+                 torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    mask = torch.zeros(L, ld, dtype=torch.bool, device="cuda")
+    for t in range(T):
+        mask[:, offs_t[t]:offs_t[t] + d] = True
+    assert torch.equal(res[mask], want_c[mask])             # corrected over the tensors
+    assert torch.equal(res[~mask], r_before[~mask])         # nothing outside them touched
+    for t in range(T):
+        for w in range(L):
+            m = torch.zeros(rows * cols, dtype=torch.float64, device="cuda")
+            m[:d] = want_c[w, offs_t[t]:offs_t[t] + d].double()
+            ref = m.reshape(rows, cols) @ q[t].double()
+            got = p[t * L + w].double()
+            assert (got - ref).abs().max().item() <= 1e-5 * ref.abs().max().item(), (t, w)   # the contract
