@@ -343,6 +343,12 @@ int gc_psgd_mq_deferred_supported(const gc_psgd_batch *b, const int64_t *host_te
 /* Q_w = M_w^T P_hat (pipelines.py:354). */
 int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                 const float *p_hat, float *q, void *workspace, void *stream);
+/* The same for a batch of T same-shape tensors with row offsets, given the host copy of the tensor
+ * offsets (host_tensor_offsets[T], as gc_psgd_mq_deferred_batched): one tensor map per tensor when
+ * the rows are 16-byte aligned; NULL (or unaligned rows) takes the cp.async-fed pass. */
+int gc_psgd_mtp_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offsets, int64_t d, int64_t rows,
+                        int64_t cols, int32_t rank, const float *c, const float *p_hat, float *q, void *workspace,
+                        void *stream);
 /* Q_w = M_w^T P_hat (pipelines.py:354) fused with the EF update r_w = c_w - P_hat Q_w^T
  * (pipelines.py:357-361, the own-decode half of gc_psgd_decode): resid holds the corrected
  * matrices on entry and the residuals on return, q receives Q_w.  One read and one write of M

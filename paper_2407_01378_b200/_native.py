@@ -127,6 +127,7 @@ SIGNATURES = {
     "gc_psgd_mq_deferred_batched": (c_int, [POINTER(PsgdBatch), P, I64, I64, I64, I32, P, P, P, P, P, P, P, P]),
     "gc_psgd_mq_deferred_supported": (c_int, [POINTER(PsgdBatch), P, I64, I64, I64, I32, P, P]),
     "gc_psgd_mtp": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P, P]),
+    "gc_psgd_mtp_batched": (c_int, [POINTER(PsgdBatch), P, I64, I64, I64, I32, P, P, P, P, P]),
     "gc_psgd_mtp_ef_supported": (c_int, [I64, I64, I32, I32]),
     "gc_psgd_mtp_ef": (c_int, [POINTER(PsgdBatch), I64, I64, I64, I32, P, P, P, P]),
     "gc_psgd_orthonormalize": (c_int, [I32, I64, I32, P, P, P, P, P]),

@@ -31,7 +31,8 @@ int gc_psgd_mq_tma_launch(int32_t T, int32_t L, const int64_t *host_tensor_offse
                           int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
                           float *resid, const float *q, const float *ef_ph, const float *ef_qw, double *partial,
                           int64_t max_splits, cudaStream_t st);
-int gc_psgd_mtp_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
+int gc_psgd_mtp_tma_launch(int32_t T, int32_t L, const int64_t *host_tensor_offsets, const int64_t *row_start,
+                           int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                            const float *p_hat, double *partial, int64_t max_splits, cudaStream_t st);
 int gc_psgd_mtp_umma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                             const float *p_hat, double *partial, int64_t max_splits, cudaStream_t st);
@@ -40,6 +41,9 @@ int gc_psgd_mq_async_launch(int32_t T, int32_t L, const int64_t *row_offsets, co
                             int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
                             float *resid, const float *q, const float *ef_ph, const float *ef_qw, double *partial,
                             int64_t max_splits, cudaStream_t st);
+int gc_psgd_mtp_async_launch(int32_t V, int32_t L, const int64_t *row_offsets, int64_t ld, int64_t d, int64_t rows,
+                             int64_t cols, int32_t rank, const float *c, const float *p_hat, double *partial,
+                             int64_t max_splits, cudaStream_t st);
 #define GC_LAUNCH_CHECK(what)                                                     \
   do {                                                                            \
     cudaError_t e_ = cudaGetLastError();                                          \

@@ -1107,6 +1107,12 @@ int gc_psgd_mq_deferred(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t
 
 int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                 const float *p_hat, float *q, void *workspace, void *stream) {
+  return gc_psgd_mtp_batched(b, nullptr, d, rows, cols, rank, c, p_hat, q, workspace, stream);
+}
+
+int gc_psgd_mtp_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offsets, int64_t d, int64_t rows,
+                        int64_t cols, int32_t rank, const float *c, const float *p_hat, float *q, void *workspace,
+                        void *stream) {
   if (int rc = check_batch(b)) return rc;
   GC_REQUIRE(d >= 1 && rows * cols >= d && c && p_hat && q && workspace, "invalid argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1118,16 +1124,27 @@ int gc_psgd_mtp(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, i
   // TMA-fed passes (gc_psgd_tma.cu), the same split-K partials and ordered reduction.  Default:
   // ranks 5..16 on tcgen05 (MN-major A straight from the TMA boxes; 2.3x the CUDA-core pass at
   // ranks 8 and 16), ranks 1..4 on the CUDA-core TMA slabs (the 3xTF32 MMAs' shared-memory
-  // traffic costs more than rank-4 FFMA).  GC_PSGD_MTP=umma | slab | cores forces a path.
+  // traffic costs more than rank-4 FFMA); layouts without a tensor map (batches, unaligned rows)
+  // on cp.async-fed slabs for ranks 1..4.  GC_PSGD_MTP=umma | async | cores | vec forces a path.
   const char *impl_env = getenv("GC_PSGD_MTP");
   const std::string impl = impl_env ? impl_env : "";
-  const bool tma_ok = b->tensors == 1 && b->row_offsets == nullptr &&
-                      gc_psgd_mq_tma_supported_impl(1, b->workers, nullptr, b->ld, d, rows, cols, rank, c, c);
+  const bool single = b->tensors == 1 && b->row_offsets == nullptr;
+  // a batch with row offsets takes tensor maps only with its host tensor offsets
+  const bool maps_ok = (single || (host_tensor_offsets != nullptr && b->row_offsets != nullptr)) &&
+                       gc_psgd_mq_tma_supported_impl(b->tensors, b->workers, single ? nullptr : host_tensor_offsets,
+                                                     b->ld, d, rows, cols, rank, c, c);
+  const bool tma_ok = single && maps_ok;
   if (tma_ok && (impl == "umma" || (impl.empty() && rank > 4))) {
     splits = gc_psgd_mtp_umma_launch(L, b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);
     if (splits < 0) return splits;
-  } else if (tma_ok && rank <= 4 && impl != "cores") {
-    splits = gc_psgd_mtp_tma_launch(L, b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);
+  } else if (maps_ok && rank <= 4 && impl != "cores" && impl != "async") {
+    splits = gc_psgd_mtp_tma_launch(b->tensors, b->workers, single ? nullptr : host_tensor_offsets, b->row_offsets,
+                                    b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);
+    if (splits < 0) return splits;
+  } else if (rank <= 4 && impl != "cores" && impl != "vec") {
+    // batches of tensors and unaligned row pitches: the cp.async-fed slabs (gc_psgd_async.cu)
+    splits = gc_psgd_mtp_async_launch(L, b->workers, b->row_offsets, b->ld, d, rows, cols, rank, c, p_hat, partial,
+                                      splits, st);
     if (splits < 0) return splits;
   } else if (vec) {
     GC_RANK_SWITCH(rank, ({

@@ -482,6 +482,122 @@ __global__ void __launch_bounds__(kThreads, 1) mq_async_kernel(const __grid_cons
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
 }
 
+// ------------------------------------------------------------------ Q_w = M_w^T P_hat (pipelines.py:354)
+// for batches of tensors and row pitches TMA cannot describe: the CUDA-core column slabs of
+// gc_psgd_tma.cu's mtp_tma_kernel (a CTA owns 32 columns and a range of rows; thread = float4 column
+// group x row group; 4 columns x R products per row in fp32, folded into fp64 per 128-row box,
+// the 32 row groups reduced in order) fed by cp.async: every thread copies exactly the elements it
+// reads -- 16-byte cp.async.cg (no L1 allocation) when its rows are 16-byte aligned, else 8- or
+// 4-byte copies -- so a per-thread cp.async.wait_group is the only synchronisation.  The width is
+// picked per (tensor, worker) row at run time from its offset.  Elements past d (the partly filled
+// last row) or past the matrix copy as zeros.  Ranks 1..4.
+constexpr int kMtaThreads = 256;
+constexpr int kMtaAhead = 3;
+constexpr int kMtaStages = kMtaAhead + 1;
+constexpr int kMtaStage = kM * kKc * 4;   // 16 KB: 128 rows x 32 columns, row-major
+
+template <int R>
+__global__ void __launch_bounds__(kMtaThreads) mtp_async_kernel(int64_t d, int64_t rows, int64_t cols, const float *c,
+                                                                const int64_t *row_offs, int64_t ld, int L,
+                                                                const float *ph, int64_t rows_per_split,
+                                                                double *partial, int splits) {
+  static_assert(R <= 4, "rank <= 4");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[kMtaThreads / 8][32][R];
+  const int tid = threadIdx.x;
+  const int v = blockIdx.z, split = blockIdx.y;
+  const int64_t col0 = static_cast<int64_t>(blockIdx.x) * kKc;
+  const int64_t r_begin = split * rows_per_split;
+  const int64_t r_end = min(rows, r_begin + rows_per_split);
+  const int64_t nbox = r_end > r_begin ? (r_end - r_begin + kM - 1) / kM : 0;
+  const int g4 = tid & 7, rg = tid >> 3;   // float4 column group, row group (rows rg + 32 k)
+  const int64_t rb = row_offs ? row_offs[v] : static_cast<int64_t>(v) * ld;
+  const float *cw = c + rb;
+  const float *pht = ph + static_cast<int64_t>(v / L) * rows * R;
+  const int64_t col = col0 + 4 * g4;
+  const int ncol = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(4), cols - col)));
+  // copy width from the alignment of this row's elements (uniform over the CTA)
+  const uintptr_t base_addr = reinterpret_cast<uintptr_t>(cw);
+  const int width = (cols % 4 == 0 && base_addr % 16 == 0) ? 4 : ((cols % 2 == 0 && base_addr % 8 == 0) ? 2 : 1);
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  auto copy_box = [&](int64_t bx, int s) {
+    const int64_t i0 = r_begin + bx * kM;
+#pragma unroll
+    for (int k = 0; k < kM / 32; ++k) {
+      const int row = rg + 32 * k;
+      const int64_t grow = i0 + row;
+      const int64_t e = grow * cols + col;
+      const uint32_t dst = sbase + s * kMtaStage + row * 128 + g4 * 16;
+      // elements of this float4 that are data: columns < cols, index < d, row < r_end
+      const int64_t left = grow < r_end ? min(static_cast<int64_t>(ncol), d - e) : 0;
+      if (left == 4 && width == 4) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(cw + e) : "memory");
+      } else if (left == 4 && width == 2) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(cw + e) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8), "l"(cw + e + 2) : "memory");
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (t < left)
+            cp_async4(dst + 4 * t, cw + e + t);
+          else
+            *reinterpret_cast<float *>(smem_raw + s * kMtaStage + row * 128 + g4 * 16 + 4 * t) = 0.0f;
+        }
+      }
+    }
+  };
+  double acc64[4][R];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc64[t][b] = 0.0;
+  for (int p = 0; p < kMtaAhead; ++p) {
+    if (p < nbox) copy_box(p, p);
+    cp_async_commit();
+  }
+  for (int64_t bx = 0; bx < nbox; ++bx) {
+    const int s = static_cast<int>(bx % kMtaStages);
+    if (bx + kMtaAhead < nbox) copy_box(bx + kMtaAhead, static_cast<int>((bx + kMtaAhead) % kMtaStages));
+    cp_async_commit();
+    cp_async_wait<kMtaAhead>();   // this thread's elements of box bx have landed
+    const int64_t i0 = r_begin + bx * kM;
+    float acc[4][R];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[t][b] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kM / 32; ++k) {
+      const int row = rg + 32 * k;
+      const float4 m = *reinterpret_cast<const float4 *>(smem_raw + s * kMtaStage + row * 128 + g4 * 16);
+      float p[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) p[b] = i0 + row < r_end ? __ldg(pht + (i0 + row) * R + b) : 0.0f;
+      const float mv[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int b = 0; b < R; ++b) acc[t][b] = fmaf(mv[t], p[b], acc[t][b]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc64[t][b] += static_cast<double>(acc[t][b]);
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) red[rg][4 * g4 + t][b] = acc64[t][b];
+  __syncthreads();
+  for (int e = tid; e < 32 * R; e += kMtaThreads) {
+    const int cc = e / R, b = e - cc * R;
+    double x = 0.0;
+#pragma unroll 8
+    for (int w = 0; w < kMtaThreads / 8; ++w) x += red[w][cc][b];
+    if (col0 + cc < cols) partial[((static_cast<int64_t>(v) * splits + split) * cols + col0 + cc) * R + b] = x;
+  }
+}
+
 }  // namespace
 
 int gc_psgd_mq_async_supported_impl(int32_t rank, const void *grads, const void *resid) {
@@ -562,6 +678,42 @@ int gc_psgd_mq_async_launch(int32_t T, int32_t L, const int64_t *row_offsets, co
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     gc_set_error(std::string("mq_async_kernel: ") + cudaGetErrorString(e));
+    return GC_ERR_CUDA;
+  }
+  return static_cast<int>(splits);
+}
+
+// fp64 split-K partials partial[v][split][col][R] of Q_w = M_w^T P_hat for V = T * L virtual rows
+// (rank <= 4, any layout); returns the split count (<= max_splits) or a negative status.
+int gc_psgd_mtp_async_launch(int32_t V, int32_t L, const int64_t *row_offsets, int64_t ld, int64_t d, int64_t rows,
+                             int64_t cols, int32_t rank, const float *c, const float *p_hat, double *partial,
+                             int64_t max_splits, cudaStream_t st) {
+  const int64_t slabs = (cols + kKc - 1) / kKc;
+  const int64_t boxes = (rows + kM - 1) / kM;
+  int64_t splits = (4 * 148 + slabs * V - 1) / (slabs * V);
+  if (splits > max_splits) splits = max_splits;
+  if (splits > boxes) splits = boxes;
+  if (splits < 1) splits = 1;
+  const int64_t per = (boxes + splits - 1) / splits;
+  splits = (boxes + per - 1) / per;
+  const dim3 grid(static_cast<unsigned>(slabs), static_cast<unsigned>(splits), static_cast<unsigned>(V));
+  const int smem = kMtaStages * kMtaStage;
+#define GC_MTA(RR)                                                                                      \
+  case RR:                                                                                              \
+    cudaFuncSetAttribute(mtp_async_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
+    mtp_async_kernel<RR><<<grid, kMtaThreads, smem, st>>>(d, rows, cols, c, row_offsets, ld, L, p_hat, per * kM, \
+                                                          partial, static_cast<int>(splits));           \
+    break;
+  switch (rank) {
+    GC_MTA(1) GC_MTA(2) GC_MTA(3) GC_MTA(4)
+    default:
+      gc_set_error("rank must be 1..4");
+      return GC_ERR_UNSUPPORTED;
+  }
+#undef GC_MTA
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    gc_set_error(std::string("mtp_async_kernel: ") + cudaGetErrorString(e));
     return GC_ERR_CUDA;
   }
   return static_cast<int>(splits);

@@ -462,15 +462,21 @@ constexpr int kMtpSmem = kMtpStages * kMtpStage + 64 + 1024;
 struct MtpArgs {
   int64_t d, rows, cols, rows_full, ld;
   const float *c;          // corrected matrices (the partial row is read from here)
-  const float *ph;         // P_hat [rows][R]
-  double *partial;         // [L][splits][cols][R]
+  const float *ph;         // P_hat [T][rows][R]
+  double *partial;         // [V][splits][cols][R]
   int splits;
   int64_t rows_per_split;  // multiple of kM
   int stages, slots, stage_bytes, op_bytes;   // mtp_umma_kernel's rings
+  int L, v_base;           // mtp_tma_kernel batches: virtual row v = v_base + blockIdx.z = t * L + w
+  const int64_t *row_start;   // device [V] element offset of each virtual row, or null (v * ld)
+};
+// one tensor map [L workers][rows_full][cols] per tensor of a batch (<= kMaxMapT per launch)
+struct MtpMaps {
+  CUtensorMap m[kMaxMapT];
 };
 
 template <int R>
-__global__ void __launch_bounds__(kMtpThreads, 1) mtp_tma_kernel(const __grid_constant__ CUtensorMap map_c,
+__global__ void __launch_bounds__(kMtpThreads, 1) mtp_tma_kernel(const __grid_constant__ MtpMaps maps,
                                                                 const __grid_constant__ MtpArgs a) {
   static_assert(R <= 4, "rank <= 4");
   extern __shared__ unsigned char smem_raw[];
@@ -480,7 +486,10 @@ __global__ void __launch_bounds__(kMtpThreads, 1) mtp_tma_kernel(const __grid_co
   const uint32_t bars = base + kMtpStages * kMtpStage;   // loaded[S], empty[S]
   __shared__ double red[kMtpConsumers / 8][32][R];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int v = blockIdx.z, split = blockIdx.y;
+  const int vl = blockIdx.z, v = a.v_base + vl, split = blockIdx.y;
+  const CUtensorMap *map_c = &maps.m[vl / a.L];
+  const int w = vl % a.L;
+  const float *ph = a.ph + static_cast<int64_t>(v / a.L) * a.rows * R;
   const int64_t col0 = static_cast<int64_t>(blockIdx.x) * kKc;
   const int64_t r_begin = split * a.rows_per_split;
   const int64_t r_end = min(a.rows_full, r_begin + a.rows_per_split);
@@ -502,8 +511,8 @@ __global__ void __launch_bounds__(kMtpThreads, 1) mtp_tma_kernel(const __grid_co
           mbar_wait(bars + 8 * (kMtpStages + s), static_cast<uint32_t>(((b / kMtpStages) - 1) & 1));
         const bool full = i0 + kM <= r_end;   // partial boxes read P_hat with plain loads
         mbar_expect_tx(bars + 8 * s, kTile + (full ? kM * R * 4 : 0));
-        tma_load_3d(base + s * kMtpStage, &map_c, static_cast<int>(col0), static_cast<int>(i0), v, bars + 8 * s);
-        if (full) bulk_load(base + s * kMtpStage + kTile, a.ph + i0 * R, kM * R * 4, bars + 8 * s);
+        tma_load_3d(base + s * kMtpStage, map_c, static_cast<int>(col0), static_cast<int>(i0), w, bars + 8 * s);
+        if (full) bulk_load(base + s * kMtpStage + kTile, ph + i0 * R, kM * R * 4, bars + 8 * s);
       }
     }
     return;
@@ -536,7 +545,7 @@ __global__ void __launch_bounds__(kMtpThreads, 1) mtp_tma_kernel(const __grid_co
         for (int b = 0; b < R; ++b) p[b] = phs[row * R + b];
       } else {
 #pragma unroll
-        for (int b = 0; b < R; ++b) p[b] = i0 + row < r_end ? __ldg(a.ph + (i0 + row) * R + b) : 0.0f;
+        for (int b = 0; b < R; ++b) p[b] = i0 + row < r_end ? __ldg(ph + (i0 + row) * R + b) : 0.0f;
       }
       const float mv[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
@@ -557,9 +566,10 @@ __global__ void __launch_bounds__(kMtpThreads, 1) mtp_tma_kernel(const __grid_co
       const int64_t col = col0 + 4 * g4 + t;
       const int64_t off = a.rows_full * a.cols + col;
       if (col < a.cols && off < a.d) {
-        const double m = static_cast<double>(a.c[v * a.ld + off]);
+        const int64_t rs = a.row_start ? a.row_start[v] : static_cast<int64_t>(v) * a.ld;
+        const double m = static_cast<double>(a.c[rs + off]);
 #pragma unroll
-        for (int b = 0; b < R; ++b) acc64[t][b] += m * static_cast<double>(a.ph[a.rows_full * R + b]);
+        for (int b = 0; b < R; ++b) acc64[t][b] += m * static_cast<double>(ph[a.rows_full * R + b]);
       }
     }
   }
@@ -883,7 +893,8 @@ int gc_psgd_mq_tma_supported_impl(int32_t tensors, int32_t workers, const int64_
 
 // TMA-fed Q_w = M_w^T P_hat: fp64 split-K partials partial[w][split][col][R] (max_splits slots
 // sized by the caller); returns the split count or a negative status.
-int gc_psgd_mtp_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
+int gc_psgd_mtp_tma_launch(int32_t T, int32_t L, const int64_t *host_tensor_offsets, const int64_t *row_start,
+                           int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
                            const float *p_hat, double *partial, int64_t max_splits, cudaStream_t st) {
   const int64_t rows_full = d / cols;
   const int64_t slabs = (cols + kKc - 1) / kKc;
@@ -891,17 +902,13 @@ int gc_psgd_mtp_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t boxes = (rows_full + kM - 1) / kM;
-  int64_t splits = (2 * sms + slabs * L - 1) / (slabs * L);
+  const int64_t V = static_cast<int64_t>(T) * L;
+  int64_t splits = (2 * sms + slabs * V - 1) / (slabs * V);
   if (splits > max_splits) splits = max_splits;
   if (splits > boxes) splits = boxes;
   if (splits < 1) splits = 1;
   const int64_t per = (boxes + splits - 1) / splits;
   splits = (boxes + per - 1) / per;
-  CUtensorMap mc;
-  if (!make_map(&mc, c, L, rows_full, cols, ld)) {
-    gc_set_error("cuTensorMapEncodeTiled failed for the Q = M^T P_hat operand");
-    return GC_ERR_CUDA;
-  }
   MtpArgs a{};
   a.d = d;
   a.rows = rows;
@@ -913,23 +920,37 @@ int gc_psgd_mtp_tma_launch(int32_t L, int64_t ld, int64_t d, int64_t rows, int64
   a.partial = partial;
   a.splits = static_cast<int>(splits);
   a.rows_per_split = per * kM;
-  const dim3 grid(static_cast<unsigned>(slabs), static_cast<unsigned>(splits), static_cast<unsigned>(L));
-#define GC_MTPT(RR)                                                                                  \
-  case RR:                                                                                           \
-    cudaFuncSetAttribute(mtp_tma_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMtpSmem); \
-    mtp_tma_kernel<RR><<<grid, kMtpThreads, kMtpSmem, st>>>(mc, a);                                 \
+  a.L = L;
+  a.row_start = row_start;
+  MtpMaps maps;
+  for (int t0 = 0; t0 < T; t0 += kMaxMapT) {
+    const int tc = T - t0 < kMaxMapT ? T - t0 : kMaxMapT;
+    for (int k = 0; k < tc; ++k) {
+      const int64_t off = host_tensor_offsets ? host_tensor_offsets[t0 + k] : 0;
+      if (!make_map(&maps.m[k], c + off, L, rows_full, cols, ld)) {
+        gc_set_error("cuTensorMapEncodeTiled failed for the Q = M^T P_hat operand");
+        return GC_ERR_CUDA;
+      }
+    }
+    a.v_base = t0 * L;
+    const dim3 grid(static_cast<unsigned>(slabs), static_cast<unsigned>(splits), static_cast<unsigned>(tc * L));
+#define GC_MTPT(RR)                                                                                    \
+  case RR:                                                                                             \
+    cudaFuncSetAttribute(mtp_tma_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMtpSmem);   \
+    mtp_tma_kernel<RR><<<grid, kMtpThreads, kMtpSmem, st>>>(maps, a);                                 \
     break;
-  switch (rank) {
-    GC_MTPT(1) GC_MTPT(2) GC_MTPT(3) GC_MTPT(4)
-    default:
-      gc_set_error("the TMA Q = M^T P_hat pass takes ranks 1..4");
-      return GC_ERR_UNSUPPORTED;
-  }
+    switch (rank) {
+      GC_MTPT(1) GC_MTPT(2) GC_MTPT(3) GC_MTPT(4)
+      default:
+        gc_set_error("the TMA Q = M^T P_hat pass takes ranks 1..4");
+        return GC_ERR_UNSUPPORTED;
+    }
 #undef GC_MTPT
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    gc_set_error(std::string("mtp_tma_kernel: ") + cudaGetErrorString(e));
-    return GC_ERR_CUDA;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      gc_set_error(std::string("mtp_tma_kernel: ") + cudaGetErrorString(e));
+      return GC_ERR_CUDA;
+    }
   }
   return static_cast<int>(splits);
 }

@@ -708,8 +708,8 @@ class PowerSgdGroup:
             if mtp_ef:
                 _native.call("gc_psgd_mtp_ef", bref, d, rows, cols, rc, resid_ptr, ph_c.data_ptr(), qw_c.data_ptr(), sp)
             else:
-                _native.call("gc_psgd_mtp", bref, d, rows, cols, rc, c_ptr, ph_c.data_ptr(), qw_c.data_ptr(),
-                             self.ws.data_ptr(), sp)
+                _native.call("gc_psgd_mtp_batched", bref, hoffs, d, rows, cols, rc, c_ptr, ph_c.data_ptr(),
+                             qw_c.data_ptr(), self.ws.data_ptr(), sp)
             if multi:
                 qw[..., c0:c0 + rc].copy_(qw_c)
             ph_chunks.append(ph_c)

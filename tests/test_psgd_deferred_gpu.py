@@ -297,3 +297,54 @@ def test_async_mq_pass(r, layout, monkeypatch):
             ref = m.reshape(rows, cols) @ q[t].double()
             got = p[t * L + w].double()
             assert (got - ref).abs().max().item() <= 1e-5 * ref.abs().max().item(), (t, w)   # the contract
+
+
+@pytest.mark.parametrize("r", [1, 3, 4])
+@pytest.mark.parametrize("layout", ["unaligned", "even", "aligned"])
+def test_async_mtp_pass(r, layout, monkeypatch):
+    """Q_w = M_w^T P_hat on a batch of T = 3 tensors with row offsets: gc_psgd_mtp (no host
+    offsets: the cp.async-fed slabs, 16-, 8- or 4-byte copies by row alignment), the CUDA-core
+    float4 / scalar pass (GC_PSGD_MTP=vec) and gc_psgd_mtp_batched (one tensor map per tensor when
+    the rows are 16-byte aligned) against fp64, all far inside the 1e-5 contract."""
+    import ctypes
+    from paper_2407_01378_b200 import _native
+    from paper_2407_01378_b200.configs import matrix_shape_for
+    d = {"unaligned": 150 * 150 - 7, "even": 150 * 150 - 8, "aligned": 200 * 200 - 8}[layout]
+    pad = {"unaligned": 1, "even": 2, "aligned": 0}[layout]
+    rows, cols = matrix_shape_for(d)
+    T, L = 3, 2
+    ld = T * (d + pad) + 3 * pad
+    offs_t = [t * (d + pad) + pad for t in range(T)]
+    row_offs = torch.tensor([w * ld + offs_t[t] for t in range(T) for w in range(L)], dtype=torch.int64,
+                            device="cuda")
+    c = torch.randn(L, ld, device="cuda")
+    ph = torch.randn(T, rows, r, device="cuda")
+    aligned = layout == "aligned"
+    batch = _native.PsgdBatch(T, L, row_offs.data_ptr(), ld, None, 1 if aligned else 0, 0)
+    lib = _native.lib()
+    ws = torch.empty(int(lib.gc_psgd_workspace_bytes(T * L, rows, cols, r)), dtype=torch.uint8, device="cuda")
+    sp = torch.cuda.current_stream().cuda_stream
+    outs = []
+    hoffs = (ctypes.c_int64 * T)(*offs_t)
+    for impl in ("", "vec", "batched"):   # batched: tensor maps per tensor when the rows allow (aligned)
+        if impl == "vec":
+            monkeypatch.setenv("GC_PSGD_MTP", impl)
+        else:
+            monkeypatch.delenv("GC_PSGD_MTP", raising=False)
+        q = torch.empty(T * L, cols, r, device="cuda")
+        if impl == "batched":
+            _native.call("gc_psgd_mtp_batched", ctypes.byref(batch), hoffs, d, rows, cols, r, c.data_ptr(),
+                         ph.data_ptr(), q.data_ptr(), ws.data_ptr(), sp)
+        else:
+            _native.call("gc_psgd_mtp", ctypes.byref(batch), d, rows, cols, r, c.data_ptr(), ph.data_ptr(),
+                         q.data_ptr(), ws.data_ptr(), sp)
+        outs.append(q)
+    torch.cuda.synchronize()
+    for t in range(T):
+        for w in range(L):
+            m = torch.zeros(rows * cols, dtype=torch.float64, device="cuda")
+            m[:d] = c[w, offs_t[t]:offs_t[t] + d].double()
+            ref = m.reshape(rows, cols).T @ ph[t].double()
+            scale = ref.abs().max().item()
+            for q in outs:
+                assert (q[t * L + w].double() - ref).abs().max().item() <= 1e-6 * scale, (t, w)
