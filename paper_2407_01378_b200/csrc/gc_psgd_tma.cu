@@ -38,6 +38,7 @@
 #include <string>
 
 #include "gc_internal.h"
+#include "gc_umma.cuh"
 
 namespace {
 
@@ -74,6 +75,20 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
          (2ull << 61);
 }
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((kN >> 3) << 17) | ((kM >> 4) << 24);
+#ifndef GC_MQT_PACK
+#define GC_MQT_PACK 1
+#endif
+// P = M Q's B operand: with GC_MQT_PACK, [Q_big^T ; Q_small^T] packed along N (rows h < H the tf32
+// heads, H + h the remainders; H = 8, or 16 for rank 16) so each k-step is two MMAs
+//     D += A_small [B_big B_small] + A_big [B_big B_small]
+// instead of three with N = 16 -- every MMA costs ~50 cycles up to N = 64 (profiles/r02_umma_rate.txt)
+// and reads the 4 KB A slice from shared memory; columns h and H + h of D are summed in the fold
+template <int R>
+struct MqPack {
+  static constexpr int H = GC_MQT_PACK ? (R <= 8 ? 8 : 16) : kN;
+  static constexpr int N = GC_MQT_PACK ? 2 * H : kN;
+  static constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((kM >> 4) << 24);
+};
 
 __device__ __forceinline__ void split3(float c, float &big, float &small) {
   big = __uint_as_float(__float_as_uint(c) & 0xFFFFE000u);
@@ -202,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
                      static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot)))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -245,16 +260,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp < 4) {
       mbar_wait(acc_bar(static_cast<int>(gi & 1)), static_cast<uint32_t>((gi >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t x[16];
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>((gi & 1) * kN);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
-            "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      constexpr int H = MqPack<R>::H, N = MqPack<R>::N;
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>((gi & 1) * N);
 #pragma unroll
-      for (int b = 0; b < R; ++b) acc64[b] += static_cast<double>(__uint_as_float(x[b]));
+      for (int part = 0; part < N / 16; ++part) {
+        uint32_t x[16];
+        gcu::tmem_ld16(taddr + 16 * part, x);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {   // column 16 part + j is rank (16 part + j) mod H
+          const int b = (16 * part + j) % H;
+          if (b < R) acc64[b] += static_cast<double>(__uint_as_float(x[j]));
+        }
+      }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     }
   };
@@ -271,15 +288,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t gi = k / kGroup;
         mbar_wait(full_bar(s), static_cast<uint32_t>((k / kStages) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t dcol = tmem + static_cast<uint32_t>((gi & 1) * kN);
+        const uint32_t dcol = tmem + static_cast<uint32_t>((gi & 1) * MqPack<R>::N);
 #pragma unroll
         for (int kk = 0; kk < kKc / 8; ++kk) {
           const uint64_t ab = sdesc(stage(s) + kOffC + 32 * kk), as = sdesc(stage(s) + kOffG + 32 * kk);
           const uint64_t bb = sdesc(stage(s) + kOffBb + 32 * kk), bs = sdesc(stage(s) + kOffBs + 32 * kk);
           const uint32_t accum = (k % kGroup != 0 || kk != 0) ? 1u : 0u;
-          umma_tf32(dcol, as, bb, accum);
-          umma_tf32(dcol, ab, bs, 1u);
-          umma_tf32(dcol, ab, bb, 1u);
+          if (GC_MQT_PACK) {
+            gcu::umma_tf32(dcol, as, bb, MqPack<R>::idesc, accum);
+            gcu::umma_tf32(dcol, ab, bb, MqPack<R>::idesc, 1u);
+          } else {
+            umma_tf32(dcol, as, bb, accum);
+            umma_tf32(dcol, ab, bs, 1u);
+            umma_tf32(dcol, ab, bb, 1u);
+          }
         }
         umma_commit(empty_bar(s));
         if (k % kGroup == kGroup - 1 || k == nloc - 1) umma_commit(acc_bar(static_cast<int>(gi & 1)));
@@ -364,7 +386,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         split3(t[3], hb.w, hs.w);
         const uint32_t off = sw128(n, ch);
         *reinterpret_cast<float4 *>(st + kOffBb + off) = hb;
-        *reinterpret_cast<float4 *>(st + kOffBs + off) = hs;
+        // packed: the remainders are rows H.. of the same (contiguous, up to 32-row) B tile
+        *reinterpret_cast<float4 *>(st + (GC_MQT_PACK ? kOffBb + sw128(MqPack<R>::H + n, ch) : kOffBs + off)) = hs;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full_bar(s)) : "memory");
@@ -384,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
 }
 
 // The row of the matrix that is only partly inside d (to_matrix's zero padding starts in it):

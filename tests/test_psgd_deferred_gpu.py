@@ -115,7 +115,8 @@ def test_residual_reads_and_writes_between_rounds():
 
 def test_tma_pass_matches_register_pass():
     """P = M Q from the TMA-fed kernel against the register-fed tcgen05 kernel: same 3xTF32 split
-    and fold cadence, so the factors agree to far inside the 1e-5 contract."""
+    (A_big is the raw fp32 box, truncated by the tensor core) and fold cadence, so the factors agree
+    to far inside the 1e-5 contract."""
     import ctypes
     import paper_2407_01378_b200 as gcb
     from paper_2407_01378_b200 import _native
@@ -140,10 +141,11 @@ def test_tma_pass_matches_register_pass():
     torch.cuda.synchronize()
     assert torch.equal(r1, r2)                       # corrected = f32(g + r) written over r
     assert torch.equal(r1, g + res)
-    # rows wholly inside d: the same 3xTF32 products in the same order -- identical only if the
-    # tensor core truncates the raw fp32 A_big operand to tf32 exactly as the register kernel's mask
+    # the same three 3xTF32 products (the TMA pass packs B_big / B_small along N: two MMAs per
+    # k-step, the halves summed in the fp64 fold): equal to a few fp32 ulps of the dot products
     rf = d // cols
-    assert torch.equal(p1[:, :rf], p2[:, :rf])
+    tol = 1e-6 * p2[:, :rf].abs().max().item()
+    assert (p1[:, :rf] - p2[:, :rf]).abs().max().item() <= tol
     m = torch.zeros(n, rows * cols, dtype=torch.float64, device="cuda")
     m[:, :d] = (g + res).double()
     ref = torch.einsum("wij,jb->wib", m.reshape(n, rows, cols), q.double())
