@@ -17,8 +17,12 @@ FN=ILi10ELb1E python tools/ncu_lines.py ${o}_thc_fused.ncu-rep ${EVIDENCE_LIB:-p
   paper_2407_01378_b200/csrc/gc_thc_fused.cu thc_fused > $p/${r}_thc_fused_lines.txt 2>&1
 python tools/ncu_summary.py ${o}_psgd_tma.ncu-rep > $p/${r}_psgd_tma_ncu_full.txt 2>&1
 python tools/ncu_summary.py ${o}_thc_rank.ncu-rep > $p/${r}_thc_rank_ncu_full.txt 2>&1
+python tools/ncu_summary.py ${o}_mtp_umma.ncu-rep > $p/${r}_mtp_umma_ncu_full.txt 2>&1
+python tools/ncu_summary.py ${o}_psgd_async.ncu-rep > $p/${r}_psgd_async_ncu_full.txt 2>&1
+cp ${o}_umma_rate.jsonl $p/${r}_umma_rate.jsonl
+cp ${o}_unaligned_stream.jsonl $p/${r}_unaligned_stream.jsonl
 grep -v NCCL ${o}_rank.jsonl > $p/${r}_rank_350m.jsonl
-for s in thc psgd psgd_gpt2 fp16; do
+for s in thc psgd psgd_gpt2 psgd_gpt2_dist fp16; do
   { echo "ncu launch list of one per-rank round at d = 350M (tools/time_rank.py --scheme $s): cold-cache, serialised";
     python tools/launch_summary.py ${o}_rank_${s}_launches.csv; } > $p/${r}_rank_${s}_launch_summary.txt
 done

@@ -14,13 +14,19 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-north-star > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:thc_fused_kernel -s 1 -c 1 \
   -o ${o}_thc_fused -f python tools/prof_thc.py 25557032 8 1 2 > /dev/null 2>&1
-for s in thc psgd psgd_gpt2 fp16; do
+for s in thc psgd psgd_gpt2 psgd_gpt2_dist fp16; do
   timeout 300 python tools/time_rank.py --scheme $s --steps 10 >> ${o}_rank.jsonl 2>> ${o}_rank.err
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file ${o}_rank_${s}_launches.csv python tools/time_rank.py --scheme $s --steps 1 > /dev/null 2>&1
 done
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"mq_tma_kernel|mtp_tma_kernel|decode_vec" \
   -s 5 -c 3 -o ${o}_psgd_tma -f python tools/time_rank.py --scheme psgd --steps 1 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"mtp_umma_kernel" -s 1 -c 1 \
+  -o ${o}_mtp_umma -f python tools/time_rank.py --scheme psgd --rank 8 --steps 1 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"mq_async_kernel|mtp_async_kernel|mtp_tma_kernel" \
+  -s 3 -c 3 -o ${o}_psgd_async -f python tools/time_rank.py --scheme psgd_gpt2 --steps 1 > /dev/null 2>&1
+timeout 120 ./build/ubench/umma_rate > ${o}_umma_rate.jsonl 2>&1
+timeout 120 ./build/ubench/unaligned_stream > ${o}_unaligned_stream.jsonl 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:"rank_quant|rank_ranges|rank_decode" -s 3 -c 3 \
   -o ${o}_thc_rank -f python tools/time_rank.py --scheme thc --steps 1 > /dev/null 2>&1
 timeout 1500 python tools/sweep.py --synthetic --warmup 3 --steps 8 > ${o}_sweep_synthetic.jsonl 2> ${o}_sweep.err
