@@ -3,7 +3,7 @@
 python tools/time_rank.py [--scheme thc|psgd|psgd_gpt2|fp16] [--d 350000000] [--n 1] [--q 4 --b 8]
                           [--segs 1024,4096,...] [--steps 10]
 One JSON line per configuration: ms/round (CUDA events), Gelem/s, algorithmic-bytes rate."""
-import argparse, json, os, sys
+import argparse, json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import torch.distributed as dist
@@ -59,8 +59,10 @@ for seg in [int(x) for x in a.segs.split(",")]:
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
     s.record()
+    t_host = time.perf_counter()
     for r in range(a.steps):
         pipe.run_round(g[r % 2], 3 + r)
+    host_ms = (time.perf_counter() - t_host) * 1e3 / a.steps   # host time to issue a round (no final sync)
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / a.steps
@@ -73,6 +75,6 @@ for seg in [int(x) for x in a.segs.split(",")]:
         alg = (4 * a.n + 4) * a.d
     print(json.dumps({"scheme": a.scheme, "d": a.d, "n": a.n, "q": a.q, "b": a.b, "seg_tiles": seg,
                       "ms": round(ms, 4), "gelem_s": round(a.d / ms / 1e6, 2), "alg_GBps": round(alg / ms / 1e6, 1),
-                      "hbm_frac": round(alg / ms / 1e6 / 6548.5, 4)}), flush=True)
+                      "hbm_frac": round(alg / ms / 1e6 / 6548.5, 4), "host_issue_ms": round(host_ms, 4)}), flush=True)
     del pipe
 dist.destroy_process_group()
