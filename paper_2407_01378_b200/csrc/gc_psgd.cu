@@ -642,68 +642,6 @@ constexpr int kDecRows = 64;
 #endif
 constexpr int kDecBatch = GC_PSGD_DEC_BATCH;   // rows whose loads are in flight together
 
-// The estimate alone (deferred EF) for row pitches without float4 rows: walk the estimate as a flat
-// array -- 16-byte aligned quads whatever the matrix's row pitch -- and find each element's (i, j)
-// from its flat index; est = P_hat[i,:] . Q_sum[j,:] / n in decode_vec_kernel's arithmetic (bit for
-// bit).  The fp64 division of a quad's first index by cols is exact for indices < 2^53.
-template <int R>
-__global__ void __launch_bounds__(256) decode_est_flat_kernel(int n, int64_t d, int64_t rows, int64_t cols,
-                                                              const float *ph, const float *qsum, float *est,
-                                                              const int64_t *est_offs, int est_acc) {
-  const int t = blockIdx.y;
-  ph += static_cast<int64_t>(t) * rows * R;
-  qsum += static_cast<int64_t>(t) * cols * R;
-  float *e_t = est + (est_offs ? est_offs[t] : 0);
-  const gc::DivN dn(n);
-  // elements before the first 16-byte boundary of this tensor's estimate slice
-  const int64_t head = min(d, static_cast<int64_t>(((16 - (reinterpret_cast<uintptr_t>(e_t) & 15)) & 15) / 4));
-  const double inv_cols = 1.0 / static_cast<double>(cols);
-  auto value = [&](int64_t i, int64_t j) {
-    float pa[R], qv[R];
-#pragma unroll
-    for (int b = 0; b < R; ++b) pa[b] = __ldg(ph + i * R + b), qv[b] = __ldg(qsum + j * R + b);
-    float v = __fmul_rn(pa[0], qv[0]);   // no contraction into the division below
-#pragma unroll
-    for (int b = 1; b < R; ++b) v = fmaf(pa[b], qv[b], v);
-    return dn(v);
-  };
-  auto row_of = [&](int64_t e) {
-    int64_t i = static_cast<int64_t>(static_cast<double>(e) * inv_cols);
-    if (i * cols > e) --i;
-    else if ((i + 1) * cols <= e) ++i;
-    return i;
-  };
-  const int64_t nquad = (d - head) / 4;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t qd = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; qd < nquad; qd += stride) {
-    const int64_t e0 = head + 4 * qd;
-    int64_t i = row_of(e0), j = e0 - i * cols;
-    float4 o;
-    float *ov = reinterpret_cast<float *>(&o);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      ov[k] = value(i, j);
-      if (++j == cols) j = 0, ++i;
-    }
-    float4 *dst = reinterpret_cast<float4 *>(e_t + e0);
-    if (est_acc) {
-      const float4 pv = *dst;
-      o.x += pv.x; o.y += pv.y; o.z += pv.z; o.w += pv.w;
-    }
-    __stcs(dst, o);
-  }
-  // the head and the tail past the last whole quad
-  const int64_t tail0 = head + 4 * nquad;
-  const int64_t extra = head + (d - tail0);
-  if (blockIdx.x == 0 && threadIdx.x < extra) {
-    const int64_t e = threadIdx.x < head ? threadIdx.x : tail0 + (threadIdx.x - head);
-    const int64_t i = row_of(e);
-    float v = value(i, e - i * cols);
-    if (est_acc) v += e_t[e];
-    e_t[e] = v;
-  }
-}
-
 template <int R, bool A16>
 __global__ void __launch_bounds__(256) decode_vec_kernel(int L, int n, int64_t d, int64_t rows, int64_t cols,
                                                          const float *ph, const float *qw, const float *qsum,
@@ -1336,17 +1274,6 @@ int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t r
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // float4 accesses need cols % 4 == 0 and 16-byte aligned rows; otherwise coalesced scalars
   const bool a16 = cols % 4 == 0 && b->rows_aligned;
-  if (!a16 && resid == nullptr && estimate != nullptr && getenv_str("GC_PSGD_DECODE") != "vec") {
-    // deferred EF: the estimate alone, as a flat float4 array (any row pitch)
-    const int64_t quads = (d + 3) / 4;
-    const int bx = grid_cap(std::min<int64_t>((quads + 255) / 256, 148 * 8 / std::max(1, b->tensors) + 1));
-    GC_RANK_SWITCH(rank, ({
-      decode_est_flat_kernel<R><<<dim3(bx, b->tensors), 256, 0, st>>>(n, d, rows, cols, p_hat, q_sum, estimate,
-                                                                     b->est_offsets, b->est_accumulate);
-    }));
-    GC_LAUNCH_CHECK("decode_est_flat_kernel");
-    return GC_OK;
-  }
   const dim3 grid(grid_cap((cols + 1023) / 1024), grid_cap((rows + kDecRows - 1) / kDecRows), b->tensors);
   GC_RANK_SWITCH(rank, ({
     if (a16)
