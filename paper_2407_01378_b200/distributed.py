@@ -771,37 +771,59 @@ def _make(cfg, pipe):
     raise TypeError(f"unknown config type {type(cfg).__name__}")
 
 
+def exchange_float_groups(phase: str | None, reqs, comm: Comm, n: int, L: int) -> list:
+    """exchange_float_batched for several groups at once: reqs = [(x [T_g * L, m_g], T_g, m_g)] ->
+    [[T_g, m_g]] sums, each tensor in its own reference ring order, with ONE all-to-all and ONE
+    all-gather for all of them (a round's factor phase costs two collectives, not two per group).
+    The send buffer per destination rank is the concatenation of every group's [T_g][L][S_g]
+    slice block (S_g = ceil(m_g / W))."""
+    W = comm.world
+    S = [-(-m // W) for _, _, m in reqs]
+    blocks = []
+    for (x, T, m), Sg in zip(reqs, S):
+        xv = x.reshape(T, L, m)
+        if W * Sg != m:
+            xp = torch.zeros(T, L, W * Sg, dtype=torch.float32, device=x.device)
+            xp[:, :, :m].copy_(xv)
+            xv = xp
+        blocks.append(xv.reshape(T, L, W, Sg).permute(2, 0, 1, 3).reshape(W, T * L * Sg))
+    send = torch.cat(blocks, dim=1).contiguous()                       # [W][sum_g T_g L S_g]
+    recv = comm.all_to_all(send, phase)                                # [W][...]: every rank's workers
+    outs, col = [], 0
+    for (x, T, m), Sg in zip(reqs, S):
+        width = T * L * Sg
+        blk = recv[:, col:col + width].reshape(W, T, L, Sg)
+        col += width
+        if L == 1:
+            rows, ld, stride = blk, recv.stride(0), Sg
+        else:
+            rows, ld, stride = blk.permute(1, 0, 2, 3).reshape(T, n, Sg).contiguous(), Sg, n * Sg
+        s0 = comm.rank * Sg
+        my_len = max(0, min(Sg, m - s0))
+        out = torch.empty(T, Sg, dtype=torch.float32, device=x.device)
+        if my_len < Sg:
+            out[:, my_len:].zero_()
+        if my_len:
+            _native.call("gc_float_fold_batched_slice", T, n, my_len, rows.data_ptr(), ld, stride, s0, -(-m // n), 0,
+                         0, 0, out.data_ptr(), Sg, _sp())
+        outs.append(out.reshape(T * Sg))
+    gathered = comm.all_gather_rows(torch.cat(outs).reshape(1, -1), phase)   # [W][sum_g T_g S_g]
+    res, col = [], 0
+    for (x, T, m), Sg in zip(reqs, S):
+        blk = gathered[:, col:col + T * Sg]
+        col += T * Sg
+        if W == 1:
+            res.append(blk.reshape(T, Sg))
+        else:
+            res.append(blk.reshape(W, T, Sg).permute(1, 0, 2).reshape(T, W * Sg)[:, :m].contiguous())
+    return res
+
+
 def exchange_float_batched(x: torch.Tensor, comm: Comm, n: int, T: int, m: int, phase: str | None) -> torch.Tensor:
     """T independent fp32 FloatSum rings of length m at once (one per tensor of a shape group):
     x [T * L, m] (row t * L + l = tensor t, local worker l) -> [T, m] sums in the reference ring
-    order of each tensor (collectives.py:177-236), one all-to-all + one all-gather for the group.
-    Few launches: the send layout [W][T][L][S] is one permuted copy of x padded to W * S columns;
-    with one worker per rank the fold reads the received rows in place."""
-    W, L = comm.world, x.shape[0] // T
-    S = -(-m // W)
-    xv = x.reshape(T, L, m)
-    if W * S != m:
-        xp = torch.zeros(T, L, W * S, dtype=torch.float32, device=x.device)
-        xp[:, :, :m].copy_(xv)
-        xv = xp
-    send = xv.reshape(T, L, W, S).permute(2, 0, 1, 3).contiguous()   # [W][T][L][S]
-    recv = comm.all_to_all(send, phase)                              # [W][T][L][S]: rank r's workers
-    if L == 1:   # worker r's row of tensor t at (r * T + t) * S
-        rows, ld, stride = recv, T * S, S
-    else:
-        rows, ld, stride = recv.permute(1, 0, 2, 3).reshape(T, n, S).contiguous(), S, n * S
-    s0 = comm.rank * S
-    my_len = max(0, min(S, m - s0))
-    out = torch.empty(T, S, dtype=torch.float32, device=x.device)
-    if my_len < S:
-        out[:, my_len:].zero_()
-    if my_len:
-        _native.call("gc_float_fold_batched_slice", T, n, my_len, rows.data_ptr(), ld, stride, s0, -(-m // n), 0, 0,
-                     0, out.data_ptr(), S, _sp())
-    gathered = comm.all_gather_rows(out.reshape(1, T * S), phase)    # [W][T * S]
-    if W == 1:
-        return gathered.reshape(T, S)
-    return gathered.reshape(W, T, S).permute(1, 0, 2).reshape(T, W * S)[:, :m].contiguous()
+    order of each tensor (collectives.py:177-236), one all-to-all + one all-gather."""
+    return exchange_float_groups(phase, [(x, T, m)], comm, n, x.shape[0] // T)[0]
 
 
 class DistributedTensorListPipeline:
@@ -811,10 +833,10 @@ class DistributedTensorListPipeline:
     The tensors below bypass_below go through the dense-fp32 ring (pipelines.py:326-336): their
     corrected values are gathered from all ranks and folded per tensor in ring order
     (gc_segment_fold_ef), residual 0.  The compressed tensors are batched by shape as in
-    TensorListPipeline (TMA P = M Q with the deferred EF update where the row pitch allows); each
-    group's factor all-reduces are one exchange_float_batched (all-to-all + per-tensor ring-order
-    fold + all-gather) per phase, so a round issues 4 collectives per shape group instead of 4 per
-    tensor."""
+    TensorListPipeline (tcgen05 P = M Q with the deferred EF update); the groups run in lock step
+    (PowerSgdGroup.run_steps) and each factor phase of ALL groups is one exchange_float_groups
+    (all-to-all + per-tensor ring-order fold + all-gather): a round issues 4 collectives for the
+    factors plus one all-gather for the bypass tensors, whatever the number of tensors and shapes."""
 
     def __init__(self, config: PowerSgdConfig, num_workers: int, sizes, seeds: SeedSpec,
                  error_feedback: bool | None = None, *, group=None, device=None, validate: bool = True):
@@ -880,10 +902,6 @@ class DistributedTensorListPipeline:
         for grp in self.groups:
             grp.materialize(self._res.data_ptr())
 
-    def _fold(self, kind, x, m):
-        T = x.shape[0] // self.L
-        return exchange_float_batched(x, self.comm, self.group.size, T, m, kind)
-
     def run_round(self, local_grads, round_index: int) -> RoundResult:
         from .schemes import seed_q_groups, umma_unaligned
         L, D, n = self.L, self.dim, self.group.size
@@ -916,29 +934,45 @@ class DistributedTensorListPipeline:
             for t in self.bypass:
                 ledger.charge_ring("dense-bypass", n, self.sizes[t], 32)
                 bits += 32.0 * self.sizes[t]
+        # every group's round as a generator (PowerSgdGroup.run_steps): the groups advance in lock
+        # step and each factor phase of all groups is ONE exchange (one all-to-all + one all-gather)
+        steps = []
         for grp, q in zip(self.groups, qs):
             aligned = grp.vec and g.data_ptr() % 16 == 0 and est.data_ptr() % 16 == 0
             if res is not None:
                 grp.set_ld(D, aligned and res.data_ptr() % 16 == 0)
                 if grp.batch.rows_aligned or umma_unaligned():   # ef_apply inside the tcgen05 P = M Q
-                    grp.run(res.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, grads_ptr=g.data_ptr(),
-                            vec=bool(grp.batch.rows_aligned), fold=self._fold, q=q, ef_resid_ptr=res.data_ptr())
+                    steps.append(grp.run_steps(res.data_ptr(), res.data_ptr(), est.data_ptr(), round_index,
+                                               grads_ptr=g.data_ptr(), vec=bool(grp.batch.rows_aligned), q=q,
+                                               ef_resid_ptr=res.data_ptr()))
                 else:
                     grp.materialize(res.data_ptr())
                     for t in grp.tensor_ids:
                         off = int(self.offsets[t])
                         _native.call("gc_ef_apply", L, self.sizes[t], g.data_ptr() + 4 * off, res.data_ptr() + 4 * off,
                                      D, res.data_ptr() + 4 * off, D, sp)
-                    grp.run(res.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, vec=False, fold=self._fold,
-                            q=q)
+                    steps.append(grp.run_steps(res.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, vec=False,
+                                               q=q))
             else:
                 grp.set_ld(D, aligned)
-                grp.run(g.data_ptr(), None, est.data_ptr(), round_index, vec=bool(grp.batch.rows_aligned),
-                        fold=self._fold, q=q)
+                steps.append(grp.run_steps(g.data_ptr(), None, est.data_ptr(), round_index,
+                                           vec=bool(grp.batch.rows_aligned), q=q))
             for t in grp.tensor_ids:
                 ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
                 ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)
                 bits += 32.0 * grp.rank * (grp.rows + grp.cols)
+        reqs = [st.send(None) for st in steps]
+        while steps:
+            kind = reqs[0][0]
+            sums = exchange_float_groups(kind, [(x, x.shape[0] // L, m) for _, x, m in reqs], self.comm, n, L)
+            nxt_steps, nxt_reqs = [], []
+            for st, sm in zip(steps, sums):
+                try:
+                    nxt_reqs.append(st.send(sm))
+                    nxt_steps.append(st)
+                except StopIteration:
+                    pass
+            steps, reqs = nxt_steps, nxt_reqs
         self.launches += 4 + len(self.groups) * 11
         result = RoundResult(self.scheme, round_index, est, D, ledger, bits, _simple_stats(None))
         result.wire_bytes = dict(self.comm.sent)

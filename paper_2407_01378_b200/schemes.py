@@ -630,13 +630,26 @@ class PowerSgdGroup:
 
     def run(self, c_ptr: int, resid_ptr, est_ptr: int, round_index: int, grads_ptr=None, vec=False, fold=None,
             before_ef=None, q=None, ef_resid_ptr=None):
-        """One round for the batch.  c_ptr: corrected matrices (or raw gradients when grads_ptr is
-        given together with vec: ef_apply fused into P = M Q, corrected written over resid).
-        fold(kind, x [T*L][m], m) -> [T][m] sums in the reference ring order (simulated: local fold;
-        distributed: gather + fold).  before_ef() runs after the estimate, before the residuals
-        change (the nmse hook).  ef_resid_ptr (with grads_ptr and vec): ef_apply fused into
-        P = M Q, corrected written there (c_ptr must then point at it).  Returns warm Q
-        [T][cols][r]."""
+        """One round for the batch (run_steps driven with `fold` at its two factor all-reduces)."""
+        steps = self.run_steps(c_ptr, resid_ptr, est_ptr, round_index, grads_ptr=grads_ptr, vec=vec,
+                               before_ef=before_ef, q=q, ef_resid_ptr=ef_resid_ptr)
+        req = next(steps)
+        try:
+            while True:
+                req = steps.send(fold(*req))
+        except StopIteration as stop:
+            return stop.value
+
+    def run_steps(self, c_ptr: int, resid_ptr, est_ptr: int, round_index: int, grads_ptr=None, vec=False,
+                  before_ef=None, q=None, ef_resid_ptr=None):
+        """One round for the batch as a generator: it yields each factor all-reduce as
+        (kind, x [T*L][m], m) and resumes with its [T][m] sums in the reference ring order
+        (simulated: local fold; distributed: exchange), so a caller can exchange the factors of
+        several groups in one collective.  c_ptr: corrected matrices (or raw gradients when
+        grads_ptr is given together with vec: ef_apply fused into P = M Q, corrected written over
+        resid).  before_ef() runs after the estimate, before the residuals change (the nmse hook).
+        ef_resid_ptr (with grads_ptr and vec): ef_apply fused into P = M Q, corrected written there
+        (c_ptr must then point at it).  Returns warm Q [T][cols][r]."""
         sp = _sp()
         T, L, n, d, rows, cols, r = self.T, self.L, self.n, self.d, self.rows, self.cols, self.rank
         bref = ctypes.byref(self.batch)
@@ -691,7 +704,7 @@ class PowerSgdGroup:
                 _native.call("gc_psgd_mq", bref, d, rows, cols, rc, c_ptr, q_c.data_ptr(), p_c.data_ptr(), sp)
             if multi:
                 p[..., c0:c0 + rc].copy_(p_c)
-        p_sum = fold("left-factor", p, rows * r).reshape(T, rows, r)
+        p_sum = (yield ("left-factor", p, rows * r)).reshape(T, rows, r)
         p_hat = self._buf("p_hat", (T, rows, r))
         status = self._buf("status", (T,), torch.int32).zero_()
         _native.call("gc_psgd_orthonormalize", T, rows, r, p_sum.data_ptr(), p_hat.data_ptr(), self.mgs_ws.data_ptr(),
@@ -714,7 +727,7 @@ class PowerSgdGroup:
                 qw[..., c0:c0 + rc].copy_(qw_c)
             ph_chunks.append(ph_c)
             qw_chunks.append(qw_c)
-        q_sum = fold("right-factor", qw, cols * r).reshape(T, cols, r)
+        q_sum = (yield ("right-factor", qw, cols * r)).reshape(T, cols, r)
         # warm Q (pipelines.py:366) before the decode, and its Gram copied to pinned host memory
         # behind an event: the next round's rank check (ensure_full_rank) then reads it without
         # draining the device, so that round's kernels queue while this round's decode runs
