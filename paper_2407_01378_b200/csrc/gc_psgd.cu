@@ -988,7 +988,7 @@ int gc_psgd_splits(int32_t rows_total, int64_t cols) {
 int64_t gc_psgd_workspace_bytes(int32_t rows_total, int64_t rows, int64_t cols, int32_t rank) {
   const int64_t splits = gc_psgd_splits(rows_total, cols);
   const int64_t mtp = 8 * (static_cast<int64_t>(rows_total) * splits * cols * rank);
-  const int64_t mq = 8 * (static_cast<int64_t>(rows_total) * ((cols + 1023) / 1024) * rows * rank);
+  const int64_t mq = 8 * (static_cast<int64_t>(rows_total) * gc_psgd_mq_max_splits(cols) * rows * rank);
   return (mtp > mq ? mtp : mq) + 256;
 }
 
@@ -1080,13 +1080,21 @@ int gc_psgd_mq_deferred_batched(const gc_psgd_batch *b, const int64_t *host_tens
   // TMA boxes when a tensor map describes the rows, else the cp.async-fed pass (gc_psgd_async.cu)
   const bool tma = gc_psgd_mq_tma_supported_batched(b, host_tensor_offsets, d, rows, cols, rank, grads, resid) &&
                    getenv_str("GC_PSGD_MQ_FEED") != "async";
+  // cols = 2 (mod 4) with aligned tensor starts: tensor maps over row pairs (GPT-2's shapes)
+  const bool pair = !tma && getenv_str("GC_PSGD_MQ_FEED") != "async" &&
+                    (b->tensors == 1 && b->row_offsets == nullptr ? true : host_tensor_offsets != nullptr) &&
+                    gc_psgd_mq_pair_supported_impl(b->tensors, b->workers, host_tensor_offsets, b->ld, d, rows, cols,
+                                                   rank, grads, resid);
   const int slabs =
-      tma ? gc_psgd_mq_tma_launch(b->tensors, b->workers, host_tensor_offsets, b->row_offsets, b->ld, d, rows, cols,
+      pair ? gc_psgd_mq_pair_launch(b->tensors, b->workers, host_tensor_offsets, b->row_offsets, b->ld, d, rows, cols,
+                                    rank, grads, resid, q, ef_p_hat, ef_q_workers, static_cast<double *>(workspace),
+                                    gc_psgd_mq_max_splits(cols), st)
+      : tma ? gc_psgd_mq_tma_launch(b->tensors, b->workers, host_tensor_offsets, b->row_offsets, b->ld, d, rows, cols,
                                   rank, grads, resid, q, ef_p_hat, ef_q_workers, static_cast<double *>(workspace),
-                                  (cols + 1023) / 1024, st)
+                                  gc_psgd_mq_max_splits(cols), st)
           : gc_psgd_mq_async_launch(b->tensors, b->workers, b->row_offsets, host_tensor_offsets, b->ld, d, rows, cols,
                                     rank, grads, resid, q, ef_p_hat, ef_q_workers, static_cast<double *>(workspace),
-                                    (cols + 1023) / 1024, st);
+                                    gc_psgd_mq_max_splits(cols), st);
   if (slabs < 0) return slabs;
   const int64_t total = static_cast<int64_t>(L) * rows * rank;
   mq_reduce_kernel<<<grid_cap((total + 255) / 256 > 148 * 8 ? 148 * 8 : (total + 255) / 256), 256, 0, st>>>(

@@ -161,6 +161,8 @@ struct TmaArgs {
   int splits;
   int64_t chunks_per_split;
   int has_resid;
+  float *r_out;            // mq_pair_kernel: the residual buffer (odd rows' corrected values)
+  int64_t ld;              // ... and its row pitch when row_start is null
 };
 
 // own = P_hat_prev[i,:] . Q_w_prev[j,:] exactly as decode_vec_kernel forms it (fp32 product then
@@ -863,6 +865,297 @@ __global__ void __launch_bounds__(kQtThreads, 1) mtp_umma_kernel(const __grid_co
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
 }
 
+// ------------------------------------------------------------------ P = M Q for cols = 2 (mod 4)
+// GPT-2-medium's chunked PowerSGD matrices (1774 x 1774, 7174 x 7174) have a row pitch of
+// 8 (mod 16) bytes, which no tensor map describes.  Row PAIRS do: a pair of rows is 2 cols floats
+// = a multiple of 16 bytes.  Two maps per operand over the pair rows -- even rows at the tensor
+// start, odd rows at start + (cols - 2) floats (16-byte aligned when the tensor start is) -- so an
+// odd-row box at column c0 holds that row's columns c0 - 2 .. c0 + 29.  A CTA's 128-row band is
+// tile rows 0..63 = its 64 even rows and 64..127 = its 64 odd rows; the odd half simply computes
+// with a B shifted by two columns (Q rows c0 - 2 ..), as a second M = 64 MMA chain into its own
+// TMEM accumulator.  Everything else is mq_tma_kernel's: TMA boxes (SWIZZLE_128B) formed in place,
+// deferred EF, packed 3xTF32, fp64 folds; the even half's corrected box goes back by TMA store, the
+// odd half's (and the last chunk's even half) by 16-byte stores (an odd box's first two columns of
+// the first chunk are the even row's tail: neither used nor stored).  Ranks 4, 8, 16 (16-byte Q-row
+// windows).
+constexpr int kPrM = 64;                     // rows per half (UMMA M)
+constexpr int kPrRaw = 36 * 16 * 4;          // Q (or Q_w_prev) rows c0 - 4 .. c0 + 31, rank <= 16
+constexpr int kPrOffG = 0, kPrOffC = kTile, kPrOffBe = 2 * kTile, kPrOffBo = 2 * kTile + 4096,
+              kPrOffQ = 2 * kTile + 8192, kPrOffW = kPrOffQ + kPrRaw;
+constexpr int kPrStage = (kPrOffW + kPrRaw + 1023) / 1024 * 1024;
+constexpr int kPrStages = 4;
+constexpr int kPrSmem = kPrStages * kPrStage + kPhBytes + 512 + 1024;
+struct PairMapSet {   // per tensor: g even / odd, residual even / odd
+  CUtensorMap ge[kMaxMapT / 2], go[kMaxMapT / 2], re[kMaxMapT / 2], ro[kMaxMapT / 2];
+};
+template <int R>
+struct PairShape {
+  static constexpr int H = R <= 8 ? 8 : 16;
+  static constexpr int N = 2 * H;
+  static constexpr uint32_t idesc = gcu::idesc_tf32(kPrM, N);
+};
+
+template <int R, bool DEF>
+__global__ void __launch_bounds__(kThreads, 1)
+    mq_pair_kernel(const __grid_constant__ PairMapSet maps, const __grid_constant__ TmaArgs a) {
+  static_assert(R % 4 == 0, "16-byte Q-row windows");
+  constexpr int H = PairShape<R>::H, N = PairShape<R>::N;
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char *sm = smem_raw + (base - raw);
+  auto stage = [&](int s) { return base + static_cast<uint32_t>(s * kPrStage); };
+  float *ph_s = reinterpret_cast<float *>(sm + kPrStages * kPrStage);
+  const uint32_t bars = base + kPrStages * kPrStage + kPhBytes;   // loaded[S], empty[S], full[S], acc[2]
+  auto loaded_bar = [&](int s) { return bars + 8 * s; };
+  auto empty_bar = [&](int s) { return bars + 8 * (kPrStages + s); };
+  auto full_bar = [&](int s) { return bars + 8 * (2 * kPrStages + s); };
+  auto acc_bar = [&](int x) { return bars + 8 * (3 * kPrStages + x); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + kPrStages * kPrStage + kPhBytes + 8 * (3 * kPrStages + 2));
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int vl = blockIdx.z, v = a.v_base + vl;
+  const int tl = vl / a.L, w = vl - tl * a.L, t = v / a.L;
+  const float *qt = a.q + static_cast<int64_t>(t) * a.cols * R;
+  const float *pht = DEF ? a.ef_ph + static_cast<int64_t>(t) * a.rows * R : nullptr;
+  const float *qw_prev = DEF ? a.ef_qw + static_cast<int64_t>(v) * a.cols * R : nullptr;
+  const int split = blockIdx.y;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kM;   // even
+  const int k0 = static_cast<int>(row0 / 2);                     // pair row
+  const int64_t nchunks_all = (a.cols + kKc - 1) / kKc;
+  const int64_t c_begin = split * a.chunks_per_split;
+  const int64_t c_end = min(nchunks_all, c_begin + a.chunks_per_split);
+  const int64_t nloc = c_end - c_begin;
+  // matrix row of tile row tr: even half 2 tr, odd half 2 (tr - 64) + 1
+  auto mrow = [&](int tr) { return row0 + (tr < kPrM ? 2 * tr : 2 * (tr - kPrM) + 1); };
+
+  if (tid == 0) {
+    for (int s = 0; s < kPrStages; ++s) {
+      mbar_init(loaded_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+      mbar_init(full_bar(s), kProducers);
+    }
+    mbar_init(acc_bar(0), 1);
+    mbar_init(acc_bar(1), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {   // two groups x (even, odd) accumulators of N <= 32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot)))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int e = tid; e < kPrStages * 8192 / 16; e += kThreads) {   // both B tiles: padding rows stay zero
+    const int s = e / (8192 / 16), o = e - s * (8192 / 16);
+    *reinterpret_cast<uint4 *>(sm + s * kPrStage + kPrOffBe + o * 16) = make_uint4(0, 0, 0, 0);
+  }
+  if (DEF) {   // P_hat_prev rows in tile order
+    for (int e = tid; e < kM * R; e += kThreads) {
+      const int64_t i = mrow(e / R);
+      ph_s[e] = i < a.rows ? pht[i * R + e % R] : 0.0f;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  const uint32_t tx_box = static_cast<uint32_t>(kTile) * (a.has_resid ? 2u : 1u);
+  auto issue_load = [&](int64_t k) {
+    const int s = static_cast<int>(k % kPrStages);
+    const int64_t col0 = (c_begin + k) * kKc;
+    // Q rows col0 - 4 .. col0 + 31 (the window starts at col0 for the first chunk, 4 rows in)
+    const int64_t q0 = col0 >= 4 ? col0 - 4 : 0;
+    const int64_t qn = min(col0 + kKc, a.cols) - q0;
+    const uint32_t qbytes = static_cast<uint32_t>(qn * R * 4), qdst = col0 >= 4 ? 0u : 4u * R * 4;
+    mbar_expect_tx(loaded_bar(s), tx_box + qbytes * (DEF ? 2u : 1u));
+    const int c0i = static_cast<int>(col0);
+    tma_load_3d(stage(s) + kPrOffG, &maps.ge[tl], c0i, k0, w, loaded_bar(s));
+    tma_load_3d(stage(s) + kPrOffG + kTile / 2, &maps.go[tl], c0i, k0, w, loaded_bar(s));
+    if (a.has_resid) {
+      tma_load_3d(stage(s) + kPrOffC, &maps.re[tl], c0i, k0, w, loaded_bar(s));
+      tma_load_3d(stage(s) + kPrOffC + kTile / 2, &maps.ro[tl], c0i, k0, w, loaded_bar(s));
+    }
+    bulk_load(stage(s) + kPrOffQ + qdst, qt + q0 * R, qbytes, loaded_bar(s));
+    if (DEF) bulk_load(stage(s) + kPrOffW + qdst, qw_prev + q0 * R, qbytes, loaded_bar(s));
+  };
+
+  double acc_e[R], acc_o[R];
+#pragma unroll
+  for (int b = 0; b < R; ++b) acc_e[b] = acc_o[b] = 0.0;
+  auto fold_group = [&](int64_t gi) {   // M = 64: row r of a half at lane 32 (r / 16) + r % 16
+    if (warp < 4) {
+      mbar_wait(acc_bar(static_cast<int>(gi & 1)), static_cast<uint32_t>((gi >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>((gi & 1) * 2 * N);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+#pragma unroll
+        for (int part = 0; part < N / 16; ++part) {
+          uint32_t x[16];
+          gcu::tmem_ld16(taddr + half * N + 16 * part, x);
+          if (lane < 16) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int b = (16 * part + j) % H;
+              if (b < R) (half ? acc_o : acc_e)[b] += static_cast<double>(__uint_as_float(x[j]));
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+  };
+
+  if (warp == kProducers / 32) {   // ---- control warp: TMA ring, MMA issue, TMA stores (even half)
+    if (lane == 0) {
+      for (int64_t k = 0; k < min(static_cast<int64_t>(kPrStages), nloc); ++k) issue_load(k);
+      for (int64_t k = 0; k < nloc; ++k) {
+        const int s = static_cast<int>(k % kPrStages);
+        const int64_t col0 = (c_begin + k) * kKc;
+        const int64_t gi = k / kGroup;
+        mbar_wait(full_bar(s), static_cast<uint32_t>((k / kPrStages) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t de = tmem + static_cast<uint32_t>((gi & 1) * 2 * N), dodd = de + N;
+#pragma unroll
+        for (int kk = 0; kk < kKc / 8; ++kk) {
+          const uint32_t accum = (k % kGroup != 0 || kk != 0) ? 1u : 0u;
+          const uint64_t abe = gcu::sdesc(stage(s) + kPrOffC + 32 * kk), ase = gcu::sdesc(stage(s) + kPrOffG + 32 * kk);
+          const uint64_t abo = gcu::sdesc(stage(s) + kPrOffC + kTile / 2 + 32 * kk),
+                         aso = gcu::sdesc(stage(s) + kPrOffG + kTile / 2 + 32 * kk);
+          const uint64_t be = gcu::sdesc(stage(s) + kPrOffBe + 32 * kk), bo = gcu::sdesc(stage(s) + kPrOffBo + 32 * kk);
+          gcu::umma_tf32(de, ase, be, PairShape<R>::idesc, accum);
+          gcu::umma_tf32(de, abe, be, PairShape<R>::idesc, 1u);
+          gcu::umma_tf32(dodd, aso, bo, PairShape<R>::idesc, accum);
+          gcu::umma_tf32(dodd, abo, bo, PairShape<R>::idesc, 1u);
+        }
+        umma_commit(empty_bar(s));
+        if (k % kGroup == kGroup - 1 || k == nloc - 1) umma_commit(acc_bar(static_cast<int>(gi & 1)));
+        // the even half's corrected box back over the residual buffer -- except in the last chunk:
+        // TMA clips the inner dimension at 16-byte granularity and cols * 4 = 8 (mod 16) bytes, so
+        // a clipped store would also write the odd row's first two elements (the producers store it)
+        if (a.has_resid && col0 + kKc <= a.cols) {
+          tma_store_3d(&maps.re[tl], stage(s) + kPrOffC, static_cast<int>(col0), k0, w);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (k >= 1 && k - 1 + kPrStages < nloc) {   // refill the stage of chunk k - 1
+          const int64_t old = k - 1;
+          mbar_wait(empty_bar(static_cast<int>(old % kPrStages)), static_cast<uint32_t>((old / kPrStages) & 1));
+          if (a.has_resid) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          issue_load(old + kPrStages);
+        }
+      }
+      if (a.has_resid) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+  } else {   // ---- producers: thread = 16-byte column chunk ch of row rg (even half) and 64 + rg (odd)
+    const int ch = tid & 7, rg = tid >> 3;
+    const int64_t rs = a.row_start ? a.row_start[v] : static_cast<int64_t>(v) * a.ld;
+    for (int64_t k = 0; k < nloc; ++k) {
+      const int s = static_cast<int>(k % kPrStages);
+      const int64_t col0 = (c_begin + k) * kKc;
+      unsigned char *st = sm + s * kPrStage;
+      const float *qraw = reinterpret_cast<const float *>(st + kPrOffQ);   // window row = col - col0 + 4
+      const float *wraw = reinterpret_cast<const float *>(st + kPrOffW);
+      mbar_wait(loaded_bar(s), static_cast<uint32_t>((k / kPrStages) & 1));
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int tr = rg + kPrM * half;
+        const int64_t m = mrow(tr);
+        const int64_t cb = col0 + 4 * ch - 2 * half;   // the thread's first column
+        const uint32_t off = sw128(tr, ch);
+        float4 gv = *reinterpret_cast<const float4 *>(st + kPrOffG + off);
+        float4 rv = a.has_resid ? *reinterpret_cast<const float4 *>(st + kPrOffC + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float g4[4] = {gv.x, gv.y, gv.z, gv.w}, r4[4] = {rv.x, rv.y, rv.z, rv.w}, c4[4];
+        const bool live = m < a.rows_full;   // the partial row is the fix-up kernel's
+        float pa[R];
+        if (DEF) {   // the row's P_hat_prev and the 4 columns' Q_w_prev rows as 16-byte loads
+#pragma unroll
+          for (int j = 0; j < R / 4; ++j) {
+            const float4 x = *reinterpret_cast<const float4 *>(ph_s + tr * R + 4 * j);
+            pa[4 * j] = x.x, pa[4 * j + 1] = x.y, pa[4 * j + 2] = x.z, pa[4 * j + 3] = x.w;
+          }
+        }
+        const float *wcol = wraw + (cb - col0 + 4) * R;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int64_t col = cb + e;
+          const bool ok = live && col >= 0 && col < a.cols;
+          float r = r4[e];
+          if (DEF && ok) {
+            float wq[R];
+#pragma unroll
+            for (int j = 0; j < R / 4; ++j) {
+              const float4 x = *reinterpret_cast<const float4 *>(wcol + e * R + 4 * j);
+              wq[4 * j] = x.x, wq[4 * j + 1] = x.y, wq[4 * j + 2] = x.z, wq[4 * j + 3] = x.w;
+            }
+            r = r - own_of<R>(pa, wq);
+          }
+          c4[e] = ok ? (a.has_resid ? g4[e] + r : g4[e]) : 0.0f;
+        }
+        const float4 c = make_float4(c4[0], c4[1], c4[2], c4[3]);
+        float4 hb, hs;
+        split3(c.x, hb.x, hs.x);
+        split3(c.y, hb.y, hs.y);
+        split3(c.z, hb.z, hs.z);
+        split3(c.w, hb.w, hs.w);
+        *reinterpret_cast<float4 *>(st + kPrOffC + off) = c;
+        *reinterpret_cast<float4 *>(st + kPrOffG + off) = hs;
+        if (a.has_resid && live && (half == 1 || col0 + kKc > a.cols)) {   // 16-byte stores of the corrected values
+          float *dst = a.r_out + rs + m * a.cols + cb;
+          if (cb >= 0 && cb + 3 < a.cols) {
+            *reinterpret_cast<float4 *>(dst) = c;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (cb + e >= 0 && cb + e < a.cols) dst[e] = c4[e];
+          }
+        }
+      }
+      // B tiles: threads 0 .. 8R - 1 the even half's (Q rows col0 ..), 256 .. 256 + 8R - 1 the odd
+      // half's (Q rows col0 - 2 ..); row n (< R) and H + n, 4 k per thread
+      if ((tid & 255) < R * 8) {
+        const int half = tid >> 8, n = (tid & 255) >> 3, c8 = tid & 7;
+        float tv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int64_t col = col0 + 4 * c8 + e - 2 * half;
+          tv[e] = col >= 0 && col < a.cols ? qraw[(col - col0 + 4) * R + n] : 0.0f;
+        }
+        float4 hb, hs;
+        split3(tv[0], hb.x, hs.x);
+        split3(tv[1], hb.y, hs.y);
+        split3(tv[2], hb.z, hs.z);
+        split3(tv[3], hb.w, hs.w);
+        unsigned char *bt = st + (half ? kPrOffBo : kPrOffBe);
+        *reinterpret_cast<float4 *>(bt + sw128(n, c8)) = hb;
+        *reinterpret_cast<float4 *>(bt + sw128(H + n, c8)) = hs;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full_bar(s)) : "memory");
+      const int64_t gi = k / kGroup;
+      if (k % kGroup == 0 && gi >= 1) fold_group(gi - 1);
+    }
+    if (nloc > 0) fold_group((nloc - 1) / kGroup);
+  }
+
+  if (warp < 4 && lane < 16) {
+    const int r16 = warp * 16 + lane;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int64_t grow = row0 + 2 * r16 + half;
+      if (grow < a.rows) {
+#pragma unroll
+        for (int b = 0; b < R; ++b)
+          a.partial[((static_cast<int64_t>(v) * a.splits + split) * a.rows + grow) * R + b] =
+              half ? acc_o[b] : acc_e[b];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -891,7 +1184,40 @@ bool make_map(CUtensorMap *m, const float *base, int64_t L, int64_t rows_full, i
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// row-pair maps for cols = 2 (mod 4): pair rows of 2 cols floats; odd = the odd rows, shifted so an
+// odd box at column c0 holds columns c0 - 2 .. c0 + 29 (boxes 32 columns x 64 pair rows)
+bool make_map_pair(CUtensorMap *m, const float *base, bool odd, int64_t L, int64_t rows_full, int64_t cols,
+                   int64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int64_t pairs = odd ? rows_full / 2 : (rows_full + 1) / 2;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(odd ? cols + 2 : cols), static_cast<cuuint64_t>(pairs),
+                        static_cast<cuuint64_t>(L)};
+  const int64_t ld_map = L == 1 ? (ld + 3) / 4 * 4 : ld;
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(2 * cols * 4), static_cast<cuuint64_t>(ld_map * 4)};
+  cuuint32_t box[3] = {kKc, kPrM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(odd ? base + cols - 2 : base), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int grid_cap(int64_t g) { return static_cast<int>(g < 1 ? 1 : (g > 65535 ? 65535 : g)); }
+
+// column splits for a grid of ctas x splits one-CTA-per-SM blocks: the fewest splits whose last
+// wave is nearly full (a 336-CTA grid runs 2.27 waves; x 2 splits, 4.54 -> 0.91 of 5 full waves)
+int64_t wave_splits(int64_t ctas, int64_t max_splits, int64_t nchunks, int sms) {
+  int64_t best = 1;
+  double best_eff = 0.0;
+  for (int64_t s = 1; s <= max_splits && nchunks / s >= 4; ++s) {
+    const int64_t items = ctas * s, waves = (items + sms - 1) / sms;
+    const double eff = static_cast<double>(items) / static_cast<double>(waves * sms);
+    if (eff > best_eff + 0.02) best = s, best_eff = eff;
+  }
+  return best;
+}
+
+
 
 }  // namespace
 
@@ -1059,9 +1385,7 @@ int gc_psgd_mq_tma_launch(int32_t T, int32_t L, const int64_t *host_tensor_offse
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t splits = sms / (row_blocks * L * T);
-  if (splits > max_splits) splits = max_splits;
-  if (splits < 1) splits = 1;
+  int64_t splits = wave_splits(row_blocks * L * T, max_splits, nchunks, sms);
   const int64_t per = (nchunks + splits - 1) / splits;
   splits = (nchunks + per - 1) / per;
   TmaArgs a{};
@@ -1119,6 +1443,100 @@ int gc_psgd_mq_tma_launch(int32_t T, int32_t L, const int64_t *host_tensor_offse
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     gc_set_error(std::string("mq_tma_kernel: ") + cudaGetErrorString(e));
+    return GC_ERR_CUDA;
+  }
+  return static_cast<int>(splits);
+}
+
+int gc_psgd_mq_pair_supported_impl(int32_t tensors, int32_t workers, const int64_t *host_tensor_offsets, int64_t ld,
+                                   int64_t d, int64_t rows, int64_t cols, int32_t rank, const void *grads,
+                                   const void *resid) {
+  if (cols % 4 != 2 || rank % 4 != 0 || rank > 16 || d / cols < 2 || cols > (int64_t{1} << 30)) return 0;
+  if (tensors > 1 && host_tensor_offsets == nullptr) return 0;
+  if (workers > 1 && ld % 4 != 0) return 0;
+  if ((reinterpret_cast<uintptr_t>(grads) | reinterpret_cast<uintptr_t>(resid)) & 15) return 0;
+  if (host_tensor_offsets)
+    for (int t = 0; t < tensors; ++t)
+      if (host_tensor_offsets[t] % 4 != 0) return 0;
+  (void)rows;
+  return 1;
+}
+
+// P = M Q over row-pair tensor maps (cols = 2 mod 4); the same split-K partials as gc_psgd_mq_tma_launch
+int gc_psgd_mq_pair_launch(int32_t T, int32_t L, const int64_t *host_tensor_offsets, const int64_t *row_start,
+                           int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
+                           float *resid, const float *q, const float *ef_ph, const float *ef_qw, double *partial,
+                           int64_t max_splits, cudaStream_t st) {
+  const int64_t rows_full = d / cols;
+  const int64_t row_blocks = (rows + kM - 1) / kM;
+  const int64_t nchunks = (cols + kKc - 1) / kKc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t splits = wave_splits(row_blocks * L * T, max_splits, nchunks, sms);
+  const int64_t per = (nchunks + splits - 1) / splits;
+  splits = (nchunks + per - 1) / per;
+  TmaArgs a{};
+  a.d = d;
+  a.rows = rows;
+  a.cols = cols;
+  a.rows_full = rows_full;
+  a.L = L;
+  a.row_start = row_start;
+  a.q = q;
+  a.ef_ph = ef_ph;
+  a.ef_qw = ef_qw;
+  a.partial = partial;
+  a.splits = static_cast<int>(splits);
+  a.chunks_per_split = per;
+  a.has_resid = resid != nullptr;
+  a.r_out = resid;
+  a.ld = ld;
+  const bool def = resid != nullptr && ef_ph != nullptr && ef_qw != nullptr;
+  const bool tail = rows_full < rows && d > rows_full * cols;
+  constexpr int kPerLaunch = kMaxMapT / 2;
+  PairMapSet maps;
+  for (int t0 = 0; t0 < T; t0 += kPerLaunch) {
+    const int tc = T - t0 < kPerLaunch ? T - t0 : kPerLaunch;
+    std::memset(&maps, 0, sizeof(maps));
+    for (int k = 0; k < tc; ++k) {
+      const int64_t off = host_tensor_offsets ? host_tensor_offsets[t0 + k] : 0;
+      bool ok = make_map_pair(&maps.ge[k], grads + off, false, L, rows_full, cols, ld) &&
+                make_map_pair(&maps.go[k], grads + off, true, L, rows_full, cols, ld);
+      if (resid)
+        ok = ok && make_map_pair(&maps.re[k], resid + off, false, L, rows_full, cols, ld) &&
+             make_map_pair(&maps.ro[k], resid + off, true, L, rows_full, cols, ld);
+      if (!ok) {
+        gc_set_error("cuTensorMapEncodeTiled failed for the row-pair P = M Q operands");
+        return GC_ERR_CUDA;
+      }
+    }
+    a.v_base = t0 * L;
+    const dim3 grid(grid_cap(row_blocks), static_cast<unsigned>(splits), static_cast<unsigned>(tc * L));
+#define GC_PAIR_LAUNCH(RR, DD)                                                                            \
+  cudaFuncSetAttribute(mq_pair_kernel<RR, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrSmem);     \
+  mq_pair_kernel<RR, DD><<<grid, kThreads, kPrSmem, st>>>(maps, a);                                       \
+  if (tail) mq_tail_row_kernel<RR, DD><<<tc * L, kTailThreads, 0, st>>>(grads, resid, ld, a);
+#define GC_PAIR_CASE(RR)        \
+  case RR:                      \
+    if (def) {                  \
+      GC_PAIR_LAUNCH(RR, true)  \
+    } else {                    \
+      GC_PAIR_LAUNCH(RR, false) \
+    }                           \
+    break;
+    switch (rank) {
+      GC_PAIR_CASE(4) GC_PAIR_CASE(8) GC_PAIR_CASE(16)
+      default:
+        gc_set_error("the row-pair P = M Q pass takes ranks 4, 8, 16");
+        return GC_ERR_UNSUPPORTED;
+    }
+#undef GC_PAIR_CASE
+#undef GC_PAIR_LAUNCH
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    gc_set_error(std::string("mq_pair_kernel: ") + cudaGetErrorString(e));
     return GC_ERR_CUDA;
   }
   return static_cast<int>(splits);

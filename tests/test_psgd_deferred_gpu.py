@@ -249,20 +249,24 @@ def test_unaligned_groups_defer_bitwise():
 
 
 @pytest.mark.parametrize("r", [1, 4, 8, 16])
-@pytest.mark.parametrize("layout", ["unaligned", "even", "aligned_forced"])
+@pytest.mark.parametrize("layout", ["unaligned", "even", "pair", "aligned_forced"])
 def test_async_mq_pass(r, layout, monkeypatch):
-    """gc_psgd_mq_deferred_batched on the cp.async feed: corrected = f32(g + r) written over the
-    residuals bit for bit, P = M Q within 1e-5 of fp64 (3xTF32 with B halves packed along N), with
-    a batch of T = 3 tensors at odd offsets (unaligned) or forced on a TMA-capable layout."""
+    """gc_psgd_mq_deferred_batched on layouts no single tensor map describes -- the cp.async feed
+    (odd offsets; cols % 4 == 2 at offsets = 2 mod 4), the row-pair tensor maps (cols % 4 == 2,
+    aligned offsets) -- and the cp.async feed forced on a TMA-capable layout: corrected =
+    f32(g + r) written over the residuals bit for bit, nothing else touched, P = M Q within 1e-5
+    of fp64, for a batch of T = 3 tensors x 2 workers."""
     import ctypes
     from paper_2407_01378_b200 import _native
     from paper_2407_01378_b200.configs import matrix_shape_for
     # unaligned: odd tensor offsets (4-byte copies); even: cols % 4 == 2 with even offsets (8-byte
     # copies, GPT-2's case); aligned_forced: a TMA-capable layout on the cp.async feed
-    d = {"unaligned": 150 * 150 - 7, "even": 150 * 150 - 8, "aligned_forced": 200 * 200 - 8}[layout]
+    # pair: cols % 4 == 2 with 16-byte aligned tensor starts -> the row-pair tensor maps (ranks 4, 8, 16)
+    d = {"unaligned": 150 * 150 - 7, "even": 150 * 150 - 8, "pair": 150 * 150 - 8,
+         "aligned_forced": 200 * 200 - 8}[layout]
     rows, cols = matrix_shape_for(d)
     T, L = 3, 2
-    pad = {"unaligned": 1, "even": 2, "aligned_forced": 0}[layout]
+    pad = {"unaligned": 1, "even": 2, "pair": 4, "aligned_forced": 0}[layout]
     ld = T * (d + pad) + 3 * pad
     offs_t = [t * (d + pad) + pad for t in range(T)]
     row_offs = torch.tensor([w * ld + offs_t[t] for t in range(T) for w in range(L)], dtype=torch.int64,

@@ -8,14 +8,16 @@ group), psgd_umma (register-fed tcgen05 P = M Q), psgd_tma (TMA-fed tcgen05 P = 
 deferred EF update, TMA Q = M^T P_hat, Cholesky orthonormalization; 3 rounds), psgd_batched (one
 tensor map per tensor of a shape group), psgd_mtp_ef (cluster / DSMEM Q + EF pass), psgd_mtp_umma
 (tcgen05 Q = M^T P_hat at ranks 4 / 8 / 16: several TMEM fold groups, a partial chunk and row),
-psgd_async (cp.async-fed deferred P = M Q: unaligned batched groups over 3 rounds), topk, topkc."""
+psgd_async (cp.async-fed deferred P = M Q: unaligned batched groups over 3 rounds), psgd_pair
+(row-pair tensor maps for cols = 2 mod 4: GPT-2-like shapes, deferred EF, 3 rounds), topk, topkc."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2407_01378_b200 as gcb
 
 cases = sys.argv[1:] or ["thc_fused", "thc_rank", "psgd_umma", "psgd_tma", "psgd_batched", "psgd_mtp_ef",
-                         "psgd_mtp_umma", "psgd_async", "topk", "topkc"]
+                         "psgd_mtp_umma", "psgd_async", "psgd_pair",
+                         "topk", "topkc"]
 torch.cuda.set_device(0)
 S = gcb.SeedSpec(7)
 
@@ -79,6 +81,12 @@ for c in cases:
     elif c == "psgd_async":
         from paper_2407_01378_b200.multitensor import TensorListPipeline
         sizes = [150 * 150, 77 * 77, 150 * 150 - 7, 600 * 602 + 3]   # > 16 chunks: TMEM fold groups
+        pipe = TensorListPipeline(gcb.PowerSgdConfig(4), 2, sizes, S, compute_nmse=False)
+        rounds(pipe, torch.randn(2, sum(sizes), device="cuda"), 3)
+        pipe.residuals
+    elif c == "psgd_pair":
+        from paper_2407_01378_b200.multitensor import TensorListPipeline
+        sizes = [150 * 150, 150 * 150 - 8, 4, 602 * 602 - 10]   # cols 150 / 602: = 2 (mod 4), aligned starts
         pipe = TensorListPipeline(gcb.PowerSgdConfig(4), 2, sizes, S, compute_nmse=False)
         rounds(pipe, torch.randn(2, sum(sizes), device="cuda"), 3)
         pipe.residuals
