@@ -51,6 +51,9 @@ int gc_psgd_mq_pair_launch(int32_t T, int32_t L, const int64_t *host_tensor_offs
                            int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *grads,
                            float *resid, const float *q, const float *ef_ph, const float *ef_qw, double *partial,
                            int64_t max_splits, cudaStream_t st);
+int gc_psgd_mtp_pair_launch(int32_t T, int32_t L, const int64_t *host_tensor_offsets, const int64_t *row_start,
+                            int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
+                            const float *p_hat, double *partial, int64_t max_splits, cudaStream_t st);
 // column splits the P = M Q passes may use (split-K partials in the workspace): >= 8 chunks each
 inline int64_t gc_psgd_mq_max_splits(int64_t cols) { return cols >= 256 ? (cols + 255) / 256 : 1; }
 #define GC_LAUNCH_CHECK(what)                                                     \

@@ -1139,7 +1139,9 @@ int gc_psgd_mtp_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offse
   const std::string impl = impl_env ? impl_env : "";
   const bool single = b->tensors == 1 && b->row_offsets == nullptr;
   // a batch with row offsets takes tensor maps only with its host tensor offsets
-  const bool maps_ok = (single || (host_tensor_offsets != nullptr && b->row_offsets != nullptr)) &&
+  // (P_hat of tensor t starts t rows R floats in: 16-byte aligned for the bulk copies iff rows R % 4 == 0)
+  const bool maps_ok = (single || (host_tensor_offsets != nullptr && b->row_offsets != nullptr &&
+                                   (rows * rank) % 4 == 0)) &&
                        gc_psgd_mq_tma_supported_impl(b->tensors, b->workers, single ? nullptr : host_tensor_offsets,
                                                      b->ld, d, rows, cols, rank, c, c);
   const bool tma_ok = single && maps_ok;
@@ -1149,6 +1151,15 @@ int gc_psgd_mtp_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offse
   } else if (maps_ok && rank <= 4 && impl != "cores" && impl != "async") {
     splits = gc_psgd_mtp_tma_launch(b->tensors, b->workers, single ? nullptr : host_tensor_offsets, b->row_offsets,
                                     b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);
+    if (splits < 0) return splits;
+  } else if (rank <= 4 && impl != "cores" && impl != "vec" && impl != "async" &&
+             (single || (host_tensor_offsets && (rows * rank) % 4 == 0)) && cols % 4 == 2 && d / cols >= 2 &&
+             (b->workers == 1 || b->ld % 4 == 0) &&
+             gc_psgd_mq_pair_supported_impl(b->tensors, b->workers, single ? nullptr : host_tensor_offsets, b->ld, d,
+                                            rows, cols, 4, c, c)) {
+    // cols = 2 (mod 4): the row-pair tensor maps (gc_psgd_tma.cu)
+    splits = gc_psgd_mtp_pair_launch(b->tensors, b->workers, single ? nullptr : host_tensor_offsets, b->row_offsets,
+                                     b->ld, d, rows, cols, rank, c, p_hat, partial, splits, st);
     if (splits < 0) return splits;
   } else if (rank <= 4 && impl != "cores" && impl != "vec") {
     // batches of tensors and unaligned row pitches: the cp.async-fed slabs (gc_psgd_async.cu)

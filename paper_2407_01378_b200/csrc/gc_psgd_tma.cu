@@ -1156,6 +1156,139 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
 }
 
+// ------------------------------------------------------------------ Q_w = M_w^T P_hat for cols = 2 (mod 4)
+// mtp_tma_kernel's column slabs over the row-pair maps: per 128-row box an even box (32 columns x
+// 64 pair rows) and an odd box 36 columns wide (the odd rows' columns c0 - 2 .. c0 + 33, no
+// swizzle: 144-byte rows) so the odd rows' columns c0 .. c0 + 31 are read at +2 floats (two
+// 8-byte loads); the thread's 4 columns are the same for both halves.  Ranks 1..4.
+constexpr int kMpEven = kPrM * kKc * 4;           // 8 KB
+constexpr int kMpOdd = kPrM * 36 * 4;             // 9 KB
+constexpr int kMpStage = (kMpEven + kMpOdd + kMtpPh + 1023) / 1024 * 1024;
+constexpr int kMpSmem = kMtpStages * kMpStage + 64 + 1024;
+
+template <int R>
+__global__ void __launch_bounds__(kMtpThreads, 1) mtp_pair_kernel(const __grid_constant__ PairMapSet maps,
+                                                                 const __grid_constant__ MtpArgs a) {
+  static_assert(R <= 4, "rank <= 4");
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char *sm = smem_raw + (base - raw);
+  const uint32_t bars = base + kMtpStages * kMpStage;   // loaded[S], empty[S]
+  __shared__ double red[kMtpConsumers / 8][32][R];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int vl = blockIdx.z, v = a.v_base + vl, split = blockIdx.y;
+  const int tl = vl / a.L, w = vl % a.L;
+  const float *ph = a.ph + static_cast<int64_t>(v / a.L) * a.rows * R;
+  const int64_t col0 = static_cast<int64_t>(blockIdx.x) * kKc;
+  const int64_t r_begin = split * a.rows_per_split;
+  const int64_t r_end = min(a.rows_full, r_begin + a.rows_per_split);
+  const int64_t nbox = r_end > r_begin ? (r_end - r_begin + kM - 1) / kM : 0;
+  if (tid == 0) {
+    for (int s = 0; s < kMtpStages; ++s) {
+      mbar_init(bars + 8 * s, 1);
+      mbar_init(bars + 8 * (kMtpStages + s), kMtpConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kMtpConsumers / 32) {   // producer warp: the TMA ring (even box, odd box, P_hat rows)
+    if (lane == 0) {
+      for (int64_t b = 0; b < nbox; ++b) {
+        const int s = static_cast<int>(b % kMtpStages);
+        const int64_t i0 = r_begin + b * kM;
+        if (b >= kMtpStages)
+          mbar_wait(bars + 8 * (kMtpStages + s), static_cast<uint32_t>(((b / kMtpStages) - 1) & 1));
+        const bool full = i0 + kM <= r_end;
+        mbar_expect_tx(bars + 8 * s, kMpEven + kMpOdd + (full ? kM * R * 4 : 0));
+        const int k0 = static_cast<int>(i0 / 2);
+        tma_load_3d(base + s * kMpStage, &maps.ge[tl], static_cast<int>(col0), k0, w, bars + 8 * s);
+        tma_load_3d(base + s * kMpStage + kMpEven, &maps.go[tl], static_cast<int>(col0), k0, w, bars + 8 * s);
+        if (full) bulk_load(base + s * kMpStage + kMpEven + kMpOdd, ph + i0 * R, kM * R * 4, bars + 8 * s);
+      }
+    }
+    return;
+  }
+  const int g4 = tid & 7, rg = tid >> 3;   // float4 column group, pair-row group (pair rows rg + 32 k)
+  double acc64[4][R];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc64[t][b] = 0.0;
+  for (int64_t bx = 0; bx < nbox; ++bx) {
+    const int s = static_cast<int>(bx % kMtpStages);
+    const int64_t i0 = r_begin + bx * kM;
+    const bool full = i0 + kM <= r_end;
+    mbar_wait(bars + 8 * s, static_cast<uint32_t>((bx / kMtpStages) & 1));
+    const unsigned char *st = sm + s * kMpStage;
+    const float *phs = reinterpret_cast<const float *>(st + kMpEven + kMpOdd);
+    float acc[4][R];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[t][b] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kPrM / 32; ++k) {
+      const int pr = rg + 32 * k;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int row = 2 * pr + half;   // row within the box
+        float mv[4];
+        if (half == 0) {
+          const float4 m = *reinterpret_cast<const float4 *>(st + sw128(pr, g4));
+          mv[0] = m.x, mv[1] = m.y, mv[2] = m.z, mv[3] = m.w;
+        } else {   // odd rows: columns c0 .. at +2 floats in the 36-wide box
+          const float *orow = reinterpret_cast<const float *>(st + kMpEven + pr * 144) + 2 + 4 * g4;
+          const float2 x = *reinterpret_cast<const float2 *>(orow), y = *reinterpret_cast<const float2 *>(orow + 2);
+          mv[0] = x.x, mv[1] = x.y, mv[2] = y.x, mv[3] = y.y;
+        }
+        float p[R];
+        if (full) {
+#pragma unroll
+          for (int b = 0; b < R; ++b) p[b] = phs[row * R + b];
+        } else {
+#pragma unroll
+          for (int b = 0; b < R; ++b) p[b] = i0 + row < r_end ? __ldg(ph + (i0 + row) * R + b) : 0.0f;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int b = 0; b < R; ++b) acc[t][b] = fmaf(mv[t], p[b], acc[t][b]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc64[t][b] += static_cast<double>(acc[t][b]);
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bars + 8 * (kMtpStages + s)) : "memory");
+  }
+  if (rg == 0 && split == a.splits - 1 && a.rows_full < a.rows) {   // the partly filled row, fp64
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int64_t col = col0 + 4 * g4 + t;
+      const int64_t off = a.rows_full * a.cols + col;
+      if (col < a.cols && off < a.d) {
+        const int64_t rs = a.row_start ? a.row_start[v] : static_cast<int64_t>(v) * a.ld;
+        const double m = static_cast<double>(a.c[rs + off]);
+#pragma unroll
+        for (int b = 0; b < R; ++b) acc64[t][b] += m * static_cast<double>(ph[a.rows_full * R + b]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int b = 0; b < R; ++b) red[rg][4 * g4 + t][b] = acc64[t][b];
+  asm volatile("bar.sync 1, %0;" ::"r"(kMtpConsumers) : "memory");
+  for (int e = tid; e < 32 * R; e += kMtpConsumers) {
+    const int cc = e / R, b = e - cc * R;
+    double x = 0.0;
+#pragma unroll 8
+    for (int q = 0; q < kMtpConsumers / 8; ++q) x += red[q][cc][b];
+    if (col0 + cc < a.cols) a.partial[((static_cast<int64_t>(v) * a.splits + split) * a.cols + col0 + cc) * R + b] = x;
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -1187,7 +1320,7 @@ bool make_map(CUtensorMap *m, const float *base, int64_t L, int64_t rows_full, i
 // row-pair maps for cols = 2 (mod 4): pair rows of 2 cols floats; odd = the odd rows, shifted so an
 // odd box at column c0 holds columns c0 - 2 .. c0 + 29 (boxes 32 columns x 64 pair rows)
 bool make_map_pair(CUtensorMap *m, const float *base, bool odd, int64_t L, int64_t rows_full, int64_t cols,
-                   int64_t ld) {
+                   int64_t ld, uint32_t box_cols = kKc, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return false;
   const int64_t pairs = odd ? rows_full / 2 : (rows_full + 1) / 2;
@@ -1195,10 +1328,10 @@ bool make_map_pair(CUtensorMap *m, const float *base, bool odd, int64_t L, int64
                         static_cast<cuuint64_t>(L)};
   const int64_t ld_map = L == 1 ? (ld + 3) / 4 * 4 : ld;
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(2 * cols * 4), static_cast<cuuint64_t>(ld_map * 4)};
-  cuuint32_t box[3] = {kKc, kPrM, 1};
+  cuuint32_t box[3] = {box_cols, kPrM, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(odd ? base + cols - 2 : base), dims, strides,
-            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1538,6 +1671,72 @@ int gc_psgd_mq_pair_launch(int32_t T, int32_t L, const int64_t *host_tensor_offs
   if (e != cudaSuccess) {
     gc_set_error(std::string("mq_pair_kernel: ") + cudaGetErrorString(e));
     return GC_ERR_CUDA;
+  }
+  return static_cast<int>(splits);
+}
+
+// Q_w = M_w^T P_hat over row-pair maps (cols = 2 mod 4, ranks 1..4): split-K partials as gc_psgd_mtp's
+int gc_psgd_mtp_pair_launch(int32_t T, int32_t L, const int64_t *host_tensor_offsets, const int64_t *row_start,
+                            int64_t ld, int64_t d, int64_t rows, int64_t cols, int32_t rank, const float *c,
+                            const float *p_hat, double *partial, int64_t max_splits, cudaStream_t st) {
+  const int64_t rows_full = d / cols;
+  const int64_t slabs = (cols + kKc - 1) / kKc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t boxes = (rows_full + kM - 1) / kM;
+  const int64_t V = static_cast<int64_t>(T) * L;
+  int64_t splits = (2 * sms + slabs * V - 1) / (slabs * V);
+  if (splits > max_splits) splits = max_splits;
+  if (splits > boxes) splits = boxes;
+  if (splits < 1) splits = 1;
+  const int64_t per = (boxes + splits - 1) / splits;
+  splits = (boxes + per - 1) / per;
+  MtpArgs a{};
+  a.d = d;
+  a.rows = rows;
+  a.cols = cols;
+  a.rows_full = rows_full;
+  a.ld = ld;
+  a.c = c;
+  a.ph = p_hat;
+  a.partial = partial;
+  a.splits = static_cast<int>(splits);
+  a.rows_per_split = per * kM;
+  a.L = L;
+  a.row_start = row_start;
+  constexpr int kPerLaunch = kMaxMapT / 2;
+  PairMapSet maps;
+  for (int t0 = 0; t0 < T; t0 += kPerLaunch) {
+    const int tc = T - t0 < kPerLaunch ? T - t0 : kPerLaunch;
+    std::memset(&maps, 0, sizeof(maps));
+    for (int k = 0; k < tc; ++k) {
+      const int64_t off = host_tensor_offsets ? host_tensor_offsets[t0 + k] : 0;
+      if (!make_map_pair(&maps.ge[k], c + off, false, L, rows_full, cols, ld) ||
+          !make_map_pair(&maps.go[k], c + off, true, L, rows_full, cols, ld, 36, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+        gc_set_error("cuTensorMapEncodeTiled failed for the row-pair Q = M^T P_hat operand");
+        return GC_ERR_CUDA;
+      }
+    }
+    a.v_base = t0 * L;
+    const dim3 grid(static_cast<unsigned>(slabs), static_cast<unsigned>(splits), static_cast<unsigned>(tc * L));
+#define GC_MTPP(RR)                                                                                   \
+  case RR:                                                                                            \
+    cudaFuncSetAttribute(mtp_pair_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpSmem);  \
+    mtp_pair_kernel<RR><<<grid, kMtpThreads, kMpSmem, st>>>(maps, a);                                \
+    break;
+    switch (rank) {
+      GC_MTPP(1) GC_MTPP(2) GC_MTPP(3) GC_MTPP(4)
+      default:
+        gc_set_error("the row-pair Q = M^T P_hat pass takes ranks 1..4");
+        return GC_ERR_UNSUPPORTED;
+    }
+#undef GC_MTPP
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      gc_set_error(std::string("mtp_pair_kernel: ") + cudaGetErrorString(e));
+      return GC_ERR_CUDA;
+    }
   }
   return static_cast<int>(splits);
 }

@@ -306,17 +306,19 @@ def test_async_mq_pass(r, layout, monkeypatch):
 
 
 @pytest.mark.parametrize("r", [1, 3, 4])
-@pytest.mark.parametrize("layout", ["unaligned", "even", "aligned"])
+@pytest.mark.parametrize("layout", ["unaligned", "even", "pair", "aligned"])
 def test_async_mtp_pass(r, layout, monkeypatch):
     """Q_w = M_w^T P_hat on a batch of T = 3 tensors with row offsets: gc_psgd_mtp (no host
     offsets: the cp.async-fed slabs, 16-, 8- or 4-byte copies by row alignment), the CUDA-core
     float4 / scalar pass (GC_PSGD_MTP=vec) and gc_psgd_mtp_batched (one tensor map per tensor when
-    the rows are 16-byte aligned) against fp64, all far inside the 1e-5 contract."""
+    the rows are 16-byte aligned; row-pair maps when cols = 2 mod 4 and every tensor's P_hat rows are
+    16-byte aligned -- "pair" at rank 4, the cp.async slabs at ranks 1 and 3) against fp64, all far
+    inside the 1e-5 contract."""
     import ctypes
     from paper_2407_01378_b200 import _native
     from paper_2407_01378_b200.configs import matrix_shape_for
-    d = {"unaligned": 150 * 150 - 7, "even": 150 * 150 - 8, "aligned": 200 * 200 - 8}[layout]
-    pad = {"unaligned": 1, "even": 2, "aligned": 0}[layout]
+    d = {"unaligned": 150 * 150 - 7, "even": 150 * 150 - 8, "pair": 150 * 150 - 8, "aligned": 200 * 200 - 8}[layout]
+    pad = {"unaligned": 1, "even": 2, "pair": 4, "aligned": 0}[layout]
     rows, cols = matrix_shape_for(d)
     T, L = 3, 2
     ld = T * (d + pad) + 3 * pad
