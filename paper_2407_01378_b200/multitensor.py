@@ -101,6 +101,8 @@ class TensorListPipeline:
 
     def _fold(self, kind, x, m):
         n = self.group.size
+        if n == 1:   # one worker: the ring sum is the row itself
+            return x.reshape(x.shape[0], m)
         key = (kind, x.data_ptr(), x.shape[0] // n, m)   # one reused output per group input buffer
         out = self._fold_out.get(key)
         if out is None:

@@ -795,6 +795,8 @@ class PowerSgdEngine(Engine):
 
     def _fold(self, kind, x, m):
         n = self.n
+        if n == 1:   # one worker: the ring sum is the row itself
+            return x.reshape(x.shape[0], m)
         out = torch.empty(x.shape[0] // n, m, dtype=torch.float32, device=self.device)
         _native.call("gc_float_fold_batched", x.shape[0] // n, n, m, x.data_ptr(), m, n * m, 0, 0, 0, out.data_ptr(),
                      m, _sp())
