@@ -359,7 +359,7 @@ int gc_psgd_mtp_batched(const gc_psgd_batch *b, const int64_t *host_tensor_offse
 int gc_psgd_mtp_ef_supported(int64_t rows, int64_t cols, int32_t rank, int32_t rows_aligned);
 int gc_psgd_mtp_ef(const gc_psgd_batch *b, int64_t d, int64_t rows, int64_t cols, int32_t rank, float *resid,
                    const float *p_hat, float *q, void *stream);
-/* orthonormalize (compressors.py:555-588) for T tensors, rank <= 64.  Ranks 1..8 and 16 first try
+/* orthonormalize (compressors.py:555-588) for T tensors, rank <= 1024.  Ranks 1..8 and 16 first try
  * the Cholesky-QR fast path (fp64 Gram of P over the whole GPU, R = chol(G) whose pivots are MGS's
  * residual norms, P_hat = P R^-1) and keep it only when every pivot is far from the degeneracy
  * floor and from cancellation; every other tensor runs fp64 Gram-Schmidt (CGS2, the c dot products
@@ -378,7 +378,7 @@ int gc_psgd_decode(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, i
 int gc_psgd_decode_fused(const gc_psgd_batch *b, int32_t n, int64_t d, int64_t rows, int64_t cols, int32_t rank,
                          const float *p_hat, const float *q_workers, const float *q_sum, float *resid, float *estimate,
                          void *stream);
-/* gram[t] = Q_t^T Q_t in fp64 (rank check of ensure_full_rank, compressors.py:595-603), rank <= 64;
+/* gram[t] = Q_t^T Q_t in fp64 (rank check of ensure_full_rank, compressors.py:595-603), rank <= 1024;
  * workspace: gc_psgd_gram_workspace_bytes(tensors, rank) (column-slice partials, summed in order). */
 int64_t gc_psgd_gram_workspace_bytes(int32_t tensors, int32_t rank);
 int gc_psgd_gram(int32_t tensors, int64_t cols, int32_t rank, const float *q, double *gram, void *workspace,

@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(1024) mgs_kernel(int64_t rows, int R, const fl
 }
 
 
-// Orthonormalization for any rank <= kMaxOrthRank (compressors.py:555-588), one CTA per tensor.
+// Orthonormalization for any rank <= kMaxOrthRank (compressors.py:555-588), one CTA per tensor
+// (the dot-product buffers are dynamic shared memory, (kOrthThreads / 32 + 1) x R doubles).
 // Column c is projected against all previous columns with classical Gram-Schmidt applied twice
 // (CGS2: as stable as the reference's MGS; both give the Q factor of the same nested column
 // spaces, agreeing to O(cond * eps) in fp64 -- far inside the 1e-5 contract).  The c dot products
@@ -204,10 +205,10 @@ __global__ void __launch_bounds__(1024) mgs_kernel(int64_t rows, int R, const fl
 // sequential block reductions -- the difference that matters at r = 64.  A column
 // whose residual norm is at or below 1e-8 * scale takes the reference's canonical-basis
 // completion (the sequential path of mgs_kernel); none left -> status = 1 (DegenerateMatrixError).
-constexpr int kMaxOrthRank = 64;
+constexpr int kMaxOrthRank = 1024;   // 9 x 1024 doubles = 72 KB of dynamic shared memory
 constexpr int kOrthThreads = 256;
 
-__device__ void orth_dots(int64_t rows, int R, const double *a, int c, double *dots, double (*wred)[kMaxOrthRank]) {
+__device__ void orth_dots(int64_t rows, int R, const double *a, int c, double *dots, double *wred) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int p0 = 0; p0 < c; p0 += 8) {
     double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -221,13 +222,13 @@ __device__ void orth_dots(int64_t rows, int R, const double *a, int c, double *d
     for (int k = 0; k < 8; ++k) {
       double v = part[k];
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && p0 + k < c) wred[warp][p0 + k] = v;
+      if (lane == 0 && p0 + k < c) wred[warp * R + p0 + k] = v;
     }
   }
   __syncthreads();
   for (int p = threadIdx.x; p < c; p += kOrthThreads) {
     double v = 0.0;
-    for (int w = 0; w < kOrthThreads / 32; ++w) v += wred[w][p];
+    for (int w = 0; w < kOrthThreads / 32; ++w) v += wred[w * R + p];
     dots[p] = v;
   }
   __syncthreads();
@@ -236,8 +237,9 @@ __device__ void orth_dots(int64_t rows, int R, const double *a, int c, double *d
 __global__ void __launch_bounds__(kOrthThreads) orth_kernel(int64_t rows, int R, const float *in, double *a,
                                                             float *out, int *status, const int *fast) {
   __shared__ double red[33];
-  __shared__ double dots[kMaxOrthRank];
-  __shared__ double wred[kOrthThreads / 32][kMaxOrthRank];
+  extern __shared__ double orth_smem[];
+  double *dots = orth_smem;        // [R]
+  double *wred = orth_smem + R;    // [kOrthThreads / 32][R]
   if (fast && fast[blockIdx.x]) return;   // the Cholesky path already wrote this tensor's P_hat
   {
     const int64_t t = blockIdx.x;
@@ -1269,7 +1271,13 @@ int gc_psgd_orthonormalize(int32_t tensors, int64_t rows, int32_t rank, const fl
     GC_LAUNCH_CHECK("orth_apply_kernel");
     fast = flags;
   }
-  orth_kernel<<<tensors, kOrthThreads, 0, st>>>(rows, rank, p, a, p_hat, status, fast);
+  const size_t orth_smem = static_cast<size_t>(kOrthThreads / 32 + 1) * rank * sizeof(double);
+  if (orth_smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(orth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(orth_smem));
+    GC_REQUIRE(e == cudaSuccess, "orth_kernel: cannot opt in to the shared memory this rank needs");
+  }
+  orth_kernel<<<tensors, kOrthThreads, orth_smem, st>>>(rows, rank, p, a, p_hat, status, fast);
   GC_LAUNCH_CHECK("orth_kernel");
   return GC_OK;
 }

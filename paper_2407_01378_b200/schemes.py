@@ -491,7 +491,7 @@ class PowerSgdGroup:
     cfg4(b) passes per-(tensor, worker) row offsets into the flat per-worker gradients."""
 
     RANKS = (1, 2, 3, 4, 5, 6, 7, 8, 16)   # ranks the factor kernels are compiled for
-    MAX_RANK = 64                           # orthonormalization / Gram limit
+    MAX_RANK = 1024                         # orthonormalization / Gram limit (kMaxOrthRank)
 
     @staticmethod
     def rank_chunks(r: int) -> list[int]:

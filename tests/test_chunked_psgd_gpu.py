@@ -69,7 +69,7 @@ def test_psgd_golden_within_tolerance(name):
 @pytest.mark.parametrize("nmse", [True, False])
 @pytest.mark.parametrize("n,d,rank", [(4, 1_000_000, 4), (2, 350_001, 1), (3, 100_000, 8), (8, 4096, 2),
                                       (2, 50_000, 16), (2, 60_001, 9), (3, 100_000, 20), (2, 100_003, 32),
-                                      (2, 200_000, 64)])
+                                      (2, 200_000, 64), (2, 200_000, 100), (2, 300_000, 256)])
 def test_psgd_vs_oracle_multi_round(n, d, rank, nmse):
     """Every rank the reference accepts (compressors.py:100-112): ranks outside the compiled set run
     their factor passes in rank chunks (16s, 8, rest); nmse=True decodes estimate and EF update
@@ -80,8 +80,8 @@ def test_psgd_vs_oracle_multi_round(n, d, rank, nmse):
              for r in range(3)]
     outs = oracle_rounds("powersgd", dict(rank=rank), grads, 31)
     pipe = gcb.make_pipeline(gcb.PowerSgdConfig(rank), n, d, seeds, compute_nmse=nmse)
-    if rank in (20, 64):
-        assert pipe._engine.group.chunks == ([16, 4] if rank == 20 else [16, 16, 16, 16])
+    if rank in (20, 64, 100):
+        assert pipe._engine.group.chunks == {20: [16, 4], 64: [16] * 4, 100: [16] * 6 + [4]}[rank]
     for r in range(3):
         res = pipe.run_round(grads[r], r)
         assert_close_fp32(res.estimate.logical, outs[r]["estimate"], f"round {r}")
