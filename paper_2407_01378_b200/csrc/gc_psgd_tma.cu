@@ -1339,18 +1339,72 @@ int grid_cap(int64_t g) { return static_cast<int>(g < 1 ? 1 : (g > 65535 ? 65535
 
 // column splits for a grid of ctas x splits one-CTA-per-SM blocks: the fewest splits whose last
 // wave is nearly full (a 336-CTA grid runs 2.27 waves; x 2 splits, 4.54 -> 0.91 of 5 full waves)
+// Column splits of P = M Q: a CTA is one (row block, split, tensor-worker) item and pays a fixed
+// cost (TMEM alloc, ring fill, accumulator drain and fp64 fold) worth about kSplitOverhead chunks of
+// streaming, so minimise waves x (chunks per item + overhead) rather than maximising wave fill alone
+// (GPT-2-medium's 7174-column matrix: 18 splits of 13 chunks -> 5 splits of 45; 1774 columns x 24
+// tensors: 7 -> 2).  GC_MQ_SPLIT_OVERHEAD overrides the overhead (in chunks); < 0 selects the
+// fill-only rule.
 int64_t wave_splits(int64_t ctas, int64_t max_splits, int64_t nchunks, int sms) {
+  static const double overhead = [] {
+    const char *e = getenv("GC_MQ_SPLIT_OVERHEAD");
+    return e ? atof(e) : 3.0;
+  }();
   int64_t best = 1;
-  double best_eff = 0.0;
+  double best_cost = 0.0, best_eff = 0.0;
   for (int64_t s = 1; s <= max_splits && nchunks / s >= 4; ++s) {
     const int64_t items = ctas * s, waves = (items + sms - 1) / sms;
-    const double eff = static_cast<double>(items) / static_cast<double>(waves * sms);
-    if (eff > best_eff + 0.02) best = s, best_eff = eff;
+    if (overhead < 0.0) {
+      const double eff = static_cast<double>(items) / static_cast<double>(waves * sms);
+      if (eff > best_eff + 0.02) best = s, best_eff = eff;
+      continue;
+    }
+    const double cost = static_cast<double>(waves) * (static_cast<double>((nchunks + s - 1) / s) + overhead);
+    if (s == 1 || cost < best_cost * 0.98) best = s, best_cost = cost;
   }
   return best;
 }
 
 
+// Row splits of Q = M^T P_hat: `items` (column slab, tensor-worker) CTAs per split, each walking
+// ceil(boxes / s) 128-row boxes plus a fixed cost worth ~kMtpOverhead boxes; pick s minimising
+// waves x (boxes per CTA + overhead) with `occ` resident CTAs per SM.  GC_MTP_SPLIT_OVERHEAD
+// overrides the overhead (in boxes); < 0 selects the old rule (about two CTAs per SM).
+int64_t mtp_splits(int64_t items, int64_t boxes, int64_t max_splits, int sms, int occ) {
+  static const double overhead = [] {
+    const char *e = getenv("GC_MTP_SPLIT_OVERHEAD");
+    return e ? atof(e) : 6.0;
+  }();
+  int64_t best = 1;
+  if (overhead < 0.0) {
+    best = (2 * sms + items - 1) / items;
+  } else {
+    const int64_t slots = static_cast<int64_t>(sms) * (occ < 1 ? 1 : occ);
+    double best_cost = 0.0;
+    for (int64_t s = 1; s <= max_splits && s <= boxes; ++s) {
+      const int64_t waves = (items * s + slots - 1) / slots;
+      const double cost = static_cast<double>(waves) * (static_cast<double>((boxes + s - 1) / s) + overhead);
+      if (s == 1 || cost < best_cost * 0.98) best = s, best_cost = cost;
+    }
+  }
+  if (best > max_splits) best = max_splits;
+  if (best > boxes) best = boxes;
+  return best < 1 ? 1 : best;
+}
+
+template <typename K>
+int mtp_occupancy(K kernel, int smem) {   // resident CTAs per SM, queried once per kernel type
+  static int cached = 0;
+  if (cached > 0) return cached;
+  int occ = 1;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kMtpThreads, smem) != cudaSuccess) {
+    (void)cudaGetLastError();
+    occ = 1;
+  }
+  cached = occ;
+  return occ;
+}
 
 }  // namespace
 
@@ -1385,10 +1439,7 @@ int gc_psgd_mtp_tma_launch(int32_t T, int32_t L, const int64_t *host_tensor_offs
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t boxes = (rows_full + kM - 1) / kM;
   const int64_t V = static_cast<int64_t>(T) * L;
-  int64_t splits = (2 * sms + slabs * V - 1) / (slabs * V);
-  if (splits > max_splits) splits = max_splits;
-  if (splits > boxes) splits = boxes;
-  if (splits < 1) splits = 1;
+  int64_t splits = mtp_splits(slabs * V, boxes, max_splits, sms, mtp_occupancy(mtp_tma_kernel<4>, kMtpSmem));
   const int64_t per = (boxes + splits - 1) / splits;
   splits = (boxes + per - 1) / per;
   MtpArgs a{};
@@ -1686,10 +1737,7 @@ int gc_psgd_mtp_pair_launch(int32_t T, int32_t L, const int64_t *host_tensor_off
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t boxes = (rows_full + kM - 1) / kM;
   const int64_t V = static_cast<int64_t>(T) * L;
-  int64_t splits = (2 * sms + slabs * V - 1) / (slabs * V);
-  if (splits > max_splits) splits = max_splits;
-  if (splits > boxes) splits = boxes;
-  if (splits < 1) splits = 1;
+  int64_t splits = mtp_splits(slabs * V, boxes, max_splits, sms, mtp_occupancy(mtp_pair_kernel<4>, kMpSmem));
   const int64_t per = (boxes + splits - 1) / splits;
   splits = (boxes + per - 1) / per;
   MtpArgs a{};

@@ -944,7 +944,7 @@ class DistributedTensorListPipeline:
                 if grp.batch.rows_aligned or umma_unaligned():   # ef_apply inside the tcgen05 P = M Q
                     steps.append(grp.run_steps(res.data_ptr(), res.data_ptr(), est.data_ptr(), round_index,
                                                grads_ptr=g.data_ptr(), vec=bool(grp.batch.rows_aligned), q=q,
-                                               ef_resid_ptr=res.data_ptr()))
+                                               ef_resid_ptr=res.data_ptr(), decode_phase=True))
                 else:
                     grp.materialize(res.data_ptr())
                     for t in grp.tensor_ids:
@@ -952,11 +952,11 @@ class DistributedTensorListPipeline:
                         _native.call("gc_ef_apply", L, self.sizes[t], g.data_ptr() + 4 * off, res.data_ptr() + 4 * off,
                                      D, res.data_ptr() + 4 * off, D, sp)
                     steps.append(grp.run_steps(res.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, vec=False,
-                                               q=q))
+                                               q=q, decode_phase=True))
             else:
                 grp.set_ld(D, aligned)
                 steps.append(grp.run_steps(g.data_ptr(), None, est.data_ptr(), round_index,
-                                           vec=bool(grp.batch.rows_aligned), q=q))
+                                           vec=bool(grp.batch.rows_aligned), q=q, decode_phase=True))
             for t in grp.tensor_ids:
                 ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
                 ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)
@@ -964,7 +964,10 @@ class DistributedTensorListPipeline:
         reqs = [st.send(None) for st in steps]
         while steps:
             kind = reqs[0][0]
-            sums = exchange_float_groups(kind, [(x, x.shape[0] // L, m) for _, x, m in reqs], self.comm, n, L)
+            if kind == "decode":   # every group's warm-Q Gram is queued: now all decodes
+                sums = [None] * len(steps)
+            else:
+                sums = exchange_float_groups(kind, [(x, x.shape[0] // L, m) for _, x, m in reqs], self.comm, n, L)
             nxt_steps, nxt_reqs = [], []
             for st, sm in zip(steps, sums):
                 try:

@@ -221,23 +221,32 @@ class TensorListPipeline:
             for t in self.bypass:
                 ledger.charge_ring("dense-bypass", n, self.sizes[t], 32)
                 bits += 32.0 * self.sizes[t]
+        # every group up to its decode first, then all decodes: the next round's rank check waits on
+        # the last group's warm-Q Gram while all decodes are still queued (no device bubble)
+        finish = []
         for grp, q in zip(self.groups, qs):
             grp.set_ld(c.stride(0), grp.vec and c.data_ptr() % 16 == 0 and est.data_ptr() % 16 == 0
                        and g.data_ptr() % 16 == 0 and g.stride(0) == c.stride(0))
             if fuse_ef and (grp.batch.rows_aligned or umma_unaligned()):   # ef_apply inside the tcgen05 P = M Q
-                grp.run(c.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, grads_ptr=g.data_ptr(),
-                        vec=bool(grp.batch.rows_aligned), fold=self._fold, q=q, ef_resid_ptr=res.data_ptr())
+                fin = grp.run(c.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, grads_ptr=g.data_ptr(),
+                              vec=bool(grp.batch.rows_aligned), fold=self._fold, q=q, ef_resid_ptr=res.data_ptr(),
+                              defer_decode=True)
             elif fuse_ef:   # unaligned rows: ef_apply on the group's tensors, then the plain passes
                 grp.materialize(res.data_ptr())
                 for t in grp.tensor_ids:
                     off = int(self.offsets[t])
                     _native.call("gc_ef_apply", n, self.sizes[t], g.data_ptr() + 4 * off, res.data_ptr() + 4 * off,
                                  g.stride(0), res.data_ptr() + 4 * off, res.stride(0), sp)
-                grp.run(c.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, vec=False, fold=self._fold, q=q)
+                fin = grp.run(c.data_ptr(), res.data_ptr(), est.data_ptr(), round_index, vec=False, fold=self._fold,
+                              q=q, defer_decode=True)
             else:
-                grp.run(c.data_ptr(), None, est.data_ptr(), round_index, vec=bool(grp.batch.rows_aligned),
-                        fold=self._fold, q=q)
+                fin = grp.run(c.data_ptr(), None, est.data_ptr(), round_index, vec=bool(grp.batch.rows_aligned),
+                              fold=self._fold, q=q, defer_decode=True)
+            finish.append(fin)
+        for grp, fin in zip(self.groups, finish):
+            fin()
             grp.saved = dict(grp.last)
+        for grp in self.groups:
             for t in grp.tensor_ids:
                 ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
                 ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)

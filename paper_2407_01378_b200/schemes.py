@@ -436,6 +436,31 @@ class ChunkedEngine(Engine):
 
 
 # ----------------------------------------------------------------------------- PowerSGD
+def _rank_ok_many(groups, host_grams, q_devs):
+    """PowerSgdGroup._rank_ok_host for several groups of the same rank with one eigvalsh call:
+    per tensor np.linalg.matrix_rank(q) == rank (compressors.py:599) from the fp64 Gram eigenvalues,
+    the exact numpy call on a host copy near numpy's tolerance."""
+    import numpy as np
+    if not groups:
+        return []
+    r = groups[0].rank
+    sig = np.sqrt(np.clip(np.linalg.eigvalsh(np.concatenate(host_grams).reshape(-1, r, r)), 0.0, None))
+    width = np.concatenate([np.full(hg.shape[0], max(grp.cols, r), dtype=np.float64)
+                            for grp, hg in zip(groups, host_grams)])
+    tol = sig.max(axis=1) * width * np.finfo(np.float32).eps
+    clear = np.all((sig > 2 * tol[:, None]) | (sig < 0.5 * tol[:, None]), axis=1)
+    ok = np.count_nonzero(sig > tol[:, None], axis=1) == r
+    out, off = [], 0
+    for grp, hg, q in zip(groups, host_grams, q_devs):
+        t_n = hg.shape[0]
+        o = [bool(x) for x in ok[off:off + t_n]]
+        for t in np.nonzero(~clear[off:off + t_n])[0]:
+            o[t] = int(np.linalg.matrix_rank(q[t].cpu().numpy())) == r
+        out.append(o)
+        off += t_n
+    return out
+
+
 def seed_q_groups(groups, round_index):
     """Seed matrices of several PowerSGD groups with one device -> host round trip: all Gram
     matrices are computed, copied back together and decided with batched eigvalsh; only the
@@ -452,20 +477,24 @@ def seed_q_groups(groups, round_index):
                 pg = grp._pending_gram
                 if pg is not None and pg[0] is grp.warm and grp.cfg.warm_start:
                     pg[1].synchronize()
-                    ready[i] = grp._gram_host.numpy().copy()
+                    ready[i] = grp._gram_host.numpy()
         todo = [i for i in pending if i not in ready]
         grams = [groups[i]._gram(state[i][0]) for i in todo]
         host = torch.cat([x.reshape(-1) for x in grams]).cpu().numpy() if grams else None   # one sync
-        off, still = 0, []
+        off, hgs = 0, []
         for i in pending:
-            grp = groups[i]
             if i in ready:
-                hg = ready[i]
+                hgs.append(ready[i])
             else:
                 gm = grams[todo.index(i)]
-                hg = host[off:off + gm.numel()].reshape(gm.shape)
+                hgs.append(host[off:off + gm.numel()].reshape(gm.shape))
                 off += gm.numel()
-            ok = grp._rank_ok_host(hg, state[i][0])
+        # one batched eigvalsh over every pending group's Gram matrices (the host step between the
+        # previous round's factor exchange and this round's first launch)
+        oks = _rank_ok_many([groups[i] for i in pending], hgs, [state[i][0] for i in pending])
+        still = []
+        for i, ok in zip(pending, oks):
+            grp = groups[i]
             if not all(ok):
                 if attempt == 3:
                     raise DegenerateMatrixError("seed matrix rank-deficient after redraws")
@@ -475,6 +504,15 @@ def seed_q_groups(groups, round_index):
             break
         pending = still
     return [q for q, _ in state]
+
+
+def _finish_steps(steps):
+    """Resume a run_steps generator paused at its decode phase and run it to the end."""
+    try:
+        steps.send(None)
+    except StopIteration as stop:
+        return stop.value
+    raise RuntimeError("PowerSGD round generator yielded after its decode phase")
 
 
 def umma_unaligned() -> bool:
@@ -629,19 +667,25 @@ class PowerSgdGroup:
             _native.lib().gc_psgd_mtp_ef_supported(self.rows, self.cols, self.rank, self.batch.rows_aligned))
 
     def run(self, c_ptr: int, resid_ptr, est_ptr: int, round_index: int, grads_ptr=None, vec=False, fold=None,
-            before_ef=None, q=None, ef_resid_ptr=None):
-        """One round for the batch (run_steps driven with `fold` at its two factor all-reduces)."""
+            before_ef=None, q=None, ef_resid_ptr=None, defer_decode=False):
+        """One round for the batch (run_steps driven with `fold` at its two factor all-reduces).
+        defer_decode: stop before the decode and return a callable that finishes the round (and
+        returns warm Q), so a caller can queue the decodes of several groups after all their warm-Q
+        Gram copies -- the next round's rank check then waits on the last Gram while every decode
+        is still queued on the device."""
         steps = self.run_steps(c_ptr, resid_ptr, est_ptr, round_index, grads_ptr=grads_ptr, vec=vec,
-                               before_ef=before_ef, q=q, ef_resid_ptr=ef_resid_ptr)
+                               before_ef=before_ef, q=q, ef_resid_ptr=ef_resid_ptr, decode_phase=defer_decode)
         req = next(steps)
         try:
             while True:
+                if req[0] == "decode":
+                    return lambda: _finish_steps(steps)
                 req = steps.send(fold(*req))
         except StopIteration as stop:
             return stop.value
 
     def run_steps(self, c_ptr: int, resid_ptr, est_ptr: int, round_index: int, grads_ptr=None, vec=False,
-                  before_ef=None, q=None, ef_resid_ptr=None):
+                  before_ef=None, q=None, ef_resid_ptr=None, decode_phase=False):
         """One round for the batch as a generator: it yields each factor all-reduce as
         (kind, x [T*L][m], m) and resumes with its [T][m] sums in the reference ring order
         (simulated: local fold; distributed: exchange), so a caller can exchange the factors of
@@ -649,7 +693,8 @@ class PowerSgdGroup:
         grads_ptr is given together with vec: ef_apply fused into P = M Q, corrected written over
         resid).  before_ef() runs after the estimate, before the residuals change (the nmse hook).
         ef_resid_ptr (with grads_ptr and vec): ef_apply fused into P = M Q, corrected written there
-        (c_ptr must then point at it).  Returns warm Q [T][cols][r]."""
+        (c_ptr must then point at it).  decode_phase: also yield ("decode", None, 0) once warm Q and
+        its Gram copy are queued, before the decode (resume with None).  Returns warm Q [T][cols][r]."""
         sp = _sp()
         T, L, n, d, rows, cols, r = self.T, self.L, self.n, self.d, self.rows, self.cols, self.rank
         bref = ctypes.byref(self.batch)
@@ -741,6 +786,8 @@ class PowerSgdGroup:
             ev = torch.cuda.Event()
             ev.record()
             self._pending_gram = (warm, ev)
+        if decode_phase:
+            yield ("decode", None, 0)
         qs_chunks = [cols_of(q_sum, c0, rc, f"qs_c{k}") for k, (c0, rc) in enumerate(spans)]
 
         def decode(resid, est):

@@ -115,8 +115,9 @@ def test_residual_reads_and_writes_between_rounds():
 
 def test_tma_pass_matches_register_pass():
     """P = M Q from the TMA-fed kernel against the register-fed tcgen05 kernel: same 3xTF32 split
-    (A_big is the raw fp32 box, truncated by the tensor core) and fold cadence, so the factors agree
-    to far inside the 1e-5 contract."""
+    (A_big is the raw fp32 box, truncated by the tensor core); the two passes pick their column
+    splits independently (different fp64 fold points), so they agree to a few 3xTF32 roundings of
+    the dot products -- far inside the 1e-5 contract, which both are also checked against."""
     import ctypes
     import paper_2407_01378_b200 as gcb
     from paper_2407_01378_b200 import _native
@@ -124,9 +125,10 @@ def test_tma_pass_matches_register_pass():
     d, _ = _dims()
     rows, cols = matrix_shape_for(d)
     n, r = 2, 4
-    g = torch.randn(n, d, device="cuda")
-    res = torch.randn(n, d, device="cuda")
-    q = torch.randn(cols, r, device="cuda")
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    g = torch.randn(n, d, device="cuda", generator=gen)
+    res = torch.randn(n, d, device="cuda", generator=gen)
+    q = torch.randn(cols, r, device="cuda", generator=gen)
     batch = _native.PsgdBatch(1, n, None, d, None, 1, 0)
     ws = torch.empty(int(_native.lib().gc_psgd_workspace_bytes(n, rows, cols, r)), dtype=torch.uint8, device="cuda")
     p1 = torch.empty(n, rows, r, device="cuda")
@@ -142,9 +144,9 @@ def test_tma_pass_matches_register_pass():
     assert torch.equal(r1, r2)                       # corrected = f32(g + r) written over r
     assert torch.equal(r1, g + res)
     # the same three 3xTF32 products (the TMA pass packs B_big / B_small along N: two MMAs per
-    # k-step, the halves summed in the fp64 fold): equal to a few fp32 ulps of the dot products
+    # k-step, the halves summed in the fp64 fold), folded at different split points
     rf = d // cols
-    tol = 1e-6 * p2[:, :rf].abs().max().item()
+    tol = 4e-6 * p2[:, :rf].abs().max().item()
     assert (p1[:, :rf] - p2[:, :rf]).abs().max().item() <= tol
     m = torch.zeros(n, rows * cols, dtype=torch.float64, device="cuda")
     m[:, :d] = (g + res).double()
