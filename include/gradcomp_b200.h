@@ -160,6 +160,12 @@ int gc_thc_decode_ef(const gc_thc_geom *g, int32_t workers, const int8_t *codes,
 int gc_thc_rank_ranges(const gc_thc_geom *g, int32_t L, const float *grads, const float *resid, int64_t ld,
                        int64_t tile_begin, int64_t tile_end, const uint32_t *sign_bits, float *neg_ranges,
                        void *stream);
+/* K1 with the rotation signs drawn inside it: the words of tiles [tile_begin, tile_end) are generated
+ * from rotation_stream exactly as gc_thc_signs would (transforms.py:80-82) and written to sign_bits
+ * for K2 / K3 -- no separate gc_thc_signs pass over the vector. */
+int gc_thc_rank_ranges_signs(const gc_thc_geom *g, int32_t L, const float *grads, const float *resid, int64_t ld,
+                             int64_t tile_begin, int64_t tile_end, const gc_pcg64 *rotation_stream,
+                             uint32_t *sign_bits, float *neg_ranges, void *stream);
 int gc_thc_merge_ranges(int32_t L, int64_t num_blocks, const float *neg_ranges_in, float *neg_ranges_out,
                         void *stream);
 int gc_thc_rank_quant(const gc_thc_geom *g, int32_t L, const float *grads, const float *resid_in, float *resid_out,

@@ -81,6 +81,7 @@ SIGNATURES = {
     "gc_thc_decode_estimate": (c_int, [POINTER(ThcGeom), I32, P, I32, P, P, P, P, P]),
     "gc_thc_decode_ef": (c_int, [POINTER(ThcGeom), I32, P, P, P, P, P, I64, P, P]),
     "gc_thc_rank_ranges": (c_int, [POINTER(ThcGeom), I32, P, P, I64, I64, I64, P, P, P]),
+    "gc_thc_rank_ranges_signs": (c_int, [POINTER(ThcGeom), I32, P, P, I64, I64, I64, POINTER(Pcg64), P, P, P]),
     "gc_thc_merge_ranges": (c_int, [I32, I64, P, P, P]),
     "gc_thc_rank_quant": (c_int, [POINTER(ThcGeom), I32, P, P, P, I64, I64, I64, P, P, POINTER(Pcg64), P, I64, I32,
                                   P, P]),

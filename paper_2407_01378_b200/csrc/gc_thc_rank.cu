@@ -51,6 +51,12 @@ struct RankArgs {
   const void *sums;           // K3: [active] saturated sums (sum_bytes each)
   int sum_bytes;
   float *est;                 // K3: [dim]
+  // K1 with signs_out: the rotation signs are drawn here (gc_thc_signs' stream layout) and written
+  // for K2 / K3; sign_jump = {mult_hi, mult_lo, c_hi, c_lo} advances a lane by 496 outputs (the
+  // next tile's word of that lane), c = plus * inc of the stream
+  uint32_t *signs_out;
+  gc_pcg64 sign_stream;
+  uint64_t sign_jump[4];
   gc_pcg64 streams[kMaxL];
 };
 
@@ -174,9 +180,35 @@ __global__ void __launch_bounds__(kWarps * 32) rank_ranges_kernel(const __grid_c
   const float *gw = a.g + l * a.ld;
   const float *rw = a.r ? a.r + l * a.ld : nullptr;
   float *out = a.neg_ranges + static_cast<int64_t>(l) * a.nb * 2;
+  // fused sign draw: the lane's word of tile t is outputs 16 (32 t + lane) .. + 15 of the
+  // rotation-signs stream (transforms.py:80-82; numpy's bounded uint32 draws, two per next64)
+  const bool gen = a.signs_out != nullptr;
+  gc::u128 sstate = 0;
+  if (gen) {
+    gc::Pcg p;
+    p.load(a.sign_stream);
+    p.jump(static_cast<uint64_t>(t_lo) * 512 + static_cast<uint64_t>(lane) * 16);
+    sstate = p.state;
+  }
   for (int64_t t = t_lo; t < t_hi; ++t) {
     const int64_t t0 = t * kTileN;
-    const uint32_t sw = a.signs[(t0 >> 5) + lane];
+    uint32_t sw;
+    if (gen) {
+      const gc::u128 inc = gc::mk128(a.sign_stream.inc_hi, a.sign_stream.inc_lo);
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        sstate = sstate * GC_PCG_MULT + inc;
+        const uint64_t u = gc::Pcg::output(sstate);
+        word |= static_cast<uint32_t>((u >> 31) & 1u) << (2 * j);
+        word |= static_cast<uint32_t>((u >> 63) & 1u) << (2 * j + 1);
+      }
+      sstate = sstate * gc::mk128(a.sign_jump[0], a.sign_jump[1]) + gc::mk128(a.sign_jump[2], a.sign_jump[3]);
+      if (l == 0) a.signs_out[(t0 >> 5) + lane] = word;
+      sw = word;
+    } else {
+      sw = a.signs[(t0 >> 5) + lane];
+    }
     load_corrected<false>(a, gw, rw, t0, cbuf, lane);
     double v[32];
     forward<K>(v, cbuf, sw, scr, lane);
@@ -552,13 +584,32 @@ int set_smem(F fn, int bytes) {
   return bytes;
 }
 
-}  // namespace
 
-extern "C" {
+// Host: the 496-step jump of a PCG64 stream (state -> m state + c), from the 2^k-step table.
+void sign_jump_consts(const gc_pcg64 &st, uint64_t out[4]) {
+  static const uint64_t table[128][4] = GC_PCG_TABLE_INIT;
+  typedef unsigned __int128 h128;
+  h128 am = 1, ap = 0;
+  uint64_t delta = 512 - 16;
+  for (int k = 0; delta; ++k, delta >>= 1) {
+    if (delta & 1) {
+      const h128 m = (static_cast<h128>(table[k][0]) << 64) | table[k][1];
+      const h128 p = (static_cast<h128>(table[k][2]) << 64) | table[k][3];
+      am *= m;
+      ap = ap * m + p;
+    }
+  }
+  const h128 inc = (static_cast<h128>(st.inc_hi) << 64) | st.inc_lo;
+  const h128 c = ap * inc;
+  out[0] = static_cast<uint64_t>(am >> 64);
+  out[1] = static_cast<uint64_t>(am);
+  out[2] = static_cast<uint64_t>(c >> 64);
+  out[3] = static_cast<uint64_t>(c);
+}
 
-int gc_thc_rank_ranges(const gc_thc_geom *g, int32_t L, const float *grads, const float *resid, int64_t ld,
-                       int64_t tile_begin, int64_t tile_end, const uint32_t *sign_bits, float *neg_ranges,
-                       void *stream) {
+int rank_ranges_launch(const gc_thc_geom *g, int32_t L, const float *grads, const float *resid, int64_t ld,
+                       int64_t tile_begin, int64_t tile_end, const uint32_t *sign_bits,
+                       const gc_pcg64 *sign_stream, uint32_t *signs_out, float *neg_ranges, void *stream) {
   RankArgs a{};
   int grid = 0;
   const int st = prepare(a, g, L, tile_begin, tile_end, grid);
@@ -571,6 +622,11 @@ int gc_thc_rank_ranges(const gc_thc_geom *g, int32_t L, const float *grads, cons
   a.aligned = ((reinterpret_cast<uintptr_t>(grads) | reinterpret_cast<uintptr_t>(resid)) & 15) == 0 && (ld % 4) == 0;
   a.signs = sign_bits;
   a.neg_ranges = neg_ranges;
+  if (signs_out) {
+    a.signs_out = signs_out;
+    a.sign_stream = *sign_stream;
+    sign_jump_consts(*sign_stream, a.sign_jump);
+  }
   const int k = log2_block(g);
   const int smem = kWarps * warp_smem(kTileN >> k, a.q).total;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -582,6 +638,26 @@ int gc_thc_rank_ranges(const gc_thc_geom *g, int32_t L, const float *grads, cons
 #undef GC_K1
   GC_LAUNCH_CHECK("rank_ranges_kernel");
   return GC_OK;
+}
+
+
+}  // namespace
+
+extern "C" {
+
+int gc_thc_rank_ranges_signs(const gc_thc_geom *g, int32_t L, const float *grads, const float *resid, int64_t ld,
+                             int64_t tile_begin, int64_t tile_end, const gc_pcg64 *rotation_stream,
+                             uint32_t *sign_bits, float *neg_ranges, void *stream) {
+  GC_REQUIRE(rotation_stream && sign_bits, "invalid argument");
+  return rank_ranges_launch(g, L, grads, resid, ld, tile_begin, tile_end, sign_bits, rotation_stream, sign_bits,
+                            neg_ranges, stream);
+}
+
+int gc_thc_rank_ranges(const gc_thc_geom *g, int32_t L, const float *grads, const float *resid, int64_t ld,
+                       int64_t tile_begin, int64_t tile_end, const uint32_t *sign_bits, float *neg_ranges,
+                       void *stream) {
+  return rank_ranges_launch(g, L, grads, resid, ld, tile_begin, tile_end, sign_bits, nullptr, nullptr, neg_ranges,
+                            stream);
 }
 
 int gc_thc_merge_ranges(int32_t L, int64_t num_blocks, const float *neg_ranges_in, float *neg_ranges_out,

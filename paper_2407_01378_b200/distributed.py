@@ -447,6 +447,7 @@ class _Thc(_Base):
         self.nibble = cfg.wire_bits <= 4
         L, W = self.L, self.comm.world
         self.fused = P >= 1024 and 32 <= B <= 1024 and L <= 16
+        self.k1_signs = os.environ.get("GC_THC_K1_SIGNS", "1") != "0"   # signs drawn inside K1
         i32 = dict(dtype=torch.int32, device=self.dev)
         self.counters = torch.zeros(4, dtype=torch.int64, device=self.dev)
         if self.fused:
@@ -500,7 +501,11 @@ class _Thc(_Base):
         sp = _sp()
         geom = ctypes.byref(self.geom)
         rot = self.seeds.pcg("rotation-signs", r)                            # transforms.py:80-82
-        _native.call("gc_thc_signs", ctypes.byref(rot), self.signs.numel() * 32, self.signs.data_ptr(), sp)
+        # the fused path draws the signs inside K1 (gc_thc_rank_ranges_signs): K1 streams g and r, so
+        # the PCG64 work rides in its spare issue slots instead of a separate pass
+        self._rot = rot if (self.fused and self.k1_signs) else None
+        if self._rot is None:
+            _native.call("gc_thc_signs", ctypes.byref(rot), self.signs.numel() * 32, self.signs.data_ptr(), sp)
         coins = self._coins(r)
         counters = self.counters = torch.zeros(4, dtype=torch.int64, device=self.dev)
         ev = self._ev()
@@ -553,8 +558,12 @@ class _Thc(_Base):
             self.launches += 1
 
         for tb, te in bounds:
-            _native.call("gc_thc_rank_ranges", geom, L, g.data_ptr(), _ptr(res), g.stride(0), tb, te,
-                         self.signs.data_ptr(), self.neg.data_ptr(), sp)
+            if self._rot is not None:
+                _native.call("gc_thc_rank_ranges_signs", geom, L, g.data_ptr(), _ptr(res), g.stride(0), tb, te,
+                             ctypes.byref(self._rot), self.signs.data_ptr(), self.neg.data_ptr(), sp)
+            else:
+                _native.call("gc_thc_rank_ranges", geom, L, g.data_ptr(), _ptr(res), g.stride(0), tb, te,
+                             self.signs.data_ptr(), self.neg.data_ptr(), sp)
             b0, b1 = tb * 1024 // B, min(te * 1024 // B, self.nb)
             if L > 1:   # this rank's L tables -> one, rows b0..b1
                 part = self.neg[:, b0:b1].contiguous()

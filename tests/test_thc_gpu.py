@@ -142,3 +142,38 @@ def test_thc_host_streamed_round_rejects_nonfinite_without_state_change():
     ref.run_round(g0, 0)
     a, b = pipe.run_round(g0, 1), ref.run_round(g0, 1)
     assert np.array_equal(a.estimate.logical, b.estimate.logical)
+
+
+@pytest.mark.parametrize("L,B,d,segs", [(1, 1024, 3_000_017, [(0, 1000), (1000, 2930)]),
+                                        (2, 256, 400_000, [(0, 7), (7, 391)]),
+                                        (3, 1024, 1_048_576, [(0, 1024)])])
+def test_rank_k1_sign_draw_matches_signs_pass(L, B, d, segs):
+    """Per-rank K1 drawing the rotation signs itself (gc_thc_rank_ranges_signs) against the separate
+    gc_thc_signs pass + K1: identical sign words for every tile of every segment (written once, by
+    worker 0's warps) and identical (-lo, hi) block tables."""
+    import ctypes
+    import paper_2407_01378_b200 as gcb
+    from paper_2407_01378_b200 import _native
+    P = 1 << (d - 1).bit_length()
+    geom = _native.ThcGeom(d, P, B, 4, 8, float(B) ** -0.5)
+    active = int(_native.lib().gc_thc_active_len(ctypes.byref(geom)))
+    tiles, nb = -(-active // 1024), active // B
+    assert segs[-1][1] == tiles
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    g = torch.randn(L, d, device="cuda", generator=gen)
+    r = torch.randn(L, d, device="cuda", generator=gen)
+    rot = gcb.SeedSpec(77).pcg("rotation-signs", 5)
+    sp = torch.cuda.current_stream().cuda_stream
+    s_ref = torch.empty(tiles * 32, dtype=torch.int32, device="cuda")
+    s_gen = torch.full((tiles * 32,), -1, dtype=torch.int32, device="cuda")
+    n_ref = torch.empty(L, nb, 2, device="cuda")
+    n_gen = torch.empty(L, nb, 2, device="cuda")
+    _native.call("gc_thc_signs", ctypes.byref(rot), tiles * 1024, s_ref.data_ptr(), sp)
+    for tb, te in segs:
+        _native.call("gc_thc_rank_ranges", ctypes.byref(geom), L, g.data_ptr(), r.data_ptr(), d, tb, te,
+                     s_ref.data_ptr(), n_ref.data_ptr(), sp)
+        _native.call("gc_thc_rank_ranges_signs", ctypes.byref(geom), L, g.data_ptr(), r.data_ptr(), d, tb, te,
+                     ctypes.byref(rot), s_gen.data_ptr(), n_gen.data_ptr(), sp)
+    torch.cuda.synchronize()
+    assert torch.equal(s_gen, s_ref)
+    assert torch.equal(n_gen, n_ref)
