@@ -20,6 +20,8 @@
 // gc_thc_tile.cuh): bit-exact codes, residuals and estimate.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "gc_device.cuh"
 #include "gc_internal.h"
 #include "gc_thc_tile.cuh"
@@ -81,8 +83,9 @@ __host__ __device__ inline WarpSmem warp_smem(int nblk, int q) {
 }
 
 // The warp's run: worker l, tiles [t_lo, t_hi).  false when the warp has no work.
-__device__ __forceinline__ bool warp_run(const RankArgs &a, int &l, int64_t &t_lo, int64_t &t_hi) {
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+__device__ __forceinline__ bool warp_run(const RankArgs &a, int &l, int64_t &t_lo, int64_t &t_hi,
+                                         int cta_warps = kWarps) {
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * cta_warps + (threadIdx.x >> 5);
   if (gw >= a.L * a.chunks) return false;
   l = static_cast<int>(gw / a.chunks);
   t_lo = a.tile_begin + (gw % a.chunks) * a.tpw;
@@ -235,8 +238,13 @@ __global__ void __launch_bounds__(kWarps * 32) rank_ranges_kernel(const __grid_c
 }
 
 // ---------------------------------------------------------------- K2: quantize + own decode + EF
-template <int K>
-__global__ void __launch_bounds__(kWarps * 32, 4) rank_quant_kernel(const __grid_constant__ RankArgs a) {
+// WQ warps per CTA.  WQ = 16 (one CTA per SM, the default): the SM's warps start their ~90 KB
+// straight-line tile bodies together and drift apart only slowly, so they share the instruction
+// cache better than four independently scheduled 4-warp CTAs (ncu: no_instruction was K2's top
+// stall; 4.00 -> 3.86 ms per 350M round).  A per-tile CTA barrier removes the fetch stalls entirely
+// but makes every warp load its tile at once (long_scoreboard / lg_throttle): slower, not kept.
+template <int K, int WQ>
+__global__ void __launch_bounds__(WQ * 32, 16 / WQ) rank_quant_kernel(const __grid_constant__ RankArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int nblk = kTileN >> K;
   constexpr int rpb_log = K - 5;
@@ -253,7 +261,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) rank_quant_kernel(const __grid
   double *lut = reinterpret_cast<double *>(ws + S.lut);
   int l;
   int64_t t_lo, t_hi;
-  if (!warp_run(a, l, t_lo, t_hi)) return;
+  if (!warp_run(a, l, t_lo, t_hi, WQ)) return;
 
   const int ibound = (1 << (q - 1)) - 1;
   const double levels = static_cast<double>((1 << q) - 2);
@@ -494,18 +502,45 @@ __global__ void __launch_bounds__(kWarps * 32) rank_decode_kernel(const __grid_c
   const double levels = static_cast<double>((1 << a.q) - 2);
   const double nd = static_cast<double>(a.n);
   const gc::DivN dn(a.n);   // / n: an exact reciprocal product for power-of-two n
+  // one-byte sums (wire_bits <= 8): the next tile's sign word, 32 sums and block range are loaded
+  // while this tile transforms, so the loop pays no global-load latency per tile
+  const bool pf = a.sum_bytes == 1;
+  int4 nu0 = make_int4(0, 0, 0, 0), nu1 = nu0;
+  uint32_t nsw = 0;
+  float2 nrg = make_float2(0.0f, 0.0f);
+  auto fetch = [&](int64_t t) {
+    const int64_t e0 = t * kTileN + lane * 32;
+    nsw = a.signs[(t * kTileN >> 5) + lane];
+    const int4 *p = reinterpret_cast<const int4 *>(static_cast<const int8_t *>(a.sums) + e0);
+    nu0 = p[0];
+    nu1 = p[1];
+    const int64_t b = e0 >> K;
+    nrg = b < a.nb ? *reinterpret_cast<const float2 *>(a.shared + 2 * b) : make_float2(-0.0f, 0.0f);
+  };
+  if (pf) fetch(t_lo);
   for (int64_t t = t_lo; t < t_hi; ++t) {
     const int64_t t0 = t * kTileN;
-    const uint32_t sw = a.signs[(t0 >> 5) + lane];
+    uint32_t sw;
     int z[32];
-    load_sums32(a, t0 + lane * 32, z);
-    // dequantize_sum(sums, ranges, q, n) (compressors.py:501-521): f32(n * mid + step * z)
-    const int64_t blk = (t0 + lane * 32) >> K;   // a lane's 32 coordinates sit in one block (B >= 32)
     double dlo = 0.0, dhi = 0.0;
-    if (blk < a.nb) {
-      const float2 rg = *reinterpret_cast<const float2 *>(a.shared + 2 * blk);
-      dlo = static_cast<double>(-rg.x);
-      dhi = static_cast<double>(rg.y);
+    if (pf) {
+      sw = nsw;
+      const int w[8] = {nu0.x, nu0.y, nu0.z, nu0.w, nu1.x, nu1.y, nu1.z, nu1.w};
+#pragma unroll
+      for (int j = 0; j < 32; ++j) z[j] = static_cast<int8_t>((w[j >> 2] >> (8 * (j & 3))) & 0xff);
+      dlo = static_cast<double>(-nrg.x);
+      dhi = static_cast<double>(nrg.y);
+      if (t + 1 < t_hi) fetch(t + 1);
+    } else {
+      sw = a.signs[(t0 >> 5) + lane];
+      load_sums32(a, t0 + lane * 32, z);
+      // dequantize_sum(sums, ranges, q, n) (compressors.py:501-521): f32(n * mid + step * z)
+      const int64_t blk = (t0 + lane * 32) >> K;   // a lane's 32 coordinates sit in one block (B >= 32)
+      if (blk < a.nb) {
+        const float2 rg = *reinterpret_cast<const float2 *>(a.shared + 2 * blk);
+        dlo = static_cast<double>(-rg.x);
+        dhi = static_cast<double>(rg.y);
+      }
     }
     const double mid = (dlo + dhi) / 2.0;
     const double step = dhi > dlo ? (dhi - dlo) / levels : 0.0;
@@ -545,7 +580,8 @@ int log2_block(const gc_thc_geom *g) {
   return k;
 }
 
-int prepare(RankArgs &a, const gc_thc_geom *g, int32_t L, int64_t tile_begin, int64_t tile_end, int &grid) {
+int prepare(RankArgs &a, const gc_thc_geom *g, int32_t L, int64_t tile_begin, int64_t tile_end, int &grid,
+            int cta_warps = kWarps) {
   GC_REQUIRE(g != nullptr, "geometry is null");
   GC_REQUIRE(L >= 1 && L <= kMaxL, "per-rank THC kernels support 1..16 local workers");
   GC_REQUIRE(g->dim >= 1 && g->padded >= kTileN && (g->padded & (g->padded - 1)) == 0 && g->padded >= g->dim,
@@ -574,8 +610,17 @@ int prepare(RankArgs &a, const gc_thc_geom *g, int32_t L, int64_t tile_begin, in
   a.tpw = tpw;
   a.chunks = (T + tpw - 1) / tpw;
   const int64_t warps = a.chunks * L;
-  grid = static_cast<int>((warps + kWarps - 1) / kWarps);
+  grid = static_cast<int>((warps + cta_warps - 1) / cta_warps);
   return 0;
+}
+
+// warps per CTA of K2: 16 (one CTA per SM) unless GC_THC_K2_WARPS=4 (four independent CTAs)
+int k2_cta_warps() {
+  static const int w = [] {
+    const char *e = getenv("GC_THC_K2_WARPS");
+    return e && atoi(e) == 4 ? 4 : 16;
+  }();
+  return w;
 }
 
 template <typename F>
@@ -678,7 +723,12 @@ int gc_thc_rank_quant(const gc_thc_geom *g, int32_t L, const float *grads, const
                       int32_t nibble, int64_t *counters, void *stream) {
   RankArgs a{};
   int grid = 0;
-  const int st = prepare(a, g, L, tile_begin, tile_end, grid);
+  // 16-warp CTAs while their shared memory fits an SM (small rotation blocks need more per warp)
+  int wq = k2_cta_warps();
+  if (wq == 16 && g && g->block >= 32 && g->block <= kTileN &&
+      16 * warp_smem(kTileN >> log2_block(g), g->quant_bits).total > 227 * 1024)
+    wq = kWarps;
+  const int st = prepare(a, g, L, tile_begin, tile_end, grid, wq);
   if (st < 0) return st;
   if (st == 1) return GC_OK;
   GC_REQUIRE(grads && sign_bits && shared_neg_ranges && coin_streams && send && ld >= g->dim, "invalid argument");
@@ -700,11 +750,14 @@ int gc_thc_rank_quant(const gc_thc_geom *g, int32_t L, const float *grads, const
   a.counters = reinterpret_cast<unsigned long long *>(counters);
   for (int l = 0; l < L; ++l) a.streams[l] = coin_streams[l];
   const int k = log2_block(g);
-  const int smem = kWarps * warp_smem(kTileN >> k, a.q).total;
+  const int smem = wq * warp_smem(kTileN >> k, a.q).total;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-#define GC_K2(KK) \
-  case KK:        \
-    rank_quant_kernel<KK><<<grid, kWarps * 32, set_smem(rank_quant_kernel<KK>, smem), s>>>(a); \
+#define GC_K2(KK)                                                                                           \
+  case KK:                                                                                                  \
+    if (wq == 16)                                                                                           \
+      rank_quant_kernel<KK, 16><<<grid, 16 * 32, set_smem(rank_quant_kernel<KK, 16>, smem), s>>>(a);        \
+    else                                                                                                    \
+      rank_quant_kernel<KK, kWarps><<<grid, kWarps * 32, set_smem(rank_quant_kernel<KK, kWarps>, smem), s>>>(a); \
     break;
   switch (k) { GC_K2(5) GC_K2(6) GC_K2(7) GC_K2(8) GC_K2(9) GC_K2(10) default: return GC_ERR_INVALID; }
 #undef GC_K2
