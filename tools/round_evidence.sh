@@ -29,12 +29,14 @@ timeout 120 ./build/ubench/umma_rate > ${o}_umma_rate.jsonl 2>&1
 timeout 120 ./build/ubench/unaligned_stream > ${o}_unaligned_stream.jsonl 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:"rank_quant|rank_ranges|rank_decode" -s 3 -c 3 \
   -o ${o}_thc_rank -f python tools/time_rank.py --scheme thc --steps 1 > /dev/null 2>&1
+if [ -z "$GC_EVIDENCE_QUICK" ]; then
 timeout 1500 python tools/sweep.py --synthetic --warmup 3 --steps 8 > ${o}_sweep_synthetic.jsonl 2> ${o}_sweep.err
 timeout 1500 python tools/sweep.py --dims 1048576,4194304,16777216,67108864,268435456,1000000000 --warmup 3 --steps 5 \
   > ${o}_sweep_dims.jsonl 2>> ${o}_sweep.err
 timeout 900 python tools/sweep.py --nmse 5 --dims 4194304 > ${o}_nmse_sweep.txt 2>> ${o}_sweep.err
 timeout 900 bash tools/run_reference_tests.sh run ${o}_ref_tests_seam.txt
 timeout 900 bash tools/run_reference_tests.sh run-core ${o}_ref_tests_core.txt
+fi
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_cases.py > ${o}_san_${tool}.txt 2>&1
   echo "rc=$?" >> ${o}_san_${tool}.txt
