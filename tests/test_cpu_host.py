@@ -134,3 +134,30 @@ def test_overflow_rate_and_ledger_api():
     assert led.to_csv().splitlines()[0] == "phase,worker,bits_sent,bits_received"
     with pytest.raises(ValueError):
         led.add("a", 0, sent=-1)
+
+
+def test_batched_rank_check_matches_per_group_and_numpy():
+    """seed_q_groups' one-eigvalsh rank check (_rank_ok_many) decides every tensor of every group as
+    the per-group check does, and both agree with np.linalg.matrix_rank (compressors.py:599) on
+    full-rank, rank-deficient and near-tolerance seed matrices."""
+    from types import SimpleNamespace
+
+    import torch
+
+    from paper_2407_01378_b200.schemes import PowerSgdGroup, _rank_ok_many
+    rng = np.random.default_rng(7)
+    r = 4
+    groups, grams, qs, expect = [], [], [], []
+    for cols, T in [(64, 3), (300, 2), (9, 4)]:
+        q = rng.standard_normal((T, cols, r)).astype(np.float32)
+        q[1, :, 3] = q[1, :, 0] * 2.0                       # exactly rank-deficient
+        if T > 2:
+            q[2, :, 2] = q[2, :, 1] + 1e-7 * q[2, :, 0]      # rank-deficient within the tolerance
+        g = np.einsum("tca,tcb->tab", q.astype(np.float64), q.astype(np.float64))
+        groups.append(SimpleNamespace(rank=r, cols=cols))
+        grams.append(g)
+        qs.append(torch.from_numpy(q))
+        expect.append([int(np.linalg.matrix_rank(q[t])) == r for t in range(T)])
+    got = _rank_ok_many(groups, grams, qs)
+    per = [PowerSgdGroup._rank_ok_host(grp, g, q) for grp, g, q in zip(groups, grams, qs)]
+    assert got == per == expect
