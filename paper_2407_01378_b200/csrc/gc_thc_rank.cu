@@ -3,6 +3,7 @@
 // Reference round (pkg/src/gradcomp/pipelines.py:260-322) split at its two exchange points:
 //
 //   K1  gc_thc_rank_ranges   ef_apply + signs + fp64 WHT + chunk_ranges           (reads g, r)
+//       (gc_thc_rank_ranges_signs: the round's rotation signs drawn here too and written for K2 / K3)
 //       -- range consensus: NCCL all-reduce MAX of (-lo, hi) --
 //   K2  gc_thc_rank_quant    ef_apply + WHT again + quantize_stochastic + own decode + ef_update:
 //                            codes straight into the all-to-all send layout, r_new written
