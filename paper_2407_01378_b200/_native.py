@@ -187,8 +187,32 @@ def check(rc: int, what: str = "") -> None:
     raise NativeError(f"{what}: {msg} (status {rc})" if what else f"{msg} (status {rc})")
 
 
+_fns = {}
+
+
 def call(name: str, *args) -> None:
-    fn = getattr(_load(), name, None)
+    fn = _fns.get(name)
     if fn is None:
-        raise NativeError(f"{name} is not exported by {LIB_PATH}")
-    check(fn(*args), name)
+        fn = getattr(_load(), name, None)
+        if fn is None:
+            raise NativeError(f"{name} is not exported by {LIB_PATH}")
+        _fns[name] = fn
+    rc = fn(*args)
+    if rc != GC_OK:
+        check(rc, name)
+
+
+try:   # the raw handle without building a torch.cuda.Stream object (host issue time per launch)
+    import torch as _torch
+    _raw_stream = _torch._C._cuda_getCurrentRawStream
+    _cur_dev = _torch._C._cuda_getDevice
+except (ImportError, AttributeError):   # pragma: no cover - older torch
+    _raw_stream = _cur_dev = None
+
+
+def current_stream_handle() -> int:
+    """cudaStream_t of torch's current stream on the current device, as an int."""
+    if _raw_stream is not None:
+        return _raw_stream(_cur_dev())
+    import torch
+    return torch.cuda.current_stream().cuda_stream

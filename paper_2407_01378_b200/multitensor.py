@@ -25,7 +25,7 @@ from .vectors import SeedSpec
 
 
 def _sp() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    return _native.current_stream_handle()
 
 
 def gpt2_medium_sizes() -> list[int]:

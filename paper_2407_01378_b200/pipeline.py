@@ -30,7 +30,7 @@ from . import schemes
 
 
 def _stream_ptr() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    return _native.current_stream_handle()
 
 
 class RoundResult:

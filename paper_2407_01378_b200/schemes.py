@@ -22,7 +22,7 @@ from .vectors import SeedSpec, next_pow2
 
 
 def _sp() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    return _native.current_stream_handle()
 
 
 def _ptr(t) -> int | None:
