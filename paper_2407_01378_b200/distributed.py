@@ -940,9 +940,8 @@ class DistributedTensorListPipeline:
             _native.call("gc_segment_fold_ef", n, len(self.bypass), self.byp_off.data_ptr(), self.byp_len.data_ptr(),
                          allc.data_ptr(), None, allc.stride(0), packed.data_ptr(), sp)
             est.index_copy_(0, self.byp_idx, packed)
-            for t in self.bypass:
-                ledger.charge_ring("dense-bypass", n, self.sizes[t], 32)
-                bits += 32.0 * self.sizes[t]
+            ledger.charge_rings("dense-bypass", n, [self.sizes[t] for t in self.bypass], 32)
+            bits += 32.0 * sum(self.sizes[t] for t in self.bypass)
         # every group's round as a generator (PowerSgdGroup.run_steps): the groups advance in lock
         # step and each factor phase of all groups is ONE exchange (one all-to-all + one all-gather)
         steps = []
@@ -966,10 +965,10 @@ class DistributedTensorListPipeline:
                 grp.set_ld(D, aligned)
                 steps.append(grp.run_steps(g.data_ptr(), None, est.data_ptr(), round_index,
                                            vec=bool(grp.batch.rows_aligned), q=q, decode_phase=True))
-            for t in grp.tensor_ids:
-                ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
-                ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)
-                bits += 32.0 * grp.rank * (grp.rows + grp.cols)
+            T = len(grp.tensor_ids)
+            ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32, times=T)
+            ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32, times=T)
+            bits += 32.0 * grp.rank * (grp.rows + grp.cols) * T
         reqs = [st.send(None) for st in steps]
         while steps:
             kind = reqs[0][0]

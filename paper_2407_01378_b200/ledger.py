@@ -70,11 +70,19 @@ class TrafficLedger:
         return "\n".join(lines) + "\n"
 
     # closed-form charges ------------------------------------------------------
-    def charge_ring(self, phase: str, n: int, length: int, element_bits: int) -> None:
-        """What ring_all_reduce charges (collectives.py:209-233)."""
+    def charge_ring(self, phase: str, n: int, length: int, element_bits: int, times: int = 1) -> None:
+        """What ring_all_reduce charges (collectives.py:209-233); `times` identical rings at once."""
         if n <= 1:
             return
-        per = 2 * (n - 1) * math.ceil(length / n) * element_bits
+        per = 2 * (n - 1) * math.ceil(length / n) * element_bits * times
+        for w in range(n):
+            self.add(phase, w, sent=per, received=per)
+
+    def charge_rings(self, phase: str, n: int, lengths, element_bits: int) -> None:
+        """charge_ring for several ring all-reduces of one phase (one add per worker)."""
+        if n <= 1:
+            return
+        per = sum(2 * (n - 1) * math.ceil(int(x) / n) * element_bits for x in lengths)
         for w in range(n):
             self.add(phase, w, sent=per, received=per)
 

@@ -218,9 +218,8 @@ class TensorListPipeline:
             else:
                 _native.call("gc_segment_fold_ef", n, len(self.bypass), self.seg_off.data_ptr(),
                              self.seg_len.data_ptr(), c.data_ptr(), None, c.stride(0), est.data_ptr(), sp)
-            for t in self.bypass:
-                ledger.charge_ring("dense-bypass", n, self.sizes[t], 32)
-                bits += 32.0 * self.sizes[t]
+            ledger.charge_rings("dense-bypass", n, [self.sizes[t] for t in self.bypass], 32)
+            bits += 32.0 * sum(self.sizes[t] for t in self.bypass)
         # every group up to its decode first, then all decodes: the next round's rank check waits on
         # the last group's warm-Q Gram while all decodes are still queued (no device bubble)
         finish = []
@@ -247,10 +246,10 @@ class TensorListPipeline:
             fin()
             grp.saved = dict(grp.last)
         for grp in self.groups:
-            for t in grp.tensor_ids:
-                ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32)
-                ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32)
-                bits += 32.0 * grp.rank * (grp.rows + grp.cols)
+            T = len(grp.tensor_ids)
+            ledger.charge_ring("left-factor", n, grp.rows * grp.rank, 32, times=T)
+            ledger.charge_ring("right-factor", n, grp.cols * grp.rank, 32, times=T)
+            bits += 32.0 * grp.rank * (grp.rows + grp.cols) * T
         if acc is not None:
             _native.call("gc_nmse_accumulate", n, D, c.data_ptr(), None, c.stride(0), est.data_ptr(), acc.data_ptr(), sp)
         if res is not None and not fuse_ef:
